@@ -1,0 +1,129 @@
+// Drop-in replacement for the CSR part of the reference's spconv/sparse.hpp
+// (inc/sparse.hpp:24-30, 77-140, 209-265).  A SparseMatrix here is a handle on
+// a DEVICE-resident CSR (int32 indices, fp32 values) built by libspconv_b200;
+// the reference's host accessors ptr()/idx()/val() still work and return the
+// CSR widened to int64/double, exported lazily on first use.  spmv() runs on
+// the GPU (fp32, column-ascending fmaf per row) -- there is no CPU path.
+#pragma once
+
+#include <cstdlib>
+#include <memory>
+#include <mutex>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "spconv/grid.hpp"
+#include "spconv_b200.h"
+
+namespace spconv {
+
+enum class Layout { CSR, CSC };
+
+inline const char* layout_name(Layout l) { return l == Layout::CSR ? "csr" : "csc"; }
+
+namespace detail {
+
+/// Maps a C-ABI status to the reference's exception types.
+inline void check(int rc) {
+    if (rc == SPCONV_OK) return;
+    if (rc == SPCONV_EINVAL) throw std::invalid_argument(spconv_last_error());
+    throw std::runtime_error(spconv_last_error());
+}
+
+struct CsrHandle {
+    spconv_csr* h = nullptr;
+    explicit CsrHandle(spconv_csr* p) : h(p) {}
+    CsrHandle(const CsrHandle&) = delete;
+    CsrHandle& operator=(const CsrHandle&) = delete;
+    ~CsrHandle() { spconv_csr_free(h); }
+};
+
+/// Device ordinal used by the drop-in API (SPCONV_DEVICE, default 0).
+inline int default_device() {
+    const char* e = std::getenv("SPCONV_DEVICE");
+    return e ? std::atoi(e) : 0;
+}
+
+}  // namespace detail
+
+/// Compressed sparse row matrix resident on the GPU (CSR only; the device
+/// path has no CSC layout).  Copies share the immutable device matrix.
+class SparseMatrix {
+public:
+    SparseMatrix() = default;
+
+    /// Adopts a C-ABI handle (takes ownership).
+    explicit SparseMatrix(spconv_csr* h) : dev_(std::make_shared<detail::CsrHandle>(h)) {
+        detail::check(spconv_csr_shape(h, &rows_, &cols_, &nnz_));
+        host_ = std::make_shared<HostCopy>();
+    }
+
+    /// Uploads a host CSR (ptr/idx int64, fp64 values narrowed to fp32).
+    static SparseMatrix from_csr(index_t rows, index_t cols, const std::vector<index_t>& ptr,
+                                 const std::vector<index_t>& idx, const std::vector<double>& val) {
+        if (static_cast<index_t>(ptr.size()) != rows + 1)
+            throw std::invalid_argument("SparseMatrix: ptr must have rows+1 entries");
+        spconv_csr* h = nullptr;
+        detail::check(spconv_csr_from_host(rows, cols, ptr.data(), idx.data(), val.data(),
+                                           detail::default_device(), nullptr, &h));
+        return SparseMatrix(h);
+    }
+
+    Layout layout() const { return Layout::CSR; }
+    index_t rows() const { return rows_; }
+    index_t cols() const { return cols_; }
+    index_t nnz() const { return nnz_; }
+    index_t major_dim() const { return rows_; }
+    index_t minor_dim() const { return cols_; }
+
+    const std::vector<index_t>& ptr() const { return exported().ptr; }
+    const std::vector<index_t>& idx() const { return exported().idx; }
+    const std::vector<double>& val() const { return exported().val; }
+
+    /// The C-ABI handle (nullptr for a default-constructed matrix).
+    spconv_csr* handle() const { return dev_ ? dev_->h : nullptr; }
+
+private:
+    struct HostCopy {
+        std::once_flag once;
+        std::vector<index_t> ptr, idx;
+        std::vector<double> val;
+    };
+    const HostCopy& exported() const {
+        if (!dev_) throw std::logic_error("SparseMatrix: empty matrix");
+        std::call_once(host_->once, [this] {
+            host_->ptr.resize(static_cast<std::size_t>(rows_) + 1);
+            host_->idx.resize(static_cast<std::size_t>(nnz_));
+            host_->val.resize(static_cast<std::size_t>(nnz_));
+            detail::check(spconv_csr_export(dev_->h, host_->ptr.data(), host_->idx.data(),
+                                            host_->val.data()));
+        });
+        return *host_;
+    }
+
+    std::shared_ptr<detail::CsrHandle> dev_;
+    std::shared_ptr<HostCopy> host_;
+    index_t rows_ = 0, cols_ = 0, nnz_ = 0;
+};
+
+/// y = M x (inc/sparse.hpp:214-261).  `threads` is accepted for source
+/// compatibility and ignored: the product runs on the GPU.
+inline DenseVector spmv(const SparseMatrix& m, std::span<const double> x, int threads = 0) {
+    (void)threads;
+    if (m.cols() != static_cast<index_t>(x.size()))
+        throw std::invalid_argument("spmv: matrix has " + std::to_string(m.cols()) +
+                                    " columns but vector has " + std::to_string(x.size()) +
+                                    " elements");
+    DenseVector y(static_cast<std::size_t>(m.rows()), 0.0);
+    detail::check(spconv_convolve_host_f64(m.handle(), x.data(), y.data(), 1));
+    return y;
+}
+
+inline DenseVector spmv(const SparseMatrix& m, const DenseVector& x, int threads = 0) {
+    return spmv(m, std::span<const double>(x), threads);
+}
+
+}  // namespace spconv

@@ -1,0 +1,121 @@
+/*
+ * spconv_b200.h -- the C-ABI drop-in boundary of the B200 conv-as-SpMV path.
+ *
+ * The reference (arxiv 2411.19419 spec implementation, /root/reference/proj)
+ * is a header-only C++20 library with no FFI; its "operator API" is the set of
+ * inline functions in namespace spconv.  Each entry point below replaces one
+ * of them (cited as inc/<file>:<line>, inc = proj/include/spconv) and is what
+ * the drop-in C++ headers in include/spconv/ call.  Plain pointers and sizes
+ * only; no torch or CUDA types cross this boundary (streams are passed as
+ * void* holding a cudaStream_t; NULL = the legacy default stream).
+ *
+ * Device format of a transform T (m_out*n_out x m*n):
+ *   row_ptr int32[rows+1], col_idx int32[nnz], vals float32[nnz]
+ * identical in structure to the reference CSR (inc/sparse.hpp:85-119);
+ * export widens to the reference's int64/int64/double.
+ *
+ * Status codes: 0 ok, 1 invalid argument (the reference would throw
+ * std::invalid_argument; the message is the reference's), 2 CUDA / out of
+ * memory / internal error.  spconv_last_error() returns the calling thread's
+ * last message.  A built handle is immutable: concurrent spconv_spmv /
+ * spconv_spmm calls on different streams are safe.
+ */
+#ifndef SPCONV_B200_H
+#define SPCONV_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPCONV_OK 0
+#define SPCONV_EINVAL 1
+#define SPCONV_ECUDA 2
+
+/* Opaque device-resident CSR (replaces spconv::Transform / SparseMatrix,
+ * inc/conv.hpp:165-168, inc/sparse.hpp:77-140). */
+typedef struct spconv_csr spconv_csr;
+
+/* Thread-local message for the last non-zero status. */
+const char* spconv_last_error(void);
+
+/* ABI version (major*100 + minor). */
+int spconv_abi_version(void);
+
+/* ConvSpec validation, inc/conv.hpp:40-48 (same two messages). */
+int spconv_spec_check(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p);
+
+/* Theorem 2.1 closed-form count, replaces nnz_bound inc/analysis.hpp:56-66. */
+int spconv_nnz_bound(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p, int64_t* out);
+
+/* One-time on-device CSR build of T = C*P for a k x k kernel (host fp32,
+ * row-major, unflipped = correlation).  Replaces build_transform
+ * inc/conv.hpp:179-204 (both routes; exact-zero taps are dropped as at
+ * inc/sparse.hpp:335 / inc/conv.hpp:201).  Runs on `device` / `stream`; the
+ * call returns once the build is enqueued and the handle is valid (the
+ * device arrays are complete when `stream` reaches this point). */
+int spconv_build_csr(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
+                     const float* kernel_kxk, int device, void* stream, spconv_csr** out);
+
+/* Uploads an arbitrary host CSR (int64 ptr/idx, double values narrowed to
+ * fp32) -- the device image of a reference SparseMatrix
+ * (inc/sparse.hpp:121-130) for spmv on matrices not built here (e.g. read
+ * with read_sparse, inc/sparse.hpp:412-432).  Columns must be strictly
+ * ascending per row (the CSR contract of inc/sparse.hpp:77-83). */
+int spconv_csr_from_host(int64_t rows, int64_t cols, const int64_t* row_ptr,
+                         const int64_t* col_idx, const double* vals, int device, void* stream,
+                         spconv_csr** out);
+
+/* rows(), cols(), nnz(): inc/sparse.hpp:121-126. */
+int spconv_csr_shape(const spconv_csr* h, int64_t* rows, int64_t* cols, int64_t* nnz);
+
+/* Geometry {m,n,k,s,p} of a built transform (Transform::spec,
+ * inc/conv.hpp:166); returns 1 for an uploaded generic CSR. */
+int spconv_csr_spec(const spconv_csr* h, int64_t spec5[5]);
+
+/* Device pointers of the CSR arrays (read-only; owned by the handle). */
+int spconv_csr_device_ptrs(const spconv_csr* h, const int32_t** row_ptr, const int32_t** col_idx,
+                           const float** vals);
+
+/* Synchronous export to host, widened to the reference's types: ptr(),
+ * idx(), val() of inc/sparse.hpp:128-130.  Any pointer may be NULL. */
+int spconv_csr_export(const spconv_csr* h, int64_t* row_ptr, int64_t* col_idx, double* vals);
+
+/* Copies the native device arrays (int32 row_ptr / int32 col_idx / fp32
+ * vals) into caller buffers, host or device (any pointer may be NULL),
+ * ordered on `stream`; returns when the copies are complete. */
+int spconv_csr_copy(const spconv_csr* h, int32_t* row_ptr, int32_t* col_idx, float* vals,
+                    void* stream);
+
+/* y = T x on device buffers (fp32).  Replaces spmv inc/sparse.hpp:214-261 /
+ * convolve inc/conv.hpp:207-215.  Per row: acc = +0.0f; for each stored
+ * entry in column-ascending order acc = fmaf(val, x[col], acc). */
+int spconv_spmv(const spconv_csr* h, const float* x_dev, float* y_dev, void* stream);
+
+/* Y[b] = T X[b] for b < batch, image-major device buffers:
+ * X[b*ldx + col], Y[b*ldy + row].  The multi-vector form the reference
+ * lacks (callers loop convolve per image, inc/bench.hpp:240-248). */
+int spconv_spmm(const spconv_csr* h, const float* X_dev, int64_t ldx, float* Y_dev, int64_t ldy,
+                int64_t batch, void* stream);
+
+/* End-to-end apply on HOST buffers (X[batch][cols] -> Y[batch][rows], fp32):
+ * chunked host->device copy, spmm and device->host copy, overlapped on
+ * internal streams; returns when Y is complete.  Pinned buffers give full
+ * PCIe overlap. */
+int spconv_convolve_host(const spconv_csr* h, const float* X_host, float* Y_host, int64_t batch);
+
+/* Same with fp64 host buffers (the reference Grid/DenseVector types,
+ * inc/grid.hpp:18-24): narrowed to fp32 on the way in, widened on the way
+ * out.  Used by the drop-in convolve()/spmv() wrappers. */
+int spconv_convolve_host_f64(const spconv_csr* h, const double* X_host, double* Y_host,
+                             int64_t batch);
+
+/* Frees the handle and its device memory (synchronises its device). */
+int spconv_csr_free(spconv_csr* h);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPCONV_B200_H */

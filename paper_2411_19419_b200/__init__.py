@@ -1,0 +1,287 @@
+"""B200-native conv-as-SpMV (arXiv 2411.19419) -- Python front-end over the C ABI.
+
+The product is ``libspconv_b200.so`` (hand-written sm_100a CUDA kernels behind
+the extern "C" boundary in ``include/spconv_b200.h``).  This module is a thin
+ctypes mirror of the reference's C++ operator API (namespace ``spconv`` in
+/root/reference/proj/include/spconv): ``ConvSpec``, ``Kernel``, ``Transform``,
+``build_transform``, ``convolve``, ``spmv`` keep the reference names, argument
+meaning and error behaviour (``ValueError`` where the reference throws
+``std::invalid_argument``, ``RuntimeError`` for ``std::runtime_error``/CUDA).
+Device tensors are torch CUDA tensors (plumbing only); every arithmetic
+operation on them runs in the CUDA library.  There is no CPU fallback: if the
+library is missing, importing this package raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+from typing import Optional, Sequence, Tuple
+
+import numpy as np
+
+__all__ = [
+    "ConvSpec", "Kernel", "Transform", "build_transform", "convolve", "convolve_batch",
+    "spmv", "spmm", "nnz_bound", "library_path", "lib",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+library_path = os.path.join(_HERE, "libspconv_b200.so")
+
+if not os.path.exists(library_path):
+    raise ImportError(
+        f"{library_path} is missing: build it with `make` (or __graft_entry__.build()); "
+        "there is no CPU fallback for the conv-as-SpMV path")
+
+lib = C.CDLL(library_path)
+
+_i64 = C.c_int64
+_vp = C.c_void_p
+_P = C.POINTER
+
+
+def _decl(name, args, res=C.c_int):
+    f = getattr(lib, name)
+    f.argtypes = args
+    f.restype = res
+    return f
+
+
+_decl("spconv_last_error", [], C.c_char_p)
+_decl("spconv_abi_version", [])
+_decl("spconv_spec_check", [_i64] * 5)
+_decl("spconv_nnz_bound", [_i64] * 5 + [_P(_i64)])
+_decl("spconv_build_csr", [_i64] * 5 + [_vp, C.c_int, _vp, _P(_vp)])
+_decl("spconv_csr_from_host", [_i64, _i64, _vp, _vp, _vp, C.c_int, _vp, _P(_vp)])
+_decl("spconv_csr_shape", [_vp, _P(_i64), _P(_i64), _P(_i64)])
+_decl("spconv_csr_spec", [_vp, _vp])
+_decl("spconv_csr_device_ptrs", [_vp, _P(_vp), _P(_vp), _P(_vp)])
+_decl("spconv_csr_export", [_vp, _vp, _vp, _vp])
+_decl("spconv_csr_copy", [_vp, _vp, _vp, _vp, _vp])
+_decl("spconv_spmv", [_vp, _vp, _vp, _vp])
+_decl("spconv_spmm", [_vp, _vp, _i64, _vp, _i64, _i64, _vp])
+_decl("spconv_convolve_host", [_vp, _vp, _vp, _i64])
+_decl("spconv_convolve_host_f64", [_vp, _vp, _vp, _i64])
+_decl("spconv_csr_free", [_vp])
+
+
+def _check(rc: int) -> None:
+    if rc == 0:
+        return
+    msg = lib.spconv_last_error().decode()
+    if rc == 1:
+        raise ValueError(msg)
+    raise RuntimeError(msg)
+
+
+def _ptr(a) -> int:
+    """Address of a numpy array or torch tensor (no copies)."""
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    return a.data_ptr()
+
+
+def _stream_handle(stream) -> Optional[int]:
+    if stream is None:
+        try:
+            import torch
+            if torch.cuda.is_available():
+                return torch.cuda.current_stream().cuda_stream
+        except ImportError:
+            pass
+        return None
+    return getattr(stream, "cuda_stream", stream)
+
+
+@dataclass(frozen=True)
+class ConvSpec:
+    """m x n input, k x k kernel, stride s, zero padding p (inc/conv.hpp:33-71)."""
+    m: int
+    n: int
+    k: int
+    s: int = 1
+    p: int = 0
+
+    def __post_init__(self):
+        _check(lib.spconv_spec_check(self.m, self.n, self.k, self.s, self.p))
+
+    @property
+    def m_out(self) -> int:
+        return (self.m + 2 * self.p - self.k) // self.s + 1
+
+    @property
+    def n_out(self) -> int:
+        return (self.n + 2 * self.p - self.k) // self.s + 1
+
+    @property
+    def input_len(self) -> int:
+        return self.m * self.n
+
+    @property
+    def output_len(self) -> int:
+        return self.m_out * self.n_out
+
+    def str(self) -> str:
+        return f"(m={self.m}, n={self.n}, k={self.k}, s={self.s}, p={self.p})"
+
+
+class Kernel:
+    """Dense k x k kernel, row-major, unflipped (inc/conv.hpp:74-96)."""
+
+    def __init__(self, k: int, values: Sequence[float]):
+        if k < 1:
+            raise ValueError("Kernel: side must be >= 1")
+        v = np.asarray(values, dtype=np.float64).reshape(-1)
+        if v.size != k * k:
+            raise ValueError(f"Kernel: expected {k * k} values, got {v.size}")
+        self.k = k
+        self.values = v
+
+    def at(self, j: int, i: int) -> float:
+        return float(self.values[j * self.k + i])
+
+
+def nnz_bound(spec: ConvSpec) -> int:
+    """Theorem 2.1 total (inc/analysis.hpp:56-66)."""
+    out = _i64()
+    _check(lib.spconv_nnz_bound(spec.m, spec.n, spec.k, spec.s, spec.p, C.byref(out)))
+    return out.value
+
+
+class Transform:
+    """Device-resident T = C*P plus its geometry (inc/conv.hpp:165-168).
+
+    ``spec`` is None for a generic CSR uploaded with :meth:`from_host`."""
+
+    def __init__(self, handle: int, spec: Optional[ConvSpec], device: int):
+        self._h = _vp(handle)
+        self.spec = spec
+        self.device = device
+        r, c, z = _i64(), _i64(), _i64()
+        _check(lib.spconv_csr_shape(self._h, C.byref(r), C.byref(c), C.byref(z)))
+        self.rows, self.cols, self.nnz = r.value, c.value, z.value
+
+    @classmethod
+    def from_host(cls, rows: int, cols: int, ptr, idx, val, device: int = 0, stream=None):
+        ptr = np.ascontiguousarray(ptr, np.int64)
+        idx = np.ascontiguousarray(idx, np.int64)
+        val = np.ascontiguousarray(val, np.float64)
+        h = _vp()
+        _check(lib.spconv_csr_from_host(rows, cols, ptr.ctypes.data, idx.ctypes.data,
+                                        val.ctypes.data, device, _stream_handle(stream),
+                                        C.byref(h)))
+        return cls(h.value, None, device)
+
+    @property
+    def handle(self) -> int:
+        return self._h.value
+
+    def export(self) -> Tuple[np.ndarray, np.ndarray, np.ndarray]:
+        """ptr(), idx(), val() widened to the reference types (inc/sparse.hpp:128-130)."""
+        ptr = np.empty(self.rows + 1, np.int64)
+        idx = np.empty(max(self.nnz, 1), np.int64)
+        val = np.empty(max(self.nnz, 1), np.float64)
+        _check(lib.spconv_csr_export(self._h, ptr.ctypes.data, idx.ctypes.data, val.ctypes.data))
+        return ptr, idx[: self.nnz], val[: self.nnz]
+
+    def device_ptrs(self) -> Tuple[int, int, int]:
+        a, b, c = _vp(), _vp(), _vp()
+        _check(lib.spconv_csr_device_ptrs(self._h, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
+    def copy_native(self, row_ptr, col_idx, vals, stream=None) -> None:
+        """Native int32/int32/fp32 arrays into caller buffers (numpy or torch,
+        host or device); synchronous."""
+        _check(lib.spconv_csr_copy(self._h, _ptr(row_ptr), _ptr(col_idx), _ptr(vals),
+                                   _stream_handle(stream)))
+
+    def close(self) -> None:
+        if self._h and self._h.value:
+            lib.spconv_csr_free(self._h)
+            self._h = _vp()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def build_transform(kern: Kernel, spec: ConvSpec, device: int = 0, stream=None) -> Transform:
+    """On-device CSR build of T (replaces inc/conv.hpp:179-204)."""
+    if kern.k != spec.k:
+        raise ValueError(f"build_conv_matrix: kernel side {kern.k} does not match spec {spec.str()}")
+    k32 = np.ascontiguousarray(kern.values, np.float32)
+    h = _vp()
+    _check(lib.spconv_build_csr(spec.m, spec.n, spec.k, spec.s, spec.p, k32.ctypes.data, device,
+                                _stream_handle(stream), C.byref(h)))
+    return Transform(h.value, spec, device)
+
+
+def _dev_f32(t, what):
+    import torch
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float32):
+        raise ValueError(f"{what}: expected a CUDA float32 tensor")
+    return t
+
+
+def spmv(t: Transform, x, y=None, stream=None):
+    """y = T x on device (replaces inc/sparse.hpp:214-261); x, y CUDA float32."""
+    import torch
+    x = _dev_f32(x, "spmv")
+    if x.numel() != t.cols:
+        raise ValueError(f"spmv: matrix has {t.cols} columns but vector has {x.numel()} elements")
+    x = x.contiguous()
+    if y is None:
+        y = torch.empty(t.rows, dtype=torch.float32, device=x.device)
+    _check(lib.spconv_spmv(t._h, x.data_ptr(), y.data_ptr(), _stream_handle(stream)))
+    return y
+
+
+def spmm(t: Transform, X, Y=None, stream=None):
+    """Y[b] = T X[b] on device; X [batch, cols] CUDA float32 (row stride = ldx)."""
+    import torch
+    X = _dev_f32(X, "spmm")
+    if X.dim() != 2 or X.shape[1] != t.cols or X.stride(1) != 1:
+        raise ValueError(f"spmm: expected X of shape [batch, {t.cols}] with unit column stride")
+    if Y is None:
+        Y = torch.empty(X.shape[0], t.rows, dtype=torch.float32, device=X.device)
+    _check(lib.spconv_spmm(t._h, X.data_ptr(), X.stride(0), Y.data_ptr(), Y.stride(0), X.shape[0],
+                           _stream_handle(stream)))
+    return Y
+
+
+def convolve_batch(t: Transform, X_host, Y_host=None):
+    """End-to-end apply on HOST fp32 buffers [batch, cols] -> [batch, rows]
+    (H2D, SpMM and D2H pipelined inside the library)."""
+    if isinstance(X_host, np.ndarray):
+        X_host = np.ascontiguousarray(X_host, np.float32)
+        batch = X_host.shape[0] if X_host.ndim == 2 else 1
+        if Y_host is None:
+            Y_host = np.empty((batch, t.rows), np.float32)
+    else:  # torch CPU tensor (pinned for full overlap)
+        import torch
+        assert X_host.device.type == "cpu" and X_host.dtype == torch.float32 and X_host.is_contiguous()
+        batch = X_host.shape[0] if X_host.dim() == 2 else 1
+        if Y_host is None:
+            Y_host = torch.empty(batch, t.rows, dtype=torch.float32, pin_memory=X_host.is_pinned())
+    n = X_host.size if isinstance(X_host, np.ndarray) else X_host.numel()
+    if n != batch * t.cols:
+        raise ValueError(f"convolve_batch: expected {batch}x{t.cols} input values, got {n}")
+    _check(lib.spconv_convolve_host(t._h, _ptr(X_host), _ptr(Y_host), batch))
+    return Y_host
+
+
+def convolve(t: Transform, a) -> np.ndarray:
+    """Reference-semantics apply of one m x n grid (inc/conv.hpp:207-215):
+    fp64 in, fp64 out (fp32 device arithmetic in between)."""
+    a = np.asarray(a, dtype=np.float64)
+    if t.spec is None:
+        raise ValueError("convolve: transform has no geometry (generic CSR)")
+    if a.ndim != 2 or a.shape != (t.spec.m, t.spec.n):
+        r, c = (a.shape + (1, 1))[:2] if a.ndim >= 1 else (0, 0)
+        raise ValueError(f"convolve: input is {r}x{c} but transform expects {t.spec.str()}")
+    a = np.ascontiguousarray(a)
+    out = np.empty(t.rows, np.float64)
+    _check(lib.spconv_convolve_host_f64(t._h, a.ctypes.data, out.ctypes.data, 1))
+    return out.reshape(t.spec.m_out, t.spec.n_out)

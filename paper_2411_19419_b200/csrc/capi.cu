@@ -1,0 +1,614 @@
+// capi.cu -- the extern "C" boundary declared in include/spconv_b200.h.
+//
+// Host-side orchestration only: argument validation with the reference's
+// exception messages, the O(k^2 + m_out + n_out) host tables of the closed-form
+// CSR build, kernel-path selection, and the chunked host<->device pipeline of
+// spconv_convolve_host.  All arithmetic on T and on images happens in the CUDA
+// kernels of csr_build.cu / spmm.cu; there is no CPU fallback.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/spconv_b200.h"
+#include "internal.h"
+
+using spb::Geom;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    return fail(SPCONV_ECUDA, std::string(what) + ": " + cudaGetErrorName(e) + " (" +
+                                  cudaGetErrorString(e) + ")");
+}
+
+#define CK(call)                                              \
+    do {                                                      \
+        cudaError_t e_ = (call);                              \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call);   \
+    } while (0)
+
+// Restores the caller's current device on scope exit.
+struct DeviceGuard {
+    int prev = -1;
+    cudaError_t err = cudaSuccess;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) err = cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+std::string spec_str(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p) {
+    char buf[160];
+    std::snprintf(buf, sizeof buf, "(m=%lld, n=%lld, k=%lld, s=%lld, p=%lld)", (long long)m,
+                  (long long)n, (long long)k, (long long)s, (long long)p);
+    return buf;
+}
+
+// inc/conv.hpp:42-47 (same messages).
+int check_spec(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p) {
+    if (m < 1 || n < 1 || k < 1 || s < 1 || p < 0)
+        return fail(SPCONV_EINVAL,
+                    "ConvSpec: need m,n,k,s >= 1 and p >= 0, got " + spec_str(m, n, k, s, p));
+    if (k > m + 2 * p || k > n + 2 * p)
+        return fail(SPCONV_EINVAL, "ConvSpec: kernel larger than padded input, " +
+                                       spec_str(m, n, k, s, p));
+    return SPCONV_OK;
+}
+
+Geom make_geom(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p) {
+    Geom g{m, n, k, s, p, (m + 2 * p - k) / s + 1, (n + 2 * p - k) / s + 1};
+    return g;
+}
+
+// Valid tap range along one axis (see csr_build.cu).
+inline void tap_range(int64_t x, int64_t dim, int64_t k, int64_t s, int64_t p, int64_t& lo,
+                      int64_t& hi) {
+    lo = std::max<int64_t>(0, p - s * x);
+    hi = std::min<int64_t>(k, dim + p - s * x);
+    lo = std::min(lo, k);
+    if (hi < lo) hi = lo;
+}
+
+// Host tables of the closed-form build.  Returns total nnz and the max row count.
+struct HostTables {
+    std::vector<float> taps;
+    std::vector<int32_t> sat;
+    std::vector<int64_t> px;
+    int64_t nnz = 0;
+    int64_t k2max = 0;
+};
+
+void make_tables(const Geom& g, const float* kernel, HostTables& ht) {
+    const int64_t k = g.k, k1 = k + 1;
+    ht.taps.assign(kernel, kernel + k * k);
+    ht.sat.assign((size_t)(k1 * k1), 0);
+    for (int64_t j = 0; j < k; ++j)
+        for (int64_t i = 0; i < k; ++i)
+            ht.sat[(j + 1) * k1 + i + 1] = ht.sat[j * k1 + i + 1] + ht.sat[(j + 1) * k1 + i] -
+                                           ht.sat[j * k1 + i] + (kernel[j * k + i] != 0.0f ? 1 : 0);
+    auto rect = [&](int64_t jlo, int64_t jhi, int64_t ilo, int64_t ihi) -> int64_t {
+        return ht.sat[jhi * k1 + ihi] - ht.sat[jlo * k1 + ihi] - ht.sat[jhi * k1 + ilo] +
+               ht.sat[jlo * k1 + ilo];
+    };
+    // cntY[i] = #{y : i in I(y)} via a difference array over the y-ranges.
+    std::vector<int64_t> diff((size_t)k1, 0);
+    std::vector<std::pair<int64_t, int64_t>> yr;  // distinct (ilo, ihi)
+    for (int64_t y = 0; y < g.no; ++y) {
+        int64_t lo, hi;
+        tap_range(y, g.n, k, g.s, g.p, lo, hi);
+        diff[lo] += 1;
+        diff[hi] -= 1;
+        if (yr.empty() || yr.back() != std::make_pair(lo, hi)) yr.emplace_back(lo, hi);
+    }
+    std::vector<int64_t> cnty((size_t)k, 0);
+    int64_t run = 0;
+    for (int64_t i = 0; i < k; ++i) cnty[i] = (run += diff[i]);
+    // W[j] = sum_i nz[j][i] * cntY[i];  RowTot(x) = sum_{j in J(x)} W[j].
+    std::vector<int64_t> pw((size_t)k1, 0);
+    for (int64_t j = 0; j < k; ++j) {
+        int64_t w = 0;
+        for (int64_t i = 0; i < k; ++i) w += (kernel[j * k + i] != 0.0f ? 1 : 0) * cnty[i];
+        pw[j + 1] = pw[j] + w;
+    }
+    std::sort(yr.begin(), yr.end());
+    yr.erase(std::unique(yr.begin(), yr.end()), yr.end());
+    ht.px.assign((size_t)(g.mo + 1), 0);
+    ht.k2max = 0;
+    std::pair<int64_t, int64_t> last_xr(-1, -1);
+    for (int64_t x = 0; x < g.mo; ++x) {
+        int64_t jlo, jhi;
+        tap_range(x, g.m, k, g.s, g.p, jlo, jhi);
+        ht.px[x + 1] = ht.px[x] + (pw[jhi] - pw[jlo]);
+        if (std::make_pair(jlo, jhi) != last_xr) {
+            last_xr = {jlo, jhi};
+            for (auto& q : yr) ht.k2max = std::max(ht.k2max, rect(jlo, jhi, q.first, q.second));
+        }
+    }
+    ht.nnz = ht.px[g.mo];
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+// Kernel-path selection (SPCONV_B200_PATH=auto|tiled|generic; auto by default).
+int path_override() {
+    const char* e = std::getenv("SPCONV_B200_PATH");
+    if (!e) return 0;
+    if (!std::strcmp(e, "tiled")) return 1;
+    if (!std::strcmp(e, "generic")) return 2;
+    if (!std::strcmp(e, "tiled_notma")) return 3;
+    return 0;
+}
+
+int run_spmm(const spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
+             int64_t batch, cudaStream_t st) {
+    if (batch == 0) return SPCONV_OK;
+    const int force = path_override();
+    bool tiled = h->is_conv && force != 2;
+    spb::TiledParams tp{};
+    int bt = 8;
+    size_t smem = 0;
+    if (tiled) {
+        const Geom& g = h->g;
+        bt = batch >= 8 ? 8 : batch >= 4 ? 4 : batch >= 2 ? 2 : 1;
+        const int k2max = std::max(h->k2max, 1);
+        // Tile height: keep the per-CTA (off, val) table <= 64 KB.
+        int th = 8;
+        while (th > 1 && (size_t)k2max * th * 32 * 8 > 64 * 1024) th >>= 1;
+        const int64_t wr = (th - 1) * g.s + g.k;
+        const int64_t wc = ((31 * g.s + g.k + 3) + 3) & ~int64_t(3);
+        const bool geom_ok = wr <= 256 && wc <= 256 && g.m < (1ll << 30) && g.n < (1ll << 30);
+        const bool align_ok = (g.n % 4 == 0) && (ldx % 4 == 0) &&
+                              (reinterpret_cast<uintptr_t>(X) % 16 == 0) && encode_fn() != nullptr &&
+                              force != 3;
+        int stages = align_ok ? 4 : 1;
+        while (true) {
+            smem = spb::tiled_smem_bytes(th, (int)wr, (int)wc, k2max, bt, stages);
+            if (smem <= 200 * 1024) break;
+            if (stages > 2) --stages;
+            else if (bt > 1) bt >>= 1;
+            else break;
+        }
+        if (smem > 227 * 1024 || !geom_ok || batch > INT32_MAX) {
+            tiled = false;
+        } else {
+            tp.row_ptr = h->row_ptr;
+            tp.col_idx = h->col_idx;
+            tp.vals = h->vals;
+            tp.X = X;
+            tp.ldx = ldx;
+            tp.Y = Y;
+            tp.ldy = ldy;
+            tp.batch = (int)batch;
+            tp.m = (int)g.m;
+            tp.n = (int)g.n;
+            tp.s = (int)g.s;
+            tp.p = (int)g.p;
+            tp.mo = (int)g.mo;
+            tp.no = (int)g.no;
+            tp.th = th;
+            tp.tiles_y = (int)((g.no + 31) / 32);
+            tp.wr = (int)wr;
+            tp.wc = (int)wc;
+            tp.k2max = k2max;
+            tp.stages = stages;
+            tp.use_tma = align_ok ? 1 : 0;
+            CUtensorMap tmap;
+            std::memset(&tmap, 0, sizeof tmap);
+            if (align_ok) {
+                const cuuint64_t dims[3] = {(cuuint64_t)g.n, (cuuint64_t)g.m, (cuuint64_t)batch};
+                const cuuint64_t strides[2] = {(cuuint64_t)(g.n * 4), (cuuint64_t)(ldx * 4)};
+                const cuuint32_t box[3] = {(cuuint32_t)wc, (cuuint32_t)wr, (cuuint32_t)bt};
+                const cuuint32_t estr[3] = {1, 1, 1};
+                CUresult cr = encode_fn()(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                                          const_cast<float*>(X), dims, strides, box, estr,
+                                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                if (cr != CUDA_SUCCESS) {
+                    return fail(SPCONV_ECUDA, "cuTensorMapEncodeTiled failed with CUresult " +
+                                                  std::to_string((int)cr));
+                }
+            }
+            CK(spb::launch_tiled(tp, &tmap, bt, smem, st));
+            return SPCONV_OK;
+        }
+    }
+    if (force == 1 && h->is_conv) return fail(SPCONV_EINVAL, "SPCONV_B200_PATH=tiled: geometry unsupported");
+    spb::GenericParams gp{h->row_ptr, h->col_idx, h->vals, X, ldx, Y, ldy, (int)h->rows, (int)batch};
+    CK(spb::launch_generic(gp, st));
+    return SPCONV_OK;
+}
+
+void free_ws(spconv_csr* h) {
+    for (int i = 0; i < 2; ++i) {
+        if (h->ws_x[i]) cudaFree(h->ws_x[i]);
+        if (h->ws_y[i]) cudaFree(h->ws_y[i]);
+        h->ws_x[i] = h->ws_y[i] = nullptr;
+    }
+    for (int s = 0; s < 3; ++s) {
+        for (int i = 0; i < 2; ++i)
+            if (h->ws_ev[s][i]) cudaEventDestroy(h->ws_ev[s][i]), h->ws_ev[s][i] = nullptr;
+        if (h->ws_stream[s]) cudaStreamDestroy(h->ws_stream[s]), h->ws_stream[s] = nullptr;
+    }
+    h->ws_chunk = 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* spconv_last_error(void) { return g_err.c_str(); }
+
+int spconv_abi_version(void) { return 100; }
+
+int spconv_spec_check(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p) {
+    return check_spec(m, n, k, s, p);
+}
+
+int spconv_nnz_bound(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p, int64_t* out) {
+    if (int rc = check_spec(m, n, k, s, p)) return rc;
+    if (!out) return fail(SPCONV_EINVAL, "spconv_nnz_bound: null output");
+    // inc/analysis.hpp:56-66 factorises: (sum_x rows(x)) * (sum_y cols(y)).
+    const Geom g = make_geom(m, n, k, s, p);
+    int64_t sx = 0, sy = 0, lo, hi;
+    for (int64_t x = 0; x < g.mo; ++x) tap_range(x, m, k, s, p, lo, hi), sx += hi - lo;
+    for (int64_t y = 0; y < g.no; ++y) tap_range(y, n, k, s, p, lo, hi), sy += hi - lo;
+    *out = sx * sy;
+    return SPCONV_OK;
+}
+
+int spconv_build_csr(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
+                     const float* kernel_kxk, int device, void* stream, spconv_csr** out) {
+    if (int rc = check_spec(m, n, k, s, p)) return rc;
+    if (!kernel_kxk || !out) return fail(SPCONV_EINVAL, "spconv_build_csr: null argument");
+    *out = nullptr;
+    const Geom g = make_geom(m, n, k, s, p);
+    if (m * n >= (1ll << 31) || g.mo * g.no >= (1ll << 31))
+        return fail(SPCONV_EINVAL, "spconv_build_csr: " + spec_str(m, n, k, s, p) +
+                                       " exceeds the int32 device index range");
+    HostTables ht;
+    make_tables(g, kernel_kxk, ht);
+    if (ht.nnz >= (1ll << 31))
+        return fail(SPCONV_EINVAL, "spconv_build_csr: nnz " + std::to_string(ht.nnz) +
+                                       " exceeds the int32 device index range");
+    DeviceGuard dg(device);
+    if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+
+    auto* h = new (std::nothrow) spconv_csr();
+    if (!h) return fail(SPCONV_ECUDA, "out of host memory");
+    h->device = device;
+    h->is_conv = true;
+    h->g = g;
+    h->rows = g.mo * g.no;
+    h->cols = m * n;
+    h->nnz = ht.nnz;
+    h->k2max = (int)ht.k2max;
+
+    // One allocation for the CSR, one for the build tables.
+    const size_t rp_bytes = ((size_t)(h->rows + 1) * 4 + 255) & ~size_t(255);
+    const size_t ix_bytes = ((size_t)std::max<int64_t>(ht.nnz, 1) * 4 + 255) & ~size_t(255);
+    char* csr = nullptr;
+    cudaError_t e = cudaMalloc(&csr, rp_bytes + 2 * ix_bytes);
+    if (e != cudaSuccess) {
+        delete h;
+        return cuda_fail(e, "cudaMalloc(CSR)");
+    }
+    h->row_ptr = reinterpret_cast<int32_t*>(csr);
+    h->col_idx = reinterpret_cast<int32_t*>(csr + rp_bytes);
+    h->vals = reinterpret_cast<float*>(csr + rp_bytes + ix_bytes);
+
+    const size_t taps_b = ((ht.taps.size() * 4) + 255) & ~size_t(255);
+    const size_t sat_b = ((ht.sat.size() * 4) + 255) & ~size_t(255);
+    const size_t px_b = ht.px.size() * 8;
+    char* tab = nullptr;
+    e = cudaMallocAsync(&tab, taps_b + sat_b + px_b, st);
+    if (e != cudaSuccess) {
+        cudaFree(csr);
+        delete h;
+        return cuda_fail(e, "cudaMallocAsync(tables)");
+    }
+    // Pageable copies are staged by the driver before the call returns.
+    cudaMemcpyAsync(tab, ht.taps.data(), ht.taps.size() * 4, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(tab + taps_b, ht.sat.data(), ht.sat.size() * 4, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(tab + taps_b + sat_b, ht.px.data(), px_b, cudaMemcpyHostToDevice, st);
+
+    spb::BuildParams bp{};
+    bp.m = (int)m;
+    bp.n = (int)n;
+    bp.k = (int)k;
+    bp.s = (int)s;
+    bp.p = (int)p;
+    bp.mo = (int)g.mo;
+    bp.no = (int)g.no;
+    bp.rows = (int)h->rows;
+    bp.t.taps = reinterpret_cast<const float*>(tab);
+    bp.t.sat = reinterpret_cast<const int32_t*>(tab + taps_b);
+    bp.t.px = reinterpret_cast<const int64_t*>(tab + taps_b + sat_b);
+    bp.row_ptr = h->row_ptr;
+    bp.col_idx = h->col_idx;
+    bp.vals = h->vals;
+    // Stage entries through shared memory when a CTA's worst case fits.
+    int block = 256;
+    const int64_t k2 = k * k;
+    while (block > 64 && (size_t)block * k2 * 8 > 64 * 1024) block >>= 1;
+    size_t smem = 0;
+    bp.stage = 0;
+    if ((size_t)block * k2 * 8 <= 96 * 1024) {
+        bp.stage = 1;
+        smem = (size_t)(((block * k2 + 3) & ~int64_t(3)) * 4) * 2;
+    } else {
+        block = 256;
+    }
+    e = spb::launch_csr_build(bp, block, smem, st);
+    cudaFreeAsync(tab, st);
+    if (e != cudaSuccess) {
+        cudaStreamSynchronize(st);
+        cudaFree(csr);
+        delete h;
+        return cuda_fail(e, "csr_build launch");
+    }
+    *out = h;
+    return SPCONV_OK;
+}
+
+int spconv_csr_from_host(int64_t rows, int64_t cols, const int64_t* row_ptr,
+                         const int64_t* col_idx, const double* vals, int device, void* stream,
+                         spconv_csr** out) {
+    if (!out || !row_ptr) return fail(SPCONV_EINVAL, "spconv_csr_from_host: null argument");
+    *out = nullptr;
+    if (rows < 1 || cols < 1)
+        return fail(SPCONV_EINVAL, "Triplets: dimensions must be at least 1x1, got " +
+                                       std::to_string(rows) + "x" + std::to_string(cols));
+    if (rows >= (1ll << 31) || cols >= (1ll << 31))
+        return fail(SPCONV_EINVAL, "spconv_csr_from_host: dimensions exceed the int32 range");
+    const int64_t nnz = row_ptr[rows];
+    if (row_ptr[0] != 0 || nnz < 0 || nnz >= (1ll << 31))
+        return fail(SPCONV_EINVAL, "spconv_csr_from_host: bad row_ptr");
+    std::vector<int32_t> rp((size_t)rows + 1), ci((size_t)std::max<int64_t>(nnz, 1));
+    std::vector<float> vv((size_t)std::max<int64_t>(nnz, 1));
+    int64_t k2max = 0;
+    for (int64_t r = 0; r < rows; ++r) {
+        if (row_ptr[r + 1] < row_ptr[r])
+            return fail(SPCONV_EINVAL, "spconv_csr_from_host: row_ptr not non-decreasing");
+        k2max = std::max(k2max, row_ptr[r + 1] - row_ptr[r]);
+        for (int64_t e = row_ptr[r]; e < row_ptr[r + 1]; ++e) {
+            if (col_idx[e] < 0 || col_idx[e] >= cols || (e > row_ptr[r] && col_idx[e] <= col_idx[e - 1]))
+                return fail(SPCONV_EINVAL, "spconv_csr_from_host: column indices must be in range "
+                                           "and strictly ascending per row");
+        }
+        rp[r] = (int32_t)row_ptr[r];
+    }
+    rp[rows] = (int32_t)nnz;
+    for (int64_t e = 0; e < nnz; ++e) ci[e] = (int32_t)col_idx[e], vv[e] = (float)vals[e];
+    DeviceGuard dg(device);
+    if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
+    auto* h = new (std::nothrow) spconv_csr();
+    if (!h) return fail(SPCONV_ECUDA, "out of host memory");
+    h->device = device;
+    h->rows = rows;
+    h->cols = cols;
+    h->nnz = nnz;
+    h->k2max = (int)k2max;
+    const size_t rp_bytes = ((size_t)(rows + 1) * 4 + 255) & ~size_t(255);
+    const size_t ix_bytes = (ci.size() * 4 + 255) & ~size_t(255);
+    char* csr = nullptr;
+    cudaError_t e = cudaMalloc(&csr, rp_bytes + 2 * ix_bytes);
+    if (e != cudaSuccess) {
+        delete h;
+        return cuda_fail(e, "cudaMalloc(CSR)");
+    }
+    h->row_ptr = reinterpret_cast<int32_t*>(csr);
+    h->col_idx = reinterpret_cast<int32_t*>(csr + rp_bytes);
+    h->vals = reinterpret_cast<float*>(csr + rp_bytes + ix_bytes);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    e = cudaMemcpyAsync(h->row_ptr, rp.data(), rp.size() * 4, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(h->col_idx, ci.data(), ci.size() * 4, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(h->vals, vv.data(), vv.size() * 4, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // host vectors die here
+    if (e != cudaSuccess) {
+        cudaFree(csr);
+        delete h;
+        return cuda_fail(e, "spconv_csr_from_host upload");
+    }
+    *out = h;
+    return SPCONV_OK;
+}
+
+int spconv_csr_shape(const spconv_csr* h, int64_t* rows, int64_t* cols, int64_t* nnz) {
+    if (!h) return fail(SPCONV_EINVAL, "null handle");
+    if (rows) *rows = h->rows;
+    if (cols) *cols = h->cols;
+    if (nnz) *nnz = h->nnz;
+    return SPCONV_OK;
+}
+
+int spconv_csr_spec(const spconv_csr* h, int64_t spec5[5]) {
+    if (!h || !spec5) return fail(SPCONV_EINVAL, "null argument");
+    if (!h->is_conv) return fail(SPCONV_EINVAL, "spconv_csr_spec: handle is a generic CSR");
+    spec5[0] = h->g.m;
+    spec5[1] = h->g.n;
+    spec5[2] = h->g.k;
+    spec5[3] = h->g.s;
+    spec5[4] = h->g.p;
+    return SPCONV_OK;
+}
+
+int spconv_csr_device_ptrs(const spconv_csr* h, const int32_t** row_ptr, const int32_t** col_idx,
+                           const float** vals) {
+    if (!h) return fail(SPCONV_EINVAL, "null handle");
+    if (row_ptr) *row_ptr = h->row_ptr;
+    if (col_idx) *col_idx = h->col_idx;
+    if (vals) *vals = h->vals;
+    return SPCONV_OK;
+}
+
+int spconv_csr_export(const spconv_csr* h, int64_t* row_ptr, int64_t* col_idx, double* vals) {
+    if (!h) return fail(SPCONV_EINVAL, "null handle");
+    DeviceGuard dg(h->device);
+    if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
+    CK(cudaDeviceSynchronize());
+    if (row_ptr) {
+        std::vector<int32_t> tmp((size_t)h->rows + 1);
+        CK(cudaMemcpy(tmp.data(), h->row_ptr, tmp.size() * 4, cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < tmp.size(); ++i) row_ptr[i] = tmp[i];
+    }
+    if (col_idx && h->nnz > 0) {
+        std::vector<int32_t> tmp((size_t)h->nnz);
+        CK(cudaMemcpy(tmp.data(), h->col_idx, tmp.size() * 4, cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < tmp.size(); ++i) col_idx[i] = tmp[i];
+    }
+    if (vals && h->nnz > 0) {
+        std::vector<float> tmp((size_t)h->nnz);
+        CK(cudaMemcpy(tmp.data(), h->vals, tmp.size() * 4, cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < tmp.size(); ++i) vals[i] = tmp[i];
+    }
+    return SPCONV_OK;
+}
+
+int spconv_csr_copy(const spconv_csr* h, int32_t* row_ptr, int32_t* col_idx, float* vals,
+                    void* stream) {
+    if (!h) return fail(SPCONV_EINVAL, "null handle");
+    DeviceGuard dg(h->device);
+    if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (row_ptr)
+        CK(cudaMemcpyAsync(row_ptr, h->row_ptr, (size_t)(h->rows + 1) * 4, cudaMemcpyDefault, st));
+    if (col_idx && h->nnz > 0)
+        CK(cudaMemcpyAsync(col_idx, h->col_idx, (size_t)h->nnz * 4, cudaMemcpyDefault, st));
+    if (vals && h->nnz > 0)
+        CK(cudaMemcpyAsync(vals, h->vals, (size_t)h->nnz * 4, cudaMemcpyDefault, st));
+    CK(cudaStreamSynchronize(st));
+    return SPCONV_OK;
+}
+
+int spconv_spmv(const spconv_csr* h, const float* x_dev, float* y_dev, void* stream) {
+    if (!h || !x_dev || !y_dev) return fail(SPCONV_EINVAL, "spconv_spmv: null argument");
+    DeviceGuard dg(h->device);
+    if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
+    return run_spmm(h, x_dev, h->cols, y_dev, h->rows, 1, static_cast<cudaStream_t>(stream));
+}
+
+int spconv_spmm(const spconv_csr* h, const float* X_dev, int64_t ldx, float* Y_dev, int64_t ldy,
+                int64_t batch, void* stream) {
+    if (!h) return fail(SPCONV_EINVAL, "spconv_spmm: null handle");
+    if (batch < 0) return fail(SPCONV_EINVAL, "spconv_spmm: negative batch");
+    if (batch > 0 && (!X_dev || !Y_dev)) return fail(SPCONV_EINVAL, "spconv_spmm: null buffer");
+    if (ldx < h->cols || ldy < h->rows)
+        return fail(SPCONV_EINVAL, "spconv_spmm: leading dimension smaller than the matrix");
+    DeviceGuard dg(h->device);
+    if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
+    return run_spmm(h, X_dev, ldx, Y_dev, ldy, batch, static_cast<cudaStream_t>(stream));
+}
+
+int spconv_convolve_host(const spconv_csr* hc, const float* X_host, float* Y_host, int64_t batch) {
+    if (!hc) return fail(SPCONV_EINVAL, "spconv_convolve_host: null handle");
+    if (batch < 0) return fail(SPCONV_EINVAL, "spconv_convolve_host: negative batch");
+    if (batch == 0) return SPCONV_OK;
+    if (!X_host || !Y_host) return fail(SPCONV_EINVAL, "spconv_convolve_host: null buffer");
+    auto* h = const_cast<spconv_csr*>(hc);  // workspace only; the matrix is untouched
+    std::lock_guard<std::mutex> lk(h->ws_mu);
+    DeviceGuard dg(h->device);
+    if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
+    // Chunks of ~64 MB of input, double-buffered: H2D(c+1) || spmm(c) || D2H(c-1).
+    const int64_t per_img = std::max<int64_t>(h->cols, 1) * 4;
+    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(batch, (64ll << 20) / per_img));
+    if (h->ws_chunk < chunk) {
+        free_ws(h);
+        for (int s = 0; s < 3; ++s) {
+            CK(cudaStreamCreateWithFlags(&h->ws_stream[s], cudaStreamNonBlocking));
+            for (int i = 0; i < 2; ++i)
+                CK(cudaEventCreateWithFlags(&h->ws_ev[s][i], cudaEventDisableTiming));
+        }
+        for (int i = 0; i < 2; ++i) {
+            CK(cudaMalloc(&h->ws_x[i], (size_t)(chunk * h->cols * 4)));
+            CK(cudaMalloc(&h->ws_y[i], (size_t)(chunk * h->rows * 4)));
+        }
+        h->ws_chunk = chunk;
+    }
+    cudaStream_t s_in = h->ws_stream[0], s_cp = h->ws_stream[1], s_out = h->ws_stream[2];
+    cudaEvent_t* ev_in = h->ws_ev[0];
+    cudaEvent_t* ev_cp = h->ws_ev[1];
+    cudaEvent_t* ev_out = h->ws_ev[2];
+    int c = 0;
+    for (int64_t b0 = 0; b0 < batch; b0 += chunk, ++c) {
+        const int i = c & 1;
+        const int64_t nb = std::min(chunk, batch - b0);
+        if (c >= 2) CK(cudaStreamWaitEvent(s_in, ev_cp[i], 0));  // spmm(c-2) done reading ws_x[i]
+        CK(cudaMemcpyAsync(h->ws_x[i], X_host + b0 * h->cols, (size_t)(nb * h->cols * 4),
+                           cudaMemcpyHostToDevice, s_in));
+        CK(cudaEventRecord(ev_in[i], s_in));
+        CK(cudaStreamWaitEvent(s_cp, ev_in[i], 0));
+        if (c >= 2) CK(cudaStreamWaitEvent(s_cp, ev_out[i], 0));  // D2H(c-2) done with ws_y[i]
+        if (int rc = run_spmm(h, h->ws_x[i], h->cols, h->ws_y[i], h->rows, nb, s_cp)) return rc;
+        CK(cudaEventRecord(ev_cp[i], s_cp));
+        CK(cudaStreamWaitEvent(s_out, ev_cp[i], 0));
+        CK(cudaMemcpyAsync(Y_host + b0 * h->rows, h->ws_y[i], (size_t)(nb * h->rows * 4),
+                           cudaMemcpyDeviceToHost, s_out));
+        CK(cudaEventRecord(ev_out[i], s_out));
+    }
+    CK(cudaStreamSynchronize(s_out));
+    CK(cudaStreamSynchronize(s_cp));
+    CK(cudaStreamSynchronize(s_in));
+    return SPCONV_OK;
+}
+
+int spconv_convolve_host_f64(const spconv_csr* h, const double* X_host, double* Y_host,
+                             int64_t batch) {
+    if (!h) return fail(SPCONV_EINVAL, "spconv_convolve_host_f64: null handle");
+    if (batch < 0) return fail(SPCONV_EINVAL, "spconv_convolve_host_f64: negative batch");
+    if (batch == 0) return SPCONV_OK;
+    if (!X_host || !Y_host) return fail(SPCONV_EINVAL, "spconv_convolve_host_f64: null buffer");
+    std::vector<float> xf((size_t)(batch * h->cols)), yf((size_t)(batch * h->rows));
+    for (size_t i = 0; i < xf.size(); ++i) xf[i] = (float)X_host[i];
+    if (int rc = spconv_convolve_host(h, xf.data(), yf.data(), batch)) return rc;
+    for (size_t i = 0; i < yf.size(); ++i) Y_host[i] = yf[i];
+    return SPCONV_OK;
+}
+
+int spconv_csr_free(spconv_csr* h) {
+    if (!h) return SPCONV_OK;
+    {
+        DeviceGuard dg(h->device);
+        cudaDeviceSynchronize();
+        free_ws(h);
+        if (h->row_ptr) cudaFree(h->row_ptr);
+    }
+    delete h;
+    return SPCONV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,174 @@
+// csr_build.cu -- one-pass on-device construction of the CSR of T = C*P.
+//
+// Replaces build_transform (inc/conv.hpp:179-204): build_conv_matrix (:141-162)
+// + build_padding_matrix (:125-135) + spgemm (inc/sparse.hpp:296-342) +
+// SparseMatrix::compile (inc/sparse.hpp:85-119).  Nothing is sorted and no
+// intermediate C or P exists: each row's entries are generated directly in
+// their final (column-ascending) order.
+//
+// Row r = x*n_out + y (inc/conv.hpp:8-12) keeps tap (j,i) iff the tap lands in
+// the input, i.e. j in [jlo(x), jhi(x)), i in [ilo(y), ihi(y)) with
+//   jlo = max(0, p - s*x),  jhi = min(k, m + p - s*x)        (and likewise i),
+// -- the paper's max(0, k - c1(x)) * max(0, k - c2(y)) count
+// (inc/analysis.hpp:21-52) -- AND the tap is not an exact zero
+// (inc/sparse.hpp:335, inc/conv.hpp:201).  Its column is
+//   (s*x + j - p)*n + (s*y + i - p).
+// The count is a summed-area-table query over the (tap != 0) mask, which
+// reduces to the closed form when no tap is zero.
+//
+// row_ptr is closed-form too: the host tabulates px[x] = nnz of all output rows
+// of image rows < x, and a CTA starting at (x0, y0) adds
+//   sum_i nzcol(x0, i) * #{y' < y0 : i in I(y')}
+// (O(k) terms), so every CTA knows its global offset without a grid-wide scan
+// or look-back; a block scan of the per-row counts finishes row_ptr.  Entries
+// are staged in shared memory and written back with coalesced stores, so HBM
+// sees each of the 8*nnz + 4*(rows+1) bytes exactly once.
+#include "internal.h"
+
+namespace spb {
+
+namespace {
+
+__device__ __forceinline__ int warp_incl_scan(int v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += u;
+    }
+    return v;
+}
+
+__device__ __forceinline__ long long warp_sum64(long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ int sat_rect(const int32_t* sat, int k1, int jlo, int jhi, int ilo,
+                                        int ihi) {
+    return __ldg(sat + jhi * k1 + ihi) - __ldg(sat + jlo * k1 + ihi) - __ldg(sat + jhi * k1 + ilo) +
+           __ldg(sat + jlo * k1 + ilo);
+}
+
+// Valid tap range [lo, hi) along one axis for slide position x (see header).
+__device__ __forceinline__ void tap_range(int x, int dim, int k, int s, int p, int& lo, int& hi) {
+    lo = max(0, p - s * x);
+    hi = min(k, dim + p - s * x);
+    lo = min(lo, k);
+    if (hi < lo) hi = lo;
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(256) csr_build_kernel(const BuildParams P) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ int s_warp[32];
+    __shared__ long long s_red[32];
+
+    const int t = threadIdx.x;
+    const int R = blockDim.x;
+    const int nw = R >> 5;
+    const int lane = t & 31, wid = t >> 5;
+    const int k1 = P.k + 1;
+    const int r0 = blockIdx.x * R;
+    const int r = r0 + t;
+
+    // ---- per-row count (Theorem 2.1 with the zero-tap mask) ----
+    int cnt = 0, x = 0, y = 0, jlo = 0, jhi = 0, ilo = 0, ihi = 0;
+    if (r < P.rows) {
+        x = r / P.no;
+        y = r - x * P.no;
+        tap_range(x, P.m, P.k, P.s, P.p, jlo, jhi);
+        tap_range(y, P.n, P.k, P.s, P.p, ilo, ihi);
+        cnt = sat_rect(P.t.sat, k1, jlo, jhi, ilo, ihi);
+    }
+
+    // ---- closed-form global offset of row r0 ----
+    const int x0 = r0 / P.no, y0 = r0 - x0 * P.no;
+    int jlo0, jhi0;
+    tap_range(x0, P.m, P.k, P.s, P.p, jlo0, jhi0);
+    long long part = 0;
+    for (int i = t; i < P.k; i += R) {
+        const int cz = sat_rect(P.t.sat, k1, jlo0, jhi0, i, i + 1);
+        const int lo = (P.p - i <= 0) ? 0 : (P.p - i + P.s - 1) / P.s;
+        const int hi = (P.n + P.p - i - 1 < 0) ? 0 : (P.n + P.p - i - 1) / P.s + 1;
+        const int py = max(0, min(y0, hi) - lo);
+        part += (long long)cz * py;
+    }
+    part = warp_sum64(part);
+    if (lane == 0) s_red[wid] = part;
+
+    // ---- block exclusive scan of counts ----
+    const int inc = warp_incl_scan(cnt);
+    if (lane == 31) s_warp[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        int w = lane < nw ? s_warp[lane] : 0;
+        long long pr = lane < nw ? s_red[lane] : 0;
+        w = warp_incl_scan(w);
+        pr = warp_sum64(pr);
+        s_warp[lane] = w;
+        if (lane == 0) s_red[0] = pr;
+    }
+    __syncthreads();
+    const int excl = inc - cnt + (wid > 0 ? s_warp[wid - 1] : 0);
+    const int total = s_warp[nw - 1];
+    const int base = (int)(__ldg(P.t.px + x0) + s_red[0]);
+
+    if (r < P.rows) {
+        P.row_ptr[r] = base + excl;
+        if (r == P.rows - 1) P.row_ptr[P.rows] = base + excl + cnt;
+    }
+
+    // ---- fill: taps of this row in (j, i) order == column-ascending ----
+    int32_t* dcol;
+    float* dval;
+    int o;
+    if (P.stage) {
+        dcol = reinterpret_cast<int32_t*>(smem);
+        dval = reinterpret_cast<float*>(smem) + ((R * P.k * P.k + 3) & ~3);
+        o = excl;
+    } else {
+        dcol = P.col_idx;
+        dval = P.vals;
+        o = base + excl;
+    }
+    if (r < P.rows && cnt > 0) {
+        const int xr = P.s * x - P.p, yc = P.s * y - P.p;
+        for (int j = jlo; j < jhi; ++j) {
+            const int rowbase = (xr + j) * P.n + yc;
+            const float* tj = P.t.taps + j * P.k;
+            for (int i = ilo; i < ihi; ++i) {
+                const float v = __ldg(tj + i);
+                if (v != 0.0f) {  // drops +-0.0, keeps NaN (inc/sparse.hpp:335)
+                    dcol[o] = rowbase + i;
+                    dval[o] = v;
+                    ++o;
+                }
+            }
+        }
+    }
+    if (P.stage) {
+        __syncthreads();
+        int32_t* gcol = P.col_idx + base;
+        float* gval = P.vals + base;
+        for (int e = t; e < total; e += R) {
+            __stcs(gcol + e, dcol[e]);
+            __stcs(gval + e, dval[e]);
+        }
+    }
+}
+
+cudaError_t launch_csr_build(const BuildParams& bp, int block, size_t smem, cudaStream_t st) {
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(csr_build_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    const int grid = (bp.rows + block - 1) / block;
+    csr_build_kernel<<<grid, block, smem, st>>>(bp);
+    return cudaGetLastError();
+}
+
+}  // namespace spb

@@ -1,0 +1,94 @@
+// internal.h -- shared host/device declarations of the B200 conv-as-SpMV library.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <mutex>
+
+namespace spb {
+
+// Geometry of one padded, strided convolution (inc/conv.hpp:33-62).
+struct Geom {
+    int64_t m, n, k, s, p;
+    int64_t mo, no;  // m_out, n_out (inc/conv.hpp:52-53)
+};
+
+// Host-precomputed tables for the closed-form row_ptr (see csr_build.cu).
+struct BuildTables {
+    const float* taps;     // k*k, fp32, row-major
+    const int32_t* sat;    // (k+1)*(k+1) summed-area table of (tap != 0)
+    const int64_t* px;     // mo+1: nnz of all output rows above image row x
+};
+
+struct BuildParams {
+    int m, n, k, s, p, mo, no;
+    int rows;
+    BuildTables t;
+    int32_t* row_ptr;
+    int32_t* col_idx;
+    float* vals;
+    int stage;  // 1: stage entries in shared memory, 0: direct stores
+};
+
+// Conv-tiled SpMM: one CTA owns a TH x 32 block of output pixels (rows of T)
+// and streams the whole batch through shared memory.
+struct TiledParams {
+    const int32_t* row_ptr;
+    const int32_t* col_idx;
+    const float* vals;
+    const float* X;
+    int64_t ldx;
+    float* Y;
+    int64_t ldy;
+    int batch;
+    int m, n, s, p, mo, no;
+    int th;          // tile height (output rows of the image); tile width is 32
+    int tiles_y;     // tiles across n_out
+    int wr, wc;      // staged input window: rows x cols (wc % 4 == 0)
+    int k2max;       // max stored entries per row of T
+    int stages;      // window pipeline depth (TMA path)
+    int use_tma;
+};
+
+struct GenericParams {
+    const int32_t* row_ptr;
+    const int32_t* col_idx;
+    const float* vals;
+    const float* X;
+    int64_t ldx;
+    float* Y;
+    int64_t ldy;
+    int rows;
+    int batch;
+};
+
+// Launchers (return cudaError_t of the launch).
+cudaError_t launch_csr_build(const BuildParams& bp, int block, size_t smem, cudaStream_t st);
+cudaError_t launch_tiled(const TiledParams& tp, const CUtensorMap* tmap, int bt, size_t smem,
+                         cudaStream_t st);
+cudaError_t launch_generic(const GenericParams& gp, cudaStream_t st);
+
+size_t tiled_smem_bytes(int th, int wr, int wc, int k2max, int bt, int stages);
+
+}  // namespace spb
+
+// The opaque handle of include/spconv_b200.h.
+struct spconv_csr {
+    int device = 0;
+    bool is_conv = false;
+    spb::Geom g{};
+    int64_t rows = 0, cols = 0, nnz = 0;
+    int k2max = 0;                 // max entries in any row
+    int32_t* row_ptr = nullptr;    // device
+    int32_t* col_idx = nullptr;    // device
+    float* vals = nullptr;         // device
+    // Workspace of spconv_convolve_host (lazily created, guarded by ws_mu).
+    std::mutex ws_mu;
+    cudaStream_t ws_stream[3] = {nullptr, nullptr, nullptr};
+    cudaEvent_t ws_ev[3][2] = {};
+    float* ws_x[2] = {nullptr, nullptr};
+    float* ws_y[2] = {nullptr, nullptr};
+    int64_t ws_chunk = 0;
+};

@@ -1,0 +1,95 @@
+"""CPU-only checks of the C-ABI boundary: the product library loads, exports
+every entry point include/*.h declares, keeps the reference's host-side
+semantics (spec validation messages, Theorem 2.1), never touches the oracle,
+and fails loudly (no CPU fallback) when asked to compute without a GPU."""
+import ctypes as C
+import glob
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+from helpers import sweep_specs
+
+import paper_2411_19419_b200 as sp
+
+
+def declared_symbols():
+    names = set()
+    for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
+        src = open(h).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        names |= set(re.findall(r"\b(spconv_[a-z0-9_]+)\s*\(", src))
+    return names
+
+
+def test_library_exports_every_declared_symbol():
+    names = declared_symbols()
+    assert len(names) >= 16
+    lib = C.CDLL(sp.library_path)
+    missing = [n for n in sorted(names) if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_library_is_sm100a_and_oracle_free():
+    so = sp.library_path
+    needed = subprocess.run(["readelf", "-d", so], capture_output=True, text=True).stdout
+    assert "oracle" not in needed and "spconv_ref" not in needed
+    syms = subprocess.run(["nm", "-D", so], capture_output=True, text=True).stdout
+    assert "orc_" not in syms and "ref_" not in syms.replace("spconv_", "")
+    sass = subprocess.run(["cuobjdump", "--list-elf", so], capture_output=True, text=True).stdout
+    assert "sm_100a" in sass
+
+
+def test_abi_version():
+    assert sp.lib.spconv_abi_version() >= 100
+
+
+def test_spec_validation_messages(ref=None):
+    with pytest.raises(ValueError, match=r"^ConvSpec: need m,n,k,s >= 1 and p >= 0, got "
+                                         r"\(m=0, n=3, k=1, s=1, p=0\)$"):
+        sp.ConvSpec(0, 3, 1, 1, 0)
+    with pytest.raises(ValueError, match=r"^ConvSpec: kernel larger than padded input, "
+                                         r"\(m=3, n=3, k=6, s=1, p=1\)$"):
+        sp.ConvSpec(3, 3, 6, 1, 1)
+    with pytest.raises(ValueError, match="Kernel: expected 4 values, got 1"):
+        sp.Kernel(2, [1.0])
+
+
+def test_spec_messages_match_reference(ref):
+    from oracle import RefError
+    for args in [(0, 3, 1, 1, 0), (3, 3, 1, 0, 0), (3, 3, 1, 1, -1), (3, 3, 6, 1, 1), (2, 9, 5, 1, 1)]:
+        with pytest.raises(RefError) as e:
+            ref.spec_check(*args)
+        with pytest.raises(ValueError) as g:
+            sp.ConvSpec(*args)
+        assert str(g.value) == str(e.value)
+
+
+def test_nnz_bound_matches_oracle(orc):
+    for spec in sweep_specs(9):
+        assert sp.nnz_bound(sp.ConvSpec(*spec)) == orc.nnz_bound(*spec)
+    for spec in [(64, 64, 3, 1, 1), (512, 512, 5, 2, 2), (1024, 1024, 3, 1, 1), (4096, 4096, 7, 2, 3),
+                 (257, 193, 11, 1, 10)]:
+        assert sp.nnz_bound(sp.ConvSpec(*spec)) == orc.nnz_bound(*spec)
+    assert sp.nnz_bound(sp.ConvSpec(4096, 4096, 7, 2, 3)) == 205348900
+
+
+def test_no_gpu_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    with pytest.raises(RuntimeError, match="cuda|CUDA"):
+        sp.build_transform(sp.Kernel(3, np.ones(9)), sp.ConvSpec(8, 8, 3, 1, 1))
+
+
+def test_dropin_headers_compile():
+    """The drop-in C++ headers compile standalone (-fsyntax-only)."""
+    src = '#include "spconv/spconv.hpp"\nint main(){ spconv::ConvSpec s(3,3,3,1,1); return (int)s.m_out(); }\n'
+    r = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-Wall", "-Wextra", "-I",
+                        os.path.join(ROOT, "include"), "-x", "c++", "-"], input=src, text=True,
+                       capture_output=True)
+    assert r.returncode == 0, r.stderr

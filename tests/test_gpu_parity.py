@@ -1,0 +1,318 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle.
+
+Structure (row_ptr, col_idx) and values of T are compared BIT-EXACTLY with the
+restatement and, through the golden digests, with the compiled reference's own
+output.  SpMV/SpMM outputs are compared bit-exactly with the fp32 ordered-fmaf
+restatement of spmv_csr_rows (inc/sparse.hpp:180-192) -- the device kernels
+accumulate each row in the same column-ascending order -- and, against the
+fp64 reference, within the north-star tolerance:
+    |y_gpu - y_ref| <= 1e-5 * sum_e |val_e * x_col_e|   (condition-aware relative).
+"""
+import os
+
+import numpy as np
+import pytest
+
+from helpers import CONFIGS, golden_cases, problem, sha, sweep_specs, zero_tap_kernel
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5  # relative fp32 tolerance of BASELINE.json north_star
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return torch
+
+
+@pytest.fixture(scope="module")
+def sp(torch_cuda):
+    import paper_2411_19419_b200 as sp
+    return sp
+
+
+def native_copy(t):
+    ptr = np.empty(t.rows + 1, np.int32)
+    idx = np.empty(max(t.nnz, 1), np.int32)
+    val = np.empty(max(t.nnz, 1), np.float32)
+    t.copy_native(ptr, idx, val)
+    return ptr, idx[: t.nnz], val[: t.nnz]
+
+
+def build(sp, spec, kern):
+    return sp.build_transform(sp.Kernel(spec[2], np.asarray(kern, np.float64)), sp.ConvSpec(*spec))
+
+
+def bits(a):
+    return np.ascontiguousarray(a).view(np.uint32)
+
+
+def assert_same_csr(t, ref_csr):
+    ptr, idx, val = native_copy(t)
+    rp, ri, rv = ref_csr
+    assert np.array_equal(ptr, rp.astype(np.int32))
+    assert np.array_equal(idx, ri.astype(np.int32))
+    assert np.array_equal(bits(val), bits(rv.astype(np.float32)))
+
+
+def run_spmm(torch, sp, t, X, path=None, ldx_pad=0):
+    """X host f32 [B, cols] -> device SpMM -> host [B, rows]."""
+    B, cols = X.shape
+    Xd = torch.zeros(B, cols + ldx_pad, dtype=torch.float32, device="cuda")
+    Xd[:, :cols] = torch.from_numpy(X)
+    old = os.environ.get("SPCONV_B200_PATH")
+    if path:
+        os.environ["SPCONV_B200_PATH"] = path
+    try:
+        Y = sp.spmm(t, Xd[:, :cols])
+    finally:
+        if path:
+            if old is None:
+                del os.environ["SPCONV_B200_PATH"]
+            else:
+                os.environ["SPCONV_B200_PATH"] = old
+    torch.cuda.synchronize()
+    return Y.cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+# CSR build
+# ---------------------------------------------------------------------------
+
+def test_build_config1_matches_reference_arrays(sp, golden):
+    _, npz = golden
+    t = build(sp, CONFIGS[0], npz["c1_kernel"])
+    ptr, idx, val = t.export()
+    assert np.array_equal(ptr, npz["c1_ptr"]) and np.array_equal(idx, npz["c1_idx"])
+    assert np.array_equal(val.view(np.uint64), npz["c1_val"].view(np.uint64))
+
+
+def test_build_zero_tap_fixture(sp, golden):
+    _, npz = golden
+    t = build(sp, (3, 3, 3, 1, 1), npz["zt_kernel"])
+    ptr, idx, val = t.export()
+    assert np.array_equal(ptr, npz["zt_ptr"]) and np.array_equal(idx, npz["zt_idx"])
+    assert np.array_equal(val, npz["zt_val"])
+
+
+def test_build_matches_reference_digests(sp, orc, golden):
+    """Config 2 and every config-5 edge spec (normal + zero-tap kernels): the
+    device CSR, widened, hashes to the reference's own digest."""
+    js, _ = golden
+    for key, spec, kern, _img in golden_cases(orc, js):
+        t = build(sp, spec, kern)
+        d = js["digests"][key]
+        assert t.nnz == d["nnz"], key
+        assert sha(*t.export()) == d["csr"], key
+
+
+def test_build_sweep_vs_oracle(sp, orc):
+    """Every geometry of the m,n <= 9 verify grid, with all-non-zero and zero-tap kernels."""
+    rng = np.random.default_rng(11)
+    for ci, spec in enumerate(sweep_specs(9)):
+        k = spec[2]
+        kern = orc.random_normal_f32(orc.derive_seed(42, 1000 + ci), k * k)
+        if ci % 4 == 0:
+            kern[rng.random(k * k) < 0.35] = 0.0
+        t = build(sp, spec, kern)
+        assert_same_csr(t, orc.build_native(*spec, kern))
+
+
+def test_build_edge_cases(sp, orc):
+    # empty rows (k=1, p=1: the whole border is padding), p > k, all-zero kernel, NaN taps
+    cases = [((257, 193, 1, 1, 1), np.ones(1, np.float32)),
+             ((5, 4, 2, 3, 4), np.arange(1, 5, dtype=np.float32)),
+             ((9, 9, 3, 2, 2), np.zeros(9, np.float32)),
+             ((6, 7, 3, 1, 1), np.array([1, np.nan, 0, -0.0, 2, np.inf, 3, 0, -1], np.float32)),
+             ((1, 1, 1, 1, 3), np.array([2.5], np.float32))]
+    for spec, kern in cases:
+        t = build(sp, spec, kern)
+        rp, ri, rv = orc.build_native(*spec, kern)
+        ptr, idx, val = native_copy(t)
+        assert np.array_equal(ptr, rp) and np.array_equal(idx, ri)
+        assert np.array_equal(bits(val), bits(rv))
+        assert t.nnz == rv.size
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_build_full_size(sp, orc, cfg):
+    """Configs 3 (1024^2 k3) and 4 (4096^2 k7 s2 p3, 205 M entries) bit-exact."""
+    spec = CONFIGS[cfg]
+    kern = orc.random_normal_f32(orc.derive_seed(orc.derive_seed(42, cfg), 1), spec[2] ** 2)
+    t = build(sp, spec, kern)
+    assert t.nnz == orc.nnz_bound(*spec)
+    ptr, idx, val = native_copy(t)
+    rp, ri, rv = orc.build_native(*spec, kern)
+    assert np.array_equal(ptr, rp)
+    assert np.array_equal(idx, ri)
+    assert np.array_equal(bits(val), bits(rv))
+    # closed form: row counts are Theorem 2.1's per-output counts
+    assert np.array_equal(np.diff(ptr.astype(np.int64)), orc.nnz_per_output(*spec))
+
+
+# ---------------------------------------------------------------------------
+# SpMV / SpMM
+# ---------------------------------------------------------------------------
+
+def test_spmv_config1_vs_reference_y(sp, orc, golden, torch_cuda):
+    _, npz = golden
+    t = build(sp, CONFIGS[0], npz["c1_kernel"])
+    x = npz["c1_image"].astype(np.float32)
+    y = sp.spmv(t, torch_cuda.from_numpy(x).cuda()).cpu().numpy()
+    ptr, idx, val = npz["c1_ptr"], npz["c1_idx"], npz["c1_val"]
+    assert np.array_equal(bits(y), bits(orc.spmv_f32_fma(ptr, idx, val, x)))
+    cond = orc.spmv_abs(ptr, idx, val, npz["c1_image"])
+    assert np.all(np.abs(y - npz["c1_y"]) <= TOL * cond)
+
+
+def test_spmv_config2_all_paths(sp, orc, torch_cuda):
+    m, n, k, s, p = CONFIGS[1]
+    kern, X = problem(orc, 1, m, n, k, batch=1)
+    t = build(sp, CONFIGS[1], kern)
+    rp, ri, rv = orc.build_native(*CONFIGS[1], kern)
+    want = orc.spmm_native(rp, ri, rv, X)
+    for path in (None, "tiled", "tiled_notma", "generic"):
+        Y = run_spmm(torch_cuda, sp, t, X, path)
+        assert np.array_equal(bits(Y), bits(want)), path
+    # fp64 reference tolerance
+    y64 = orc.spmv_f64(rp.astype(np.int64), ri.astype(np.int64), rv.astype(np.float64), X[0].astype(np.float64))
+    cond = orc.spmv_abs(rp.astype(np.int64), ri.astype(np.int64), rv.astype(np.float64), X[0].astype(np.float64))
+    assert np.all(np.abs(want[0] - y64) <= TOL * cond)
+
+
+@pytest.mark.parametrize("batch", [1, 2, 3, 5, 8, 13, 32])
+def test_spmm_batches_and_tails(sp, orc, torch_cuda, batch):
+    spec = (96, 72, 5, 2, 2)
+    kern, X = problem(orc, 7, 96, 72, 5, batch=batch)
+    t = build(sp, spec, kern)
+    want = orc.spmm_native(*orc.build_native(*spec, kern), X)
+    for path in (None, "tiled_notma", "generic"):
+        assert np.array_equal(bits(run_spmm(torch_cuda, sp, t, X, path)), bits(want)), path
+    # padded leading dimension (ldx = cols + 4 keeps TMA-legal 16B strides)
+    assert np.array_equal(bits(run_spmm(torch_cuda, sp, t, X, None, ldx_pad=4)), bits(want))
+
+
+def test_spmm_golden_specs(sp, orc, golden, torch_cuda):
+    """Every digest case (config 2 + 36 edge specs x {normal, zero-tap}): SpMM of
+    3 images bit-exact vs the ordered-fmaf oracle; image 0 within tolerance of
+    the reference fp64 output (its digest pins the oracle's fp64 y)."""
+    js, _ = golden
+    for key, spec, kern, img in golden_cases(orc, js):
+        m, n = spec[0], spec[1]
+        _, Xo = problem(orc, 9, m, n, 1, batch=2)
+        X = np.concatenate([img[None].astype(np.float32), Xo])
+        t = build(sp, spec, kern)
+        rp, ri, rv = orc.build_native(*spec, kern.astype(np.float32))
+        want = orc.spmm_native(rp, ri, rv, X)
+        Y = run_spmm(torch_cuda, sp, t, X)
+        assert np.array_equal(bits(Y), bits(want)), key
+        ptr, idx, val = orc.build_transform(*spec, kern)
+        y64 = orc.spmv_f64(ptr, idx, val, img)
+        assert sha(y64) == js["digests"][key]["y"], key
+        cond = orc.spmv_abs(ptr, idx, val, img)
+        assert np.all(np.abs(Y[0] - y64) <= TOL * cond + 1e-37), key
+
+
+def test_spmm_sweep_small(sp, orc, torch_cuda):
+    for ci, spec in enumerate(sweep_specs(7)):
+        if ci % 3:
+            continue
+        m, n, k = spec[:3]
+        kern = orc.random_normal_f32(orc.derive_seed(42, 5000 + ci), k * k)
+        X = np.stack([orc.random_normal_f32(orc.derive_seed(42, 9000 + ci + b), m * n) for b in range(3)])
+        t = build(sp, spec, kern)
+        want = orc.spmm_native(*orc.build_native(*spec, kern), X)
+        assert np.array_equal(bits(run_spmm(torch_cuda, sp, t, X)), bits(want)), spec
+
+
+def test_spmm_nonfinite_inputs(sp, orc, torch_cuda):
+    """inf/NaN pixels only reach the outputs whose rows store them (no 0*inf leaks)."""
+    spec = (32, 32, 3, 1, 1)
+    kern, X = problem(orc, 3, 32, 32, 3, batch=4)
+    X[0, 5] = np.inf
+    X[1, 100] = np.nan
+    X[2, 1023] = -np.inf
+    t = build(sp, spec, kern)
+    want = orc.spmm_native(*orc.build_native(*spec, kern), X)
+    for path in (None, "tiled_notma", "generic"):
+        Y = run_spmm(torch_cuda, sp, t, X, path)
+        assert np.array_equal(bits(Y), bits(want)), path
+
+
+@pytest.mark.slow
+def test_spmm_config3_full_size(sp, orc, torch_cuda):
+    m, n, k, s, p = CONFIGS[2]
+    kern, X = problem(orc, 2, m, n, k, batch=12)
+    t = build(sp, CONFIGS[2], kern)
+    want = orc.spmm_native(*orc.build_native(*CONFIGS[2], kern), X)
+    assert np.array_equal(bits(run_spmm(torch_cuda, sp, t, X)), bits(want))
+
+
+@pytest.mark.slow
+def test_spmm_config4_full_size(sp, orc, torch_cuda):
+    m, n, k, s, p = CONFIGS[3]
+    kern, X = problem(orc, 3, m, n, k, batch=3)
+    t = build(sp, CONFIGS[3], kern)
+    rp, ri, rv = orc.build_native(*CONFIGS[3], kern)
+    want = orc.spmm_native(rp, ri, rv, X)
+    Y = run_spmm(torch_cuda, sp, t, X)
+    assert np.array_equal(bits(Y), bits(want))
+
+
+def test_generic_csr_upload(sp, orc, torch_cuda):
+    """Arbitrary host CSR (not a conv transform) through the generic kernel."""
+    rng = np.random.default_rng(3)
+    rows, cols = 300, 517
+    ptr = [0]
+    idx, val = [], []
+    for r in range(rows):
+        c = np.sort(rng.choice(cols, size=int(rng.integers(0, 40)), replace=False))
+        idx += c.tolist()
+        val += rng.standard_normal(c.size).astype(np.float32).tolist()
+        ptr.append(len(idx))
+    ptr, idx, val = np.array(ptr, np.int64), np.array(idx, np.int64), np.array(val, np.float64)
+    t = sp.Transform.from_host(rows, cols, ptr, idx, val)
+    X = rng.standard_normal((4, cols)).astype(np.float32)
+    want = orc.spmm_f32_fma(ptr, idx, val, X)
+    assert np.array_equal(bits(run_spmm(torch_cuda, sp, t, X)), bits(want))
+    assert np.array_equal(t.export()[1], idx)
+
+
+def test_end_to_end_host_path(sp, orc, torch_cuda):
+    """convolve_batch on host buffers (chunked H2D / SpMM / D2H pipeline)."""
+    spec = (256, 200, 3, 1, 1)
+    kern, X = problem(orc, 8, 256, 200, 3, batch=70)
+    t = build(sp, spec, kern)
+    want = orc.spmm_native(*orc.build_native(*spec, kern), X)
+    Y = sp.convolve_batch(t, X)
+    assert np.array_equal(bits(Y), bits(want))
+    Xp = torch_cuda.from_numpy(X).pin_memory()
+    Yp = sp.convolve_batch(t, Xp)
+    assert np.array_equal(bits(Yp.numpy()), bits(want))
+
+
+def test_reference_semantics_convolve(sp, orc, golden):
+    """The fp64-in/fp64-out convolve() mirror: output within tolerance of the
+    reference's convolve() on config 1."""
+    _, npz = golden
+    t = build(sp, CONFIGS[0], npz["c1_kernel"])
+    out = sp.convolve(t, npz["c1_image"].reshape(64, 64))
+    cond = orc.spmv_abs(npz["c1_ptr"], npz["c1_idx"], npz["c1_val"], npz["c1_image"])
+    assert out.shape == (64, 64)
+    assert np.all(np.abs(out.reshape(-1) - npz["c1_y"]) <= TOL * cond)
+    with pytest.raises(ValueError, match=r"^convolve: input is 3x64 but transform expects \(m=64"):
+        sp.convolve(t, np.zeros((3, 64)))
+
+
+def test_errors(sp, torch_cuda):
+    t = build(sp, (8, 8, 3, 1, 1), np.ones(9, np.float32))
+    x = torch_cuda.zeros(63, device="cuda")
+    with pytest.raises(ValueError, match="spmv: matrix has 64 columns but vector has 63 elements"):
+        sp.spmv(t, x)
+    with pytest.raises(ValueError, match="leading dimension"):
+        sp._check(sp.lib.spconv_spmm(t._h, x.data_ptr(), 10, x.data_ptr(), 64, 1, None))
+    with pytest.raises(ValueError, match="build_conv_matrix: kernel side 2 does not match"):
+        sp.build_transform(sp.Kernel(2, np.ones(4)), sp.ConvSpec(8, 8, 3, 1, 1))
