@@ -8,6 +8,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -88,19 +89,22 @@ inline void tap_range(int64_t x, int64_t dim, int64_t k, int64_t s, int64_t p, i
     if (hi < lo) hi = lo;
 }
 
-// Host tables of the closed-form build.  Returns total nnz and the max row count.
+// Host tables of the closed-form build: O(k^2 + m_out + n_out) work.
 struct HostTables {
     std::vector<float> taps;
     std::vector<int32_t> sat;
-    std::vector<int64_t> px;
+    std::vector<long long> w;  // W[j] = sum_i nz[j][i] * #{y : i in I(y)}
     int64_t nnz = 0;
     int64_t k2max = 0;
+    bool dense = true;  // every tap non-zero and finite
 };
 
 void make_tables(const Geom& g, const float* kernel, HostTables& ht) {
     const int64_t k = g.k, k1 = k + 1;
     ht.taps.assign(kernel, kernel + k * k);
     ht.sat.assign((size_t)(k1 * k1), 0);
+    ht.dense = true;
+    for (int64_t q = 0; q < k * k; ++q) ht.dense &= kernel[q] != 0.0f && std::isfinite(kernel[q]);
     for (int64_t j = 0; j < k; ++j)
         for (int64_t i = 0; i < k; ++i)
             ht.sat[(j + 1) * k1 + i + 1] = ht.sat[j * k1 + i + 1] + ht.sat[(j + 1) * k1 + i] -
@@ -122,28 +126,29 @@ void make_tables(const Geom& g, const float* kernel, HostTables& ht) {
     std::vector<int64_t> cnty((size_t)k, 0);
     int64_t run = 0;
     for (int64_t i = 0; i < k; ++i) cnty[i] = (run += diff[i]);
-    // W[j] = sum_i nz[j][i] * cntY[i];  RowTot(x) = sum_{j in J(x)} W[j].
+    // W[j]; RowTot(x) = sum_{j in J(x)} W[j].
+    ht.w.assign((size_t)k, 0);
     std::vector<int64_t> pw((size_t)k1, 0);
     for (int64_t j = 0; j < k; ++j) {
-        int64_t w = 0;
-        for (int64_t i = 0; i < k; ++i) w += (kernel[j * k + i] != 0.0f ? 1 : 0) * cnty[i];
-        pw[j + 1] = pw[j] + w;
+        int64_t wj = 0;
+        for (int64_t i = 0; i < k; ++i) wj += (kernel[j * k + i] != 0.0f ? 1 : 0) * cnty[i];
+        ht.w[j] = wj;
+        pw[j + 1] = pw[j] + wj;
     }
     std::sort(yr.begin(), yr.end());
     yr.erase(std::unique(yr.begin(), yr.end()), yr.end());
-    ht.px.assign((size_t)(g.mo + 1), 0);
+    ht.nnz = 0;
     ht.k2max = 0;
     std::pair<int64_t, int64_t> last_xr(-1, -1);
     for (int64_t x = 0; x < g.mo; ++x) {
         int64_t jlo, jhi;
         tap_range(x, g.m, k, g.s, g.p, jlo, jhi);
-        ht.px[x + 1] = ht.px[x] + (pw[jhi] - pw[jlo]);
+        ht.nnz += pw[jhi] - pw[jlo];
         if (std::make_pair(jlo, jhi) != last_xr) {
             last_xr = {jlo, jhi};
             for (auto& q : yr) ht.k2max = std::max(ht.k2max, rect(jlo, jhi, q.first, q.second));
         }
     }
-    ht.nnz = ht.px[g.mo];
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -160,38 +165,104 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-// Kernel-path selection (SPCONV_B200_PATH=auto|tiled|generic; auto by default).
-int path_override() {
+// Kernel-path selection: SPCONV_B200_PATH = auto (default) | banded | tiled |
+// tiled_notma | generic.  auto = banded when instantiated for (k, s) and the
+// taps are dense, else tiled (TMA when the strides allow), generic for
+// uploaded matrices.  The overrides exist for cross-checking the paths.
+enum Path { kAuto = 0, kBanded, kTiled, kTiledNoTma, kGeneric };
+
+Path path_override() {
     const char* e = std::getenv("SPCONV_B200_PATH");
-    if (!e) return 0;
-    if (!std::strcmp(e, "tiled")) return 1;
-    if (!std::strcmp(e, "generic")) return 2;
-    if (!std::strcmp(e, "tiled_notma")) return 3;
-    return 0;
+    if (!e) return kAuto;
+    if (!std::strcmp(e, "banded")) return kBanded;
+    if (!std::strcmp(e, "tiled")) return kTiled;
+    if (!std::strcmp(e, "tiled_notma")) return kTiledNoTma;
+    if (!std::strcmp(e, "generic")) return kGeneric;
+    return kAuto;
+}
+
+// 3-D tensor map over the batch X[b][m][n] (fp32) with the given box.
+int encode_x_map(CUtensorMap* tmap, const float* X, const Geom& g, int64_t ldx, int64_t batch,
+                 int box_c, int box_r, int box_b) {
+    std::memset(tmap, 0, sizeof *tmap);
+    const cuuint64_t dims[3] = {(cuuint64_t)g.n, (cuuint64_t)g.m, (cuuint64_t)batch};
+    const cuuint64_t strides[2] = {(cuuint64_t)(g.n * 4), (cuuint64_t)(ldx * 4)};
+    const cuuint32_t box[3] = {(cuuint32_t)box_c, (cuuint32_t)box_r, (cuuint32_t)box_b};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUresult cr = encode_fn()(tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(X), dims,
+                              strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS)
+        return fail(SPCONV_ECUDA, "cuTensorMapEncodeTiled failed with CUresult " +
+                                      std::to_string((int)cr));
+    return SPCONV_OK;
+}
+
+int device_sm_count() {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
 }
 
 int run_spmm(const spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
              int64_t batch, cudaStream_t st) {
     if (batch == 0) return SPCONV_OK;
-    const int force = path_override();
-    bool tiled = h->is_conv && force != 2;
-    spb::TiledParams tp{};
-    int bt = 8;
-    size_t smem = 0;
-    if (tiled) {
-        const Geom& g = h->g;
-        bt = batch >= 8 ? 8 : batch >= 4 ? 4 : batch >= 2 ? 2 : 1;
+    if (batch > INT32_MAX) return fail(SPCONV_EINVAL, "spconv_spmm: batch exceeds int32");
+    const Path force = path_override();
+    const Geom& g = h->g;
+    const bool tma_ok = h->is_conv && (g.n % 4 == 0) && (ldx % 4 == 0) &&
+                        (reinterpret_cast<uintptr_t>(X) % 16 == 0) && encode_fn() != nullptr &&
+                        g.m < (1ll << 30) && g.n < (1ll << 30);
+
+    // ---- banded (register-blocked) path ----
+    const bool banded_geom = h->is_conv && spb::banded_supported((int)g.k, (int)g.s) && tma_ok;
+    if (force == kBanded && !banded_geom)
+        return fail(SPCONV_EINVAL, "SPCONV_B200_PATH=banded: geometry unsupported");
+    if (banded_geom && (force == kBanded || (force == kAuto && h->taps_dense))) {
+        spb::BandedShape sh{};
+        spb::BandedParams bp{};
+        CK(spb::launch_banded((int)g.k, (int)g.s, bp, nullptr, st, &sh));
+        bp.row_ptr = h->row_ptr;
+        bp.col_idx = h->col_idx;
+        bp.vals = h->vals;
+        bp.X = X;
+        bp.ldx = ldx;
+        bp.Y = Y;
+        bp.ldy = ldy;
+        bp.batch = (int)batch;
+        bp.m = (int)g.m;
+        bp.n = (int)g.n;
+        bp.p = (int)g.p;
+        bp.mo = (int)g.mo;
+        bp.no = (int)g.no;
+        bp.tiles_y = (int)((g.no + 31) / 32);
+        const int64_t tiles = ((g.mo + sh.th - 1) / sh.th) * bp.tiles_y;
+        const int64_t groups = (batch + sh.bt - 1) / sh.bt;
+        // Enough CTAs for ~8 waves at 2 CTAs/SM; each split keeps >= 2 groups.
+        const int64_t want = 16ll * device_sm_count();
+        int64_t splits = (want + tiles - 1) / tiles;
+        splits = std::max<int64_t>(1, std::min<int64_t>(splits, groups / 2));
+        bp.splits = (int)splits;
+        CUtensorMap tmap;
+        if (int rc = encode_x_map(&tmap, X, g, ldx, batch, sh.wc, sh.wr, sh.bt)) return rc;
+        CK(spb::launch_banded((int)g.k, (int)g.s, bp, &tmap, st, nullptr));
+        return SPCONV_OK;
+    }
+
+    // ---- tiled (per-entry) path ----
+    if (h->is_conv && force != kGeneric) {
+        int bt = batch >= 8 ? 8 : batch >= 4 ? 4 : batch >= 2 ? 2 : 1;
         const int k2max = std::max(h->k2max, 1);
         // Tile height: keep the per-CTA (off, val) table <= 64 KB.
         int th = 8;
         while (th > 1 && (size_t)k2max * th * 32 * 8 > 64 * 1024) th >>= 1;
         const int64_t wr = (th - 1) * g.s + g.k;
         const int64_t wc = ((31 * g.s + g.k + 3) + 3) & ~int64_t(3);
-        const bool geom_ok = wr <= 256 && wc <= 256 && g.m < (1ll << 30) && g.n < (1ll << 30);
-        const bool align_ok = (g.n % 4 == 0) && (ldx % 4 == 0) &&
-                              (reinterpret_cast<uintptr_t>(X) % 16 == 0) && encode_fn() != nullptr &&
-                              force != 3;
-        int stages = align_ok ? 4 : 1;
+        const bool use_tma = tma_ok && wr <= 256 && wc <= 256 && force != kTiledNoTma;
+        int stages = use_tma ? 4 : 1;
+        size_t smem = 0;
         while (true) {
             smem = spb::tiled_smem_bytes(th, (int)wr, (int)wc, k2max, bt, stages);
             if (smem <= 200 * 1024) break;
@@ -199,9 +270,8 @@ int run_spmm(const spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t
             else if (bt > 1) bt >>= 1;
             else break;
         }
-        if (smem > 227 * 1024 || !geom_ok || batch > INT32_MAX) {
-            tiled = false;
-        } else {
+        if (smem <= 227 * 1024 && g.m < (1ll << 30) && g.n < (1ll << 30)) {
+            spb::TiledParams tp{};
             tp.row_ptr = h->row_ptr;
             tp.col_idx = h->col_idx;
             tp.vals = h->vals;
@@ -222,29 +292,19 @@ int run_spmm(const spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t
             tp.wc = (int)wc;
             tp.k2max = k2max;
             tp.stages = stages;
-            tp.use_tma = align_ok ? 1 : 0;
+            tp.use_tma = use_tma ? 1 : 0;
             CUtensorMap tmap;
             std::memset(&tmap, 0, sizeof tmap);
-            if (align_ok) {
-                const cuuint64_t dims[3] = {(cuuint64_t)g.n, (cuuint64_t)g.m, (cuuint64_t)batch};
-                const cuuint64_t strides[2] = {(cuuint64_t)(g.n * 4), (cuuint64_t)(ldx * 4)};
-                const cuuint32_t box[3] = {(cuuint32_t)wc, (cuuint32_t)wr, (cuuint32_t)bt};
-                const cuuint32_t estr[3] = {1, 1, 1};
-                CUresult cr = encode_fn()(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
-                                          const_cast<float*>(X), dims, strides, box, estr,
-                                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-                if (cr != CUDA_SUCCESS) {
-                    return fail(SPCONV_ECUDA, "cuTensorMapEncodeTiled failed with CUresult " +
-                                                  std::to_string((int)cr));
-                }
-            }
+            if (use_tma)
+                if (int rc = encode_x_map(&tmap, X, g, ldx, batch, (int)wc, (int)wr, bt)) return rc;
             CK(spb::launch_tiled(tp, &tmap, bt, smem, st));
             return SPCONV_OK;
         }
+        if (force == kTiled || force == kTiledNoTma)
+            return fail(SPCONV_EINVAL, "SPCONV_B200_PATH=tiled: geometry unsupported");
     }
-    if (force == 1 && h->is_conv) return fail(SPCONV_EINVAL, "SPCONV_B200_PATH=tiled: geometry unsupported");
+
+    // ---- generic CSR path ----
     spb::GenericParams gp{h->row_ptr, h->col_idx, h->vals, X, ldx, Y, ldy, (int)h->rows, (int)batch};
     CK(spb::launch_generic(gp, st));
     return SPCONV_OK;
@@ -316,33 +376,21 @@ int spconv_build_csr(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
     h->nnz = ht.nnz;
     h->k2max = (int)ht.k2max;
 
-    // One allocation for the CSR, one for the build tables.
+    h->taps_dense = ht.dense;
+
+    // One stream-ordered allocation for the CSR (+256 B slack so prologue
+    // reads one-past-the-end stay in bounds).
     const size_t rp_bytes = ((size_t)(h->rows + 1) * 4 + 255) & ~size_t(255);
     const size_t ix_bytes = ((size_t)std::max<int64_t>(ht.nnz, 1) * 4 + 255) & ~size_t(255);
     char* csr = nullptr;
-    cudaError_t e = cudaMalloc(&csr, rp_bytes + 2 * ix_bytes);
+    cudaError_t e = cudaMallocAsync(&csr, rp_bytes + 2 * ix_bytes + 256, st);
     if (e != cudaSuccess) {
         delete h;
-        return cuda_fail(e, "cudaMalloc(CSR)");
+        return cuda_fail(e, "cudaMallocAsync(CSR)");
     }
     h->row_ptr = reinterpret_cast<int32_t*>(csr);
     h->col_idx = reinterpret_cast<int32_t*>(csr + rp_bytes);
     h->vals = reinterpret_cast<float*>(csr + rp_bytes + ix_bytes);
-
-    const size_t taps_b = ((ht.taps.size() * 4) + 255) & ~size_t(255);
-    const size_t sat_b = ((ht.sat.size() * 4) + 255) & ~size_t(255);
-    const size_t px_b = ht.px.size() * 8;
-    char* tab = nullptr;
-    e = cudaMallocAsync(&tab, taps_b + sat_b + px_b, st);
-    if (e != cudaSuccess) {
-        cudaFree(csr);
-        delete h;
-        return cuda_fail(e, "cudaMallocAsync(tables)");
-    }
-    // Pageable copies are staged by the driver before the call returns.
-    cudaMemcpyAsync(tab, ht.taps.data(), ht.taps.size() * 4, cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(tab + taps_b, ht.sat.data(), ht.sat.size() * 4, cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(tab + taps_b + sat_b, ht.px.data(), px_b, cudaMemcpyHostToDevice, st);
 
     spb::BuildParams bp{};
     bp.m = (int)m;
@@ -353,29 +401,60 @@ int spconv_build_csr(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
     bp.mo = (int)g.mo;
     bp.no = (int)g.no;
     bp.rows = (int)h->rows;
-    bp.t.taps = reinterpret_cast<const float*>(tab);
-    bp.t.sat = reinterpret_cast<const int32_t*>(tab + taps_b);
-    bp.t.px = reinterpret_cast<const int64_t*>(tab + taps_b + sat_b);
     bp.row_ptr = h->row_ptr;
     bp.col_idx = h->col_idx;
     bp.vals = h->vals;
+    char* tab = nullptr;
+    if (k <= spb::kSmallK) {  // tables ride in the kernel parameters: no copies, no allocation
+        bp.small = 1;
+        std::copy(ht.taps.begin(), ht.taps.end(), bp.tab.taps);
+        std::copy(ht.sat.begin(), ht.sat.end(), bp.tab.sat);
+        std::copy(ht.w.begin(), ht.w.end(), bp.tab.w);
+    } else {
+        const size_t taps_b = ((ht.taps.size() * 4) + 255) & ~size_t(255);
+        const size_t sat_b = ((ht.sat.size() * 4) + 255) & ~size_t(255);
+        const size_t w_b = ht.w.size() * 8;
+        e = cudaMallocAsync(&tab, taps_b + sat_b + w_b, st);
+        if (e != cudaSuccess) {
+            cudaFreeAsync(csr, st);
+            delete h;
+            return cuda_fail(e, "cudaMallocAsync(tables)");
+        }
+        // Pageable copies are staged by the driver before the call returns.
+        cudaMemcpyAsync(tab, ht.taps.data(), ht.taps.size() * 4, cudaMemcpyHostToDevice, st);
+        cudaMemcpyAsync(tab + taps_b, ht.sat.data(), ht.sat.size() * 4, cudaMemcpyHostToDevice, st);
+        cudaMemcpyAsync(tab + taps_b + sat_b, ht.w.data(), w_b, cudaMemcpyHostToDevice, st);
+        bp.small = 0;
+        bp.t.taps = reinterpret_cast<const float*>(tab);
+        bp.t.sat = reinterpret_cast<const int32_t*>(tab + taps_b);
+        bp.t.w = reinterpret_cast<const long long*>(tab + taps_b + sat_b);
+    }
     // Stage entries through shared memory when a CTA's worst case fits.
-    int block = 256;
     const int64_t k2 = k * k;
+    int block = 256;
     while (block > 64 && (size_t)block * k2 * 8 > 64 * 1024) block >>= 1;
-    size_t smem = 0;
+    const size_t tab_bytes = (size_t)(((k + 1) * (k + 1) + k2 + 3) & ~int64_t(3)) * 4;
+    size_t smem = tab_bytes;
     bp.stage = 0;
-    if ((size_t)block * k2 * 8 <= 96 * 1024) {
+    if ((size_t)block * k2 * 8 <= 96 * 1024 && tab_bytes <= 64 * 1024) {
         bp.stage = 1;
-        smem = (size_t)(((block * k2 + 3) & ~int64_t(3)) * 4) * 2;
+        bp.stage_words = (int)((block * k2 + 3 + 3) & ~int64_t(3));
+        smem += (size_t)bp.stage_words * 4 * 2;
     } else {
         block = 256;
     }
+    if (smem > 200 * 1024) {
+        if (tab) cudaFreeAsync(tab, st);
+        cudaFreeAsync(csr, st);
+        delete h;
+        return fail(SPCONV_EINVAL, "spconv_build_csr: kernel side " + std::to_string(k) +
+                                       " too large for the device build");
+    }
     e = spb::launch_csr_build(bp, block, smem, st);
-    cudaFreeAsync(tab, st);
+    if (tab) cudaFreeAsync(tab, st);
     if (e != cudaSuccess) {
+        cudaFreeAsync(csr, st);
         cudaStreamSynchronize(st);
-        cudaFree(csr);
         delete h;
         return cuda_fail(e, "csr_build launch");
     }

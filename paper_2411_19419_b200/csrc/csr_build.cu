@@ -7,7 +7,7 @@
 // their final (column-ascending) order.
 //
 // Row r = x*n_out + y (inc/conv.hpp:8-12) keeps tap (j,i) iff the tap lands in
-// the input, i.e. j in [jlo(x), jhi(x)), i in [ilo(y), ihi(y)) with
+// the input, i.e. j in J(x) = [jlo(x), jhi(x)), i in I(y) = [ilo(y), ihi(y)),
 //   jlo = max(0, p - s*x),  jhi = min(k, m + p - s*x)        (and likewise i),
 // -- the paper's max(0, k - c1(x)) * max(0, k - c2(y)) count
 // (inc/analysis.hpp:21-52) -- AND the tap is not an exact zero
@@ -16,12 +16,13 @@
 // The count is a summed-area-table query over the (tap != 0) mask, which
 // reduces to the closed form when no tap is zero.
 //
-// row_ptr is closed-form too: the host tabulates px[x] = nnz of all output rows
-// of image rows < x, and a CTA starting at (x0, y0) adds
-//   sum_i nzcol(x0, i) * #{y' < y0 : i in I(y')}
-// (O(k) terms), so every CTA knows its global offset without a grid-wide scan
-// or look-back; a block scan of the per-row counts finishes row_ptr.  Entries
-// are staged in shared memory and written back with coalesced stores, so HBM
+// row_ptr is closed-form as well.  With W[j] = sum_i nz[j][i] * #{y : i in I(y)}
+// (host, O(k^2)), the number of entries in all rows before (x0, y0) is
+//   sum_j W[j] * #{x' < x0 : j in J(x')}  +  sum_i nzcol(x0, i) * #{y' < y0 : i in I(y')}
+// and both counts are O(1) ranges, so every CTA computes its global offset in
+// O(k) without a grid-wide scan or look-back; a block scan of the per-row
+// counts finishes row_ptr.  Entries are staged in shared memory at the global
+// offset's alignment and written back with 16-byte streaming stores, so HBM
 // sees each of the 8*nnz + 4*(rows+1) bytes exactly once.
 #include "internal.h"
 
@@ -47,8 +48,7 @@ __device__ __forceinline__ long long warp_sum64(long long v) {
 
 __device__ __forceinline__ int sat_rect(const int32_t* sat, int k1, int jlo, int jhi, int ilo,
                                         int ihi) {
-    return __ldg(sat + jhi * k1 + ihi) - __ldg(sat + jlo * k1 + ihi) - __ldg(sat + jhi * k1 + ilo) +
-           __ldg(sat + jlo * k1 + ilo);
+    return sat[jhi * k1 + ihi] - sat[jlo * k1 + ihi] - sat[jhi * k1 + ilo] + sat[jlo * k1 + ilo];
 }
 
 // Valid tap range [lo, hi) along one axis for slide position x (see header).
@@ -57,6 +57,13 @@ __device__ __forceinline__ void tap_range(int x, int dim, int k, int s, int p, i
     hi = min(k, dim + p - s * x);
     lo = min(lo, k);
     if (hi < lo) hi = lo;
+}
+
+// #{x' in [0, x) : tap index j in J(x')}  (an O(1) range count).
+__device__ __forceinline__ int slides_before(int x, int j, int dim, int s, int p) {
+    const int lo = (p - j <= 0) ? 0 : (p - j + s - 1) / s;
+    const int hi = (dim + p - j - 1 < 0) ? 0 : (dim + p - j - 1) / s + 1;
+    return max(0, min(x, hi) - lo);
 }
 
 }  // namespace
@@ -70,7 +77,16 @@ __global__ void __launch_bounds__(256) csr_build_kernel(const BuildParams P) {
     const int R = blockDim.x;
     const int nw = R >> 5;
     const int lane = t & 31, wid = t >> 5;
-    const int k1 = P.k + 1;
+    const int k = P.k, k1 = k + 1, kk = k * k;
+
+    // Tables -> shared memory: sat[(k+1)^2] ints, taps[k^2] floats, then the staging area.
+    int32_t* s_sat = reinterpret_cast<int32_t*>(smem);
+    float* s_taps = reinterpret_cast<float*>(s_sat + k1 * k1);
+    const int tab_words = (k1 * k1 + kk + 3) & ~3;
+    for (int q = t; q < k1 * k1; q += R) s_sat[q] = P.small ? P.tab.sat[q] : __ldg(P.t.sat + q);
+    for (int q = t; q < kk; q += R) s_taps[q] = P.small ? P.tab.taps[q] : __ldg(P.t.taps + q);
+    __syncthreads();
+
     const int r0 = blockIdx.x * R;
     const int r = r0 + t;
 
@@ -79,22 +95,21 @@ __global__ void __launch_bounds__(256) csr_build_kernel(const BuildParams P) {
     if (r < P.rows) {
         x = r / P.no;
         y = r - x * P.no;
-        tap_range(x, P.m, P.k, P.s, P.p, jlo, jhi);
-        tap_range(y, P.n, P.k, P.s, P.p, ilo, ihi);
-        cnt = sat_rect(P.t.sat, k1, jlo, jhi, ilo, ihi);
+        tap_range(x, P.m, k, P.s, P.p, jlo, jhi);
+        tap_range(y, P.n, k, P.s, P.p, ilo, ihi);
+        cnt = sat_rect(s_sat, k1, jlo, jhi, ilo, ihi);
     }
 
-    // ---- closed-form global offset of row r0 ----
+    // ---- closed-form global offset of row r0 = (x0, y0) ----
     const int x0 = r0 / P.no, y0 = r0 - x0 * P.no;
     int jlo0, jhi0;
-    tap_range(x0, P.m, P.k, P.s, P.p, jlo0, jhi0);
+    tap_range(x0, P.m, k, P.s, P.p, jlo0, jhi0);
     long long part = 0;
-    for (int i = t; i < P.k; i += R) {
-        const int cz = sat_rect(P.t.sat, k1, jlo0, jhi0, i, i + 1);
-        const int lo = (P.p - i <= 0) ? 0 : (P.p - i + P.s - 1) / P.s;
-        const int hi = (P.n + P.p - i - 1 < 0) ? 0 : (P.n + P.p - i - 1) / P.s + 1;
-        const int py = max(0, min(y0, hi) - lo);
-        part += (long long)cz * py;
+    for (int q = t; q < k; q += R) {
+        const long long wj = P.small ? P.tab.w[q] : __ldg(P.t.w + q);
+        part += wj * slides_before(x0, q, P.m, P.s, P.p);
+        const int cz = sat_rect(s_sat, k1, jlo0, jhi0, q, q + 1);
+        part += (long long)cz * slides_before(y0, q, P.n, P.s, P.p);
     }
     part = warp_sum64(part);
     if (lane == 0) s_red[wid] = part;
@@ -104,17 +119,17 @@ __global__ void __launch_bounds__(256) csr_build_kernel(const BuildParams P) {
     if (lane == 31) s_warp[wid] = inc;
     __syncthreads();
     if (wid == 0) {
-        int w = lane < nw ? s_warp[lane] : 0;
+        int wv = lane < nw ? s_warp[lane] : 0;
         long long pr = lane < nw ? s_red[lane] : 0;
-        w = warp_incl_scan(w);
+        wv = warp_incl_scan(wv);
         pr = warp_sum64(pr);
-        s_warp[lane] = w;
+        s_warp[lane] = wv;
         if (lane == 0) s_red[0] = pr;
     }
     __syncthreads();
     const int excl = inc - cnt + (wid > 0 ? s_warp[wid - 1] : 0);
     const int total = s_warp[nw - 1];
-    const int base = (int)(__ldg(P.t.px + x0) + s_red[0]);
+    const int base = (int)s_red[0];
 
     if (r < P.rows) {
         P.row_ptr[r] = base + excl;
@@ -122,13 +137,14 @@ __global__ void __launch_bounds__(256) csr_build_kernel(const BuildParams P) {
     }
 
     // ---- fill: taps of this row in (j, i) order == column-ascending ----
+    const int mis = base & 3;  // stage at the global offset's 16-byte phase
     int32_t* dcol;
     float* dval;
     int o;
     if (P.stage) {
-        dcol = reinterpret_cast<int32_t*>(smem);
-        dval = reinterpret_cast<float*>(smem) + ((R * P.k * P.k + 3) & ~3);
-        o = excl;
+        dcol = reinterpret_cast<int32_t*>(smem) + tab_words;
+        dval = reinterpret_cast<float*>(dcol) + P.stage_words;
+        o = mis + excl;
     } else {
         dcol = P.col_idx;
         dval = P.vals;
@@ -138,9 +154,9 @@ __global__ void __launch_bounds__(256) csr_build_kernel(const BuildParams P) {
         const int xr = P.s * x - P.p, yc = P.s * y - P.p;
         for (int j = jlo; j < jhi; ++j) {
             const int rowbase = (xr + j) * P.n + yc;
-            const float* tj = P.t.taps + j * P.k;
+            const float* tj = s_taps + j * k;
             for (int i = ilo; i < ihi; ++i) {
-                const float v = __ldg(tj + i);
+                const float v = tj[i];
                 if (v != 0.0f) {  // drops +-0.0, keeps NaN (inc/sparse.hpp:335)
                     dcol[o] = rowbase + i;
                     dval[o] = v;
@@ -151,11 +167,26 @@ __global__ void __launch_bounds__(256) csr_build_kernel(const BuildParams P) {
     }
     if (P.stage) {
         __syncthreads();
-        int32_t* gcol = P.col_idx + base;
-        float* gval = P.vals + base;
-        for (int e = t; e < total; e += R) {
-            __stcs(gcol + e, dcol[e]);
-            __stcs(gval + e, dval[e]);
+        // Global [base, base + total) <- staged [mis, mis + total): scalar head,
+        // 16-byte body, scalar tail.
+        const int head = min(total, (4 - mis) & 3);
+        if (t < head) {
+            __stcs(P.col_idx + base + t, dcol[mis + t]);
+            __stcs(P.vals + base + t, dval[mis + t]);
+        }
+        const int nvec = (total - head) >> 2;
+        const int4* scol = reinterpret_cast<const int4*>(dcol + mis + head);
+        const float4* sval = reinterpret_cast<const float4*>(dval + mis + head);
+        int4* gcol = reinterpret_cast<int4*>(P.col_idx + base + head);
+        float4* gval = reinterpret_cast<float4*>(P.vals + base + head);
+        for (int q = t; q < nvec; q += R) {
+            __stcs(gcol + q, scol[q]);
+            __stcs(gval + q, sval[q]);
+        }
+        const int done = head + 4 * nvec;
+        if (t < total - done) {
+            __stcs(P.col_idx + base + done + t, dcol[mis + done + t]);
+            __stcs(P.vals + base + done + t, dval[mis + done + t]);
         }
     }
 }

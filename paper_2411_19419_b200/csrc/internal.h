@@ -15,21 +15,31 @@ struct Geom {
     int64_t mo, no;  // m_out, n_out (inc/conv.hpp:52-53)
 };
 
-// Host-precomputed tables for the closed-form row_ptr (see csr_build.cu).
+// Host-precomputed O(k^2) tables of the closed-form build (see csr_build.cu).
 struct BuildTables {
     const float* taps;     // k*k, fp32, row-major
     const int32_t* sat;    // (k+1)*(k+1) summed-area table of (tap != 0)
-    const int64_t* px;     // mo+1: nnz of all output rows above image row x
+    const long long* w;    // k: W[j] = sum_i nz[j][i] * #{y : i in I(y)}
+};
+
+constexpr int kSmallK = 16;  // tables travel in the kernel parameters up to this k
+struct SmallTables {
+    float taps[kSmallK * kSmallK];
+    int32_t sat[(kSmallK + 1) * (kSmallK + 1)];
+    long long w[kSmallK];
 };
 
 struct BuildParams {
     int m, n, k, s, p, mo, no;
     int rows;
+    int small;        // 1: tables in `tab`, 0: tables in device memory `t`
+    int stage;        // 1: stage entries in shared memory, 0: direct stores
+    int stage_words;  // words per staging array
+    SmallTables tab;
     BuildTables t;
     int32_t* row_ptr;
     int32_t* col_idx;
     float* vals;
-    int stage;  // 1: stage entries in shared memory, 0: direct stores
 };
 
 // Conv-tiled SpMM: one CTA owns a TH x 32 block of output pixels (rows of T)
@@ -52,6 +62,25 @@ struct TiledParams {
     int use_tma;
 };
 
+// Register-blocked conv SpMM (spmm_banded.cu).
+struct BandedParams {
+    const int32_t* row_ptr;
+    const int32_t* col_idx;
+    const float* vals;
+    const float* X;
+    int64_t ldx;
+    float* Y;
+    int64_t ldy;
+    int batch;
+    int m, n, p, mo, no;
+    int tiles_y;  // tiles across n_out (tile width 32)
+    int splits;   // batch splits per tile
+};
+
+struct BandedShape {
+    int th, wr, wc, bt, smem, threads;
+};
+
 struct GenericParams {
     const int32_t* row_ptr;
     const int32_t* col_idx;
@@ -69,6 +98,9 @@ cudaError_t launch_csr_build(const BuildParams& bp, int block, size_t smem, cuda
 cudaError_t launch_tiled(const TiledParams& tp, const CUtensorMap* tmap, int bt, size_t smem,
                          cudaStream_t st);
 cudaError_t launch_generic(const GenericParams& gp, cudaStream_t st);
+bool banded_supported(int k, int s);
+cudaError_t launch_banded(int k, int s, const BandedParams& bp, const CUtensorMap* tmap,
+                          cudaStream_t st, BandedShape* shape);
 
 size_t tiled_smem_bytes(int th, int wr, int wc, int k2max, int bt, int stages);
 
@@ -81,6 +113,7 @@ struct spconv_csr {
     spb::Geom g{};
     int64_t rows = 0, cols = 0, nnz = 0;
     int k2max = 0;                 // max entries in any row
+    bool taps_dense = false;       // every tap non-zero and finite (banded SpMM applies)
     int32_t* row_ptr = nullptr;    // device
     int32_t* col_idx = nullptr;    // device
     float* vals = nullptr;         // device

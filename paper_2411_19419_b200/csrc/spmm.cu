@@ -1,75 +1,38 @@
-// spmm.cu -- SpMV / SpMM of the conv transform T against image-major batches.
+// spmm.cu -- SpMV / SpMM of T against image-major batches: the general kernels.
 //
 // Replaces spmv + detail::spmv_csr_rows (inc/sparse.hpp:180-192, 214-261) and
 // the per-image convolve loop of its callers (inc/conv.hpp:207-215,
-// inc/bench.hpp:240-248).  Accumulation contract, both kernels:
+// inc/bench.hpp:240-248).  Accumulation contract of every kernel:
 //     acc = +0.0f; for e in row (column-ascending): acc = fmaf(val[e], x[col[e]], acc)
 // i.e. the reference's sequential row loop in fp32 with one rounding per step.
 //
-// conv_spmm_tiled -- the hot path for transforms built by csr_build.  A CTA owns
-//   a TH x 32 block of output pixels (TH*32 rows of T; warp w = one image row
-//   of the block, lane = one output column).  Prologue: each thread reads its
-//   row's (col, val) pairs from the CSR ONCE and rewrites every column as an
-//   offset into the CTA's input window (the (TH-1)s+k x 31s+k patch every
-//   entry of the block falls in); the pairs live tap-major in shared memory
-//   ([q][thread], bank-conflict free).  Main loop: the input window of BT
-//   images at a time is staged into shared memory by one TMA 3-D box load
-//   (cols x rows x images; negative / out-of-range coordinates zero-fill,
-//   so padding costs nothing), multi-buffered on mbarriers, and every thread
-//   accumulates its row for BT images from shared memory.  HBM traffic: the
-//   matrix once per launch, each input image once (+ window halo from L2),
-//   each output once; per CTA the CSR is read once per batch, not per image.
-// csr_spmm_generic -- any CSR (uploaded host matrices, misfit geometries):
-//   thread per (row, image), x gathered through L1.
+// conv_spmm_tiled -- any transform built by csr_build (any k, s, p, zero or
+//   non-finite taps).  A CTA owns a TH x 32 block of output pixels (TH*32 rows
+//   of T; warp = one image row of the block, lane = one output column).
+//   Prologue: each thread reads its row's (col, val) pairs from the CSR once and
+//   rewrites every column as an offset into the CTA's input window (the
+//   (TH-1)s+k x 31s+k patch every entry of the block falls in); the pairs live
+//   tap-major in shared memory ([q][thread], bank-conflict free).  Main loop:
+//   the windows of BT images at a time are staged into shared memory by ONE
+//   TMA 3-D box load (cols x rows x images; out-of-range coordinates
+//   zero-fill), multi-buffered on mbarriers; each thread accumulates its row
+//   for BT images.  The register-blocked fast path for the common geometries is
+//   conv_spmm_banded (spmm_banded.cu).
+// csr_spmm_generic -- any CSR (uploaded host matrices): thread per (row,
+//   image), x gathered through L1.
 #include "internal.h"
+#include "tma.cuh"
 
 namespace spb {
 
 namespace {
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
-                 : "memory");
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred P1;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-        "@!P1 bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1,
-                                            int c2, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
-        : "memory");
-}
-
 constexpr int kTileW = 32;
-
+inline __host__ __device__ int stage_floats(int bt, int win) { return (bt * win + 31) & ~31; }
 }  // namespace
 
 size_t tiled_smem_bytes(int th, int wr, int wc, int k2max, int bt, int stages) {
     const size_t bars = 128;  // mbarriers, padded so the windows stay 128B-aligned
-    const size_t win = (size_t)stages * bt * wr * wc * sizeof(float);
+    const size_t win = (size_t)stages * stage_floats(bt, wr * wc) * sizeof(float);
     const size_t pairs = (size_t)k2max * th * kTileW * 8;
     return bars + win + pairs;
 }
@@ -82,10 +45,11 @@ __global__ void __launch_bounds__(256) conv_spmm_tiled(const __grid_constant__ C
     const int t = threadIdx.x;
     const int win = P.wr * P.wc;
     const int stages = P.use_tma ? P.stages : 1;
+    const int sf = stage_floats(BT, win);
 
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
     float* xs = reinterpret_cast<float*>(smem + 128);
-    int32_t* s_off = reinterpret_cast<int32_t*>(xs + (size_t)stages * BT * win);
+    int32_t* s_off = reinterpret_cast<int32_t*>(xs + (size_t)stages * sf);
     float* s_val = reinterpret_cast<float*>(s_off + P.k2max * TILE);
 
     const int tx = blockIdx.x / P.tiles_y, ty = blockIdx.x - tx * P.tiles_y;
@@ -100,15 +64,13 @@ __global__ void __launch_bounds__(256) conv_spmm_tiled(const __grid_constant__ C
 
     // Kick off the first window loads before touching the CSR.
     if (P.use_tma && t == 0) {
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap))
-                     : "memory");
+        tma_prefetch_desc(&tmap);
         for (int st = 0; st < stages; ++st) mbar_init(&bars[st], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_fence_init();
         const uint32_t bytes = (uint32_t)(BT * win * sizeof(float));
         for (int st = 0; st < stages && st < G; ++st) {
             mbar_expect_tx(&bars[st], bytes);
-            tma_load_3d(xs + (size_t)st * BT * win, &tmap, wc0, wr0, st * BT, &bars[st]);
+            tma_load_3d(xs + (size_t)st * sf, &tmap, wc0, wr0, st * BT, &bars[st]);
         }
     }
 
@@ -117,22 +79,25 @@ __global__ void __launch_bounds__(256) conv_spmm_tiled(const __grid_constant__ C
     if (valid) {
         const int e0 = __ldg(P.row_ptr + r);
         cnt = __ldg(P.row_ptr + r + 1) - e0;
-        if (cnt > P.k2max) __trap();
+        bool bad = cnt > P.k2max;
+        cnt = bad ? 0 : cnt;
+#pragma unroll 4
         for (int q = 0; q < cnt; ++q) {
             const int c = __ldg(P.col_idx + e0 + q);
             const float v = __ldg(P.vals + e0 + q);
             const int ri = c / P.n;
             const int dr = ri - wr0, dc = c - ri * P.n - wc0;
-            if ((unsigned)dr >= (unsigned)P.wr || (unsigned)dc >= (unsigned)P.wc) __trap();
+            bad |= (unsigned)dr >= (unsigned)P.wr || (unsigned)dc >= (unsigned)P.wc;
             s_off[q * TILE + t] = dr * P.wc + dc;
             s_val[q * TILE + t] = v;
         }
+        if (bad) __trap();  // entry outside the tile window: not a transform of this geometry
     }
     __syncthreads();  // mbarrier init visible to all waiters
 
     for (int g = 0; g < G; ++g) {
         const int st = g % stages;
-        float* xw = xs + (size_t)st * BT * win;
+        float* xw = xs + (size_t)st * sf;
         if (P.use_tma) {
             mbar_wait(&bars[st], (uint32_t)((g / stages) & 1));
         } else {
@@ -155,10 +120,10 @@ __global__ void __launch_bounds__(256) conv_spmm_tiled(const __grid_constant__ C
         for (int b = 0; b < BT; ++b) acc[b] = 0.0f;
 #pragma unroll 3
         for (int q = 0; q < cnt; ++q) {
-            const int off = s_off[q * TILE + t];
+            const float* xq = xw + s_off[q * TILE + t];
             const float v = s_val[q * TILE + t];
 #pragma unroll
-            for (int b = 0; b < BT; ++b) acc[b] = fmaf(v, xw[b * win + off], acc[b]);
+            for (int b = 0; b < BT; ++b) acc[b] = fmaf(v, xq[b * win], acc[b]);
         }
         if (valid) {
 #pragma unroll
@@ -182,7 +147,8 @@ __global__ void __launch_bounds__(256) csr_spmm_generic(const GenericParams P) {
     for (int b = blockIdx.y; b < P.batch; b += gridDim.y) {
         const float* x = P.X + (int64_t)b * P.ldx;
         float acc = 0.0f;
-        for (int e = e0; e < e1; ++e) acc = fmaf(__ldg(P.vals + e), __ldg(x + __ldg(P.col_idx + e)), acc);
+        for (int e = e0; e < e1; ++e)
+            acc = fmaf(__ldg(P.vals + e), __ldg(x + __ldg(P.col_idx + e)), acc);
         P.Y[(int64_t)b * P.ldy + r] = acc;
     }
 }

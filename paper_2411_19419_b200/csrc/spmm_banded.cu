@@ -1,0 +1,268 @@
+// spmm_banded.cu -- register-blocked SpMM of the conv transform (the hot kernel).
+//
+// Same contract as spmm.cu (per row: acc = +0; acc = fmaf(val, x[col], acc)
+// over the stored entries in column order; bit-identical results), for the
+// geometries instantiated below.  Rows of T for vertically adjacent output
+// pixels (x, y), (x+1, y), ... share most of their columns: a k x k tap
+// pattern shifted by s input rows.  Each thread owns V such rows; per input
+// row of its (s(V-1)+k) x k window it loads k values from shared memory ONCE
+// into registers and feeds them to every one of its V rows that stores that
+// column, so shared-memory traffic per output drops from k^2 loads to
+// (s(V-1)+k)k/V.  (OSKI-style register blocking, with the block structure
+// read from -- and verified against -- the CSR.)
+//
+// Structure check (prologue, once per tile, amortised over the batch): the
+// CTA reads the (col, val) pairs of every one of its rows from the CSR and
+// verifies (1) each row stores exactly the taps of its placement that land
+// inside the image, at the columns (s x + j - p) n + (s y + i - p), in (j, i)
+// order, and (2) every row stores the same value for tap (j, i) -- the
+// values are taken from the CSR itself (a full row of the tile).  Tiles that
+// fail (zero or non-finite taps, any other matrix) run the general per-entry
+// loop below, still from the CSR.  For a tap that lands in the zero padding the
+// blocked loop executes fmaf(w, +0.0f, acc), which returns acc bit-for-bit
+// (acc is never -0 and w is verified finite), so skipping and executing the
+// clipped taps are indistinguishable: outputs stay bit-identical to the
+// per-entry loop.
+//
+// Input windows are staged by TMA 3-D box loads (cols x rows x BT images,
+// out-of-range coordinates zero-filled), STAGES-deep on mbarriers.  The grid
+// is tiles x batch-splits (split fastest, so the CTAs sharing a tile's CSR run
+// together and re-read it from L2).
+#include "internal.h"
+#include "tma.cuh"
+
+namespace spb {
+
+template <int K, int S, int V, int TH, int BT, int STAGES>
+struct BandedCfg {
+    static constexpr int WR = S * (TH - 1) + K;                 // window rows
+    static constexpr int WC = ((31 * S + K + 3) + 3) & ~3;      // window cols (16B multiple)
+    static constexpr int WIN = WR * WC;
+    static constexpr int THREADS = 32 * (TH / V);
+    static constexpr int SF = (BT * WIN + 31) & ~31;             // stage stride (128B aligned)
+    static constexpr int JJ = S * (V - 1) + K;                   // input rows per thread
+    static constexpr size_t SMEM = 128 + (size_t)STAGES * SF * 4 + 4 * K * K + 16;
+    static_assert(TH % V == 0, "TH must be a multiple of V");
+    static_assert(WC <= 256 && WR <= 256, "TMA box limit");
+};
+
+template <int K, int S, int V, int TH, int BT, int STAGES>
+__global__ void __launch_bounds__(BandedCfg<K, S, V, TH, BT, STAGES>::THREADS)
+    conv_spmm_banded(const __grid_constant__ CUtensorMap tmap, const BandedParams P) {
+    using C = BandedCfg<K, S, V, TH, BT, STAGES>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
+    float* xs = reinterpret_cast<float*>(smem + 128);
+    float* s_w = xs + (size_t)STAGES * C::SF;
+    int* s_src = reinterpret_cast<int*>(s_w + K * K);
+
+    const int t = threadIdx.x;
+    const int lane = t & 31, warp = t >> 5;
+    const int tile = blockIdx.x / P.splits, split = blockIdx.x - tile * P.splits;
+    const int tx = tile / P.tiles_y, ty = tile - tx * P.tiles_y;
+    const int x0 = tx * TH, y0 = ty * 32;
+    const int wr0 = S * x0 - P.p;
+    const int cstart = S * y0 - P.p;
+    const int wc0 = cstart & ~3;
+    const int delta = cstart - wc0;
+    const int y = y0 + lane;
+    const int xb = x0 + warp * V;  // this thread's first output row (image row index)
+
+    // This CTA's share of the batch, in groups of BT images.
+    const int G = (P.batch + BT - 1) / BT;
+    const int g_begin = (int)((long long)G * split / P.splits);
+    const int g_end = (int)((long long)G * (split + 1) / P.splits);
+    const int ng = g_end - g_begin;
+
+    if (t == 0) {
+        tma_prefetch_desc(&tmap);
+        for (int st = 0; st < STAGES; ++st) mbar_init(&bars[st], 1);
+        mbar_fence_init();
+        for (int st = 0; st < STAGES && st < ng; ++st) {
+            mbar_expect_tx(&bars[st], (uint32_t)(BT * C::WIN * 4));
+            tma_load_3d(xs + (size_t)st * C::SF, &tmap, wc0, wr0, (g_begin + st) * BT, &bars[st]);
+        }
+        *s_src = 0x7fffffff;
+    }
+    __syncthreads();
+
+    // ---- prologue: read this thread's V rows from the CSR, verify the band ----
+    int e0[V], cnt[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+        const int x = xb + v;
+        if (x < P.mo && y < P.no) {
+            const int r = x * P.no + y;
+            e0[v] = __ldg(P.row_ptr + r);
+            cnt[v] = __ldg(P.row_ptr + r + 1) - e0[v];
+        } else {
+            e0[v] = 0;
+            cnt[v] = -1;  // not a row of T
+        }
+    }
+    // The tap values come from a full row of this tile (lowest thread/row wins).
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+        if (cnt[v] == K * K) {
+            atomicMin(s_src, t * V + v);
+            break;
+        }
+    __syncthreads();
+    const int src = *s_src;
+    if (src != 0x7fffffff && t == src / V) {
+        int ev = 0;
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+            if (v == src % V) ev = e0[v];
+        for (int q = 0; q < K * K; ++q) s_w[q] = __ldg(P.vals + ev + q);
+    }
+    __syncthreads();
+    float w[K * K];
+    bool ok = src != 0x7fffffff;
+#pragma unroll
+    for (int q = 0; q < K * K; ++q) {
+        w[q] = s_w[q];
+        ok &= isfinite(w[q]);
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+        if (cnt[v] < 0) continue;
+        const int x = xb + v;
+        int e = e0[v];
+        const int e_last = e0[v] + max(cnt[v], 1) - 1;
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            const int gr = S * x + j - P.p;
+            const bool rin = gr >= 0 && gr < P.m;
+#pragma unroll
+            for (int i = 0; i < K; ++i) {
+                const int gc = S * y + i - P.p;
+                if (rin && gc >= 0 && gc < P.n) {
+                    const int ec = min(e, e_last);
+                    const int c = __ldg(P.col_idx + ec);
+                    const float val = __ldg(P.vals + ec);
+                    ok &= (c == gr * P.n + gc) && (__float_as_uint(val) == __float_as_uint(w[j * K + i]));
+                    ++e;
+                }
+            }
+        }
+        ok &= (e - e0[v]) == cnt[v];
+    }
+    const bool fast = __syncthreads_and(ok) != 0;
+
+    // ---- main loop over this CTA's image groups ----
+    const int tbase = (S * warp * V) * C::WC + S * lane + delta;
+    for (int g = 0; g < ng; ++g) {
+        const int st = g % STAGES;
+        const float* xw = xs + (size_t)st * C::SF;
+        mbar_wait(&bars[st], (uint32_t)((g / STAGES) & 1));
+        const int img0 = (g_begin + g) * BT;
+        if (fast) {
+            const float* xt = xw + tbase;
+#pragma unroll
+            for (int b = 0; b < BT; ++b) {
+                float acc[V];
+#pragma unroll
+                for (int v = 0; v < V; ++v) acc[v] = 0.0f;
+#pragma unroll
+                for (int jj = 0; jj < C::JJ; ++jj) {
+                    float xr[K];
+#pragma unroll
+                    for (int i = 0; i < K; ++i) xr[i] = xt[b * C::WIN + jj * C::WC + i];
+#pragma unroll
+                    for (int v = 0; v < V; ++v) {
+                        const int j = jj - S * v;
+                        if (j >= 0 && j < K) {
+#pragma unroll
+                            for (int i = 0; i < K; ++i) acc[v] = fmaf(w[j * K + i], xr[i], acc[v]);
+                        }
+                    }
+                }
+                const int img = img0 + b;
+                if (img < P.batch) {
+#pragma unroll
+                    for (int v = 0; v < V; ++v)
+                        if (cnt[v] >= 0)
+                            __stcs(P.Y + (int64_t)img * P.ldy + (int64_t)(xb + v) * P.no + y, acc[v]);
+                }
+            }
+        } else {
+            // General per-entry loop, straight from the CSR (L1-resident after the first group).
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                if (cnt[v] < 0) continue;
+                float acc[BT];
+#pragma unroll
+                for (int b = 0; b < BT; ++b) acc[b] = 0.0f;
+                for (int e = e0[v]; e < e0[v] + cnt[v]; ++e) {
+                    const int c = __ldg(P.col_idx + e);
+                    const float val = __ldg(P.vals + e);
+                    const int ri = c / P.n;
+                    const int dr = ri - wr0, dc = c - ri * P.n - wc0;
+                    if ((unsigned)dr >= (unsigned)C::WR || (unsigned)dc >= (unsigned)C::WC) __trap();
+                    const float* xq = xw + dr * C::WC + dc;
+#pragma unroll
+                    for (int b = 0; b < BT; ++b) acc[b] = fmaf(val, xq[b * C::WIN], acc[b]);
+                }
+#pragma unroll
+                for (int b = 0; b < BT; ++b)
+                    if (img0 + b < P.batch)
+                        __stcs(P.Y + (int64_t)(img0 + b) * P.ldy + (int64_t)(xb + v) * P.no + y, acc[b]);
+            }
+        }
+        __syncthreads();  // stage st fully consumed
+        if (t == 0 && g + STAGES < ng) {
+            mbar_expect_tx(&bars[st], (uint32_t)(BT * C::WIN * 4));
+            tma_load_3d(xs + (size_t)st * C::SF, &tmap, wc0, wr0, (g_begin + g + STAGES) * BT,
+                        &bars[st]);
+        }
+    }
+}
+
+namespace {
+
+template <int K, int S, int V, int TH, int BT, int STAGES>
+cudaError_t launch_cfg(const BandedParams& bp, const CUtensorMap* tmap, cudaStream_t st,
+                       BandedShape* shape) {
+    using C = BandedCfg<K, S, V, TH, BT, STAGES>;
+    auto kern = conv_spmm_banded<K, S, V, TH, BT, STAGES>;
+    if (shape) {
+        *shape = BandedShape{TH, C::WR, C::WC, BT, (int)C::SMEM, C::THREADS};
+        return cudaSuccess;
+    }
+    static bool attr_set[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!attr_set[dev & 63]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)C::SMEM);
+        if (e != cudaSuccess) return e;
+        attr_set[dev & 63] = true;
+    }
+    const int tiles_x = (bp.mo + TH - 1) / TH;
+    const int grid = tiles_x * bp.tiles_y * bp.splits;
+    kern<<<grid, C::THREADS, C::SMEM, st>>>(*tmap, bp);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+// Instantiated geometries (k, s) and their blocking.  Returns false if the
+// geometry has no banded instantiation.  With `shape` non-null only reports the
+// tile/window shape (for the host to build the tensor map and the split count).
+bool banded_supported(int k, int s) {
+    return (k == 3 && s == 1) || (k == 5 && s == 2) || (k == 7 && s == 2) || (k == 5 && s == 1) ||
+           (k == 3 && s == 2);
+}
+
+cudaError_t launch_banded(int k, int s, const BandedParams& bp, const CUtensorMap* tmap,
+                          cudaStream_t st, BandedShape* shape) {
+    if (k == 3 && s == 1) return launch_cfg<3, 1, 4, 32, 4, 4>(bp, tmap, st, shape);
+    if (k == 5 && s == 1) return launch_cfg<5, 1, 4, 16, 4, 4>(bp, tmap, st, shape);
+    if (k == 3 && s == 2) return launch_cfg<3, 2, 4, 16, 2, 4>(bp, tmap, st, shape);
+    if (k == 5 && s == 2) return launch_cfg<5, 2, 4, 16, 2, 4>(bp, tmap, st, shape);
+    if (k == 7 && s == 2) return launch_cfg<7, 2, 4, 16, 2, 4>(bp, tmap, st, shape);
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace spb

@@ -174,7 +174,7 @@ def test_spmv_config2_all_paths(sp, orc, torch_cuda):
     t = build(sp, CONFIGS[1], kern)
     rp, ri, rv = orc.build_native(*CONFIGS[1], kern)
     want = orc.spmm_native(rp, ri, rv, X)
-    for path in (None, "tiled", "tiled_notma", "generic"):
+    for path in (None, "banded", "tiled", "tiled_notma", "generic"):
         Y = run_spmm(torch_cuda, sp, t, X, path)
         assert np.array_equal(bits(Y), bits(want)), path
     # fp64 reference tolerance
@@ -189,7 +189,7 @@ def test_spmm_batches_and_tails(sp, orc, torch_cuda, batch):
     kern, X = problem(orc, 7, 96, 72, 5, batch=batch)
     t = build(sp, spec, kern)
     want = orc.spmm_native(*orc.build_native(*spec, kern), X)
-    for path in (None, "tiled_notma", "generic"):
+    for path in (None, "banded", "tiled", "tiled_notma", "generic"):
         assert np.array_equal(bits(run_spmm(torch_cuda, sp, t, X, path)), bits(want)), path
     # padded leading dimension (ldx = cols + 4 keeps TMA-legal 16B strides)
     assert np.array_equal(bits(run_spmm(torch_cuda, sp, t, X, None, ldx_pad=4)), bits(want))
@@ -228,6 +228,36 @@ def test_spmm_sweep_small(sp, orc, torch_cuda):
         assert np.array_equal(bits(run_spmm(torch_cuda, sp, t, X)), bits(want)), spec
 
 
+BANDED = [(3, 1), (5, 1), (3, 2), (5, 2), (7, 2)]
+
+
+@pytest.mark.parametrize("ks", BANDED)
+def test_banded_borders_and_fallback(sp, orc, torch_cuda, ks):
+    """Register-blocked kernel on border-heavy shapes (partial tiles, p > 0, odd
+    sizes with n % 4 == 0), and its in-kernel fallback: a zero tap or a NaN tap
+    makes every tile fail the band check and take the per-entry loop."""
+    k, s = ks
+    rng = np.random.default_rng(k * 10 + s)
+    for (m, n, p) in [(33, 36, k // 2), (70, 44, 0), (19, 20, k - 1), (k, 8, 1)]:
+        spec = (m, n, k, s, p)
+        if orc.spec_check(*spec):
+            continue
+        kern = orc.random_normal_f32(orc.derive_seed(77, m * n + k), k * k)
+        X = rng.standard_normal((9, m * n)).astype(np.float32)
+        X[3, rng.integers(0, m * n)] = np.inf
+        for variant in ("dense", "zero", "nan"):
+            kv = kern.copy()
+            if variant == "zero":
+                kv[k * k // 2] = 0.0
+            elif variant == "nan":
+                kv[0] = np.nan
+            t = build(sp, spec, kv)
+            want = orc.spmm_native(*orc.build_native(*spec, kv), X)
+            for path in (None, "banded"):
+                Y = run_spmm(torch_cuda, sp, t, X, path)
+                assert np.array_equal(bits(Y), bits(want)), (spec, variant, path)
+
+
 def test_spmm_nonfinite_inputs(sp, orc, torch_cuda):
     """inf/NaN pixels only reach the outputs whose rows store them (no 0*inf leaks)."""
     spec = (32, 32, 3, 1, 1)
@@ -237,7 +267,7 @@ def test_spmm_nonfinite_inputs(sp, orc, torch_cuda):
     X[2, 1023] = -np.inf
     t = build(sp, spec, kern)
     want = orc.spmm_native(*orc.build_native(*spec, kern), X)
-    for path in (None, "tiled_notma", "generic"):
+    for path in (None, "banded", "tiled", "tiled_notma", "generic"):
         Y = run_spmm(torch_cuda, sp, t, X, path)
         assert np.array_equal(bits(Y), bits(want)), path
 
