@@ -96,7 +96,8 @@ struct HostTables {
     std::vector<long long> w;  // W[j] = sum_i nz[j][i] * #{y : i in I(y)}
     int64_t nnz = 0;
     int64_t k2max = 0;
-    bool dense = true;  // every tap non-zero and finite
+    bool dense = true;    // every tap non-zero and finite
+    bool nonzero = true;  // every tap non-zero
 };
 
 void make_tables(const Geom& g, const float* kernel, HostTables& ht) {
@@ -104,7 +105,11 @@ void make_tables(const Geom& g, const float* kernel, HostTables& ht) {
     ht.taps.assign(kernel, kernel + k * k);
     ht.sat.assign((size_t)(k1 * k1), 0);
     ht.dense = true;
-    for (int64_t q = 0; q < k * k; ++q) ht.dense &= kernel[q] != 0.0f && std::isfinite(kernel[q]);
+    ht.nonzero = true;
+    for (int64_t q = 0; q < k * k; ++q) {
+        ht.dense &= kernel[q] != 0.0f && std::isfinite(kernel[q]);
+        ht.nonzero &= kernel[q] != 0.0f;
+    }
     for (int64_t j = 0; j < k; ++j)
         for (int64_t i = 0; i < k; ++i)
             ht.sat[(j + 1) * k1 + i + 1] = ht.sat[j * k1 + i + 1] + ht.sat[(j + 1) * k1 + i] -
@@ -165,11 +170,11 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-// Kernel-path selection: SPCONV_B200_PATH = auto (default) | banded | tiled |
-// tiled_notma | generic.  auto = banded when instantiated for (k, s) and the
-// taps are dense, else tiled (TMA when the strides allow), generic for
-// uploaded matrices.  The overrides exist for cross-checking the paths.
-enum Path { kAuto = 0, kBanded, kTiled, kTiledNoTma, kGeneric };
+// Kernel-path selection: SPCONV_B200_PATH = auto (default) | spmv | banded |
+// tiled | tiled_notma | generic.  auto = spmv (latency kernel) for batch <= 2,
+// else banded when instantiated for (k, s) and the taps are dense, else tiled
+// (TMA when the strides allow); generic for uploaded matrices.  The overrides exist for cross-checking the paths.
+enum Path { kAuto = 0, kBanded, kTiled, kTiledNoTma, kGeneric, kSpmv };
 
 Path path_override() {
     const char* e = std::getenv("SPCONV_B200_PATH");
@@ -178,6 +183,7 @@ Path path_override() {
     if (!std::strcmp(e, "tiled")) return kTiled;
     if (!std::strcmp(e, "tiled_notma")) return kTiledNoTma;
     if (!std::strcmp(e, "generic")) return kGeneric;
+    if (!std::strcmp(e, "spmv")) return kSpmv;
     return kAuto;
 }
 
@@ -215,6 +221,17 @@ int run_spmm(const spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t
     const bool tma_ok = h->is_conv && (g.n % 4 == 0) && (ldx % 4 == 0) &&
                         (reinterpret_cast<uintptr_t>(X) % 16 == 0) && encode_fn() != nullptr &&
                         g.m < (1ll << 30) && g.n < (1ll << 30);
+
+    // ---- latency path for one or two vectors ----
+    const bool spmv_ok = h->k2max <= 49;
+    if (force == kSpmv && !spmv_ok)
+        return fail(SPCONV_EINVAL, "SPCONV_B200_PATH=spmv: rows longer than 49 entries");
+    if (spmv_ok && (force == kSpmv || (force == kAuto && batch <= 2))) {
+        spb::GenericParams gp{h->row_ptr, h->col_idx, h->vals, X, ldx, Y, ldy, (int)h->rows,
+                              (int)batch};
+        CK(spb::launch_spmv_unrolled(gp, h->k2max, st));
+        return SPCONV_OK;
+    }
 
     // ---- banded (register-blocked) path ----
     const bool banded_geom = h->is_conv && spb::banded_supported((int)g.k, (int)g.s) && tma_ok;
@@ -450,7 +467,7 @@ int spconv_build_csr(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
         return fail(SPCONV_EINVAL, "spconv_build_csr: kernel side " + std::to_string(k) +
                                        " too large for the device build");
     }
-    e = spb::launch_csr_build(bp, block, smem, st);
+    e = spb::launch_csr_build(bp, ht.nonzero, block, smem, st);
     if (tab) cudaFreeAsync(tab, st);
     if (e != cudaSuccess) {
         cudaFreeAsync(csr, st);

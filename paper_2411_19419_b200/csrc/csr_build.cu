@@ -68,6 +68,9 @@ __device__ __forceinline__ int slides_before(int x, int j, int dim, int s, int p
 
 }  // namespace
 
+// KC = compile-time kernel side (0: runtime P.k).  DENSE: every tap is
+// non-zero, so the zero-tap test folds away.
+template <int KC, bool DENSE>
 __global__ void __launch_bounds__(256) csr_build_kernel(const BuildParams P) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int s_warp[32];
@@ -77,7 +80,8 @@ __global__ void __launch_bounds__(256) csr_build_kernel(const BuildParams P) {
     const int R = blockDim.x;
     const int nw = R >> 5;
     const int lane = t & 31, wid = t >> 5;
-    const int k = P.k, k1 = k + 1, kk = k * k;
+    const int k = KC ? KC : P.k;
+    const int k1 = k + 1, kk = k * k;
 
     // Tables -> shared memory: sat[(k+1)^2] ints, taps[k^2] floats, then the staging area.
     int32_t* s_sat = reinterpret_cast<int32_t*>(smem);
@@ -97,7 +101,7 @@ __global__ void __launch_bounds__(256) csr_build_kernel(const BuildParams P) {
         y = r - x * P.no;
         tap_range(x, P.m, k, P.s, P.p, jlo, jhi);
         tap_range(y, P.n, k, P.s, P.p, ilo, ihi);
-        cnt = sat_rect(s_sat, k1, jlo, jhi, ilo, ihi);
+        cnt = DENSE ? (jhi - jlo) * (ihi - ilo) : sat_rect(s_sat, k1, jlo, jhi, ilo, ihi);
     }
 
     // ---- closed-form global offset of row r0 = (x0, y0) ----
@@ -152,15 +156,34 @@ __global__ void __launch_bounds__(256) csr_build_kernel(const BuildParams P) {
     }
     if (r < P.rows && cnt > 0) {
         const int xr = P.s * x - P.p, yc = P.s * y - P.p;
-        for (int j = jlo; j < jhi; ++j) {
-            const int rowbase = (xr + j) * P.n + yc;
-            const float* tj = s_taps + j * k;
-            for (int i = ilo; i < ihi; ++i) {
-                const float v = tj[i];
-                if (v != 0.0f) {  // drops +-0.0, keeps NaN (inc/sparse.hpp:335)
-                    dcol[o] = rowbase + i;
-                    dval[o] = v;
-                    ++o;
+        if (KC) {
+            // Fully unrolled K x K pattern; clipped / zero taps are predicated off.
+#pragma unroll
+            for (int j = 0; j < KC; ++j) {
+                const int rowbase = (xr + j) * P.n + yc;
+                const bool jin = j >= jlo && j < jhi;
+#pragma unroll
+                for (int i = 0; i < KC; ++i) {
+                    const float v = s_taps[j * KC + i];
+                    const bool keep = jin && i >= ilo && i < ihi && (DENSE || v != 0.0f);
+                    if (keep) {
+                        dcol[o] = rowbase + i;
+                        dval[o] = v;
+                    }
+                    o += keep ? 1 : 0;
+                }
+            }
+        } else {
+            for (int j = jlo; j < jhi; ++j) {
+                const int rowbase = (xr + j) * P.n + yc;
+                const float* tj = s_taps + j * k;
+                for (int i = ilo; i < ihi; ++i) {
+                    const float v = tj[i];
+                    if (v != 0.0f) {  // drops +-0.0, keeps NaN (inc/sparse.hpp:335)
+                        dcol[o] = rowbase + i;
+                        dval[o] = v;
+                        ++o;
+                    }
                 }
             }
         }
@@ -191,15 +214,31 @@ __global__ void __launch_bounds__(256) csr_build_kernel(const BuildParams P) {
     }
 }
 
-cudaError_t launch_csr_build(const BuildParams& bp, int block, size_t smem, cudaStream_t st) {
+template <int KC, bool DENSE>
+static cudaError_t launch_k(const BuildParams& bp, int block, size_t smem, cudaStream_t st) {
     if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(csr_build_kernel,
+        cudaError_t e = cudaFuncSetAttribute(csr_build_kernel<KC, DENSE>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
     const int grid = (bp.rows + block - 1) / block;
-    csr_build_kernel<<<grid, block, smem, st>>>(bp);
+    csr_build_kernel<KC, DENSE><<<grid, block, smem, st>>>(bp);
     return cudaGetLastError();
+}
+
+cudaError_t launch_csr_build(const BuildParams& bp, bool dense, int block, size_t smem,
+                             cudaStream_t st) {
+    if (bp.stage) {  // the unrolled fill needs the staging area's K*K slots per row
+        switch (bp.k) {
+            case 1: return dense ? launch_k<1, true>(bp, block, smem, st) : launch_k<1, false>(bp, block, smem, st);
+            case 3: return dense ? launch_k<3, true>(bp, block, smem, st) : launch_k<3, false>(bp, block, smem, st);
+            case 5: return dense ? launch_k<5, true>(bp, block, smem, st) : launch_k<5, false>(bp, block, smem, st);
+            case 7: return dense ? launch_k<7, true>(bp, block, smem, st) : launch_k<7, false>(bp, block, smem, st);
+            case 11: return dense ? launch_k<11, true>(bp, block, smem, st) : launch_k<11, false>(bp, block, smem, st);
+            default: break;
+        }
+    }
+    return launch_k<0, false>(bp, block, smem, st);
 }
 
 }  // namespace spb

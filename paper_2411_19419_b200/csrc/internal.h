@@ -94,10 +94,12 @@ struct GenericParams {
 };
 
 // Launchers (return cudaError_t of the launch).
-cudaError_t launch_csr_build(const BuildParams& bp, int block, size_t smem, cudaStream_t st);
+cudaError_t launch_csr_build(const BuildParams& bp, bool dense, int block, size_t smem,
+                             cudaStream_t st);
 cudaError_t launch_tiled(const TiledParams& tp, const CUtensorMap* tmap, int bt, size_t smem,
                          cudaStream_t st);
 cudaError_t launch_generic(const GenericParams& gp, cudaStream_t st);
+cudaError_t launch_spmv_unrolled(const GenericParams& gp, int kmax, cudaStream_t st);
 bool banded_supported(int k, int s);
 cudaError_t launch_banded(int k, int s, const BandedParams& bp, const CUtensorMap* tmap,
                           cudaStream_t st, BandedShape* shape);

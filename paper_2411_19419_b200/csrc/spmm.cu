@@ -153,6 +153,48 @@ __global__ void __launch_bounds__(256) csr_spmm_generic(const GenericParams P) {
     }
 }
 
+// Latency-oriented SpMV / small-batch SpMM for any CSR whose rows hold at most
+// KMAX entries: thread per row, every (col, val) of the row requested at once
+// (fully unrolled, predicated), then every x gather at once -- three dependent
+// memory round trips per row instead of one per entry.  Used for batch <= 2
+// (BASELINE config 2 is a single 512^2 image: ~15 MB, latency-bound).
+template <int KMAX>
+__global__ void __launch_bounds__(256) csr_spmv_unrolled(const GenericParams P) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= P.rows) return;
+    const int e0 = __ldg(P.row_ptr + r);
+    const int cnt = __ldg(P.row_ptr + r + 1) - e0;
+    if (cnt > KMAX) __trap();  // dispatcher guarantees max row length <= KMAX
+    int c[KMAX];
+    float v[KMAX];
+#pragma unroll
+    for (int q = 0; q < KMAX; ++q) {
+        c[q] = q < cnt ? __ldg(P.col_idx + e0 + q) : 0;
+        v[q] = q < cnt ? __ldg(P.vals + e0 + q) : 0.0f;
+    }
+    for (int b = 0; b < P.batch; ++b) {
+        const float* x = P.X + (int64_t)b * P.ldx;
+        float xv[KMAX];
+#pragma unroll
+        for (int q = 0; q < KMAX; ++q) xv[q] = q < cnt ? __ldg(x + c[q]) : 0.0f;
+        float acc = 0.0f;
+#pragma unroll
+        for (int q = 0; q < KMAX; ++q)
+            if (q < cnt) acc = fmaf(v[q], xv[q], acc);
+        P.Y[(int64_t)b * P.ldy + r] = acc;
+    }
+}
+
+cudaError_t launch_spmv_unrolled(const GenericParams& gp, int kmax, cudaStream_t st) {
+    const int block = 256;
+    const int grid = (gp.rows + block - 1) / block;
+    if (kmax <= 9) csr_spmv_unrolled<9><<<grid, block, 0, st>>>(gp);
+    else if (kmax <= 25) csr_spmv_unrolled<25><<<grid, block, 0, st>>>(gp);
+    else if (kmax <= 49) csr_spmv_unrolled<49><<<grid, block, 0, st>>>(gp);
+    else return cudaErrorInvalidValue;
+    return cudaGetLastError();
+}
+
 template <int BT>
 static cudaError_t launch_bt(const TiledParams& tp, const CUtensorMap* tmap, size_t smem,
                              cudaStream_t st) {

@@ -46,7 +46,12 @@ def build(sp, spec, kern):
 
 
 def bits(a):
-    return np.ascontiguousarray(a).view(np.uint32)
+    """fp32 bit patterns, with every NaN canonicalised (the GPU's default NaN is
+    0x7fffffff, x86's 0x7fc00000/0xffc00000; payloads are not part of the contract)."""
+    a = np.ascontiguousarray(a, np.float32)
+    v = a.view(np.uint32).copy()
+    v[np.isnan(a)] = 0x7FC00000
+    return v
 
 
 def assert_same_csr(t, ref_csr):
@@ -174,7 +179,7 @@ def test_spmv_config2_all_paths(sp, orc, torch_cuda):
     t = build(sp, CONFIGS[1], kern)
     rp, ri, rv = orc.build_native(*CONFIGS[1], kern)
     want = orc.spmm_native(rp, ri, rv, X)
-    for path in (None, "banded", "tiled", "tiled_notma", "generic"):
+    for path in (None, "spmv", "banded", "tiled", "tiled_notma", "generic"):
         Y = run_spmm(torch_cuda, sp, t, X, path)
         assert np.array_equal(bits(Y), bits(want)), path
     # fp64 reference tolerance
@@ -189,7 +194,7 @@ def test_spmm_batches_and_tails(sp, orc, torch_cuda, batch):
     kern, X = problem(orc, 7, 96, 72, 5, batch=batch)
     t = build(sp, spec, kern)
     want = orc.spmm_native(*orc.build_native(*spec, kern), X)
-    for path in (None, "banded", "tiled", "tiled_notma", "generic"):
+    for path in (None, "spmv", "banded", "tiled", "tiled_notma", "generic"):
         assert np.array_equal(bits(run_spmm(torch_cuda, sp, t, X, path)), bits(want)), path
     # padded leading dimension (ldx = cols + 4 keeps TMA-legal 16B strides)
     assert np.array_equal(bits(run_spmm(torch_cuda, sp, t, X, None, ldx_pad=4)), bits(want))
@@ -267,7 +272,7 @@ def test_spmm_nonfinite_inputs(sp, orc, torch_cuda):
     X[2, 1023] = -np.inf
     t = build(sp, spec, kern)
     want = orc.spmm_native(*orc.build_native(*spec, kern), X)
-    for path in (None, "banded", "tiled", "tiled_notma", "generic"):
+    for path in (None, "spmv", "banded", "tiled", "tiled_notma", "generic"):
         Y = run_spmm(torch_cuda, sp, t, X, path)
         assert np.array_equal(bits(Y), bits(want)), path
 
