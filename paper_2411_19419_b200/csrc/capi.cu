@@ -205,6 +205,20 @@ int encode_x_map(CUtensorMap* tmap, const float* X, const Geom& g, int64_t ldx, 
     return SPCONV_OK;
 }
 
+// Transforms are allocated from the device's stream-ordered pool; keep freed
+// blocks in the pool (instead of unmapping them at every synchronisation) so a
+// rebuild costs the kernel, not a page-table update.
+void keep_pool_memory(int device) {
+    static std::once_flag flags[64];
+    std::call_once(flags[device & 63], [device] {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+    });
+}
+
 int device_sm_count() {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -382,6 +396,7 @@ int spconv_build_csr(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
     DeviceGuard dg(device);
     if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    keep_pool_memory(device);
 
     auto* h = new (std::nothrow) spconv_csr();
     if (!h) return fail(SPCONV_ECUDA, "out of host memory");

@@ -12,8 +12,8 @@
 // read from -- and verified against -- the CSR.)
 //
 // Structure check (prologue, once per tile, amortised over the batch): the
-// CTA reads the (col, val) pairs of every one of its rows from the CSR and
-// verifies (1) each row stores exactly the taps of its placement that land
+// CTA streams the (col, val) pairs of every one of its rows from the CSR
+// (coalesced 16-byte loads) and verifies (1) each row stores exactly the taps of its placement that land
 // inside the image, at the columns (s x + j - p) n + (s y + i - p), in (j, i)
 // order, and (2) every row stores the same value for tap (j, i) -- the
 // values are taken from the CSR itself (a full row of the tile).  Tiles that
@@ -110,11 +110,11 @@ __global__ void __launch_bounds__(BandedCfg<K, S, V, TH, BT, STAGES>::THREADS)
     __syncthreads();
     const int src = *s_src;
     if (src != 0x7fffffff && t == src / V) {
-        int ev = 0;
+        int es = 0;
 #pragma unroll
         for (int v = 0; v < V; ++v)
-            if (v == src % V) ev = e0[v];
-        for (int q = 0; q < K * K; ++q) s_w[q] = __ldg(P.vals + ev + q);
+            if (v == src % V) es = e0[v];
+        for (int q = 0; q < K * K; ++q) s_w[q] = __ldg(P.vals + es + q);
     }
     __syncthreads();
     float w[K * K];
@@ -124,29 +124,67 @@ __global__ void __launch_bounds__(BandedCfg<K, S, V, TH, BT, STAGES>::THREADS)
         w[q] = s_w[q];
         ok &= isfinite(w[q]);
     }
-#pragma unroll
+    // Warp w checks the 32 rows (xb+v, y0..y0+31) of each v.  Consecutive
+    // output columns are consecutive rows of T, so an interior segment (every
+    // row full) is one contiguous run of 32*K*K pairs: it is streamed with
+    // coalesced 16-byte loads and each lane checks four entries at a time.
+    // Border segments (clipped rows) are walked row by row.
+#pragma unroll 1
     for (int v = 0; v < V; ++v) {
-        if (cnt[v] < 0) continue;
+        // Select (not index) so e0[] / cnt[] stay in registers.
+        int cv = cnt[0], ev = e0[0];
+#pragma unroll
+        for (int u = 1; u < V; ++u)
+            if (u == v) cv = cnt[u], ev = e0[u];
         const int x = xb + v;
-        int e = e0[v];
-        const int e_last = e0[v] + max(cnt[v], 1) - 1;
+        const bool has = cv >= 0;
+        const unsigned vmask = __ballot_sync(0xffffffffu, has);
+        if (vmask == 0u) continue;
+        if (__all_sync(0xffffffffu, !has || cv == K * K)) {
+            const int nval = __popc(vmask);  // valid lanes form a prefix
+            const int S0 = __shfl_sync(0xffffffffu, ev, 0);
+            const int len = nval * K * K;
+            const int gx = S * x - P.p, gy0 = S * y0 - P.p;
+            const int lead = S0 & 3;
+#pragma unroll 4
+            for (int d4 = lane * 4 - lead; d4 < len; d4 += 128) {
+                const int4 c4 = __ldg(reinterpret_cast<const int4*>(P.col_idx + S0 + d4));
+                const float4 v4 = __ldg(reinterpret_cast<const float4*>(P.vals + S0 + d4));
+                const int cc[4] = {c4.x, c4.y, c4.z, c4.w};
+                const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
-        for (int j = 0; j < K; ++j) {
-            const int gr = S * x + j - P.p;
-            const bool rin = gr >= 0 && gr < P.m;
-#pragma unroll
-            for (int i = 0; i < K; ++i) {
-                const int gc = S * y + i - P.p;
-                if (rin && gc >= 0 && gc < P.n) {
-                    const int ec = min(e, e_last);
-                    const int c = __ldg(P.col_idx + ec);
-                    const float val = __ldg(P.vals + ec);
-                    ok &= (c == gr * P.n + gc) && (__float_as_uint(val) == __float_as_uint(w[j * K + i]));
-                    ++e;
+                for (int u = 0; u < 4; ++u) {
+                    const int d = d4 + u;
+                    if (d >= 0 && d < len) {
+                        const int l = d / (K * K), q = d - l * (K * K);
+                        const int j = q / K, i = q - j * K;
+                        ok &= (cc[u] == (gx + j) * P.n + gy0 + S * l + i) &&
+                              (__float_as_uint(vv[u]) == __float_as_uint(s_w[q]));
+                    }
                 }
             }
+        } else if (has) {
+            int e = ev;
+            const int e_last = ev + max(cv, 1) - 1;
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+                const int gr = S * x + j - P.p;
+                const bool rin = gr >= 0 && gr < P.m;
+#pragma unroll
+                for (int i = 0; i < K; ++i) {
+                    const int gc = S * y + i - P.p;
+                    if (rin && gc >= 0 && gc < P.n) {
+                        const int ec = min(e, e_last);
+                        const int c = __ldg(P.col_idx + ec);
+                        const float val = __ldg(P.vals + ec);
+                        ok &= (c == gr * P.n + gc) &&
+                              (__float_as_uint(val) == __float_as_uint(w[j * K + i]));
+                        ++e;
+                    }
+                }
+            }
+            ok &= (e - ev) == cv;
         }
-        ok &= (e - e0[v]) == cnt[v];
     }
     const bool fast = __syncthreads_and(ok) != 0;
 
