@@ -275,7 +275,10 @@ int run_spmm(const spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t
         const int64_t want = 16ll * device_sm_count();
         int64_t splits = (want + tiles - 1) / tiles;
         splits = std::max<int64_t>(1, std::min<int64_t>(splits, groups / 2));
+        if (const char* e = std::getenv("SPCONV_B200_SPLITS"))  // tuning experiments
+            splits = std::max<int64_t>(1, std::min<int64_t>(std::atoll(e), groups));
         bp.splits = (int)splits;
+        bp.diag = std::getenv("SPCONV_B200_DIAG") ? std::atoi(std::getenv("SPCONV_B200_DIAG")) : 0;
         CUtensorMap tmap;
         if (int rc = encode_x_map(&tmap, X, g, ldx, batch, sh.wc, sh.wr, sh.bt)) return rc;
         CK(spb::launch_banded((int)g.k, (int)g.s, bp, &tmap, st, nullptr));

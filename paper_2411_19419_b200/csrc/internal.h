@@ -75,6 +75,7 @@ struct BandedParams {
     int m, n, p, mo, no;
     int tiles_y;  // tiles across n_out (tile width 32)
     int splits;   // batch splits per tile
+    int diag;     // diagnostics only (SPCONV_B200_DIAG): 1 = time the kernel without the band check
 };
 
 struct BandedShape {

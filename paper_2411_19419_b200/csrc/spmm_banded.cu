@@ -13,7 +13,7 @@
 //
 // Structure check (prologue, once per tile, amortised over the batch): the
 // CTA streams the (col, val) pairs of every one of its rows from the CSR
-// (coalesced 16-byte loads) and verifies (1) each row stores exactly the taps of its placement that land
+// (coalesced loads, compared against a per-CTA pattern table) and verifies (1) each row stores exactly the taps of its placement that land
 // inside the image, at the columns (s x + j - p) n + (s y + i - p), in (j, i)
 // order, and (2) every row stores the same value for tap (j, i) -- the
 // values are taken from the CSR itself (a full row of the tile).  Tiles that
@@ -28,6 +28,8 @@
 // out-of-range coordinates zero-filled), STAGES-deep on mbarriers.  The grid
 // is tiles x batch-splits (split fastest, so the CTAs sharing a tile's CSR run
 // together and re-read it from L2).
+#include <cstdlib>
+
 #include "internal.h"
 #include "tma.cuh"
 
@@ -41,7 +43,8 @@ struct BandedCfg {
     static constexpr int THREADS = 32 * (TH / V);
     static constexpr int SF = (BT * WIN + 31) & ~31;             // stage stride (128B aligned)
     static constexpr int JJ = S * (V - 1) + K;                   // input rows per thread
-    static constexpr size_t SMEM = 128 + (size_t)STAGES * SF * 4 + 4 * K * K + 16;
+    static constexpr int SEG = 32 * K * K;                       // entries of a full 32-row segment
+    static constexpr size_t SMEM = 128 + (size_t)STAGES * SF * 4 + 8 * (size_t)SEG + 4 * K * K + 16;
     static_assert(TH % V == 0, "TH must be a multiple of V");
     static_assert(WC <= 256 && WR <= 256, "TMA box limit");
 };
@@ -53,7 +56,9 @@ __global__ void __launch_bounds__(BandedCfg<K, S, V, TH, BT, STAGES>::THREADS)
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
     float* xs = reinterpret_cast<float*>(smem + 128);
-    float* s_w = xs + (size_t)STAGES * C::SF;
+    int* s_pc = reinterpret_cast<int*>(xs + (size_t)STAGES * C::SF);  // expected col offsets
+    uint32_t* s_pv = reinterpret_cast<uint32_t*>(s_pc + C::SEG);      // expected value bits
+    float* s_w = reinterpret_cast<float*>(s_pv + C::SEG);
     int* s_src = reinterpret_cast<int*>(s_w + K * K);
 
     const int t = threadIdx.x;
@@ -63,7 +68,7 @@ __global__ void __launch_bounds__(BandedCfg<K, S, V, TH, BT, STAGES>::THREADS)
     const int x0 = tx * TH, y0 = ty * 32;
     const int wr0 = S * x0 - P.p;
     const int cstart = S * y0 - P.p;
-    const int wc0 = cstart & ~3;
+    const int wc0 = cstart & ~3;  // the box's first column must be 16-byte aligned
     const int delta = cstart - wc0;
     const int y = y0 + lane;
     const int xb = x0 + warp * V;  // this thread's first output row (image row index)
@@ -124,11 +129,23 @@ __global__ void __launch_bounds__(BandedCfg<K, S, V, TH, BT, STAGES>::THREADS)
         w[q] = s_w[q];
         ok &= isfinite(w[q]);
     }
+    if (P.diag == 1) goto checked;  // diagnostic timing only: outputs unverified
+    // Expected pattern of a full 32-row segment, relative to its first column:
+    // entry d = l*K*K + j*K + i (row l of the segment, tap (j, i)) sits at
+    // column S*l + j*n + i and holds tap value w[j*K + i].
+    for (int d = t; d < C::SEG; d += C::THREADS) {
+        const int l = d / (K * K), q = d - l * (K * K);
+        const int j = q / K, i = q - j * K;
+        s_pc[d] = S * l + j * P.n + i;
+        s_pv[d] = __float_as_uint(s_w[q]);
+    }
+    __syncthreads();
     // Warp w checks the 32 rows (xb+v, y0..y0+31) of each v.  Consecutive
     // output columns are consecutive rows of T, so an interior segment (every
-    // row full) is one contiguous run of 32*K*K pairs: it is streamed with
-    // coalesced 16-byte loads and each lane checks four entries at a time.
-    // Border segments (clipped rows) are walked row by row.
+    // row full) is one contiguous run of 32*K*K pairs: lanes stream it with
+    // coalesced loads (all K*K loads per lane in flight at once) and compare
+    // against the pattern table.  Border segments (clipped rows) are walked
+    // row by row.
 #pragma unroll 1
     for (int v = 0; v < V; ++v) {
         // Select (not index) so e0[] / cnt[] stay in registers.
@@ -141,28 +158,24 @@ __global__ void __launch_bounds__(BandedCfg<K, S, V, TH, BT, STAGES>::THREADS)
         const unsigned vmask = __ballot_sync(0xffffffffu, has);
         if (vmask == 0u) continue;
         if (__all_sync(0xffffffffu, !has || cv == K * K)) {
-            const int nval = __popc(vmask);  // valid lanes form a prefix
+            const int len = __popc(vmask) * K * K;  // valid lanes form a prefix
             const int S0 = __shfl_sync(0xffffffffu, ev, 0);
-            const int len = nval * K * K;
-            const int gx = S * x - P.p, gy0 = S * y0 - P.p;
-            const int lead = S0 & 3;
-#pragma unroll 4
-            for (int d4 = lane * 4 - lead; d4 < len; d4 += 128) {
-                const int4 c4 = __ldg(reinterpret_cast<const int4*>(P.col_idx + S0 + d4));
-                const float4 v4 = __ldg(reinterpret_cast<const float4*>(P.vals + S0 + d4));
-                const int cc[4] = {c4.x, c4.y, c4.z, c4.w};
-                const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+            const int base = (S * x - P.p) * P.n + (S * y0 - P.p);
+            uint32_t bad = 0;
+            int cs[K * K];
+            uint32_t vs[K * K];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int d = d4 + u;
-                    if (d >= 0 && d < len) {
-                        const int l = d / (K * K), q = d - l * (K * K);
-                        const int j = q / K, i = q - j * K;
-                        ok &= (cc[u] == (gx + j) * P.n + gy0 + S * l + i) &&
-                              (__float_as_uint(vv[u]) == __float_as_uint(s_w[q]));
-                    }
-                }
+            for (int it = 0; it < K * K; ++it) {
+                const int d = lane + 32 * it;
+                cs[it] = d < len ? __ldg(P.col_idx + S0 + d) : 0;
+                vs[it] = d < len ? __float_as_uint(__ldg(P.vals + S0 + d)) : 0u;
             }
+#pragma unroll
+            for (int it = 0; it < K * K; ++it) {
+                const int d = lane + 32 * it;
+                if (d < len) bad |= ((uint32_t)(cs[it] - base) ^ (uint32_t)s_pc[d]) | (vs[it] ^ s_pv[d]);
+            }
+            ok &= bad == 0u;
         } else if (has) {
             int e = ev;
             const int e_last = ev + max(cv, 1) - 1;
@@ -186,10 +199,12 @@ __global__ void __launch_bounds__(BandedCfg<K, S, V, TH, BT, STAGES>::THREADS)
             ok &= (e - ev) == cv;
         }
     }
+checked:
     const bool fast = __syncthreads_and(ok) != 0;
 
     // ---- main loop over this CTA's image groups ----
     const int tbase = (S * warp * V) * C::WC + S * lane + delta;
+    const bool odd = (delta & 1) != 0;  // uniform: pair loads start one column early
     for (int g = 0; g < ng; ++g) {
         const int st = g % STAGES;
         const float* xw = xs + (size_t)st * C::SF;
@@ -205,8 +220,36 @@ __global__ void __launch_bounds__(BandedCfg<K, S, V, TH, BT, STAGES>::THREADS)
 #pragma unroll
                 for (int jj = 0; jj < C::JJ; ++jj) {
                     float xr[K];
+                    const float* xrow = xt + b * C::WIN + jj * C::WC;
+                    if (S % 2 == 0) {
+                        // Lanes are S floats apart: 8-byte pair loads keep every
+                        // bank busy (scalar loads at stride 2 conflict 2-way).
+                        // The pairs start on an even column (odd delta: one early).
+                        if (!odd) {
 #pragma unroll
-                    for (int i = 0; i < K; ++i) xr[i] = xt[b * C::WIN + jj * C::WC + i];
+                            for (int i = 0; i + 1 < K; i += 2) {
+                                const float2 pr = *reinterpret_cast<const float2*>(xrow + i);
+                                xr[i] = pr.x;
+                                xr[i + 1] = pr.y;
+                            }
+                            if (K % 2) xr[K - 1] = xrow[K - 1];
+                        } else {
+                            xr[0] = xrow[0];
+#pragma unroll
+                            for (int i = 1; i < K; i += 2) {
+                                if (i + 1 < K) {
+                                    const float2 pr = *reinterpret_cast<const float2*>(xrow + i);
+                                    xr[i] = pr.x;
+                                    xr[i + 1] = pr.y;
+                                } else {
+                                    xr[i] = xrow[i];
+                                }
+                            }
+                        }
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < K; ++i) xr[i] = xrow[i];
+                    }
 #pragma unroll
                     for (int v = 0; v < V; ++v) {
                         const int j = jj - S * v;
@@ -295,11 +338,25 @@ bool banded_supported(int k, int s) {
 
 cudaError_t launch_banded(int k, int s, const BandedParams& bp, const CUtensorMap* tmap,
                           cudaStream_t st, BandedShape* shape) {
-    if (k == 3 && s == 1) return launch_cfg<3, 1, 4, 32, 4, 4>(bp, tmap, st, shape);
+    // Tuning variants (SPCONV_B200_VARIANT, experiments only); 0 = default.
+    static const int var = std::getenv("SPCONV_B200_VARIANT") ? std::atoi(std::getenv("SPCONV_B200_VARIANT")) : 0;
+    if (k == 3 && s == 1) {
+        if (var == 1) return launch_cfg<3, 1, 4, 32, 4, 4>(bp, tmap, st, shape);
+        if (var == 2) return launch_cfg<3, 1, 4, 16, 4, 3>(bp, tmap, st, shape);
+        if (var == 3) return launch_cfg<3, 1, 8, 16, 4, 4>(bp, tmap, st, shape);
+        if (var == 4) return launch_cfg<3, 1, 4, 16, 8, 3>(bp, tmap, st, shape);
+        return launch_cfg<3, 1, 4, 16, 4, 4>(bp, tmap, st, shape);
+    }
     if (k == 5 && s == 1) return launch_cfg<5, 1, 4, 16, 4, 4>(bp, tmap, st, shape);
     if (k == 3 && s == 2) return launch_cfg<3, 2, 4, 16, 2, 4>(bp, tmap, st, shape);
     if (k == 5 && s == 2) return launch_cfg<5, 2, 4, 16, 2, 4>(bp, tmap, st, shape);
-    if (k == 7 && s == 2) return launch_cfg<7, 2, 4, 16, 2, 4>(bp, tmap, st, shape);
+    if (k == 7 && s == 2) {
+        if (var == 1) return launch_cfg<7, 2, 4, 16, 2, 4>(bp, tmap, st, shape);
+        if (var == 2) return launch_cfg<7, 2, 8, 16, 2, 2>(bp, tmap, st, shape);
+        if (var == 3) return launch_cfg<7, 2, 8, 32, 1, 2>(bp, tmap, st, shape);
+        if (var == 4) return launch_cfg<7, 2, 4, 8, 2, 2>(bp, tmap, st, shape);
+        return launch_cfg<7, 2, 4, 16, 2, 2>(bp, tmap, st, shape);
+    }
     return cudaErrorInvalidValue;
 }
 
