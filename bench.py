@@ -7,12 +7,14 @@ CSR transform T (9,424,900 stored entries).  With N GPUs (torchrun, one rank
 per GPU) every rank builds its own CSR replica on its device and owns a
 contiguous slice of the batch; there is no collective on the data path.
 
-One step = one SpMM launch over this rank's batch slice, inputs resident in
-HBM (each X slice is larger than the 126 MB L2, so no flush is needed; for
---config 2, whose working set fits in L2, a 512 MB scrub runs between steps
-outside the timed events).  value = whole-job nnz-MACs per second (total
-images x nnz / max-over-ranks device time).  e2e = the same metric through the
-C ABI with pinned HOST buffers (H2D + SpMM + D2H pipelined in the library).
+One step = one spconv_spmm call over this rank's images (the CSR band check
++ the register-blocked apply: two launches), inputs resident in HBM (config
+3's 1 GB X slice is larger than the 126 MB L2, so no flush is needed; working
+sets under 2x L2 get a 512 MB scrub between steps outside the timed events).
+Scaling is weak: each rank owns per_gpu_batch images.  value = whole-job
+nnz-MACs per second (total images x nnz / max-over-ranks device time).
+e2e = the same metric through the C ABI with pinned HOST buffers (H2D + SpMM
++ D2H pipelined in the library).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 """
@@ -31,13 +33,16 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# per_gpu_batch: images each rank owns (weak scaling: the job grows with N).
 CONFIGS = {
-    1: dict(spec=(64, 64, 3, 1, 1), batch=1, name="config1: 64x64 single image, k3 s1 p1"),
-    2: dict(spec=(512, 512, 5, 2, 2), batch=1, name="config2: 512x512 single image, k5 s2 p2 SpMV"),
-    3: dict(spec=(1024, 1024, 3, 1, 1), batch=256,
-            name="config3: batch 256 of 1024x1024 images, k3 s1 p1, batched SpMM"),
-    4: dict(spec=(4096, 4096, 7, 2, 3), batch=64,
-            name="config4: batch 64 of 4096x4096 images, k7 s2 p3, build + batched SpMM"),
+    1: dict(spec=(64, 64, 3, 1, 1), per_gpu_batch=1, name="config1: 64x64 single image, k3 s1 p1"),
+    2: dict(spec=(512, 512, 5, 2, 2), per_gpu_batch=1,
+            name="config2: 512x512 single image, k5 s2 p2 SpMV"),
+    3: dict(spec=(1024, 1024, 3, 1, 1), per_gpu_batch=256,
+            name="config3: 1024x1024 images, k3 s1 p1, batched SpMM, 256 images per GPU"),
+    4: dict(spec=(4096, 4096, 7, 2, 3), per_gpu_batch=8,
+            name="config4: 4096x4096 images, k7 s2 p3, build + batched SpMM, 8 images per GPU "
+                 "(batch 64 over 8 GPUs)"),
 }
 METRIC = "SpMV-conv nnz-MAC/s (whole job) with HBM GB/s and CSR build ms"
 UNIT = "G nnz-MAC/s"
@@ -52,15 +57,22 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(cfg: int):
-    """dram bytes per launch of the SpMM kernel from the committed ncu capture."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
-            j = json.load(f)
-        e = j.get(f"config{cfg}")
-        return (float(e["dram_bytes_per_launch"]), e.get("source")) if e else (None, None)
-    except Exception:
-        return None, None
+def ncu_traffic(cfg: int, batch: int):
+    """DRAM bytes (read + write) of one spmm call at this config and per-GPU
+    batch, from the newest committed ncu --set full capture (profiles/*/
+    ncu_summary.json, written by scripts/make_profiles.py); None if absent."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "ncu_summary.json")), reverse=True):
+        try:
+            with open(path) as f:
+                j = json.load(f)
+        except Exception:
+            continue
+        hits = [e for e in j.values() if e.get("config") == cfg and e.get("batch") == batch
+                and e.get("role") == "spmm"]
+        if hits:
+            return sum(e["dram_bytes_per_launch"] for e in hits), ", ".join(e["source"] for e in hits)
+    return None, None
 
 
 class ClockSampler:
@@ -210,7 +222,7 @@ def run_reference(args, cfg):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg["name"] + " -- one image per step (bounded CPU sample)",
                    "m": m, "n": n, "k": k, "s": s, "p": p, "nnz": nnz},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
@@ -224,12 +236,94 @@ def run_reference(args, cfg):
 # Our arm
 # ----------------------------------------------------------------------------
 
+def timed_build(sp, torch, kern, spec, dev, stream, reps=5, warm=3):
+    """Device time of the one-time CSR build (kernel only: a GPU-side sleep
+    queued first keeps the stream busy while the host enqueues the build, so
+    the events bracket GPU work, not host latency) and host wall time of the call."""
+    out, t = [], None
+    for i in range(warm + reps):
+        if t is not None:
+            t.close()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(2_000_000)
+        e0.record(stream)
+        h0 = time.perf_counter()
+        t = sp.build_transform(kern, spec, device=dev.index, stream=stream)
+        h1 = time.perf_counter()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        if i >= warm:
+            out.append((e0.elapsed_time(e1), (h1 - h0) * 1e3))
+    return t, statistics.median(x[0] for x in out), statistics.median(x[1] for x in out)
+
+
+def device_steps(sp, torch, t, b, steps, warmup, dev, stream, seed):
+    """Times `steps` spmm calls over a resident [b, cols] batch (CUDA events on
+    the launching stream).  Inputs smaller than 2x L2 get a 512 MB scrub
+    between steps, outside the events."""
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(seed)
+    X = torch.randn(max(b, 1), t.cols, generator=gen, device=dev, dtype=torch.float32)
+    Y = torch.empty(max(b, 1), t.rows, device=dev, dtype=torch.float32)
+    l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
+    need_flush = 4 * b * (t.cols + t.rows) + 8 * t.nnz < 2 * l2_bytes
+    scrub = torch.empty(512 << 20, dtype=torch.uint8, device=dev) if need_flush else None
+    for i in range(warmup):
+        if scrub is not None:
+            scrub.fill_(i & 0xFF)
+        sp.spmm(t, X[:b], Y[:b], stream=stream)
+    torch.cuda.synchronize(dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(steps)]
+    for i in range(steps):
+        if scrub is not None:
+            scrub.fill_(i & 0xFF)  # outside the events: evicts X, Y and T from L2
+        ev[i][0].record(stream)
+        sp.spmm(t, X[:b], Y[:b], stream=stream)
+        ev[i][1].record(stream)
+    torch.cuda.synchronize(dev)
+    ms = [a.elapsed_time(c) for a, c in ev]
+    l2 = ("512 MB scrub between steps (outside events)" if need_flush else
+          f"working set larger than L2 (X+Y+T {(4 * b * (t.cols + t.rows) + 8 * t.nnz) / 1e6:.0f} MB"
+          f" > 2 x {l2_bytes / 1e6:.0f} MB)")
+    return X, Y, ms, l2
+
+
+def secondary(sp, torch, dev, stream, steps):
+    """N=1 extras: config 2 (single-image SpMV, cold L2) and config 4 at its
+    per-GPU batch (8 images) -- kernel time, roofline fraction and build."""
+    out = {}
+    peak, _ = peaks()
+    rng = np.random.default_rng(99)
+    for c in (2, 4):
+        cfg = CONFIGS[c]
+        m, n, k, s, p = cfg["spec"]
+        b = cfg["per_gpu_batch"]
+        spec = sp.ConvSpec(m, n, k, s, p)
+        kern = sp.Kernel(k, rng.standard_normal(k * k).astype(np.float32))
+        t, bld_ms, _ = timed_build(sp, torch, kern, spec, dev, stream)
+        X, Y, ms, l2 = device_steps(sp, torch, t, b, steps, 3, dev, stream, 7)
+        alg = algorithmic_bytes(t.rows, t.cols, t.nnz, b)
+        mean = statistics.mean(ms)
+        bb = 8 * t.nnz + 4 * (t.rows + 1)
+        out[f"config{c}"] = {
+            "workload": cfg["name"], "batch": b, "kernel": t.last_kernel, "ms_per_step": mean,
+            "ms_min": min(ms), "value": b * t.nnz / (mean * 1e-3) / 1e9, "unit": UNIT,
+            "gb_per_s": alg / (mean * 1e-3) / 1e9, "frac": alg / (mean * 1e-3) / 1e9 / peak,
+            "l2": l2, "build_ms_device": bld_ms, "build_frac": bb / (bld_ms * 1e-3) / 1e9 / peak,
+        }
+        del X, Y
+        t.close()
+    return out
+
+
 def run_ours(args, cfg):
     import torch
     import torch.distributed as dist
 
     import paper_2411_19419_b200 as sp
-    from paper_2411_19419_b200.shard import batch_slice, max_over_ranks, sum_over_ranks
+    from paper_2411_19419_b200.shard import max_over_ranks, sum_over_ranks
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -242,74 +336,41 @@ def run_ours(args, cfg):
         dist.init_process_group("nccl", device_id=dev)
 
     m, n, k, s, p = cfg["spec"]
-    total_batch = args.batch or cfg["batch"]
-    b0, b = batch_slice(total_batch, rank, world)
+    # Weak scaling: every rank owns a fixed slice of `b` images (the batch
+    # shards with no collective); the whole job processes b * world images.
+    b = args.batch or cfg["per_gpu_batch"]
+    total_batch = b * world
     spec = sp.ConvSpec(m, n, k, s, p)
     rng = np.random.default_rng(1234)
     kern = sp.Kernel(k, rng.standard_normal(k * k).astype(np.float32))
     stream = torch.cuda.current_stream(dev)
 
-    # ---- CSR build (one-time cost), device-timed ----
-    build_ms = []
-    t = None
-    for i in range(3 + 5):
-        if t is not None:
-            t.close()
-        torch.cuda.synchronize(dev)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        h0 = time.perf_counter()
-        e0.record(stream)
-        t = sp.build_transform(kern, spec, device=local, stream=stream)
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        if i >= 3:
-            build_ms.append((e0.elapsed_time(e1), (time.perf_counter() - h0) * 1e3))
+    # ---- CSR build (one-time cost), device-timed: a local replica per rank ----
+    t, bld_dev, bld_host = timed_build(sp, torch, kern, spec, dev, stream)
     rows, cols, nnz = t.rows, t.cols, t.nnz
 
-    # ---- inputs resident in HBM ----
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(1000 + rank)
-    X = torch.randn(max(b, 1), cols, generator=gen, device=dev, dtype=torch.float32)
-    Y = torch.empty(max(b, 1), rows, device=dev, dtype=torch.float32)
-    l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
-    need_flush = 4 * b * cols < 2 * l2_bytes
-    scrub = torch.empty(512 << 20, dtype=torch.uint8, device=dev) if need_flush else None
-
-    def step():
-        sp.spmm(t, X[:b], Y[:b], stream=stream)
-
-    for _ in range(args.warmup):
-        if scrub is not None:
-            scrub.fill_(1)
-        step()
+    # ---- timed region: inputs resident in HBM ----
     sampler = ClockSampler(local).start()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
     w0 = time.perf_counter()
-    for i in range(args.steps):
-        if scrub is not None:
-            scrub.fill_(i & 0xFF)  # outside the events: evicts X, Y and T from L2
-        ev[i][0].record(stream)
-        step()
-        ev[i][1].record(stream)
-    torch.cuda.synchronize(dev)
+    X, Y, ms, l2 = device_steps(sp, torch, t, b, args.steps, args.warmup, dev, stream, 1000 + rank)
     w1 = time.perf_counter()
     if world > 1:
         dist.barrier()
     sampler.stop()
-    elapsed_ms = sum(a.elapsed_time(c) for a, c in ev)
+    kernel = t.last_kernel
+    launches_per_step = kernel.count("+") + 1
+    elapsed_ms = sum(ms)
     max_ms = max_over_ranks(elapsed_ms, dev)
     ms_per_step = max_ms / args.steps
-    macs = total_batch * nnz * args.steps
-    value = macs / (max_ms * 1e-3) / 1e9
-    launch_ms = elapsed_ms / args.steps  # this rank's average launch duration
+    value = total_batch * nnz * args.steps / (max_ms * 1e-3) / 1e9
+    launch_ms = elapsed_ms / args.steps  # this rank's average step (all launches of one call)
     alg = algorithmic_bytes(rows, cols, nnz, b)
     peak, peak_src = peaks()
     achieved = alg / (launch_ms * 1e-3) / 1e9
-    traffic, traffic_src = ncu_traffic(args.config)
+    traffic, traffic_src = ncu_traffic(args.config, b)
     clocks = sampler.summary(w0, w1)
 
     # ---- e2e through the C ABI with pinned host buffers ----
@@ -317,6 +378,7 @@ def run_ours(args, cfg):
     Xh = torch.empty(max(b, 1), cols, dtype=torch.float32, pin_memory=True)
     Xh.copy_(X.cpu())
     Yh = torch.empty(max(b, 1), rows, dtype=torch.float32, pin_memory=True)
+    del X, Y
     sp.convolve_batch(t, Xh[:b], Yh[:b])  # warm (workspace allocation)
     if world > 1:
         dist.barrier()
@@ -328,10 +390,11 @@ def run_ours(args, cfg):
     e2e_value = total_batch * nnz * e2e_steps / (e2e_max * 1e-3) / 1e9
     h2d = int(sum_over_ranks(4 * b * cols, dev))
     d2h = int(sum_over_ranks(4 * b * rows, dev))
-
-    bld_dev = statistics.median(x[0] for x in build_ms)
-    bld_host = statistics.median(x[1] for x in build_ms)
     bld_bytes = 8 * nnz + 4 * (rows + 1)
+
+    extra = None
+    if rank == 0 and world == 1 and not args.no_secondary:
+        extra = secondary(sp, torch, dev, stream, max(10, min(args.steps, 30)))
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -341,22 +404,22 @@ def run_ours(args, cfg):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
             "config": {
                 "workload": cfg["name"], "m": m, "n": n, "k": k, "s": s, "p": p,
                 "global_batch": total_batch, "per_gpu_batch": b, "rows": rows, "cols": cols,
                 "nnz": nnz, "parallelism": f"batch-dp{world} (CSR replica per GPU, no collective)",
-                "l2": ("512 MB scrub between steps (outside events)" if need_flush else
-                       f"inputs larger than L2 (X slice {4 * b * cols / 1e6:.0f} MB > "
-                       f"{l2_bytes / 1e6:.0f} MB)"),
+                "l2": l2,
             },
             "gb_per_s": achieved,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "algorithmic_bytes": alg, "kernel": "conv_spmm_tiled",
+                         "algorithmic_bytes": alg, "kernel": kernel,
                          "launch_ms": launch_ms, "peak_source": peak_src,
-                         "traffic_source": traffic_src},
+                         "traffic_source": traffic_src,
+                         "note": "achieved = SURVEY 8(d) bytes of one spmm call (all its launches) / "
+                                 "its CUDA-event duration"},
             "build": {"ms_device": bld_dev, "ms_host_wall": bld_host, "bytes": bld_bytes,
                       "gb_per_s": bld_bytes / (bld_dev * 1e-3) / 1e9,
                       "frac": bld_bytes / (bld_dev * 1e-3) / 1e9 / peak},
@@ -364,8 +427,9 @@ def run_ours(args, cfg):
                     "d2h_bytes_per_step": d2h, "steps": e2e_steps,
                     "ms_per_step": e2e_max / e2e_steps,
                     "path": "spconv_convolve_host (C ABI), pinned host buffers"},
-            "gpu_launches": args.steps,
+            "gpu_launches": args.steps * launches_per_step,
             "clocks": clocks,
+            "secondary": extra,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
@@ -382,10 +446,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, choices=sorted(CONFIGS), default=3)
-    ap.add_argument("--batch", type=int, default=0, help="override the global batch")
+    ap.add_argument("--batch", type=int, default=0, help="override the per-GPU batch")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the config 2/4 extras")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")

@@ -111,6 +111,11 @@ int spconv_convolve_host(const spconv_csr* h, const float* X_host, float* Y_host
 int spconv_convolve_host_f64(const spconv_csr* h, const double* X_host, double* Y_host,
                              int64_t batch);
 
+/* Name of the kernel(s) the last spconv_spmv / spconv_spmm /
+ * spconv_convolve_host call on this handle launched (diagnostics; "" before
+ * the first call).  The string is static. */
+const char* spconv_csr_last_kernel(const spconv_csr* h);
+
 /* Frees the handle and its device memory (synchronises its device). */
 int spconv_csr_free(spconv_csr* h);
 

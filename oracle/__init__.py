@@ -207,6 +207,8 @@ class Ref:
         L.ref_direct_conv.argtypes = [i64] * 5 + [C.c_void_p] * 3
         L.ref_run_verification.argtypes = [i64, C.c_int, C.c_void_p, C.c_void_p]
         L.ref_hardware_concurrency.restype = C.c_uint
+        if hasattr(L, "ref_run_layer_bench"):
+            L.ref_run_layer_bench.argtypes = [C.c_char_p] + [i64] * 7 + [u64, C.c_int, C.c_void_p]
         self.L = L
 
     def _chk(self, rc: int):
@@ -267,6 +269,14 @@ class Ref:
 
     def hardware_concurrency(self) -> int:
         return int(self.L.ref_hardware_concurrency())
+
+    def run_layer_bench(self, name, m, n, k, s, p, trials, warmup, seed, threads=1):
+        """inc/bench.hpp:202-261 on one layer -> {method: (mean_us, sem_us, build_us)}."""
+        out = np.zeros(9, np.float64)
+        self._chk(self.L.ref_run_layer_bench(name.encode(), m, n, k, s, p, trials, warmup, seed,
+                                             threads, _p(out)))
+        return {meth: tuple(out[3 * i: 3 * i + 3]) for i, meth in
+                enumerate(("CSR-SpMV", "CSC-SpMV", "im2col"))}
 
 
 class RefTransform:

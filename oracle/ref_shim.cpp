@@ -151,6 +151,29 @@ int ref_run_verification(int64_t max_dim, int seeds, int64_t* out4, double* dev2
     });
 }
 
+// run_layer_bench (inc/bench.hpp:202-261) on one layer: CSR, CSC and im2col
+// timings (mean/sem/build us, 3 x 3 doubles in method order), the
+// reference's own cross-check included.  Layer i of a table uses
+// derive_seed(seed, i) as run_table_bench does (inc/bench.hpp:264-276).
+int ref_run_layer_bench(const char* name, int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
+                        int64_t trials, int64_t warmup, uint64_t seed, int threads, double* out9) {
+    return guarded([&] {
+        spconv::LayerConfig cfg;
+        cfg.name = name;
+        cfg.m = m;
+        cfg.n = n;
+        cfg.k = k;
+        cfg.s = s;
+        cfg.p = p;
+        const auto rs = spconv::run_layer_bench(cfg, trials, warmup, seed, threads);
+        for (size_t i = 0; i < rs.size() && i < 3; ++i) {
+            out9[3 * i] = rs[i].mean_us;
+            out9[3 * i + 1] = rs[i].sem_us;
+            out9[3 * i + 2] = rs[i].build_time_us;
+        }
+    });
+}
+
 unsigned ref_hardware_concurrency() { return std::thread::hardware_concurrency(); }
 
 }  // extern "C"

@@ -62,6 +62,7 @@ _decl("spconv_spmv", [_vp, _vp, _vp, _vp])
 _decl("spconv_spmm", [_vp, _vp, _i64, _vp, _i64, _i64, _vp])
 _decl("spconv_convolve_host", [_vp, _vp, _vp, _i64])
 _decl("spconv_convolve_host_f64", [_vp, _vp, _vp, _i64])
+_decl("spconv_csr_last_kernel", [_vp], C.c_char_p)
 _decl("spconv_csr_free", [_vp])
 
 
@@ -194,6 +195,11 @@ class Transform:
         host or device); synchronous."""
         _check(lib.spconv_csr_copy(self._h, _ptr(row_ptr), _ptr(col_idx), _ptr(vals),
                                    _stream_handle(stream)))
+
+    @property
+    def last_kernel(self) -> str:
+        """Kernel(s) the last apply on this transform launched ("a+b" = two launches)."""
+        return lib.spconv_csr_last_kernel(self._h).decode()
 
     def close(self) -> None:
         if self._h and self._h.value:

@@ -170,11 +170,14 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-// Kernel-path selection: SPCONV_B200_PATH = auto (default) | spmv | banded |
-// tiled | tiled_notma | generic.  auto = spmv (latency kernel) for batch <= 2,
-// else banded when instantiated for (k, s) and the taps are dense, else tiled
-// (TMA when the strides allow); generic for uploaded matrices.  The overrides exist for cross-checking the paths.
-enum Path { kAuto = 0, kBanded, kTiled, kTiledNoTma, kGeneric, kSpmv };
+// Kernel-path selection: SPCONV_B200_PATH = auto (default) | spmv | spmv_plain |
+// banded | tiled | tiled_notma | generic (| banded1: the previous band kernel,
+// kept for A/B timing).  auto = the latency kernels for batch <= 2 (speculative
+// conv_spmv_spec for dense-tap transforms, else csr_spmv_unrolled), else the
+// band path (CSR band check + register-blocked apply) when instantiated for
+// (k, s) with dense taps, else tiled (TMA when the strides allow); generic for
+// uploaded matrices.  The overrides exist for cross-checking the paths.
+enum Path { kAuto = 0, kBanded, kTiled, kTiledNoTma, kGeneric, kSpmv, kBanded1, kSpmvPlain };
 
 Path path_override() {
     const char* e = std::getenv("SPCONV_B200_PATH");
@@ -184,6 +187,8 @@ Path path_override() {
     if (!std::strcmp(e, "tiled_notma")) return kTiledNoTma;
     if (!std::strcmp(e, "generic")) return kGeneric;
     if (!std::strcmp(e, "spmv")) return kSpmv;
+    if (!std::strcmp(e, "banded1")) return kBanded1;
+    if (!std::strcmp(e, "spmv_plain")) return kSpmvPlain;
     return kAuto;
 }
 
@@ -226,7 +231,7 @@ int device_sm_count() {
     return sms;
 }
 
-int run_spmm(const spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
+int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
              int64_t batch, cudaStream_t st) {
     if (batch == 0) return SPCONV_OK;
     if (batch > INT32_MAX) return fail(SPCONV_EINVAL, "spconv_spmm: batch exceeds int32");
@@ -238,20 +243,90 @@ int run_spmm(const spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t
 
     // ---- latency path for one or two vectors ----
     const bool spmv_ok = h->k2max <= 49;
-    if (force == kSpmv && !spmv_ok)
+    if ((force == kSpmv || force == kSpmvPlain) && !spmv_ok)
         return fail(SPCONV_EINVAL, "SPCONV_B200_PATH=spmv: rows longer than 49 entries");
-    if (spmv_ok && (force == kSpmv || (force == kAuto && batch <= 2))) {
+    if (spmv_ok && (force == kSpmv || force == kSpmvPlain || (force == kAuto && batch <= 2))) {
+        if (h->is_conv && h->taps_dense && force != kSpmvPlain) {
+            spb::SpecParams sp{};
+            sp.row_ptr = h->row_ptr;
+            sp.col_idx = h->col_idx;
+            sp.vals = h->vals;
+            sp.X = X;
+            sp.ldx = ldx;
+            sp.Y = Y;
+            sp.ldy = ldy;
+            sp.rows = (int)h->rows;
+            sp.batch = (int)batch;
+            sp.m = (int)g.m;
+            sp.n = (int)g.n;
+            sp.k = (int)g.k;
+            sp.s = (int)g.s;
+            sp.p = (int)g.p;
+            sp.mo = (int)g.mo;
+            sp.no = (int)g.no;
+            int64_t sy = 0, lo, hi;
+            for (int64_t yy = 0; yy < g.no; ++yy) tap_range(yy, g.n, g.k, g.s, g.p, lo, hi), sy += hi - lo;
+            sp.sy = (int)sy;
+            const char* sk = std::getenv("SPCONV_B200_SPEC_SKEW");
+            sp.skew = sk ? std::atoi(sk) : 0;
+            // Strided gathers need the batch loop per thread: one launch covers <= 2 images.
+            for (int64_t b0 = 0; b0 < batch; b0 += 2) {
+                sp.X = X + b0 * ldx;
+                sp.Y = Y + b0 * ldy;
+                sp.batch = (int)std::min<int64_t>(2, batch - b0);
+                CK(spb::launch_spmv_spec(sp, h->k2max, st));
+            }
+            h->last_kernel.store("conv_spmv_spec");
+            return SPCONV_OK;
+        }
         spb::GenericParams gp{h->row_ptr, h->col_idx, h->vals, X, ldx, Y, ldy, (int)h->rows,
                               (int)batch};
         CK(spb::launch_spmv_unrolled(gp, h->k2max, st));
+        h->last_kernel.store("csr_spmv_unrolled");
         return SPCONV_OK;
     }
 
-    // ---- banded (register-blocked) path ----
-    const bool banded_geom = h->is_conv && spb::banded_supported((int)g.k, (int)g.s) && tma_ok;
-    if (force == kBanded && !banded_geom)
+    // ---- band path: CSR band check + register-blocked apply ----
+    const bool band_geom = h->is_conv && h->band_tw > 0 && tma_ok;
+    if (force == kBanded && !band_geom)
         return fail(SPCONV_EINVAL, "SPCONV_B200_PATH=banded: geometry unsupported");
-    if (banded_geom && (force == kBanded || (force == kAuto && h->taps_dense))) {
+    if (band_geom && (force == kBanded || (force == kAuto && h->taps_dense))) {
+        const int sms = device_sm_count();
+        spb::BandShape sh{};
+        spb::BandParams bp{};
+        bp.p = (int)g.p;
+        CK(spb::launch_band((int)g.k, (int)g.s, bp, nullptr, st, &sh, sms));
+        bp.row_ptr = h->row_ptr;
+        bp.col_idx = h->col_idx;
+        bp.vals = h->vals;
+        bp.taps = h->taps;
+        bp.seg_ok = h->seg_ok;
+        bp.X = X;
+        bp.ldx = ldx;
+        bp.Y = Y;
+        bp.ldy = ldy;
+        bp.batch = (int)batch;
+        bp.m = (int)g.m;
+        bp.n = (int)g.n;
+        bp.mo = (int)g.mo;
+        bp.no = (int)g.no;
+        bp.tiles_y = (int)((g.no + sh.tw - 1) / sh.tw);
+        bp.tiles = (int)(((g.mo + sh.th - 1) / sh.th) * bp.tiles_y);
+        bp.fast_allowed = h->taps_dense ? 1 : 0;
+        const int cpt = sh.tw / 32;
+        bp.y_vec = (ldy % cpt == 0) && (g.no % cpt == 0) &&
+                   (reinterpret_cast<uintptr_t>(Y) % (4 * cpt) == 0);
+        CUtensorMap tmap;
+        if (int rc = encode_x_map(&tmap, X, g, ldx, batch, sh.wc, sh.wr, 1)) return rc;
+        CK(spb::launch_band_check((int)g.k, (int)g.s, bp, st));
+        CK(spb::launch_band((int)g.k, (int)g.s, bp, &tmap, st, nullptr, sms));
+        h->last_kernel.store("conv_band_check+conv_spmm_band");
+        return SPCONV_OK;
+    }
+
+    // ---- legacy banded kernel (A/B experiments only: SPCONV_B200_PATH=banded1) ----
+    const bool banded_geom = h->is_conv && spb::banded_supported((int)g.k, (int)g.s) && tma_ok;
+    if (force == kBanded1 && banded_geom) {
         spb::BandedShape sh{};
         spb::BandedParams bp{};
         CK(spb::launch_banded((int)g.k, (int)g.s, bp, nullptr, st, &sh));
@@ -271,17 +346,15 @@ int run_spmm(const spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t
         bp.tiles_y = (int)((g.no + 31) / 32);
         const int64_t tiles = ((g.mo + sh.th - 1) / sh.th) * bp.tiles_y;
         const int64_t groups = (batch + sh.bt - 1) / sh.bt;
-        // Enough CTAs for ~8 waves at 2 CTAs/SM; each split keeps >= 2 groups.
         const int64_t want = 16ll * device_sm_count();
         int64_t splits = (want + tiles - 1) / tiles;
         splits = std::max<int64_t>(1, std::min<int64_t>(splits, groups / 2));
-        if (const char* e = std::getenv("SPCONV_B200_SPLITS"))  // tuning experiments
-            splits = std::max<int64_t>(1, std::min<int64_t>(std::atoll(e), groups));
         bp.splits = (int)splits;
-        bp.diag = std::getenv("SPCONV_B200_DIAG") ? std::atoi(std::getenv("SPCONV_B200_DIAG")) : 0;
+        bp.diag = 0;
         CUtensorMap tmap;
         if (int rc = encode_x_map(&tmap, X, g, ldx, batch, sh.wc, sh.wr, sh.bt)) return rc;
         CK(spb::launch_banded((int)g.k, (int)g.s, bp, &tmap, st, nullptr));
+        h->last_kernel.store("conv_spmm_banded");
         return SPCONV_OK;
     }
 
@@ -332,6 +405,7 @@ int run_spmm(const spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t
             if (use_tma)
                 if (int rc = encode_x_map(&tmap, X, g, ldx, batch, (int)wc, (int)wr, bt)) return rc;
             CK(spb::launch_tiled(tp, &tmap, bt, smem, st));
+            h->last_kernel.store("conv_spmm_tiled");
             return SPCONV_OK;
         }
         if (force == kTiled || force == kTiledNoTma)
@@ -341,6 +415,7 @@ int run_spmm(const spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t
     // ---- generic CSR path ----
     spb::GenericParams gp{h->row_ptr, h->col_idx, h->vals, X, ldx, Y, ldy, (int)h->rows, (int)batch};
     CK(spb::launch_generic(gp, st));
+    h->last_kernel.store("csr_spmm_generic");
     return SPCONV_OK;
 }
 
@@ -417,8 +492,14 @@ int spconv_build_csr(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
     // reads one-past-the-end stay in bounds).
     const size_t rp_bytes = ((size_t)(h->rows + 1) * 4 + 255) & ~size_t(255);
     const size_t ix_bytes = ((size_t)std::max<int64_t>(ht.nnz, 1) * 4 + 255) & ~size_t(255);
+    const size_t tap_bytes = ((size_t)(k * k) * 4 + 255) & ~size_t(255);
+    size_t seg_bytes = 0;
+    if (spb::band_supported((int)k, (int)s)) {
+        h->band_tw = spb::band_tile_width((int)k, (int)s);
+        seg_bytes = ((size_t)(g.mo * ((g.no + h->band_tw - 1) / h->band_tw)) + 255) & ~size_t(255);
+    }
     char* csr = nullptr;
-    cudaError_t e = cudaMallocAsync(&csr, rp_bytes + 2 * ix_bytes + 256, st);
+    cudaError_t e = cudaMallocAsync(&csr, rp_bytes + 2 * ix_bytes + 256 + tap_bytes + seg_bytes, st);
     if (e != cudaSuccess) {
         delete h;
         return cuda_fail(e, "cudaMallocAsync(CSR)");
@@ -426,6 +507,8 @@ int spconv_build_csr(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
     h->row_ptr = reinterpret_cast<int32_t*>(csr);
     h->col_idx = reinterpret_cast<int32_t*>(csr + rp_bytes);
     h->vals = reinterpret_cast<float*>(csr + rp_bytes + ix_bytes);
+    h->taps = reinterpret_cast<float*>(csr + rp_bytes + 2 * ix_bytes + 256);
+    if (seg_bytes) h->seg_ok = reinterpret_cast<uint8_t*>(csr + rp_bytes + 2 * ix_bytes + 256 + tap_bytes);
 
     spb::BuildParams bp{};
     bp.m = (int)m;
@@ -439,6 +522,7 @@ int spconv_build_csr(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
     bp.row_ptr = h->row_ptr;
     bp.col_idx = h->col_idx;
     bp.vals = h->vals;
+    bp.taps_out = h->taps;
     char* tab = nullptr;
     if (k <= spb::kSmallK) {  // tables ride in the kernel parameters: no copies, no allocation
         bp.small = 1;
@@ -633,7 +717,8 @@ int spconv_spmv(const spconv_csr* h, const float* x_dev, float* y_dev, void* str
     if (!h || !x_dev || !y_dev) return fail(SPCONV_EINVAL, "spconv_spmv: null argument");
     DeviceGuard dg(h->device);
     if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
-    return run_spmm(h, x_dev, h->cols, y_dev, h->rows, 1, static_cast<cudaStream_t>(stream));
+    return run_spmm(const_cast<spconv_csr*>(h), x_dev, h->cols, y_dev, h->rows, 1,
+                    static_cast<cudaStream_t>(stream));
 }
 
 int spconv_spmm(const spconv_csr* h, const float* X_dev, int64_t ldx, float* Y_dev, int64_t ldy,
@@ -645,7 +730,8 @@ int spconv_spmm(const spconv_csr* h, const float* X_dev, int64_t ldx, float* Y_d
         return fail(SPCONV_EINVAL, "spconv_spmm: leading dimension smaller than the matrix");
     DeviceGuard dg(h->device);
     if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
-    return run_spmm(h, X_dev, ldx, Y_dev, ldy, batch, static_cast<cudaStream_t>(stream));
+    return run_spmm(const_cast<spconv_csr*>(h), X_dev, ldx, Y_dev, ldy, batch,
+                    static_cast<cudaStream_t>(stream));
 }
 
 int spconv_convolve_host(const spconv_csr* hc, const float* X_host, float* Y_host, int64_t batch) {
@@ -711,6 +797,12 @@ int spconv_convolve_host_f64(const spconv_csr* h, const double* X_host, double* 
     if (int rc = spconv_convolve_host(h, xf.data(), yf.data(), batch)) return rc;
     for (size_t i = 0; i < yf.size(); ++i) Y_host[i] = yf[i];
     return SPCONV_OK;
+}
+
+const char* spconv_csr_last_kernel(const spconv_csr* h) {
+    if (!h) return "";
+    const char* k = h->last_kernel.load();
+    return k ? k : "";
 }
 
 int spconv_csr_free(spconv_csr* h) {

@@ -90,6 +90,8 @@ __global__ void __launch_bounds__(256) csr_build_kernel(const BuildParams P) {
     for (int q = t; q < k1 * k1; q += R) s_sat[q] = P.small ? P.tab.sat[q] : __ldg(P.t.sat + q);
     for (int q = t; q < kk; q += R) s_taps[q] = P.small ? P.tab.taps[q] : __ldg(P.t.taps + q);
     __syncthreads();
+    if (blockIdx.x == 0 && P.taps_out)
+        for (int q = t; q < kk; q += R) P.taps_out[q] = s_taps[q];
 
     const int r0 = blockIdx.x * R;
     const int r = r0 + t;

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <mutex>
 
 namespace spb {
@@ -40,6 +41,7 @@ struct BuildParams {
     int32_t* row_ptr;
     int32_t* col_idx;
     float* vals;
+    float* taps_out;  // k*k taps copied here by block 0 (the handle's device tap table)
 };
 
 // Conv-tiled SpMM: one CTA owns a TH x 32 block of output pixels (rows of T)
@@ -82,6 +84,44 @@ struct BandedShape {
     int th, wr, wc, bt, smem, threads;
 };
 
+// Two-kernel conv SpMM (spmm_band.cu): band check + register-blocked apply.
+struct BandParams {
+    const int32_t* row_ptr;
+    const int32_t* col_idx;
+    const float* vals;
+    const float* taps;   // k*k fp32 taps of the handle (device)
+    uint8_t* seg_ok;     // [mo][tiles_y] band-check result
+    const float* X;
+    int64_t ldx;
+    float* Y;
+    int64_t ldy;
+    int batch;
+    int m, n, p, mo, no;
+    int tiles_y;       // tiles across n_out
+    int tiles;         // tiles_x * tiles_y
+    int fast_allowed;  // every tap finite and non-zero
+    int y_vec;         // Y rows admit CPT-wide vector stores
+};
+
+struct BandShape {
+    int th, tw, wr, wc, smem, threads, occ;
+};
+
+// Speculative conv SpMV (spmm.cu, batch <= 2, dense taps).
+struct SpecParams {
+    const int32_t* row_ptr;
+    const int32_t* col_idx;
+    const float* vals;
+    const float* X;
+    int64_t ldx;
+    float* Y;
+    int64_t ldy;
+    int rows, batch;
+    int m, n, k, s, p, mo, no;
+    int sy;    // sum over output columns y of cy(y)
+    int skew;  // test hook: offsets the predicted row start (forces the mismatch path)
+};
+
 struct GenericParams {
     const int32_t* row_ptr;
     const int32_t* col_idx;
@@ -101,9 +141,16 @@ cudaError_t launch_tiled(const TiledParams& tp, const CUtensorMap* tmap, int bt,
                          cudaStream_t st);
 cudaError_t launch_generic(const GenericParams& gp, cudaStream_t st);
 cudaError_t launch_spmv_unrolled(const GenericParams& gp, int kmax, cudaStream_t st);
+cudaError_t launch_spmv_spec(const SpecParams& sp, int kmax, cudaStream_t st);
 bool banded_supported(int k, int s);
 cudaError_t launch_banded(int k, int s, const BandedParams& bp, const CUtensorMap* tmap,
                           cudaStream_t st, BandedShape* shape);
+
+bool band_supported(int k, int s);
+int band_tile_width(int k, int s);
+cudaError_t launch_band(int k, int s, const BandParams& bp, const CUtensorMap* tmap, cudaStream_t st,
+                        BandShape* shape, int sms);
+cudaError_t launch_band_check(int k, int s, const BandParams& bp, cudaStream_t st);
 
 size_t tiled_smem_bytes(int th, int wr, int wc, int k2max, int bt, int stages);
 
@@ -120,6 +167,10 @@ struct spconv_csr {
     int32_t* row_ptr = nullptr;    // device
     int32_t* col_idx = nullptr;    // device
     float* vals = nullptr;         // device
+    float* taps = nullptr;         // device k*k taps (conv transforms)
+    uint8_t* seg_ok = nullptr;     // device band-check bytes [mo][tiles_y] (band geometries)
+    int band_tw = 0;               // tile width seg_ok was sized for (0: none)
+    std::atomic<const char*> last_kernel{nullptr};  // diagnostics: last SpMM kernel launched
     // Workspace of spconv_convolve_host (lazily created, guarded by ws_mu).
     std::mutex ws_mu;
     cudaStream_t ws_stream[3] = {nullptr, nullptr, nullptr};

@@ -195,6 +195,80 @@ cudaError_t launch_spmv_unrolled(const GenericParams& gp, int kmax, cudaStream_t
     return cudaGetLastError();
 }
 
+// Speculative single-pass SpMV / small-batch SpMM of a conv transform built
+// with dense taps (BASELINE config 2: one 512^2 image, ~15 MB -- a latency
+// problem).  The CSR is still what is multiplied: every thread loads its row's
+// row_ptr pair and (col, val) pairs, but it issues those loads TOGETHER with
+// the x gathers at the columns the closed form predicts (row (x, y) starts at
+// CX(x)*SY + cx(x)*CY(y), taps in (j, i) order), so a row costs one memory
+// round trip instead of three.  The prediction never decides the result:
+// each stored column is compared with its prediction and a mismatch reloads
+// x[col] (a row whose row_ptr pair disagrees takes the plain loop), so the
+// output is exactly  acc = fmaf(val[e], x[col[e]], acc)  over the stored row.
+__device__ __forceinline__ int slides_before_dev(int x, int j, int dim, int s, int p) {
+    const int lo = (p - j <= 0) ? 0 : (p - j + s - 1) / s;
+    const int hi = (dim + p - j - 1 < 0) ? 0 : (dim + p - j - 1) / s + 1;
+    return max(0, min(x, hi) - lo);
+}
+
+template <int KMAX>
+__global__ void __launch_bounds__(256) conv_spmv_spec(const SpecParams P) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= P.rows) return;
+    const int x = r / P.no, y = r - x * P.no;
+    const int jlo = min(max(0, P.p - P.s * x), P.k), jhi = max(jlo, min(P.k, P.m + P.p - P.s * x));
+    const int ilo = min(max(0, P.p - P.s * y), P.k), ihi = max(ilo, min(P.k, P.n + P.p - P.s * y));
+    const int cy = ihi - ilo;
+    const int cnt = (jhi - jlo) * cy;
+    int cxb = 0, cyb = 0;  // sum_{x' < x} cx(x'), sum_{y' < y} cy(y')
+    for (int j = 0; j < P.k; ++j) {
+        cxb += slides_before_dev(x, j, P.m, P.s, P.p);
+        cyb += slides_before_dev(y, j, P.n, P.s, P.p);
+    }
+    const int e0 = cxb * P.sy + (jhi - jlo) * cyb + P.skew;
+    const int a = __ldg(P.row_ptr + r), b = __ldg(P.row_ptr + r + 1);
+    int c[KMAX];
+    float v[KMAX];
+    int pc[KMAX];
+    {
+        int j = jlo, i = ilo;
+#pragma unroll
+        for (int q = 0; q < KMAX; ++q) {
+            const bool on = q < cnt;
+            c[q] = on ? __ldg(P.col_idx + e0 + q) : 0;
+            v[q] = on ? __ldg(P.vals + e0 + q) : 0.0f;
+            pc[q] = (P.s * x + j - P.p) * P.n + (P.s * y + i - P.p);
+            if (++i == ihi) i = ilo, ++j;
+        }
+    }
+    const bool row_ok = a == e0 && b == e0 + cnt;
+    for (int bi = 0; bi < P.batch; ++bi) {
+        const float* X = P.X + (int64_t)bi * P.ldx;
+        float acc = 0.0f;
+        if (row_ok) {
+            float xv[KMAX];
+#pragma unroll
+            for (int q = 0; q < KMAX; ++q) xv[q] = q < cnt ? __ldg(X + pc[q]) : 0.0f;
+#pragma unroll
+            for (int q = 0; q < KMAX; ++q)
+                if (q < cnt) acc = fmaf(v[q], c[q] == pc[q] ? xv[q] : __ldg(X + c[q]), acc);
+        } else {
+            for (int e = a; e < b; ++e) acc = fmaf(__ldg(P.vals + e), __ldg(X + __ldg(P.col_idx + e)), acc);
+        }
+        P.Y[(int64_t)bi * P.ldy + r] = acc;
+    }
+}
+
+cudaError_t launch_spmv_spec(const SpecParams& sp, int kmax, cudaStream_t st) {
+    const int block = 256;
+    const int grid = (sp.rows + block - 1) / block;
+    if (kmax <= 9) conv_spmv_spec<9><<<grid, block, 0, st>>>(sp);
+    else if (kmax <= 25) conv_spmv_spec<25><<<grid, block, 0, st>>>(sp);
+    else if (kmax <= 49) conv_spmv_spec<49><<<grid, block, 0, st>>>(sp);
+    else return cudaErrorInvalidValue;
+    return cudaGetLastError();
+}
+
 template <int BT>
 static cudaError_t launch_bt(const TiledParams& tp, const CUtensorMap* tmap, size_t smem,
                              cudaStream_t st) {

@@ -1,0 +1,14 @@
+#!/bin/bash
+# r01b: new two-kernel band path + speculative SpMV -- parity, bench, A/B vs the old kernels, ncu.
+cd "${GRAFT_REPO_ROOT:-/root/repo}"
+mkdir -p gpurun_out
+rm -f gpurun_out/status.txt gpurun_out/exp.txt
+timeout 900 python -m pytest tests -m gpu -q -x --durations=10 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/status.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/status.txt
+timeout 600 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/status.txt
+timeout 900 python scripts/exp_run.py gpurun_out/exp.txt "--config 3|" "--config 3|SPCONV_B200_PATH=banded1" "--config 4|" "--config 4|SPCONV_B200_PATH=banded1" "--config 4 --batch 64|" "--config 4 --batch 64|SPCONV_B200_PATH=banded1" "--config 2|" "--config 2|SPCONV_B200_PATH=spmv_plain" > /dev/null 2>&1; echo "exp rc=$?" >> gpurun_out/status.txt
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c3.csv python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-secondary --e2e-steps 2 > gpurun_out/ncu_launch_c3.log 2>&1; echo "ncu-l3 rc=$?" >> gpurun_out/status.txt
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"conv_band_check|conv_spmm_band" -s 6 -c 2 -o gpurun_out/prof_spmm_c3_b256 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-secondary --e2e-steps 2 > gpurun_out/ncu_full_c3.log 2>&1; echo "ncu-full-c3 rc=$?" >> gpurun_out/status.txt
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"conv_band_check|conv_spmm_band" -s 6 -c 2 -o gpurun_out/prof_spmm_c4_b8 python bench.py --config 4 --steps 3 --warmup 3 --no-cpu-baseline --no-secondary --e2e-steps 2 > gpurun_out/ncu_full_c4.log 2>&1; echo "ncu-full-c4 rc=$?" >> gpurun_out/status.txt
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:conv_spmv_spec -s 3 -c 1 -o gpurun_out/prof_spmm_c2_b1 python bench.py --config 2 --steps 3 --warmup 3 --no-cpu-baseline --no-secondary --e2e-steps 2 > gpurun_out/ncu_full_c2.log 2>&1; echo "ncu-full-c2 rc=$?" >> gpurun_out/status.txt
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:csr_build -s 3 -c 1 -o gpurun_out/prof_build_c3 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-secondary --e2e-steps 2 > gpurun_out/ncu_full_build.log 2>&1; echo "ncu-full-build rc=$?" >> gpurun_out/status.txt

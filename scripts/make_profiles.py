@@ -17,6 +17,7 @@ import collections
 import csv
 import json
 import os
+import re
 import shutil
 import sys
 
@@ -67,7 +68,9 @@ def main():
         elif f.endswith(".ncu-rep"):
             res = raw(p)
             lines = []
-            for r in res:
+            name = f.replace(".ncu-rep", "")
+            mt = re.match(r"prof_(\w+?)_c(\d+)(?:_b(\d+))?$", name)
+            for ri, r in enumerate(res):
                 lines.append(f"== {r['kernel']}")
                 for k in KEYS:
                     if k in r:
@@ -75,8 +78,10 @@ def main():
                 lines.append(f"   top stalls (pc sampling share): {r['top_stalls']}")
                 rd = float(r["dram__bytes_read.sum"][0].replace(",", "")) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[r["dram__bytes_read.sum"][1]]
                 wr = float(r["dram__bytes_write.sum"][0].replace(",", "")) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[r["dram__bytes_write.sum"][1]]
-                name = f.replace(".ncu-rep", "")
-                summary[name] = {"kernel": r["kernel"], "dram_read_bytes": rd, "dram_write_bytes": wr,
+                summary[f"{name}#{ri}"] = {"kernel": r["kernel"], "dram_read_bytes": rd, "dram_write_bytes": wr,
+                                 "role": mt.group(1) if mt else None,
+                                 "config": int(mt.group(2)) if mt else None,
+                                 "batch": int(mt.group(3)) if mt and mt.group(3) else None,
                                  "dram_bytes_per_launch": rd + wr,
                                  "duration_us": float(r["gpu__time_duration.sum"][0].replace(",", "")) *
                                  UNIT_US.get(r["gpu__time_duration.sum"][1], 1.0),

@@ -179,7 +179,7 @@ def test_spmv_config2_all_paths(sp, orc, torch_cuda):
     t = build(sp, CONFIGS[1], kern)
     rp, ri, rv = orc.build_native(*CONFIGS[1], kern)
     want = orc.spmm_native(rp, ri, rv, X)
-    for path in (None, "spmv", "banded", "tiled", "tiled_notma", "generic"):
+    for path in (None, "spmv", "spmv_plain", "banded", "tiled", "tiled_notma", "generic"):
         Y = run_spmm(torch_cuda, sp, t, X, path)
         assert np.array_equal(bits(Y), bits(want)), path
     # fp64 reference tolerance
@@ -194,7 +194,7 @@ def test_spmm_batches_and_tails(sp, orc, torch_cuda, batch):
     kern, X = problem(orc, 7, 96, 72, 5, batch=batch)
     t = build(sp, spec, kern)
     want = orc.spmm_native(*orc.build_native(*spec, kern), X)
-    for path in (None, "spmv", "banded", "tiled", "tiled_notma", "generic"):
+    for path in (None, "spmv", "spmv_plain", "banded", "tiled", "tiled_notma", "generic"):
         assert np.array_equal(bits(run_spmm(torch_cuda, sp, t, X, path)), bits(want)), path
     # padded leading dimension (ldx = cols + 4 keeps TMA-legal 16B strides)
     assert np.array_equal(bits(run_spmm(torch_cuda, sp, t, X, None, ldx_pad=4)), bits(want))
@@ -272,7 +272,7 @@ def test_spmm_nonfinite_inputs(sp, orc, torch_cuda):
     X[2, 1023] = -np.inf
     t = build(sp, spec, kern)
     want = orc.spmm_native(*orc.build_native(*spec, kern), X)
-    for path in (None, "spmv", "banded", "tiled", "tiled_notma", "generic"):
+    for path in (None, "spmv", "spmv_plain", "banded", "tiled", "tiled_notma", "generic"):
         Y = run_spmm(torch_cuda, sp, t, X, path)
         assert np.array_equal(bits(Y), bits(want)), path
 
@@ -351,3 +351,66 @@ def test_errors(sp, torch_cuda):
         sp._check(sp.lib.spconv_spmm(t._h, x.data_ptr(), 10, x.data_ptr(), 64, 1, None))
     with pytest.raises(ValueError, match="build_conv_matrix: kernel side 2 does not match"):
         sp.build_transform(sp.Kernel(2, np.ones(4)), sp.ConvSpec(8, 8, 3, 1, 1))
+
+
+@pytest.mark.parametrize("spec", [(1024, 1024, 3, 1, 1), (512, 512, 5, 2, 2), (300, 260, 7, 2, 3),
+                                  (200, 132, 5, 1, 2), (130, 68, 3, 2, 0)])
+def test_band_path_is_default(sp, orc, torch_cuda, spec):
+    """Dense taps on a band geometry: the auto path is the two-kernel band path
+    (CSR band check + register-blocked apply), bit-exact vs the oracle, with
+    unaligned output rows (n_out % 4 != 0) and padded ldy included."""
+    m, n, k = spec[:3]
+    kern, X = problem(orc, 11, m, n, k, batch=5)
+    t = build(sp, spec, kern)
+    want = orc.spmm_native(*orc.build_native(*spec, kern), X)
+    Y = run_spmm(torch_cuda, sp, t, X)
+    assert t.last_kernel == "conv_band_check+conv_spmm_band"
+    assert np.array_equal(bits(Y), bits(want)), spec
+    # ldy padded by one float: Y rows lose 16-byte alignment -> scalar stores
+    Xd = torch_cuda.from_numpy(X).cuda()
+    Yd = torch_cuda.full((5, t.rows + 1), -7.0, device="cuda")
+    sp.spmm(t, Xd, Yd[:, : t.rows])
+    torch_cuda.cuda.synchronize()
+    Yh = Yd.cpu().numpy()
+    assert np.array_equal(bits(Yh[:, : t.rows]), bits(want))
+    assert np.all(Yh[:, t.rows] == -7.0)  # nothing written past the row
+
+
+def test_band_concurrent_streams(sp, orc, torch_cuda):
+    """One immutable handle applied on two streams at once (the band check's
+    per-segment bytes are rewritten with identical values: benign)."""
+    spec = (256, 256, 3, 1, 1)
+    kern, X = problem(orc, 12, 256, 256, 3, batch=16)
+    t = build(sp, spec, kern)
+    want = orc.spmm_native(*orc.build_native(*spec, kern), X)
+    Xd = torch_cuda.from_numpy(X).cuda()
+    s1, s2 = torch_cuda.cuda.Stream(), torch_cuda.cuda.Stream()
+    torch_cuda.cuda.synchronize()
+    outs = []
+    for _ in range(20):
+        Y1 = torch_cuda.empty(16, t.rows, device="cuda")
+        Y2 = torch_cuda.empty(16, t.rows, device="cuda")
+        sp.spmm(t, Xd, Y1, stream=s1)
+        sp.spmm(t, Xd, Y2, stream=s2)
+        outs += [Y1, Y2]
+    torch_cuda.cuda.synchronize()
+    for Y in outs:
+        assert np.array_equal(bits(Y.cpu().numpy()), bits(want))
+
+
+@pytest.mark.parametrize("skew", [1, -1, 3])
+def test_spmv_spec_mispredicted_rows(sp, orc, torch_cuda, skew):
+    """The speculative SpMV's prediction never decides the result: with the
+    predicted row starts deliberately skewed (test hook), every row takes the
+    mismatch path and the output is still bit-exact."""
+    spec = (64, 48, 5, 2, 2)
+    kern, X = problem(orc, 13, 64, 48, 5, batch=2)
+    t = build(sp, spec, kern)
+    want = orc.spmm_native(*orc.build_native(*spec, kern), X)
+    os.environ["SPCONV_B200_SPEC_SKEW"] = str(skew)
+    try:
+        Y = run_spmm(torch_cuda, sp, t, X)
+    finally:
+        del os.environ["SPCONV_B200_SPEC_SKEW"]
+    assert t.last_kernel == "conv_spmv_spec"
+    assert np.array_equal(bits(Y), bits(want))
