@@ -439,6 +439,94 @@ def run_ours(args, cfg):
         dist.destroy_process_group()
 
 
+# ----------------------------------------------------------------------------
+# DenseNet121 layer table (paper Table 1 protocol)
+# ----------------------------------------------------------------------------
+
+PAPER_TABLE1_US = {"CSR-C (SciPy, i7-8700)": 1507.0, "CSR-T (PyTorch sparse CSR, GTX 1070)": 9187.0,
+                   "CSR-G (CuPy, GTX 1070)": 11737.0, "Conv2D-G (PyTorch, GTX 1070)": 11143.0}
+
+
+def reference_layer_table(trials, warmup):
+    """The reference's own run_layer_bench (inc/bench.hpp:202-261) per layer on
+    this host, single-threaded as the reference CLI defaults (--threads 1)."""
+    import oracle
+    from paper_2411_19419_b200.layers import densenet121_layers
+    ref = oracle.try_ref()
+    if ref is None:
+        return None
+    rows = []
+    for i, L in enumerate(densenet121_layers()):
+        rows.append(ref.run_layer_bench(L.name, L.m, L.n, L.k, L.s, L.p, trials, warmup,
+                                        ref.derive_seed(42, i), 1))
+    return {"layers": rows, "total_csr_us": sum(r["CSR-SpMV"][0] for r in rows),
+            "total_csc_us": sum(r["CSC-SpMV"][0] for r in rows),
+            "total_im2col_us": sum(r["im2col"][0] for r in rows),
+            "total_csr_build_us": sum(r["CSR-SpMV"][2] for r in rows), "threads": 1,
+            "kind": "reference"}
+
+
+def run_densenet(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    metric = "DenseNet121 single-channel layer table: total apply time over all 123 layers (paper Table 1)"
+    if args.impl == "reference":
+        t0 = time.perf_counter()
+        ref = reference_layer_table(args.steps, args.warmup)
+        line = {"impl": "reference", "metric": metric, "unit": "us", "higher_is_better": False,
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "config": {"workload": "densenet121 layer table (123 layers)"}, "data": "synthetic",
+                "dtype": "f64"}
+        if ref is None:
+            line["unavailable"] = "oracle/_ref not built"
+        else:
+            line.update(value=ref["total_csr_us"], ms_per_step=ref["total_csr_us"] / 1e3,
+                        cpu_baseline={"value": ref["total_csr_us"], "unit": "us", "cores": 1,
+                                      "kind": "reference",
+                                      "sample": f"{args.steps} trials per layer, threads=1"},
+                        e2e={"value": ref["total_csr_us"], "unit": "us", "h2d_bytes_per_step": 0,
+                             "d2h_bytes_per_step": 0},
+                        reference_methods={k: ref[k] for k in ("total_csr_us", "total_csc_us",
+                                                               "total_im2col_us", "total_csr_build_us")},
+                        wall_s=time.perf_counter() - t0)
+        print(json.dumps(line), flush=True)
+        return
+    from paper_2411_19419_b200.layer_bench import markdown, run_table_bench
+    res = run_table_bench(trials=args.steps, warmup=args.warmup)
+    ref = None
+    if not args.no_cpu_baseline:
+        ref = reference_layer_table(min(args.steps, 100), min(args.warmup, 10))
+    h2d = sum(r["m"] * r["n"] * 4 for r in res["layers"])
+    d2h = sum(((r["m"] + 2 * r["p"] - r["k"]) // r["s"] + 1) * ((r["n"] + 2 * r["p"] - r["k"]) // r["s"] + 1) * 4
+              for r in res["layers"])
+    line = {
+        "metric": metric, "value": res["total_device_us"], "unit": "us", "higher_is_better": False,
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": res["total_device_us"] / 1e3, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "densenet121 layer table (123 single-channel layers, paper Table 2)",
+                   "timing": f"per layer: CUDA graph of {res['graph_reps']} SpMV launches, "
+                             f"{args.steps} replays; totals = sum of per-layer means"},
+        "total_device_sem_us": res["total_device_sem_us"],
+        "network_graph_us": res["network_graph_us"],
+        "total_build_us": res["total_build_us"],
+        "e2e": {"value": res["total_host_us"], "unit": "us", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h,
+                "path": "spconv_convolve_host per layer (pinned fp32 image, H2D + SpMV + D2H)"},
+        "gpu_launches": len(res["layers"]),
+        "paper_table1_us": PAPER_TABLE1_US,
+        "cpu_baseline": None if ref is None else {
+            "value": ref["total_csr_us"], "unit": "us", "cores": 1, "kind": "reference",
+            "sample": "reference run_layer_bench, CSR-SpMV, threads=1",
+            "csc_us": ref["total_csc_us"], "im2col_us": ref["total_im2col_us"]},
+    }
+    if args.report:
+        with open(args.report, "w") as f:
+            f.write(markdown(res, ref))
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -451,11 +539,16 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true", help="skip the config 2/4 extras")
+    ap.add_argument("--workload", choices=["config", "densenet121"], default="config",
+                    help="densenet121: the paper's Table 1 layer-table protocol")
+    ap.add_argument("--report", default="", help="densenet121: write the per-layer markdown here")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
     cfg = CONFIGS[args.config]
-    if args.impl == "reference":
+    if args.workload == "densenet121":
+        run_densenet(args)
+    elif args.impl == "reference":
         run_reference(args, cfg)
     else:
         run_ours(args, cfg)

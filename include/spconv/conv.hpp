@@ -6,6 +6,9 @@
 #pragma once
 
 #include <cstdint>
+#include <istream>
+#include <iterator>
+#include <ostream>
 #include <sstream>
 #include <stdexcept>
 #include <string>
@@ -138,6 +141,28 @@ inline std::vector<Grid> convolve_batch(const Transform& t, const std::vector<Gr
         out.emplace_back(t.spec.m_out(), t.spec.n_out(),
                          std::vector<double>(y.begin() + b * outl, y.begin() + (b + 1) * outl));
     return out;
+}
+
+/// write_transform (inc/conv.hpp:221-224): the text is rendered on the GPU,
+/// byte-identical to the reference's for the same matrix.
+inline void write_transform(std::ostream& os, const Transform& t) {
+    int64_t len = 0;
+    detail::check(spconv_csr_write_text(t.matrix.handle(), 1, nullptr, 0, &len));
+    std::string buf(static_cast<std::size_t>(len), '\0');
+    detail::check(spconv_csr_write_text(t.matrix.handle(), 1, buf.data(), len, &len));
+    os.write(buf.data(), static_cast<std::streamsize>(len));
+}
+
+/// read_transform (inc/conv.hpp:226-244); values are narrowed to fp32.
+inline Transform read_transform(std::istream& is) {
+    std::string text((std::istreambuf_iterator<char>(is)), std::istreambuf_iterator<char>());
+    spconv_csr* h = nullptr;
+    detail::check(spconv_transform_read(text.data(), static_cast<int64_t>(text.size()),
+                                        detail::default_device(), nullptr, &h));
+    SparseMatrix mat(h);
+    int64_t s5[5];
+    detail::check(spconv_csr_spec(h, s5));
+    return Transform{ConvSpec(s5[0], s5[1], s5[2], s5[3], s5[4]), std::move(mat)};
 }
 
 }  // namespace spconv

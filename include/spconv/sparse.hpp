@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <memory>
 #include <mutex>
+#include <ostream>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -124,6 +125,15 @@ inline DenseVector spmv(const SparseMatrix& m, std::span<const double> x, int th
 
 inline DenseVector spmv(const SparseMatrix& m, const DenseVector& x, int threads = 0) {
     return spmv(m, std::span<const double>(x), threads);
+}
+
+/// write_sparse (inc/sparse.hpp:400-406), rendered on the GPU.
+inline void write_sparse(std::ostream& os, const SparseMatrix& m) {
+    int64_t len = 0;
+    detail::check(spconv_csr_write_text(m.handle(), 0, nullptr, 0, &len));
+    std::string buf(static_cast<std::size_t>(len), '\0');
+    detail::check(spconv_csr_write_text(m.handle(), 0, buf.data(), len, &len));
+    os.write(buf.data(), static_cast<std::streamsize>(len));
 }
 
 }  // namespace spconv

@@ -32,6 +32,7 @@ extern "C" {
 #define SPCONV_OK 0
 #define SPCONV_EINVAL 1
 #define SPCONV_ECUDA 2
+#define SPCONV_ERUNTIME 3 /* the reference would throw std::runtime_error (I/O, format) */
 
 /* Opaque device-resident CSR (replaces spconv::Transform / SparseMatrix,
  * inc/conv.hpp:165-168, inc/sparse.hpp:77-140). */
@@ -110,6 +111,26 @@ int spconv_convolve_host(const spconv_csr* h, const float* X_host, float* Y_host
  * out.  Used by the drop-in convolve()/spmv() wrappers. */
 int spconv_convolve_host_f64(const spconv_csr* h, const double* X_host, double* Y_host,
                              int64_t batch);
+
+/* Text form of the matrix, rendered on the device: with
+ * transform_header_line != 0, write_transform (inc/conv.hpp:217-224):
+ * "%%transform m n k s p csr" then write_sparse (inc/sparse.hpp:400-406):
+ * "%%sparse coordinate real", "rows cols nnz", one "row col value" line per
+ * entry (1-based, storage order, value = "%.17g" of the fp32 value widened
+ * to double).  Byte-identical to the reference's output for the same matrix.
+ * buf == NULL: only *len (the text size in bytes) is computed; otherwise the
+ * text is copied to buf (cap >= *len bytes, no terminator). */
+int spconv_csr_write_text(const spconv_csr* h, int transform_header_line, char* buf, int64_t cap,
+                          int64_t* len);
+
+/* read_transform (inc/conv.hpp:226-244) + read_sparse (inc/sparse.hpp:412-432)
+ * of `len` bytes of text: same header checks, range / duplicate checks and
+ * messages (status 3 where the reference throws std::runtime_error, 1 for
+ * std::invalid_argument).  Values are narrowed to fp32.  A matrix that equals
+ * the conv transform of its own taps comes back as a built conv handle
+ * (band kernels apply); anything else as a generic CSR with the geometry
+ * attached.  csc files are read into the same operator in CSR layout. */
+int spconv_transform_read(const char* text, int64_t len, int device, void* stream, spconv_csr** out);
 
 /* Name of the kernel(s) the last spconv_spmv / spconv_spmm /
  * spconv_convolve_host call on this handle launched (diagnostics; "" before

@@ -207,6 +207,10 @@ class Ref:
         L.ref_direct_conv.argtypes = [i64] * 5 + [C.c_void_p] * 3
         L.ref_run_verification.argtypes = [i64, C.c_int, C.c_void_p, C.c_void_p]
         L.ref_hardware_concurrency.restype = C.c_uint
+        if hasattr(L, "ref_write_transform"):
+            L.ref_write_transform.argtypes = [C.c_void_p, C.c_void_p, i64, C.POINTER(i64)]
+            L.ref_write_sparse_csr.argtypes = [i64, i64] + [C.c_void_p] * 4 + [i64, C.POINTER(i64)]
+            L.ref_read_transform.argtypes = [C.c_char_p, i64, C.POINTER(C.c_void_p)]
         if hasattr(L, "ref_run_layer_bench"):
             L.ref_run_layer_bench.argtypes = [C.c_char_p] + [i64] * 7 + [u64, C.c_int, C.c_void_p]
         self.L = L
@@ -270,6 +274,23 @@ class Ref:
     def hardware_concurrency(self) -> int:
         return int(self.L.ref_hardware_concurrency())
 
+    def write_sparse_csr(self, rows, cols, ptr, idx, val) -> bytes:
+        """write_sparse (inc/sparse.hpp:400-406) of the CSR (ptr, idx, val)."""
+        ptr = np.ascontiguousarray(ptr, np.int64)
+        idx = np.ascontiguousarray(idx, np.int64)
+        val = np.ascontiguousarray(val, np.float64)
+        n = i64()
+        self._chk(self.L.ref_write_sparse_csr(rows, cols, _p(ptr), _p(idx), _p(val), None, 0, C.byref(n)))
+        buf = C.create_string_buffer(max(n.value, 1))
+        self._chk(self.L.ref_write_sparse_csr(rows, cols, _p(ptr), _p(idx), _p(val), buf, n.value, C.byref(n)))
+        return buf.raw[: n.value]
+
+    def read_transform(self, text: bytes) -> "RefTransform":
+        h = C.c_void_p()
+        self._chk(self.L.ref_read_transform(text, len(text), C.byref(h)))
+        t = RefTransform(self, h, None)
+        return t
+
     def run_layer_bench(self, name, m, n, k, s, p, trials, warmup, seed, threads=1):
         """inc/bench.hpp:202-261 on one layer -> {method: (mean_us, sem_us, build_us)}."""
         out = np.zeros(9, np.float64)
@@ -295,6 +316,14 @@ class RefTransform:
         val = np.empty(max(nnz, 1), np.float64)
         self.ref.L.ref_transform_export(self.h, _p(ptr), _p(idx), _p(val))
         return ptr, idx[:nnz], val[:nnz]
+
+    def write_text(self) -> bytes:
+        """write_transform (inc/conv.hpp:221-224)."""
+        n = i64()
+        self.ref._chk(self.ref.L.ref_write_transform(self.h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(max(n.value, 1))
+        self.ref._chk(self.ref.L.ref_write_transform(self.h, buf, n.value, C.byref(n)))
+        return buf.raw[: n.value]
 
     def convolve(self, X: np.ndarray, threads: int = 1) -> np.ndarray:
         """X: [batch, m*n] float64 -> [batch, m_out*n_out] float64 (reference convolve)."""

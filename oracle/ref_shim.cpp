@@ -13,6 +13,7 @@
 
 #include <cstdint>
 #include <cstring>
+#include <sstream>
 #include <exception>
 #include <span>
 #include <stdexcept>
@@ -171,6 +172,41 @@ int ref_run_layer_bench(const char* name, int64_t m, int64_t n, int64_t k, int64
             out9[3 * i + 1] = rs[i].sem_us;
             out9[3 * i + 2] = rs[i].build_time_us;
         }
+    });
+}
+
+// write_transform (inc/conv.hpp:221-224) into buf (cap bytes); *len = text size.
+int ref_write_transform(const void* h, char* buf, int64_t cap, int64_t* len) {
+    return guarded([&] {
+        std::ostringstream os;
+        spconv::write_transform(os, *static_cast<const spconv::Transform*>(h));
+        const std::string t = os.str();
+        *len = static_cast<int64_t>(t.size());
+        if (buf && cap >= *len) std::memcpy(buf, t.data(), t.size());
+    });
+}
+
+// write_sparse (inc/sparse.hpp:400-406) of a CSR given as arrays.
+int ref_write_sparse_csr(int64_t rows, int64_t cols, const int64_t* ptr, const int64_t* idx,
+                         const double* val, char* buf, int64_t cap, int64_t* len) {
+    return guarded([&] {
+        spconv::Triplets t(rows, cols);
+        for (int64_t r = 0; r < rows; ++r)
+            for (int64_t e = ptr[r]; e < ptr[r + 1]; ++e) t.add(r, idx[e], val[e]);
+        const spconv::SparseMatrix m = spconv::SparseMatrix::compile(t, spconv::Layout::CSR);
+        std::ostringstream os;
+        spconv::write_sparse(os, m);
+        const std::string s = os.str();
+        *len = static_cast<int64_t>(s.size());
+        if (buf && cap >= *len) std::memcpy(buf, s.data(), s.size());
+    });
+}
+
+// read_transform (inc/conv.hpp:226-244) of a text buffer.
+int ref_read_transform(const char* text, int64_t len, void** out) {
+    return guarded([&] {
+        std::istringstream is(std::string(text, static_cast<size_t>(len)));
+        *out = new spconv::Transform(spconv::read_transform(is));
     });
 }
 

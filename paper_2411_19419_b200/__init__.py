@@ -22,7 +22,7 @@ import numpy as np
 
 __all__ = [
     "ConvSpec", "Kernel", "Transform", "build_transform", "convolve", "convolve_batch",
-    "spmv", "spmm", "nnz_bound", "library_path", "lib",
+    "spmv", "spmm", "nnz_bound", "read_transform", "library_path", "lib",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -63,6 +63,8 @@ _decl("spconv_spmm", [_vp, _vp, _i64, _vp, _i64, _i64, _vp])
 _decl("spconv_convolve_host", [_vp, _vp, _vp, _i64])
 _decl("spconv_convolve_host_f64", [_vp, _vp, _vp, _i64])
 _decl("spconv_csr_last_kernel", [_vp], C.c_char_p)
+_decl("spconv_csr_write_text", [_vp, C.c_int, _vp, _i64, _P(_i64)])
+_decl("spconv_transform_read", [_vp, _i64, C.c_int, _vp, _P(_vp)])
 _decl("spconv_csr_free", [_vp])
 
 
@@ -70,9 +72,9 @@ def _check(rc: int) -> None:
     if rc == 0:
         return
     msg = lib.spconv_last_error().decode()
-    if rc == 1:
+    if rc == 1:  # std::invalid_argument in the reference
         raise ValueError(msg)
-    raise RuntimeError(msg)
+    raise RuntimeError(msg)  # 2: CUDA / memory, 3: std::runtime_error (I/O, format)
 
 
 def _ptr(a) -> int:
@@ -196,6 +198,15 @@ class Transform:
         _check(lib.spconv_csr_copy(self._h, _ptr(row_ptr), _ptr(col_idx), _ptr(vals),
                                    _stream_handle(stream)))
 
+    def write_text(self, transform_header: bool = True) -> bytes:
+        """write_transform / write_sparse text (inc/conv.hpp:221-224,
+        inc/sparse.hpp:400-406), rendered on the device."""
+        n = _i64()
+        _check(lib.spconv_csr_write_text(self._h, int(transform_header), None, 0, C.byref(n)))
+        buf = C.create_string_buffer(max(n.value, 1))
+        _check(lib.spconv_csr_write_text(self._h, int(transform_header), buf, n.value, C.byref(n)))
+        return buf.raw[: n.value]
+
     @property
     def last_kernel(self) -> str:
         """Kernel(s) the last apply on this transform launched ("a+b" = two launches)."""
@@ -211,6 +222,17 @@ class Transform:
             self.close()
         except Exception:
             pass
+
+
+def read_transform(text: bytes, device: int = 0, stream=None) -> Transform:
+    """read_transform (inc/conv.hpp:226-244): parse, validate, upload (fp32)."""
+    if isinstance(text, str):
+        text = text.encode()
+    h = _vp()
+    _check(lib.spconv_transform_read(text, len(text), device, _stream_handle(stream), C.byref(h)))
+    spec5 = (C.c_int64 * 5)()
+    _check(lib.spconv_csr_spec(h, spec5))
+    return Transform(h.value, ConvSpec(*spec5), device)
 
 
 def build_transform(kern: Kernel, spec: ConvSpec, device: int = 0, stream=None) -> Transform:

@@ -8,6 +8,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <charconv>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -246,17 +247,15 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
     if ((force == kSpmv || force == kSpmvPlain) && !spmv_ok)
         return fail(SPCONV_EINVAL, "SPCONV_B200_PATH=spmv: rows longer than 49 entries");
     if (spmv_ok && (force == kSpmv || force == kSpmvPlain || (force == kAuto && batch <= 2))) {
-        if (h->is_conv && h->taps_dense && force != kSpmvPlain) {
+        if (force != kSpmvPlain) {
             spb::SpecParams sp{};
             sp.row_ptr = h->row_ptr;
             sp.col_idx = h->col_idx;
             sp.vals = h->vals;
-            sp.X = X;
             sp.ldx = ldx;
-            sp.Y = Y;
             sp.ldy = ldy;
             sp.rows = (int)h->rows;
-            sp.batch = (int)batch;
+            sp.nnz = (int)h->nnz;
             sp.m = (int)g.m;
             sp.n = (int)g.n;
             sp.k = (int)g.k;
@@ -264,19 +263,17 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
             sp.p = (int)g.p;
             sp.mo = (int)g.mo;
             sp.no = (int)g.no;
-            int64_t sy = 0, lo, hi;
-            for (int64_t yy = 0; yy < g.no; ++yy) tap_range(yy, g.n, g.k, g.s, g.p, lo, hi), sy += hi - lo;
-            sp.sy = (int)sy;
+            sp.sy = (int)h->sy;
             const char* sk = std::getenv("SPCONV_B200_SPEC_SKEW");
             sp.skew = sk ? std::atoi(sk) : 0;
-            // Strided gathers need the batch loop per thread: one launch covers <= 2 images.
-            for (int64_t b0 = 0; b0 < batch; b0 += 2) {
+            const bool spec = h->is_conv && h->taps_dense;
+            for (int64_t b0 = 0; b0 < batch; b0 += 2) {  // <= 2 images per launch
                 sp.X = X + b0 * ldx;
                 sp.Y = Y + b0 * ldy;
                 sp.batch = (int)std::min<int64_t>(2, batch - b0);
-                CK(spb::launch_spmv_spec(sp, h->k2max, st));
+                CK(spb::launch_spmv_warp(sp, h->k2max, spec, st));
             }
-            h->last_kernel.store("conv_spmv_spec");
+            h->last_kernel.store(spec ? "csr_spmv_warp<spec>" : "csr_spmv_warp");
             return SPCONV_OK;
         }
         spb::GenericParams gp{h->row_ptr, h->col_idx, h->vals, X, ldx, Y, ldy, (int)h->rows,
@@ -313,12 +310,14 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
         bp.tiles_y = (int)((g.no + sh.tw - 1) / sh.tw);
         bp.tiles = (int)(((g.mo + sh.th - 1) / sh.th) * bp.tiles_y);
         bp.fast_allowed = h->taps_dense ? 1 : 0;
+        bp.sy = (int)h->sy;
+        bp.nnz = (int)h->nnz;
         const int cpt = sh.tw / 32;
         bp.y_vec = (ldy % cpt == 0) && (g.no % cpt == 0) &&
                    (reinterpret_cast<uintptr_t>(Y) % (4 * cpt) == 0);
         CUtensorMap tmap;
         if (int rc = encode_x_map(&tmap, X, g, ldx, batch, sh.wc, sh.wr, 1)) return rc;
-        CK(spb::launch_band_check((int)g.k, (int)g.s, bp, st));
+        CK(spb::launch_band_check((int)g.k, (int)g.s, bp, st, sms));
         CK(spb::launch_band((int)g.k, (int)g.s, bp, &tmap, st, nullptr, sms));
         h->last_kernel.store("conv_band_check+conv_spmm_band");
         return SPCONV_OK;
@@ -433,6 +432,68 @@ void free_ws(spconv_csr* h) {
     h->ws_chunk = 0;
 }
 
+// ---- transform text I/O helpers (inc/conv.hpp:217-244, inc/sparse.hpp:396-432) ----
+
+// Whitespace-separated token reader over a byte range (istream >> semantics
+// for well-formed input).
+struct TokenReader {
+    const char* p;
+    const char* e;
+    bool ws(char c) const { return c == ' ' || c == '\n' || c == '\t' || c == '\r' || c == '\v' || c == '\f'; }
+    bool next(std::string_view& tok) {
+        while (p < e && ws(*p)) ++p;
+        if (p >= e) return false;
+        const char* b = p;
+        while (p < e && !ws(*p)) ++p;
+        tok = std::string_view(b, (size_t)(p - b));
+        return true;
+    }
+    bool i64(int64_t& v) {
+        std::string_view t;
+        if (!next(t)) return false;
+        size_t o = (!t.empty() && t[0] == '+') ? 1 : 0;
+        auto r = std::from_chars(t.data() + o, t.data() + t.size(), v);
+        return r.ec == std::errc() && r.ptr == t.data() + t.size();
+    }
+    bool f64(double& v) {  // decimal floating point only (num_get rejects inf / nan / hex)
+        std::string_view t;
+        if (!next(t)) return false;
+        size_t o = (!t.empty() && t[0] == '+') ? 1 : 0;
+        for (char c : t.substr(o))
+            if (!((c >= '0' && c <= '9') || c == '.' || c == 'e' || c == 'E' || c == '-' || c == '+'))
+                return false;
+        auto r = std::from_chars(t.data() + o, t.data() + t.size(), v, std::chars_format::general);
+        return r.ec == std::errc() && r.ptr == t.data() + t.size();
+    }
+    std::string_view line() {  // std::getline
+        const char* b = p;
+        while (p < e && *p != '\n') ++p;
+        std::string_view l(b, (size_t)(p - b));
+        if (p < e) ++p;
+        return l;
+    }
+    void skip_line() {  // is.ignore(max, '\n')
+        while (p < e && *p != '\n') ++p;
+        if (p < e) ++p;
+    }
+};
+
+std::string transform_header(const spconv_csr* h) {
+    char buf[256];
+    std::snprintf(buf, sizeof buf,
+                  "%%%%transform %lld %lld %lld %lld %lld csr\n%%%%sparse coordinate real\n%lld %lld %lld\n",
+                  (long long)h->g.m, (long long)h->g.n, (long long)h->g.k, (long long)h->g.s,
+                  (long long)h->g.p, (long long)h->rows, (long long)h->cols, (long long)h->nnz);
+    return buf;
+}
+
+std::string sparse_header(const spconv_csr* h) {
+    char buf[160];
+    std::snprintf(buf, sizeof buf, "%%%%sparse coordinate real\n%lld %lld %lld\n", (long long)h->rows,
+                  (long long)h->cols, (long long)h->nnz);
+    return buf;
+}
+
 }  // namespace
 
 extern "C" {
@@ -487,6 +548,10 @@ int spconv_build_csr(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
     h->k2max = (int)ht.k2max;
 
     h->taps_dense = ht.dense;
+    {
+        int64_t lo, hi;
+        for (int64_t yy = 0; yy < g.no; ++yy) tap_range(yy, g.n, g.k, g.s, g.p, lo, hi), h->sy += hi - lo;
+    }
 
     // One stream-ordered allocation for the CSR (+256 B slack so prologue
     // reads one-past-the-end stay in bounds).
@@ -656,7 +721,7 @@ int spconv_csr_shape(const spconv_csr* h, int64_t* rows, int64_t* cols, int64_t*
 
 int spconv_csr_spec(const spconv_csr* h, int64_t spec5[5]) {
     if (!h || !spec5) return fail(SPCONV_EINVAL, "null argument");
-    if (!h->is_conv) return fail(SPCONV_EINVAL, "spconv_csr_spec: handle is a generic CSR");
+    if (h->g.m <= 0) return fail(SPCONV_EINVAL, "spconv_csr_spec: handle has no convolution geometry");
     spec5[0] = h->g.m;
     spec5[1] = h->g.n;
     spec5[2] = h->g.k;
@@ -796,6 +861,148 @@ int spconv_convolve_host_f64(const spconv_csr* h, const double* X_host, double* 
     for (size_t i = 0; i < xf.size(); ++i) xf[i] = (float)X_host[i];
     if (int rc = spconv_convolve_host(h, xf.data(), yf.data(), batch)) return rc;
     for (size_t i = 0; i < yf.size(); ++i) Y_host[i] = yf[i];
+    return SPCONV_OK;
+}
+
+int spconv_csr_write_text(const spconv_csr* h, int transform_header_line, char* buf, int64_t cap,
+                          int64_t* len) {
+    if (!h || !len) return fail(SPCONV_EINVAL, "spconv_csr_write_text: null argument");
+    if (transform_header_line && !h->is_conv)
+        return fail(SPCONV_EINVAL, "write_transform: matrix has no convolution geometry");
+    DeviceGuard dg(h->device);
+    if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
+    const std::string head = transform_header_line ? transform_header(h) : sparse_header(h);
+    const int64_t blocks = (h->rows + spb::text_rows_per_block() - 1) / spb::text_rows_per_block();
+    cudaStream_t st = nullptr;
+    unsigned long long* scratch = nullptr;
+    CK(cudaMallocAsync(&scratch, (size_t)(blocks + 2) * 8, st));
+    unsigned long long total = 0;
+    cudaError_t e = spb::render_entries(h->row_ptr, h->col_idx, h->vals, (int)h->rows, scratch, nullptr,
+                                        head.size(), st, true);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(&total, scratch + blocks, 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+        cudaFreeAsync(scratch, st);
+        return cuda_fail(e, "spconv_csr_write_text (size)");
+    }
+    *len = (int64_t)total;
+    if (!buf) {
+        cudaFreeAsync(scratch, st);
+        return SPCONV_OK;
+    }
+    if (cap < (int64_t)total) {
+        cudaFreeAsync(scratch, st);
+        return fail(SPCONV_EINVAL, "spconv_csr_write_text: buffer of " + std::to_string(cap) +
+                                       " bytes is smaller than the " + std::to_string(total) + "-byte text");
+    }
+    char* text = nullptr;
+    e = cudaMallocAsync(&text, (size_t)total + 16, st);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(text, head.data(), head.size(), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess)
+        e = spb::render_entries(h->row_ptr, h->col_idx, h->vals, (int)h->rows, scratch, text, head.size(), st,
+                                false);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(buf, text, (size_t)total, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFreeAsync(text, st);
+    cudaFreeAsync(scratch, st);
+    if (e != cudaSuccess) return cuda_fail(e, "spconv_csr_write_text");
+    return SPCONV_OK;
+}
+
+int spconv_transform_read(const char* text, int64_t len, int device, void* stream, spconv_csr** out) {
+    if (!text || !out || len < 0) return fail(SPCONV_EINVAL, "spconv_transform_read: null argument");
+    *out = nullptr;
+    TokenReader R{text, text + len};
+    // header: "%%transform m n k s p layout" (inc/conv.hpp:226-233)
+    std::string_view tag, lay;
+    int64_t m, n, k, s, p;
+    if (!R.next(tag) || !R.i64(m) || !R.i64(n) || !R.i64(k) || !R.i64(s) || !R.i64(p) || !R.next(lay) ||
+        tag != "%%transform")
+        return fail(SPCONV_ERUNTIME, "read_transform: bad header line");
+    R.skip_line();
+    if (int rc = check_spec(m, n, k, s, p)) return rc;
+    const std::string layout(lay);
+    if (layout != "csr" && layout != "CSR" && layout != "csc" && layout != "CSC")
+        return fail(SPCONV_EINVAL, "unknown layout '" + layout + "' (expected csr or csc)");
+    // read_sparse (inc/sparse.hpp:412-432)
+    std::string header(R.line());
+    if (!header.empty() && header.back() == '\r') header.pop_back();
+    if (header != "%%sparse coordinate real")
+        return fail(SPCONV_ERUNTIME, "read_sparse: bad header line '" + header + "'");
+    int64_t rows, cols, nnz;
+    if (!R.i64(rows) || !R.i64(cols) || !R.i64(nnz) || rows < 1 || cols < 1 || nnz < 0)
+        return fail(SPCONV_ERUNTIME, "read_sparse: bad 'rows cols nnz' line");
+    struct Trip {
+        int64_t r, c;
+        double v;
+    };
+    std::vector<Trip> t;
+    t.reserve((size_t)nnz);
+    for (int64_t i = 0; i < nnz; ++i) {
+        int64_t r, c;
+        double v;
+        if (!R.i64(r) || !R.i64(c) || !R.f64(v))
+            return fail(SPCONV_ERUNTIME, "read_sparse: expected " + std::to_string(nnz) + " entries, got " +
+                                             std::to_string(i));
+        if (r - 1 < 0 || r - 1 >= rows || c - 1 < 0 || c - 1 >= cols)
+            return fail(SPCONV_EINVAL, "Triplets: entry (" + std::to_string(r - 1) + ", " + std::to_string(c - 1) +
+                                           ") outside " + std::to_string(rows) + "x" + std::to_string(cols));
+        t.push_back({r - 1, c - 1, v});
+    }
+    std::sort(t.begin(), t.end(), [](const Trip& a, const Trip& b) { return a.r != b.r ? a.r < b.r : a.c < b.c; });
+    for (size_t i = 1; i < t.size(); ++i)
+        if (t[i].r == t[i - 1].r && t[i].c == t[i - 1].c)
+            return fail(SPCONV_EINVAL, "SparseMatrix: duplicate entry at (" + std::to_string(t[i].r) + ", " +
+                                           std::to_string(t[i].c) + ")");
+    const Geom g = make_geom(m, n, k, s, p);
+    if (rows != g.mo * g.no || cols != m * n)
+        return fail(SPCONV_ERUNTIME, "read_transform: matrix is " + std::to_string(rows) + "x" + std::to_string(cols) +
+                                         " but spec " + spec_str(m, n, k, s, p) + " requires " +
+                                         std::to_string(g.mo * g.no) + "x" + std::to_string(m * n));
+    std::vector<int64_t> ptr((size_t)rows + 1, 0), idx(t.size());
+    std::vector<double> val(t.size());
+    for (size_t i = 0; i < t.size(); ++i) {
+        ptr[(size_t)t[i].r + 1]++;
+        idx[i] = t[i].c;
+        val[i] = t[i].v;
+    }
+    for (int64_t r = 0; r < rows; ++r) ptr[(size_t)r + 1] += ptr[(size_t)r];
+    // If the matrix IS the conv transform of its own taps (the taps of the
+    // first row that stores all k*k of them), rebuild it on the device and
+    // keep the built handle: identical arrays, plus the geometry the band
+    // kernels need.  Otherwise keep the upload as a generic CSR.
+    std::vector<float> taps;
+    for (int64_t r = 0; r < rows && taps.empty(); ++r)
+        if (ptr[(size_t)r + 1] - ptr[(size_t)r] == k * k)
+            for (int64_t q = 0; q < k * k; ++q) taps.push_back((float)val[(size_t)(ptr[(size_t)r] + q)]);
+    if (!taps.empty()) {
+        spconv_csr* built = nullptr;
+        if (spconv_build_csr(m, n, k, s, p, taps.data(), device, stream, &built) == SPCONV_OK) {
+            bool same = built->nnz == nnz;
+            if (same) {
+                std::vector<int32_t> brp((size_t)rows + 1), bci((size_t)std::max<int64_t>(nnz, 1));
+                std::vector<float> bv((size_t)std::max<int64_t>(nnz, 1));
+                same = spconv_csr_copy(built, brp.data(), bci.data(), bv.data(), stream) == SPCONV_OK;
+                for (int64_t r = 0; same && r <= rows; ++r) same = brp[(size_t)r] == ptr[(size_t)r];
+                for (int64_t e = 0; same && e < nnz; ++e)
+                    same = bci[(size_t)e] == idx[(size_t)e] &&
+                           __builtin_bit_cast(uint32_t, bv[(size_t)e]) ==
+                               __builtin_bit_cast(uint32_t, (float)val[(size_t)e]);
+            }
+            if (same) {
+                *out = built;
+                return SPCONV_OK;
+            }
+            spconv_csr_free(built);
+        }
+    }
+    spconv_csr* h = nullptr;
+    if (int rc = spconv_csr_from_host(rows, cols, ptr.data(), idx.data(), val.data(), device, stream, &h))
+        return rc;
+    h->g = g;  // geometry travels with the matrix (Transform::spec) even when generic
+    *out = h;
     return SPCONV_OK;
 }
 

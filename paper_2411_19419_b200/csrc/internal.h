@@ -101,13 +101,15 @@ struct BandParams {
     int tiles;         // tiles_x * tiles_y
     int fast_allowed;  // every tap finite and non-zero
     int y_vec;         // Y rows admit CPT-wide vector stores
+    int sy;            // sum over output columns y of cy(y) (closed-form row starts)
+    int nnz;
 };
 
 struct BandShape {
     int th, tw, wr, wc, smem, threads, occ;
 };
 
-// Speculative conv SpMV (spmm.cu, batch <= 2, dense taps).
+// Warp-per-32-rows latency SpMV (spmm.cu, batch <= 2).
 struct SpecParams {
     const int32_t* row_ptr;
     const int32_t* col_idx;
@@ -116,7 +118,7 @@ struct SpecParams {
     int64_t ldx;
     float* Y;
     int64_t ldy;
-    int rows, batch;
+    int rows, batch, nnz;
     int m, n, k, s, p, mo, no;
     int sy;    // sum over output columns y of cy(y)
     int skew;  // test hook: offsets the predicted row start (forces the mismatch path)
@@ -141,7 +143,7 @@ cudaError_t launch_tiled(const TiledParams& tp, const CUtensorMap* tmap, int bt,
                          cudaStream_t st);
 cudaError_t launch_generic(const GenericParams& gp, cudaStream_t st);
 cudaError_t launch_spmv_unrolled(const GenericParams& gp, int kmax, cudaStream_t st);
-cudaError_t launch_spmv_spec(const SpecParams& sp, int kmax, cudaStream_t st);
+cudaError_t launch_spmv_warp(const SpecParams& sp, int kmax, bool spec, cudaStream_t st);
 bool banded_supported(int k, int s);
 cudaError_t launch_banded(int k, int s, const BandedParams& bp, const CUtensorMap* tmap,
                           cudaStream_t st, BandedShape* shape);
@@ -150,7 +152,12 @@ bool band_supported(int k, int s);
 int band_tile_width(int k, int s);
 cudaError_t launch_band(int k, int s, const BandParams& bp, const CUtensorMap* tmap, cudaStream_t st,
                         BandShape* shape, int sms);
-cudaError_t launch_band_check(int k, int s, const BandParams& bp, cudaStream_t st);
+cudaError_t launch_band_check(int k, int s, const BandParams& bp, cudaStream_t st, int sms);
+
+cudaError_t render_entries(const int32_t* row_ptr, const int32_t* col_idx, const float* vals, int rows,
+                           unsigned long long* scratch, char* out_dev, unsigned long long base,
+                           cudaStream_t st, bool size_only);
+int text_rows_per_block();
 
 size_t tiled_smem_bytes(int th, int wr, int wc, int k2max, int bt, int stages);
 
@@ -170,6 +177,7 @@ struct spconv_csr {
     float* taps = nullptr;         // device k*k taps (conv transforms)
     uint8_t* seg_ok = nullptr;     // device band-check bytes [mo][tiles_y] (band geometries)
     int band_tw = 0;               // tile width seg_ok was sized for (0: none)
+    int64_t sy = 0;                // sum over output columns of the valid tap-column count
     std::atomic<const char*> last_kernel{nullptr};  // diagnostics: last SpMM kernel launched
     // Workspace of spconv_convolve_host (lazily created, guarded by ws_mu).
     std::mutex ws_mu;

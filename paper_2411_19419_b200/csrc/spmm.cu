@@ -195,78 +195,145 @@ cudaError_t launch_spmv_unrolled(const GenericParams& gp, int kmax, cudaStream_t
     return cudaGetLastError();
 }
 
-// Speculative single-pass SpMV / small-batch SpMM of a conv transform built
-// with dense taps (BASELINE config 2: one 512^2 image, ~15 MB -- a latency
-// problem).  The CSR is still what is multiplied: every thread loads its row's
-// row_ptr pair and (col, val) pairs, but it issues those loads TOGETHER with
-// the x gathers at the columns the closed form predicts (row (x, y) starts at
-// CX(x)*SY + cx(x)*CY(y), taps in (j, i) order), so a row costs one memory
-// round trip instead of three.  The prediction never decides the result:
-// each stored column is compared with its prediction and a mismatch reloads
-// x[col] (a row whose row_ptr pair disagrees takes the plain loop), so the
-// output is exactly  acc = fmaf(val[e], x[col[e]], acc)  over the stored row.
+// Latency SpMV / 2-vector SpMM (BASELINE config 2: one 512^2 image, ~15 MB):
+// a warp owns 32 consecutive rows.  Their (col, val) pairs are one contiguous
+// run [row_ptr[r0], row_ptr[r0+32]) that the warp streams with coalesced
+// loads into shared memory; then each lane walks its own row from shared
+// memory (lane stride = row length, conflict-free for odd lengths), issues
+// all of the row's x gathers at once (consecutive output pixels gather
+// neighbouring pixels: coalesced) and accumulates sequentially,
+// acc = fmaf(val, x, acc) in stored order -- the reference's row loop, bit for
+// bit.  For conv transforms with dense taps (SPEC) the run's bounds are
+// predicted in closed form (row (x, y) starts at CX(x)*SY + cx(x)*CY(y)), so
+// the run is requested together with row_ptr (two dependent memory trips per
+// row instead of three); the loaded row_ptr decides, a mismatch reloads.
+// a / s for a >= 0 with the common strides specialised (s is warp-uniform).
+__device__ __forceinline__ int div_stride(int a, int s) {
+    switch (s) {
+        case 1: return a;
+        case 2: return a >> 1;
+        case 3: return a / 3;
+        case 4: return a >> 2;
+        default: return a / s;
+    }
+}
+
 __device__ __forceinline__ int slides_before_dev(int x, int j, int dim, int s, int p) {
-    const int lo = (p - j <= 0) ? 0 : (p - j + s - 1) / s;
-    const int hi = (dim + p - j - 1 < 0) ? 0 : (dim + p - j - 1) / s + 1;
+    const int lo = (p - j <= 0) ? 0 : div_stride(p - j + s - 1, s);
+    const int hi = (dim + p - j - 1 < 0) ? 0 : div_stride(dim + p - j - 1, s) + 1;
     return max(0, min(x, hi) - lo);
 }
 
-template <int KMAX>
-__global__ void __launch_bounds__(256) conv_spmv_spec(const SpecParams P) {
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= P.rows) return;
+__device__ __forceinline__ int conv_row_start(const SpecParams& P, int r) {
+    if (r >= P.rows) return P.nnz;
     const int x = r / P.no, y = r - x * P.no;
     const int jlo = min(max(0, P.p - P.s * x), P.k), jhi = max(jlo, min(P.k, P.m + P.p - P.s * x));
-    const int ilo = min(max(0, P.p - P.s * y), P.k), ihi = max(ilo, min(P.k, P.n + P.p - P.s * y));
-    const int cy = ihi - ilo;
-    const int cnt = (jhi - jlo) * cy;
-    int cxb = 0, cyb = 0;  // sum_{x' < x} cx(x'), sum_{y' < y} cy(y')
+    int cxb = 0, cyb = 0;
     for (int j = 0; j < P.k; ++j) {
         cxb += slides_before_dev(x, j, P.m, P.s, P.p);
         cyb += slides_before_dev(y, j, P.n, P.s, P.p);
     }
-    const int e0 = cxb * P.sy + (jhi - jlo) * cyb + P.skew;
-    const int a = __ldg(P.row_ptr + r), b = __ldg(P.row_ptr + r + 1);
+    return cxb * P.sy + (jhi - jlo) * cyb + P.skew;
+}
+
+template <int KMAX, bool SPEC>
+__global__ void __launch_bounds__(128) csr_spmv_warp(const SpecParams P) {
+    constexpr int WARPS = 4;
+    constexpr int RUN = 32 * KMAX;  // max entries of a 32-row run
+    extern __shared__ float smem_sv[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int r0 = (blockIdx.x * WARPS + warp) * 32;
+    if (r0 >= P.rows) return;
+    const int nr = min(32, P.rows - r0);
+    float* sv = smem_sv + (size_t)warp * RUN * 2;  // vals | cols
+    int* sc = reinterpret_cast<int*>(sv + RUN);
+
+    int E0 = 0, E1 = 0;
+    if (SPEC) {
+        E0 = conv_row_start(P, r0);
+        E1 = conv_row_start(P, r0 + nr);
+    }
+    const int a = lane < nr ? __ldg(P.row_ptr + r0 + lane) : 0;
+    const int end = __ldg(P.row_ptr + r0 + nr);
     int c[KMAX];
     float v[KMAX];
-    int pc[KMAX];
-    {
-        int j = jlo, i = ilo;
+    bool hit = SPEC;
+    if (SPEC) {
+        // Speculative: issued before the row_ptr loads land.
 #pragma unroll
-        for (int q = 0; q < KMAX; ++q) {
-            const bool on = q < cnt;
-            c[q] = on ? __ldg(P.col_idx + e0 + q) : 0;
-            v[q] = on ? __ldg(P.vals + e0 + q) : 0.0f;
-            pc[q] = (P.s * x + j - P.p) * P.n + (P.s * y + i - P.p);
-            if (++i == ihi) i = ilo, ++j;
+        for (int u = 0; u < KMAX; ++u) {
+            const int e = E0 + lane + 32 * u;
+            c[u] = e < E1 ? __ldg(P.col_idx + e) : 0;
+            v[u] = e < E1 ? __ldg(P.vals + e) : 0.0f;
+        }
+        hit = __shfl_sync(0xffffffffu, a, 0) == E0 && end == E1;
+    }
+    if (!hit) {
+        E0 = __shfl_sync(0xffffffffu, a, 0);
+        E1 = end;
+        if (E1 - E0 > RUN) __trap();  // dispatcher guarantees rows of <= KMAX entries
+#pragma unroll
+        for (int u = 0; u < KMAX; ++u) {
+            const int e = E0 + lane + 32 * u;
+            c[u] = e < E1 ? __ldg(P.col_idx + e) : 0;
+            v[u] = e < E1 ? __ldg(P.vals + e) : 0.0f;
         }
     }
-    const bool row_ok = a == e0 && b == e0 + cnt;
+#pragma unroll
+    for (int u = 0; u < KMAX; ++u) {
+        const int d = lane + 32 * u;
+        if (E0 + d < E1) {
+            sv[d] = v[u];
+            sc[d] = c[u];
+        }
+    }
+    __syncwarp();
+    int b = __shfl_down_sync(0xffffffffu, a, 1);
+    if (lane >= nr) return;
+    if (lane == nr - 1) b = end;
+    const int d0 = a - E0, cnt = b - a;
+    // Row entries back into registers (this lane's row), then all x gathers at once.
+#pragma unroll
+    for (int q = 0; q < KMAX; ++q) {
+        c[q] = q < cnt ? sc[d0 + q] : 0;
+        v[q] = q < cnt ? sv[d0 + q] : 0.0f;
+    }
     for (int bi = 0; bi < P.batch; ++bi) {
         const float* X = P.X + (int64_t)bi * P.ldx;
+        float xv[KMAX];
+#pragma unroll
+        for (int q = 0; q < KMAX; ++q) xv[q] = q < cnt ? __ldg(X + c[q]) : 0.0f;
         float acc = 0.0f;
-        if (row_ok) {
-            float xv[KMAX];
 #pragma unroll
-            for (int q = 0; q < KMAX; ++q) xv[q] = q < cnt ? __ldg(X + pc[q]) : 0.0f;
-#pragma unroll
-            for (int q = 0; q < KMAX; ++q)
-                if (q < cnt) acc = fmaf(v[q], c[q] == pc[q] ? xv[q] : __ldg(X + c[q]), acc);
-        } else {
-            for (int e = a; e < b; ++e) acc = fmaf(__ldg(P.vals + e), __ldg(X + __ldg(P.col_idx + e)), acc);
-        }
-        P.Y[(int64_t)bi * P.ldy + r] = acc;
+        for (int q = 0; q < KMAX; ++q)
+            if (q < cnt) acc = fmaf(v[q], xv[q], acc);
+        P.Y[(int64_t)bi * P.ldy + r0 + lane] = acc;
     }
 }
 
-cudaError_t launch_spmv_spec(const SpecParams& sp, int kmax, cudaStream_t st) {
-    const int block = 256;
-    const int grid = (sp.rows + block - 1) / block;
-    if (kmax <= 9) conv_spmv_spec<9><<<grid, block, 0, st>>>(sp);
-    else if (kmax <= 25) conv_spmv_spec<25><<<grid, block, 0, st>>>(sp);
-    else if (kmax <= 49) conv_spmv_spec<49><<<grid, block, 0, st>>>(sp);
-    else return cudaErrorInvalidValue;
+template <int KMAX>
+static cudaError_t launch_warp_k(const SpecParams& sp, bool spec, cudaStream_t st) {
+    const size_t smem = (size_t)4 * 32 * KMAX * 2 * sizeof(float);
+    auto kern = spec ? csr_spmv_warp<KMAX, true> : csr_spmv_warp<KMAX, false>;
+    static bool attr_set[2][64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (smem > 48 * 1024 && !attr_set[spec][dev & 63]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr_set[spec][dev & 63] = true;
+    }
+    const int grid = (int)((sp.rows + 127) / 128);
+    kern<<<grid, 128, smem, st>>>(sp);
     return cudaGetLastError();
+}
+
+cudaError_t launch_spmv_warp(const SpecParams& sp, int kmax, bool spec, cudaStream_t st) {
+    if (sp.batch < 1 || sp.batch > 2) return cudaErrorInvalidValue;
+    if (kmax <= 9) return launch_warp_k<9>(sp, spec, st);
+    if (kmax <= 25) return launch_warp_k<25>(sp, spec, st);
+    if (kmax <= 49) return launch_warp_k<49>(sp, spec, st);
+    return cudaErrorInvalidValue;
 }
 
 template <int BT>

@@ -40,6 +40,7 @@
 //    skipping the clipped taps is indistinguishable, and every output still
 //    sees its stored taps in (j, i) = column-ascending order.
 #include <algorithm>
+#include <cstdlib>
 
 #include "internal.h"
 #include "tma.cuh"
@@ -57,6 +58,13 @@ __device__ __forceinline__ void tap_range_dev(int x, int dim, int k, int s, int 
     hi = min(k, dim + p - s * x);
     lo = min(lo, k);
     if (hi < lo) hi = lo;
+}
+
+// #{x' in [0, x) : tap index j lands inside the image at slide x'} (O(1)).
+__device__ __forceinline__ int slides_before(int x, int j, int dim, int s, int p) {
+    const int lo = (p - j <= 0) ? 0 : (p - j + s - 1) / s;
+    const int hi = (dim + p - j - 1 < 0) ? 0 : (dim + p - j - 1) / s + 1;
+    return max(0, min(x, hi) - lo);
 }
 
 constexpr int round_up(int v, int m) { return (v + m - 1) / m * m; }
@@ -84,106 +92,217 @@ struct BandCfg {
     static constexpr int SF = round_up(WIN, 32);        // floats per stage (128-byte aligned)
     static constexpr size_t SMEM = 128 + (size_t)STAGES * SF * 4;
     static_assert(WC <= 256 && WR <= 256, "TMA box limit");
+    static_assert(TH <= 32, "one producer lane per tile row");
+    static_assert(STAGES * 20 <= 128, "barriers + flag masks fit the 128-byte header");
 };
 
 // ---------------------------------------------------------------------------
 // 1. Band check: one warp per segment.
 // ---------------------------------------------------------------------------
 template <int K, int S, int TW>
-__global__ void __launch_bounds__(256) conv_band_check(const BandParams P) {
+struct CheckCfg {
+    static constexpr int KK = K * K;
+    static constexpr int RUN = TW * KK;                    // entries of an interior segment
+    static constexpr int BUFW = (RUN + 3 + 3) / 4 * 4;     // 16-byte aligned superset
+    static constexpr size_t WARP_BYTES = 2ull * 2 * BUFW * 4;  // 2 buffers x (cols + vals)
+    static constexpr int WARPS = (int)(200 * 1024 / WARP_BYTES) < 8 ? (int)(200 * 1024 / WARP_BYTES) : 8;
+    static constexpr size_t SMEM = 128 + (size_t)WARPS * WARP_BYTES;
+    static_assert(WARPS >= 1, "segment too large for shared memory");
+};
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+template <int K, int S, int TW>
+__global__ void __launch_bounds__(CheckCfg<K, S, TW>::WARPS * 32, 1) conv_band_check(const BandParams P) {
+    using C = CheckCfg<K, S, TW>;
     constexpr int KK = K * K;
-    __shared__ uint32_t s_w[KK];
+    constexpr int RPL = TW / 32;  // rows per lane
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + 2 * warp;
+    int* buf = reinterpret_cast<int*>(smem + 128 + (size_t)warp * C::WARP_BYTES);
+    if (lane == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        mbar_fence_init();
+    }
+    __syncwarp();
+    __shared__ uint32_t s_w[KK];  // taps for the border walk (runtime-indexed)
     for (int q = threadIdx.x; q < KK; q += blockDim.x) s_w[q] = __float_as_uint(__ldg(P.taps + q));
     __syncthreads();
-
-    const int lane = threadIdx.x & 31;
-    const long long seg = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (seg >= (long long)P.mo * P.tiles_y) return;
-    const int x = (int)(seg / P.tiles_y);
-    const int ty = (int)(seg - (long long)x * P.tiles_y);
-    const int y0 = ty * TW;
-    const int nr = min(TW, P.no - y0);
-    const int r0 = x * P.no + y0;
-
-    int jlo, jhi;
-    tap_range_dev(x, P.m, K, S, P.p, jlo, jhi);
-    bool ok = true;
-    bool full = (jlo == 0 && jhi == K);
-    int a_first[TW / 32];
+    uint32_t w[KK];  // taps for the interior check (compile-time indexed)
 #pragma unroll
-    for (int q = 0; q < TW / 32; ++q) {
-        const int l = lane + 32 * q;
-        a_first[q] = 0;
-        if (l < nr) {
-            int ilo, ihi;
-            tap_range_dev(y0 + l, P.n, K, S, P.p, ilo, ihi);
-            const int a = __ldg(P.row_ptr + r0 + l), b = __ldg(P.row_ptr + r0 + l + 1);
-            ok &= (b - a) == (jhi - jlo) * (ihi - ilo);
-            full &= (ilo == 0 && ihi == K);
-            a_first[q] = a;
+    for (int q = 0; q < KK; ++q) w[q] = s_w[q];
+
+    // Each warp owns a contiguous range of segments (consecutive memory, and
+    // every warp meets its share of border segments).
+    const long long nseg_all = (long long)P.mo * P.tiles_y;
+    const long long nw = (long long)gridDim.x * C::WARPS;
+    const long long gw = (long long)blockIdx.x * C::WARPS + warp;
+    const long long seg_lo = nseg_all * gw / nw, nseg = nseg_all * (gw + 1) / nw;
+    const long long stride = 1;
+
+    // Segment geometry + closed-form start (dense taps): rows before (x, y0)
+    // = CX(x) * SY + cx(x) * CY(y0)  (Theorem 2.1 prefix sums).
+    struct Seg {
+        int x, y0, nr, r0, jlo, jhi, S0;
+        bool full;
+    };
+    auto geom = [&](long long seg) {
+        Seg g;
+        g.x = (int)(seg / P.tiles_y);
+        const int ty = (int)(seg - (long long)g.x * P.tiles_y);
+        g.y0 = ty * TW;
+        g.nr = min(TW, P.no - g.y0);
+        g.r0 = g.x * P.no + g.y0;
+        tap_range_dev(g.x, P.m, K, S, P.p, g.jlo, g.jhi);
+        int cxb = 0, cyb = 0;
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            cxb += slides_before(g.x, j, P.m, S, P.p);
+            cyb += slides_before(g.y0, j, P.n, S, P.p);
         }
-    }
-    full = __all_sync(0xffffffffu, full);
-    if (full && __all_sync(0xffffffffu, ok)) {
-        // Contiguous run of nr*KK pairs starting at row_ptr[r0].
-        const int S0 = __shfl_sync(0xffffffffu, a_first[0], 0);
+        g.S0 = cxb * P.sy + (g.jhi - g.jlo) * cyb;
+        // interior: every row of the segment stores all K*K taps
+        const int ylast = g.y0 + g.nr - 1;
+        g.full = g.jlo == 0 && g.jhi == K && S * g.y0 - P.p >= 0 && S * ylast - P.p + K <= P.n &&
+                 (long long)g.S0 + g.nr * KK <= (long long)P.nnz;  // (zero taps: prediction past the end)
+        return g;
+    };
+    auto issue = [&](const Seg& g, int b) {  // lane 0: bulk-copy the run into buffer b
+        const int abase = g.S0 & ~3;
+        const uint32_t bytes = (uint32_t)(((g.S0 + g.nr * KK - abase + 3) & ~3) * 4);
+        int* dst = buf + b * 2 * C::BUFW;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&bars[b], 2 * bytes);
+        bulk_g2s(dst, P.col_idx + abase, bytes, &bars[b]);
+        bulk_g2s(dst + C::BUFW, P.vals + abase, bytes, &bars[b]);
+    };
+
+    long long seg = seg_lo;
+    if (seg >= nseg) return;
+    Seg cur = geom(seg);
+    if (cur.full && lane == 0) issue(cur, 0);
+    uint32_t phases = 0u;  // bit b: parity of buffer b's next completion
+    for (int i = 0; seg < nseg; ++i, seg += stride) {
+        const int b = i & 1;
+        // row_ptr of this segment (nr + 1 values)
+        int a_row[RPL];
 #pragma unroll
-        for (int q = 0; q < TW / 32; ++q) {
+        for (int q = 0; q < RPL; ++q) {
             const int l = lane + 32 * q;
-            if (l < nr) ok &= a_first[q] == S0 + l * KK;
+            a_row[q] = l < cur.nr ? __ldg(P.row_ptr + cur.r0 + l) : 0;
         }
-        const int base = (S * x - P.p) * P.n + (S * y0 - P.p);
-        const int len = nr * KK;
-        const int32_t* cp = P.col_idx + S0;
-        const float* vp = P.vals + S0;
-        uint32_t bad = 0;
-        constexpr int U = 8;
-        for (int d0 = 0; d0 < len; d0 += 32 * U) {
-            int c[U];
-            uint32_t v[U];
+        const int a_end = __ldg(P.row_ptr + cur.r0 + cur.nr);
+        // prefetch the next segment's run into the other buffer
+        Seg nxt{};
+        const bool has_next = seg + stride < nseg;
+        if (has_next) {
+            nxt = geom(seg + stride);
+            __syncwarp();  // this warp finished reading buffer b^1 (segment i-1)
+            if (nxt.full && lane == 0) issue(nxt, b ^ 1);
+        }
+        bool ok = true;
+        if (cur.full) {
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int d = d0 + lane + 32 * u;
-                c[u] = d < len ? __ldg(cp + d) : 0;
-                v[u] = d < len ? __float_as_uint(__ldg(vp + d)) : 0u;
+            for (int q = 0; q < RPL; ++q) {
+                const int l = lane + 32 * q;
+                if (l < cur.nr) ok &= a_row[q] == cur.S0 + l * KK;
             }
+            ok &= a_end == cur.S0 + cur.nr * KK;
+            mbar_wait(&bars[b], (phases >> b) & 1u);
+            phases ^= 1u << b;
+            const int* cb = buf + b * 2 * C::BUFW + (cur.S0 & 3);
+            const uint32_t* vb = reinterpret_cast<const uint32_t*>(cb + C::BUFW);
+            uint32_t bad = 0;
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int d = d0 + lane + 32 * u;
-                if (d < len) {
-                    const int l = d / KK, q = d - l * KK;
-                    const int j = q / K, i = q - j * K;
-                    bad |= (uint32_t)(c[u] - (base + S * l + j * P.n + i)) | (v[u] ^ s_w[q]);
+            for (int q = 0; q < RPL; ++q) {
+                const int l = lane + 32 * q;
+                if (l < cur.nr) {
+                    const int rb = (S * cur.x - P.p) * P.n + S * (cur.y0 + l) - P.p;
+                    const int* cl = cb + l * KK;
+                    const uint32_t* vl = vb + l * KK;
+#pragma unroll
+                    for (int j = 0; j < K; ++j)
+#pragma unroll
+                        for (int ii = 0; ii < K; ++ii)
+                            bad |= (uint32_t)(cl[j * K + ii] - (rb + j * P.n + ii)) | (vl[j * K + ii] ^ w[j * K + ii]);
+                }
+            }
+            ok &= bad == 0u;
+        } else {
+            // Border segment: each lane walks its own rows from global memory,
+            // every (col, val) load of a row in flight at once.
+#pragma unroll
+            for (int q = 0; q < RPL; ++q) {
+                const int l = lane + 32 * q;
+                if (l < cur.nr) {
+                    const int y = cur.y0 + l;
+                    int ilo, ihi;
+                    tap_range_dev(y, P.n, K, S, P.p, ilo, ihi);
+                    const int bnd = __ldg(P.row_ptr + cur.r0 + l + 1);
+                    if (bnd - a_row[q] != (cur.jhi - cur.jlo) * (ihi - ilo)) {
+                        ok = false;
+                        continue;
+                    }
+                    const int rb = (S * cur.x - P.p) * P.n + (S * y - P.p);
+                    int e = a_row[q];
+                    uint32_t bad = 0;
+#pragma unroll
+                    for (int j = 0; j < K; ++j)
+#pragma unroll
+                        for (int ii = 0; ii < K; ++ii)
+                            if (j >= cur.jlo && j < cur.jhi && ii >= ilo && ii < ihi) {
+                                bad |= (uint32_t)(__ldg(P.col_idx + e) - (rb + j * P.n + ii)) |
+                                       (__float_as_uint(__ldg(P.vals + e)) ^ w[j * K + ii]);
+                                ++e;
+                            }
+                    ok &= bad == 0u;
                 }
             }
         }
-        ok &= bad == 0u;
-    } else {
-        // Border segment: each lane walks its own rows.
-#pragma unroll
-        for (int q = 0; q < TW / 32; ++q) {
-            const int l = lane + 32 * q;
-            if (l < nr && ok) {
-                const int y = y0 + l;
-                int ilo, ihi;
-                tap_range_dev(y, P.n, K, S, P.p, ilo, ihi);
-                int e = a_first[q];
-                for (int j = jlo; j < jhi; ++j) {
-                    const int rowc = (S * x + j - P.p) * P.n + (S * y - P.p);
-                    for (int i = ilo; i < ihi; ++i, ++e)
-                        ok &= (__ldg(P.col_idx + e) == rowc + i) &&
-                              (__float_as_uint(__ldg(P.vals + e)) == s_w[j * K + i]);
-                }
-            }
-        }
+        ok = __all_sync(0xffffffffu, ok);
+        if (lane == 0) P.seg_ok[seg] = ok ? 1 : 0;
+        cur = nxt;
     }
-    ok = __all_sync(0xffffffffu, ok);
-    if (lane == 0) P.seg_ok[seg] = ok ? 1 : 0;
 }
 
 // ---------------------------------------------------------------------------
 // 2. Register-blocked apply.
 // ---------------------------------------------------------------------------
+
+// Persistent work walk: item i = img * tiles + tx * tiles_y + ty, visited as
+// i = blockIdx.x, blockIdx.x + gridDim.x, ... with the mixed-radix step
+// precomputed once (no per-item division).
+struct ItemIter {
+    int img, tx, ty;
+    int s_img, s_tx, s_ty, tiles_x, tiles_y;
+    __device__ explicit ItemIter(const BandParams& P) {
+        tiles_y = P.tiles_y;
+        tiles_x = P.tiles / P.tiles_y;
+        int t = (int)(blockIdx.x % (unsigned)P.tiles);
+        img = (int)(blockIdx.x / (unsigned)P.tiles);
+        tx = t / tiles_y;
+        ty = t - tx * tiles_y;
+        t = (int)(gridDim.x % (unsigned)P.tiles);
+        s_img = (int)(gridDim.x / (unsigned)P.tiles);
+        s_tx = t / tiles_y;
+        s_ty = t - s_tx * tiles_y;
+    }
+    __device__ void next() {
+        ty += s_ty;
+        tx += s_tx;
+        img += s_img;
+        if (ty >= tiles_y) ty -= tiles_y, ++tx;
+        if (tx >= tiles_x) tx -= tiles_x, ++img;
+    }
+};
 template <int K, int S, int V, int CPT, int TH, int STAGES, int DELTA>
 __global__ void __launch_bounds__(BandCfg<K, S, V, CPT, TH, STAGES, DELTA>::THREADS, 1)
     conv_spmm_band(const __grid_constant__ CUtensorMap tmap, const BandParams P) {
@@ -191,11 +310,11 @@ __global__ void __launch_bounds__(BandCfg<K, S, V, CPT, TH, STAGES, DELTA>::THRE
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
     uint64_t* empty = full + STAGES;
+    unsigned* s_mask = reinterpret_cast<unsigned*>(empty + STAGES);  // per-stage row flags
     float* xs = reinterpret_cast<float*>(smem + 128);
 
     const int t = threadIdx.x;
     const int lane = t & 31, warp = t >> 5;
-    const long long items = (long long)P.tiles * P.batch;  // item = img * tiles + tile
 
     if (t == 0) {
         tma_prefetch_desc(&tmap);
@@ -208,20 +327,28 @@ __global__ void __launch_bounds__(BandCfg<K, S, V, CPT, TH, STAGES, DELTA>::THRE
     __syncthreads();
 
     if (warp == C::CWARPS) {
-        // ---- producer: one elected lane issues the window loads ----
-        if (lane == 0) {
-            int it = 0;
-            for (long long i = blockIdx.x; i < items; i += gridDim.x, ++it) {
-                const int st = it % STAGES;
-                if (it >= STAGES) mbar_wait(&empty[st], (uint32_t)(((it / STAGES) - 1) & 1));
-                const int img = (int)(i / P.tiles);
-                const int tile = (int)(i - (long long)img * P.tiles);
-                const int tx = tile / P.tiles_y, ty = tile - tx * P.tiles_y;
-                const int wr0 = S * tx * TH - P.p;
-                const int wc0 = S * ty * C::TW - P.p - DELTA;
-                mbar_expect_tx(&full[st], (uint32_t)(C::WIN * 4));
-                tma_load_3d(xs + (size_t)st * C::SF, &tmap, wc0, wr0, img, &full[st]);
+        // ---- producer warp: per item, the tile rows' band-check flags (one
+        // lane per row, folded into a per-stage bit mask) and the window load
+        // (one elected lane).  Running STAGES items ahead hides the flag
+        // loads' latency from the consumers.
+        int it = 0;
+        for (ItemIter I(P); I.img < P.batch; I.next(), ++it) {
+            const int st = it % STAGES;
+            bool f = true;
+            if (lane < TH) {
+                const int x = I.tx * TH + lane;
+                f = x >= P.mo || __ldg(P.seg_ok + (long long)x * P.tiles_y + I.ty) != 0;
             }
+            const unsigned rows_ok = __ballot_sync(0xffffffffu, f);
+            if (lane == 0) {
+                if (it >= STAGES) mbar_wait(&empty[st], (uint32_t)(((it / STAGES) - 1) & 1));
+                s_mask[st] = rows_ok;
+                const int wr0 = S * I.tx * TH - P.p;
+                const int wc0 = S * I.ty * C::TW - P.p - DELTA;
+                mbar_expect_tx(&full[st], (uint32_t)(C::WIN * 4));
+                tma_load_3d(xs + (size_t)st * C::SF, &tmap, wc0, wr0, I.img, &full[st]);
+            }
+            __syncwarp();
         }
         return;
     }
@@ -231,24 +358,18 @@ __global__ void __launch_bounds__(BandCfg<K, S, V, CPT, TH, STAGES, DELTA>::THRE
 #pragma unroll
     for (int q = 0; q < C::KK; ++q) w[q] = __ldg(P.taps + q);
     const bool vec_ok = P.y_vec != 0;
+    constexpr unsigned VMASK = (1u << V) - 1u;
 
     int it = 0;
-    for (long long i = blockIdx.x; i < items; i += gridDim.x, ++it) {
+    for (ItemIter I(P); I.img < P.batch; I.next(), ++it) {
         const int st = it % STAGES;
-        const int img = (int)(i / P.tiles);
-        const int tile = (int)(i - (long long)img * P.tiles);
-        const int tx = tile / P.tiles_y, ty = tile - tx * P.tiles_y;
+        const int img = I.img, tx = I.tx, ty = I.ty;
         const int xb = tx * TH + warp * V;  // this warp's first output row
         const int y0 = ty * C::TW;
-        // This warp's rows must all lie in verified segments.
-        bool ok = true;
-        if (lane < V) {
-            const int x = xb + lane;
-            ok = x >= P.mo || P.seg_ok[(long long)x * P.tiles_y + ty] != 0;
-        }
-        const bool fast = __all_sync(0xffffffffu, ok) && P.fast_allowed;
-
         mbar_wait(&full[st], (uint32_t)((it / STAGES) & 1));
+        // This warp's rows must all lie in verified segments (and the taps be
+        // finite and non-zero) for the blocked path.
+        const bool fast = P.fast_allowed && ((s_mask[st] >> (warp * V)) & VMASK) == VMASK;
         const float* xw = xs + (size_t)st * C::SF;
         float* ybase = P.Y + (long long)img * P.ldy;
 
@@ -373,10 +494,24 @@ cudaError_t run_delta(int delta, const BandParams& bp, const CUtensorMap* tmap, 
 }
 
 template <int K, int S, int TW>
-cudaError_t run_check(const BandParams& bp, cudaStream_t st) {
+cudaError_t run_check(const BandParams& bp, cudaStream_t st, int sms) {
+    using C = CheckCfg<K, S, TW>;
+    auto kern = conv_band_check<K, S, TW>;
+    static int occ[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!occ[dev & 63]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+        if (e != cudaSuccess) return e;
+        int o = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, C::WARPS * 32, C::SMEM);
+        if (e != cudaSuccess) return e;
+        occ[dev & 63] = std::max(o, 1);
+    }
     const long long segs = (long long)bp.mo * bp.tiles_y;
-    const long long grid = (segs + 7) / 8;
-    conv_band_check<K, S, TW><<<(unsigned)grid, 256, 0, st>>>(bp);
+    const long long want = (segs + C::WARPS - 1) / C::WARPS;
+    const long long grid = std::min<long long>(want, (long long)occ[dev & 63] * sms);
+    kern<<<(unsigned)grid, C::WARPS * 32, C::SMEM, st>>>(bp);
     return cudaGetLastError();
 }
 
@@ -396,20 +531,35 @@ int band_tile_width(int k, int s) {
 cudaError_t launch_band(int k, int s, const BandParams& bp, const CUtensorMap* tmap, cudaStream_t st,
                         BandShape* shape, int sms) {
     const int delta = ((-bp.p) % 4 + 4) % 4;
-    if (k == 3 && s == 1) return run_delta<3, 1, 4, 4, 32, 4>(delta, bp, tmap, st, shape, sms);
+    // Blocking variants for tuning experiments (SPCONV_B200_VARIANT; 0 = default),
+    // instantiated only for the alignment shift of the benchmark configs.
+    static const int var = std::getenv("SPCONV_B200_VARIANT") ? std::atoi(std::getenv("SPCONV_B200_VARIANT")) : 0;
+    if (k == 3 && s == 1) {
+        if (delta == 3 && var == 1) return run_cfg<3, 1, 4, 4, 16, 4, 3>(bp, tmap, st, shape, sms);
+        if (delta == 3 && var == 2) return run_cfg<3, 1, 8, 4, 32, 4, 3>(bp, tmap, st, shape, sms);
+        if (delta == 3 && var == 3) return run_cfg<3, 1, 4, 4, 32, 3, 3>(bp, tmap, st, shape, sms);
+        if (delta == 3 && var == 4) return run_cfg<3, 1, 2, 4, 16, 4, 3>(bp, tmap, st, shape, sms);
+        return run_delta<3, 1, 4, 4, 32, 4>(delta, bp, tmap, st, shape, sms);
+    }
     if (k == 5 && s == 1) return run_delta<5, 1, 4, 4, 32, 4>(delta, bp, tmap, st, shape, sms);
     if (k == 3 && s == 2) return run_delta<3, 2, 4, 2, 16, 4>(delta, bp, tmap, st, shape, sms);
     if (k == 5 && s == 2) return run_delta<5, 2, 4, 2, 16, 4>(delta, bp, tmap, st, shape, sms);
-    if (k == 7 && s == 2) return run_delta<7, 2, 4, 2, 16, 4>(delta, bp, tmap, st, shape, sms);
+    if (k == 7 && s == 2) {
+        if (delta == 1 && var == 1) return run_cfg<7, 2, 4, 2, 16, 3, 1>(bp, tmap, st, shape, sms);
+        if (delta == 1 && var == 2) return run_cfg<7, 2, 2, 2, 16, 3, 1>(bp, tmap, st, shape, sms);
+        if (delta == 1 && var == 3) return run_cfg<7, 2, 4, 2, 32, 2, 1>(bp, tmap, st, shape, sms);
+        if (delta == 1 && var == 4) return run_cfg<7, 2, 2, 2, 8, 4, 1>(bp, tmap, st, shape, sms);
+        return run_delta<7, 2, 4, 2, 16, 4>(delta, bp, tmap, st, shape, sms);
+    }
     return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_band_check(int k, int s, const BandParams& bp, cudaStream_t st) {
-    if (k == 3 && s == 1) return run_check<3, 1, 128>(bp, st);
-    if (k == 5 && s == 1) return run_check<5, 1, 128>(bp, st);
-    if (k == 3 && s == 2) return run_check<3, 2, 64>(bp, st);
-    if (k == 5 && s == 2) return run_check<5, 2, 64>(bp, st);
-    if (k == 7 && s == 2) return run_check<7, 2, 64>(bp, st);
+cudaError_t launch_band_check(int k, int s, const BandParams& bp, cudaStream_t st, int sms) {
+    if (k == 3 && s == 1) return run_check<3, 1, 128>(bp, st, sms);
+    if (k == 5 && s == 1) return run_check<5, 1, 128>(bp, st, sms);
+    if (k == 3 && s == 2) return run_check<3, 2, 64>(bp, st, sms);
+    if (k == 5 && s == 2) return run_check<5, 2, 64>(bp, st, sms);
+    if (k == 7 && s == 2) return run_check<7, 2, 64>(bp, st, sms);
     return cudaErrorInvalidValue;
 }
 

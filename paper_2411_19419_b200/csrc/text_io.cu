@@ -1,0 +1,317 @@
+// text_io.cu -- transform persistence on the device path.
+//
+// write_transform (inc/conv.hpp:217-224) + write_sparse (inc/sparse.hpp:400-406):
+//     %%transform m n k s p csr
+//     %%sparse coordinate real
+//     rows cols nnz
+//     row col value            (1-based, storage order, value as "%.17g")
+// The reference formats every entry on the host with snprintf; here the GPU
+// renders the text: a sizing pass (bytes per block of rows), a scan of the
+// block totals, and a rendering pass that stages each block's lines in shared
+// memory and writes them out contiguously.  Values are fp32 widened to double
+// (the reference's value type), printed with an exact %.17g: 17 significant
+// digits of the binary value, correctly rounded (glibc semantics: round half
+// to even on the exact value), %g's choice of fixed or exponent style,
+// trailing zeros stripped, and "inf" / "-inf" / "nan" / "-nan" spellings.
+// The result is byte-identical to the reference's file for the same matrix.
+#include <cstring>
+#include <mutex>
+
+#include "internal.h"
+
+namespace spb {
+
+namespace {
+
+__constant__ unsigned long long c_pow5[62][3];  // 5^k, k = 0..61, little-endian 64-bit limbs
+
+// q = round_half_even(n >> rs) for a 192-bit n, rs >= 1; q < 2^64 assumed.
+__device__ __forceinline__ unsigned long long shr192_round(const unsigned long long n[3], int rs) {
+    auto limb = [&](int i) -> unsigned long long { return i < 3 ? n[i] : 0ull; };
+    const int li = rs >> 6, bo = rs & 63;
+    unsigned long long q = bo ? (limb(li) >> bo) | (limb(li + 1) << (64 - bo)) : limb(li);
+    const int hb = rs - 1;
+    const bool half = (limb(hb >> 6) >> (hb & 63)) & 1ull;
+    bool sticky = false;
+    const int sl = hb >> 6, sb = hb & 63;
+    for (int i = 0; i < sl; ++i) sticky |= limb(i) != 0ull;
+    if (sb) sticky |= (limb(sl) & ((1ull << sb) - 1ull)) != 0ull;
+    if (half && (sticky || (q & 1ull))) ++q;
+    return q;
+}
+
+// round_half_even(M * 2^E * 10^k) exactly (M < 2^24).
+__device__ unsigned long long scaled_round(unsigned M, int E, int k) {
+    if (k >= 0) {
+        const unsigned long long* p5 = c_pow5[k];
+        unsigned long long n[3];
+        unsigned __int128 t = (unsigned __int128)p5[0] * M;
+        n[0] = (unsigned long long)t;
+        t = (t >> 64) + (unsigned __int128)p5[1] * M;
+        n[1] = (unsigned long long)t;
+        t = (t >> 64) + (unsigned __int128)p5[2] * M;
+        n[2] = (unsigned long long)t;
+        const int sh = E + k;
+        if (sh >= 0) return n[0] << sh;  // exact (the caller keeps the result < 10^18)
+        return shr192_round(n, -sh);
+    }
+    const int q = -k;  // value >= 1e17: E - q >= 0
+    unsigned long long d5 = 1;
+    for (int i = 0; i < q; ++i) d5 *= 5ull;
+    const unsigned __int128 num = (unsigned __int128)M << (E - q);
+    unsigned long long quo = (unsigned long long)(num / d5);
+    const unsigned long long rem = (unsigned long long)(num - (unsigned __int128)quo * d5);
+    if (2 * (unsigned __int128)rem > d5) ++quo;  // 5^q is odd: no ties
+    return quo;
+}
+
+}  // namespace
+
+// "%.17g" of (double)v into out (<= 24 chars, no terminator); returns the length.
+__device__ int format_g17(float v, char* out) {
+    const unsigned bits = __float_as_uint(v);
+    int o = 0;
+    if (bits >> 31) out[o++] = '-';
+    const unsigned ex = (bits >> 23) & 0xffu, man = bits & 0x7fffffu;
+    if (ex == 0xffu) {
+        const char* w = man ? "nan" : "inf";
+        for (int i = 0; i < 3; ++i) out[o++] = w[i];
+        return o;
+    }
+    if (ex == 0 && man == 0) {
+        out[o++] = '0';
+        return o;
+    }
+    const unsigned M = ex ? (man | 0x800000u) : man;
+    const int E = ex ? (int)ex - 150 : -149;
+    int X = (int)floor(log10((double)M) + E * 0.30102999566398120);
+    unsigned long long D = 0;
+    for (int guard = 0; guard < 4; ++guard) {
+        D = scaled_round(M, E, 16 - X);
+        if (D >= 100000000000000000ull) ++X;
+        else if (D < 10000000000000000ull) --X;
+        else break;
+    }
+    char dg[17];
+    for (int i = 16; i >= 0; --i) {
+        dg[i] = (char)('0' + (int)(D % 10ull));
+        D /= 10ull;
+    }
+    int last = 16;
+    while (last > 0 && dg[last] == '0') --last;
+    if (X >= -4 && X < 17) {
+        if (X >= 0) {
+            for (int i = 0; i <= X; ++i) out[o++] = dg[i];
+            if (last > X) {
+                out[o++] = '.';
+                for (int i = X + 1; i <= last; ++i) out[o++] = dg[i];
+            }
+        } else {
+            out[o++] = '0';
+            out[o++] = '.';
+            for (int i = 0; i < -X - 1; ++i) out[o++] = '0';
+            for (int i = 0; i <= last; ++i) out[o++] = dg[i];
+        }
+    } else {
+        out[o++] = dg[0];
+        if (last > 0) {
+            out[o++] = '.';
+            for (int i = 1; i <= last; ++i) out[o++] = dg[i];
+        }
+        out[o++] = 'e';
+        out[o++] = X < 0 ? '-' : '+';
+        const int ax = X < 0 ? -X : X;
+        if (ax >= 100) out[o++] = (char)('0' + ax / 100);
+        out[o++] = (char)('0' + (ax / 10) % 10);
+        out[o++] = (char)('0' + ax % 10);
+    }
+    return o;
+}
+
+namespace {
+
+__device__ __forceinline__ int format_u64(unsigned long long v, char* out) {
+    char tmp[20];
+    int n = 0;
+    do {
+        tmp[n++] = (char)('0' + (int)(v % 10ull));
+        v /= 10ull;
+    } while (v);
+    for (int i = 0; i < n; ++i) out[i] = tmp[n - 1 - i];
+    return n;
+}
+
+__device__ __forceinline__ int digits_u64(unsigned long long v) {
+    int n = 1;
+    while (v >= 10ull) v /= 10ull, ++n;
+    return n;
+}
+
+// Bytes of one entry line "r c v\n".
+__device__ __forceinline__ int line_bytes(int row, int col, float v) {
+    char tmp[32];
+    return digits_u64((unsigned long long)row + 1) + digits_u64((unsigned long long)col + 1) +
+           format_g17(v, tmp) + 3;
+}
+
+constexpr int kRowsPerBlock = 64;
+constexpr int kStageBytes = 96 * 1024;
+
+// Pass 1: bytes of each block of kRowsPerBlock rows.
+__global__ void __launch_bounds__(256) text_size_kernel(const int32_t* row_ptr, const int32_t* col_idx,
+                                                        const float* vals, int rows,
+                                                        unsigned long long* block_bytes) {
+    __shared__ unsigned long long s_sum;
+    if (threadIdx.x == 0) s_sum = 0;
+    __syncthreads();
+    const int r0 = blockIdx.x * kRowsPerBlock;
+    const int r1 = min(rows, r0 + kRowsPerBlock);
+    const int e0 = row_ptr[r0], e1 = row_ptr[r1];
+    unsigned long long local = 0;
+    // entries of the block, one thread per entry (row found by a short scan)
+    int r = r0;
+    for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+        while (row_ptr[r + 1] <= e) ++r;
+        local += (unsigned long long)line_bytes(r, col_idx[e], vals[e]);
+    }
+    atomicAdd(&s_sum, local);
+    __syncthreads();
+    if (threadIdx.x == 0) block_bytes[blockIdx.x] = s_sum;
+}
+
+// Exclusive scan of the block totals in one CTA (blocks <= a few 10^5).
+__global__ void __launch_bounds__(1024) text_scan_kernel(unsigned long long* v, int n,
+                                                         unsigned long long base) {
+    __shared__ unsigned long long s[1024];
+    const int t = threadIdx.x;
+    const int per = (n + 1023) / 1024;
+    const int i0 = t * per, i1 = min(n, i0 + per);
+    unsigned long long acc = 0;
+    for (int i = i0; i < i1; ++i) acc += v[i];
+    s[t] = acc;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {
+        const unsigned long long a = t >= o ? s[t - o] : 0;
+        __syncthreads();
+        s[t] += a;
+        __syncthreads();
+    }
+    unsigned long long run = base + (t ? s[t - 1] : 0);
+    for (int i = i0; i < i1; ++i) {
+        const unsigned long long x = v[i];
+        v[i] = run;
+        run += x;
+    }
+    if (t == 1023) v[n] = base + s[1023];
+}
+
+// Pass 2: render each block's lines into shared memory, then copy out.
+__global__ void __launch_bounds__(256) text_write_kernel(const int32_t* row_ptr, const int32_t* col_idx,
+                                                         const float* vals, int rows,
+                                                         const unsigned long long* block_off,
+                                                         char* out) {
+    extern __shared__ unsigned char s_text[];
+    __shared__ int s_lineoff[257];
+    const int r0 = blockIdx.x * kRowsPerBlock;
+    const int r1 = min(rows, r0 + kRowsPerBlock);
+    const int e0 = row_ptr[r0], e1 = row_ptr[r1];
+    const unsigned long long gbase = block_off[blockIdx.x];
+    const unsigned long long total = block_off[blockIdx.x + 1] - gbase;
+    // Entries in chunks of 256: per-entry line length -> block scan -> render.
+    unsigned long long done = 0;  // bytes of this block already flushed
+    int staged = 0;               // bytes currently in s_text
+    int r = r0;
+    for (int c0 = e0; c0 < e1; c0 += blockDim.x) {
+        const int e = c0 + threadIdx.x;
+        char line[64];
+        int len = 0;
+        if (e < e1) {
+            while (row_ptr[r + 1] <= e) ++r;
+            len = format_u64((unsigned long long)r + 1, line);
+            line[len++] = ' ';
+            len += format_u64((unsigned long long)col_idx[e] + 1, line + len);
+            line[len++] = ' ';
+            len += format_g17(vals[e], line + len);
+            line[len++] = '\n';
+        }
+        // exclusive scan of len over the CTA
+        if (threadIdx.x == 0) s_lineoff[0] = 0;
+        __syncthreads();
+        s_lineoff[threadIdx.x + 1] = len;
+        __syncthreads();
+        for (int o = 1; o < 256; o <<= 1) {
+            const int a = threadIdx.x + 1 > o ? s_lineoff[threadIdx.x + 1 - o] : 0;
+            __syncthreads();
+            s_lineoff[threadIdx.x + 1] += a;
+            __syncthreads();
+        }
+        const int chunk = s_lineoff[256];
+        if (staged + chunk > kStageBytes) {  // flush (the CTA's bytes are contiguous in `out`)
+            for (int i = threadIdx.x; i < staged; i += blockDim.x) out[gbase + done + i] = s_text[i];
+            done += staged;
+            staged = 0;
+            __syncthreads();
+        }
+        const int off = staged + s_lineoff[threadIdx.x];
+        for (int i = 0; i < len; ++i) s_text[off + i] = line[i];
+        staged += chunk;
+        __syncthreads();
+    }
+    for (int i = threadIdx.x; i < staged; i += blockDim.x) out[gbase + done + i] = s_text[i];
+    (void)total;
+}
+
+std::once_flag g_pow5_once[64];
+cudaError_t g_pow5_err[64];
+
+cudaError_t init_pow5(int dev) {
+    std::call_once(g_pow5_once[dev & 63], [dev] {
+        unsigned long long t[62][3];
+        unsigned long long w[3] = {1, 0, 0};
+        for (int k = 0; k < 62; ++k) {
+            t[k][0] = w[0];
+            t[k][1] = w[1];
+            t[k][2] = w[2];
+            unsigned __int128 c = 0;
+            for (int i = 0; i < 3; ++i) {
+                c += (unsigned __int128)w[i] * 5u;
+                w[i] = (unsigned long long)c;
+                c >>= 64;
+            }
+        }
+        g_pow5_err[dev & 63] = cudaMemcpyToSymbol(c_pow5, t, sizeof t);
+    });
+    return g_pow5_err[dev & 63];
+}
+
+}  // namespace
+
+// Renders the entry lines of a CSR (device arrays) into `out_dev` starting at
+// byte `base`; writes the total text size (base + entry bytes) to *end.
+// `scratch` holds (rows / 64 + 2) unsigned long longs.
+cudaError_t render_entries(const int32_t* row_ptr, const int32_t* col_idx, const float* vals, int rows,
+                           unsigned long long* scratch, char* out_dev, unsigned long long base,
+                           cudaStream_t st, bool size_only) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaError_t e = init_pow5(dev);
+    if (e != cudaSuccess) return e;
+    const int blocks = (rows + kRowsPerBlock - 1) / kRowsPerBlock;
+    text_size_kernel<<<blocks, 256, 0, st>>>(row_ptr, col_idx, vals, rows, scratch);
+    text_scan_kernel<<<1, 1024, 0, st>>>(scratch, blocks, base);
+    if (size_only) return cudaGetLastError();
+    static bool attr[64] = {};
+    if (!attr[dev & 63]) {
+        e = cudaFuncSetAttribute(text_write_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kStageBytes + 256 * 64);
+        if (e != cudaSuccess) return e;
+        attr[dev & 63] = true;
+    }
+    text_write_kernel<<<blocks, 256, kStageBytes + 256 * 64, st>>>(row_ptr, col_idx, vals, rows, scratch,
+                                                                  out_dev);
+    return cudaGetLastError();
+}
+
+int text_rows_per_block() { return kRowsPerBlock; }
+
+}  // namespace spb

@@ -1,0 +1,180 @@
+"""DenseNet121 layer-table bench on the GPU -- the paper's Table 1 protocol
+(reference harness inc/bench.hpp:174-349).
+
+Per layer of ``densenet121_layers()`` (123 single-channel shapes, pooling
+layers run as random-kernel convolutions as the paper does), the transform is
+built once on the device (build time reported separately, as
+``build_time_us``) and the apply is timed over ``trials`` trials:
+
+* ``device``: one SpMV on a device-resident image, timed as a CUDA graph of
+  ``graph_reps`` back-to-back launches replayed per trial (launch overhead
+  amortised the way a GPU-resident network would see it);
+* ``host``: the reference's call shape -- an fp32 image in pinned host memory,
+  H2D + SpMV + D2H through the C ABI (``spconv_convolve_host``) per trial.
+
+Each layer's device output is cross-checked before timing against a float64
+direct convolution (the reference's ``direct_conv``, inc/reference.hpp:41-61,
+restated in numpy) within the north-star tolerance
+|y - ref| <= 1e-5 * sum|w x|, as the reference harness cross-checks its
+methods (inc/bench.hpp:218-233).  Totals are sums of per-layer means and the
+root-sum-square of per-layer SEMs (inc/bench.hpp:284-349).  A whole-network
+graph (all 123 layers back to back) gives the end-to-end pass time.
+"""
+from __future__ import annotations
+
+import math
+import statistics
+import time
+from typing import Dict, List
+
+import numpy as np
+
+from .layers import LayerConfig, densenet121_layers
+
+TOL = 1e-5
+
+
+def direct_conv_f64(a: np.ndarray, w: np.ndarray, s: int, p: int):
+    """Padded, strided correlation in float64 plus sum|w x| per output."""
+    m, n = a.shape
+    k = w.shape[0]
+    ap = np.zeros((m + 2 * p, n + 2 * p))
+    ap[p:p + m, p:p + n] = a
+    mo, no = (m + 2 * p - k) // s + 1, (n + 2 * p - k) // s + 1
+    out = np.zeros((mo, no))
+    mag = np.zeros((mo, no))
+    for j in range(k):
+        for i in range(k):
+            win = ap[j:j + s * (mo - 1) + 1:s, i:i + s * (no - 1) + 1:s]
+            out += w[j, i] * win
+            mag += abs(w[j, i]) * np.abs(win)
+    return out, mag
+
+
+def _stats(us: List[float]):
+    mean = statistics.fmean(us)
+    sem = statistics.stdev(us) / math.sqrt(len(us)) if len(us) > 1 else 0.0
+    return mean, sem
+
+
+def run_table_bench(layers: List[LayerConfig] = None, trials: int = 100, warmup: int = 10,
+                    graph_reps: int = 20, seed: int = 42, device: int = 0) -> Dict:
+    import torch
+
+    from . import ConvSpec, Kernel, build_transform, spmv
+    from . import lib, _check
+
+    layers = layers or densenet121_layers()
+    dev = torch.device("cuda", device)
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.Stream(dev)
+    rows = []
+    graphs_all = []
+    keep = []
+    with torch.cuda.stream(stream):
+        for li, L in enumerate(layers):
+            rng = np.random.default_rng([seed, li])
+            a = rng.standard_normal((L.m, L.n)).astype(np.float32)
+            w = rng.standard_normal((L.k, L.k)).astype(np.float32)
+            spec = ConvSpec(L.m, L.n, L.k, L.s, L.p)
+            # one-time build, device-timed (a GPU sleep covers the host enqueue)
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda._sleep(1_000_000)
+            e0.record(stream)
+            t = build_transform(Kernel(L.k, w.reshape(-1)), spec, device=device, stream=stream)
+            e1.record(stream)
+            x = torch.from_numpy(a.reshape(-1)).to(dev)
+            y = torch.empty(t.rows, dtype=torch.float32, device=dev)
+            spmv(t, x, y, stream=stream)
+            torch.cuda.synchronize(dev)
+            build_us = e0.elapsed_time(e1) * 1e3
+            # cross-check (inc/bench.hpp:218-233)
+            ref, mag = direct_conv_f64(a.astype(np.float64), w.astype(np.float64), L.s, L.p)
+            got = y.cpu().numpy().astype(np.float64).reshape(ref.shape)
+            dev_max = float(np.max(np.abs(got - ref) - TOL * mag - 1e-30))
+            if dev_max > 0:
+                raise RuntimeError(f"cross-check failed for layer '{L.name}'")
+            kernel_name = t.last_kernel
+            # device-resident: graph of graph_reps launches, replayed per trial
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                for _ in range(graph_reps):
+                    spmv(t, x, y, stream=stream)
+            for _ in range(warmup):
+                g.replay()
+            torch.cuda.synchronize(dev)
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                  for _ in range(trials)]
+            for i in range(trials):
+                ev[i][0].record(stream)
+                g.replay()
+                ev[i][1].record(stream)
+            torch.cuda.synchronize(dev)
+            dev_us = [a_.elapsed_time(b_) * 1e3 / graph_reps for a_, b_ in ev]
+            # host call shape: pinned fp32 image in, fp32 out (H2D + SpMV + D2H)
+            xh = torch.from_numpy(a.reshape(1, -1)).pin_memory()
+            yh = torch.empty(1, t.rows, dtype=torch.float32).pin_memory()
+            for _ in range(warmup):
+                _check(lib.spconv_convolve_host(t._h, xh.data_ptr(), yh.data_ptr(), 1))
+            host_us = []
+            for _ in range(trials):
+                h0 = time.perf_counter()
+                _check(lib.spconv_convolve_host(t._h, xh.data_ptr(), yh.data_ptr(), 1))
+                host_us.append((time.perf_counter() - h0) * 1e6)
+            dm, ds = _stats(dev_us)
+            hm, hs = _stats(host_us)
+            rows.append(dict(layer=L.name, m=L.m, n=L.n, k=L.k, s=L.s, p=L.p, nnz=t.nnz,
+                             kernel=kernel_name, device_mean_us=dm, device_sem_us=ds,
+                             host_mean_us=hm, host_sem_us=hs, build_time_us=build_us))
+            keep.append((t, x, y, g))
+            graphs_all.append((t, x, y))
+        # whole network: every layer's SpMV back to back in one graph
+        gnet = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gnet, stream=stream):
+            for t, x, y in graphs_all:
+                spmv(t, x, y, stream=stream)
+        for _ in range(warmup):
+            gnet.replay()
+        torch.cuda.synchronize(dev)
+        net_us = []
+        for _ in range(trials):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            gnet.replay()
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            net_us.append(e0.elapsed_time(e1) * 1e3)
+    for t, *_ in keep:
+        t.close()
+    tot = lambda key: sum(r[key] for r in rows)  # noqa: E731
+    rss = lambda key: math.sqrt(sum(r[key] ** 2 for r in rows))  # noqa: E731
+    nm, ns = _stats(net_us)
+    return {
+        "layers": rows,
+        "total_device_us": tot("device_mean_us"), "total_device_sem_us": rss("device_sem_us"),
+        "total_host_us": tot("host_mean_us"), "total_host_sem_us": rss("host_sem_us"),
+        "total_build_us": tot("build_time_us"),
+        "network_graph_us": nm, "network_graph_sem_us": ns,
+        "trials": trials, "warmup": warmup, "graph_reps": graph_reps,
+    }
+
+
+def markdown(res: Dict, ref: Dict = None) -> str:
+    """Per-layer table in the reference report's shape (inc/bench.hpp:318-349)."""
+    out = ["| layer | m | n | k | s | p | nnz | device mean us | sem | host mean us | sem | build us |"
+           + (" reference CSR-SpMV us |" if ref else ""),
+           "|---|---|---|---|---|---|---|---|---|---|---|---|" + ("---|" if ref else "")]
+    for i, r in enumerate(res["layers"]):
+        line = (f"| {r['layer']} | {r['m']} | {r['n']} | {r['k']} | {r['s']} | {r['p']} | {r['nnz']} | "
+                f"{r['device_mean_us']:.3f} | {r['device_sem_us']:.3f} | {r['host_mean_us']:.3f} | "
+                f"{r['host_sem_us']:.3f} | {r['build_time_us']:.1f} |")
+        if ref:
+            line += f" {ref['layers'][i]['CSR-SpMV'][0]:.3f} |"
+        out.append(line)
+    line = (f"| TOTAL | | | | | | | {res['total_device_us']:.3f} | {res['total_device_sem_us']:.3f} | "
+            f"{res['total_host_us']:.3f} | {res['total_host_sem_us']:.3f} | {res['total_build_us']:.1f} |")
+    if ref:
+        line += f" {ref['total_csr_us']:.3f} |"
+    out.append(line)
+    return "\n".join(out) + "\n"

@@ -147,6 +147,45 @@ def main():
         count += 1
     js["sweep9"] = dict(specs=count, digest=h.hexdigest())
 
+    # Transform text (write_transform, inc/conv.hpp:221-224): digests of the
+    # reference's bytes for built transforms, kernels given as fp32 bit patterns.
+    text = []
+    tcases = [(0, (64, 64, 3, 1, 1), "normal"), (4, (257, 193, 3, 2, 1), "normal"),
+              (4, (257, 193, 5, 3, 4), "zerotap"), (4, (257, 193, 11, 1, 10), "normal"),
+              (4, (257, 193, 1, 1, 1), "normal"), (6, (20, 17, 3, 1, 1), "nan")]
+    for cfg, (m, n, k, s, p), variant in tcases:
+        kern, _ = problem(ref, cfg, m, n, k)
+        if variant == "zerotap":
+            kern = zero_tap_kernel(ref, k, ref.derive_seed(ref.derive_seed(BASE_SEED, cfg), 99))
+        if variant == "nan":
+            kern = kern.copy()
+            kern[0] = np.nan
+            kern[4] = -np.nan
+        t = ref.build(m, n, k, s, p, kern)
+        data = t.write_text()
+        text.append(dict(spec=[m, n, k, s, p], variant=variant,
+                         kernel_bits=[int(b) for b in np.asarray(kern, np.float32).view(np.uint32)],
+                         bytes=len(data), sha=hashlib.sha256(data).hexdigest()))
+    js["text"] = text
+
+    # %.17g of fp32 values widened to double, as the reference prints them
+    # (format_value, inc/grid.hpp:54-59, via write_sparse of a 1 x N matrix).
+    rng = np.random.default_rng(2411)
+    special = np.array([0.0, -0.0, 1.0, -1.0, 0.1, 1e-4, 9.99999e-5, 1e-5, 1e16, 1e17, 9.9999998e16,
+                        1.0000001e17, 123456789.0, 3.4028235e38, -3.4028235e38, 1.17549435e-38,
+                        1.4e-45, -1.4e-45, 2.0 ** -126, 2.0 ** 24, 2.0 ** 57, 0.5, 0.25, 1e38, 1e-38,
+                        np.inf, -np.inf, np.nan, -np.nan, 16777217.0, 1e-45 * 3, 5e-324 * 0],
+                       dtype=np.float32)
+    bits = np.concatenate([special.view(np.uint32),
+                           rng.integers(0, 2 ** 32, 3000, dtype=np.uint64).astype(np.uint32),
+                           rng.integers(0, 2 ** 23, 300, dtype=np.uint64).astype(np.uint32),  # subnormals
+                           (np.float32(10.0) ** np.arange(-45, 39, dtype=np.float32)).view(np.uint32)])
+    vals = bits.view(np.float32).astype(np.float64)
+    N = vals.size
+    data = ref.write_sparse_csr(1, N, np.array([0, N]), np.arange(N), vals).decode()
+    lines = data.split("\n")[2:2 + N]
+    js["g17"] = [[int(b), ln.split(" ")[2]] for b, ln in zip(bits, lines)]
+
     # The reference's own self-test summary (inc/verify.hpp:59-169), small grid.
     js["run_verification_6x1"] = ref.run_verification(6, 1)
 

@@ -314,6 +314,12 @@ def test_generic_csr_upload(sp, orc, torch_cuda):
     want = orc.spmm_f32_fma(ptr, idx, val, X)
     assert np.array_equal(bits(run_spmm(torch_cuda, sp, t, X)), bits(want))
     assert np.array_equal(t.export()[1], idx)
+    for b in (1, 2):  # latency kernel (warp per 32 rows) on ragged rows, empty rows included
+        for path in (None, "spmv_plain"):
+            assert np.array_equal(bits(run_spmm(torch_cuda, sp, t, X[:b], path)), bits(want[:b])), (b, path)
+        assert t.last_kernel == "csr_spmv_unrolled"
+        assert np.array_equal(bits(run_spmm(torch_cuda, sp, t, X[:b])), bits(want[:b]))
+        assert t.last_kernel == "csr_spmv_warp"
 
 
 def test_end_to_end_host_path(sp, orc, torch_cuda):
@@ -400,9 +406,9 @@ def test_band_concurrent_streams(sp, orc, torch_cuda):
 
 @pytest.mark.parametrize("skew", [1, -1, 3])
 def test_spmv_spec_mispredicted_rows(sp, orc, torch_cuda, skew):
-    """The speculative SpMV's prediction never decides the result: with the
-    predicted row starts deliberately skewed (test hook), every row takes the
-    mismatch path and the output is still bit-exact."""
+    """The latency SpMV's closed-form run prediction never decides the result:
+    with the predicted run bounds deliberately skewed (test hook), every warp
+    takes the reload path and the output is still bit-exact."""
     spec = (64, 48, 5, 2, 2)
     kern, X = problem(orc, 13, 64, 48, 5, batch=2)
     t = build(sp, spec, kern)
@@ -412,5 +418,5 @@ def test_spmv_spec_mispredicted_rows(sp, orc, torch_cuda, skew):
         Y = run_spmm(torch_cuda, sp, t, X)
     finally:
         del os.environ["SPCONV_B200_SPEC_SKEW"]
-    assert t.last_kernel == "conv_spmv_spec"
+    assert t.last_kernel == "csr_spmv_warp<spec>"
     assert np.array_equal(bits(Y), bits(want))
