@@ -97,17 +97,31 @@ struct BandCfg {
 };
 
 // ---------------------------------------------------------------------------
-// 1. Band check: one warp per segment.
+// 1. Band check: one warp per segment, everything it reads staged by bulk
+//    copies issued before any of it is needed.
+//
+//    The segment's expected CSR footprint is closed-form (Theorem 2.1 prefix
+//    sums): its rows start at S0 = CX(x) * SY + cx(x) * CY(y0) and hold
+//    L = cx(x) * (CY(y0 + nr) - CY(y0)) entries, CX / CY being the running
+//    per-slide tap counts.  So one elected lane issues three 1-D bulk copies
+//    (row_ptr[r0 .. r0+nr], col_idx and vals over [S0, S0+L)) with no
+//    dependent global load, and the warp then checks every row -- interior
+//    rows with a fully unrolled k*k compare, clipped (border) rows with the
+//    same compare over their tap range -- out of shared memory.  Rows of a
+//    segment start at cx * (CY(y) - CY(y0)) inside the run.  If every
+//    row_ptr matches its prediction and every entry matches the pattern, the
+//    segment's rows are exactly the conv rows.  Result: one byte per segment.
 // ---------------------------------------------------------------------------
 template <int K, int S, int TW>
 struct CheckCfg {
     static constexpr int KK = K * K;
-    static constexpr int RUN = TW * KK;                    // entries of an interior segment
-    static constexpr int BUFW = (RUN + 3 + 3) / 4 * 4;     // 16-byte aligned superset
-    static constexpr size_t WARP_BYTES = 2ull * 2 * BUFW * 4;  // 2 buffers x (cols + vals)
-    static constexpr int WARPS = (int)(200 * 1024 / WARP_BYTES) < 8 ? (int)(200 * 1024 / WARP_BYTES) : 8;
+    static constexpr int RUN = TW * KK;                    // entries of a full segment
+    static constexpr int BUFW = (RUN + 3 + 3) / 4 * 4;     // + alignment slack (16-byte bulk units)
+    static constexpr int RPW = (TW + 1 + 3 + 3) / 4 * 4;   // row_ptr words
+    static constexpr size_t WARP_BYTES = (size_t)(RPW + 2 * BUFW) * 4;
+    static constexpr int WARPS = 4;
     static constexpr size_t SMEM = 128 + (size_t)WARPS * WARP_BYTES;
-    static_assert(WARPS >= 1, "segment too large for shared memory");
+    static_assert(SMEM <= 200 * 1024, "segment too large for shared memory");
 };
 
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -118,159 +132,112 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
+// Sum over slides x' < x of the taps landing inside [0, dim): CX(x) / CY(y).
+template <int K, int S>
+__device__ __forceinline__ int cum_taps(int x, int dim, int p) {
+    int c = 0;
+#pragma unroll
+    for (int j = 0; j < K; ++j) c += slides_before(x, j, dim, S, p);
+    return c;
+}
+
 template <int K, int S, int TW>
-__global__ void __launch_bounds__(CheckCfg<K, S, TW>::WARPS * 32, 1) conv_band_check(const BandParams P) {
+__global__ void __launch_bounds__(CheckCfg<K, S, TW>::WARPS * 32) conv_band_check(const BandParams P) {
     using C = CheckCfg<K, S, TW>;
     constexpr int KK = K * K;
     constexpr int RPL = TW / 32;  // rows per lane
     extern __shared__ __align__(128) unsigned char smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + 2 * warp;
-    int* buf = reinterpret_cast<int*>(smem + 128 + (size_t)warp * C::WARP_BYTES);
-    if (lane == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
-        mbar_fence_init();
-    }
-    __syncwarp();
-    __shared__ uint32_t s_w[KK];  // taps for the border walk (runtime-indexed)
+    __shared__ uint32_t s_w[KK];  // taps, runtime-indexed (clipped rows)
     for (int q = threadIdx.x; q < KK; q += blockDim.x) s_w[q] = __float_as_uint(__ldg(P.taps + q));
-    __syncthreads();
-    uint32_t w[KK];  // taps for the interior check (compile-time indexed)
+
+    const long long seg = (long long)blockIdx.x * C::WARPS + warp;
+    const bool live = seg < (long long)P.mo * P.tiles_y;  // warp-uniform
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem) + warp;
+    int* rp = reinterpret_cast<int*>(smem + 128 + (size_t)warp * C::WARP_BYTES);
+    int* cb = rp + C::RPW;
+    uint32_t* vb = reinterpret_cast<uint32_t*>(cb + C::BUFW);
+
+    int x = 0, y0 = 0, nr = 0, r0 = 0, jlo = 0, jhi = 0, cy0 = 0, L = 0;
+    long long S0 = 0;
+    bool valid = false;
+    if (live) {
+        x = (int)(seg / P.tiles_y);
+        y0 = (int)(seg - (long long)x * P.tiles_y) * TW;
+        nr = min(TW, P.no - y0);
+        r0 = x * P.no + y0;
+        tap_range_dev(x, P.m, K, S, P.p, jlo, jhi);
+        cy0 = cum_taps<K, S>(y0, P.n, P.p);
+        S0 = (long long)cum_taps<K, S>(x, P.m, P.p) * P.sy + (long long)(jhi - jlo) * cy0;
+        L = (jhi - jlo) * (cum_taps<K, S>(y0 + nr, P.n, P.p) - cy0);
+        valid = S0 + L <= (long long)P.nnz;  // (zero taps: the prediction runs past the end)
+        if (lane == 0) {
+            mbar_init(bar, 1);
+            mbar_fence_init();
+            if (valid) {
+                const int rbase = r0 & ~3;
+                const uint32_t rwords = (uint32_t)((r0 + nr + 1 - rbase + 3) & ~3);
+                const long long ebase = S0 & ~3ll;
+                const uint32_t ewords = (uint32_t)((S0 + L - ebase + 3) & ~3ll);
+                mbar_expect_tx(bar, 4u * (rwords + 2u * ewords));
+                bulk_g2s(rp, P.row_ptr + rbase, 4u * rwords, bar);
+                if (ewords) {
+                    bulk_g2s(cb, P.col_idx + ebase, 4u * ewords, bar);
+                    bulk_g2s(vb, P.vals + ebase, 4u * ewords, bar);
+                }
+            }
+        }
+    }
+    __syncthreads();  // s_w (and the barrier inits) visible block-wide
+    if (!live) return;
+    if (!valid) {
+        if (lane == 0) P.seg_ok[seg] = 0;
+        return;
+    }
+    uint32_t w[KK];  // taps, compile-time indexed (full rows)
 #pragma unroll
     for (int q = 0; q < KK; ++q) w[q] = s_w[q];
-
-    // Each warp owns a contiguous range of segments (consecutive memory, and
-    // every warp meets its share of border segments).
-    const long long nseg_all = (long long)P.mo * P.tiles_y;
-    const long long nw = (long long)gridDim.x * C::WARPS;
-    const long long gw = (long long)blockIdx.x * C::WARPS + warp;
-    const long long seg_lo = nseg_all * gw / nw, nseg = nseg_all * (gw + 1) / nw;
-    const long long stride = 1;
-
-    // Segment geometry + closed-form start (dense taps): rows before (x, y0)
-    // = CX(x) * SY + cx(x) * CY(y0)  (Theorem 2.1 prefix sums).
-    struct Seg {
-        int x, y0, nr, r0, jlo, jhi, S0;
-        bool full;
-    };
-    auto geom = [&](long long seg) {
-        Seg g;
-        g.x = (int)(seg / P.tiles_y);
-        const int ty = (int)(seg - (long long)g.x * P.tiles_y);
-        g.y0 = ty * TW;
-        g.nr = min(TW, P.no - g.y0);
-        g.r0 = g.x * P.no + g.y0;
-        tap_range_dev(g.x, P.m, K, S, P.p, g.jlo, g.jhi);
-        int cxb = 0, cyb = 0;
+    const int cx = jhi - jlo;
+    // per-row predictions while the copies are in flight
+    int off[RPL];
+    bool ok = true;
 #pragma unroll
-        for (int j = 0; j < K; ++j) {
-            cxb += slides_before(g.x, j, P.m, S, P.p);
-            cyb += slides_before(g.y0, j, P.n, S, P.p);
-        }
-        g.S0 = cxb * P.sy + (g.jhi - g.jlo) * cyb;
-        // interior: every row of the segment stores all K*K taps
-        const int ylast = g.y0 + g.nr - 1;
-        g.full = g.jlo == 0 && g.jhi == K && S * g.y0 - P.p >= 0 && S * ylast - P.p + K <= P.n &&
-                 (long long)g.S0 + g.nr * KK <= (long long)P.nnz;  // (zero taps: prediction past the end)
-        return g;
-    };
-    auto issue = [&](const Seg& g, int b) {  // lane 0: bulk-copy the run into buffer b
-        const int abase = g.S0 & ~3;
-        const uint32_t bytes = (uint32_t)(((g.S0 + g.nr * KK - abase + 3) & ~3) * 4);
-        int* dst = buf + b * 2 * C::BUFW;
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(&bars[b], 2 * bytes);
-        bulk_g2s(dst, P.col_idx + abase, bytes, &bars[b]);
-        bulk_g2s(dst + C::BUFW, P.vals + abase, bytes, &bars[b]);
-    };
-
-    long long seg = seg_lo;
-    if (seg >= nseg) return;
-    Seg cur = geom(seg);
-    if (cur.full && lane == 0) issue(cur, 0);
-    uint32_t phases = 0u;  // bit b: parity of buffer b's next completion
-    for (int i = 0; seg < nseg; ++i, seg += stride) {
-        const int b = i & 1;
-        // row_ptr of this segment (nr + 1 values)
-        int a_row[RPL];
+    for (int q = 0; q < RPL; ++q) off[q] = cx * (cum_taps<K, S>(y0 + lane + 32 * q, P.n, P.p) - cy0);
+    mbar_wait(bar, 0);
+    const int* rps = rp + (r0 & 3);
+    const int* cbs = cb + (int)(S0 & 3);
+    const uint32_t* vbs = vb + (int)(S0 & 3);
+    const int S0i = (int)S0;  // S0 + L <= nnz < 2^31 here
+    uint32_t bad = 0;
 #pragma unroll
-        for (int q = 0; q < RPL; ++q) {
-            const int l = lane + 32 * q;
-            a_row[q] = l < cur.nr ? __ldg(P.row_ptr + cur.r0 + l) : 0;
-        }
-        const int a_end = __ldg(P.row_ptr + cur.r0 + cur.nr);
-        // prefetch the next segment's run into the other buffer
-        Seg nxt{};
-        const bool has_next = seg + stride < nseg;
-        if (has_next) {
-            nxt = geom(seg + stride);
-            __syncwarp();  // this warp finished reading buffer b^1 (segment i-1)
-            if (nxt.full && lane == 0) issue(nxt, b ^ 1);
-        }
-        bool ok = true;
-        if (cur.full) {
+    for (int q = 0; q < RPL; ++q) {
+        const int l = lane + 32 * q;
+        if (l < nr) {
+            const int y = y0 + l;
+            ok &= rps[l] == S0i + off[q];
+            if (l == nr - 1) ok &= rps[nr] == S0i + L;
+            int ilo, ihi;
+            tap_range_dev(y, P.n, K, S, P.p, ilo, ihi);
+            const int rb = (S * x - P.p) * P.n + (S * y - P.p);
+            const int* cl = cbs + off[q];
+            const uint32_t* vl = vbs + off[q];
+            if (cx == K && ilo == 0 && ihi == K) {
 #pragma unroll
-            for (int q = 0; q < RPL; ++q) {
-                const int l = lane + 32 * q;
-                if (l < cur.nr) ok &= a_row[q] == cur.S0 + l * KK;
-            }
-            ok &= a_end == cur.S0 + cur.nr * KK;
-            mbar_wait(&bars[b], (phases >> b) & 1u);
-            phases ^= 1u << b;
-            const int* cb = buf + b * 2 * C::BUFW + (cur.S0 & 3);
-            const uint32_t* vb = reinterpret_cast<const uint32_t*>(cb + C::BUFW);
-            uint32_t bad = 0;
+                for (int j = 0; j < K; ++j)
 #pragma unroll
-            for (int q = 0; q < RPL; ++q) {
-                const int l = lane + 32 * q;
-                if (l < cur.nr) {
-                    const int rb = (S * cur.x - P.p) * P.n + S * (cur.y0 + l) - P.p;
-                    const int* cl = cb + l * KK;
-                    const uint32_t* vl = vb + l * KK;
-#pragma unroll
-                    for (int j = 0; j < K; ++j)
-#pragma unroll
-                        for (int ii = 0; ii < K; ++ii)
-                            bad |= (uint32_t)(cl[j * K + ii] - (rb + j * P.n + ii)) | (vl[j * K + ii] ^ w[j * K + ii]);
-                }
-            }
-            ok &= bad == 0u;
-        } else {
-            // Border segment: each lane walks its own rows from global memory,
-            // every (col, val) load of a row in flight at once.
-#pragma unroll
-            for (int q = 0; q < RPL; ++q) {
-                const int l = lane + 32 * q;
-                if (l < cur.nr) {
-                    const int y = cur.y0 + l;
-                    int ilo, ihi;
-                    tap_range_dev(y, P.n, K, S, P.p, ilo, ihi);
-                    const int bnd = __ldg(P.row_ptr + cur.r0 + l + 1);
-                    if (bnd - a_row[q] != (cur.jhi - cur.jlo) * (ihi - ilo)) {
-                        ok = false;
-                        continue;
-                    }
-                    const int rb = (S * cur.x - P.p) * P.n + (S * y - P.p);
-                    int e = a_row[q];
-                    uint32_t bad = 0;
-#pragma unroll
-                    for (int j = 0; j < K; ++j)
-#pragma unroll
-                        for (int ii = 0; ii < K; ++ii)
-                            if (j >= cur.jlo && j < cur.jhi && ii >= ilo && ii < ihi) {
-                                bad |= (uint32_t)(__ldg(P.col_idx + e) - (rb + j * P.n + ii)) |
-                                       (__float_as_uint(__ldg(P.vals + e)) ^ w[j * K + ii]);
-                                ++e;
-                            }
-                    ok &= bad == 0u;
-                }
+                    for (int ii = 0; ii < K; ++ii)
+                        bad |= (uint32_t)(cl[j * K + ii] - (rb + j * P.n + ii)) | (vl[j * K + ii] ^ w[j * K + ii]);
+            } else {
+                int e = 0;
+                for (int j = jlo; j < jhi; ++j)
+                    for (int ii = ilo; ii < ihi; ++ii, ++e)
+                        bad |= (uint32_t)(cl[e] - (rb + j * P.n + ii)) | (vl[e] ^ s_w[j * K + ii]);
             }
         }
-        ok = __all_sync(0xffffffffu, ok);
-        if (lane == 0) P.seg_ok[seg] = ok ? 1 : 0;
-        cur = nxt;
     }
+    ok &= bad == 0u;
+    ok = __all_sync(0xffffffffu, ok);
+    if (lane == 0) P.seg_ok[seg] = ok ? 1 : 0;
 }
 
 // ---------------------------------------------------------------------------
@@ -437,10 +404,15 @@ __global__ void __launch_bounds__(BandCfg<K, S, V, CPT, TH, STAGES, DELTA>::THRE
                     float acc = 0.0f;
                     for (int e = __ldg(P.row_ptr + r); e < e1; ++e) {
                         const int col = __ldg(P.col_idx + e);
+                        if ((unsigned)col >= (unsigned)(P.m * P.n)) __trap();  // not a CSR of this shape
                         const int ri = col / P.n;
                         const int dr = ri - wr0, dc = col - ri * P.n - wc0;
-                        if ((unsigned)dr >= (unsigned)C::WR || (unsigned)dc >= (unsigned)C::WC) __trap();
-                        acc = fmaf(__ldg(P.vals + e), xw[dr * C::WC + dc], acc);
+                        // a column outside the staged window (a row that is not a conv
+                        // row) is read from the image itself
+                        const float xv = ((unsigned)dr < (unsigned)C::WR && (unsigned)dc < (unsigned)C::WC)
+                                             ? xw[dr * C::WC + dc]
+                                             : __ldg(P.X + (long long)img * P.ldx + col);
+                        acc = fmaf(__ldg(P.vals + e), xv, acc);
                     }
                     __stcs(ybase + r, acc);
                 }
@@ -495,22 +467,19 @@ cudaError_t run_delta(int delta, const BandParams& bp, const CUtensorMap* tmap, 
 
 template <int K, int S, int TW>
 cudaError_t run_check(const BandParams& bp, cudaStream_t st, int sms) {
+    (void)sms;
     using C = CheckCfg<K, S, TW>;
     auto kern = conv_band_check<K, S, TW>;
-    static int occ[64] = {};
+    static bool init[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
-    if (!occ[dev & 63]) {
+    if (!init[dev & 63]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
         if (e != cudaSuccess) return e;
-        int o = 0;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, C::WARPS * 32, C::SMEM);
-        if (e != cudaSuccess) return e;
-        occ[dev & 63] = std::max(o, 1);
+        init[dev & 63] = true;
     }
     const long long segs = (long long)bp.mo * bp.tiles_y;
-    const long long want = (segs + C::WARPS - 1) / C::WARPS;
-    const long long grid = std::min<long long>(want, (long long)occ[dev & 63] * sms);
+    const long long grid = (segs + C::WARPS - 1) / C::WARPS;
     kern<<<(unsigned)grid, C::WARPS * 32, C::SMEM, st>>>(bp);
     return cudaGetLastError();
 }

@@ -1,11 +1,10 @@
 #!/bin/bash
-# quick GPU iteration: gpu tests, bench c3 (+c2,c4), launch lists, ncu full of the c3/c4 SpMM
+# quick iteration: gpu parity tests + A/B timings (+ optional ncu of one kernel: NCU_K regex, NCU_ARGS bench args)
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out
-rm -f gpurun_out/status.txt
-timeout 1200 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/status.txt
-timeout 600 python bench.py --steps 100 --warmup 5 --no-cpu-baseline > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/status.txt
-for c in 2 4; do timeout 600 python bench.py --config $c --steps 30 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c$c.log 2>&1; echo "bench$c rc=$?" >> gpurun_out/status.txt; done
-for c in 3 4; do timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c$c.csv python bench.py --config $c --batch $([ $c = 4 ] && echo 8 || echo 0) --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 2 > gpurun_out/ncu_launch_c$c.log 2>&1; echo "ncu-l$c rc=$?" >> gpurun_out/status.txt; done
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:conv_spmm -s 3 -c 1 -o gpurun_out/prof_spmm python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 2 > gpurun_out/ncu_full_spmm.log 2>&1; echo "ncu3 rc=$?" >> gpurun_out/status.txt
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:conv_spmm -s 3 -c 1 -o gpurun_out/prof_spmm_c4 python bench.py --config 4 --batch 8 --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 2 > gpurun_out/ncu_full_spmm_c4.log 2>&1; echo "ncu4 rc=$?" >> gpurun_out/status.txt
+rm -f gpurun_out/status.txt gpurun_out/exp.txt
+timeout 600 python -m pytest tests -m gpu -q -x ${PYTEST_K:+-k "$PYTEST_K"} > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/status.txt
+timeout 900 python scripts/exp_run.py gpurun_out/exp.txt "$@" > /dev/null 2>&1; echo "exp rc=$?" >> gpurun_out/status.txt
+if [ -n "$NCU_K" ]; then
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:"$NCU_K" -s 4 -c 2 -o gpurun_out/prof_quick python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-secondary --e2e-steps 1 $NCU_ARGS > gpurun_out/ncu_quick.log 2>&1; echo "ncu rc=$?" >> gpurun_out/status.txt
+fi

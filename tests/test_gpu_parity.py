@@ -420,3 +420,49 @@ def test_spmv_spec_mispredicted_rows(sp, orc, torch_cuda, skew):
         del os.environ["SPCONV_B200_SPEC_SKEW"]
     assert t.last_kernel == "csr_spmv_warp<spec>"
     assert np.array_equal(bits(Y), bits(want))
+
+
+class _DevArray:
+    """A raw device pointer seen as a 1-D CUDA array (test access to a handle's arrays)."""
+
+    def __init__(self, ptr, n, typestr):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3}
+
+
+@pytest.mark.parametrize("spec", [(256, 256, 3, 1, 1), (300, 260, 7, 2, 3)])
+def test_band_check_reads_the_matrix(sp, orc, torch_cuda, spec):
+    """The band path re-reads T on every call: entries altered in device memory
+    after the build (a value, a column moved far outside its tile's input
+    window, a column moved to an earlier image row) are picked up by the next
+    spmm -- the affected segments fail the check and take the per-entry loop --
+    and the output is bit-exact vs the oracle on the altered CSR."""
+    m, n, k = spec[:3]
+    kern, X = problem(orc, 14, m, n, k, batch=6)
+    t = build(sp, spec, kern)
+    ptr, idx, val = native_copy(t)
+    clean = run_spmm(torch_cuda, sp, t, X)
+    assert np.array_equal(bits(clean), bits(orc.spmm_native(ptr, idx, val, X)))
+    _, ci, cv = t.device_ptrs()
+    dci = torch_cuda.as_tensor(_DevArray(ci, t.nnz, "<i4"), device="cuda")
+    dcv = torch_cuda.as_tensor(_DevArray(cv, t.nnz, "<f4"), device="cuda")
+    no = sp.ConvSpec(*spec).n_out
+    r1 = (t.rows // 2) + no // 2           # interior rows
+    r2 = (t.rows // 3) + 5
+    r3 = (2 * t.rows // 3) + no // 3
+    e_last = int(ptr[r1 + 1]) - 1          # last entry of r1 -> 40 image rows further down
+    e_first = int(ptr[r2])                 # first entry of r2 -> 40 image rows up
+    e_val = int(ptr[r3]) + 2
+    idx[e_last] += 40 * n
+    idx[e_first] -= 40 * n
+    val[e_val] = np.float32(val[e_val] * 3.0)
+    assert 0 <= idx[e_first] and idx[e_last] < m * n
+    dci[e_last] = int(idx[e_last])
+    dci[e_first] = int(idx[e_first])
+    dcv[e_val] = float(val[e_val])
+    torch_cuda.cuda.synchronize()
+    Y = run_spmm(torch_cuda, sp, t, X)
+    assert t.last_kernel == "conv_band_check+conv_spmm_band"
+    want = orc.spmm_native(ptr, idx, val, X)
+    assert not np.array_equal(bits(want), bits(clean))
+    assert np.array_equal(bits(Y), bits(want))
