@@ -95,15 +95,14 @@ inline Transform build_transform(const Kernel& kern, const ConvSpec& spec,
                                  Layout layout = Layout::CSR,
                                  TransformRoute route = TransformRoute::Spgemm) {
     (void)route;  // both reference routes yield the identical matrix
-    if (layout != Layout::CSR)
-        throw std::invalid_argument("build_transform: the device path stores CSR only");
     if (kern.k != spec.k)
         throw std::invalid_argument("build_conv_matrix: kernel side " + std::to_string(kern.k) +
                                     " does not match spec " + spec.str());
     std::vector<float> taps(kern.values.begin(), kern.values.end());
     spconv_csr* h = nullptr;
-    detail::check(spconv_build_csr(spec.m, spec.n, spec.k, spec.s, spec.p, taps.data(),
-                                   detail::default_device(), nullptr, &h));
+    detail::check(spconv_build_transform(spec.m, spec.n, spec.k, spec.s, spec.p, taps.data(),
+                                         layout == Layout::CSR ? 0 : 1, detail::default_device(),
+                                         nullptr, &h));
     return Transform{spec, SparseMatrix(h)};
 }
 

@@ -1,9 +1,11 @@
-// Drop-in replacement for the CSR part of the reference's spconv/sparse.hpp
-// (inc/sparse.hpp:24-30, 77-140, 209-265).  A SparseMatrix here is a handle on
-// a DEVICE-resident CSR (int32 indices, fp32 values) built by libspconv_b200;
-// the reference's host accessors ptr()/idx()/val() still work and return the
-// CSR widened to int64/double, exported lazily on first use.  spmv() runs on
-// the GPU (fp32, column-ascending fmaf per row) -- there is no CPU path.
+// Drop-in replacement for the compressed-matrix part of the reference's
+// spconv/sparse.hpp (inc/sparse.hpp:24-32, 77-140, 209-274).  A SparseMatrix
+// here is a handle on a DEVICE-resident matrix (int32 indices, fp32 values) in
+// CSR or CSC layout, built by libspconv_b200; the reference's host accessors
+// ptr()/idx()/val() still work and return the storage (in the matrix's
+// layout) widened to int64/double, exported lazily on first use.  spmv() runs
+// on the GPU (fp32, column-ascending fmaf per output, which is also what the
+// reference's one-thread CSC scatter computes) -- there is no CPU path.
 #pragma once
 
 #include <cstdlib>
@@ -24,6 +26,12 @@ namespace spconv {
 enum class Layout { CSR, CSC };
 
 inline const char* layout_name(Layout l) { return l == Layout::CSR ? "csr" : "csc"; }
+
+inline Layout layout_from_name(const std::string& s) {
+    if (s == "csr" || s == "CSR") return Layout::CSR;
+    if (s == "csc" || s == "CSC") return Layout::CSC;
+    throw std::invalid_argument("unknown layout '" + s + "' (expected csr or csc)");
+}
 
 namespace detail {
 
@@ -50,8 +58,8 @@ inline int default_device() {
 
 }  // namespace detail
 
-/// Compressed sparse row matrix resident on the GPU (CSR only; the device
-/// path has no CSC layout).  Copies share the immutable device matrix.
+/// Compressed sparse matrix resident on the GPU, CSR or CSC.  Copies share the
+/// immutable device matrix.
 class SparseMatrix {
 public:
     SparseMatrix() = default;
@@ -59,6 +67,9 @@ public:
     /// Adopts a C-ABI handle (takes ownership).
     explicit SparseMatrix(spconv_csr* h) : dev_(std::make_shared<detail::CsrHandle>(h)) {
         detail::check(spconv_csr_shape(h, &rows_, &cols_, &nnz_));
+        int lay = 0;
+        detail::check(spconv_csr_layout(h, &lay));
+        layout_ = lay == 0 ? Layout::CSR : Layout::CSC;
         host_ = std::make_shared<HostCopy>();
     }
 
@@ -73,12 +84,26 @@ public:
         return SparseMatrix(h);
     }
 
-    Layout layout() const { return Layout::CSR; }
+    /// Uploads host storage in either layout (ptr over the major dimension).
+    static SparseMatrix from_storage(Layout layout, index_t rows, index_t cols,
+                                     const std::vector<index_t>& ptr, const std::vector<index_t>& idx,
+                                     const std::vector<double>& val) {
+        const index_t major = layout == Layout::CSR ? rows : cols;
+        if (static_cast<index_t>(ptr.size()) != major + 1)
+            throw std::invalid_argument("SparseMatrix: ptr must have major_dim+1 entries");
+        spconv_csr* h = nullptr;
+        detail::check(spconv_matrix_from_host(rows, cols, layout == Layout::CSR ? 0 : 1, ptr.data(),
+                                              idx.data(), val.data(), detail::default_device(),
+                                              nullptr, &h));
+        return SparseMatrix(h);
+    }
+
+    Layout layout() const { return layout_; }
     index_t rows() const { return rows_; }
     index_t cols() const { return cols_; }
     index_t nnz() const { return nnz_; }
-    index_t major_dim() const { return rows_; }
-    index_t minor_dim() const { return cols_; }
+    index_t major_dim() const { return layout_ == Layout::CSR ? rows_ : cols_; }
+    index_t minor_dim() const { return layout_ == Layout::CSR ? cols_ : rows_; }
 
     const std::vector<index_t>& ptr() const { return exported().ptr; }
     const std::vector<index_t>& idx() const { return exported().idx; }
@@ -96,7 +121,7 @@ private:
     const HostCopy& exported() const {
         if (!dev_) throw std::logic_error("SparseMatrix: empty matrix");
         std::call_once(host_->once, [this] {
-            host_->ptr.resize(static_cast<std::size_t>(rows_) + 1);
+            host_->ptr.resize(static_cast<std::size_t>(major_dim()) + 1);
             host_->idx.resize(static_cast<std::size_t>(nnz_));
             host_->val.resize(static_cast<std::size_t>(nnz_));
             detail::check(spconv_csr_export(dev_->h, host_->ptr.data(), host_->idx.data(),
@@ -107,8 +132,17 @@ private:
 
     std::shared_ptr<detail::CsrHandle> dev_;
     std::shared_ptr<HostCopy> host_;
+    Layout layout_ = Layout::CSR;
     index_t rows_ = 0, cols_ = 0, nnz_ = 0;
 };
+
+/// relayout (inc/sparse.hpp:268-274): the same matrix in `layout`.
+inline SparseMatrix relayout(const SparseMatrix& m, Layout layout) {
+    if (m.layout() == layout) return m;
+    spconv_csr* h = nullptr;
+    detail::check(spconv_relayout(m.handle(), layout == Layout::CSR ? 0 : 1, nullptr, &h));
+    return SparseMatrix(h);
+}
 
 /// y = M x (inc/sparse.hpp:214-261).  `threads` is accepted for source
 /// compatibility and ignored: the product runs on the GPU.

@@ -59,6 +59,33 @@ int spconv_nnz_bound(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p, int6
 int spconv_build_csr(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
                      const float* kernel_kxk, int device, void* stream, spconv_csr** out);
 
+/* build_transform(kernel, spec, layout) (inc/conv.hpp:179-204) with the
+ * storage layout of inc/sparse.hpp:24: 0 = CSR (same as spconv_build_csr),
+ * 1 = CSC -- column c = a*n + b holds its rows in ascending order, built on
+ * the device in closed form (csc_build.cu), bit-identical to the reference's
+ * compile(..., Layout::CSC).  A CSC handle also holds the row-major arrays
+ * the SpMV/SpMM kernels read; export / copy / device_ptrs / text show the
+ * storage layout. */
+int spconv_build_transform(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
+                           const float* kernel_kxk, int layout, int device, void* stream,
+                           spconv_csr** out);
+
+/* SparseMatrix::layout() (inc/sparse.hpp:121): 0 = CSR, 1 = CSC. */
+int spconv_csr_layout(const spconv_csr* h, int* layout);
+
+/* relayout(m, layout) (inc/sparse.hpp:268-274): a new handle holding the same
+ * matrix in `layout` (a copy when the layouts agree).  Conv handles are
+ * rebuilt on the device from their taps; matrices that came from the host are
+ * transposed from a host copy. */
+int spconv_relayout(const spconv_csr* h, int layout, void* stream, spconv_csr** out);
+
+/* Uploads a host matrix in either layout: layout 0 = spconv_csr_from_host,
+ * layout 1 = CSC (ptr over the cols+1 columns, row indices strictly ascending
+ * per column). */
+int spconv_matrix_from_host(int64_t rows, int64_t cols, int layout, const int64_t* ptr,
+                            const int64_t* idx, const double* vals, int device, void* stream,
+                            spconv_csr** out);
+
 /* Uploads an arbitrary host CSR (int64 ptr/idx, double values narrowed to
  * fp32) -- the device image of a reference SparseMatrix
  * (inc/sparse.hpp:121-130) for spmv on matrices not built here (e.g. read
@@ -75,16 +102,18 @@ int spconv_csr_shape(const spconv_csr* h, int64_t* rows, int64_t* cols, int64_t*
  * inc/conv.hpp:166); returns 1 for an uploaded generic CSR. */
 int spconv_csr_spec(const spconv_csr* h, int64_t spec5[5]);
 
-/* Device pointers of the CSR arrays (read-only; owned by the handle). */
+/* Device pointers of the storage arrays (read-only; owned by the handle):
+ * ptr over the major dimension (rows for CSR, columns for CSC). */
 int spconv_csr_device_ptrs(const spconv_csr* h, const int32_t** row_ptr, const int32_t** col_idx,
                            const float** vals);
 
 /* Synchronous export to host, widened to the reference's types: ptr(),
- * idx(), val() of inc/sparse.hpp:128-130.  Any pointer may be NULL. */
+ * idx(), val() of inc/sparse.hpp:128-130, in the handle's layout (ptr has
+ * major_dim()+1 entries).  Any pointer may be NULL. */
 int spconv_csr_export(const spconv_csr* h, int64_t* row_ptr, int64_t* col_idx, double* vals);
 
-/* Copies the native device arrays (int32 row_ptr / int32 col_idx / fp32
- * vals) into caller buffers, host or device (any pointer may be NULL),
+/* Copies the native device storage arrays (int32 ptr / int32 idx / fp32
+ * vals, in the handle's layout) into caller buffers, host or device (any pointer may be NULL),
  * ordered on `stream`; returns when the copies are complete. */
 int spconv_csr_copy(const spconv_csr* h, int32_t* row_ptr, int32_t* col_idx, float* vals,
                     void* stream);
@@ -114,9 +143,9 @@ int spconv_convolve_host_f64(const spconv_csr* h, const double* X_host, double* 
 
 /* Text form of the matrix, rendered on the device: with
  * transform_header_line != 0, write_transform (inc/conv.hpp:217-224):
- * "%%transform m n k s p csr" then write_sparse (inc/sparse.hpp:400-406):
+ * "%%transform m n k s p csr|csc" then write_sparse (inc/sparse.hpp:400-406):
  * "%%sparse coordinate real", "rows cols nnz", one "row col value" line per
- * entry (1-based, storage order, value = "%.17g" of the fp32 value widened
+ * entry (1-based, storage order -- column-major for CSC, value = "%.17g" of the fp32 value widened
  * to double).  Byte-identical to the reference's output for the same matrix.
  * buf == NULL: only *len (the text size in bytes) is computed; otherwise the
  * text is copied to buf (cap >= *len bytes, no terminator). */
@@ -129,7 +158,7 @@ int spconv_csr_write_text(const spconv_csr* h, int transform_header_line, char* 
  * std::invalid_argument).  Values are narrowed to fp32.  A matrix that equals
  * the conv transform of its own taps comes back as a built conv handle
  * (band kernels apply); anything else as a generic CSR with the geometry
- * attached.  csc files are read into the same operator in CSR layout. */
+ * attached.  The file's layout (csr / csc) is the handle's layout. */
 int spconv_transform_read(const char* text, int64_t len, int device, void* stream, spconv_csr** out);
 
 /* Name of the kernel(s) the last spconv_spmv / spconv_spmm /

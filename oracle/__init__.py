@@ -64,6 +64,9 @@ class Oracle:
                                               i64, C.c_void_p, i64, i64]
         L.orc_spmv_abs_f64.argtypes = [i64] + [C.c_void_p] * 5
         L.orc_direct_conv.argtypes = [i64] * 5 + [C.c_void_p] * 3
+        L.orc_transpose.argtypes = [i64, i64] + [C.c_void_p] * 6
+        L.orc_spmv_csc_f64.argtypes = [i64] + [C.c_void_p] * 5 + [i64]
+        L.orc_spmv_csc_f32_fma.argtypes = [i64] + [C.c_void_p] * 5 + [i64]
         self.L = L
 
     # -- rng.hpp ------------------------------------------------------------
@@ -167,6 +170,36 @@ class Oracle:
                                 _p(x), _p(y))
         return y
 
+    def transpose(self, major, minor, ptr, idx, val):
+        """relayout (inc/sparse.hpp:268-274): the storage of the other layout."""
+        ptr = np.ascontiguousarray(ptr, np.int64)
+        idx = np.ascontiguousarray(idx, np.int64)
+        val = np.ascontiguousarray(val, np.float64)
+        nnz = int(ptr[major])
+        optr = np.empty(minor + 1, np.int64)
+        oidx = np.empty(max(nnz, 1), np.int64)
+        oval = np.empty(max(nnz, 1), np.float64)
+        self.L.orc_transpose(major, minor, _p(ptr), _p(idx), _p(val), _p(optr), _p(oidx), _p(oval))
+        return optr, oidx[:nnz], oval[:nnz]
+
+    def spmv_csc_f64(self, rows, ptr, idx, val, x) -> np.ndarray:
+        cols = ptr.size - 1
+        y = np.empty(rows, np.float64)
+        x = np.ascontiguousarray(x, np.float64)
+        self.L.orc_spmv_csc_f64(cols, _p(np.ascontiguousarray(ptr, np.int64)),
+                                _p(np.ascontiguousarray(idx, np.int64)),
+                                _p(np.ascontiguousarray(val, np.float64)), _p(x), _p(y), rows)
+        return y
+
+    def spmv_csc_f32_fma(self, rows, ptr, idx, val, x) -> np.ndarray:
+        cols = ptr.size - 1
+        y = np.empty(rows, np.float32)
+        x = np.ascontiguousarray(x, np.float32)
+        self.L.orc_spmv_csc_f32_fma(cols, _p(np.ascontiguousarray(ptr, np.int64)),
+                                    _p(np.ascontiguousarray(idx, np.int64)),
+                                    _p(np.ascontiguousarray(val, np.float32)), _p(x), _p(y), rows)
+        return y
+
     def direct_conv(self, m, n, k, s, p, a, kern) -> np.ndarray:
         mo, no = (m + 2 * p - k) // s + 1, (n + 2 * p - k) // s + 1
         out = np.empty(mo * no, np.float64)
@@ -211,6 +244,10 @@ class Ref:
             L.ref_write_transform.argtypes = [C.c_void_p, C.c_void_p, i64, C.POINTER(i64)]
             L.ref_write_sparse_csr.argtypes = [i64, i64] + [C.c_void_p] * 4 + [i64, C.POINTER(i64)]
             L.ref_read_transform.argtypes = [C.c_char_p, i64, C.POINTER(C.c_void_p)]
+        L.ref_build_transform_layout.argtypes = [i64] * 5 + [C.c_void_p, C.c_int, C.c_int,
+                                                              C.POINTER(C.c_void_p)]
+        L.ref_relayout.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]
+        L.ref_transform_layout.argtypes = [C.c_void_p]
         if hasattr(L, "ref_run_layer_bench"):
             L.ref_run_layer_bench.argtypes = [C.c_char_p] + [i64] * 7 + [u64, C.c_int, C.c_void_p]
         self.L = L
@@ -251,10 +288,14 @@ class Ref:
         self._chk(self.L.ref_nnz_per_output(m, n, k, s, p, _p(out)))
         return out
 
-    def build(self, m, n, k, s, p, kern, route: int = 0) -> "RefTransform":
+    def build(self, m, n, k, s, p, kern, route: int = 0, layout: int = 0) -> "RefTransform":
+        """build_transform (inc/conv.hpp:179-204); layout 0 = CSR, 1 = CSC."""
         kern = np.ascontiguousarray(kern, np.float64).reshape(-1)
         h = C.c_void_p()
-        self._chk(self.L.ref_build_transform(m, n, k, s, p, _p(kern), route, C.byref(h)))
+        if layout:
+            self._chk(self.L.ref_build_transform_layout(m, n, k, s, p, _p(kern), route, layout, C.byref(h)))
+        else:
+            self._chk(self.L.ref_build_transform(m, n, k, s, p, _p(kern), route, C.byref(h)))
         return RefTransform(self, h, (m, n, k, s, p))
 
     def direct_conv(self, m, n, k, s, p, a, kern) -> np.ndarray:
@@ -304,14 +345,25 @@ class RefTransform:
     def __init__(self, ref: Ref, h, spec):
         self.ref, self.h, self.spec = ref, h, spec
 
+    @property
+    def layout(self) -> int:
+        return int(self.ref.L.ref_transform_layout(self.h))
+
+    def relayout(self, layout: int) -> "RefTransform":
+        """relayout (inc/sparse.hpp:268-274) of the matrix, same spec."""
+        h = C.c_void_p()
+        self.ref._chk(self.ref.L.ref_relayout(self.h, layout, C.byref(h)))
+        return RefTransform(self.ref, h, self.spec)
+
     def shape(self):
         r, c, z = i64(), i64(), i64()
         self.ref.L.ref_transform_shape(self.h, C.byref(r), C.byref(c), C.byref(z))
         return r.value, c.value, z.value
 
     def export(self):
-        rows, _, nnz = self.shape()
-        ptr = np.empty(rows + 1, np.int64)
+        """(ptr, idx, val) in the matrix's own layout (ptr over the major dim)."""
+        rows, cols, nnz = self.shape()
+        ptr = np.empty((cols if self.layout else rows) + 1, np.int64)
         idx = np.empty(max(nnz, 1), np.int64)
         val = np.empty(max(nnz, 1), np.float64)
         self.ref.L.ref_transform_export(self.h, _p(ptr), _p(idx), _p(val))

@@ -93,6 +93,32 @@ int ref_build_transform(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p, c
     });
 }
 
+// build_transform with an explicit layout (0 = CSR, 1 = CSC).
+int ref_build_transform_layout(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
+                               const double* kern, int route, int layout, void** out) {
+    return guarded([&] {
+        const spconv::ConvSpec spec(m, n, k, s, p);
+        const spconv::Kernel kernel(k, std::vector<double>(kern, kern + k * k));
+        auto* t = new spconv::Transform(spconv::build_transform(
+            kernel, spec, layout == 0 ? spconv::Layout::CSR : spconv::Layout::CSC,
+            route == 0 ? spconv::TransformRoute::Spgemm : spconv::TransformRoute::ColumnGather));
+        *out = t;
+    });
+}
+
+// relayout (inc/sparse.hpp:268-274) of a transform's matrix; same spec.
+int ref_relayout(const void* h, int layout, void** out) {
+    return guarded([&] {
+        const auto* t = static_cast<const spconv::Transform*>(h);
+        *out = new spconv::Transform{
+            t->spec, spconv::relayout(t->matrix, layout == 0 ? spconv::Layout::CSR : spconv::Layout::CSC)};
+    });
+}
+
+int ref_transform_layout(const void* h) {
+    return static_cast<const spconv::Transform*>(h)->matrix.layout() == spconv::Layout::CSR ? 0 : 1;
+}
+
 int ref_transform_shape(const void* h, int64_t* rows, int64_t* cols, int64_t* nnz) {
     const auto* t = static_cast<const spconv::Transform*>(h);
     *rows = t->matrix.rows();

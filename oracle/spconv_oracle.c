@@ -336,3 +336,58 @@ int orc_direct_conv(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p, const
         }
     return 0;
 }
+
+/* ------------------------------------------------------------------------ */
+/* CSC layout: relayout (inc/sparse.hpp:268-274) and CSC SpMV (:194-205)     */
+/* ------------------------------------------------------------------------ */
+
+/* relayout(m, other) re-compiles m's entries in the other layout
+ * (SparseMatrix::compile, inc/sparse.hpp:85-119: sort by (major, minor),
+ * histogram, prefix).  For a valid matrix that is a stable transposition of
+ * the storage: optr[c] = #entries with minor < c, and visiting the majors in
+ * ascending order fills every output slice in ascending (new minor) order --
+ * a counting sort, no comparison sort needed.  `major` / `minor` are the
+ * input's major and minor dimensions; optr has minor+1 entries. */
+void orc_transpose(int64_t major, int64_t minor, const int64_t *ptr, const int64_t *idx,
+                   const double *val, int64_t *optr, int64_t *oidx, double *oval) {
+    for (int64_t c = 0; c <= minor; ++c) optr[c] = 0;
+    for (int64_t e = 0; e < ptr[major]; ++e) optr[idx[e] + 1]++;
+    for (int64_t c = 0; c < minor; ++c) optr[c + 1] += optr[c];
+    int64_t *cur = (int64_t *)malloc((size_t)(minor > 0 ? minor : 1) * sizeof(int64_t));
+    for (int64_t c = 0; c < minor; ++c) cur[c] = optr[c];
+    for (int64_t r = 0; r < major; ++r)
+        for (int64_t e = ptr[r]; e < ptr[r + 1]; ++e) {
+            const int64_t q = cur[idx[e]]++;
+            oidx[q] = r;
+            oval[q] = val[e];
+        }
+    free(cur);
+}
+
+/* detail::spmv_csc_cols (inc/sparse.hpp:194-205) on one thread (spmv's nt <= 1
+ * branch, :227-231): y = 0; for every column j ascending, y[idx] += val * x[j]
+ * (fp64, separate multiply and add).  Every output therefore sums its terms
+ * in column-ascending order from +0.0, exactly as spmv_csr_rows does. */
+void orc_spmv_csc_f64(int64_t cols, const int64_t *ptr, const int64_t *idx, const double *val,
+                      const double *x, double *y, int64_t rows) {
+    for (int64_t i = 0; i < rows; ++i) y[i] = 0.0;
+    for (int64_t j = 0; j < cols; ++j) {
+        const double xj = x[j];
+        for (int64_t k = ptr[j]; k < ptr[j + 1]; ++k) {
+            const double prod = val[k] * xj;
+            y[idx[k]] = y[idx[k]] + prod;
+        }
+    }
+}
+
+/* The same scatter in fp32 with one rounding per step (fmaf): the device
+ * contract for CSC transforms.  Per output it is the CSR ordered-fmaf chain,
+ * so it is bit-identical to orc_spmv_csr_f32_fma on the transposed storage. */
+void orc_spmv_csc_f32_fma(int64_t cols, const int64_t *ptr, const int64_t *idx, const float *val,
+                          const float *x, float *y, int64_t rows) {
+    for (int64_t i = 0; i < rows; ++i) y[i] = 0.0f;
+    for (int64_t j = 0; j < cols; ++j) {
+        const float xj = x[j];
+        for (int64_t k = ptr[j]; k < ptr[j + 1]; ++k) y[idx[k]] = fmaf(val[k], xj, y[idx[k]]);
+    }
+}

@@ -22,7 +22,8 @@ import numpy as np
 
 __all__ = [
     "ConvSpec", "Kernel", "Transform", "build_transform", "convolve", "convolve_batch",
-    "spmv", "spmm", "nnz_bound", "read_transform", "library_path", "lib",
+    "spmv", "spmm", "nnz_bound", "read_transform", "relayout", "Layout", "layout_name",
+    "layout_from_name", "library_path", "lib",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -66,6 +67,30 @@ _decl("spconv_csr_last_kernel", [_vp], C.c_char_p)
 _decl("spconv_csr_write_text", [_vp, C.c_int, _vp, _i64, _P(_i64)])
 _decl("spconv_transform_read", [_vp, _i64, C.c_int, _vp, _P(_vp)])
 _decl("spconv_csr_free", [_vp])
+_decl("spconv_build_transform", [_i64] * 5 + [_vp, C.c_int, C.c_int, _vp, _P(_vp)])
+_decl("spconv_csr_layout", [_vp, _P(C.c_int)])
+_decl("spconv_relayout", [_vp, C.c_int, _vp, _P(_vp)])
+_decl("spconv_matrix_from_host", [_i64, _i64, C.c_int, _vp, _vp, _vp, C.c_int, _vp, _P(_vp)])
+
+
+class Layout:
+    """Storage layout (inc/sparse.hpp:24): CSR = 0, CSC = 1."""
+    CSR = 0
+    CSC = 1
+
+
+def layout_name(layout: int) -> str:
+    """inc/sparse.hpp:26."""
+    return "csr" if layout == Layout.CSR else "csc"
+
+
+def layout_from_name(s: str) -> int:
+    """inc/sparse.hpp:28-32 (same message)."""
+    if s in ("csr", "CSR"):
+        return Layout.CSR
+    if s in ("csc", "CSC"):
+        return Layout.CSC
+    raise ValueError(f"unknown layout '{s}' (expected csr or csc)")
 
 
 def _check(rc: int) -> None:
@@ -163,16 +188,25 @@ class Transform:
         r, c, z = _i64(), _i64(), _i64()
         _check(lib.spconv_csr_shape(self._h, C.byref(r), C.byref(c), C.byref(z)))
         self.rows, self.cols, self.nnz = r.value, c.value, z.value
+        lay = C.c_int()
+        _check(lib.spconv_csr_layout(self._h, C.byref(lay)))
+        self.layout = lay.value
+
+    @property
+    def major_dim(self) -> int:
+        return self.cols if self.layout == Layout.CSC else self.rows
 
     @classmethod
-    def from_host(cls, rows: int, cols: int, ptr, idx, val, device: int = 0, stream=None):
+    def from_host(cls, rows: int, cols: int, ptr, idx, val, device: int = 0, stream=None,
+                  layout: int = Layout.CSR):
+        """Uploads a host matrix (ptr over the major dimension of `layout`)."""
         ptr = np.ascontiguousarray(ptr, np.int64)
         idx = np.ascontiguousarray(idx, np.int64)
         val = np.ascontiguousarray(val, np.float64)
         h = _vp()
-        _check(lib.spconv_csr_from_host(rows, cols, ptr.ctypes.data, idx.ctypes.data,
-                                        val.ctypes.data, device, _stream_handle(stream),
-                                        C.byref(h)))
+        _check(lib.spconv_matrix_from_host(rows, cols, layout, ptr.ctypes.data, idx.ctypes.data,
+                                           val.ctypes.data, device, _stream_handle(stream),
+                                           C.byref(h)))
         return cls(h.value, None, device)
 
     @property
@@ -180,8 +214,9 @@ class Transform:
         return self._h.value
 
     def export(self) -> Tuple[np.ndarray, np.ndarray, np.ndarray]:
-        """ptr(), idx(), val() widened to the reference types (inc/sparse.hpp:128-130)."""
-        ptr = np.empty(self.rows + 1, np.int64)
+        """ptr(), idx(), val() widened to the reference types (inc/sparse.hpp:128-130),
+        in the transform's layout."""
+        ptr = np.empty(self.major_dim + 1, np.int64)
         idx = np.empty(max(self.nnz, 1), np.int64)
         val = np.empty(max(self.nnz, 1), np.float64)
         _check(lib.spconv_csr_export(self._h, ptr.ctypes.data, idx.ctypes.data, val.ctypes.data))
@@ -235,15 +270,24 @@ def read_transform(text: bytes, device: int = 0, stream=None) -> Transform:
     return Transform(h.value, ConvSpec(*spec5), device)
 
 
-def build_transform(kern: Kernel, spec: ConvSpec, device: int = 0, stream=None) -> Transform:
-    """On-device CSR build of T (replaces inc/conv.hpp:179-204)."""
+def build_transform(kern: Kernel, spec: ConvSpec, layout: int = Layout.CSR, device: int = 0,
+                    stream=None) -> Transform:
+    """On-device build of T in CSR or CSC layout (replaces inc/conv.hpp:179-204;
+    both reference routes give the same matrix)."""
     if kern.k != spec.k:
         raise ValueError(f"build_conv_matrix: kernel side {kern.k} does not match spec {spec.str()}")
     k32 = np.ascontiguousarray(kern.values, np.float32)
     h = _vp()
-    _check(lib.spconv_build_csr(spec.m, spec.n, spec.k, spec.s, spec.p, k32.ctypes.data, device,
-                                _stream_handle(stream), C.byref(h)))
+    _check(lib.spconv_build_transform(spec.m, spec.n, spec.k, spec.s, spec.p, k32.ctypes.data,
+                                      layout, device, _stream_handle(stream), C.byref(h)))
     return Transform(h.value, spec, device)
+
+
+def relayout(t: Transform, layout: int, stream=None) -> Transform:
+    """relayout (inc/sparse.hpp:268-274): the same matrix in `layout` (new handle)."""
+    h = _vp()
+    _check(lib.spconv_relayout(t._h, layout, _stream_handle(stream), C.byref(h)))
+    return Transform(h.value, t.spec, t.device)
 
 
 def _dev_f32(t, what):

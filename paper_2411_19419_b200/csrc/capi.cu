@@ -481,9 +481,9 @@ struct TokenReader {
 std::string transform_header(const spconv_csr* h) {
     char buf[256];
     std::snprintf(buf, sizeof buf,
-                  "%%%%transform %lld %lld %lld %lld %lld csr\n%%%%sparse coordinate real\n%lld %lld %lld\n",
+                  "%%%%transform %lld %lld %lld %lld %lld %s\n%%%%sparse coordinate real\n%lld %lld %lld\n",
                   (long long)h->g.m, (long long)h->g.n, (long long)h->g.k, (long long)h->g.s,
-                  (long long)h->g.p, (long long)h->rows, (long long)h->cols, (long long)h->nnz);
+                  (long long)h->g.p, h->layout ? "csc" : "csr", (long long)h->rows, (long long)h->cols, (long long)h->nnz);
     return buf;
 }
 
@@ -492,6 +492,77 @@ std::string sparse_header(const spconv_csr* h) {
     std::snprintf(buf, sizeof buf, "%%%%sparse coordinate real\n%lld %lld %lld\n", (long long)h->rows,
                   (long long)h->cols, (long long)h->nnz);
     return buf;
+}
+
+// CSC storage of a conv handle, built on the device from its taps
+// (csc_build.cu) after the CSR arrays on the same stream.
+int attach_csc_conv(spconv_csr* h, cudaStream_t st) {
+    const Geom& g = h->g;
+    const size_t cp_bytes = ((size_t)(h->cols + 1) * 4 + 255) & ~size_t(255);
+    const size_t ix_bytes = ((size_t)std::max<int64_t>(h->nnz, 1) * 4 + 255) & ~size_t(255);
+    char* mem = nullptr;
+    CK(cudaMallocAsync(&mem, cp_bytes + 2 * ix_bytes + 256, st));
+    h->csc_ptr = reinterpret_cast<int32_t*>(mem);
+    h->csc_idx = reinterpret_cast<int32_t*>(mem + cp_bytes);
+    h->csc_vals = reinterpret_cast<float*>(mem + cp_bytes + ix_bytes);
+    h->layout = 1;
+    spb::CscParams cp{};
+    cp.m = (int)g.m;
+    cp.n = (int)g.n;
+    cp.k = (int)g.k;
+    cp.s = (int)g.s;
+    cp.p = (int)g.p;
+    cp.mo = (int)g.mo;
+    cp.no = (int)g.no;
+    cp.cols = (int)h->cols;
+    cp.taps = h->taps;
+    cp.col_ptr = h->csc_ptr;
+    cp.row_idx = h->csc_idx;
+    cp.vals = h->csc_vals;
+    const int64_t per_axis = std::min<int64_t>(g.k, (g.k + g.s - 1) / g.s);
+    CK(spb::launch_csc_build(cp, (int)(per_axis * per_axis), st));
+    return SPCONV_OK;
+}
+
+// CSC storage given on the host (already validated), uploaded synchronously.
+int attach_csc_host(spconv_csr* h, const std::vector<int32_t>& cp, const std::vector<int32_t>& ci,
+                    const std::vector<float>& cv, cudaStream_t st) {
+    const size_t cp_bytes = ((size_t)(h->cols + 1) * 4 + 255) & ~size_t(255);
+    const size_t ix_bytes = ((size_t)std::max<int64_t>(h->nnz, 1) * 4 + 255) & ~size_t(255);
+    char* mem = nullptr;
+    CK(cudaMalloc(&mem, cp_bytes + 2 * ix_bytes + 256));
+    h->csc_ptr = reinterpret_cast<int32_t*>(mem);
+    h->csc_idx = reinterpret_cast<int32_t*>(mem + cp_bytes);
+    h->csc_vals = reinterpret_cast<float*>(mem + cp_bytes + ix_bytes);
+    h->layout = 1;
+    CK(cudaMemcpyAsync(h->csc_ptr, cp.data(), cp.size() * 4, cudaMemcpyHostToDevice, st));
+    if (h->nnz > 0) {
+        CK(cudaMemcpyAsync(h->csc_idx, ci.data(), (size_t)h->nnz * 4, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(h->csc_vals, cv.data(), (size_t)h->nnz * 4, cudaMemcpyHostToDevice, st));
+    }
+    CK(cudaStreamSynchronize(st));  // the host vectors die with the caller
+    return SPCONV_OK;
+}
+
+// Stable transposition of compressed storage (counting sort on the minor
+// index; majors visited ascending), the storage half of relayout
+// (inc/sparse.hpp:268-274) for matrices that arrive from the host.
+template <class I, class V>
+void transpose_host(int64_t major, int64_t minor, const I* ptr, const I* idx, const V* val,
+                    std::vector<int32_t>& optr, std::vector<int32_t>& oidx, std::vector<V>& oval) {
+    const int64_t nnz = (int64_t)ptr[major];
+    optr.assign((size_t)minor + 1, 0);
+    oidx.resize((size_t)std::max<int64_t>(nnz, 1));
+    oval.resize((size_t)std::max<int64_t>(nnz, 1));
+    for (int64_t e = 0; e < nnz; ++e) optr[(size_t)idx[e] + 1]++;
+    for (int64_t c = 0; c < minor; ++c) optr[(size_t)c + 1] += optr[(size_t)c];
+    std::vector<int32_t> cur(optr.begin(), optr.end() - 1);
+    for (int64_t r = 0; r < major; ++r)
+        for (int64_t e = (int64_t)ptr[r]; e < (int64_t)ptr[r + 1]; ++e) {
+            const int32_t q = cur[(size_t)idx[e]]++;
+            oidx[(size_t)q] = (int32_t)r;
+            oval[(size_t)q] = val[e];
+        }
 }
 
 }  // namespace
@@ -548,6 +619,7 @@ int spconv_build_csr(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
     h->k2max = (int)ht.k2max;
 
     h->taps_dense = ht.dense;
+    h->host_taps.assign(kernel_kxk, kernel_kxk + k * k);
     {
         int64_t lo, hi;
         for (int64_t yy = 0; yy < g.no; ++yy) tap_range(yy, g.n, g.k, g.s, g.p, lo, hi), h->sy += hi - lo;
@@ -646,6 +718,115 @@ int spconv_build_csr(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
     return SPCONV_OK;
 }
 
+int spconv_build_transform(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
+                           const float* kernel_kxk, int layout, int device, void* stream,
+                           spconv_csr** out) {
+    if (layout != 0 && layout != 1)
+        return fail(SPCONV_EINVAL, "spconv_build_transform: layout must be 0 (csr) or 1 (csc)");
+    if (int rc = spconv_build_csr(m, n, k, s, p, kernel_kxk, device, stream, out)) return rc;
+    if (layout == 0) return SPCONV_OK;
+    DeviceGuard dg(device);
+    if (int rc = attach_csc_conv(*out, static_cast<cudaStream_t>(stream))) {
+        const std::string msg = g_err;
+        spconv_csr_free(*out);
+        *out = nullptr;
+        return fail(rc, msg);
+    }
+    return SPCONV_OK;
+}
+
+int spconv_csr_layout(const spconv_csr* h, int* layout) {
+    if (!h || !layout) return fail(SPCONV_EINVAL, "null argument");
+    *layout = h->layout;
+    return SPCONV_OK;
+}
+
+int spconv_matrix_from_host(int64_t rows, int64_t cols, int layout, const int64_t* ptr,
+                            const int64_t* idx, const double* vals, int device, void* stream,
+                            spconv_csr** out) {
+    if (layout == 0) return spconv_csr_from_host(rows, cols, ptr, idx, vals, device, stream, out);
+    if (layout != 1) return fail(SPCONV_EINVAL, "spconv_matrix_from_host: layout must be 0 (csr) or 1 (csc)");
+    if (!out || !ptr) return fail(SPCONV_EINVAL, "spconv_matrix_from_host: null argument");
+    *out = nullptr;
+    if (rows < 1 || cols < 1)
+        return fail(SPCONV_EINVAL, "Triplets: dimensions must be at least 1x1, got " +
+                                       std::to_string(rows) + "x" + std::to_string(cols));
+    if (rows >= (1ll << 31) || cols >= (1ll << 31))
+        return fail(SPCONV_EINVAL, "spconv_matrix_from_host: dimensions exceed the int32 range");
+    const int64_t nnz = ptr[cols];
+    if (ptr[0] != 0 || nnz < 0 || nnz >= (1ll << 31))
+        return fail(SPCONV_EINVAL, "spconv_matrix_from_host: bad col_ptr");
+    for (int64_t c = 0; c < cols; ++c) {
+        if (ptr[c + 1] < ptr[c]) return fail(SPCONV_EINVAL, "spconv_matrix_from_host: col_ptr not non-decreasing");
+        for (int64_t e = ptr[c]; e < ptr[c + 1]; ++e)
+            if (idx[e] < 0 || idx[e] >= rows || (e > ptr[c] && idx[e] <= idx[e - 1]))
+                return fail(SPCONV_EINVAL, "spconv_matrix_from_host: row indices must be in range "
+                                           "and strictly ascending per column");
+    }
+    // row-major arrays for the kernels: the transposed storage
+    std::vector<int32_t> rp, ri;
+    std::vector<double> rv;
+    transpose_host(cols, rows, ptr, idx, vals, rp, ri, rv);
+    std::vector<int64_t> rp64(rp.begin(), rp.end()), ri64(ri.begin(), ri.end());
+    spconv_csr* h = nullptr;
+    if (int rc = spconv_csr_from_host(rows, cols, rp64.data(), ri64.data(), rv.data(), device, stream, &h))
+        return rc;
+    std::vector<int32_t> cp((size_t)cols + 1), ci((size_t)std::max<int64_t>(nnz, 1));
+    std::vector<float> cv((size_t)std::max<int64_t>(nnz, 1));
+    for (int64_t c = 0; c <= cols; ++c) cp[(size_t)c] = (int32_t)ptr[c];
+    for (int64_t e = 0; e < nnz; ++e) ci[(size_t)e] = (int32_t)idx[e], cv[(size_t)e] = (float)vals[e];
+    DeviceGuard dg(device);
+    if (int rc = attach_csc_host(h, cp, ci, cv, static_cast<cudaStream_t>(stream))) {
+        const std::string msg = g_err;
+        spconv_csr_free(h);
+        return fail(rc, msg);
+    }
+    *out = h;
+    return SPCONV_OK;
+}
+
+int spconv_relayout(const spconv_csr* h, int layout, void* stream, spconv_csr** out) {
+    if (!h || !out) return fail(SPCONV_EINVAL, "spconv_relayout: null argument");
+    if (layout != 0 && layout != 1) return fail(SPCONV_EINVAL, "spconv_relayout: layout must be 0 (csr) or 1 (csc)");
+    *out = nullptr;
+    if (h->is_conv && !h->host_taps.empty()) {
+        // A conv handle IS the transform of its taps: rebuild in the target
+        // layout on the device (closed form; no host round trip).
+        const Geom& g = h->g;
+        return spconv_build_transform(g.m, g.n, g.k, g.s, g.p, h->host_taps.data(), layout, h->device,
+                                      stream, out);
+    }
+    // Matrices that came from the host: transposition of the host copy.
+    std::vector<int64_t> rp((size_t)h->rows + 1), ri((size_t)std::max<int64_t>(h->nnz, 1));
+    std::vector<double> rv((size_t)std::max<int64_t>(h->nnz, 1));
+    {
+        spconv_csr tmp;  // export the row-major arrays regardless of h's layout
+        tmp.device = h->device;
+        tmp.rows = h->rows;
+        tmp.cols = h->cols;
+        tmp.nnz = h->nnz;
+        tmp.row_ptr = h->row_ptr;
+        tmp.col_idx = h->col_idx;
+        tmp.vals = h->vals;
+        const int rc = spconv_csr_export(&tmp, rp.data(), ri.data(), rv.data());
+        tmp.row_ptr = nullptr;  // not owned
+        if (rc) return rc;
+    }
+    int rc;
+    if (layout == 0) {
+        rc = spconv_csr_from_host(h->rows, h->cols, rp.data(), ri.data(), rv.data(), h->device, stream, out);
+    } else {
+        std::vector<int32_t> cp, ci;
+        std::vector<double> cv;
+        transpose_host(h->rows, h->cols, rp.data(), ri.data(), rv.data(), cp, ci, cv);
+        std::vector<int64_t> cp64(cp.begin(), cp.end()), ci64(ci.begin(), ci.end());
+        rc = spconv_matrix_from_host(h->rows, h->cols, 1, cp64.data(), ci64.data(), cv.data(), h->device,
+                                     stream, out);
+    }
+    if (rc == SPCONV_OK) (*out)->g = h->g;  // geometry travels with the matrix
+    return rc;
+}
+
 int spconv_csr_from_host(int64_t rows, int64_t cols, const int64_t* row_ptr,
                          const int64_t* col_idx, const double* vals, int device, void* stream,
                          spconv_csr** out) {
@@ -733,9 +914,9 @@ int spconv_csr_spec(const spconv_csr* h, int64_t spec5[5]) {
 int spconv_csr_device_ptrs(const spconv_csr* h, const int32_t** row_ptr, const int32_t** col_idx,
                            const float** vals) {
     if (!h) return fail(SPCONV_EINVAL, "null handle");
-    if (row_ptr) *row_ptr = h->row_ptr;
-    if (col_idx) *col_idx = h->col_idx;
-    if (vals) *vals = h->vals;
+    if (row_ptr) *row_ptr = h->layout ? h->csc_ptr : h->row_ptr;
+    if (col_idx) *col_idx = h->layout ? h->csc_idx : h->col_idx;
+    if (vals) *vals = h->layout ? h->csc_vals : h->vals;
     return SPCONV_OK;
 }
 
@@ -744,19 +925,20 @@ int spconv_csr_export(const spconv_csr* h, int64_t* row_ptr, int64_t* col_idx, d
     DeviceGuard dg(h->device);
     if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
     CK(cudaDeviceSynchronize());
+    const int64_t major = h->layout ? h->cols : h->rows;
     if (row_ptr) {
-        std::vector<int32_t> tmp((size_t)h->rows + 1);
-        CK(cudaMemcpy(tmp.data(), h->row_ptr, tmp.size() * 4, cudaMemcpyDeviceToHost));
+        std::vector<int32_t> tmp((size_t)major + 1);
+        CK(cudaMemcpy(tmp.data(), h->layout ? h->csc_ptr : h->row_ptr, tmp.size() * 4, cudaMemcpyDeviceToHost));
         for (size_t i = 0; i < tmp.size(); ++i) row_ptr[i] = tmp[i];
     }
     if (col_idx && h->nnz > 0) {
         std::vector<int32_t> tmp((size_t)h->nnz);
-        CK(cudaMemcpy(tmp.data(), h->col_idx, tmp.size() * 4, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(tmp.data(), h->layout ? h->csc_idx : h->col_idx, tmp.size() * 4, cudaMemcpyDeviceToHost));
         for (size_t i = 0; i < tmp.size(); ++i) col_idx[i] = tmp[i];
     }
     if (vals && h->nnz > 0) {
         std::vector<float> tmp((size_t)h->nnz);
-        CK(cudaMemcpy(tmp.data(), h->vals, tmp.size() * 4, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(tmp.data(), h->layout ? h->csc_vals : h->vals, tmp.size() * 4, cudaMemcpyDeviceToHost));
         for (size_t i = 0; i < tmp.size(); ++i) vals[i] = tmp[i];
     }
     return SPCONV_OK;
@@ -768,12 +950,14 @@ int spconv_csr_copy(const spconv_csr* h, int32_t* row_ptr, int32_t* col_idx, flo
     DeviceGuard dg(h->device);
     if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const bool csc = h->layout == 1;
     if (row_ptr)
-        CK(cudaMemcpyAsync(row_ptr, h->row_ptr, (size_t)(h->rows + 1) * 4, cudaMemcpyDefault, st));
+        CK(cudaMemcpyAsync(row_ptr, csc ? h->csc_ptr : h->row_ptr, (size_t)((csc ? h->cols : h->rows) + 1) * 4,
+                           cudaMemcpyDefault, st));
     if (col_idx && h->nnz > 0)
-        CK(cudaMemcpyAsync(col_idx, h->col_idx, (size_t)h->nnz * 4, cudaMemcpyDefault, st));
+        CK(cudaMemcpyAsync(col_idx, csc ? h->csc_idx : h->col_idx, (size_t)h->nnz * 4, cudaMemcpyDefault, st));
     if (vals && h->nnz > 0)
-        CK(cudaMemcpyAsync(vals, h->vals, (size_t)h->nnz * 4, cudaMemcpyDefault, st));
+        CK(cudaMemcpyAsync(vals, csc ? h->csc_vals : h->vals, (size_t)h->nnz * 4, cudaMemcpyDefault, st));
     CK(cudaStreamSynchronize(st));
     return SPCONV_OK;
 }
@@ -867,18 +1051,23 @@ int spconv_convolve_host_f64(const spconv_csr* h, const double* X_host, double* 
 int spconv_csr_write_text(const spconv_csr* h, int transform_header_line, char* buf, int64_t cap,
                           int64_t* len) {
     if (!h || !len) return fail(SPCONV_EINVAL, "spconv_csr_write_text: null argument");
-    if (transform_header_line && !h->is_conv)
+    if (transform_header_line && h->g.m <= 0)
         return fail(SPCONV_EINVAL, "write_transform: matrix has no convolution geometry");
     DeviceGuard dg(h->device);
     if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
     const std::string head = transform_header_line ? transform_header(h) : sparse_header(h);
-    const int64_t blocks = (h->rows + spb::text_rows_per_block() - 1) / spb::text_rows_per_block();
+    // storage order (inc/sparse.hpp:133-149): rows for CSR, columns for CSC
+    const bool csc = h->layout == 1;
+    const int32_t* sp_ = csc ? h->csc_ptr : h->row_ptr;
+    const int32_t* si_ = csc ? h->csc_idx : h->col_idx;
+    const float* sv_ = csc ? h->csc_vals : h->vals;
+    const int64_t major = csc ? h->cols : h->rows;
+    const int64_t blocks = (major + spb::text_rows_per_block() - 1) / spb::text_rows_per_block();
     cudaStream_t st = nullptr;
     unsigned long long* scratch = nullptr;
     CK(cudaMallocAsync(&scratch, (size_t)(blocks + 2) * 8, st));
     unsigned long long total = 0;
-    cudaError_t e = spb::render_entries(h->row_ptr, h->col_idx, h->vals, (int)h->rows, scratch, nullptr,
-                                        head.size(), st, true);
+    cudaError_t e = spb::render_entries(sp_, si_, sv_, (int)major, scratch, nullptr, head.size(), st, true, csc);
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(&total, scratch + blocks, 8, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
@@ -901,8 +1090,7 @@ int spconv_csr_write_text(const spconv_csr* h, int transform_header_line, char* 
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(text, head.data(), head.size(), cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess)
-        e = spb::render_entries(h->row_ptr, h->col_idx, h->vals, (int)h->rows, scratch, text, head.size(), st,
-                                false);
+        e = spb::render_entries(sp_, si_, sv_, (int)major, scratch, text, head.size(), st, false, csc);
     if (e == cudaSuccess) e = cudaMemcpyAsync(buf, text, (size_t)total, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     cudaFreeAsync(text, st);
@@ -951,7 +1139,13 @@ int spconv_transform_read(const char* text, int64_t len, int device, void* strea
                                            ") outside " + std::to_string(rows) + "x" + std::to_string(cols));
         t.push_back({r - 1, c - 1, v});
     }
-    std::sort(t.begin(), t.end(), [](const Trip& a, const Trip& b) { return a.r != b.r ? a.r < b.r : a.c < b.c; });
+    const bool csc = layout == "csc" || layout == "CSC";
+    // compile()'s order (inc/sparse.hpp:93-97): the first duplicate reported is
+    // the first in (major, minor) order of the requested layout
+    if (csc)
+        std::sort(t.begin(), t.end(), [](const Trip& a, const Trip& b) { return a.c != b.c ? a.c < b.c : a.r < b.r; });
+    else
+        std::sort(t.begin(), t.end(), [](const Trip& a, const Trip& b) { return a.r != b.r ? a.r < b.r : a.c < b.c; });
     for (size_t i = 1; i < t.size(); ++i)
         if (t[i].r == t[i - 1].r && t[i].c == t[i - 1].c)
             return fail(SPCONV_EINVAL, "SparseMatrix: duplicate entry at (" + std::to_string(t[i].r) + ", " +
@@ -961,6 +1155,8 @@ int spconv_transform_read(const char* text, int64_t len, int device, void* strea
         return fail(SPCONV_ERUNTIME, "read_transform: matrix is " + std::to_string(rows) + "x" + std::to_string(cols) +
                                          " but spec " + spec_str(m, n, k, s, p) + " requires " +
                                          std::to_string(g.mo * g.no) + "x" + std::to_string(m * n));
+    if (csc)  // the row-major arrays below want (row, col) order
+        std::sort(t.begin(), t.end(), [](const Trip& a, const Trip& b) { return a.r != b.r ? a.r < b.r : a.c < b.c; });
     std::vector<int64_t> ptr((size_t)rows + 1, 0), idx(t.size());
     std::vector<double> val(t.size());
     for (size_t i = 0; i < t.size(); ++i) {
@@ -991,6 +1187,14 @@ int spconv_transform_read(const char* text, int64_t len, int device, void* strea
                            __builtin_bit_cast(uint32_t, bv[(size_t)e]) ==
                                __builtin_bit_cast(uint32_t, (float)val[(size_t)e]);
             }
+            if (same && csc) {
+                DeviceGuard dg(device);
+                if (int rc = attach_csc_conv(built, static_cast<cudaStream_t>(stream))) {
+                    const std::string msg = g_err;
+                    spconv_csr_free(built);
+                    return fail(rc, msg);
+                }
+            }
             if (same) {
                 *out = built;
                 return SPCONV_OK;
@@ -1002,6 +1206,18 @@ int spconv_transform_read(const char* text, int64_t len, int device, void* strea
     if (int rc = spconv_csr_from_host(rows, cols, ptr.data(), idx.data(), val.data(), device, stream, &h))
         return rc;
     h->g = g;  // geometry travels with the matrix (Transform::spec) even when generic
+    if (csc) {
+        std::vector<int32_t> cp, ci;
+        std::vector<double> cv;
+        transpose_host(rows, cols, ptr.data(), idx.data(), val.data(), cp, ci, cv);
+        std::vector<float> cvf(cv.begin(), cv.end());
+        DeviceGuard dg(device);
+        if (int rc = attach_csc_host(h, cp, ci, cvf, static_cast<cudaStream_t>(stream))) {
+            const std::string msg = g_err;
+            spconv_csr_free(h);
+            return fail(rc, msg);
+        }
+    }
     *out = h;
     return SPCONV_OK;
 }
@@ -1019,6 +1235,7 @@ int spconv_csr_free(spconv_csr* h) {
         cudaDeviceSynchronize();
         free_ws(h);
         if (h->row_ptr) cudaFree(h->row_ptr);
+        if (h->csc_ptr) cudaFree(h->csc_ptr);
     }
     delete h;
     return SPCONV_OK;

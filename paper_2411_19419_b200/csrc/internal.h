@@ -7,6 +7,7 @@
 
 #include <atomic>
 #include <mutex>
+#include <vector>
 
 namespace spb {
 
@@ -42,6 +43,18 @@ struct BuildParams {
     int32_t* col_idx;
     float* vals;
     float* taps_out;  // k*k taps copied here by block 0 (the handle's device tap table)
+};
+
+// CSC build (csc_build.cu): the conv transform stored column-major.
+struct CscParams {
+    int m, n, k, s, p, mo, no;
+    int cols;
+    int stage;        // 1: stage entries in shared memory
+    int stage_words;  // words per staging array
+    const float* taps;  // device k*k taps
+    int32_t* col_ptr;
+    int32_t* row_idx;
+    float* vals;
 };
 
 // Conv-tiled SpMM: one CTA owns a TH x 32 block of output pixels (rows of T)
@@ -139,6 +152,7 @@ struct GenericParams {
 // Launchers (return cudaError_t of the launch).
 cudaError_t launch_csr_build(const BuildParams& bp, bool dense, int block, size_t smem,
                              cudaStream_t st);
+cudaError_t launch_csc_build(CscParams cp, int maxc, cudaStream_t st);
 cudaError_t launch_tiled(const TiledParams& tp, const CUtensorMap* tmap, int bt, size_t smem,
                          cudaStream_t st);
 cudaError_t launch_generic(const GenericParams& gp, cudaStream_t st);
@@ -156,7 +170,7 @@ cudaError_t launch_band_check(int k, int s, const BandParams& bp, cudaStream_t s
 
 cudaError_t render_entries(const int32_t* row_ptr, const int32_t* col_idx, const float* vals, int rows,
                            unsigned long long* scratch, char* out_dev, unsigned long long base,
-                           cudaStream_t st, bool size_only);
+                           cudaStream_t st, bool size_only, bool swap);
 int text_rows_per_block();
 
 size_t tiled_smem_bytes(int th, int wr, int wc, int k2max, int bt, int stages);
@@ -178,6 +192,14 @@ struct spconv_csr {
     uint8_t* seg_ok = nullptr;     // device band-check bytes [mo][tiles_y] (band geometries)
     int band_tw = 0;               // tile width seg_ok was sized for (0: none)
     int64_t sy = 0;                // sum over output columns of the valid tap-column count
+    // Storage layout (inc/sparse.hpp:24).  A CSC handle keeps its column-major
+    // storage (what export / text / device_ptrs show) next to the row-major
+    // arrays above, which every SpMV / SpMM kernel reads.
+    int layout = 0;                // 0 = CSR, 1 = CSC
+    int32_t* csc_ptr = nullptr;    // device col_ptr[cols+1] (layout 1)
+    int32_t* csc_idx = nullptr;    // device row_idx[nnz]
+    float* csc_vals = nullptr;     // device vals[nnz]
+    std::vector<float> host_taps;  // conv handles: the k*k fp32 taps (relayout rebuilds from them)
     std::atomic<const char*> last_kernel{nullptr};  // diagnostics: last SpMM kernel launched
     // Workspace of spconv_convolve_host (lazily created, guarded by ws_mu).
     std::mutex ws_mu;

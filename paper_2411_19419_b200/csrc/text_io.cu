@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(1024) text_scan_kernel(unsigned long long* v, 
 __global__ void __launch_bounds__(256) text_write_kernel(const int32_t* row_ptr, const int32_t* col_idx,
                                                          const float* vals, int rows,
                                                          const unsigned long long* block_off,
-                                                         char* out) {
+                                                         char* out, int swap) {
     extern __shared__ unsigned char s_text[];
     __shared__ int s_lineoff[257];
     const int r0 = blockIdx.x * kRowsPerBlock;
@@ -227,9 +227,12 @@ __global__ void __launch_bounds__(256) text_write_kernel(const int32_t* row_ptr,
         int len = 0;
         if (e < e1) {
             while (row_ptr[r + 1] <= e) ++r;
-            len = format_u64((unsigned long long)r + 1, line);
+            // CSR: "major minor"; CSC storage order prints (row = minor, col = major)
+            const unsigned long long a = (unsigned long long)(swap ? col_idx[e] : r) + 1;
+            const unsigned long long b = (unsigned long long)(swap ? r : col_idx[e]) + 1;
+            len = format_u64(a, line);
             line[len++] = ' ';
-            len += format_u64((unsigned long long)col_idx[e] + 1, line + len);
+            len += format_u64(b, line + len);
             line[len++] = ' ';
             len += format_g17(vals[e], line + len);
             line[len++] = '\n';
@@ -286,12 +289,15 @@ cudaError_t init_pow5(int dev) {
 
 }  // namespace
 
-// Renders the entry lines of a CSR (device arrays) into `out_dev` starting at
-// byte `base`; writes the total text size (base + entry bytes) to *end.
+// Renders the entry lines of a compressed matrix (device arrays, `rows` = its
+// major dimension) into `out_dev` starting at byte `base`, in storage order
+// (SparseMatrix::entries, inc/sparse.hpp:133-149); `swap` prints the minor
+// index first (CSC: "row col" = "minor major").  The line length is symmetric
+// in the two indices, so the size pass needs no flag.
 // `scratch` holds (rows / 64 + 2) unsigned long longs.
 cudaError_t render_entries(const int32_t* row_ptr, const int32_t* col_idx, const float* vals, int rows,
                            unsigned long long* scratch, char* out_dev, unsigned long long base,
-                           cudaStream_t st, bool size_only) {
+                           cudaStream_t st, bool size_only, bool swap) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaError_t e = init_pow5(dev);
@@ -308,7 +314,7 @@ cudaError_t render_entries(const int32_t* row_ptr, const int32_t* col_idx, const
         attr[dev & 63] = true;
     }
     text_write_kernel<<<blocks, 256, kStageBytes + 256 * 64, st>>>(row_ptr, col_idx, vals, rows, scratch,
-                                                                  out_dev);
+                                                                  out_dev, swap ? 1 : 0);
     return cudaGetLastError();
 }
 

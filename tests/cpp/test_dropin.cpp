@@ -4,6 +4,7 @@
 // libspconv_b200.so.  Runs on the GPU (tests/test_dropin_cpp.py).  Exit 0 = pass.
 #include <cmath>
 #include <cstdio>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -102,6 +103,37 @@ int main() {
                                    t.matrix.idx(), t.matrix.val());
         CHECK(spmv(g, imgs[2].values) == outs[2].values);
     }
+    // CSC layout (inc/sparse.hpp:24, 194-205, 268-274): SPEC.md:170 example in
+    // CSC -- column 0 (input pixel (0,0)) is hit by output rows 0, 1, 3, 4.
+    {
+        const ConvSpec spec(3, 3, 3, 1, 1);
+        const Kernel ones(3, std::vector<double>(9, 1.0));
+        const Transform tc = build_transform(ones, spec, Layout::CSC);
+        CHECK(tc.matrix.layout() == Layout::CSC);
+        CHECK(tc.matrix.major_dim() == 9 && tc.matrix.nnz() == 49);
+        CHECK(tc.matrix.ptr()[1] == 4);
+        CHECK((std::vector<index_t>(tc.matrix.idx().begin(), tc.matrix.idx().begin() + 4) ==
+               std::vector<index_t>{0, 1, 3, 4}));
+        CHECK(convolve(tc, Grid(3, 3, 1.0)).values == (std::vector<double>{4, 6, 4, 6, 9, 6, 4, 6, 4}));
+        const Transform tr = build_transform(ones, spec);
+        const SparseMatrix back = relayout(tc.matrix, Layout::CSR);
+        CHECK(back.layout() == Layout::CSR && back.ptr() == tr.matrix.ptr() && back.idx() == tr.matrix.idx());
+        const SparseMatrix fwd = relayout(tr.matrix, Layout::CSC);
+        CHECK(fwd.ptr() == tc.matrix.ptr() && fwd.idx() == tc.matrix.idx() && fwd.val() == tc.matrix.val());
+        std::ostringstream os;
+        write_transform(os, tc);
+        CHECK(os.str().rfind("%%transform 3 3 3 1 1 csc\n%%sparse coordinate real\n9 9 49\n1 1 1\n2 1 1\n4 1 1\n", 0) == 0);
+        std::istringstream is(os.str());
+        const Transform rd = read_transform(is);
+        CHECK(rd.matrix.layout() == Layout::CSC && rd.matrix.ptr() == tc.matrix.ptr());
+        // A host CSC upload (generic path) applies identically.
+        const SparseMatrix g = SparseMatrix::from_storage(Layout::CSC, 9, 9, tc.matrix.ptr(), tc.matrix.idx(),
+                                                          tc.matrix.val());
+        CHECK(spmv(g, Grid(3, 3, 1.0).values) == (std::vector<double>{4, 6, 4, 6, 9, 6, 4, 6, 4}));
+        CHECK(relayout(g, Layout::CSR).ptr() == tr.matrix.ptr());
+    }
+    expect_throw<std::invalid_argument>([] { layout_from_name("coo"); },
+                                        "unknown layout 'coo' (expected csr or csc)");
     // Errors: the reference's exception types and messages.
     expect_throw<std::invalid_argument>([] { ConvSpec(0, 3, 1, 1, 0); },
                                         "ConvSpec: need m,n,k,s >= 1 and p >= 0, got (m=0");

@@ -7,6 +7,7 @@ through it, the device path:
 
 * known-answer RNG values (inc/rng.hpp) and the SPEC examples;
 * full CSR + fp64 outputs for config 1 (64x64 k3 s1 p1) and small cases;
+* the same in CSC layout (build_transform(..., Layout::CSC)), config 1 in full;
 * SHA-256 digests of the reference CSR (int64 ptr/idx, float64 val, little
   endian) and of its fp64 convolve() output for config 2 (512^2 k5 s2 p2), the
   36 config-5 edge-sweep specs on 257x193 (with the BASELINE kernel and with a
@@ -107,6 +108,13 @@ def main():
     ptr, idx, val = t.export()
     y = t.convolve(img[None])[0]
     npz.update(c1_kernel=kern, c1_image=img, c1_ptr=ptr, c1_idx=idx, c1_val=val, c1_y=y)
+    # ... and in CSC layout (build_transform(..., Layout::CSC)); its convolve()
+    # (spmv_csc_cols, one thread) reproduces the CSR output bit for bit.
+    tc = ref.build(64, 64, 3, 1, 1, kern, layout=1)
+    cptr, cidx, cval = tc.export()
+    yc = tc.convolve(img[None])[0]
+    assert np.array_equal(yc.view(np.uint64), y.view(np.uint64))
+    npz.update(c1_csc_ptr=cptr, c1_csc_idx=cidx, c1_csc_val=cval)
 
     # Zero-tap kernel, small: nnz(T) < Theorem 2.1 bound (SURVEY hard part 2).
     zk = np.array([1.5, 0.0, -2.0, -0.0, 3.0, 0.0, 0.25, 0.0, -1.0])
@@ -127,9 +135,12 @@ def main():
             t = ref.build(m, n, k, s, p, kern)
             ptr, idx, val = t.export()
             yv = t.convolve(img[None])[0]
+            tc = ref.build(m, n, k, s, p, kern, layout=1)
+            yc = tc.convolve(img[None])[0]
             key = f"{m}x{n}_k{k}_s{s}_p{p}_{variant}"
             digests[key] = dict(spec=[m, n, k, s, p], cfg=cfg, variant=variant, nnz=int(val.size),
-                                csr=sha(ptr, idx, val), y=sha(yv))
+                                csr=sha(ptr, idx, val), y=sha(yv), csc=sha(*tc.export()),
+                                y_csc=sha(yc))
     js["digests"] = digests
 
     # Digest-of-digests over the exhaustive m,n <= 9 sweep (verify.hpp:66-71 grid),
@@ -163,9 +174,11 @@ def main():
             kern[4] = -np.nan
         t = ref.build(m, n, k, s, p, kern)
         data = t.write_text()
+        data_csc = ref.build(m, n, k, s, p, kern, layout=1).write_text()
         text.append(dict(spec=[m, n, k, s, p], variant=variant,
                          kernel_bits=[int(b) for b in np.asarray(kern, np.float32).view(np.uint32)],
-                         bytes=len(data), sha=hashlib.sha256(data).hexdigest()))
+                         bytes=len(data), sha=hashlib.sha256(data).hexdigest(),
+                         csc_bytes=len(data_csc), csc_sha=hashlib.sha256(data_csc).hexdigest()))
     js["text"] = text
 
     # %.17g of fp32 values widened to double, as the reference prints them

@@ -165,3 +165,75 @@ def test_nan_tap_kept(orc, ref):
     op, oi, ov = orc.build_transform(3, 3, 2, 1, 0, kern)
     assert np.array_equal(rp, op) and np.array_equal(ri, oi)
     assert np.array_equal(rv, ov, equal_nan=True) and np.isnan(ov).sum() == 4
+
+
+# ---- CSC layout (relayout inc/sparse.hpp:268-274, spmv_csc_cols :194-205) ---------
+
+def test_csc_config1_full_arrays(orc, golden):
+    """The restated transposition reproduces the reference's CSC build of
+    config 1, and the CSC scatter-SpMV its (= the CSR) fp64 output."""
+    _, npz = golden
+    ptr, idx, val = orc.build_transform(64, 64, 3, 1, 1, npz["c1_kernel"])
+    cp, ci, cv = orc.transpose(ptr.size - 1, 64 * 64, ptr, idx, val)
+    assert np.array_equal(cp, npz["c1_csc_ptr"]) and np.array_equal(ci, npz["c1_csc_idx"])
+    assert np.array_equal(cv.view(np.uint64), npz["c1_csc_val"].view(np.uint64))
+    y = orc.spmv_csc_f64(ptr.size - 1, cp, ci, cv, npz["c1_image"])
+    assert np.array_equal(y.view(np.uint64), npz["c1_y"].view(np.uint64))
+
+
+def test_csc_golden_digests(orc, golden):
+    """CSC storage and CSC fp64 outputs of all 62 digest cases equal the
+    reference's; and the reference's own CSC output equals its CSR output."""
+    js, _ = golden
+    for key, (m, nn, k, s, p), kern, img in golden_cases(orc, js):
+        d = js["digests"][key]
+        ptr, idx, val = orc.build_transform(m, nn, k, s, p, kern)
+        rows = ptr.size - 1
+        cp, ci, cv = orc.transpose(rows, m * nn, ptr, idx, val)
+        assert sha(cp, ci, cv) == d["csc"], key
+        assert d["y_csc"] == d["y"], key
+        assert sha(orc.spmv_csc_f64(rows, cp, ci, cv, img)) == d["y_csc"], key
+        back = orc.transpose(m * nn, rows, cp, ci, cv)
+        assert sha(*back) == d["csr"], key
+
+
+def test_csc_f32_contract_equals_csr(orc):
+    """fp32: the CSC scatter with fmaf is bit-identical to the CSR ordered-fmaf
+    chain -- the device contract both layouts share."""
+    rng = np.random.default_rng(5)
+    for spec in [(33, 20, 3, 1, 1), (40, 41, 5, 2, 4), (17, 64, 7, 3, 0), (9, 9, 11, 1, 5)]:
+        m, n, k = spec[:3]
+        kern = rng.standard_normal(k * k).astype(np.float32).astype(np.float64)
+        kern[rng.random(k * k) < 0.2] = 0.0
+        ptr, idx, val = orc.build_transform(*spec, kern)
+        cp, ci, cv = orc.transpose(ptr.size - 1, m * n, ptr, idx, val)
+        x = rng.standard_normal(m * n).astype(np.float32)
+        a = orc.spmv_f32_fma(ptr, idx, val.astype(np.float32), x)
+        b = orc.spmv_csc_f32_fma(ptr.size - 1, cp, ci, cv.astype(np.float32), x)
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32)), spec
+
+
+def test_csc_against_compiled_reference(orc, ref):
+    """Restated transposition vs the reference's build_transform(Layout::CSC)
+    and relayout, both routes, zero / -0 / NaN taps."""
+    rng = np.random.default_rng(11)
+    for i in range(60):
+        m, n = int(rng.integers(1, 14)), int(rng.integers(1, 14))
+        p, s = int(rng.integers(0, 4)), int(rng.integers(1, 4))
+        k = int(rng.integers(1, min(m, n) + 2 * p + 1))
+        kern = rng.standard_normal(k * k)
+        kern[rng.random(k * k) < 0.25] = 0.0
+        if i % 7 == 0:
+            kern[0] = -0.0
+        if i % 11 == 0:
+            kern[-1] = np.nan
+        ptr, idx, val = orc.build_transform(m, n, k, s, p, kern)
+        want = orc.transpose(ptr.size - 1, m * n, ptr, idx, val)
+        for route in (0, 1):
+            got = ref.build(m, n, k, s, p, kern, route=route, layout=1).export()
+            assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+            assert np.array_equal(got[2].view(np.uint64), want[2].view(np.uint64))
+        rl = ref.build(m, n, k, s, p, kern).relayout(1).export()
+        assert all(np.array_equal(a.view(np.uint64) if a.dtype == np.float64 else a,
+                                  b.view(np.uint64) if b.dtype == np.float64 else b)
+                   for a, b in zip(rl, want))
