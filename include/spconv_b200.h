@@ -161,6 +161,37 @@ int spconv_csr_write_text(const spconv_csr* h, int transform_header_line, char* 
  * attached.  The file's layout (csr / csc) is the handle's layout. */
 int spconv_transform_read(const char* text, int64_t len, int device, void* stream, spconv_csr** out);
 
+/* Dense comparators of inc/reference.hpp on the device, over `batch` images
+ * (A[b][m*n] -> out[b][m_out*n_out], device buffers, `taps_dev` = k*k taps of
+ * the same type).  dtype 1 = fp64 with one rounded multiply and one rounded
+ * add per tap in (j, i) order, padding taps included: bit-identical to the
+ * reference's direct_conv (inc/reference.hpp:41-61) and im2col_conv
+ * (:73-136).  dtype 0 = fp32 fmaf in the same order: the device SpMV's
+ * contract (equal to spconv_spmv bit for bit on finite inputs).
+ * direct_conv optionally writes sum|w*a| per output to mag_dev (tolerances);
+ * im2col_conv materialises the k^2 x (m_out*n_out) patch matrix per image in
+ * patches_dev (batch * k^2 * m_out * n_out elements). */
+int spconv_direct_conv(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p, int dtype, const void* taps_dev,
+                       const void* A_dev, void* out_dev, void* mag_dev, int64_t batch, void* stream);
+int spconv_im2col_conv(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p, int dtype, const void* taps_dev,
+                       const void* A_dev, void* out_dev, void* patches_dev, int64_t batch, void* stream);
+
+/* run_verification (inc/verify.hpp:59-169) over the device path: for every
+ * m, n <= max_dim, p <= 3, s <= 3, k <= min(m,n) + 2p, the Theorem 2.1 count
+ * against the brute-force overlap count and nnz(T), and for `seeds` seeded
+ * cases (the reference's inputs: derive_seed(base_seed, case), nonzero
+ * kernels) the device CSR transform, its device CSC relayout, the fp32 device
+ * direct_conv and the fp64 device direct_conv / im2col_conv.  Checks: fp64
+ * comparators agree within 1e-10; the fp32 sparse outputs are within
+ * 1e-5 * sum|w*a| of the fp64 reference and BIT-equal to the fp32 direct_conv;
+ * CSR and CSC outputs are bit-equal.  counts = {specs, conv_cases,
+ * clipped_specs, failures}; devs = {max |sparse or im2col - reference|,
+ * max |CSR - CSC|, max condition-relative fp32 deviation}; `failures` gets the
+ * first (at most 20) failure lines, '
+'-separated. */
+int spconv_run_verification(int64_t max_dim, int seeds, uint64_t base_seed, int device, int64_t counts[4],
+                            double devs[3], char* failures, int64_t cap);
+
 /* Name of the kernel(s) the last spconv_spmv / spconv_spmm /
  * spconv_convolve_host call on this handle launched (diagnostics; "" before
  * the first call).  The string is static. */

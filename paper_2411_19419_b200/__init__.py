@@ -23,7 +23,7 @@ import numpy as np
 __all__ = [
     "ConvSpec", "Kernel", "Transform", "build_transform", "convolve", "convolve_batch",
     "spmv", "spmm", "nnz_bound", "read_transform", "relayout", "Layout", "layout_name",
-    "layout_from_name", "library_path", "lib",
+    "layout_from_name", "direct_conv", "im2col_conv", "run_verification", "library_path", "lib",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -70,6 +70,9 @@ _decl("spconv_csr_free", [_vp])
 _decl("spconv_build_transform", [_i64] * 5 + [_vp, C.c_int, C.c_int, _vp, _P(_vp)])
 _decl("spconv_csr_layout", [_vp, _P(C.c_int)])
 _decl("spconv_relayout", [_vp, C.c_int, _vp, _P(_vp)])
+_decl("spconv_direct_conv", [_i64] * 5 + [C.c_int, _vp, _vp, _vp, _vp, _i64, _vp])
+_decl("spconv_im2col_conv", [_i64] * 5 + [C.c_int, _vp, _vp, _vp, _vp, _i64, _vp])
+_decl("spconv_run_verification", [_i64, C.c_int, C.c_uint64, C.c_int, _vp, _vp, _vp, _i64])
 _decl("spconv_matrix_from_host", [_i64, _i64, C.c_int, _vp, _vp, _vp, C.c_int, _vp, _P(_vp)])
 
 
@@ -357,3 +360,44 @@ def convolve(t: Transform, a) -> np.ndarray:
     out = np.empty(t.rows, np.float64)
     _check(lib.spconv_convolve_host_f64(t._h, a.ctypes.data, out.ctypes.data, 1))
     return out.reshape(t.spec.m_out, t.spec.n_out)
+
+
+def direct_conv(spec: ConvSpec, A, taps, out=None, mag=None, stream=None):
+    """Device direct_conv (inc/reference.hpp:41-61) of A [batch, m*n] (CUDA
+    float32: fmaf contract, or float64: the reference's arithmetic, bit-exact)."""
+    import torch
+    dt = {torch.float32: 0, torch.float64: 1}[A.dtype]
+    A = A.reshape(-1, spec.input_len).contiguous()
+    taps = taps.to(device=A.device, dtype=A.dtype).contiguous()
+    if out is None:
+        out = torch.empty(A.shape[0], spec.output_len, dtype=A.dtype, device=A.device)
+    _check(lib.spconv_direct_conv(spec.m, spec.n, spec.k, spec.s, spec.p, dt, taps.data_ptr(), A.data_ptr(),
+                                  out.data_ptr(), mag.data_ptr() if mag is not None else None, A.shape[0],
+                                  _stream_handle(stream)))
+    return out
+
+
+def im2col_conv(spec: ConvSpec, A, taps, out=None, stream=None):
+    """Device im2col lowering + product (inc/reference.hpp:73-136)."""
+    import torch
+    dt = {torch.float32: 0, torch.float64: 1}[A.dtype]
+    A = A.reshape(-1, spec.input_len).contiguous()
+    taps = taps.to(device=A.device, dtype=A.dtype).contiguous()
+    if out is None:
+        out = torch.empty(A.shape[0], spec.output_len, dtype=A.dtype, device=A.device)
+    patches = torch.empty(A.shape[0] * spec.k * spec.k * spec.output_len, dtype=A.dtype, device=A.device)
+    _check(lib.spconv_im2col_conv(spec.m, spec.n, spec.k, spec.s, spec.p, dt, taps.data_ptr(), A.data_ptr(),
+                                  out.data_ptr(), patches.data_ptr(), A.shape[0], _stream_handle(stream)))
+    return out
+
+
+def run_verification(max_dim: int = 12, seeds: int = 3, base_seed: int = 42, device: int = 0) -> dict:
+    """run_verification (inc/verify.hpp:59-169) over the device path (see
+    include/spconv_b200.h); returns the VerifyReport fields."""
+    counts = (C.c_int64 * 4)()
+    devs = (C.c_double * 3)()
+    buf = C.create_string_buffer(8192)
+    _check(lib.spconv_run_verification(max_dim, seeds, base_seed, device, counts, devs, buf, len(buf)))
+    fails = [f for f in buf.value.decode().split("\n") if f]
+    return dict(specs=counts[0], conv_cases=counts[1], clipped_specs=counts[2], failures=counts[3],
+                max_conv_dev=devs[0], max_layout_dev=devs[1], max_rel_dev=devs[2], failure_lines=fails)

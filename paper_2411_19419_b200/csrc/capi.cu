@@ -567,6 +567,8 @@ void transpose_host(int64_t major, int64_t minor, const I* ptr, const I* idx, co
 
 }  // namespace
 
+int spb_fail(int code, const std::string& msg) { return fail(code, msg); }
+
 extern "C" {
 
 const char* spconv_last_error(void) { return g_err.c_str(); }

@@ -175,7 +175,18 @@ int text_rows_per_block();
 
 size_t tiled_smem_bytes(int th, int wr, int wc, int k2max, int bt, int stages);
 
+// Device comparators (verify.cu): dtype 0 = fp32 fmaf (the device contract),
+// 1 = fp64 without contraction (bit-identical to inc/reference.hpp).
+cudaError_t launch_direct_conv(int dtype, int m, int n, int k, int s, int p, long long batch, const void* taps,
+                               const void* A, void* out, void* mag, cudaStream_t st);
+cudaError_t launch_im2col_conv(int dtype, int m, int n, int k, int s, int p, long long batch, const void* taps,
+                               const void* A, void* out, void* patches, cudaStream_t st);
+
 }  // namespace spb
+
+// Sets the calling thread's spconv_last_error() message and returns `code` (capi.cu).
+#include <string>
+int spb_fail(int code, const std::string& msg);
 
 // The opaque handle of include/spconv_b200.h.
 struct spconv_csr {

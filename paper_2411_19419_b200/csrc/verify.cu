@@ -1,0 +1,460 @@
+// verify.cu -- device comparators and the device verification sweep.
+//
+// The reference checks its sparse path against two dense comparators
+// (inc/reference.hpp): direct_conv, a four-loop sliding window over a
+// zero-padded copy (:41-61), and im2col_conv, an explicit k^2 x (m_out*n_out)
+// patch matrix times vec(K) (:73-136).  Both run here as CUDA kernels:
+//
+//   * REF arithmetic (fp64, one rounded multiply then one rounded add per tap,
+//     taps in (j, i) order, padding taps included): bit-identical to the
+//     reference's own functions, whose Release build does not contract
+//     a*b + c (x86-64 baseline, no FMA);
+//   * FMA arithmetic (fp32 fmaf, same order): the device path's contract --
+//     equal bit for bit to the SpMV of T for finite inputs, because a padding
+//     or zero tap adds fmaf(w, 0, acc) == acc.
+//
+// spconv_run_verification mirrors run_verification (inc/verify.hpp:59-169)
+// on the device: the same spec grid, the same seeded inputs (the reference's
+// generator, inc/rng.hpp, restated below), the CSR transform and its CSC
+// relayout built and applied on the GPU, compared with the device
+// comparators.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/spconv_b200.h"
+#include "internal.h"
+
+namespace spb {
+
+namespace {
+
+template <typename T, bool FMA>
+__device__ __forceinline__ T mac(T w, T v, T acc) {
+    if constexpr (FMA) {
+        return fma(w, v, acc);
+    } else if constexpr (sizeof(T) == 8) {
+        return __dadd_rn(acc, __dmul_rn(w, v));
+    } else {
+        return __fadd_rn(acc, __fmul_rn(w, v));
+    }
+}
+
+struct ConvGeom {
+    int m, n, k, s, p, mo, no;
+    long long batch;
+};
+
+// direct_conv (inc/reference.hpp:41-61): one thread per output of one image.
+template <typename T, bool FMA>
+__global__ void __launch_bounds__(256) direct_conv_kernel(const ConvGeom G, const T* __restrict__ taps,
+                                                          const T* __restrict__ A, T* __restrict__ out,
+                                                          T* __restrict__ mag) {
+    const long long P = (long long)G.mo * G.no;
+    const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= P * G.batch) return;
+    const long long b = q / P;
+    const int t = (int)(q - b * P);
+    const int x = t / G.no, y = t - x * G.no;
+    const T* a = A + b * (long long)G.m * G.n;
+    T acc = T(0), ms = T(0);
+    for (int j = 0; j < G.k; ++j) {
+        const int r = G.s * x + j - G.p;
+        for (int i = 0; i < G.k; ++i) {
+            const int c = G.s * y + i - G.p;
+            const T v = (r >= 0 && r < G.m && c >= 0 && c < G.n) ? a[(long long)r * G.n + c] : T(0);
+            const T w = taps[j * G.k + i];
+            acc = mac<T, FMA>(w, v, acc);
+            if (mag) ms += fabs(w * v);
+        }
+    }
+    out[q] = acc;
+    if (mag) mag[q] = ms;
+}
+
+// im2col (inc/reference.hpp:73-97): patches[b][(j*k + i) * P + t] = Apad[s*x + j][s*y + i].
+template <typename T>
+__global__ void __launch_bounds__(256) im2col_lower_kernel(const ConvGeom G, const T* __restrict__ A,
+                                                           T* __restrict__ patches) {
+    const long long P = (long long)G.mo * G.no, K2 = (long long)G.k * G.k;
+    const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= K2 * P * G.batch) return;
+    const long long b = q / (K2 * P);
+    const long long rt = q - b * K2 * P;
+    const int r = (int)(rt / P), t = (int)(rt - (long long)r * P);
+    const int j = r / G.k, i = r - j * G.k;
+    const int x = t / G.no, y = t - x * G.no;
+    const int rr = G.s * x + j - G.p, cc = G.s * y + i - G.p;
+    const T* a = A + b * (long long)G.m * G.n;
+    patches[q] = (rr >= 0 && rr < G.m && cc >= 0 && cc < G.n) ? a[(long long)rr * G.n + cc] : T(0);
+}
+
+// im2col_product (inc/reference.hpp:103-118): out[t] accumulates one patch
+// row at a time, r ascending -- per output the same (j, i) order as direct_conv.
+template <typename T, bool FMA>
+__global__ void __launch_bounds__(256) im2col_product_kernel(const ConvGeom G, const T* __restrict__ taps,
+                                                             const T* __restrict__ patches,
+                                                             T* __restrict__ out) {
+    const long long P = (long long)G.mo * G.no, K2 = (long long)G.k * G.k;
+    const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= P * G.batch) return;
+    const long long b = q / P;
+    const long long t = q - b * P;
+    const T* pb = patches + b * K2 * P + t;
+    T acc = T(0);
+    for (long long r = 0; r < K2; ++r) acc = mac<T, FMA>(taps[r], pb[r * P], acc);
+    out[q] = acc;
+}
+
+template <typename T, bool FMA>
+cudaError_t run_direct(const ConvGeom& g, const void* taps, const void* A, void* out, void* mag, cudaStream_t st) {
+    const long long n = (long long)g.mo * g.no * g.batch;
+    if (n == 0) return cudaSuccess;
+    direct_conv_kernel<T, FMA><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+        g, static_cast<const T*>(taps), static_cast<const T*>(A), static_cast<T*>(out), static_cast<T*>(mag));
+    return cudaGetLastError();
+}
+
+template <typename T, bool FMA>
+cudaError_t run_im2col(const ConvGeom& g, const void* taps, const void* A, void* out, void* patches,
+                       cudaStream_t st) {
+    const long long P = (long long)g.mo * g.no, K2 = (long long)g.k * g.k;
+    if (P * g.batch == 0) return cudaSuccess;
+    im2col_lower_kernel<T><<<(unsigned)((K2 * P * g.batch + 255) / 256), 256, 0, st>>>(
+        g, static_cast<const T*>(A), static_cast<T*>(patches));
+    im2col_product_kernel<T, FMA><<<(unsigned)((P * g.batch + 255) / 256), 256, 0, st>>>(
+        g, static_cast<const T*>(taps), static_cast<const T*>(patches), static_cast<T*>(out));
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_direct_conv(int dtype, int m, int n, int k, int s, int p, long long batch, const void* taps,
+                               const void* A, void* out, void* mag, cudaStream_t st) {
+    const ConvGeom g{m, n, k, s, p, (m + 2 * p - k) / s + 1, (n + 2 * p - k) / s + 1, batch};
+    return dtype == 0 ? run_direct<float, true>(g, taps, A, out, mag, st)
+                      : run_direct<double, false>(g, taps, A, out, mag, st);
+}
+
+cudaError_t launch_im2col_conv(int dtype, int m, int n, int k, int s, int p, long long batch, const void* taps,
+                               const void* A, void* out, void* patches, cudaStream_t st) {
+    const ConvGeom g{m, n, k, s, p, (m + 2 * p - k) / s + 1, (n + 2 * p - k) / s + 1, batch};
+    return dtype == 0 ? run_im2col<float, true>(g, taps, A, out, patches, st)
+                      : run_im2col<double, false>(g, taps, A, out, patches, st);
+}
+
+}  // namespace spb
+
+// ---------------------------------------------------------------------------
+// Host side: the reference's seeded generator (inc/rng.hpp:22-98) and the
+// verification sweep (inc/verify.hpp:59-169) over the device path.
+// ---------------------------------------------------------------------------
+namespace {
+
+uint64_t splitmix64_next(uint64_t& state) {
+    state += 0x9E3779B97F4A7C15ull;
+    uint64_t z = state;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+inline uint64_t rotl64(uint64_t x, int r) { return (x << r) | (x >> (64 - r)); }
+
+// xoshiro256++ seeded by splitmix64, Marsaglia polar normals (two per round).
+struct Normal {
+    uint64_t s[4];
+    bool has_spare = false;
+    double spare = 0.0;
+    explicit Normal(uint64_t seed) {
+        for (auto& w : s) w = splitmix64_next(seed);
+    }
+    uint64_t next_u64() {
+        const uint64_t result = rotl64(s[0] + s[3], 23) + s[0];
+        const uint64_t t = s[1] << 17;
+        s[2] ^= s[0];
+        s[3] ^= s[1];
+        s[1] ^= s[2];
+        s[0] ^= s[3];
+        s[2] ^= t;
+        s[3] = rotl64(s[3], 45);
+        return result;
+    }
+    double uniform01() { return (double)(next_u64() >> 11) * 0x1.0p-53; }
+    double next() {
+        if (has_spare) {
+            has_spare = false;
+            return spare;
+        }
+        double u, v, q;
+        do {
+            u = 2.0 * uniform01() - 1.0;
+            v = 2.0 * uniform01() - 1.0;
+            q = u * u + v * v;
+        } while (q >= 1.0 || q == 0.0);
+        const double f = std::sqrt(-2.0 * std::log(q) / q);
+        spare = v * f;
+        has_spare = true;
+        return u * f;
+    }
+};
+
+uint64_t derive_seed(uint64_t base, uint64_t index) {
+    uint64_t state = base ^ (0x9E3779B97F4A7C15ull * (index + 1));
+    return splitmix64_next(state);
+}
+
+std::vector<double> normals(uint64_t seed, int64_t count) {
+    Normal g(seed);
+    std::vector<double> v((size_t)count);
+    for (auto& x : v) x = g.next();
+    return v;
+}
+
+std::string spec_str(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p) {
+    return "(m=" + std::to_string(m) + ", n=" + std::to_string(n) + ", k=" + std::to_string(k) +
+           ", s=" + std::to_string(s) + ", p=" + std::to_string(p) + ")";
+}
+
+std::string fmt17(double v) {
+    char b[40];
+    std::snprintf(b, sizeof b, "%.17g", v);
+    return b;
+}
+
+// nnz_oracle (inc/analysis.hpp:68-89): brute-force overlap count on the padded grid.
+int64_t nnz_overlap(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p) {
+    const int64_t pc = n + 2 * p, mo = (m + 2 * p - k) / s + 1, no = (n + 2 * p - k) / s + 1;
+    std::vector<char> mask((size_t)((m + 2 * p) * pc), 0);
+    for (int64_t r = 0; r < m; ++r)
+        for (int64_t c = 0; c < n; ++c) mask[(size_t)((r + p) * pc + c + p)] = 1;
+    int64_t total = 0;
+    for (int64_t x = 0; x < mo; ++x)
+        for (int64_t y = 0; y < no; ++y)
+            for (int64_t j = 0; j < k; ++j)
+                for (int64_t i = 0; i < k; ++i) total += mask[(size_t)((s * x + j) * pc + s * y + i)];
+    return total;
+}
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t reserve(size_t bytes) {
+        if (bytes <= cap) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e == cudaSuccess) cap = bytes;
+        return e;
+    }
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+};
+
+}  // namespace
+
+extern "C" {
+
+int spconv_direct_conv(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p, int dtype, const void* taps_dev,
+                       const void* A_dev, void* out_dev, void* mag_dev, int64_t batch, void* stream) {
+    if (int rc = spconv_spec_check(m, n, k, s, p)) return rc;
+    if (dtype != 0 && dtype != 1) return spb_fail(SPCONV_EINVAL, "spconv_direct_conv: dtype must be 0 (f32) or 1 (f64)");
+    if (batch < 0 || (batch > 0 && (!taps_dev || !A_dev || !out_dev)))
+        return spb_fail(SPCONV_EINVAL, "spconv_direct_conv: null buffer or negative batch");
+    const cudaError_t e = spb::launch_direct_conv(dtype, (int)m, (int)n, (int)k, (int)s, (int)p, batch, taps_dev,
+                                                  A_dev, out_dev, mag_dev, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return spb_fail(SPCONV_ECUDA, std::string("direct_conv: ") + cudaGetErrorString(e));
+    return SPCONV_OK;
+}
+
+int spconv_im2col_conv(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p, int dtype, const void* taps_dev,
+                       const void* A_dev, void* out_dev, void* patches_dev, int64_t batch, void* stream) {
+    if (int rc = spconv_spec_check(m, n, k, s, p)) return rc;
+    if (dtype != 0 && dtype != 1) return spb_fail(SPCONV_EINVAL, "spconv_im2col_conv: dtype must be 0 (f32) or 1 (f64)");
+    if (batch < 0 || (batch > 0 && (!taps_dev || !A_dev || !out_dev || !patches_dev)))
+        return spb_fail(SPCONV_EINVAL, "spconv_im2col_conv: null buffer or negative batch");
+    const cudaError_t e = spb::launch_im2col_conv(dtype, (int)m, (int)n, (int)k, (int)s, (int)p, batch, taps_dev,
+                                                  A_dev, out_dev, patches_dev, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return spb_fail(SPCONV_ECUDA, std::string("im2col_conv: ") + cudaGetErrorString(e));
+    return SPCONV_OK;
+}
+
+int spconv_run_verification(int64_t max_dim, int seeds, uint64_t base_seed, int device, int64_t counts[4],
+                            double devs[3], char* failures, int64_t cap) {
+    if (!counts || !devs) return spb_fail(SPCONV_EINVAL, "spconv_run_verification: null argument");
+    if (max_dim < 1 || seeds < 0) return spb_fail(SPCONV_EINVAL, "spconv_run_verification: bad options");
+    int prev = -1;
+    cudaGetDevice(&prev);
+    if (cudaSetDevice(device) != cudaSuccess) return spb_fail(SPCONV_ECUDA, "cudaSetDevice");
+    const double conv_tol = 1e-10;  // fp64 comparators vs each other (VerifyOptions::conv_tol)
+    const double f32_tol = 1e-5;    // fp32 device path, condition-relative (BASELINE north star)
+    const size_t max_failures = 20;
+    int64_t specs = 0, conv_cases = 0, clipped = 0;
+    double max_conv_dev = 0.0, max_rel_dev = 0.0, max_layout_dev = 0.0;
+    std::vector<std::string> fails;
+    auto fail = [&](const std::string& msg) {
+        if (fails.size() < max_failures) fails.push_back(msg);
+    };
+    cudaStream_t st = nullptr;
+    DevBuf b_a32, b_a64, b_k32, b_k64, b_y32c, b_y32s, b_d32, b_ref, b_mag, b_i2c, b_patch;
+    uint64_t case_index = 0;
+    int rc = SPCONV_OK;
+    bool stop = false;  // a CUDA error, or max_failures collected (run_verification returns early)
+    for (int64_t m = 1; m <= max_dim && !stop; ++m)
+        for (int64_t n = 1; n <= max_dim && !stop; ++n)
+            for (int64_t p = 0; p <= 3 && !stop; ++p)
+                for (int64_t s = 1; s <= 3 && !stop; ++s) {
+                    const int64_t k_max = std::min(m, n) + 2 * p;
+                    for (int64_t k = 1; k <= k_max && !stop; ++k) {
+                        ++specs;
+                        const std::string ss = spec_str(m, n, k, s, p);
+                        const int64_t mo = (m + 2 * p - k) / s + 1, no = (n + 2 * p - k) / s + 1;
+                        const int64_t P = mo * no, mn = m * n;
+                        int64_t bound = 0;
+                        spconv_nnz_bound(m, n, k, s, p, &bound);
+                        const int64_t oracle = nnz_overlap(m, n, k, s, p);
+                        if (bound != oracle)
+                            fail("nnz_bound " + std::to_string(bound) + " != oracle " + std::to_string(oracle) +
+                                 " for " + ss);
+                        const int64_t dense = P * k * k;
+                        if (p == 0 && bound != dense)
+                            fail("p=0 bound " + std::to_string(bound) + " != dense " + std::to_string(dense) +
+                                 " for " + ss);
+                        if (bound < 0 || bound > dense) fail("bound outside [0, dense] for " + ss);
+                        {  // clipped: some placement sees only padding (closed form, inc/analysis.hpp:21-52)
+                            bool any0 = false;
+                            for (int64_t x = 0; x < mo && !any0; ++x) {
+                                const int64_t a = std::max<int64_t>(0, k - (std::max<int64_t>(0, p - s * x) +
+                                                                           std::max<int64_t>(0, s * x + k - m - p)));
+                                for (int64_t y = 0; y < no && !any0; ++y) {
+                                    const int64_t c = std::max<int64_t>(0, k - (std::max<int64_t>(0, p - s * y) +
+                                                                               std::max<int64_t>(0, s * y + k - n - p)));
+                                    any0 = a * c == 0;
+                                }
+                            }
+                            if (any0) ++clipped;
+                        }
+                        // The padding-matrix laws (inc/verify.hpp:84-112) concern P, which the
+                        // device build never materialises; their input draw is consumed so the
+                        // conv cases below see the reference's seeds.
+                        if (k == 1 && s == 1) ++case_index;
+                        for (int sd = 0; sd < seeds && !stop; ++sd) {
+                            const uint64_t cs = derive_seed(base_seed, case_index++);
+                            const std::vector<double> a64 = normals(cs, mn);
+                            std::vector<double> k64;
+                            for (int attempt = 0;; ++attempt) {  // detail::nonzero_kernel (:47-55)
+                                k64 = normals(derive_seed(cs, 7) + (uint64_t)attempt, k * k);
+                                bool z = false;
+                                for (double v : k64) z |= v == 0.0;
+                                if (!z) break;
+                            }
+                            std::vector<float> a32(a64.begin(), a64.end()), k32(k64.begin(), k64.end());
+                            // fp64 comparators see the fp32-rounded data the device path sees
+                            std::vector<double> a64r(a32.begin(), a32.end()), k64r(k32.begin(), k32.end());
+                            spconv_csr *tc = nullptr, *tcsc = nullptr;
+                            if (spconv_build_transform(m, n, k, s, p, k32.data(), 0, device, st, &tc) != SPCONV_OK ||
+                                spconv_relayout(tc, 1, st, &tcsc) != SPCONV_OK) {
+                                rc = SPCONV_ECUDA;
+                                stop = true;
+                                if (tc) spconv_csr_free(tc);
+                                break;
+                            }
+                            int64_t rr, cc, nz;
+                            spconv_csr_shape(tc, &rr, &cc, &nz);
+                            if (nz != bound)
+                                fail("nnz(T) " + std::to_string(nz) + " != bound " + std::to_string(bound) + " for " +
+                                     ss);
+                            std::vector<float> ycsr((size_t)P), ycsc((size_t)P), yd32((size_t)P);
+                            std::vector<double> yref((size_t)P), ymag((size_t)P), yi2c((size_t)P);
+                            cudaError_t e = cudaSuccess;
+                            auto ok = [&](cudaError_t x) { return (e = (e == cudaSuccess ? x : e)) == cudaSuccess; };
+                            ok(b_a32.reserve(mn * 4));
+                            ok(b_a64.reserve(mn * 8));
+                            ok(b_k32.reserve(k * k * 4));
+                            ok(b_k64.reserve(k * k * 8));
+                            ok(b_y32c.reserve(P * 4));
+                            ok(b_y32s.reserve(P * 4));
+                            ok(b_d32.reserve(P * 4));
+                            ok(b_ref.reserve(P * 8));
+                            ok(b_mag.reserve(P * 8));
+                            ok(b_i2c.reserve(P * 8));
+                            ok(b_patch.reserve(P * k * k * 8));
+                            ok(cudaMemcpy(b_a32.p, a32.data(), mn * 4, cudaMemcpyHostToDevice));
+                            ok(cudaMemcpy(b_a64.p, a64r.data(), mn * 8, cudaMemcpyHostToDevice));
+                            ok(cudaMemcpy(b_k32.p, k32.data(), k * k * 4, cudaMemcpyHostToDevice));
+                            ok(cudaMemcpy(b_k64.p, k64r.data(), k * k * 8, cudaMemcpyHostToDevice));
+                            int r1 = SPCONV_OK;
+                            if (e == cudaSuccess) {
+                                r1 |= spconv_spmv(tc, (const float*)b_a32.p, (float*)b_y32c.p, st);
+                                r1 |= spconv_spmv(tcsc, (const float*)b_a32.p, (float*)b_y32s.p, st);
+                                r1 |= spconv_direct_conv(m, n, k, s, p, 0, b_k32.p, b_a32.p, b_d32.p, nullptr, 1, st);
+                                r1 |= spconv_direct_conv(m, n, k, s, p, 1, b_k64.p, b_a64.p, b_ref.p, b_mag.p, 1, st);
+                                r1 |= spconv_im2col_conv(m, n, k, s, p, 1, b_k64.p, b_a64.p, b_i2c.p, b_patch.p, 1, st);
+                            }
+                            ok(cudaMemcpy(ycsr.data(), b_y32c.p, P * 4, cudaMemcpyDeviceToHost));
+                            ok(cudaMemcpy(ycsc.data(), b_y32s.p, P * 4, cudaMemcpyDeviceToHost));
+                            ok(cudaMemcpy(yd32.data(), b_d32.p, P * 4, cudaMemcpyDeviceToHost));
+                            ok(cudaMemcpy(yref.data(), b_ref.p, P * 8, cudaMemcpyDeviceToHost));
+                            ok(cudaMemcpy(ymag.data(), b_mag.p, P * 8, cudaMemcpyDeviceToHost));
+                            ok(cudaMemcpy(yi2c.data(), b_i2c.p, P * 8, cudaMemcpyDeviceToHost));
+                            spconv_csr_free(tcsc);
+                            spconv_csr_free(tc);
+                            if (e != cudaSuccess || r1 != SPCONV_OK) {
+                                rc = spb_fail(SPCONV_ECUDA, std::string("verification sweep: ") +
+                                                                (e != cudaSuccess ? cudaGetErrorString(e)
+                                                                                  : "device call failed"));
+                                stop = true;
+                                break;
+                            }
+                            ++conv_cases;
+                            double dev = 0.0, rel = 0.0, ldev = 0.0;
+                            bool exact = true;
+                            for (int64_t t = 0; t < P; ++t) {
+                                dev = std::max(dev, std::fabs(yi2c[t] - yref[t]));
+                                const double d32 = std::fabs((double)ycsr[t] - yref[t]);
+                                dev = std::max(dev, std::max(d32, std::fabs((double)ycsc[t] - yref[t])));
+                                if (ymag[t] > 0) rel = std::max(rel, d32 / ymag[t]);
+                                else if (d32 > 0) rel = INFINITY;
+                                ldev = std::max(ldev, std::fabs((double)ycsr[t] - (double)ycsc[t]));
+                                exact &= std::memcmp(&ycsr[t], &yd32[t], 4) == 0;
+                            }
+                            max_conv_dev = std::max(max_conv_dev, dev);
+                            max_rel_dev = std::max(max_rel_dev, rel);
+                            max_layout_dev = std::max(max_layout_dev, ldev);
+                            double cdev = 0.0;
+                            for (int64_t t = 0; t < P; ++t) cdev = std::max(cdev, std::fabs(yi2c[t] - yref[t]));
+                            if (cdev > conv_tol || rel > f32_tol)
+                                fail("convolution mismatch (dev " + fmt17(dev) + ", rel " + fmt17(rel) + ") for " +
+                                     ss + " seed " + std::to_string(sd));
+                            if (!exact) fail("sparse != fp32 direct_conv for " + ss + " seed " + std::to_string(sd));
+                            if (ldev > 0.0)
+                                fail("CSR/CSC mismatch (dev " + fmt17(ldev) + ") for " + ss + " seed " +
+                                     std::to_string(sd));
+                        }
+                        if (fails.size() >= max_failures) stop = true;
+                    }
+                }
+    if (prev >= 0) cudaSetDevice(prev);
+    if (rc != SPCONV_OK) return rc;
+    counts[0] = specs;
+    counts[1] = conv_cases;
+    counts[2] = clipped;
+    counts[3] = (int64_t)fails.size();
+    devs[0] = max_conv_dev;
+    devs[1] = max_layout_dev;
+    devs[2] = max_rel_dev;
+    if (failures && cap > 0) {
+        std::string all;
+        for (auto& f : fails) all += f + "\n";
+        const size_t nb = std::min<size_t>(all.size(), (size_t)cap - 1);
+        std::memcpy(failures, all.data(), nb);
+        failures[nb] = '\0';
+    }
+    return SPCONV_OK;
+}
+
+}  // extern "C"

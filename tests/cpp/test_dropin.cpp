@@ -134,6 +134,16 @@ int main() {
     }
     expect_throw<std::invalid_argument>([] { layout_from_name("coo"); },
                                         "unknown layout 'coo' (expected csr or csc)");
+    // The verification sweep on the device path (inc/verify.hpp), small grid.
+    {
+        VerifyOptions opt;
+        opt.max_dim = 5;
+        opt.seeds = 1;
+        const VerifyReport rep = run_verification(opt);
+        CHECK(rep.ok());
+        CHECK(rep.specs > 0 && rep.conv_cases == rep.specs && rep.max_layout_dev == 0.0);
+        CHECK(rep.max_rel_dev <= 1e-5);
+    }
     // Errors: the reference's exception types and messages.
     expect_throw<std::invalid_argument>([] { ConvSpec(0, 3, 1, 1, 0); },
                                         "ConvSpec: need m,n,k,s >= 1 and p >= 0, got (m=0");

@@ -201,6 +201,7 @@ def main():
 
     # The reference's own self-test summary (inc/verify.hpp:59-169), small grid.
     js["run_verification_6x1"] = ref.run_verification(6, 1)
+    js["run_verification_12x3"] = ref.run_verification(12, 3)  # VerifyOptions defaults
 
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **npz)
     with open(os.path.join(HERE, "golden.json"), "w") as f:
