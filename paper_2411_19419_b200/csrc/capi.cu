@@ -273,7 +273,7 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
                 sp.batch = (int)std::min<int64_t>(2, batch - b0);
                 CK(spb::launch_spmv_warp(sp, h->k2max, spec, st));
             }
-            h->last_kernel.store(spec ? "csr_spmv_warp<spec>" : "csr_spmv_warp");
+            h->last_kernel.store(spec ? "csr_spmv_bulk<spec>" : "csr_spmv_bulk");
             return SPCONV_OK;
         }
         spb::GenericParams gp{h->row_ptr, h->col_idx, h->vals, X, ldx, Y, ldy, (int)h->rows,
@@ -870,7 +870,8 @@ int spconv_csr_from_host(int64_t rows, int64_t cols, const int64_t* row_ptr,
     const size_t rp_bytes = ((size_t)(rows + 1) * 4 + 255) & ~size_t(255);
     const size_t ix_bytes = (ci.size() * 4 + 255) & ~size_t(255);
     char* csr = nullptr;
-    cudaError_t e = cudaMalloc(&csr, rp_bytes + 2 * ix_bytes);
+    // +256 B: 16-byte bulk copies round a run's end up by up to 12 bytes
+    cudaError_t e = cudaMalloc(&csr, rp_bytes + 2 * ix_bytes + 256);
     if (e != cudaSuccess) {
         delete h;
         return cuda_fail(e, "cudaMalloc(CSR)");

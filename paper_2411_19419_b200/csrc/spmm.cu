@@ -236,68 +236,99 @@ __device__ __forceinline__ int conv_row_start(const SpecParams& P, int r) {
     return cxb * P.sy + (jhi - jlo) * cyb + P.skew;
 }
 
-template <int KMAX, bool SPEC>
-__global__ void __launch_bounds__(128) csr_spmv_warp(const SpecParams P) {
-    constexpr int WARPS = 4;
-    constexpr int RUN = 32 * KMAX;  // max entries of a 32-row run
-    extern __shared__ float smem_sv[];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int r0 = (blockIdx.x * WARPS + warp) * 32;
-    if (r0 >= P.rows) return;
-    const int nr = min(32, P.rows - r0);
-    float* sv = smem_sv + (size_t)warp * RUN * 2;  // vals | cols
-    int* sc = reinterpret_cast<int*>(sv + RUN);
+// Bulk-staged latency SpMV: per warp, ONE elected lane issues three 1-D bulk
+// copies (cp.async.bulk, completing on an mbarrier): row_ptr[r0 .. r0+32] and
+// the (col, val) run of the warp's 32 rows.  For conv transforms with dense
+// taps (SPEC) the run's bounds are closed-form, so all three copies leave at
+// once, with no dependent load; otherwise row_ptr[r0], row_ptr[r0+32] are
+// read first.  The copied row_ptr decides: a mismatch (test hook `skew`, or a
+// matrix that is not its geometry's transform) takes a per-lane reload from
+// global memory.  Programmatic dependent launch: the matrix loads are issued
+// before griddepcontrol.wait, the x gathers and y stores after it, so a
+// PDL-launched SpMV overlaps its matrix fetch with the previous kernel.
+__device__ __forceinline__ void bulk_g2s_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
 
-    int E0 = 0, E1 = 0;
+template <int KMAX>
+struct BulkCfg {
+    static constexpr int WARPS = 4;
+    static constexpr int RUN = 32 * KMAX;                 // max entries of a 32-row run
+    static constexpr int BUFW = (RUN + 3 + 3) / 4 * 4;    // + 16-byte alignment slack
+    static constexpr int RPW = 40;                        // 33 row_ptr words + slack
+    static constexpr size_t WARP_BYTES = (size_t)(RPW + 2 * BUFW) * 4;
+    static constexpr size_t SMEM = 128 + WARPS * WARP_BYTES;
+};
+
+template <int KMAX, bool SPEC>
+__global__ void __launch_bounds__(128) csr_spmv_bulk(const SpecParams P) {
+    using C = BulkCfg<KMAX>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int r0 = (blockIdx.x * C::WARPS + warp) * 32;
+    if (r0 >= P.rows) return;  // warp-uniform; no block-wide barrier follows
+    const int nr = min(32, P.rows - r0);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem) + warp;
+    int* rp = reinterpret_cast<int*>(smem + 128 + (size_t)warp * C::WARP_BYTES);
+    int* cb = rp + C::RPW;
+    float* vb = reinterpret_cast<float*>(cb + C::BUFW);
+
+    int E0, E1;
+    bool issue;
     if (SPEC) {
         E0 = conv_row_start(P, r0);
         E1 = conv_row_start(P, r0 + nr);
+        issue = E0 >= 0 && E1 >= E0 && E1 - E0 <= C::RUN && E1 <= P.nnz;
+    } else {
+        E0 = __ldg(P.row_ptr + r0);
+        E1 = __ldg(P.row_ptr + r0 + nr);
+        if (E1 - E0 > C::RUN) __trap();  // dispatcher guarantees rows of <= KMAX entries
+        issue = true;
     }
-    const int a = lane < nr ? __ldg(P.row_ptr + r0 + lane) : 0;
-    const int end = __ldg(P.row_ptr + r0 + nr);
-    int c[KMAX];
-    float v[KMAX];
-    bool hit = SPEC;
-    if (SPEC) {
-        // Speculative: issued before the row_ptr loads land.
-#pragma unroll
-        for (int u = 0; u < KMAX; ++u) {
-            const int e = E0 + lane + 32 * u;
-            c[u] = e < E1 ? __ldg(P.col_idx + e) : 0;
-            v[u] = e < E1 ? __ldg(P.vals + e) : 0.0f;
-        }
-        hit = __shfl_sync(0xffffffffu, a, 0) == E0 && end == E1;
-    }
-    if (!hit) {
-        E0 = __shfl_sync(0xffffffffu, a, 0);
-        E1 = end;
-        if (E1 - E0 > RUN) __trap();  // dispatcher guarantees rows of <= KMAX entries
-#pragma unroll
-        for (int u = 0; u < KMAX; ++u) {
-            const int e = E0 + lane + 32 * u;
-            c[u] = e < E1 ? __ldg(P.col_idx + e) : 0;
-            v[u] = e < E1 ? __ldg(P.vals + e) : 0.0f;
-        }
-    }
-#pragma unroll
-    for (int u = 0; u < KMAX; ++u) {
-        const int d = lane + 32 * u;
-        if (E0 + d < E1) {
-            sv[d] = v[u];
-            sc[d] = c[u];
+    if (lane == 0) {
+        mbar_init(bar, 1);
+        mbar_fence_init();
+        const int rbase = r0 & ~3;
+        const uint32_t rwords = (uint32_t)((r0 + nr + 1 - rbase + 3) & ~3);
+        const int ebase = E0 & ~3;
+        const uint32_t ewords = issue && E1 > E0 ? (uint32_t)((E1 - ebase + 3) & ~3) : 0u;
+        mbar_expect_tx(bar, 4u * (rwords + 2u * ewords));
+        bulk_g2s_1d(rp, P.row_ptr + rbase, 4u * rwords, bar);
+        if (ewords) {
+            bulk_g2s_1d(cb, P.col_idx + ebase, 4u * ewords, bar);
+            bulk_g2s_1d(vb, P.vals + ebase, 4u * ewords, bar);
         }
     }
     __syncwarp();
-    int b = __shfl_down_sync(0xffffffffu, a, 1);
+    mbar_wait(bar, 0);
+    const int* rps = rp + (r0 & 3);
+    const bool hit = issue && rps[0] == E0 && rps[nr] == E1;
     if (lane >= nr) return;
-    if (lane == nr - 1) b = end;
-    const int d0 = a - E0, cnt = b - a;
-    // Row entries back into registers (this lane's row), then all x gathers at once.
+    const int a = rps[lane], cnt = rps[lane + 1] - a;
+    int c[KMAX];
+    float v[KMAX];
+    if (hit) {
+        const int d0 = a - (E0 & ~3);
 #pragma unroll
-    for (int q = 0; q < KMAX; ++q) {
-        c[q] = q < cnt ? sc[d0 + q] : 0;
-        v[q] = q < cnt ? sv[d0 + q] : 0.0f;
+        for (int q = 0; q < KMAX; ++q) {
+            c[q] = q < cnt ? cb[d0 + q] : 0;
+            v[q] = q < cnt ? vb[d0 + q] : 0.0f;
+        }
+    } else {
+        if (cnt > KMAX) __trap();
+#pragma unroll
+        for (int q = 0; q < KMAX; ++q) {
+            c[q] = q < cnt ? __ldg(P.col_idx + a + q) : 0;
+            v[q] = q < cnt ? __ldg(P.vals + a + q) : 0.0f;
+        }
     }
+    // x may be the previous kernel's output: everything below waits for it.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     for (int bi = 0; bi < P.batch; ++bi) {
         const float* X = P.X + (int64_t)bi * P.ldx;
         float xv[KMAX];
@@ -312,27 +343,35 @@ __global__ void __launch_bounds__(128) csr_spmv_warp(const SpecParams P) {
 }
 
 template <int KMAX>
-static cudaError_t launch_warp_k(const SpecParams& sp, bool spec, cudaStream_t st) {
-    const size_t smem = (size_t)4 * 32 * KMAX * 2 * sizeof(float);
-    auto kern = spec ? csr_spmv_warp<KMAX, true> : csr_spmv_warp<KMAX, false>;
+static cudaError_t launch_bulk_k(const SpecParams& sp, bool spec, cudaStream_t st) {
+    using C = BulkCfg<KMAX>;
+    auto kern = spec ? csr_spmv_bulk<KMAX, true> : csr_spmv_bulk<KMAX, false>;
     static bool attr_set[2][64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
-    if (smem > 48 * 1024 && !attr_set[spec][dev & 63]) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (!attr_set[spec][dev & 63]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
         if (e != cudaSuccess) return e;
         attr_set[spec][dev & 63] = true;
     }
-    const int grid = (int)((sp.rows + 127) / 128);
-    kern<<<grid, 128, smem, st>>>(sp);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)((sp.rows + 32 * C::WARPS - 1) / (32 * C::WARPS)));
+    cfg.blockDim = dim3(32 * C::WARPS);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, sp);
 }
 
 cudaError_t launch_spmv_warp(const SpecParams& sp, int kmax, bool spec, cudaStream_t st) {
     if (sp.batch < 1 || sp.batch > 2) return cudaErrorInvalidValue;
-    if (kmax <= 9) return launch_warp_k<9>(sp, spec, st);
-    if (kmax <= 25) return launch_warp_k<25>(sp, spec, st);
-    if (kmax <= 49) return launch_warp_k<49>(sp, spec, st);
+    if (kmax <= 9) return launch_bulk_k<9>(sp, spec, st);
+    if (kmax <= 25) return launch_bulk_k<25>(sp, spec, st);
+    if (kmax <= 49) return launch_bulk_k<49>(sp, spec, st);
     return cudaErrorInvalidValue;
 }
 

@@ -319,7 +319,7 @@ def test_generic_csr_upload(sp, orc, torch_cuda):
             assert np.array_equal(bits(run_spmm(torch_cuda, sp, t, X[:b], path)), bits(want[:b])), (b, path)
         assert t.last_kernel == "csr_spmv_unrolled"
         assert np.array_equal(bits(run_spmm(torch_cuda, sp, t, X[:b])), bits(want[:b]))
-        assert t.last_kernel == "csr_spmv_warp"
+        assert t.last_kernel == "csr_spmv_bulk"
 
 
 def test_end_to_end_host_path(sp, orc, torch_cuda):
@@ -418,7 +418,7 @@ def test_spmv_spec_mispredicted_rows(sp, orc, torch_cuda, skew):
         Y = run_spmm(torch_cuda, sp, t, X)
     finally:
         del os.environ["SPCONV_B200_SPEC_SKEW"]
-    assert t.last_kernel == "csr_spmv_warp<spec>"
+    assert t.last_kernel == "csr_spmv_bulk<spec>"
     assert np.array_equal(bits(Y), bits(want))
 
 
