@@ -361,6 +361,23 @@ def run_ours(args, cfg):
         dist.barrier()
     sampler.stop()
     kernel = t.last_kernel
+    gather = None
+    if args.gather and world > 1:
+        # the optional final gather of every rank's outputs to rank 0 (NCCL
+        # over NVLink), timed separately from the step: max over ranks
+        from paper_2411_19419_b200.shard import gather_outputs
+        dist.barrier()
+        torch.cuda.synchronize(dev)
+        ge0, ge1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ge0.record(stream)
+        out = gather_outputs(Y[:b], total_batch)  # the result is ordered on the current stream
+        ge1.record(stream)
+        torch.cuda.synchronize(dev)
+        g_ms = max_over_ranks(ge0.elapsed_time(ge1), dev)
+        moved = 4 * (total_batch - b) * rows
+        gather = {"ms": g_ms, "bytes_to_root": moved, "gb_per_s": moved / (g_ms * 1e-3) / 1e9,
+                  "collective": "torch.distributed.gather (NCCL)"}
+        del out
     launches_per_step = kernel.count("+") + 1
     elapsed_ms = sum(ms)
     max_ms = max_over_ranks(elapsed_ms, dev)
@@ -429,6 +446,7 @@ def run_ours(args, cfg):
                     "path": "spconv_convolve_host (C ABI), pinned host buffers"},
             "gpu_launches": args.steps * launches_per_step,
             "clocks": clocks,
+            "gather": gather,
             "secondary": extra,
             "cpu_baseline": cpu,
         }
@@ -539,6 +557,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true", help="skip the config 2/4 extras")
+    ap.add_argument("--gather", action="store_true",
+                    help="N>1: also time the optional final gather of all outputs to rank 0")
     ap.add_argument("--workload", choices=["config", "densenet121"], default="config",
                     help="densenet121: the paper's Table 1 layer-table protocol")
     ap.add_argument("--report", default="", help="densenet121: write the per-layer markdown here")

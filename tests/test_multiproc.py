@@ -57,3 +57,39 @@ def test_gloo_world2_shards_and_max():
     assert [(r[1], r[2]) for r in res] == [(0, 128), (128, 128)]
     assert all(r[3] == 15.0 for r in res)  # max over ranks, seen identically by all
     assert all(r[4] == 256 for r in res)
+
+
+def _gather_worker(rank, world, port, total, q):
+    import torch
+    import torch.distributed as dist
+    from paper_2411_19419_b200.shard import batch_slice, gather_outputs
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    start, count = batch_slice(total, rank, world)
+    # each image b's "output" row is b * 10 + column index
+    Y = torch.arange(start, start + count, dtype=torch.float32)[:, None] * 10 + torch.arange(6.0)[None]
+    out = gather_outputs(Y, total)
+    q.put((rank, None if out is None else out.tolist()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("total", [7, 8])
+def test_gloo_world2_final_gather(total):
+    """The optional final gather puts every rank's slice on rank 0 in batch
+    order (ragged slices included); other ranks get None."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, world, port, total, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    res = dict(q.get(timeout=10) for _ in range(world))
+    assert res[1] is None
+    want = [[b * 10.0 + c for c in range(6)] for b in range(total)]
+    assert res[0] == want
