@@ -24,6 +24,9 @@
 // counts finishes row_ptr.  Entries are staged in shared memory at the global
 // offset's alignment and written back with 16-byte streaming stores, so HBM
 // sees each of the 8*nnz + 4*(rows+1) bytes exactly once.
+#include <cstdlib>
+#include <cstring>
+
 #include "internal.h"
 
 namespace spb {
@@ -216,6 +219,124 @@ __global__ void __launch_bounds__(256) csr_build_kernel(const BuildParams P) {
     }
 }
 
+
+// Warp-local variant (the default for the unrolled k): each warp owns 32
+// consecutive rows, finds its global offset in closed form (lanes over the k
+// tap indices, a warp reduction), scans its counts with shuffles, stages its
+// entries in its own shared-memory slice and streams them out with 16-byte
+// stores -- no block-wide barrier after the table load, so a warp never waits
+// for the slowest warp of its CTA (the block version's dominant stall).
+template <int KC, bool DENSE>
+__global__ void __launch_bounds__(256) csr_build_warp(const BuildParams P) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int K1 = KC + 1, KK = KC * KC;
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    int32_t* s_sat = reinterpret_cast<int32_t*>(smem);
+    float* s_taps = reinterpret_cast<float*>(s_sat + K1 * K1);
+    constexpr int TAB_WORDS = (K1 * K1 + KK + 3) & ~3;
+    for (int q = t; q < K1 * K1; q += blockDim.x) s_sat[q] = P.small ? P.tab.sat[q] : __ldg(P.t.sat + q);
+    for (int q = t; q < KK; q += blockDim.x) s_taps[q] = P.small ? P.tab.taps[q] : __ldg(P.t.taps + q);
+    __syncthreads();
+    if (blockIdx.x == 0 && P.taps_out)
+        for (int q = t; q < KK; q += blockDim.x) P.taps_out[q] = s_taps[q];
+
+    const int r0 = (blockIdx.x * (blockDim.x >> 5) + wid) * 32;
+    if (r0 >= P.rows) return;
+    const int r = r0 + lane;
+    int cnt = 0, x = 0, y = 0, jlo = 0, jhi = 0, ilo = 0, ihi = 0;
+    if (r < P.rows) {
+        x = r / P.no;
+        y = r - x * P.no;
+        tap_range(x, P.m, KC, P.s, P.p, jlo, jhi);
+        tap_range(y, P.n, KC, P.s, P.p, ilo, ihi);
+        cnt = DENSE ? (jhi - jlo) * (ihi - ilo) : sat_rect(s_sat, K1, jlo, jhi, ilo, ihi);
+    }
+    // closed-form global offset of row r0 = (x0, y0)
+    const int x0 = r0 / P.no, y0 = r0 - x0 * P.no;
+    long long part = 0;
+    if (lane < KC) {
+        int jlo0, jhi0;
+        tap_range(x0, P.m, KC, P.s, P.p, jlo0, jhi0);
+        const long long wj = P.small ? P.tab.w[lane] : __ldg(P.t.w + lane);
+        part = wj * slides_before(x0, lane, P.m, P.s, P.p) +
+               (long long)sat_rect(s_sat, K1, jlo0, jhi0, lane, lane + 1) * slides_before(y0, lane, P.n, P.s, P.p);
+    }
+    const int base = (int)warp_sum64(part);
+    const int inc = warp_incl_scan(cnt);
+    const int excl = inc - cnt;
+    const int total = __shfl_sync(0xffffffffu, inc, 31);
+    if (r < P.rows) {
+        P.row_ptr[r] = base + excl;
+        if (r == P.rows - 1) P.row_ptr[P.rows] = base + excl + cnt;
+    }
+    // stage this warp's entries at the global offset's 16-byte phase
+    const int mis = base & 3;
+    int32_t* dcol = reinterpret_cast<int32_t*>(smem) + TAB_WORDS + wid * 2 * P.stage_words;
+    float* dval = reinterpret_cast<float*>(dcol + P.stage_words);
+    int o = mis + excl;
+    if (r < P.rows && cnt > 0) {
+        const int xr = P.s * x - P.p, yc = P.s * y - P.p;
+#pragma unroll
+        for (int j = 0; j < KC; ++j) {
+            const int rowbase = (xr + j) * P.n + yc;
+            const bool jin = j >= jlo && j < jhi;
+#pragma unroll
+            for (int i = 0; i < KC; ++i) {
+                const float v = s_taps[j * KC + i];
+                const bool keep = jin && i >= ilo && i < ihi && (DENSE || v != 0.0f);
+                if (keep) {
+                    dcol[o] = rowbase + i;
+                    dval[o] = v;
+                }
+                o += keep ? 1 : 0;
+            }
+        }
+    }
+    __syncwarp();
+    const int head = min(total, (4 - mis) & 3);
+    if (lane < head) {
+        __stcs(P.col_idx + base + lane, dcol[mis + lane]);
+        __stcs(P.vals + base + lane, dval[mis + lane]);
+    }
+    const int nvec = (total - head) >> 2;
+    const int4* scol = reinterpret_cast<const int4*>(dcol + mis + head);
+    const float4* sval = reinterpret_cast<const float4*>(dval + mis + head);
+    int4* gcol = reinterpret_cast<int4*>(P.col_idx + base + head);
+    float4* gval = reinterpret_cast<float4*>(P.vals + base + head);
+    for (int q = lane; q < nvec; q += 32) {
+        __stcs(gcol + q, scol[q]);
+        __stcs(gval + q, sval[q]);
+    }
+    const int done = head + 4 * nvec;
+    if (lane < total - done) {
+        __stcs(P.col_idx + base + done + lane, dcol[mis + done + lane]);
+        __stcs(P.vals + base + done + lane, dval[mis + done + lane]);
+    }
+}
+
+template <int KC, bool DENSE>
+static cudaError_t launch_w(BuildParams bp, cudaStream_t st) {
+    constexpr int KK = KC * KC;
+    const size_t tab_bytes = (size_t)(((KC + 1) * (KC + 1) + KK + 3) & ~3) * 4;
+    bp.stage_words = (32 * KK + 3 + 3) & ~3;
+    const size_t per_warp = (size_t)bp.stage_words * 8;
+    int warps = 8;
+    while (warps > 1 && tab_bytes + warps * per_warp > 100 * 1024) warps >>= 1;
+    const size_t smem = tab_bytes + warps * per_warp;
+    static bool attr[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (smem > 48 * 1024 && !attr[dev & 63]) {
+        cudaError_t e = cudaFuncSetAttribute(csr_build_warp<KC, DENSE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             100 * 1024 + (int)tab_bytes);
+        if (e != cudaSuccess) return e;
+        attr[dev & 63] = true;
+    }
+    const long long grid = ((long long)bp.rows + 32 * warps - 1) / (32 * warps);
+    csr_build_warp<KC, DENSE><<<(unsigned)grid, 32 * warps, smem, st>>>(bp);
+    return cudaGetLastError();
+}
+
 template <int KC, bool DENSE>
 static cudaError_t launch_k(const BuildParams& bp, int block, size_t smem, cudaStream_t st) {
     if (smem > 48 * 1024) {
@@ -230,6 +351,22 @@ static cudaError_t launch_k(const BuildParams& bp, int block, size_t smem, cudaS
 
 cudaError_t launch_csr_build(const BuildParams& bp, bool dense, int block, size_t smem,
                              cudaStream_t st) {
+    // Warp-local build for k >= 7 (config 4: 349 -> 329 us); for small k the
+    // per-warp closed form costs more instructions than the block barriers it
+    // removes (config 3: 27.6 -> 31.7 us), so the block kernel stays
+    // (profiles/r01k/exp.txt).  SPCONV_B200_BUILD=block|warp overrides.
+    const char* bsel = std::getenv("SPCONV_B200_BUILD");
+    const bool warp_build = bsel ? !std::strcmp(bsel, "warp") : bp.k >= 7;
+    if (warp_build) {
+        switch (bp.k) {
+            case 1: return dense ? launch_w<1, true>(bp, st) : launch_w<1, false>(bp, st);
+            case 3: return dense ? launch_w<3, true>(bp, st) : launch_w<3, false>(bp, st);
+            case 5: return dense ? launch_w<5, true>(bp, st) : launch_w<5, false>(bp, st);
+            case 7: return dense ? launch_w<7, true>(bp, st) : launch_w<7, false>(bp, st);
+            case 11: return dense ? launch_w<11, true>(bp, st) : launch_w<11, false>(bp, st);
+            default: break;
+        }
+    }
     if (bp.stage) {  // the unrolled fill needs the staging area's K*K slots per row
         switch (bp.k) {
             case 1: return dense ? launch_k<1, true>(bp, block, smem, st) : launch_k<1, false>(bp, block, smem, st);
