@@ -20,6 +20,9 @@
 //   conv_spmm_banded (spmm_banded.cu).
 // csr_spmm_generic -- any CSR (uploaded host matrices): thread per (row,
 //   image), x gathered through L1.
+#include <cstdlib>
+#include <cstring>
+
 #include "internal.h"
 #include "tma.cuh"
 
@@ -264,7 +267,7 @@ struct BulkCfg {
     static constexpr size_t SMEM = 128 + WARPS * WARP_BYTES;
 };
 
-template <int KMAX, bool SPEC>
+template <int KMAX, bool SPEC, bool BULK>
 __global__ void __launch_bounds__(128) csr_spmv_bulk(const SpecParams P) {
     using C = BulkCfg<KMAX>;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -290,22 +293,48 @@ __global__ void __launch_bounds__(128) csr_spmv_bulk(const SpecParams P) {
         if (E1 - E0 > C::RUN) __trap();  // dispatcher guarantees rows of <= KMAX entries
         issue = true;
     }
-    if (lane == 0) {
-        mbar_init(bar, 1);
-        mbar_fence_init();
-        const int rbase = r0 & ~3;
-        const uint32_t rwords = (uint32_t)((r0 + nr + 1 - rbase + 3) & ~3);
-        const int ebase = E0 & ~3;
-        const uint32_t ewords = issue && E1 > E0 ? (uint32_t)((E1 - ebase + 3) & ~3) : 0u;
-        mbar_expect_tx(bar, 4u * (rwords + 2u * ewords));
-        bulk_g2s_1d(rp, P.row_ptr + rbase, 4u * rwords, bar);
-        if (ewords) {
-            bulk_g2s_1d(cb, P.col_idx + ebase, 4u * ewords, bar);
-            bulk_g2s_1d(vb, P.vals + ebase, 4u * ewords, bar);
+    const int rbase = r0 & ~3;
+    const uint32_t rwords = (uint32_t)((r0 + nr + 1 - rbase + 3) & ~3);
+    const int ebase = E0 & ~3;
+    const uint32_t ewords = issue && E1 > E0 ? (uint32_t)((E1 - ebase + 3) & ~3) : 0u;
+    if (BULK) {  // one elected lane, three bulk copies on an mbarrier
+        if (lane == 0) {
+            mbar_init(bar, 1);
+            mbar_fence_init();
+            mbar_expect_tx(bar, 4u * (rwords + 2u * ewords));
+            bulk_g2s_1d(rp, P.row_ptr + rbase, 4u * rwords, bar);
+            if (ewords) {
+                bulk_g2s_1d(cb, P.col_idx + ebase, 4u * ewords, bar);
+                bulk_g2s_1d(vb, P.vals + ebase, 4u * ewords, bar);
+            }
         }
+        __syncwarp();
+        mbar_wait(bar, 0);
+    } else {  // every lane: 16-byte loads, all in flight, then shared stores
+        constexpr int NV = (C::BUFW / 4 + 31) / 32;
+        const int nv = (int)(ewords >> 2);
+        int4 cr[NV], vr[NV];
+#pragma unroll
+        for (int u = 0; u < NV; ++u) {
+            const int q = lane + 32 * u;
+            if (q < nv) {
+                cr[u] = __ldg(reinterpret_cast<const int4*>(P.col_idx + ebase) + q);
+                vr[u] = __ldg(reinterpret_cast<const int4*>(P.vals + ebase) + q);
+            }
+        }
+        const int rq = (int)(rwords >> 2);
+        int4 rr = lane < rq ? __ldg(reinterpret_cast<const int4*>(P.row_ptr + rbase) + lane) : make_int4(0, 0, 0, 0);
+#pragma unroll
+        for (int u = 0; u < NV; ++u) {
+            const int q = lane + 32 * u;
+            if (q < nv) {
+                reinterpret_cast<int4*>(cb)[q] = cr[u];
+                reinterpret_cast<int4*>(vb)[q] = vr[u];
+            }
+        }
+        if (lane < rq) reinterpret_cast<int4*>(rp)[lane] = rr;
+        __syncwarp();
     }
-    __syncwarp();
-    mbar_wait(bar, 0);
     const int* rps = rp + (r0 & 3);
     const bool hit = issue && rps[0] == E0 && rps[nr] == E1;
     if (lane >= nr) return;
@@ -345,14 +374,20 @@ __global__ void __launch_bounds__(128) csr_spmv_bulk(const SpecParams P) {
 template <int KMAX>
 static cudaError_t launch_bulk_k(const SpecParams& sp, bool spec, cudaStream_t st) {
     using C = BulkCfg<KMAX>;
-    auto kern = spec ? csr_spmv_bulk<KMAX, true> : csr_spmv_bulk<KMAX, false>;
-    static bool attr_set[2][64] = {};
+    // staging: per-lane 16-byte loads (default; config 2 14.6 vs 16.0 us, DenseNet
+    // table 144 vs 151 us, profiles/r01l) or bulk copies (SPCONV_B200_STAGE=bulk)
+    const char* sel = std::getenv("SPCONV_B200_STAGE");
+    const bool bulk = sel && !std::strcmp(sel, "bulk");
+    auto kern = spec ? (bulk ? csr_spmv_bulk<KMAX, true, true> : csr_spmv_bulk<KMAX, true, false>)
+                     : (bulk ? csr_spmv_bulk<KMAX, false, true> : csr_spmv_bulk<KMAX, false, false>);
+    static bool attr_set[4][64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
-    if (!attr_set[spec][dev & 63]) {
+    const int which = (spec ? 2 : 0) + (bulk ? 1 : 0);
+    if (!attr_set[which][dev & 63]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
         if (e != cudaSuccess) return e;
-        attr_set[spec][dev & 63] = true;
+        attr_set[which][dev & 63] = true;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)((sp.rows + 32 * C::WARPS - 1) / (32 * C::WARPS)));

@@ -466,3 +466,23 @@ def test_band_check_reads_the_matrix(sp, orc, torch_cuda, spec):
     want = orc.spmm_native(ptr, idx, val, X)
     assert not np.array_equal(bits(want), bits(clean))
     assert np.array_equal(bits(Y), bits(want))
+
+
+@pytest.mark.parametrize("variant", ["block", "warp"])
+def test_build_variants_bitexact(sp, orc, variant):
+    """Both CSR build kernels (block scan / warp-local, SPCONV_B200_BUILD) give
+    the oracle's arrays for every unrolled k, dense and zero-tap kernels."""
+    rng = np.random.default_rng(21)
+    os.environ["SPCONV_B200_BUILD"] = variant
+    try:
+        for spec in [(70, 45, 1, 1, 1), (130, 97, 3, 1, 1), (64, 80, 5, 2, 2), (101, 77, 7, 2, 3),
+                     (48, 50, 11, 3, 10), (33, 20, 3, 2, 0)]:
+            k = spec[2]
+            for zero in (False, True):
+                kern = rng.standard_normal(k * k).astype(np.float32)
+                if zero:
+                    kern[rng.random(k * k) < 0.3] = 0.0
+                t = build(sp, spec, kern)
+                assert_same_csr(t, orc.build_native(*spec, kern))
+    finally:
+        del os.environ["SPCONV_B200_BUILD"]
