@@ -172,13 +172,12 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // Kernel-path selection: SPCONV_B200_PATH = auto (default) | spmv | spmv_plain |
-// banded | tiled | tiled_notma | generic (| banded1: the previous band kernel,
-// kept for A/B timing).  auto = the latency kernels for batch <= 2 (speculative
-// conv_spmv_spec for dense-tap transforms, else csr_spmv_unrolled), else the
+// banded | tiled | tiled_notma | generic.  auto = the latency kernel for batch <= 2
+// (csr_spmv_bulk: closed-form row runs for dense-tap transforms), else the
 // band path (CSR band check + register-blocked apply) when instantiated for
 // (k, s) with dense taps, else tiled (TMA when the strides allow); generic for
 // uploaded matrices.  The overrides exist for cross-checking the paths.
-enum Path { kAuto = 0, kBanded, kTiled, kTiledNoTma, kGeneric, kSpmv, kBanded1, kSpmvPlain };
+enum Path { kAuto = 0, kBanded, kTiled, kTiledNoTma, kGeneric, kSpmv, kSpmvPlain };
 
 Path path_override() {
     const char* e = std::getenv("SPCONV_B200_PATH");
@@ -188,7 +187,6 @@ Path path_override() {
     if (!std::strcmp(e, "tiled_notma")) return kTiledNoTma;
     if (!std::strcmp(e, "generic")) return kGeneric;
     if (!std::strcmp(e, "spmv")) return kSpmv;
-    if (!std::strcmp(e, "banded1")) return kBanded1;
     if (!std::strcmp(e, "spmv_plain")) return kSpmvPlain;
     return kAuto;
 }
@@ -320,40 +318,6 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
         CK(spb::launch_band_check((int)g.k, (int)g.s, bp, st, sms));
         CK(spb::launch_band((int)g.k, (int)g.s, bp, &tmap, st, nullptr, sms));
         h->last_kernel.store("conv_band_check+conv_spmm_band");
-        return SPCONV_OK;
-    }
-
-    // ---- legacy banded kernel (A/B experiments only: SPCONV_B200_PATH=banded1) ----
-    const bool banded_geom = h->is_conv && spb::banded_supported((int)g.k, (int)g.s) && tma_ok;
-    if (force == kBanded1 && banded_geom) {
-        spb::BandedShape sh{};
-        spb::BandedParams bp{};
-        CK(spb::launch_banded((int)g.k, (int)g.s, bp, nullptr, st, &sh));
-        bp.row_ptr = h->row_ptr;
-        bp.col_idx = h->col_idx;
-        bp.vals = h->vals;
-        bp.X = X;
-        bp.ldx = ldx;
-        bp.Y = Y;
-        bp.ldy = ldy;
-        bp.batch = (int)batch;
-        bp.m = (int)g.m;
-        bp.n = (int)g.n;
-        bp.p = (int)g.p;
-        bp.mo = (int)g.mo;
-        bp.no = (int)g.no;
-        bp.tiles_y = (int)((g.no + 31) / 32);
-        const int64_t tiles = ((g.mo + sh.th - 1) / sh.th) * bp.tiles_y;
-        const int64_t groups = (batch + sh.bt - 1) / sh.bt;
-        const int64_t want = 16ll * device_sm_count();
-        int64_t splits = (want + tiles - 1) / tiles;
-        splits = std::max<int64_t>(1, std::min<int64_t>(splits, groups / 2));
-        bp.splits = (int)splits;
-        bp.diag = 0;
-        CUtensorMap tmap;
-        if (int rc = encode_x_map(&tmap, X, g, ldx, batch, sh.wc, sh.wr, sh.bt)) return rc;
-        CK(spb::launch_banded((int)g.k, (int)g.s, bp, &tmap, st, nullptr));
-        h->last_kernel.store("conv_spmm_banded");
         return SPCONV_OK;
     }
 

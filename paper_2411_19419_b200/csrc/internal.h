@@ -77,26 +77,6 @@ struct TiledParams {
     int use_tma;
 };
 
-// Register-blocked conv SpMM (spmm_banded.cu).
-struct BandedParams {
-    const int32_t* row_ptr;
-    const int32_t* col_idx;
-    const float* vals;
-    const float* X;
-    int64_t ldx;
-    float* Y;
-    int64_t ldy;
-    int batch;
-    int m, n, p, mo, no;
-    int tiles_y;  // tiles across n_out (tile width 32)
-    int splits;   // batch splits per tile
-    int diag;     // diagnostics only (SPCONV_B200_DIAG): 1 = time the kernel without the band check
-};
-
-struct BandedShape {
-    int th, wr, wc, bt, smem, threads;
-};
-
 // Two-kernel conv SpMM (spmm_band.cu): band check + register-blocked apply.
 struct BandParams {
     const int32_t* row_ptr;
@@ -158,9 +138,6 @@ cudaError_t launch_tiled(const TiledParams& tp, const CUtensorMap* tmap, int bt,
 cudaError_t launch_generic(const GenericParams& gp, cudaStream_t st);
 cudaError_t launch_spmv_unrolled(const GenericParams& gp, int kmax, cudaStream_t st);
 cudaError_t launch_spmv_warp(const SpecParams& sp, int kmax, bool spec, cudaStream_t st);
-bool banded_supported(int k, int s);
-cudaError_t launch_banded(int k, int s, const BandedParams& bp, const CUtensorMap* tmap,
-                          cudaStream_t st, BandedShape* shape);
 
 bool band_supported(int k, int s);
 int band_tile_width(int k, int s);

@@ -17,9 +17,11 @@
 //   TMA 3-D box load (cols x rows x images; out-of-range coordinates
 //   zero-fill), multi-buffered on mbarriers; each thread accumulates its row
 //   for BT images.  The register-blocked fast path for the common geometries is
-//   conv_spmm_banded (spmm_banded.cu).
+//   conv_band_check + conv_spmm_band (spmm_band.cu).
 // csr_spmm_generic -- any CSR (uploaded host matrices): thread per (row,
 //   image), x gathered through L1.
+// csr_spmv_bulk -- the latency kernel for batch <= 2 (below).
+// csr_spmv_unrolled -- thread per row, a cross-check path (SPCONV_B200_PATH=spmv_plain).
 #include <cstdlib>
 #include <cstring>
 

@@ -486,3 +486,28 @@ def test_build_variants_bitexact(sp, orc, variant):
                 assert_same_csr(t, orc.build_native(*spec, kern))
     finally:
         del os.environ["SPCONV_B200_BUILD"]
+
+
+@pytest.mark.parametrize("stage", ["bulk", "lsu"])
+def test_latency_spmv_staging_variants(sp, orc, torch_cuda, stage):
+    """Both stagings of the latency SpMV (bulk copies / per-lane 16-byte
+    loads, SPCONV_B200_STAGE), dense-tap (closed-form run) and zero-tap
+    (row_ptr-driven) transforms, batch 1 and 2: bit-exact."""
+    rng = np.random.default_rng(31)
+    os.environ["SPCONV_B200_STAGE"] = stage
+    try:
+        for spec in [(512, 512, 5, 2, 2), (97, 130, 3, 1, 1), (64, 72, 7, 2, 3), (33, 35, 5, 3, 4)]:
+            m, n, k = spec[:3]
+            kern, X = problem(orc, 51, m, n, k, batch=2)
+            for zero in (False, True):
+                kv = kern.copy()
+                if zero:
+                    kv[rng.random(k * k) < 0.3] = 0.0
+                t = build(sp, spec, kv)
+                want = orc.spmm_native(*orc.build_native(*spec, kv), X)
+                for b in (1, 2):
+                    Y = run_spmm(torch_cuda, sp, t, X[:b])
+                    assert t.last_kernel.startswith("csr_spmv_bulk")
+                    assert np.array_equal(bits(Y), bits(want[:b])), (spec, zero, b)
+    finally:
+        del os.environ["SPCONV_B200_STAGE"]
