@@ -323,16 +323,19 @@ def secondary(sp, torch, dev, stream, steps):
                 sp.spmm(t, Xw[i:i + 1], Yw[i:i + 1], stream=stream)
             torch.cuda.synchronize(dev)
             # one CUDA graph of the 64 launches: host enqueue cost out of the timing
+            cs = torch.cuda.Stream(dev)  # graphs are captured on a side stream
             g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=stream):
+            with torch.cuda.graph(g, stream=cs):
                 for i in range(64):
-                    sp.spmm(t, Xw[i % 8:i % 8 + 1], Yw[i % 8:i % 8 + 1], stream=stream)
-            g.replay()
+                    sp.spmm(t, Xw[i % 8:i % 8 + 1], Yw[i % 8:i % 8 + 1], stream=cs)
+            with torch.cuda.stream(cs):
+                g.replay()
             torch.cuda.synchronize(dev)
             w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            w0.record(stream)
-            g.replay()
-            w1.record(stream)
+            with torch.cuda.stream(cs):
+                w0.record(cs)
+                g.replay()
+                w1.record(cs)
             torch.cuda.synchronize(dev)
             wm = w0.elapsed_time(w1) / 64
             del g

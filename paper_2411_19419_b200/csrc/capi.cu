@@ -264,7 +264,7 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
             sp.sy = (int)h->sy;
             const char* sk = std::getenv("SPCONV_B200_SPEC_SKEW");
             sp.skew = sk ? std::atoi(sk) : 0;
-            const bool spec = h->is_conv && h->taps_dense;
+            const bool spec = h->is_conv && h->taps_dense && g.k <= 16;  // conv_run_bounds: k <= 16 lanes
             for (int64_t b0 = 0; b0 < batch; b0 += 2) {  // <= 2 images per launch
                 sp.X = X + b0 * ldx;
                 sp.Y = Y + b0 * ldy;

@@ -259,6 +259,31 @@ __device__ __forceinline__ void bulk_g2s_1d(void* dst, const void* src, uint32_t
         : "memory");
 }
 
+// Both bounds of a warp's run at once, lane-parallel: lanes 0..15 work on row
+// ra, lanes 16..31 on row rb, lane j of a half on tap index j (k <= 16); two
+// 16-lane reductions replace the 2 x k sequential slides_before terms.
+__device__ __forceinline__ void conv_run_bounds(const SpecParams& P, int ra, int rb, int& Ea, int& Eb) {
+    const int lane = threadIdx.x & 31;
+    const int j = lane & 15;
+    const int r = lane < 16 ? ra : rb;
+    const int rr = min(r, P.rows - 1);
+    const int x = rr / P.no, y = rr - x * P.no;
+    int tx = 0, ty = 0;
+    if (j < P.k) {
+        tx = slides_before_dev(x, j, P.m, P.s, P.p);
+        ty = slides_before_dev(y, j, P.n, P.s, P.p);
+    }
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) {
+        tx += __shfl_xor_sync(0xffffffffu, tx, o);
+        ty += __shfl_xor_sync(0xffffffffu, ty, o);
+    }
+    const int jlo = min(max(0, P.p - P.s * x), P.k), jhi = max(jlo, min(P.k, P.m + P.p - P.s * x));
+    const int E = r >= P.rows ? P.nnz : tx * P.sy + (jhi - jlo) * ty + P.skew;
+    Ea = __shfl_sync(0xffffffffu, E, 0);
+    Eb = __shfl_sync(0xffffffffu, E, 16);
+}
+
 template <int KMAX>
 struct BulkCfg {
     static constexpr int WARPS = 4;
@@ -286,8 +311,7 @@ __global__ void __launch_bounds__(128) csr_spmv_bulk(const SpecParams P) {
     int E0, E1;
     bool issue;
     if (SPEC) {
-        E0 = conv_row_start(P, r0);
-        E1 = conv_row_start(P, r0 + nr);
+        conv_run_bounds(P, r0, r0 + nr, E0, E1);
         issue = E0 >= 0 && E1 >= E0 && E1 - E0 <= C::RUN && E1 <= P.nnz;
     } else {
         E0 = __ldg(P.row_ptr + r0);
