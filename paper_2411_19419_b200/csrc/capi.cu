@@ -484,7 +484,9 @@ int attach_csc_conv(spconv_csr* h, cudaStream_t st) {
     cp.row_idx = h->csc_idx;
     cp.vals = h->csc_vals;
     const int64_t per_axis = std::min<int64_t>(g.k, (g.k + g.s - 1) / g.s);
-    CK(spb::launch_csc_build(cp, (int)(per_axis * per_axis), st));
+    bool nonzero = true;
+    for (float v : h->host_taps) nonzero &= v != 0.0f;
+    CK(spb::launch_csc_build(cp, (int)(per_axis * per_axis), nonzero && !h->host_taps.empty(), st));
     return SPCONV_OK;
 }
 
@@ -961,7 +963,10 @@ int spconv_convolve_host(const spconv_csr* hc, const float* X_host, float* Y_hos
     if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
     // Chunks of ~64 MB of input, double-buffered: H2D(c+1) || spmm(c) || D2H(c-1).
     const int64_t per_img = std::max<int64_t>(h->cols, 1) * 4;
-    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(batch, (64ll << 20) / per_img));
+    static const int64_t chunk_bytes = std::getenv("SPCONV_B200_E2E_CHUNK_MB")
+                                           ? std::atoll(std::getenv("SPCONV_B200_E2E_CHUNK_MB")) << 20
+                                           : (64ll << 20);
+    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(batch, chunk_bytes / per_img));
     if (h->ws_chunk < chunk) {
         free_ws(h);
         for (int s = 0; s < 3; ++s) {

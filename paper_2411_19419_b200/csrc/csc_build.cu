@@ -57,12 +57,14 @@ __device__ __forceinline__ void tap_set(int a, int k, int s, int p, int mo, int&
 
 }  // namespace
 
+// KC = compile-time kernel side (0: runtime P.k); DENSE: no zero taps.
+template <int KC, bool DENSE>
 __global__ void __launch_bounds__(256) csc_build_kernel(const CscParams P) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int s_warp[32];
     __shared__ long long s_base;
     const int t = threadIdx.x, R = blockDim.x, nw = R >> 5, lane = t & 31, wid = t >> 5;
-    const int k = P.k, kk = k * k;
+    const int k = KC ? KC : P.k, kk = k * k, S = P.s;
     float* s_taps = reinterpret_cast<float*>(smem);
     const int tab_words = (kk + 3) & ~3;
     for (int q = t; q < kk; q += R) s_taps[q] = __ldg(P.taps + q);
@@ -71,31 +73,41 @@ __global__ void __launch_bounds__(256) csc_build_kernel(const CscParams P) {
 
     const int c0 = blockIdx.x * R;
     const int c = c0 + t;
-    int a = 0, b = 0, cnt = 0, jtop = -1, jbot = 0, itop = -1, ibot = 0;
+    // J(a) = {jtop, jtop - s, ...} down to > jlo; x runs up from x_top as j steps down
+    int a = 0, b = 0, cnt = 0, jtop = -1, jlo = 0, itop = -1, ilo = 0;
     if (c < P.cols) {
         a = c / P.n;
         b = c - a * P.n;
-        tap_set(a, k, P.s, P.p, P.mo, jtop, jbot);
-        tap_set(b, k, P.s, P.p, P.no, itop, ibot);
-        for (int j = jtop; j > jbot && j >= 0; j -= P.s)
-            for (int i = itop; i > ibot && i >= 0; i -= P.s) cnt += s_taps[j * k + i] != 0.0f ? 1 : 0;
+        int jbot, ibot;
+        tap_set(a, k, S, P.p, P.mo, jtop, jbot);
+        tap_set(b, k, S, P.p, P.no, itop, ibot);
+        jlo = max(jbot, -1);
+        ilo = max(ibot, -1);
+        const int nj = jtop > jlo ? (jtop - jlo - 1) / S + 1 : 0;
+        const int ni = itop > ilo ? (itop - ilo - 1) / S + 1 : 0;
+        if (DENSE) {
+            cnt = nj * ni;
+        } else {
+            for (int j = jtop; j > jlo; j -= S)
+                for (int i = itop; i > ilo; i -= S) cnt += s_taps[j * k + i] != 0.0f ? 1 : 0;
+        }
     }
 
     // ---- closed-form global offset of column c0 = (a0, b0): warp 0, lanes over j ----
     if (wid == 0) {
         const int a0 = c0 / P.n, b0 = c0 - a0 * P.n;
         int jt0, jb0;
-        tap_set(a0, k, P.s, P.p, P.mo, jt0, jb0);
+        tap_set(a0, k, S, P.p, P.mo, jt0, jb0);
         long long part = 0;
         for (int j = lane; j < k; j += 32) {
             long long rt = 0, rb = 0;
             for (int i = 0; i < k; ++i) {
-                if (s_taps[j * k + i] == 0.0f) continue;
-                rt += slide_count(i, 0, P.n, P.no, P.s, P.p);
-                rb += slide_count(i, 0, b0, P.no, P.s, P.p);
+                if (!DENSE && s_taps[j * k + i] == 0.0f) continue;
+                rt += slide_count(i, 0, P.n, P.no, S, P.p);
+                rb += slide_count(i, 0, b0, P.no, S, P.p);
             }
-            part += rt * slide_count(j, 0, a0, P.mo, P.s, P.p);
-            const bool in_a0 = j <= jt0 && j > jb0 && ((jt0 - j) % P.s) == 0;
+            part += rt * slide_count(j, 0, a0, P.mo, S, P.p);
+            const bool in_a0 = j <= jt0 && j > jb0 && ((jt0 - j) % S) == 0;
             if (in_a0) part += rb;
         }
 #pragma unroll
@@ -121,7 +133,7 @@ __global__ void __launch_bounds__(256) csc_build_kernel(const CscParams P) {
         if (c == P.cols - 1) P.col_ptr[P.cols] = base + excl + cnt;
     }
 
-    // ---- fill: rows ascending = j descending, then i descending ----
+    // ---- fill: rows ascending = j descending (x ascending), then i descending ----
     const int mis = base & 3;
     int32_t* drow;
     float* dval;
@@ -136,12 +148,14 @@ __global__ void __launch_bounds__(256) csc_build_kernel(const CscParams P) {
         o = base + excl;
     }
     if (c < P.cols && cnt > 0) {
-        for (int j = jtop; j > jbot && j >= 0; j -= P.s) {
-            const int xrow = ((a + P.p - j) / P.s) * P.no;
-            for (int i = itop; i > ibot && i >= 0; i -= P.s) {
+        const int x0 = (a + P.p - jtop) / S, y0 = (b + P.p - itop) / S;  // exact: jtop == a+p (mod s)
+        int xrow = x0 * P.no;
+        for (int j = jtop; j > jlo; j -= S, xrow += P.no) {
+            int y = y0;
+            for (int i = itop; i > ilo; i -= S, ++y) {
                 const float v = s_taps[j * k + i];
-                if (v != 0.0f) {  // drops +-0.0, keeps NaN
-                    drow[o] = xrow + (b + P.p - i) / P.s;
+                if (DENSE || v != 0.0f) {  // drops +-0.0, keeps NaN
+                    drow[o] = xrow + y;
                     dval[o] = v;
                     ++o;
                 }
@@ -173,7 +187,7 @@ __global__ void __launch_bounds__(256) csc_build_kernel(const CscParams P) {
 }
 
 // Block size and staging for a per-column maximum of `maxc` entries.
-cudaError_t launch_csc_build(CscParams cp, int maxc, cudaStream_t st) {
+cudaError_t launch_csc_build(CscParams cp, int maxc, bool dense, cudaStream_t st) {
     const int kk = cp.k * cp.k;
     const size_t tab_bytes = (size_t)((kk + 3) & ~3) * 4;
     int block = 256;
@@ -188,12 +202,30 @@ cudaError_t launch_csc_build(CscParams cp, int maxc, cudaStream_t st) {
         block = 256;
     }
     if (smem > 200 * 1024) return cudaErrorInvalidValue;
+    auto kern = csc_build_kernel<0, false>;
+    if (dense) {
+        switch (cp.k) {
+            case 1: kern = csc_build_kernel<1, true>; break;
+            case 3: kern = csc_build_kernel<3, true>; break;
+            case 5: kern = csc_build_kernel<5, true>; break;
+            case 7: kern = csc_build_kernel<7, true>; break;
+            case 11: kern = csc_build_kernel<11, true>; break;
+            default: kern = csc_build_kernel<0, true>; break;
+        }
+    } else {
+        switch (cp.k) {
+            case 3: kern = csc_build_kernel<3, false>; break;
+            case 5: kern = csc_build_kernel<5, false>; break;
+            case 7: kern = csc_build_kernel<7, false>; break;
+            default: break;
+        }
+    }
     if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(csc_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
     const long long grid = (cp.cols + block - 1) / block;
-    csc_build_kernel<<<(unsigned)grid, block, smem, st>>>(cp);
+    kern<<<(unsigned)grid, block, smem, st>>>(cp);
     return cudaGetLastError();
 }
 

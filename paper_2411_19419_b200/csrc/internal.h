@@ -132,7 +132,7 @@ struct GenericParams {
 // Launchers (return cudaError_t of the launch).
 cudaError_t launch_csr_build(const BuildParams& bp, bool dense, int block, size_t smem,
                              cudaStream_t st);
-cudaError_t launch_csc_build(CscParams cp, int maxc, cudaStream_t st);
+cudaError_t launch_csc_build(CscParams cp, int maxc, bool dense, cudaStream_t st);  // dense: no zero taps
 cudaError_t launch_tiled(const TiledParams& tp, const CUtensorMap* tmap, int bt, size_t smem,
                          cudaStream_t st);
 cudaError_t launch_generic(const GenericParams& gp, cudaStream_t st);
