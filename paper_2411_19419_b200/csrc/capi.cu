@@ -315,7 +315,34 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
                    (reinterpret_cast<uintptr_t>(Y) % (4 * cpt) == 0);
         CUtensorMap tmap;
         if (int rc = encode_x_map(&tmap, X, g, ldx, batch, sh.wc, sh.wr, 1)) return rc;
-        CK(spb::launch_band_check((int)g.k, (int)g.s, bp, st, sms));
+        // The check depends only on the (immutable) matrix: off the caller's
+        // stream it overlaps whatever precedes the call there (in a loop of
+        // calls: the previous apply).  That pays when the matrix dominates the
+        // call's bytes (config 4 at 8 images: 341 -> 319 us); when the images
+        // dominate, the check's CTAs delay the persistent apply's start
+        // (config 3: 401 -> 406 us, config 4 at 64 images: 1047 -> 1270 us,
+        // profiles/r01n/exp.txt), so it stays on the caller's stream.
+        // SPCONV_B200_CHECK=side|same overrides; never while the stream is
+        // being captured into a graph.
+        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+        CK(cudaStreamIsCapturing(st, &cap));
+        const char* csel = std::getenv("SPCONV_B200_CHECK");
+        const bool matrix_bound = 8.0 * (double)h->nnz > 4.0 * (double)batch * (double)(h->rows + h->cols);
+        const bool side = cap == cudaStreamCaptureStatusNone &&
+                          (csel ? !std::strcmp(csel, "side") : matrix_bound);
+        if (side) {
+            std::lock_guard<std::mutex> lk(h->chk_mu);
+            if (!h->chk_stream) {
+                CK(cudaStreamCreateWithFlags(&h->chk_stream, cudaStreamNonBlocking));
+                CK(cudaEventCreateWithFlags(&h->chk_done, cudaEventDisableTiming));
+                if (h->built) CK(cudaStreamWaitEvent(h->chk_stream, h->built, 0));  // the matrix exists
+            }
+            CK(spb::launch_band_check((int)g.k, (int)g.s, bp, h->chk_stream, sms));
+            CK(cudaEventRecord(h->chk_done, h->chk_stream));
+            CK(cudaStreamWaitEvent(st, h->chk_done, 0));
+        } else {
+            CK(spb::launch_band_check((int)g.k, (int)g.s, bp, st, sms));
+        }
         CK(spb::launch_band((int)g.k, (int)g.s, bp, &tmap, st, nullptr, sms));
         h->last_kernel.store("conv_band_check+conv_spmm_band");
         return SPCONV_OK;
@@ -675,8 +702,15 @@ int spconv_build_csr(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
                                        " too large for the device build");
     }
     e = spb::launch_csr_build(bp, ht.nonzero, block, smem, st);
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (e == cudaSuccess) e = cudaStreamIsCapturing(st, &cap);
+    if (e == cudaSuccess && cap == cudaStreamCaptureStatusNone) {  // (a captured build has no event)
+        e = cudaEventCreateWithFlags(&h->built, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventRecord(h->built, st);
+    }
     if (tab) cudaFreeAsync(tab, st);
     if (e != cudaSuccess) {
+        if (h->built) cudaEventDestroy(h->built);
         cudaFreeAsync(csr, st);
         cudaStreamSynchronize(st);
         delete h;
@@ -1206,6 +1240,9 @@ int spconv_csr_free(spconv_csr* h) {
         DeviceGuard dg(h->device);
         cudaDeviceSynchronize();
         free_ws(h);
+        if (h->chk_done) cudaEventDestroy(h->chk_done);
+        if (h->built) cudaEventDestroy(h->built);
+        if (h->chk_stream) cudaStreamDestroy(h->chk_stream);
         if (h->row_ptr) cudaFree(h->row_ptr);
         if (h->csc_ptr) cudaFree(h->csc_ptr);
     }

@@ -188,6 +188,13 @@ struct spconv_csr {
     int32_t* csc_idx = nullptr;    // device row_idx[nnz]
     float* csc_vals = nullptr;     // device vals[nnz]
     std::vector<float> host_taps;  // conv handles: the k*k fp32 taps (relayout rebuilds from them)
+    // Side stream of the band check (run_spmm): the check reads only the
+    // immutable matrix, so it need not wait for the caller's stream and can
+    // overlap the previous call's apply; the apply waits on chk_done.
+    std::mutex chk_mu;
+    cudaStream_t chk_stream = nullptr;
+    cudaEvent_t chk_done = nullptr;
+    cudaEvent_t built = nullptr;  // recorded after the build on the build stream (side checks wait on it)
     std::atomic<const char*> last_kernel{nullptr};  // diagnostics: last SpMM kernel launched
     // Workspace of spconv_convolve_host (lazily created, guarded by ws_mu).
     std::mutex ws_mu;

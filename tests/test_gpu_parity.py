@@ -430,13 +430,15 @@ class _DevArray:
                                          "version": 3}
 
 
+@pytest.mark.parametrize("check", ["side", "same"])
 @pytest.mark.parametrize("spec", [(256, 256, 3, 1, 1), (300, 260, 7, 2, 3)])
-def test_band_check_reads_the_matrix(sp, orc, torch_cuda, spec):
+def test_band_check_reads_the_matrix(sp, orc, torch_cuda, spec, check, monkeypatch):
     """The band path re-reads T on every call: entries altered in device memory
     after the build (a value, a column moved far outside its tile's input
     window, a column moved to an earlier image row) are picked up by the next
     spmm -- the affected segments fail the check and take the per-entry loop --
     and the output is bit-exact vs the oracle on the altered CSR."""
+    monkeypatch.setenv("SPCONV_B200_CHECK", check)  # check kernel on a side stream / the caller's
     m, n, k = spec[:3]
     kern, X = problem(orc, 14, m, n, k, batch=6)
     t = build(sp, spec, kern)
