@@ -138,7 +138,9 @@ __global__ void __launch_bounds__(256) csc_build_kernel(const CscParams P) {
     int32_t* drow;
     float* dval;
     int o;
-    if (P.stage) {
+    // compile-time for the unrolled k (always staged): shared, not generic, accesses
+    const bool staged = KC > 0 || P.stage != 0;
+    if (staged) {
         drow = reinterpret_cast<int32_t*>(smem) + tab_words;
         dval = reinterpret_cast<float*>(drow) + P.stage_words;
         o = mis + excl;
@@ -162,7 +164,7 @@ __global__ void __launch_bounds__(256) csc_build_kernel(const CscParams P) {
             }
         }
     }
-    if (P.stage) {
+    if (staged) {
         __syncthreads();
         const int head = min(total, (4 - mis) & 3);
         if (t < head) {
@@ -202,8 +204,10 @@ cudaError_t launch_csc_build(CscParams cp, int maxc, bool dense, cudaStream_t st
         block = 256;
     }
     if (smem > 200 * 1024) return cudaErrorInvalidValue;
-    auto kern = csc_build_kernel<0, false>;
-    if (dense) {
+    auto kern = csc_build_kernel<0, false>;  // (the unrolled variants assume staging)
+    if (!cp.stage) {
+        if (dense) kern = csc_build_kernel<0, true>;
+    } else if (dense) {
         switch (cp.k) {
             case 1: kern = csc_build_kernel<1, true>; break;
             case 3: kern = csc_build_kernel<3, true>; break;

@@ -150,7 +150,9 @@ __global__ void __launch_bounds__(256) csr_build_kernel(const BuildParams P) {
     int32_t* dcol;
     float* dval;
     int o;
-    if (P.stage) {
+    // compile-time for the unrolled k (always staged): shared, not generic, accesses
+    const bool staged = KC > 0 || P.stage != 0;
+    if (staged) {
         dcol = reinterpret_cast<int32_t*>(smem) + tab_words;
         dval = reinterpret_cast<float*>(dcol) + P.stage_words;
         o = mis + excl;
@@ -193,7 +195,7 @@ __global__ void __launch_bounds__(256) csr_build_kernel(const BuildParams P) {
             }
         }
     }
-    if (P.stage) {
+    if (staged) {
         __syncthreads();
         // Global [base, base + total) <- staged [mis, mis + total): scalar head,
         // 16-byte body, scalar tail.

@@ -92,8 +92,8 @@ struct BandCfg {
     static constexpr int SF = round_up(WIN, 32);        // floats per stage (128-byte aligned)
     static constexpr size_t SMEM = 128 + (size_t)STAGES * SF * 4;
     static_assert(WC <= 256 && WR <= 256, "TMA box limit");
-    static_assert(TH <= 32, "one producer lane per tile row");
-    static_assert(STAGES * 20 <= 128, "barriers + flag masks fit the 128-byte header");
+    static_assert(TH <= 64, "at most two producer lanes per tile row");
+    static_assert(STAGES * 24 <= 128, "barriers + flag masks fit the 128-byte header");
 };
 
 // ---------------------------------------------------------------------------
@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(BandCfg<K, S, V, CPT, TH, STAGES, DELTA>::THRE
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
     uint64_t* empty = full + STAGES;
-    unsigned* s_mask = reinterpret_cast<unsigned*>(empty + STAGES);  // per-stage row flags
+    unsigned long long* s_mask = reinterpret_cast<unsigned long long*>(empty + STAGES);  // per-stage row flags
     float* xs = reinterpret_cast<float*>(smem + 128);
 
     const int t = threadIdx.x;
@@ -314,12 +314,16 @@ __global__ void __launch_bounds__(BandCfg<K, S, V, CPT, TH, STAGES, DELTA>::THRE
         int it = 0;
         for (ItemIter I(P); I.img < P.batch; I.next(), ++it) {
             const int st = it % STAGES;
-            bool f = true;
-            if (lane < TH) {
-                const int x = I.tx * TH + lane;
-                f = x >= P.mo || __ldg(P.seg_ok + (long long)x * P.tiles_y + I.ty) != 0;
+            unsigned long long rows_ok = 0;
+#pragma unroll
+            for (int h = 0; h < (TH + 31) / 32; ++h) {  // one lane per tile row
+                bool f = true;
+                if (32 * h + lane < TH) {
+                    const int x = I.tx * TH + 32 * h + lane;
+                    f = x >= P.mo || __ldg(P.seg_ok + (long long)x * P.tiles_y + I.ty) != 0;
+                }
+                rows_ok |= (unsigned long long)__ballot_sync(0xffffffffu, f) << (32 * h);
             }
-            const unsigned rows_ok = __ballot_sync(0xffffffffu, f);
             if (lane == 0) {
                 if (it >= STAGES) mbar_wait(&empty[st], (uint32_t)(((it / STAGES) - 1) & 1));
                 s_mask[st] = rows_ok;
@@ -338,7 +342,7 @@ __global__ void __launch_bounds__(BandCfg<K, S, V, CPT, TH, STAGES, DELTA>::THRE
 #pragma unroll
     for (int q = 0; q < C::KK; ++q) w[q] = __ldg(P.taps + q);
     const bool vec_ok = P.y_vec != 0;
-    constexpr unsigned VMASK = (1u << V) - 1u;
+    constexpr unsigned long long VMASK = (1ull << V) - 1ull;
 
     int it = 0;
     for (ItemIter I(P); I.img < P.batch; I.next(), ++it) {
@@ -516,14 +520,22 @@ cudaError_t launch_band(int k, int s, const BandParams& bp, const CUtensorMap* t
     // Blocking variants for tuning experiments (SPCONV_B200_VARIANT; 0 = default),
     // instantiated only for the alignment shift of the benchmark configs.
     static const int var = std::getenv("SPCONV_B200_VARIANT") ? std::atoi(std::getenv("SPCONV_B200_VARIANT")) : 0;
-    // Defaults from the r01f/r01j A/B runs (profiles/r01j/exp.txt): V = 8 rows
-    // per thread for k3 s1, a 3-stage pipeline for k7 s2.
+    // Defaults from the A/B runs (profiles/r01p/exp.txt): k3 s1 -- V = 16 rows
+    // x 4 columns per thread, 64-row tiles, 4 stages (one CTA per SM; config 3
+    // 404 -> 382 us); k7 s2 -- V = 8, 32-row tiles, 3 stages.
     if (k == 3 && s == 1) {
         if (delta == 3 && var == 1) return run_cfg<3, 1, 4, 4, 16, 4, 3>(bp, tmap, st, shape, sms);
         if (delta == 3 && var == 2) return run_cfg<3, 1, 4, 4, 32, 4, 3>(bp, tmap, st, shape, sms);
         if (delta == 3 && var == 3) return run_cfg<3, 1, 4, 4, 32, 3, 3>(bp, tmap, st, shape, sms);
         if (delta == 3 && var == 4) return run_cfg<3, 1, 2, 4, 16, 4, 3>(bp, tmap, st, shape, sms);
-        return run_delta<3, 1, 8, 4, 32, 4>(delta, bp, tmap, st, shape, sms);
+        if (delta == 3 && var == 5) return run_cfg<3, 1, 8, 4, 64, 3, 3>(bp, tmap, st, shape, sms);
+        if (delta == 3 && var == 6) return run_cfg<3, 1, 8, 4, 64, 2, 3>(bp, tmap, st, shape, sms);
+        if (delta == 3 && var == 7) return run_cfg<3, 1, 16, 4, 64, 4, 3>(bp, tmap, st, shape, sms);
+        if (delta == 3 && var == 8) return run_cfg<3, 1, 16, 4, 64, 3, 3>(bp, tmap, st, shape, sms);
+        if (delta == 3 && var == 9) return run_cfg<3, 1, 16, 4, 64, 5, 3>(bp, tmap, st, shape, sms);
+        if (delta == 3 && var == 10) return run_cfg<3, 1, 16, 4, 32, 4, 3>(bp, tmap, st, shape, sms);
+        if (delta == 3 && var == 11) return run_cfg<3, 1, 8, 4, 32, 4, 3>(bp, tmap, st, shape, sms);
+        return run_delta<3, 1, 16, 4, 64, 4>(delta, bp, tmap, st, shape, sms);
     }
     if (k == 5 && s == 1) return run_delta<5, 1, 4, 4, 32, 4>(delta, bp, tmap, st, shape, sms);
     if (k == 3 && s == 2) return run_delta<3, 2, 4, 2, 16, 4>(delta, bp, tmap, st, shape, sms);
@@ -533,7 +545,11 @@ cudaError_t launch_band(int k, int s, const BandParams& bp, const CUtensorMap* t
         if (delta == 1 && var == 2) return run_cfg<7, 2, 2, 2, 16, 3, 1>(bp, tmap, st, shape, sms);
         if (delta == 1 && var == 3) return run_cfg<7, 2, 4, 2, 32, 2, 1>(bp, tmap, st, shape, sms);
         if (delta == 1 && var == 4) return run_cfg<7, 2, 2, 2, 8, 4, 1>(bp, tmap, st, shape, sms);
-        return run_delta<7, 2, 4, 2, 16, 3>(delta, bp, tmap, st, shape, sms);
+        if (delta == 1 && var == 5) return run_cfg<7, 2, 8, 2, 32, 3, 1>(bp, tmap, st, shape, sms);
+        if (delta == 1 && var == 6) return run_cfg<7, 2, 8, 2, 16, 4, 1>(bp, tmap, st, shape, sms);
+        if (delta == 1 && var == 7) return run_cfg<7, 2, 16, 2, 32, 3, 1>(bp, tmap, st, shape, sms);
+        if (delta == 1 && var == 8) return run_cfg<7, 2, 4, 2, 16, 3, 1>(bp, tmap, st, shape, sms);
+        return run_delta<7, 2, 8, 2, 32, 3>(delta, bp, tmap, st, shape, sms);
     }
     return cudaErrorInvalidValue;
 }
