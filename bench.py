@@ -615,6 +615,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, choices=sorted(CONFIGS), default=3)
     ap.add_argument("--batch", type=int, default=0, help="override the per-GPU batch")
+    ap.add_argument("--spec", default="", help="tuning only: m,n,k,s,p replacing the config's geometry")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -628,6 +629,9 @@ def main():
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
     cfg = CONFIGS[args.config]
+    if args.spec:
+        spec = tuple(int(v) for v in args.spec.split(","))
+        cfg = dict(cfg, spec=spec, name=f"custom spec {spec} (tuning run, not a BASELINE config)")
     if args.workload == "densenet121":
         run_densenet(args)
     elif args.impl == "reference":
