@@ -513,3 +513,31 @@ def test_latency_spmv_staging_variants(sp, orc, torch_cuda, stage):
                     assert np.array_equal(bits(Y), bits(want[:b])), (spec, zero, b)
     finally:
         del os.environ["SPCONV_B200_STAGE"]
+
+
+@pytest.mark.parametrize("batch", [1, 2, 6])
+def test_spmm_misaligned_buffers(sp, orc, torch_cuda, batch):
+    """X and Y one float off 16-byte alignment (TMA can't describe X; Y can't
+    take vector stores): every path still bit-exact, nothing written outside Y."""
+    torch = torch_cuda
+    spec = (64, 64, 3, 1, 1)
+    kern, X = problem(orc, 16, 64, 64, 3, batch=batch)
+    t = build(sp, spec, kern)
+    want = orc.spmm_native(*orc.build_native(*spec, kern), X)
+    xb = torch.zeros(batch * t.cols + 1, device="cuda")
+    xb[1:] = torch.from_numpy(X.reshape(-1)).cuda()
+    yb = torch.full((batch * t.rows + 2,), -3.0, device="cuda")
+    Xd = xb[1:].view(batch, t.cols)
+    Yd = yb[1:-1].view(batch, t.rows)
+    for path in (None, "tiled", "generic"):
+        if path:
+            os.environ["SPCONV_B200_PATH"] = path
+        try:
+            sp.spmm(t, Xd, Yd)
+        finally:
+            if path:
+                del os.environ["SPCONV_B200_PATH"]
+        torch.cuda.synchronize()
+        got = yb.cpu().numpy()
+        assert got[0] == -3.0 and got[-1] == -3.0, path
+        assert np.array_equal(bits(got[1:-1].reshape(batch, t.rows)), bits(want)), path
