@@ -75,6 +75,11 @@ int main() {
     CHECK(nnz_bound(ConvSpec(4, 4, 3, 1, 0)) == 36);
     CHECK(nnz_bound(ConvSpec(1, 1, 1, 1, 2)) == 1);
     CHECK(c1(0, ConvSpec(3, 3, 3, 1, 1)) == 1 && c1(1, ConvSpec(3, 3, 3, 1, 1)) == 0);
+    {   // tests/CMakeLists.txt:23-24 cli_nnz regex "3,3,3,1,1,49,81,"
+        const NnzReport r = make_nnz_report(ConvSpec(3, 3, 3, 1, 1));
+        CHECK(r.bound == 49 && r.dense_count == 81 && nnz_oracle(r.spec) == 49);
+        CHECK(r.savings_ratio > 0.395 && r.savings_ratio < 0.396);
+    }
     // Zero taps are not stored (inc/sparse.hpp:335): nnz(T) < bound.
     {
         const Kernel z(3, {1.5, 0.0, -2.0, -0.0, 3.0, 0.0, 0.25, 0.0, -1.0});
