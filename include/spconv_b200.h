@@ -176,6 +176,14 @@ int spconv_direct_conv(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p, in
 int spconv_im2col_conv(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p, int dtype, const void* taps_dev,
                        const void* A_dev, void* out_dev, void* patches_dev, int64_t batch, void* stream);
 
+/* The same fp64 comparators on HOST buffers for one image (the reference's
+ * own signatures, inc/reference.hpp:41-136): mode 0 = direct_conv,
+ * 1 = im2col_conv (out: m_out*n_out values), 2 = im2col lowering only (out:
+ * the k^2 x m_out*n_out patch matrix, row-major; `kernel` unused).  Computed
+ * on `device`, bit-identical to the reference's fp64 results. */
+int spconv_reference_host(int mode, int64_t m, int64_t n, int64_t k, int64_t s, int64_t p, const double* kernel,
+                          const double* A, double* out, int device);
+
 /* run_verification (inc/verify.hpp:59-169) over the device path: for every
  * m, n <= max_dim, p <= 3, s <= 3, k <= min(m,n) + 2p, the Theorem 2.1 count
  * against the brute-force overlap count and nnz(T), and for `seeds` seeded

@@ -158,6 +158,8 @@ cudaError_t launch_direct_conv(int dtype, int m, int n, int k, int s, int p, lon
                                const void* A, void* out, void* mag, cudaStream_t st);
 cudaError_t launch_im2col_conv(int dtype, int m, int n, int k, int s, int p, long long batch, const void* taps,
                                const void* A, void* out, void* patches, cudaStream_t st);
+cudaError_t launch_im2col_lower(int dtype, int m, int n, int k, int s, int p, long long batch, const void* A,
+                                void* patches, cudaStream_t st);
 
 }  // namespace spb
 

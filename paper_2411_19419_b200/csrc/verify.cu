@@ -145,6 +145,20 @@ cudaError_t launch_im2col_conv(int dtype, int m, int n, int k, int s, int p, lon
                       : run_im2col<double, false>(g, taps, A, out, patches, st);
 }
 
+cudaError_t launch_im2col_lower(int dtype, int m, int n, int k, int s, int p, long long batch, const void* A,
+                                void* patches, cudaStream_t st) {
+    const ConvGeom g{m, n, k, s, p, (m + 2 * p - k) / s + 1, (n + 2 * p - k) / s + 1, batch};
+    const long long P = (long long)g.mo * g.no, K2 = (long long)k * k, total = K2 * P * batch;
+    if (total == 0) return cudaSuccess;
+    if (dtype == 0)
+        im2col_lower_kernel<float><<<(unsigned)((total + 255) / 256), 256, 0, st>>>(
+            g, static_cast<const float*>(A), static_cast<float*>(patches));
+    else
+        im2col_lower_kernel<double><<<(unsigned)((total + 255) / 256), 256, 0, st>>>(
+            g, static_cast<const double*>(A), static_cast<double*>(patches));
+    return cudaGetLastError();
+}
+
 }  // namespace spb
 
 // ---------------------------------------------------------------------------
@@ -280,6 +294,39 @@ int spconv_im2col_conv(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p, in
     const cudaError_t e = spb::launch_im2col_conv(dtype, (int)m, (int)n, (int)k, (int)s, (int)p, batch, taps_dev,
                                                   A_dev, out_dev, patches_dev, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return spb_fail(SPCONV_ECUDA, std::string("im2col_conv: ") + cudaGetErrorString(e));
+    return SPCONV_OK;
+}
+
+// Host-buffer fp64 forms of the comparators (the reference's own signatures
+// take host grids): device buffers for one call, the device kernels, copies
+// back.  mode 0 = direct_conv, 1 = im2col_conv, 2 = the im2col lowering only
+// (out = the k^2 x m_out*n_out patch matrix, row-major, inc/reference.hpp:73-97).
+int spconv_reference_host(int mode, int64_t m, int64_t n, int64_t k, int64_t s, int64_t p, const double* kernel,
+                          const double* A, double* out, int device) {
+    if (int rc = spconv_spec_check(m, n, k, s, p)) return rc;
+    if (mode < 0 || mode > 2) return spb_fail(SPCONV_EINVAL, "spconv_reference_host: mode must be 0, 1 or 2");
+    if (!A || !out || (mode != 2 && !kernel)) return spb_fail(SPCONV_EINVAL, "spconv_reference_host: null buffer");
+    int prev = -1;
+    cudaGetDevice(&prev);
+    if (cudaSetDevice(device) != cudaSuccess) return spb_fail(SPCONV_ECUDA, "cudaSetDevice");
+    const int64_t P = ((m + 2 * p - k) / s + 1) * ((n + 2 * p - k) / s + 1);
+    const int64_t outn = mode == 2 ? k * k * P : P;
+    DevBuf da, dk, dout, dpatch;
+    cudaError_t e = da.reserve((size_t)(m * n) * 8);
+    if (e == cudaSuccess) e = dk.reserve((size_t)(k * k) * 8);
+    if (e == cudaSuccess) e = dout.reserve((size_t)outn * 8);
+    if (e == cudaSuccess && mode == 1) e = dpatch.reserve((size_t)(k * k * P) * 8);
+    if (e == cudaSuccess) e = cudaMemcpy(da.p, A, (size_t)(m * n) * 8, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && mode != 2) e = cudaMemcpy(dk.p, kernel, (size_t)(k * k) * 8, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        const int M = (int)m, N = (int)n, K = (int)k, S = (int)s, Pd = (int)p;
+        if (mode == 0) e = spb::launch_direct_conv(1, M, N, K, S, Pd, 1, dk.p, da.p, dout.p, nullptr, nullptr);
+        else if (mode == 1) e = spb::launch_im2col_conv(1, M, N, K, S, Pd, 1, dk.p, da.p, dout.p, dpatch.p, nullptr);
+        else e = spb::launch_im2col_lower(1, M, N, K, S, Pd, 1, da.p, dout.p, nullptr);
+    }
+    if (e == cudaSuccess) e = cudaMemcpy(out, dout.p, (size_t)outn * 8, cudaMemcpyDeviceToHost);
+    if (prev >= 0) cudaSetDevice(prev);
+    if (e != cudaSuccess) return spb_fail(SPCONV_ECUDA, std::string("spconv_reference_host: ") + cudaGetErrorString(e));
     return SPCONV_OK;
 }
 

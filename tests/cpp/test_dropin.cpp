@@ -139,6 +139,25 @@ int main() {
     }
     expect_throw<std::invalid_argument>([] { layout_from_name("coo"); },
                                         "unknown layout 'coo' (expected csr or csc)");
+    // Dense comparators (inc/reference.hpp) on the device, fp64: the SPEC.md:175
+    // example exactly, and direct == im2col bit for bit on a padded, strided case.
+    {
+        std::vector<double> v(16);
+        for (int i = 0; i < 16; ++i) v[i] = i + 1;
+        const ConvSpec spec(4, 4, 2, 2, 0);
+        const Kernel ones(2, {1, 1, 1, 1});
+        CHECK((direct_conv(Grid(4, 4, v), ones, spec).values == std::vector<double>{14, 22, 46, 54}));
+        const ConvSpec sp2(9, 7, 3, 2, 2);
+        std::vector<double> a(63), kv(9);
+        for (int i = 0; i < 63; ++i) a[i] = std::sin(0.37 * i);
+        for (int i = 0; i < 9; ++i) kv[i] = std::cos(1.3 * i);
+        const Grid d = direct_conv(Grid(9, 7, a), Kernel(3, kv), sp2);
+        CHECK(d.values == im2col_conv(Grid(9, 7, a), Kernel(3, kv), sp2).values);
+        const Im2colMatrix im = im2col(Grid(9, 7, a), sp2);
+        CHECK(im.rows == 9 && im.cols == sp2.output_len() && im.values[0] == 0.0);  // corner patch: padding
+        expect_throw<std::invalid_argument>([] { direct_conv(Grid(3, 3), Kernel(1, {1.0}), ConvSpec(4, 4, 1, 1, 0)); },
+                                            "direct_conv: input is 3x3 but spec is (m=4");
+    }
     // The verification sweep on the device path (inc/verify.hpp), small grid.
     {
         VerifyOptions opt;

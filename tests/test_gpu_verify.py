@@ -98,3 +98,30 @@ def test_verification_sweep_default_grid(sp, golden):
     for key in ("specs", "conv_cases", "clipped_specs"):
         assert rep[key] == want[key], key
     assert rep["max_layout_dev"] == 0.0 and rep["max_rel_dev"] <= 1e-5
+
+
+def test_reference_host_comparators_bitexact(sp, ref):
+    """spconv_reference_host (host-buffer fp64 direct_conv / im2col_conv /
+    im2col lowering, the drop-in reference.hpp's backend) == the compiled
+    reference, bit for bit."""
+    import ctypes as C
+    rng = np.random.default_rng(8)
+    for spec in [(20, 17, 3, 1, 1), (33, 8, 4, 3, 2), (9, 9, 11, 1, 5)]:
+        m, n, k, s, p = spec
+        mo, no = (m + 2 * p - k) // s + 1, (n + 2 * p - k) // s + 1
+        a = rng.standard_normal(m * n)
+        w = rng.standard_normal(k * k)
+        want = ref.direct_conv(*spec, a, w)
+        for mode in (0, 1):
+            out = np.empty(mo * no)
+            sp._check(sp.lib.spconv_reference_host(mode, m, n, k, s, p, w.ctypes.data, a.ctypes.data,
+                                                   out.ctypes.data, 0))
+            assert np.array_equal(out.view(np.uint64), want.view(np.uint64)), (spec, mode)
+        patches = np.empty(k * k * mo * no)
+        sp._check(sp.lib.spconv_reference_host(2, m, n, k, s, p, None, a.ctypes.data, patches.ctypes.data, 0))
+        pad = np.zeros((m + 2 * p, n + 2 * p))
+        pad[p:p + m, p:p + n] = a.reshape(m, n)
+        for j in range(k):
+            for i in range(k):
+                row = pad[j:j + s * (mo - 1) + 1:s, i:i + s * (no - 1) + 1:s].reshape(-1)
+                assert np.array_equal(patches[(j * k + i) * mo * no:(j * k + i + 1) * mo * no], row)
