@@ -104,7 +104,6 @@ def test_reference_host_comparators_bitexact(sp, ref):
     """spconv_reference_host (host-buffer fp64 direct_conv / im2col_conv /
     im2col lowering, the drop-in reference.hpp's backend) == the compiled
     reference, bit for bit."""
-    import ctypes as C
     rng = np.random.default_rng(8)
     for spec in [(20, 17, 3, 1, 1), (33, 8, 4, 3, 2), (9, 9, 11, 1, 5)]:
         m, n, k, s, p = spec
