@@ -541,3 +541,26 @@ def test_spmm_misaligned_buffers(sp, orc, torch_cuda, batch):
         got = yb.cpu().numpy()
         assert got[0] == -3.0 and got[-1] == -3.0, path
         assert np.array_equal(bits(got[1:-1].reshape(batch, t.rows)), bits(want)), path
+
+
+@pytest.mark.parametrize("spec,batch", [((256, 256, 3, 1, 1), 6), ((300, 260, 7, 2, 3), 3), ((512, 512, 5, 2, 2), 1)])
+def test_spmm_in_cuda_graph(sp, orc, torch_cuda, spec, batch):
+    """spmm captured into a CUDA graph (the band check then stays on the
+    captured stream) and replayed on new inputs: bit-exact."""
+    torch = torch_cuda
+    m, n, k = spec[:3]
+    kern, X = problem(orc, 17, m, n, k, batch=2 * batch)
+    t = build(sp, spec, kern)
+    want = orc.spmm_native(*orc.build_native(*spec, kern), X)
+    Xd = torch.from_numpy(X[:batch]).cuda()
+    Yd = torch.empty(batch, t.rows, device="cuda")
+    cs = torch.cuda.Stream()
+    sp.spmm(t, Xd, Yd, stream=cs)  # warm (attributes, workspaces) outside the capture
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=cs):
+        sp.spmm(t, Xd, Yd, stream=cs)
+    Xd.copy_(torch.from_numpy(X[batch:]))
+    g.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(bits(Yd.cpu().numpy()), bits(want[batch:]))
