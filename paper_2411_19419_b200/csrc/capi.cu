@@ -1015,6 +1015,15 @@ int spconv_convolve_host(const spconv_csr* hc, const float* X_host, float* Y_hos
         h->ws_chunk = chunk;
     }
     cudaStream_t s_in = h->ws_stream[0], s_cp = h->ws_stream[1], s_out = h->ws_stream[2];
+    if (batch <= chunk) {
+        // One chunk: nothing to overlap -- H2D, apply, D2H in order on one
+        // stream and a single synchronisation (the latency path of small calls).
+        CK(cudaMemcpyAsync(h->ws_x[0], X_host, (size_t)(batch * h->cols * 4), cudaMemcpyHostToDevice, s_cp));
+        if (int rc = run_spmm(h, h->ws_x[0], h->cols, h->ws_y[0], h->rows, batch, s_cp)) return rc;
+        CK(cudaMemcpyAsync(Y_host, h->ws_y[0], (size_t)(batch * h->rows * 4), cudaMemcpyDeviceToHost, s_cp));
+        CK(cudaStreamSynchronize(s_cp));
+        return SPCONV_OK;
+    }
     cudaEvent_t* ev_in = h->ws_ev[0];
     cudaEvent_t* ev_cp = h->ws_ev[1];
     cudaEvent_t* ev_out = h->ws_ev[2];
