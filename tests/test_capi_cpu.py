@@ -93,3 +93,17 @@ def test_dropin_headers_compile():
                         os.path.join(ROOT, "include"), "-x", "c++", "-"], input=src, text=True,
                        capture_output=True)
     assert r.returncode == 0, r.stderr
+
+
+def test_int32_range_rejected_before_any_device_work():
+    """Geometries past the int32 device index range (m*n or nnz >= 2^31) are
+    rejected with std::invalid_argument semantics before the device is touched
+    (so this runs without a GPU)."""
+    with pytest.raises(ValueError, match="exceeds the int32 device index range"):
+        sp.build_transform(sp.Kernel(1, [1.0]), sp.ConvSpec(46341, 46341, 1, 1, 0))
+    with pytest.raises(ValueError, match=r"nnz \d+ exceeds the int32 device index range"):
+        sp.build_transform(sp.Kernel(11, np.ones(121)), sp.ConvSpec(20000, 20000, 11, 1, 5))
+    with pytest.raises(ValueError, match="layout must be 0"):
+        sp.build_transform(sp.Kernel(3, np.ones(9)), sp.ConvSpec(8, 8, 3, 1, 1), layout=2)
+    with pytest.raises(ValueError, match="unknown layout 'coo'"):
+        sp.layout_from_name("coo")
