@@ -392,10 +392,18 @@ def run_ours(args, cfg):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # One rank per GPU.  SPCONV_B200_DIST_BACKEND=gloo (+ more ranks than GPUs,
+    # ranks sharing devices) exists only to exercise the multi-rank logic on a
+    # one-GPU box; the measured configuration is NCCL with one GPU per rank.
+    backend = os.environ.get("SPCONV_B200_DIST_BACKEND", "nccl")
+    local = local % max(torch.cuda.device_count(), 1) if backend != "nccl" else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     m, n, k, s, p = cfg["spec"]
     # Weak scaling: every rank owns a fixed slice of `b` images (the batch

@@ -65,8 +65,11 @@ def gather_outputs(Y_local, total: int, root: int = 0):
         send = torch.zeros(most, rows, dtype=Y_local.dtype, device=Y_local.device)
         send[:count] = Y_local
     send = send.contiguous()
+    dev = send.device
+    if dist.get_backend() != "nccl":  # gloo gathers host tensors
+        send = send.cpu()
     bufs = [torch.empty_like(send) for _ in range(world)] if rank == root else None
     dist.gather(send, gather_list=bufs, dst=root)
     if rank != root:
         return None
-    return torch.cat([bufs[r][: batch_slice(total, r, world)[1]] for r in range(world)], dim=0)
+    return torch.cat([bufs[r][: batch_slice(total, r, world)[1]] for r in range(world)], dim=0).to(dev)
