@@ -446,7 +446,7 @@ def run_ours(args, cfg):
         g_ms = max_over_ranks(ge0.elapsed_time(ge1), dev)
         moved = 4 * (total_batch - b) * rows
         gather = {"ms": g_ms, "bytes_to_root": moved, "gb_per_s": moved / (g_ms * 1e-3) / 1e9,
-                  "collective": "torch.distributed.gather (NCCL)"}
+                  "collective": f"torch.distributed.gather ({dist.get_backend()})"}
         del out
     launches_per_step = kernel.count("+") + 1
     elapsed_ms = sum(ms)
