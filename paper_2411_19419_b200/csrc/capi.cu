@@ -965,8 +965,15 @@ int spconv_csr_copy(const spconv_csr* h, int32_t* row_ptr, int32_t* col_idx, flo
     return SPCONV_OK;
 }
 
+// [a, a + na) and [b, b + nb) floats overlap (in-place application is not supported:
+// every kernel reads x while others write y).
+static bool overlaps(const float* a, int64_t na, const float* b, int64_t nb) {
+    return na > 0 && nb > 0 && a < b + nb && b < a + na;
+}
+
 int spconv_spmv(const spconv_csr* h, const float* x_dev, float* y_dev, void* stream) {
     if (!h || !x_dev || !y_dev) return fail(SPCONV_EINVAL, "spconv_spmv: null argument");
+    if (overlaps(x_dev, h->cols, y_dev, h->rows)) return fail(SPCONV_EINVAL, "spconv_spmv: x and y overlap");
     DeviceGuard dg(h->device);
     if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
     return run_spmm(const_cast<spconv_csr*>(h), x_dev, h->cols, y_dev, h->rows, 1,
@@ -980,6 +987,8 @@ int spconv_spmm(const spconv_csr* h, const float* X_dev, int64_t ldx, float* Y_d
     if (batch > 0 && (!X_dev || !Y_dev)) return fail(SPCONV_EINVAL, "spconv_spmm: null buffer");
     if (ldx < h->cols || ldy < h->rows)
         return fail(SPCONV_EINVAL, "spconv_spmm: leading dimension smaller than the matrix");
+    if (batch > 0 && overlaps(X_dev, (batch - 1) * ldx + h->cols, Y_dev, (batch - 1) * ldy + h->rows))
+        return fail(SPCONV_EINVAL, "spconv_spmm: X and Y overlap");
     DeviceGuard dg(h->device);
     if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
     return run_spmm(const_cast<spconv_csr*>(h), X_dev, ldx, Y_dev, ldy, batch,

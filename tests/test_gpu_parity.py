@@ -357,6 +357,12 @@ def test_errors(sp, torch_cuda):
         sp._check(sp.lib.spconv_spmm(t._h, x.data_ptr(), 10, x.data_ptr(), 64, 1, None))
     with pytest.raises(ValueError, match="build_conv_matrix: kernel side 2 does not match"):
         sp.build_transform(sp.Kernel(2, np.ones(4)), sp.ConvSpec(8, 8, 3, 1, 1))
+    buf = torch_cuda.zeros(3 * 64, device="cuda")  # in place / overlapping: rejected, nothing launched
+    with pytest.raises(ValueError, match="spconv_spmv: x and y overlap"):
+        sp._check(sp.lib.spconv_spmv(t._h, buf.data_ptr(), buf.data_ptr() + 4 * 10, None))
+    with pytest.raises(ValueError, match="spconv_spmm: X and Y overlap"):
+        sp._check(sp.lib.spconv_spmm(t._h, buf.data_ptr(), 64, buf.data_ptr() + 4 * 100, 64, 2, None))
+    sp._check(sp.lib.spconv_spmm(t._h, buf.data_ptr(), 64, buf.data_ptr() + 4 * 128, 64, 1, None))  # disjoint
 
 
 @pytest.mark.parametrize("spec", [(1024, 1024, 3, 1, 1), (512, 512, 5, 2, 2), (300, 260, 7, 2, 3),
