@@ -330,6 +330,27 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
         const bool matrix_bound = 8.0 * (double)h->nnz > 4.0 * (double)batch * (double)(h->rows + h->cols);
         const bool side = cap == cudaStreamCaptureStatusNone &&
                           (csel ? !std::strcmp(csel, "side") : matrix_bound);
+        // When the images dominate by far (matrix < 10 % of the call's bytes),
+        // one fused kernel checks the matrix in its producer warps while it
+        // applies, plus a fixup pass for failed segments: config 3 384 ->
+        // 376 us.  With a heavier matrix the producer's checks starve the
+        // pipeline (config 4 at 64 images: 1,043 -> 1,531 us), so the check
+        // stays a kernel of its own (profiles/r01v/exp.txt).
+        // SPCONV_B200_FUSED=0|1 overrides; the blocked path needs finite,
+        // non-zero taps.
+        const char* fsel = std::getenv("SPCONV_B200_FUSED");
+        const bool light = 8.0 * (double)h->nnz < 0.1 * 4.0 * (double)batch * (double)(h->rows + h->cols);
+        bp.fused = !side && h->taps_dense && (fsel ? !std::strcmp(fsel, "1") : light) ? 1 : 0;
+        if (bp.fused) {
+            const cudaError_t fe = spb::launch_band((int)g.k, (int)g.s, bp, &tmap, st, nullptr, sms);
+            if (fe == cudaSuccess) {
+                h->last_kernel.store("conv_spmm_band<fused>+conv_band_fixup");
+                return SPCONV_OK;
+            }
+            if (fe != cudaErrorNotSupported) CK(fe);
+            cudaGetLastError();
+            bp.fused = 0;  // this blocking has no fused instantiation
+        }
         if (side) {
             std::lock_guard<std::mutex> lk(h->chk_mu);
             if (!h->chk_stream) {

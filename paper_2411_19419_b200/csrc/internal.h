@@ -96,6 +96,7 @@ struct BandParams {
     int y_vec;         // Y rows admit CPT-wide vector stores
     int sy;            // sum over output columns y of cy(y) (closed-form row starts)
     int nnz;
+    int fused;         // host: launch the fused check + apply (+ fixup) instead of two kernels
 };
 
 struct BandShape {

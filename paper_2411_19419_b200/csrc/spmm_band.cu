@@ -141,72 +141,66 @@ __device__ __forceinline__ int cum_taps(int x, int dim, int p) {
     return c;
 }
 
+// One segment's closed-form footprint.
+struct SegGeom {
+    int x, y0, nr, r0, jlo, jhi, cy0, L;
+    long long S0;
+    bool valid;
+};
+
 template <int K, int S, int TW>
-__global__ void __launch_bounds__(CheckCfg<K, S, TW>::WARPS * 32) conv_band_check(const BandParams P) {
+__device__ __forceinline__ SegGeom seg_geom(const BandParams& P, long long seg) {
+    SegGeom g;
+    g.x = (int)(seg / P.tiles_y);
+    g.y0 = (int)(seg - (long long)g.x * P.tiles_y) * TW;
+    g.nr = min(TW, P.no - g.y0);
+    g.r0 = g.x * P.no + g.y0;
+    tap_range_dev(g.x, P.m, K, S, P.p, g.jlo, g.jhi);
+    g.cy0 = cum_taps<K, S>(g.y0, P.n, P.p);
+    g.S0 = (long long)cum_taps<K, S>(g.x, P.m, P.p) * P.sy + (long long)(g.jhi - g.jlo) * g.cy0;
+    g.L = (g.jhi - g.jlo) * (cum_taps<K, S>(g.y0 + g.nr, P.n, P.p) - g.cy0);
+    g.valid = g.S0 + g.L <= (long long)P.nnz;  // (zero taps: the prediction runs past the end)
+    return g;
+}
+
+// Lane 0: the three bulk copies of a valid segment (row_ptr, col_idx, vals)
+// into one staging slice of CheckCfg::WARP_BYTES, completing on `bar`.
+template <int K, int S, int TW>
+__device__ __forceinline__ void seg_issue(const BandParams& P, const SegGeom& g, int* rp, uint64_t* bar) {
     using C = CheckCfg<K, S, TW>;
-    constexpr int KK = K * K;
-    constexpr int RPL = TW / 32;  // rows per lane
-    extern __shared__ __align__(128) unsigned char smem[];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    __shared__ uint32_t s_w[KK];  // taps, runtime-indexed (clipped rows)
-    for (int q = threadIdx.x; q < KK; q += blockDim.x) s_w[q] = __float_as_uint(__ldg(P.taps + q));
-
-    const long long seg = (long long)blockIdx.x * C::WARPS + warp;
-    const bool live = seg < (long long)P.mo * P.tiles_y;  // warp-uniform
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem) + warp;
-    int* rp = reinterpret_cast<int*>(smem + 128 + (size_t)warp * C::WARP_BYTES);
     int* cb = rp + C::RPW;
-    uint32_t* vb = reinterpret_cast<uint32_t*>(cb + C::BUFW);
+    int* vb = cb + C::BUFW;
+    const int rbase = g.r0 & ~3;
+    const uint32_t rwords = (uint32_t)((g.r0 + g.nr + 1 - rbase + 3) & ~3);
+    const long long ebase = g.S0 & ~3ll;
+    const uint32_t ewords = (uint32_t)((g.S0 + g.L - ebase + 3) & ~3ll);
+    mbar_expect_tx(bar, 4u * (rwords + 2u * ewords));
+    bulk_g2s(rp, P.row_ptr + rbase, 4u * rwords, bar);
+    if (ewords) {
+        bulk_g2s(cb, P.col_idx + ebase, 4u * ewords, bar);
+        bulk_g2s(vb, P.vals + ebase, 4u * ewords, bar);
+    }
+}
 
-    int x = 0, y0 = 0, nr = 0, r0 = 0, jlo = 0, jhi = 0, cy0 = 0, L = 0;
-    long long S0 = 0;
-    bool valid = false;
-    if (live) {
-        x = (int)(seg / P.tiles_y);
-        y0 = (int)(seg - (long long)x * P.tiles_y) * TW;
-        nr = min(TW, P.no - y0);
-        r0 = x * P.no + y0;
-        tap_range_dev(x, P.m, K, S, P.p, jlo, jhi);
-        cy0 = cum_taps<K, S>(y0, P.n, P.p);
-        S0 = (long long)cum_taps<K, S>(x, P.m, P.p) * P.sy + (long long)(jhi - jlo) * cy0;
-        L = (jhi - jlo) * (cum_taps<K, S>(y0 + nr, P.n, P.p) - cy0);
-        valid = S0 + L <= (long long)P.nnz;  // (zero taps: the prediction runs past the end)
-        if (lane == 0) {
-            mbar_init(bar, 1);
-            mbar_fence_init();
-            if (valid) {
-                const int rbase = r0 & ~3;
-                const uint32_t rwords = (uint32_t)((r0 + nr + 1 - rbase + 3) & ~3);
-                const long long ebase = S0 & ~3ll;
-                const uint32_t ewords = (uint32_t)((S0 + L - ebase + 3) & ~3ll);
-                mbar_expect_tx(bar, 4u * (rwords + 2u * ewords));
-                bulk_g2s(rp, P.row_ptr + rbase, 4u * rwords, bar);
-                if (ewords) {
-                    bulk_g2s(cb, P.col_idx + ebase, 4u * ewords, bar);
-                    bulk_g2s(vb, P.vals + ebase, 4u * ewords, bar);
-                }
-            }
-        }
-    }
-    __syncthreads();  // s_w (and the barrier inits) visible block-wide
-    if (!live) return;
-    if (!valid) {
-        if (lane == 0) P.seg_ok[seg] = 0;
-        return;
-    }
-    uint32_t w[KK];  // taps, compile-time indexed (full rows)
-#pragma unroll
-    for (int q = 0; q < KK; ++q) w[q] = s_w[q];
-    const int cx = jhi - jlo;
-    // Per-row predictions while the copies are in flight: row l stores
-    // cx * cy(y0 + l) entries; its offset in the run is a warp scan of those.
+// Whole warp, segment landed in the slice at `rp`: per-row offsets (a warp
+// scan of cx * cy(y)), then every row checked from shared memory -- interior
+// rows with the fully unrolled k*k compare, clipped rows over their tap
+// range.  Returns the verdict (warp-uniform).
+template <int K, int S, int TW>
+__device__ __forceinline__ bool seg_verify(const BandParams& P, const SegGeom& g, const int* rp,
+                                           const uint32_t (&w)[K * K], const uint32_t* s_w, int lane) {
+    using C = CheckCfg<K, S, TW>;
+    constexpr int RPL = TW / 32;  // rows per lane
+    const int* cb = rp + C::RPW;
+    const uint32_t* vb = reinterpret_cast<const uint32_t*>(cb + C::BUFW);
+    const int cx = g.jhi - g.jlo;
     int off[RPL], ilo_[RPL], ihi_[RPL];
     int run = 0;
 #pragma unroll
     for (int q = 0; q < RPL; ++q) {
         const int l = lane + 32 * q;
-        tap_range_dev(y0 + l, P.n, K, S, P.p, ilo_[q], ihi_[q]);
-        const int c = l < nr ? cx * (ihi_[q] - ilo_[q]) : 0;
+        tap_range_dev(g.y0 + l, P.n, K, S, P.p, ilo_[q], ihi_[q]);
+        const int c = l < g.nr ? cx * (ihi_[q] - ilo_[q]) : 0;
         int inc = c;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -216,22 +210,21 @@ __global__ void __launch_bounds__(CheckCfg<K, S, TW>::WARPS * 32) conv_band_chec
         off[q] = run + inc - c;
         run += __shfl_sync(0xffffffffu, inc, 31);
     }
-    bool ok = run == L;
-    mbar_wait(bar, 0);
-    const int* rps = rp + (r0 & 3);
-    const int* cbs = cb + (int)(S0 & 3);
-    const uint32_t* vbs = vb + (int)(S0 & 3);
-    const int S0i = (int)S0;  // S0 + L <= nnz < 2^31 here
+    bool ok = run == g.L;
+    const int* rps = rp + (g.r0 & 3);
+    const int* cbs = cb + (int)(g.S0 & 3);
+    const uint32_t* vbs = vb + (int)(g.S0 & 3);
+    const int S0i = (int)g.S0;  // S0 + L <= nnz < 2^31 here
     uint32_t bad = 0;
 #pragma unroll
     for (int q = 0; q < RPL; ++q) {
         const int l = lane + 32 * q;
-        if (l < nr) {
-            const int y = y0 + l;
+        if (l < g.nr) {
+            const int y = g.y0 + l;
             ok &= rps[l] == S0i + off[q];
-            if (l == nr - 1) ok &= rps[nr] == S0i + L;
+            if (l == g.nr - 1) ok &= rps[g.nr] == S0i + g.L;
             const int ilo = ilo_[q], ihi = ihi_[q];
-            const int rb = (S * x - P.p) * P.n + (S * y - P.p);
+            const int rb = (S * g.x - P.p) * P.n + (S * y - P.p);
             const int* cl = cbs + off[q];
             const uint32_t* vl = vbs + off[q];
             if (cx == K && ilo == 0 && ihi == K) {
@@ -242,14 +235,49 @@ __global__ void __launch_bounds__(CheckCfg<K, S, TW>::WARPS * 32) conv_band_chec
                         bad |= (uint32_t)(cl[j * K + ii] - (rb + j * P.n + ii)) | (vl[j * K + ii] ^ w[j * K + ii]);
             } else {
                 int e = 0;
-                for (int j = jlo; j < jhi; ++j)
+                for (int j = g.jlo; j < g.jhi; ++j)
                     for (int ii = ilo; ii < ihi; ++ii, ++e)
                         bad |= (uint32_t)(cl[e] - (rb + j * P.n + ii)) | (vl[e] ^ s_w[j * K + ii]);
             }
         }
     }
     ok &= bad == 0u;
-    ok = __all_sync(0xffffffffu, ok);
+    return __all_sync(0xffffffffu, ok);
+}
+
+template <int K, int S, int TW>
+__global__ void __launch_bounds__(CheckCfg<K, S, TW>::WARPS * 32) conv_band_check(const BandParams P) {
+    using C = CheckCfg<K, S, TW>;
+    constexpr int KK = K * K;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __shared__ uint32_t s_w[KK];  // taps, runtime-indexed (clipped rows)
+    for (int q = threadIdx.x; q < KK; q += blockDim.x) s_w[q] = __float_as_uint(__ldg(P.taps + q));
+
+    const long long seg = (long long)blockIdx.x * C::WARPS + warp;
+    const bool live = seg < (long long)P.mo * P.tiles_y;  // warp-uniform
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem) + warp;
+    int* rp = reinterpret_cast<int*>(smem + 128 + (size_t)warp * C::WARP_BYTES);
+    SegGeom g{};
+    if (live) {
+        g = seg_geom<K, S, TW>(P, seg);
+        if (lane == 0) {
+            mbar_init(bar, 1);
+            mbar_fence_init();
+            if (g.valid) seg_issue<K, S, TW>(P, g, rp, bar);
+        }
+    }
+    __syncthreads();  // s_w (and the barrier inits) visible block-wide
+    if (!live) return;
+    if (!g.valid) {
+        if (lane == 0) P.seg_ok[seg] = 0;
+        return;
+    }
+    uint32_t w[KK];  // taps, compile-time indexed (full rows)
+#pragma unroll
+    for (int q = 0; q < KK; ++q) w[q] = s_w[q];
+    mbar_wait(bar, 0);
+    const bool ok = seg_verify<K, S, TW>(P, g, rp, w, s_w, lane);
     if (lane == 0) P.seg_ok[seg] = ok ? 1 : 0;
 }
 
@@ -283,15 +311,25 @@ struct ItemIter {
         if (tx >= tiles_x) tx -= tiles_x, ++img;
     }
 };
-template <int K, int S, int V, int CPT, int TH, int STAGES, int DELTA>
+// FUSED: one kernel does the band check and the apply.  The producer warp,
+// between window loads, checks segments blockIdx.x, blockIdx.x + gridDim.x,
+// ... (bulk copies double-buffered in two extra staging slices), and the
+// consumers take the blocked path unconditionally; conv_band_fixup, launched
+// right after on the same stream, recomputes the rows of any segment that
+// failed its check from the CSR (normally none: it only reads the flags).
+template <int K, int S, int V, int CPT, int TH, int STAGES, int DELTA, bool FUSED>
 __global__ void __launch_bounds__(BandCfg<K, S, V, CPT, TH, STAGES, DELTA>::THREADS, 1)
     conv_spmm_band(const __grid_constant__ CUtensorMap tmap, const BandParams P) {
     using C = BandCfg<K, S, V, CPT, TH, STAGES, DELTA>;
+    using CC = CheckCfg<K, S, C::TW>;
+    static_assert(!FUSED || STAGES * 24 + 16 <= 128, "check barriers fit the 128-byte header");
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
     uint64_t* empty = full + STAGES;
     unsigned long long* s_mask = reinterpret_cast<unsigned long long*>(empty + STAGES);  // per-stage row flags
+    uint64_t* cbar = reinterpret_cast<uint64_t*>(s_mask + STAGES);                       // (FUSED) check slices
     float* xs = reinterpret_cast<float*>(smem + 128);
+    __shared__ uint32_t s_w[FUSED ? C::KK : 1];
 
     const int t = threadIdx.x;
     const int lane = t & 31, warp = t >> 5;
@@ -302,9 +340,82 @@ __global__ void __launch_bounds__(BandCfg<K, S, V, CPT, TH, STAGES, DELTA>::THRE
             mbar_init(&full[st], 1);
             mbar_init(&empty[st], C::CWARPS);
         }
+        if (FUSED) {
+            mbar_init(&cbar[0], 1);
+            mbar_init(&cbar[1], 1);
+        }
         mbar_fence_init();
     }
+    if (FUSED)
+        for (int q = t; q < C::KK; q += blockDim.x) s_w[q] = __float_as_uint(__ldg(P.taps + q));
     __syncthreads();
+
+    if (FUSED && warp == C::CWARPS) {
+        // ---- producer warp, fused: window loads whenever a stage is free,
+        // one segment check (double-buffered) between them.
+        uint32_t w[C::KK];
+#pragma unroll
+        for (int q = 0; q < C::KK; ++q) w[q] = s_w[q];
+        int* cslice = reinterpret_cast<int*>(smem + 128 + (size_t)STAGES * C::SF * 4);
+        constexpr int SLICE = (int)(CC::WARP_BYTES / 4);
+        const long long nseg = (long long)P.mo * P.tiles_y;
+        long long cseg = blockIdx.x, vseg = -1;
+        SegGeom vg{};
+        int cb = 0;
+        uint32_t cph = 0;
+        auto seg_next = [&]() {  // geometry of the next segment, copies into slice cb
+            if (cseg < nseg) {
+                vg = seg_geom<K, S, C::TW>(P, cseg);
+                vseg = cseg;
+                cseg += gridDim.x;
+                if (lane == 0 && vg.valid) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    seg_issue<K, S, C::TW>(P, vg, cslice + cb * SLICE, &cbar[cb]);
+                }
+            } else {
+                vseg = -1;
+            }
+        };
+        seg_next();
+        int it = 0;
+        ItemIter I(P);
+        while (I.img < P.batch || vseg >= 0) {
+            while (I.img < P.batch) {
+                const int st = it % STAGES;
+                int fr = 1;
+                if (lane == 0 && it >= STAGES) fr = mbar_try_wait(&empty[st], (uint32_t)(((it / STAGES) - 1) & 1));
+                if (!__shfl_sync(0xffffffffu, fr, 0)) break;
+                if (lane == 0) {
+                    const int wr0 = S * I.tx * TH - P.p;
+                    const int wc0 = S * I.ty * C::TW - P.p - DELTA;
+                    mbar_expect_tx(&full[st], (uint32_t)(C::WIN * 4));
+                    tma_load_3d(xs + (size_t)st * C::SF, &tmap, wc0, wr0, I.img, &full[st]);
+                }
+                __syncwarp();
+                ++it;
+                I.next();
+            }
+            if (vseg >= 0) {
+                const SegGeom g = vg;
+                const long long sg = vseg;
+                const int b = cb;
+                cb ^= 1;
+                __syncwarp();  // slice cb's previous segment was fully read before its verdict
+                seg_next();
+                bool ok = false;
+                if (g.valid) {
+                    mbar_wait(&cbar[b], (cph >> b) & 1u);
+                    cph ^= 1u << b;
+                    ok = seg_verify<K, S, C::TW>(P, g, cslice + b * SLICE, w, s_w, lane);
+                }
+                if (lane == 0) P.seg_ok[sg] = ok ? 1 : 0;
+            } else if (I.img < P.batch) {  // all checked: wait for the next free stage
+                if (lane == 0) mbar_wait(&empty[it % STAGES], (uint32_t)(((it / STAGES) - 1) & 1));
+                __syncwarp();
+            }
+        }
+        return;
+    }
 
     if (warp == C::CWARPS) {
         // ---- producer warp: per item, the tile rows' band-check flags (one
@@ -353,7 +464,7 @@ __global__ void __launch_bounds__(BandCfg<K, S, V, CPT, TH, STAGES, DELTA>::THRE
         mbar_wait(&full[st], (uint32_t)((it / STAGES) & 1));
         // This warp's rows must all lie in verified segments (and the taps be
         // finite and non-zero) for the blocked path.
-        const bool fast = P.fast_allowed && ((s_mask[st] >> (warp * V)) & VMASK) == VMASK;
+        const bool fast = FUSED || (P.fast_allowed && ((s_mask[st] >> (warp * V)) & VMASK) == VMASK);
         const float* xw = xs + (size_t)st * C::SF;
         float* ybase = P.Y + (long long)img * P.ldy;
 
@@ -440,16 +551,89 @@ __global__ void __launch_bounds__(BandCfg<K, S, V, CPT, TH, STAGES, DELTA>::THRE
     }
 }
 
+// After a fused call: the rows of every segment whose check failed, for every
+// image, recomputed from the CSR in stored order (per-entry, bit-exact).  A
+// programmatic dependent of the fused kernel: resident early, it reads the
+// flags only after griddepcontrol.wait (the fused grid complete and visible).
+template <int TW>
+__global__ void __launch_bounds__(256) conv_band_fixup(const BandParams P) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const long long nseg = (long long)P.mo * P.tiles_y;
+    for (long long seg = blockIdx.x; seg < nseg; seg += gridDim.x) {
+        if (P.seg_ok[seg]) continue;  // block-uniform
+        const int x = (int)(seg / P.tiles_y);
+        const int y0 = (int)(seg - (long long)x * P.tiles_y) * TW;
+        const int nr = min(TW, P.no - y0);
+        const int r0 = x * P.no + y0;
+        for (int q = threadIdx.x; q < nr * P.batch; q += blockDim.x) {
+            const int img = q / nr, r = r0 + (q - img * nr);
+            const float* X = P.X + (long long)img * P.ldx;
+            float acc = 0.0f;
+            for (int e = __ldg(P.row_ptr + r), e1 = __ldg(P.row_ptr + r + 1); e < e1; ++e)
+                acc = fmaf(__ldg(P.vals + e), __ldg(X + __ldg(P.col_idx + e)), acc);
+            P.Y[(long long)img * P.ldy + r] = acc;
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Host side: per-(k, s) blocking and launch.
 // ---------------------------------------------------------------------------
 namespace {
 
+template <typename Kern>
+cudaError_t launch_pdl(Kern kern, unsigned grid, unsigned block, size_t smem, cudaStream_t st, const BandParams& bp) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, bp);
+}
+
+// Fused check + apply (conv_spmm_band<..., true>) and its fixup kernel.
+template <int K, int S, int V, int CPT, int TH, int STAGES, int DELTA>
+cudaError_t run_fused(const BandParams& bp, const CUtensorMap* tmap, cudaStream_t st, int sms) {
+    using C = BandCfg<K, S, V, CPT, TH, STAGES, DELTA>;
+    using CC = CheckCfg<K, S, C::TW>;
+    constexpr size_t SMEM = C::SMEM + 2 * CC::WARP_BYTES;
+    if constexpr (SMEM > 227 * 1024 || STAGES * 24 + 16 > 128) {
+        return cudaErrorNotSupported;
+    } else {
+        auto kern = conv_spmm_band<K, S, V, CPT, TH, STAGES, DELTA, true>;
+        static int occ[64] = {};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (!occ[dev & 63]) {
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+            if (e != cudaSuccess) return e;
+            int o = 0;
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, C::THREADS, SMEM);
+            if (e != cudaSuccess) return e;
+            occ[dev & 63] = std::max(o, 1);
+        }
+        const long long items = (long long)bp.tiles * bp.batch;
+        // every CTA also owns segments: at least one CTA per SM even for short batches
+        const long long grid = std::min<long long>(std::max<long long>(items, sms), (long long)occ[dev & 63] * sms);
+        kern<<<(unsigned)grid, C::THREADS, SMEM, st>>>(*tmap, bp);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        const long long segs = (long long)bp.mo * bp.tiles_y;
+        return launch_pdl(conv_band_fixup<C::TW>, (unsigned)std::min<long long>(segs, 8ll * sms), 256, 0, st, bp);
+    }
+}
+
 template <int K, int S, int V, int CPT, int TH, int STAGES, int DELTA>
 cudaError_t run_cfg(const BandParams& bp, const CUtensorMap* tmap, cudaStream_t st, BandShape* shape,
                     int sms) {
     using C = BandCfg<K, S, V, CPT, TH, STAGES, DELTA>;
-    auto kern = conv_spmm_band<K, S, V, CPT, TH, STAGES, DELTA>;
+    if (!shape && bp.fused) return run_fused<K, S, V, CPT, TH, STAGES, DELTA>(bp, tmap, st, sms);
+    auto kern = conv_spmm_band<K, S, V, CPT, TH, STAGES, DELTA, false>;
     static int occ[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);

@@ -68,3 +68,8 @@ def golden_cases(orc, js):
         if d["variant"] == "zerotap":
             kern = zero_tap_kernel(orc, k, orc.derive_seed(orc.derive_seed(BASE_SEED, d["cfg"]), 99))
         yield key, (m, n, k, s, p), kern, X[0].astype(np.float64)
+
+
+# Kernel pairs of the band path (spconv_csr_last_kernel): the check kernel +
+# apply, or the fused check-and-apply + its fixup pass.
+BAND_KERNELS = ("conv_band_check+conv_spmm_band", "conv_spmm_band<fused>+conv_band_fixup")

@@ -13,7 +13,7 @@ import os
 import numpy as np
 import pytest
 
-from helpers import CONFIGS, golden_cases, problem, sha, sweep_specs, zero_tap_kernel
+from helpers import CONFIGS, golden_cases, problem, sha, sweep_specs, zero_tap_kernel, BAND_KERNELS
 
 pytestmark = pytest.mark.gpu
 
@@ -376,7 +376,7 @@ def test_band_path_is_default(sp, orc, torch_cuda, spec):
     t = build(sp, spec, kern)
     want = orc.spmm_native(*orc.build_native(*spec, kern), X)
     Y = run_spmm(torch_cuda, sp, t, X)
-    assert t.last_kernel == "conv_band_check+conv_spmm_band"
+    assert t.last_kernel in BAND_KERNELS
     assert np.array_equal(bits(Y), bits(want)), spec
     # ldy padded by one float: Y rows lose 16-byte alignment -> scalar stores
     Xd = torch_cuda.from_numpy(X).cuda()
@@ -436,7 +436,7 @@ class _DevArray:
                                          "version": 3}
 
 
-@pytest.mark.parametrize("check", ["side", "same"])
+@pytest.mark.parametrize("check", ["side", "same", "fused"])
 @pytest.mark.parametrize("spec", [(256, 256, 3, 1, 1), (300, 260, 7, 2, 3)])
 def test_band_check_reads_the_matrix(sp, orc, torch_cuda, spec, check, monkeypatch):
     """The band path re-reads T on every call: entries altered in device memory
@@ -444,7 +444,9 @@ def test_band_check_reads_the_matrix(sp, orc, torch_cuda, spec, check, monkeypat
     window, a column moved to an earlier image row) are picked up by the next
     spmm -- the affected segments fail the check and take the per-entry loop --
     and the output is bit-exact vs the oracle on the altered CSR."""
-    monkeypatch.setenv("SPCONV_B200_CHECK", check)  # check kernel on a side stream / the caller's
+    # check kernel on a side stream / on the caller's stream / fused into the apply
+    monkeypatch.setenv("SPCONV_B200_CHECK", "side" if check == "side" else "same")
+    monkeypatch.setenv("SPCONV_B200_FUSED", "1" if check == "fused" else "0")
     m, n, k = spec[:3]
     kern, X = problem(orc, 14, m, n, k, batch=6)
     t = build(sp, spec, kern)
@@ -470,7 +472,7 @@ def test_band_check_reads_the_matrix(sp, orc, torch_cuda, spec, check, monkeypat
     dcv[e_val] = float(val[e_val])
     torch_cuda.cuda.synchronize()
     Y = run_spmm(torch_cuda, sp, t, X)
-    assert t.last_kernel == "conv_band_check+conv_spmm_band"
+    assert t.last_kernel in BAND_KERNELS
     want = orc.spmm_native(ptr, idx, val, X)
     assert not np.array_equal(bits(want), bits(clean))
     assert np.array_equal(bits(Y), bits(want))
@@ -570,3 +572,20 @@ def test_spmm_in_cuda_graph(sp, orc, torch_cuda, spec, batch):
     g.replay()
     torch.cuda.synchronize()
     assert np.array_equal(bits(Yd.cpu().numpy()), bits(want[batch:]))
+
+
+@pytest.mark.parametrize("fused", ["0", "1"])
+@pytest.mark.parametrize("spec", [(1024, 1024, 3, 1, 1), (200, 132, 5, 1, 2), (130, 68, 3, 2, 0),
+                                  (300, 260, 7, 2, 3), (97, 64, 5, 2, 2), (64, 40, 3, 1, 1)])
+def test_band_fused_and_two_kernel(sp, orc, torch_cuda, spec, fused, monkeypatch):
+    """The fused check-and-apply (segments checked by the producer warps, a
+    fixup pass after) and the two-kernel form give the same bit-exact results
+    on every band geometry, including grids with more CTAs than work items."""
+    monkeypatch.setenv("SPCONV_B200_FUSED", fused)
+    monkeypatch.setenv("SPCONV_B200_CHECK", "same")
+    m, n, k = spec[:3]
+    kern, X = problem(orc, 18, m, n, k, batch=5)
+    t = build(sp, spec, kern)
+    Y = run_spmm(torch_cuda, sp, t, X)
+    assert t.last_kernel == BAND_KERNELS[int(fused)]
+    assert np.array_equal(bits(Y), bits(orc.spmm_native(*orc.build_native(*spec, kern), X)))
