@@ -531,6 +531,10 @@ int attach_csc_conv(spconv_csr* h, cudaStream_t st) {
     cp.col_ptr = h->csc_ptr;
     cp.row_idx = h->csc_idx;
     cp.vals = h->csc_vals;
+    {
+        const char* bs = std::getenv("SPCONV_B200_BULK_STORE");
+        cp.bulk_store = bs ? std::atoi(bs) : 1;
+    }
     const int64_t per_axis = std::min<int64_t>(g.k, (g.k + g.s - 1) / g.s);
     bool nonzero = true;
     for (float v : h->host_taps) nonzero &= v != 0.0f;
@@ -676,6 +680,10 @@ int spconv_build_csr(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
     bp.col_idx = h->col_idx;
     bp.vals = h->vals;
     bp.taps_out = h->taps;
+    {
+        const char* bs = std::getenv("SPCONV_B200_BULK_STORE");
+        bp.bulk_store = bs ? std::atoi(bs) : 1;
+    }
     char* tab = nullptr;
     if (k <= spb::kSmallK) {  // tables ride in the kernel parameters: no copies, no allocation
         bp.small = 1;

@@ -20,6 +20,7 @@
 // Entries are staged in shared memory at the global offset's 16-byte phase and
 // streamed out with vector stores (as csr_build.cu does).
 #include "internal.h"
+#include "tma.cuh"
 
 namespace spb {
 
@@ -165,6 +166,7 @@ __global__ void __launch_bounds__(256) csc_build_kernel(const CscParams P) {
         }
     }
     if (staged) {
+        if (P.bulk_store) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();
         const int head = min(total, (4 - mis) & 3);
         if (t < head) {
@@ -176,9 +178,17 @@ __global__ void __launch_bounds__(256) csc_build_kernel(const CscParams P) {
         const float4* sval = reinterpret_cast<const float4*>(dval + mis + head);
         int4* grow = reinterpret_cast<int4*>(P.row_idx + base + head);
         float4* gval = reinterpret_cast<float4*>(P.vals + base + head);
-        for (int q = t; q < nvec; q += R) {
-            __stcs(grow + q, srow[q]);
-            __stcs(gval + q, sval[q]);
+        if (P.bulk_store) {  // the 16-byte body through the TMA engine: two instructions
+            if (t == 0 && nvec > 0) {
+                bulk_s2g(grow, srow, (uint32_t)nvec * 16u);
+                bulk_s2g(gval, sval, (uint32_t)nvec * 16u);
+                bulk_commit_wait_read();
+            }
+        } else {
+            for (int q = t; q < nvec; q += R) {
+                __stcs(grow + q, srow[q]);
+                __stcs(gval + q, sval[q]);
+            }
         }
         const int done = head + 4 * nvec;
         if (t < total - done) {

@@ -28,6 +28,7 @@
 #include <cstring>
 
 #include "internal.h"
+#include "tma.cuh"
 
 namespace spb {
 
@@ -196,6 +197,7 @@ __global__ void __launch_bounds__(256) csr_build_kernel(const BuildParams P) {
         }
     }
     if (staged) {
+        if (P.bulk_store) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();
         // Global [base, base + total) <- staged [mis, mis + total): scalar head,
         // 16-byte body, scalar tail.
@@ -209,9 +211,17 @@ __global__ void __launch_bounds__(256) csr_build_kernel(const BuildParams P) {
         const float4* sval = reinterpret_cast<const float4*>(dval + mis + head);
         int4* gcol = reinterpret_cast<int4*>(P.col_idx + base + head);
         float4* gval = reinterpret_cast<float4*>(P.vals + base + head);
-        for (int q = t; q < nvec; q += R) {
-            __stcs(gcol + q, scol[q]);
-            __stcs(gval + q, sval[q]);
+        if (P.bulk_store) {  // the 16-byte body through the TMA engine: two instructions
+            if (t == 0 && nvec > 0) {
+                bulk_s2g(gcol, scol, (uint32_t)nvec * 16u);
+                bulk_s2g(gval, sval, (uint32_t)nvec * 16u);
+                bulk_commit_wait_read();
+            }
+        } else {
+            for (int q = t; q < nvec; q += R) {
+                __stcs(gcol + q, scol[q]);
+                __stcs(gval + q, sval[q]);
+            }
         }
         const int done = head + 4 * nvec;
         if (t < total - done) {
@@ -294,6 +304,7 @@ __global__ void __launch_bounds__(256) csr_build_warp(const BuildParams P) {
             }
         }
     }
+    if (P.bulk_store) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     const int head = min(total, (4 - mis) & 3);
     if (lane < head) {
@@ -305,9 +316,17 @@ __global__ void __launch_bounds__(256) csr_build_warp(const BuildParams P) {
     const float4* sval = reinterpret_cast<const float4*>(dval + mis + head);
     int4* gcol = reinterpret_cast<int4*>(P.col_idx + base + head);
     float4* gval = reinterpret_cast<float4*>(P.vals + base + head);
-    for (int q = lane; q < nvec; q += 32) {
-        __stcs(gcol + q, scol[q]);
-        __stcs(gval + q, sval[q]);
+    if (P.bulk_store) {
+        if (lane == 0 && nvec > 0) {
+            bulk_s2g(gcol, scol, (uint32_t)nvec * 16u);
+            bulk_s2g(gval, sval, (uint32_t)nvec * 16u);
+            bulk_commit_wait_read();
+        }
+    } else {
+        for (int q = lane; q < nvec; q += 32) {
+            __stcs(gcol + q, scol[q]);
+            __stcs(gval + q, sval[q]);
+        }
     }
     const int done = head + 4 * nvec;
     if (lane < total - done) {

@@ -43,6 +43,7 @@ struct BuildParams {
     int32_t* col_idx;
     float* vals;
     float* taps_out;  // k*k taps copied here by block 0 (the handle's device tap table)
+    int bulk_store;   // write staged entries back with TMA bulk stores (else 16-byte st.global)
 };
 
 // CSC build (csc_build.cu): the conv transform stored column-major.
@@ -51,6 +52,7 @@ struct CscParams {
     int cols;
     int stage;        // 1: stage entries in shared memory
     int stage_words;  // words per staging array
+    int bulk_store;   // write staged entries back with TMA bulk stores
     const float* taps;  // device k*k taps
     int32_t* col_ptr;
     int32_t* row_idx;

@@ -478,11 +478,15 @@ def test_band_check_reads_the_matrix(sp, orc, torch_cuda, spec, check, monkeypat
     assert np.array_equal(bits(Y), bits(want))
 
 
+@pytest.mark.parametrize("bulk_store", ["0", "1"])
 @pytest.mark.parametrize("variant", ["block", "warp"])
-def test_build_variants_bitexact(sp, orc, variant):
-    """Both CSR build kernels (block scan / warp-local, SPCONV_B200_BUILD) give
-    the oracle's arrays for every unrolled k, dense and zero-tap kernels."""
+def test_build_variants_bitexact(sp, orc, variant, bulk_store, monkeypatch):
+    """Both CSR build kernels (block scan / warp-local, SPCONV_B200_BUILD), with
+    the staged entries written back by TMA bulk stores or by 16-byte stores
+    (SPCONV_B200_BULK_STORE), give the oracle's arrays for every unrolled k,
+    dense and zero-tap kernels; so does the CSC build."""
     rng = np.random.default_rng(21)
+    monkeypatch.setenv("SPCONV_B200_BULK_STORE", bulk_store)
     os.environ["SPCONV_B200_BUILD"] = variant
     try:
         for spec in [(70, 45, 1, 1, 1), (130, 97, 3, 1, 1), (64, 80, 5, 2, 2), (101, 77, 7, 2, 3),
@@ -494,6 +498,13 @@ def test_build_variants_bitexact(sp, orc, variant):
                     kern[rng.random(k * k) < 0.3] = 0.0
                 t = build(sp, spec, kern)
                 assert_same_csr(t, orc.build_native(*spec, kern))
+                tc = sp.build_transform(sp.Kernel(k, kern.astype(np.float64)), sp.ConvSpec(*spec),
+                                        layout=sp.Layout.CSC)
+                ptr, idx, val = orc.build_transform(*spec, kern.astype(np.float64))
+                want = orc.transpose(ptr.size - 1, spec[0] * spec[1], ptr, idx, val)
+                got = tc.export()
+                assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+                assert np.array_equal(got[2].view(np.uint64), want[2].view(np.uint64))
     finally:
         del os.environ["SPCONV_B200_BUILD"]
 
