@@ -344,7 +344,7 @@ static cudaError_t launch_w(BuildParams bp, cudaStream_t st) {
     int warps = 8;
     while (warps > 1 && tab_bytes + warps * per_warp > 100 * 1024) warps >>= 1;
     const size_t smem = tab_bytes + warps * per_warp;
-    static bool attr[64] = {};
+    static std::atomic<bool> attr[64];  // per device (benign concurrent first use)
     int dev = 0;
     cudaGetDevice(&dev);
     if (smem > 48 * 1024 && !attr[dev & 63]) {

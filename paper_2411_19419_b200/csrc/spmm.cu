@@ -406,7 +406,7 @@ static cudaError_t launch_bulk_k(const SpecParams& sp, bool spec, cudaStream_t s
     const bool bulk = sel && !std::strcmp(sel, "bulk");
     auto kern = spec ? (bulk ? csr_spmv_bulk<KMAX, true, true> : csr_spmv_bulk<KMAX, true, false>)
                      : (bulk ? csr_spmv_bulk<KMAX, false, true> : csr_spmv_bulk<KMAX, false, false>);
-    static bool attr_set[4][64] = {};
+    static std::atomic<bool> attr_set[4][64];
     int dev = 0;
     cudaGetDevice(&dev);
     const int which = (spec ? 2 : 0) + (bulk ? 1 : 0);
@@ -439,7 +439,7 @@ cudaError_t launch_spmv_warp(const SpecParams& sp, int kmax, bool spec, cudaStre
 template <int BT>
 static cudaError_t launch_bt(const TiledParams& tp, const CUtensorMap* tmap, size_t smem,
                              cudaStream_t st) {
-    static bool attr_set[64] = {};
+    static std::atomic<bool> attr_set[64];
     int dev = 0;
     cudaGetDevice(&dev);
     if (!attr_set[dev & 63]) {

@@ -606,7 +606,7 @@ cudaError_t run_fused(const BandParams& bp, const CUtensorMap* tmap, cudaStream_
         return cudaErrorNotSupported;
     } else {
         auto kern = conv_spmm_band<K, S, V, CPT, TH, STAGES, DELTA, true>;
-        static int occ[64] = {};
+        static std::atomic<int> occ[64];  // per device; 0 = not yet queried
         int dev = 0;
         cudaGetDevice(&dev);
         if (!occ[dev & 63]) {
@@ -634,7 +634,7 @@ cudaError_t run_cfg(const BandParams& bp, const CUtensorMap* tmap, cudaStream_t 
     using C = BandCfg<K, S, V, CPT, TH, STAGES, DELTA>;
     if (!shape && bp.fused) return run_fused<K, S, V, CPT, TH, STAGES, DELTA>(bp, tmap, st, sms);
     auto kern = conv_spmm_band<K, S, V, CPT, TH, STAGES, DELTA, false>;
-    static int occ[64] = {};
+    static std::atomic<int> occ[64];  // per device; 0 = not yet queried
     int dev = 0;
     cudaGetDevice(&dev);
     if (!occ[dev & 63]) {
@@ -671,7 +671,7 @@ cudaError_t run_check(const BandParams& bp, cudaStream_t st, int sms) {
     (void)sms;
     using C = CheckCfg<K, S, TW>;
     auto kern = conv_band_check<K, S, TW>;
-    static bool init[64] = {};
+    static std::atomic<bool> init[64];
     int dev = 0;
     cudaGetDevice(&dev);
     if (!init[dev & 63]) {

@@ -306,7 +306,7 @@ cudaError_t render_entries(const int32_t* row_ptr, const int32_t* col_idx, const
     text_size_kernel<<<blocks, 256, 0, st>>>(row_ptr, col_idx, vals, rows, scratch);
     text_scan_kernel<<<1, 1024, 0, st>>>(scratch, blocks, base);
     if (size_only) return cudaGetLastError();
-    static bool attr[64] = {};
+    static std::atomic<bool> attr[64];  // per device (benign concurrent first use)
     if (!attr[dev & 63]) {
         e = cudaFuncSetAttribute(text_write_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  kStageBytes + 256 * 64);
