@@ -180,10 +180,20 @@ def cpu_baseline(spec, seconds: float = 10.0):
         if time.perf_counter() - t0 >= seconds:
             break
     dt = time.perf_counter() - t0
+    single = None
+    if kind == "reference" and cores > 1:  # threads=1 beside threads=nproc
+        T.convolve(img, threads=1)
+        s0 = time.perf_counter()
+        reps1 = 0
+        while time.perf_counter() - s0 < min(3.0, seconds):
+            T.convolve(img, threads=1)
+            reps1 += 1
+        d1 = time.perf_counter() - s0
+        single = {"value": nnz * reps1 / d1 / 1e9, "cores": 1, "us_per_image": d1 / reps1 * 1e6}
     return {"value": nnz * reps / dt / 1e9, "unit": UNIT, "cores": cores, "kind": kind,
             "sample": f"{reps} single-image convolve() calls on {m}x{n} k{k} s{s} p{p} "
                       f"({dt:.1f} s, threads={cores}); build_transform {build_s * 1e3:.0f} ms",
-            "build_ms": build_s * 1e3, "us_per_image": dt / reps * 1e6}
+            "build_ms": build_s * 1e3, "us_per_image": dt / reps * 1e6, "single_thread": single}
 
 
 def run_reference(args, cfg):
