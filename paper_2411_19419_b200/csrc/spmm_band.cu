@@ -559,19 +559,25 @@ template <int TW>
 __global__ void __launch_bounds__(256) conv_band_fixup(const BandParams P) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     const long long nseg = (long long)P.mo * P.tiles_y;
-    for (long long seg = blockIdx.x; seg < nseg; seg += gridDim.x) {
-        if (P.seg_ok[seg]) continue;  // block-uniform
-        const int x = (int)(seg / P.tiles_y);
-        const int y0 = (int)(seg - (long long)x * P.tiles_y) * TW;
-        const int nr = min(TW, P.no - y0);
-        const int r0 = x * P.no + y0;
-        for (int q = threadIdx.x; q < nr * P.batch; q += blockDim.x) {
-            const int img = q / nr, r = r0 + (q - img * nr);
-            const float* X = P.X + (long long)img * P.ldx;
-            float acc = 0.0f;
-            for (int e = __ldg(P.row_ptr + r), e1 = __ldg(P.row_ptr + r + 1); e < e1; ++e)
-                acc = fmaf(__ldg(P.vals + e), __ldg(X + __ldg(P.col_idx + e)), acc);
-            P.Y[(long long)img * P.ldy + r] = acc;
+    // one flag per thread; a chunk without failures costs one load and one barrier
+    for (long long base = (long long)blockIdx.x * blockDim.x; base < nseg; base += (long long)gridDim.x * blockDim.x) {
+        const long long mine = base + threadIdx.x;
+        const bool bad = mine < nseg && P.seg_ok[mine] == 0;
+        if (!__syncthreads_or(bad)) continue;
+        for (long long seg = base; seg < min(nseg, base + (long long)blockDim.x); ++seg) {
+            if (P.seg_ok[seg]) continue;  // block-uniform
+            const int x = (int)(seg / P.tiles_y);
+            const int y0 = (int)(seg - (long long)x * P.tiles_y) * TW;
+            const int nr = min(TW, P.no - y0);
+            const int r0 = x * P.no + y0;
+            for (int q = threadIdx.x; q < nr * P.batch; q += blockDim.x) {
+                const int img = q / nr, r = r0 + (q - img * nr);
+                const float* X = P.X + (long long)img * P.ldx;
+                float acc = 0.0f;
+                for (int e = __ldg(P.row_ptr + r), e1 = __ldg(P.row_ptr + r + 1); e < e1; ++e)
+                    acc = fmaf(__ldg(P.vals + e), __ldg(X + __ldg(P.col_idx + e)), acc);
+                P.Y[(long long)img * P.ldy + r] = acc;
+            }
         }
     }
 }
@@ -624,7 +630,8 @@ cudaError_t run_fused(const BandParams& bp, const CUtensorMap* tmap, cudaStream_
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
         const long long segs = (long long)bp.mo * bp.tiles_y;
-        return launch_pdl(conv_band_fixup<C::TW>, (unsigned)std::min<long long>(segs, 8ll * sms), 256, 0, st, bp);
+        return launch_pdl(conv_band_fixup<C::TW>, (unsigned)std::min<long long>((segs + 255) / 256, sms), 256, 0, st,
+                          bp);
     }
 }
 
