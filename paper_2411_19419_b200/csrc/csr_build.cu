@@ -99,19 +99,23 @@ __global__ void __launch_bounds__(256) csr_build_kernel(const BuildParams P) {
 
     const int r0 = blockIdx.x * R;
     const int r = r0 + t;
+    const int x0 = r0 / P.no, y0 = r0 - x0 * P.no;  // (block-uniform: one division)
 
     // ---- per-row count (Theorem 2.1 with the zero-tap mask) ----
     int cnt = 0, x = 0, y = 0, jlo = 0, jhi = 0, ilo = 0, ihi = 0;
     if (r < P.rows) {
-        x = r / P.no;
-        y = r - x * P.no;
+        x = x0;
+        y = y0 + t;
+        if (y >= P.no) {  // the block spans image rows: at most a few wraps unless n_out is tiny
+            x += y / P.no;
+            y -= (y / P.no) * P.no;
+        }
         tap_range(x, P.m, k, P.s, P.p, jlo, jhi);
         tap_range(y, P.n, k, P.s, P.p, ilo, ihi);
         cnt = DENSE ? (jhi - jlo) * (ihi - ilo) : sat_rect(s_sat, k1, jlo, jhi, ilo, ihi);
     }
 
     // ---- closed-form global offset of row r0 = (x0, y0) ----
-    const int x0 = r0 / P.no, y0 = r0 - x0 * P.no;
     int jlo0, jhi0;
     tap_range(x0, P.m, k, P.s, P.p, jlo0, jhi0);
     long long part = 0;
@@ -164,7 +168,18 @@ __global__ void __launch_bounds__(256) csr_build_kernel(const BuildParams P) {
     }
     if (r < P.rows && cnt > 0) {
         const int xr = P.s * x - P.p, yc = P.s * y - P.p;
-        if (KC) {
+        if (KC && DENSE && cnt == KC * KC) {
+            // Interior row (every tap stored): the K x K pattern, no predicates.
+#pragma unroll
+            for (int j = 0; j < KC; ++j) {
+                const int rowbase = (xr + j) * P.n + yc;
+#pragma unroll
+                for (int i = 0; i < KC; ++i) {
+                    dcol[o + j * KC + i] = rowbase + i;
+                    dval[o + j * KC + i] = s_taps[j * KC + i];
+                }
+            }
+        } else if (KC) {
             // Fully unrolled K x K pattern; clipped / zero taps are predicated off.
 #pragma unroll
             for (int j = 0; j < KC; ++j) {
