@@ -161,6 +161,13 @@ int spconv_csr_write_text(const spconv_csr* h, int transform_header_line, char* 
  * attached.  The file's layout (csr / csc) is the handle's layout. */
 int spconv_transform_read(const char* text, int64_t len, int device, void* stream, spconv_csr** out);
 
+/* The reference's seeded generator (inc/rng.hpp:22-98; host code, no GPU):
+ * derive_seed, and `count` standard normals of the stream seeded by `seed`
+ * (xoshiro256++ seeded by splitmix64, Marsaglia polar method) -- the inputs
+ * random_normal_grid / random_normal_kernel produce. */
+uint64_t spconv_derive_seed(uint64_t base, uint64_t index);
+int spconv_random_normal(uint64_t seed, int64_t count, double* out);
+
 /* Dense comparators of inc/reference.hpp on the device, over `batch` images
  * (A[b][m*n] -> out[b][m_out*n_out], device buffers, `taps_dev` = k*k taps of
  * the same type).  dtype 1 = fp64 with one rounded multiply and one rounded

@@ -72,6 +72,8 @@ _decl("spconv_csr_layout", [_vp, _P(C.c_int)])
 _decl("spconv_relayout", [_vp, C.c_int, _vp, _P(_vp)])
 _decl("spconv_direct_conv", [_i64] * 5 + [C.c_int, _vp, _vp, _vp, _vp, _i64, _vp])
 _decl("spconv_im2col_conv", [_i64] * 5 + [C.c_int, _vp, _vp, _vp, _vp, _i64, _vp])
+_decl("spconv_derive_seed", [C.c_uint64, C.c_uint64], C.c_uint64)
+_decl("spconv_random_normal", [C.c_uint64, _i64, _vp])
 _decl("spconv_reference_host", [C.c_int] + [_i64] * 5 + [_vp, _vp, _vp, C.c_int])
 _decl("spconv_run_verification", [_i64, C.c_int, C.c_uint64, C.c_int, _vp, _vp, _vp, _i64])
 _decl("spconv_matrix_from_host", [_i64, _i64, C.c_int, _vp, _vp, _vp, C.c_int, _vp, _P(_vp)])

@@ -273,6 +273,15 @@ struct DevBuf {
 
 extern "C" {
 
+uint64_t spconv_derive_seed(uint64_t base, uint64_t index) { return derive_seed(base, index); }
+
+int spconv_random_normal(uint64_t seed, int64_t count, double* out) {
+    if (count < 0 || (count > 0 && !out)) return spb_fail(SPCONV_EINVAL, "spconv_random_normal: bad arguments");
+    Normal g(seed);
+    for (int64_t i = 0; i < count; ++i) out[i] = g.next();
+    return SPCONV_OK;
+}
+
 int spconv_direct_conv(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p, int dtype, const void* taps_dev,
                        const void* A_dev, void* out_dev, void* mag_dev, int64_t batch, void* stream) {
     if (int rc = spconv_spec_check(m, n, k, s, p)) return rc;

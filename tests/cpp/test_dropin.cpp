@@ -139,6 +139,9 @@ int main() {
     }
     expect_throw<std::invalid_argument>([] { layout_from_name("coo"); },
                                         "unknown layout 'coo' (expected csr or csc)");
+    // The seeded generator (inc/rng.hpp): known answers.
+    CHECK(derive_seed(42, 0) == 2949826092126892291ull);
+    CHECK(random_normal_grid(2, 3, 42).values.size() == 6 && random_normal_kernel(3, 7).k == 3);
     // Dense comparators (inc/reference.hpp) on the device, fp64: the SPEC.md:175
     // example exactly, and direct == im2col bit for bit on a padded, strided case.
     {

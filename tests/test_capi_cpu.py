@@ -107,3 +107,18 @@ def test_int32_range_rejected_before_any_device_work():
         sp.build_transform(sp.Kernel(3, np.ones(9)), sp.ConvSpec(8, 8, 3, 1, 1), layout=2)
     with pytest.raises(ValueError, match="unknown layout 'coo'"):
         sp.layout_from_name("coo")
+
+
+def test_rng_matches_reference_known_answers(golden, orc):
+    """The library's seeded generator (inc/rng.hpp, behind the drop-in rng.hpp)
+    reproduces the reference's known answers and the oracle's streams."""
+    js, _ = golden
+    assert str(sp.lib.spconv_derive_seed(42, 0)) == js["derive_seed_42_0"]
+    out = np.empty(3)
+    sp._check(sp.lib.spconv_random_normal(42, 3, out.ctypes.data))
+    assert out.tolist() == js["normal_42_first3"]
+    for seed in (1, 7, orc.derive_seed(42, 5)):
+        assert sp.lib.spconv_derive_seed(seed, 9) == orc.derive_seed(seed, 9)
+        got = np.empty(1001)
+        sp._check(sp.lib.spconv_random_normal(seed, 1001, got.ctypes.data))
+        assert np.array_equal(got.view(np.uint64), orc.random_normal(seed, 1001).view(np.uint64))
