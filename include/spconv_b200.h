@@ -191,6 +191,16 @@ int spconv_im2col_conv(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p, in
 int spconv_reference_host(int mode, int64_t m, int64_t n, int64_t k, int64_t s, int64_t p, const double* kernel,
                           const double* A, double* out, int device);
 
+/* Device-resident timing for the layer-table bench (inc/bench.hpp:202-261 with
+ * a GPU method column): `reps` back-to-back applies captured in one CUDA graph,
+ * replayed `warmup` times untimed and `trials` times between CUDA events;
+ * *mean_us / *sem_us per apply.  method 0 = spconv_spmm of `h` over `batch`
+ * device-resident images; method 1 = the fp32 device im2col_conv of
+ * (m,n,k,s,p) with `taps_host` (one image; h unused). */
+int spconv_time_apply(int method, const spconv_csr* h, int64_t batch, int64_t m, int64_t n, int64_t k, int64_t s,
+                      int64_t p, const float* taps_host, int64_t reps, int64_t trials, int64_t warmup,
+                      double* mean_us, double* sem_us);
+
 /* run_verification (inc/verify.hpp:59-169) over the device path: for every
  * m, n <= max_dim, p <= 3, s <= 3, k <= min(m,n) + 2p, the Theorem 2.1 count
  * against the brute-force overlap count and nnz(T), and for `seeds` seeded

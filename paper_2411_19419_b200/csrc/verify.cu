@@ -306,6 +306,94 @@ int spconv_im2col_conv(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p, in
     return SPCONV_OK;
 }
 
+// Device-resident timing of one apply method (the layer-table bench's GPU
+// column): `reps` back-to-back calls captured in one CUDA graph on a private
+// stream, replayed `warmup` times untimed and `trials` times between CUDA
+// events; per-call mean and SEM over the trials in microseconds.
+// method 0 = spconv_spmm on `h` (batch images), 1 = fp32 im2col_conv of the
+// geometry and k*k taps given (one image).
+int spconv_time_apply(int method, const spconv_csr* h, int64_t batch, int64_t m, int64_t n, int64_t k, int64_t s,
+                      int64_t p, const float* taps_host, int64_t reps, int64_t trials, int64_t warmup,
+                      double* mean_us, double* sem_us) {
+    if (!mean_us || !sem_us || reps < 1 || trials < 1 || warmup < 0 || batch < 1)
+        return spb_fail(SPCONV_EINVAL, "spconv_time_apply: bad arguments");
+    if (method == 0 && !h) return spb_fail(SPCONV_EINVAL, "spconv_time_apply: null handle");
+    if (method == 1) {
+        if (int rc = spconv_spec_check(m, n, k, s, p)) return rc;
+        if (!taps_host) return spb_fail(SPCONV_EINVAL, "spconv_time_apply: null taps");
+    }
+    if (method != 0 && method != 1) return spb_fail(SPCONV_EINVAL, "spconv_time_apply: method must be 0 or 1");
+    int64_t rows, cols;
+    if (method == 0) {
+        int64_t nz;
+        spconv_csr_shape(h, &rows, &cols, &nz);
+    } else {
+        rows = ((m + 2 * p - k) / s + 1) * ((n + 2 * p - k) / s + 1);
+        cols = m * n;
+        batch = 1;
+    }
+    cudaStream_t st = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    DevBuf dx, dy, dk, dpatch;
+    std::vector<double> us;
+    cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = dx.reserve((size_t)(batch * cols) * 4);
+    if (e == cudaSuccess) e = dy.reserve((size_t)(batch * rows) * 4);
+    if (e == cudaSuccess) e = cudaMemset(dx.p, 0, (size_t)(batch * cols) * 4);
+    if (e == cudaSuccess && method == 1) {
+        e = dk.reserve((size_t)(k * k) * 4);
+        if (e == cudaSuccess) e = dpatch.reserve((size_t)(k * k * rows) * 4);
+        if (e == cudaSuccess) e = cudaMemcpy(dk.p, taps_host, (size_t)(k * k) * 4, cudaMemcpyHostToDevice);
+    }
+    int rc = SPCONV_OK;
+    auto call = [&]() -> int {
+        if (method == 0)
+            return spconv_spmm(h, (const float*)dx.p, cols, (float*)dy.p, rows, batch, st);
+        const cudaError_t ce = spb::launch_im2col_conv(0, (int)m, (int)n, (int)k, (int)s, (int)p, 1, dk.p, dx.p,
+                                                       dy.p, dpatch.p, st);
+        return ce == cudaSuccess ? SPCONV_OK : spb_fail(SPCONV_ECUDA, cudaGetErrorString(ce));
+    };
+    if (e == cudaSuccess) rc = call();  // first use outside the capture (attributes, workspaces)
+    if (e == cudaSuccess && rc == SPCONV_OK) e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess && rc == SPCONV_OK) e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess && rc == SPCONV_OK) {
+        for (int64_t i = 0; i < reps && rc == SPCONV_OK; ++i) rc = call();
+        const cudaError_t ec = cudaStreamEndCapture(st, &graph);
+        if (e == cudaSuccess) e = ec;
+    }
+    if (e == cudaSuccess && rc == SPCONV_OK) e = cudaGraphInstantiate(&exec, graph, 0);
+    if (e == cudaSuccess && rc == SPCONV_OK) e = cudaEventCreate(&e0);
+    if (e == cudaSuccess && rc == SPCONV_OK) e = cudaEventCreate(&e1);
+    for (int64_t i = 0; i < warmup && e == cudaSuccess && rc == SPCONV_OK; ++i) e = cudaGraphLaunch(exec, st);
+    if (e == cudaSuccess && rc == SPCONV_OK) e = cudaStreamSynchronize(st);
+    for (int64_t i = 0; i < trials && e == cudaSuccess && rc == SPCONV_OK; ++i) {
+        float ms = 0.0f;
+        e = cudaEventRecord(e0, st);
+        if (e == cudaSuccess) e = cudaGraphLaunch(exec, st);
+        if (e == cudaSuccess) e = cudaEventRecord(e1, st);
+        if (e == cudaSuccess) e = cudaEventSynchronize(e1);
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, e0, e1);
+        us.push_back(ms * 1e3 / (double)reps);
+    }
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    if (st) cudaStreamDestroy(st);
+    if (rc != SPCONV_OK) return rc;
+    if (e != cudaSuccess) return spb_fail(SPCONV_ECUDA, std::string("spconv_time_apply: ") + cudaGetErrorString(e));
+    double sum = 0.0;
+    for (double v : us) sum += v;
+    const double mean = sum / (double)us.size();
+    double sq = 0.0;
+    for (double v : us) sq += (v - mean) * (v - mean);
+    *mean_us = mean;
+    *sem_us = us.size() > 1 ? std::sqrt(sq / (double)(us.size() - 1)) / std::sqrt((double)us.size()) : 0.0;
+    return SPCONV_OK;
+}
+
 // Host-buffer fp64 forms of the comparators (the reference's own signatures
 // take host grids): device buffers for one call, the device kernels, copies
 // back.  mode 0 = direct_conv, 1 = im2col_conv, 2 = the im2col lowering only

@@ -161,6 +161,24 @@ int main() {
         expect_throw<std::invalid_argument>([] { direct_conv(Grid(3, 3), Kernel(1, {1.0}), ConvSpec(4, 4, 1, 1, 0)); },
                                             "direct_conv: input is 3x3 but spec is (m=4");
     }
+    // The layer-table bench (inc/bench.hpp) on the GPU: parser checks, one
+    // tiny table, the report format.
+    {
+        std::istringstream csv("name,m,n,k,s,p\nconvA,16,16,3,1,1\npoolA,16,16,2,2,0\n");
+        const std::vector<LayerConfig> table = load_layer_table(csv, "t.csv");
+        CHECK(table.size() == 2 && table[1].name == "poolA" && table[1].k == 2);
+        const std::vector<BenchResult> rs = run_table_bench(table, 5, 2, 42);
+        CHECK(rs.size() == 6);
+        for (const BenchResult& r : rs) CHECK(r.mean_us > 0.0 && r.trials == 5);
+        const std::string md = emit_report(rs, ReportFormat::Markdown);
+        CHECK(md.find("| TOTAL | CSR-SpMV |") != std::string::npos);
+        CHECK(emit_report(rs, ReportFormat::Csv).rfind("layer,method,mean_us,sem_us,build_time_us\nconvA,CSR-SpMV,", 0) == 0);
+        std::istringstream bad("name,m,n,k,s,p\nx,4,4,9,1,0\n");
+        expect_throw<std::runtime_error>([&] { load_layer_table(bad, "b.csv"); },
+                                         "b.csv:2: layer 'x': ConvSpec: kernel larger than padded input");
+        std::istringstream bad2("name,m,n,k,s,p\nx,4,4x,3,1,0\n");
+        expect_throw<std::runtime_error>([&] { load_layer_table(bad2, "c.csv"); }, "c.csv:2: not an integer: '4x'");
+    }
     // The verification sweep on the device path (inc/verify.hpp), small grid.
     {
         VerifyOptions opt;
