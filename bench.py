@@ -517,6 +517,10 @@ def run_ours(args, cfg):
                 "workload": cfg["name"], "m": m, "n": n, "k": k, "s": s, "p": p,
                 "global_batch": total_batch, "per_gpu_batch": b, "rows": rows, "cols": cols,
                 "nnz": nnz, "parallelism": f"batch-dp{world} (CSR replica per GPU, no collective)",
+                "why_this_config": ("BASELINE metric is quoted 'at 1/2/4/8 B200': configs[2] (batch 256 of "
+                                    "1024^2, sharded over 1/2/4/8); configs[1] (single 512^2 SpMV, 14.6 MB, "
+                                    "L2-sized) is reported under secondary.config2 (cold and warm)")
+                if args.config == 3 and not args.spec else None,
                 "l2": l2,
             },
             "gb_per_s": achieved,
