@@ -71,6 +71,13 @@ struct Kernel {
     double at(index_t j, index_t i) const { return values[static_cast<std::size_t>(j * k + i)]; }
 };
 
+/// The kernel rotated by 180 degrees (inc/conv.hpp:98-109): passing
+/// flipped(K) gives textbook convolution instead of correlation.
+inline Kernel flipped(const Kernel& kern) {
+    std::vector<double> v(kern.values.rbegin(), kern.values.rend());  // (j, i) -> (k-1-j, k-1-i)
+    return Kernel(kern.k, std::move(v));
+}
+
 inline DenseVector vectorize(const Grid& a) { return a.values; }
 
 inline Grid unvectorize(DenseVector x, index_t rows, index_t cols) {

@@ -9,6 +9,8 @@
 #pragma once
 
 #include <cstdlib>
+#include <istream>
+#include <iterator>
 #include <memory>
 #include <mutex>
 #include <ostream>
@@ -57,6 +59,13 @@ inline int default_device() {
 }
 
 }  // namespace detail
+
+/// One stored coordinate (inc/sparse.hpp:35-40).
+struct Entry {
+    index_t row;
+    index_t col;
+    double value;
+};
 
 /// Compressed sparse matrix resident on the GPU, CSR or CSC.  Copies share the
 /// immutable device matrix.
@@ -109,6 +118,28 @@ public:
     const std::vector<index_t>& idx() const { return exported().idx; }
     const std::vector<double>& val() const { return exported().val; }
 
+    /// Stored entries in storage order (row-major for CSR, column-major for
+    /// CSC), from the exported storage (inc/sparse.hpp:133-149).
+    std::vector<Entry> entries() const {
+        const HostCopy& hc = exported();
+        std::vector<Entry> out;
+        out.reserve(static_cast<std::size_t>(nnz_));
+        const bool csr = layout_ == Layout::CSR;
+        for (index_t maj = 0; maj < major_dim(); ++maj)
+            for (index_t e = hc.ptr[static_cast<std::size_t>(maj)]; e < hc.ptr[static_cast<std::size_t>(maj) + 1]; ++e) {
+                const index_t mn = hc.idx[static_cast<std::size_t>(e)];
+                out.push_back(Entry{csr ? maj : mn, csr ? mn : maj, hc.val[static_cast<std::size_t>(e)]});
+            }
+        return out;
+    }
+
+    /// Row-major dense expansion (inc/sparse.hpp:152-158).
+    std::vector<double> to_dense() const {
+        std::vector<double> d(static_cast<std::size_t>(rows_ * cols_), 0.0);
+        for (const Entry& e : entries()) d[static_cast<std::size_t>(e.row * cols_ + e.col)] = e.value;
+        return d;
+    }
+
     /// The C-ABI handle (nullptr for a default-constructed matrix).
     spconv_csr* handle() const { return dev_ ? dev_->h : nullptr; }
 
@@ -159,6 +190,15 @@ inline DenseVector spmv(const SparseMatrix& m, std::span<const double> x, int th
 
 inline DenseVector spmv(const SparseMatrix& m, const DenseVector& x, int threads = 0) {
     return spmv(m, std::span<const double>(x), threads);
+}
+
+/// read_sparse (inc/sparse.hpp:409-432): values narrowed to fp32 on upload.
+inline SparseMatrix read_sparse(std::istream& is, Layout layout = Layout::CSR) {
+    std::string text((std::istreambuf_iterator<char>(is)), std::istreambuf_iterator<char>());
+    spconv_csr* h = nullptr;
+    detail::check(spconv_sparse_read(text.data(), static_cast<int64_t>(text.size()), layout == Layout::CSR ? 0 : 1,
+                                     detail::default_device(), nullptr, &h));
+    return SparseMatrix(h);
 }
 
 /// write_sparse (inc/sparse.hpp:400-406), rendered on the GPU.

@@ -217,6 +217,11 @@ int spconv_time_apply(int method, const spconv_csr* h, int64_t batch, int64_t m,
 int spconv_run_verification(int64_t max_dim, int seeds, uint64_t base_seed, int device, int64_t counts[4],
                             double devs[3], char* failures, int64_t cap);
 
+/* read_sparse(is, layout) (inc/sparse.hpp:409-432): the coordinate text alone
+ * (no transform header) into a generic matrix in `layout` (0 csr, 1 csc);
+ * same checks and messages as spconv_transform_read. */
+int spconv_sparse_read(const char* text, int64_t len, int layout, int device, void* stream, spconv_csr** out);
+
 /* Name of the kernel(s) the last spconv_spmv / spconv_spmm /
  * spconv_convolve_host call on this handle launched (diagnostics; "" before
  * the first call).  The string is static. */

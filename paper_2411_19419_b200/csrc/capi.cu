@@ -583,6 +583,56 @@ void transpose_host(int64_t major, int64_t minor, const I* ptr, const I* idx, co
         }
 }
 
+
+// read_sparse (inc/sparse.hpp:409-432) of the text at R: same header, dims and
+// entry checks and messages, compile()'s duplicate rejection in the (major,
+// minor) order of the requested layout; returns the row-major arrays.
+int parse_sparse(TokenReader& R, bool csc, int64_t& rows, int64_t& cols, std::vector<int64_t>& ptr,
+                 std::vector<int64_t>& idx, std::vector<double>& val) {
+    std::string header(R.line());
+    if (!header.empty() && header.back() == '\r') header.pop_back();
+    if (header != "%%sparse coordinate real")
+        return fail(SPCONV_ERUNTIME, "read_sparse: bad header line '" + header + "'");
+    int64_t nnz;
+    if (!R.i64(rows) || !R.i64(cols) || !R.i64(nnz) || rows < 1 || cols < 1 || nnz < 0)
+        return fail(SPCONV_ERUNTIME, "read_sparse: bad 'rows cols nnz' line");
+    struct Trip {
+        int64_t r, c;
+        double v;
+    };
+    std::vector<Trip> t;
+    t.reserve((size_t)nnz);
+    for (int64_t i = 0; i < nnz; ++i) {
+        int64_t r, c;
+        double v;
+        if (!R.i64(r) || !R.i64(c) || !R.f64(v))
+            return fail(SPCONV_ERUNTIME, "read_sparse: expected " + std::to_string(nnz) + " entries, got " +
+                                             std::to_string(i));
+        if (r - 1 < 0 || r - 1 >= rows || c - 1 < 0 || c - 1 >= cols)
+            return fail(SPCONV_EINVAL, "Triplets: entry (" + std::to_string(r - 1) + ", " + std::to_string(c - 1) +
+                                           ") outside " + std::to_string(rows) + "x" + std::to_string(cols));
+        t.push_back({r - 1, c - 1, v});
+    }
+    auto by_row = [](const Trip& a, const Trip& b) { return a.r != b.r ? a.r < b.r : a.c < b.c; };
+    auto by_col = [](const Trip& a, const Trip& b) { return a.c != b.c ? a.c < b.c : a.r < b.r; };
+    if (csc) std::sort(t.begin(), t.end(), by_col);
+    else std::sort(t.begin(), t.end(), by_row);
+    for (size_t i = 1; i < t.size(); ++i)
+        if (t[i].r == t[i - 1].r && t[i].c == t[i - 1].c)
+            return fail(SPCONV_EINVAL, "SparseMatrix: duplicate entry at (" + std::to_string(t[i].r) + ", " +
+                                           std::to_string(t[i].c) + ")");
+    if (csc) std::sort(t.begin(), t.end(), by_row);  // the row-major arrays want (row, col) order
+    ptr.assign((size_t)rows + 1, 0);
+    idx.resize(t.size());
+    val.resize(t.size());
+    for (size_t i = 0; i < t.size(); ++i) {
+        ptr[(size_t)t[i].r + 1]++;
+        idx[i] = t[i].c;
+        val[i] = t[i].v;
+    }
+    for (int64_t r = 0; r < rows; ++r) ptr[(size_t)r + 1] += ptr[(size_t)r];
+    return SPCONV_OK;
+}
 }  // namespace
 
 int spb_fail(int code, const std::string& msg) { return fail(code, msg); }
@@ -1152,6 +1202,23 @@ int spconv_csr_write_text(const spconv_csr* h, int transform_header_line, char* 
     return SPCONV_OK;
 }
 
+int spconv_sparse_read(const char* text, int64_t len, int layout, int device, void* stream, spconv_csr** out) {
+    if (!text || !out || len < 0) return fail(SPCONV_EINVAL, "spconv_sparse_read: null argument");
+    if (layout != 0 && layout != 1) return fail(SPCONV_EINVAL, "spconv_sparse_read: layout must be 0 (csr) or 1 (csc)");
+    *out = nullptr;
+    TokenReader R{text, text + len};
+    int64_t rows, cols;
+    std::vector<int64_t> ptr, idx;
+    std::vector<double> val;
+    if (int rc = parse_sparse(R, layout == 1, rows, cols, ptr, idx, val)) return rc;
+    if (layout == 0) return spconv_csr_from_host(rows, cols, ptr.data(), idx.data(), val.data(), device, stream, out);
+    std::vector<int32_t> cp, ci;
+    std::vector<double> cv;
+    transpose_host(rows, cols, ptr.data(), idx.data(), val.data(), cp, ci, cv);
+    std::vector<int64_t> cp64(cp.begin(), cp.end()), ci64(ci.begin(), ci.end());
+    return spconv_matrix_from_host(rows, cols, 1, cp64.data(), ci64.data(), cv.data(), device, stream, out);
+}
+
 int spconv_transform_read(const char* text, int64_t len, int device, void* stream, spconv_csr** out) {
     if (!text || !out || len < 0) return fail(SPCONV_EINVAL, "spconv_transform_read: null argument");
     *out = nullptr;
@@ -1167,57 +1234,17 @@ int spconv_transform_read(const char* text, int64_t len, int device, void* strea
     const std::string layout(lay);
     if (layout != "csr" && layout != "CSR" && layout != "csc" && layout != "CSC")
         return fail(SPCONV_EINVAL, "unknown layout '" + layout + "' (expected csr or csc)");
-    // read_sparse (inc/sparse.hpp:412-432)
-    std::string header(R.line());
-    if (!header.empty() && header.back() == '\r') header.pop_back();
-    if (header != "%%sparse coordinate real")
-        return fail(SPCONV_ERUNTIME, "read_sparse: bad header line '" + header + "'");
-    int64_t rows, cols, nnz;
-    if (!R.i64(rows) || !R.i64(cols) || !R.i64(nnz) || rows < 1 || cols < 1 || nnz < 0)
-        return fail(SPCONV_ERUNTIME, "read_sparse: bad 'rows cols nnz' line");
-    struct Trip {
-        int64_t r, c;
-        double v;
-    };
-    std::vector<Trip> t;
-    t.reserve((size_t)nnz);
-    for (int64_t i = 0; i < nnz; ++i) {
-        int64_t r, c;
-        double v;
-        if (!R.i64(r) || !R.i64(c) || !R.f64(v))
-            return fail(SPCONV_ERUNTIME, "read_sparse: expected " + std::to_string(nnz) + " entries, got " +
-                                             std::to_string(i));
-        if (r - 1 < 0 || r - 1 >= rows || c - 1 < 0 || c - 1 >= cols)
-            return fail(SPCONV_EINVAL, "Triplets: entry (" + std::to_string(r - 1) + ", " + std::to_string(c - 1) +
-                                           ") outside " + std::to_string(rows) + "x" + std::to_string(cols));
-        t.push_back({r - 1, c - 1, v});
-    }
     const bool csc = layout == "csc" || layout == "CSC";
-    // compile()'s order (inc/sparse.hpp:93-97): the first duplicate reported is
-    // the first in (major, minor) order of the requested layout
-    if (csc)
-        std::sort(t.begin(), t.end(), [](const Trip& a, const Trip& b) { return a.c != b.c ? a.c < b.c : a.r < b.r; });
-    else
-        std::sort(t.begin(), t.end(), [](const Trip& a, const Trip& b) { return a.r != b.r ? a.r < b.r : a.c < b.c; });
-    for (size_t i = 1; i < t.size(); ++i)
-        if (t[i].r == t[i - 1].r && t[i].c == t[i - 1].c)
-            return fail(SPCONV_EINVAL, "SparseMatrix: duplicate entry at (" + std::to_string(t[i].r) + ", " +
-                                           std::to_string(t[i].c) + ")");
+    int64_t rows, cols;
+    std::vector<int64_t> ptr, idx;
+    std::vector<double> val;
+    if (int rc = parse_sparse(R, csc, rows, cols, ptr, idx, val)) return rc;
+    const int64_t nnz = (int64_t)val.size();
     const Geom g = make_geom(m, n, k, s, p);
     if (rows != g.mo * g.no || cols != m * n)
         return fail(SPCONV_ERUNTIME, "read_transform: matrix is " + std::to_string(rows) + "x" + std::to_string(cols) +
                                          " but spec " + spec_str(m, n, k, s, p) + " requires " +
                                          std::to_string(g.mo * g.no) + "x" + std::to_string(m * n));
-    if (csc)  // the row-major arrays below want (row, col) order
-        std::sort(t.begin(), t.end(), [](const Trip& a, const Trip& b) { return a.r != b.r ? a.r < b.r : a.c < b.c; });
-    std::vector<int64_t> ptr((size_t)rows + 1, 0), idx(t.size());
-    std::vector<double> val(t.size());
-    for (size_t i = 0; i < t.size(); ++i) {
-        ptr[(size_t)t[i].r + 1]++;
-        idx[i] = t[i].c;
-        val[i] = t[i].v;
-    }
-    for (int64_t r = 0; r < rows; ++r) ptr[(size_t)r + 1] += ptr[(size_t)r];
     // If the matrix IS the conv transform of its own taps (the taps of the
     // first row that stores all k*k of them), rebuild it on the device and
     // keep the built handle: identical arrays, plus the geometry the band

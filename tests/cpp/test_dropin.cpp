@@ -137,6 +137,23 @@ int main() {
         CHECK(spmv(g, Grid(3, 3, 1.0).values) == (std::vector<double>{4, 6, 4, 6, 9, 6, 4, 6, 4}));
         CHECK(relayout(g, Layout::CSR).ptr() == tr.matrix.ptr());
     }
+    // entries / to_dense / read_sparse / flipped (inc/sparse.hpp, inc/conv.hpp)
+    {
+        const Transform t = build_transform(Kernel(2, {1, 2, 3, 4}), ConvSpec(3, 3, 2, 1, 0));
+        const std::vector<Entry> es = t.matrix.entries();
+        CHECK(es.size() == 16 && es[0].row == 0 && es[0].col == 0 && es[0].value == 1.0 && es[3].col == 4);
+        const std::vector<double> d = t.matrix.to_dense();
+        CHECK(d.size() == 4 * 9 && d[0 * 9 + 4] == 4.0 && d[3 * 9 + 8] == 4.0 && d[3 * 9 + 0] == 0.0);
+        std::ostringstream os;
+        write_sparse(os, t.matrix);
+        std::istringstream is(os.str());
+        const SparseMatrix r = read_sparse(is, Layout::CSC);
+        CHECK(r.layout() == Layout::CSC && r.to_dense() == d);
+        const Kernel f = flipped(Kernel(2, {1, 2, 3, 4}));
+        CHECK((f.values == std::vector<double>{4, 3, 2, 1}));
+        std::istringstream bad("%%sparse coordinate real\n2 2 1\n3 1 1.0\n");
+        expect_throw<std::invalid_argument>([&] { read_sparse(bad); }, "Triplets: entry (2, 0) outside 2x2");
+    }
     expect_throw<std::invalid_argument>([] { layout_from_name("coo"); },
                                         "unknown layout 'coo' (expected csr or csc)");
     // The seeded generator (inc/rng.hpp): known answers.
