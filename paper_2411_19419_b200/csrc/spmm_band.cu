@@ -1,5 +1,6 @@
 // spmm_band.cu -- the hot path: SpMM of the conv transform T against an
-// image-major batch, as two kernels per call.
+// image-major batch, as two launches per call (check + apply, or the fused
+// check-and-apply + its fixup pass; see 3. below).
 //
 // Contract (shared with spmm.cu): for every row of T,
 //     acc = +0.0f; for e in row (column-ascending): acc = fmaf(val[e], x[col[e]], acc)
@@ -13,9 +14,10 @@
 //    handle's k x k taps: row (x, y) holds the taps (j, i) whose input pixel
 //    (s x + j - p, s y + i - p) lies inside the image, at column
 //    (s x + j - p) n + (s y + i - p), in (j, i) order, with value w[j][i].
-//    An interior segment (every row full) is one contiguous run of TW*k*k
-//    (col, val) pairs: a warp streams it with coalesced loads and compares
-//    against the closed-form pattern.  Border segments are walked row by row.
+//    A segment's rows are one contiguous run whose start and length are
+//    closed-form: one warp per segment bulk-copies row_ptr and the run into
+//    shared memory (no dependent load) and checks every row there -- interior
+//    rows with an unrolled k*k compare, clipped rows over their tap range.
 //    Result: one byte per segment (seg_ok).
 //
 // 2. conv_spmm_band -- register-blocked apply.  A CTA tile is TH output rows x
@@ -33,6 +35,13 @@
 //    halos shared by neighbouring tiles are L2 hits.  A warp whose rows all lie
 //    in verified segments (and whose taps are finite and non-zero) takes the
 //    blocked path; otherwise it runs the per-entry loop straight from the CSR.
+//
+// 3. Fused form (FUSED = true): the producer warp of each persistent CTA also
+//    checks segments (same device functions as 1.) between its window loads;
+//    the consumers take the blocked path unconditionally and conv_band_fixup
+//    (a programmatic dependent) recomputes, from the CSR, the rows of any
+//    segment that failed.  Used when the matrix is a small part of the call's
+//    bytes; the host (capi.cu run_spmm) picks the form.
 //
 //    Blocked == per-entry, bit for bit: a tap that lands in the zero padding
 //    executes fmaf(w, +0.0f, acc), which returns acc unchanged (acc starts at
