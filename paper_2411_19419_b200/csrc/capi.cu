@@ -2,9 +2,12 @@
 //
 // Host-side orchestration only: argument validation with the reference's
 // exception messages, the O(k^2 + m_out + n_out) host tables of the closed-form
-// CSR build, kernel-path selection, and the chunked host<->device pipeline of
-// spconv_convolve_host.  All arithmetic on T and on images happens in the CUDA
-// kernels of csr_build.cu / spmm.cu; there is no CPU fallback.
+// CSR build, kernel-path selection (run_spmm), the chunked host<->device
+// pipeline of spconv_convolve_host, and the text parsing of read_transform /
+// read_sparse.  All arithmetic on T and on images happens in the CUDA kernels
+// of csr_build.cu, csc_build.cu, spmm.cu, spmm_band.cu, text_io.cu and
+// verify.cu; there is no CPU fallback.  (Matrices that arrive from the host --
+// uploads and non-conv text files -- are transposed on the host for relayout.)
 #include <cudaTypedefs.h>
 
 #include <algorithm>
