@@ -388,9 +388,12 @@ def test_band_path_is_default(sp, orc, torch_cuda, spec):
     assert np.all(Yh[:, t.rows] == -7.0)  # nothing written past the row
 
 
-def test_band_concurrent_streams(sp, orc, torch_cuda):
+@pytest.mark.parametrize("fused", ["0", "1"])
+def test_band_concurrent_streams(sp, orc, torch_cuda, fused, monkeypatch):
     """One immutable handle applied on two streams at once (the band check's
-    per-segment bytes are rewritten with identical values: benign)."""
+    per-segment bytes are rewritten with identical values: benign), with the
+    check kernel and with the fused check-and-apply."""
+    monkeypatch.setenv("SPCONV_B200_FUSED", fused)
     spec = (256, 256, 3, 1, 1)
     kern, X = problem(orc, 12, 256, 256, 3, batch=16)
     t = build(sp, spec, kern)
