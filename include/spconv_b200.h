@@ -135,9 +135,18 @@ int spconv_spmm(const spconv_csr* h, const float* X_dev, int64_t ldx, float* Y_d
  * PCIe overlap. */
 int spconv_convolve_host(const spconv_csr* h, const float* X_host, float* Y_host, int64_t batch);
 
-/* Same with fp64 host buffers (the reference Grid/DenseVector types,
- * inc/grid.hpp:18-24): narrowed to fp32 on the way in, widened on the way
- * out.  Used by the drop-in convolve()/spmv() wrappers. */
+/* fp64 SpMM on device buffers with the reference's own arithmetic: per row
+ * acc = 0.0; acc = acc + (double)val * x[col] over the stored entries in
+ * order, one rounded multiply and one rounded add each (inc/sparse.hpp:185-191
+ * as its Release build evaluates it).  Bit-identical to the reference's
+ * spmv() whenever the stored values equal the reference's, i.e. for
+ * fp32-representable taps. */
+int spconv_spmm_f64(const spconv_csr* h, const double* X_dev, int64_t ldx, double* Y_dev, int64_t ldy,
+                    int64_t batch, void* stream);
+
+/* The reference-semantics apply on fp64 HOST buffers (the reference
+ * Grid/DenseVector types, inc/grid.hpp:18-24), used by the drop-in
+ * convolve()/spmv(): fp64 in, spconv_spmm_f64 on the device, fp64 out. */
 int spconv_convolve_host_f64(const spconv_csr* h, const double* X_host, double* Y_host,
                              int64_t batch);
 

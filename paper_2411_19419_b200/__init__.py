@@ -22,7 +22,7 @@ import numpy as np
 
 __all__ = [
     "ConvSpec", "Kernel", "Transform", "build_transform", "convolve", "convolve_batch",
-    "spmv", "spmm", "nnz_bound", "read_transform", "relayout", "Layout", "layout_name",
+    "spmv", "spmm", "spmm_f64", "nnz_bound", "read_transform", "relayout", "Layout", "layout_name",
     "layout_from_name", "direct_conv", "im2col_conv", "run_verification", "library_path", "lib",
 ]
 
@@ -63,6 +63,7 @@ _decl("spconv_spmv", [_vp, _vp, _vp, _vp])
 _decl("spconv_spmm", [_vp, _vp, _i64, _vp, _i64, _i64, _vp])
 _decl("spconv_convolve_host", [_vp, _vp, _vp, _i64])
 _decl("spconv_convolve_host_f64", [_vp, _vp, _vp, _i64])
+_decl("spconv_spmm_f64", [_vp, _vp, _i64, _vp, _i64, _i64, _vp])
 _decl("spconv_csr_last_kernel", [_vp], C.c_char_p)
 _decl("spconv_csr_write_text", [_vp, C.c_int, _vp, _i64, _P(_i64)])
 _decl("spconv_transform_read", [_vp, _i64, C.c_int, _vp, _P(_vp)])
@@ -350,9 +351,26 @@ def convolve_batch(t: Transform, X_host, Y_host=None):
     return Y_host
 
 
+def spmm_f64(t: Transform, X, Y=None, stream=None):
+    """Y[b] = T X[b] in fp64 with the reference's arithmetic (spconv_spmm_f64):
+    X [batch, cols] CUDA float64; bit-identical to the reference's spmv() for
+    fp32-representable taps."""
+    import torch
+    if not (isinstance(X, torch.Tensor) and X.is_cuda and X.dtype == torch.float64):
+        raise ValueError("spmm_f64: expected a CUDA float64 tensor")
+    if X.dim() != 2 or X.shape[1] != t.cols or X.stride(1) != 1:
+        raise ValueError(f"spmm_f64: expected X of shape [batch, {t.cols}] with unit column stride")
+    if Y is None:
+        Y = torch.empty(X.shape[0], t.rows, dtype=torch.float64, device=X.device)
+    _check(lib.spconv_spmm_f64(t._h, X.data_ptr(), X.stride(0), Y.data_ptr(), Y.stride(0), X.shape[0],
+                               _stream_handle(stream)))
+    return Y
+
+
 def convolve(t: Transform, a) -> np.ndarray:
     """Reference-semantics apply of one m x n grid (inc/conv.hpp:207-215):
-    fp64 in, fp64 out (fp32 device arithmetic in between)."""
+    fp64 in, fp64 device arithmetic with the reference's rounding, fp64 out --
+    bit-identical to the reference for fp32-representable taps."""
     a = np.asarray(a, dtype=np.float64)
     if t.spec is None:
         raise ValueError("convolve: transform has no geometry (generic CSR)")

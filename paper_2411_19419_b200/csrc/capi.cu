@@ -1141,16 +1141,56 @@ int spconv_convolve_host(const spconv_csr* hc, const float* X_host, float* Y_hos
     return SPCONV_OK;
 }
 
-int spconv_convolve_host_f64(const spconv_csr* h, const double* X_host, double* Y_host,
+int spconv_spmm_f64(const spconv_csr* h, const double* X_dev, int64_t ldx, double* Y_dev, int64_t ldy,
+                    int64_t batch, void* stream) {
+    if (!h) return fail(SPCONV_EINVAL, "spconv_spmm_f64: null handle");
+    if (batch < 0) return fail(SPCONV_EINVAL, "spconv_spmm_f64: negative batch");
+    if (batch == 0) return SPCONV_OK;
+    if (!X_dev || !Y_dev) return fail(SPCONV_EINVAL, "spconv_spmm_f64: null buffer");
+    if (batch > INT32_MAX) return fail(SPCONV_EINVAL, "spconv_spmm_f64: batch exceeds int32");
+    if (ldx < h->cols || ldy < h->rows)
+        return fail(SPCONV_EINVAL, "spconv_spmm_f64: leading dimension smaller than the matrix");
+    const char* xa = reinterpret_cast<const char*>(X_dev);
+    const char* ya = reinterpret_cast<const char*>(Y_dev);
+    if (xa < ya + 8 * ((batch - 1) * ldy + h->rows) && ya < xa + 8 * ((batch - 1) * ldx + h->cols))
+        return fail(SPCONV_EINVAL, "spconv_spmm_f64: X and Y overlap");
+    DeviceGuard dg(h->device);
+    if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
+    spb::F64Params fp{h->row_ptr, h->col_idx, h->vals, X_dev, ldx, Y_dev, ldy, (int)h->rows, (int)batch};
+    CK(spb::launch_spmm_f64(fp, static_cast<cudaStream_t>(stream)));
+    const_cast<spconv_csr*>(h)->last_kernel.store("csr_spmm_f64");
+    return SPCONV_OK;
+}
+
+int spconv_convolve_host_f64(const spconv_csr* hc, const double* X_host, double* Y_host,
                              int64_t batch) {
-    if (!h) return fail(SPCONV_EINVAL, "spconv_convolve_host_f64: null handle");
+    if (!hc) return fail(SPCONV_EINVAL, "spconv_convolve_host_f64: null handle");
     if (batch < 0) return fail(SPCONV_EINVAL, "spconv_convolve_host_f64: negative batch");
     if (batch == 0) return SPCONV_OK;
     if (!X_host || !Y_host) return fail(SPCONV_EINVAL, "spconv_convolve_host_f64: null buffer");
-    std::vector<float> xf((size_t)(batch * h->cols)), yf((size_t)(batch * h->rows));
-    for (size_t i = 0; i < xf.size(); ++i) xf[i] = (float)X_host[i];
-    if (int rc = spconv_convolve_host(h, xf.data(), yf.data(), batch)) return rc;
-    for (size_t i = 0; i < yf.size(); ++i) Y_host[i] = yf[i];
+    // The reference-semantics path (the drop-in convolve / spmv): fp64 in,
+    // fp64 arithmetic on the device (csr_spmm_f64), fp64 out.
+    auto* h = const_cast<spconv_csr*>(hc);
+    std::lock_guard<std::mutex> lk(h->ws_mu);
+    DeviceGuard dg(h->device);
+    if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
+    keep_pool_memory(h->device);
+    if (!h->ws_stream[1]) CK(cudaStreamCreateWithFlags(&h->ws_stream[1], cudaStreamNonBlocking));
+    cudaStream_t st = h->ws_stream[1];
+    const size_t xb = (size_t)(batch * h->cols) * 8, yb = (size_t)(batch * h->rows) * 8;
+    char* buf = nullptr;
+    CK(cudaMallocAsync(&buf, xb + yb, st));
+    cudaError_t e = cudaMemcpyAsync(buf, X_host, xb, cudaMemcpyHostToDevice, st);
+    int rc = SPCONV_OK;
+    if (e == cudaSuccess)
+        rc = spconv_spmm_f64(h, reinterpret_cast<const double*>(buf), h->cols, reinterpret_cast<double*>(buf + xb),
+                             h->rows, batch, st);
+    if (e == cudaSuccess && rc == SPCONV_OK) e = cudaMemcpyAsync(Y_host, buf + xb, yb, cudaMemcpyDeviceToHost, st);
+    cudaFreeAsync(buf, st);
+    const cudaError_t es = cudaStreamSynchronize(st);
+    if (rc != SPCONV_OK) return rc;
+    if (e == cudaSuccess) e = es;
+    if (e != cudaSuccess) return cuda_fail(e, "spconv_convolve_host_f64");
     return SPCONV_OK;
 }
 

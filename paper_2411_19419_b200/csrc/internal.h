@@ -139,6 +139,17 @@ cudaError_t launch_csc_build(CscParams cp, int maxc, bool dense, cudaStream_t st
 cudaError_t launch_tiled(const TiledParams& tp, const CUtensorMap* tmap, int bt, size_t smem,
                          cudaStream_t st);
 cudaError_t launch_generic(const GenericParams& gp, cudaStream_t st);
+struct F64Params {
+    const int32_t* row_ptr;
+    const int32_t* col_idx;
+    const float* vals;
+    const double* X;
+    int64_t ldx;
+    double* Y;
+    int64_t ldy;
+    int rows, batch;
+};
+cudaError_t launch_spmm_f64(const F64Params& fp, cudaStream_t st);
 cudaError_t launch_spmv_unrolled(const GenericParams& gp, int kmax, cudaStream_t st);
 cudaError_t launch_spmv_warp(const SpecParams& sp, int kmax, bool spec, cudaStream_t st);
 

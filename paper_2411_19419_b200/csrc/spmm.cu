@@ -145,6 +145,31 @@ __global__ void __launch_bounds__(256) conv_spmm_tiled(const __grid_constant__ C
     }
 }
 
+// fp64 SpMM with the reference's own arithmetic: per row acc = 0.0; for each
+// stored entry in order acc = acc + (double)val * x (one rounded multiply, one
+// rounded add -- no contraction, as the reference's Release build evaluates
+// inc/sparse.hpp:185-191).  With fp32-representable taps the stored values are
+// the reference's exactly, so the output is bit-identical to its spmv().
+__global__ void __launch_bounds__(256) csr_spmm_f64(const F64Params P) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= P.rows) return;
+    const int e0 = __ldg(P.row_ptr + r), e1 = __ldg(P.row_ptr + r + 1);
+    for (int b = blockIdx.y; b < P.batch; b += gridDim.y) {
+        const double* x = P.X + (int64_t)b * P.ldx;
+        double acc = 0.0;
+        for (int e = e0; e < e1; ++e)
+            acc = __dadd_rn(acc, __dmul_rn((double)__ldg(P.vals + e), __ldg(x + __ldg(P.col_idx + e))));
+        P.Y[(int64_t)b * P.ldy + r] = acc;
+    }
+}
+
+cudaError_t launch_spmm_f64(const F64Params& fp, cudaStream_t st) {
+    const int gx = (fp.rows + 255) / 256;
+    const int gy = fp.batch < 65535 ? fp.batch : 65535;
+    csr_spmm_f64<<<dim3(gx, gy), 256, 0, st>>>(fp);
+    return cudaGetLastError();
+}
+
 __global__ void __launch_bounds__(256) csr_spmm_generic(const GenericParams P) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= P.rows) return;

@@ -336,14 +336,15 @@ def test_end_to_end_host_path(sp, orc, torch_cuda):
 
 
 def test_reference_semantics_convolve(sp, orc, golden):
-    """The fp64-in/fp64-out convolve() mirror: output within tolerance of the
-    reference's convolve() on config 1."""
+    """The fp64-in/fp64-out convolve() mirror computes in fp64 with the
+    reference's rounding: BIT-identical to the reference's convolve() on
+    config 1 (fp32-representable taps)."""
     _, npz = golden
     t = build(sp, CONFIGS[0], npz["c1_kernel"])
     out = sp.convolve(t, npz["c1_image"].reshape(64, 64))
-    cond = orc.spmv_abs(npz["c1_ptr"], npz["c1_idx"], npz["c1_val"], npz["c1_image"])
     assert out.shape == (64, 64)
-    assert np.all(np.abs(out.reshape(-1) - npz["c1_y"]) <= TOL * cond)
+    assert np.array_equal(out.reshape(-1).view(np.uint64), npz["c1_y"].view(np.uint64))
+    assert t.last_kernel == "csr_spmm_f64"
     with pytest.raises(ValueError, match=r"^convolve: input is 3x64 but transform expects \(m=64"):
         sp.convolve(t, np.zeros((3, 64)))
 
@@ -603,3 +604,26 @@ def test_band_fused_and_two_kernel(sp, orc, torch_cuda, spec, fused, monkeypatch
     Y = run_spmm(torch_cuda, sp, t, X)
     assert t.last_kernel == BAND_KERNELS[int(fused)]
     assert np.array_equal(bits(Y), bits(orc.spmm_native(*orc.build_native(*spec, kern), X)))
+
+
+def test_fp64_path_bitexact_vs_reference_digests(sp, orc, golden, torch_cuda):
+    """The fp64 device SpMV (reference arithmetic) reproduces the reference's
+    own fp64 convolve() output BIT FOR BIT for config 2 and all 36 config-5
+    edge specs, normal and zero-tap kernels (golden SHA-256 digests), and
+    the CSC handle gives the same bits."""
+    js, _ = golden
+    for key, spec, kern, img in golden_cases(orc, js):
+        m, n = spec[:2]
+        t = build(sp, spec, kern)
+        y = sp.convolve(t, img.reshape(m, n)).reshape(-1)
+        assert sha(y) == js["digests"][key]["y"], key
+        X = torch_cuda.from_numpy(np.stack([img, img[::-1].copy()])).cuda()
+        Y = sp.spmm_f64(t, X).cpu().numpy()
+        assert sha(Y[0]) == js["digests"][key]["y"], key
+        ptr, idx, val = orc.build_transform(*spec, kern)
+        assert np.array_equal(Y[1].view(np.uint64), orc.spmv_f64(ptr, idx, val, img[::-1].copy()).view(np.uint64))
+    tc = sp.build_transform(sp.Kernel(5, kern if spec[2] == 5 else np.ones(25)), sp.ConvSpec(40, 36, 5, 2, 2),
+                            layout=sp.Layout.CSC)
+    tr = sp.relayout(tc, sp.Layout.CSR)
+    a = np.linspace(-1, 1, 40 * 36).reshape(40, 36)
+    assert np.array_equal(sp.convolve(tc, a).view(np.uint64), sp.convolve(tr, a).view(np.uint64))
