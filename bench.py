@@ -310,13 +310,17 @@ def device_steps(sp, torch, t, b, steps, warmup, dev, stream, seed):
     return X, Y, ms, l2
 
 
-def secondary(sp, torch, dev, stream, steps):
-    """N=1 extras: config 2 (single-image SpMV, cold L2) and config 4 at its
-    per-GPU batch (8 images) -- kernel time, roofline fraction and build."""
+def secondary(sp, torch, dev, stream, steps, world=1):
+    """Extras: config 4 at its per-GPU batch (8 images; at N GPUs the job is
+    BASELINE's 'batch 64 over 8 B200' when N = 8: every rank times its own
+    slice, max over ranks) and, at N = 1 only, config 2 (single-image SpMV,
+    cold and warm L2) and config 3 in CSC layout -- kernel time, roofline
+    fraction and build."""
+    from paper_2411_19419_b200.shard import max_over_ranks
     out = {}
     peak, _ = peaks()
     rng = np.random.default_rng(99)
-    for c in (2, 4):
+    for c in ((2, 4) if world == 1 else (4,)):
         cfg = CONFIGS[c]
         m, n, k, s, p = cfg["spec"]
         b = cfg["per_gpu_batch"]
@@ -325,12 +329,14 @@ def secondary(sp, torch, dev, stream, steps):
         t, bld_ms, _ = timed_build(sp, torch, kern, spec, dev, stream)
         X, Y, ms, l2 = device_steps(sp, torch, t, b, steps, 3, dev, stream, 7)
         alg = algorithmic_bytes(t.rows, t.cols, t.nnz, b)
-        mean = statistics.mean(ms)
+        mean = max_over_ranks(sum(ms), dev) / len(ms)  # max over ranks (identity at N = 1)
+        bld_ms = max_over_ranks(bld_ms, dev)
         bb = 8 * t.nnz + 4 * (t.rows + 1)
         out[f"config{c}"] = {
-            "workload": cfg["name"], "batch": b, "kernel": t.last_kernel, "ms_per_step": mean,
-            "ms_min": min(ms), "value": b * t.nnz / (mean * 1e-3) / 1e9, "unit": UNIT,
-            "gb_per_s": alg / (mean * 1e-3) / 1e9, "frac": alg / (mean * 1e-3) / 1e9 / peak,
+            "workload": cfg["name"], "batch": b, "n_gpus": world, "global_batch": b * world,
+            "kernel": t.last_kernel, "ms_per_step": mean,
+            "ms_min": min(ms), "value": world * b * t.nnz / (mean * 1e-3) / 1e9, "unit": UNIT,
+            "gb_per_s": alg / (mean * 1e-3) / 1e9, "frac": alg / (mean * 1e-3) / 1e9 / peak,  # per GPU
             "l2": l2, "build_ms_device": bld_ms, "build_frac": bb / (bld_ms * 1e-3) / 1e9 / peak,
         }
         if c == 2:
@@ -367,6 +373,8 @@ def secondary(sp, torch, dev, stream, steps):
             del Xw, Yw
         del X, Y
         t.close()
+    if world > 1:
+        return out
     # config 3 in CSC layout: the CSC build (CSR arrays + column-major
     # storage) and the apply through the same kernels
     cfg = CONFIGS[3]
@@ -500,8 +508,8 @@ def run_ours(args, cfg):
     bld_bytes = 8 * nnz + 4 * (rows + 1)
 
     extra = None
-    if rank == 0 and world == 1 and not args.no_secondary:
-        extra = secondary(sp, torch, dev, stream, max(10, min(args.steps, 30)))
+    if not args.no_secondary:  # (collective timing at N > 1: every rank takes part)
+        extra = secondary(sp, torch, dev, stream, max(10, min(args.steps, 30)), world)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
