@@ -387,12 +387,12 @@ static cudaError_t launch_k(const BuildParams& bp, int block, size_t smem, cudaS
 
 cudaError_t launch_csr_build(const BuildParams& bp, bool dense, int block, size_t smem,
                              cudaStream_t st) {
-    // Warp-local build for k >= 7 (config 4: 349 -> 329 us); for small k the
-    // per-warp closed form costs more instructions than the block barriers it
-    // removes (config 3: 27.6 -> 31.7 us), so the block kernel stays
-    // (profiles/r01k/exp.txt).  SPCONV_B200_BUILD=block|warp overrides.
+    // The block kernel for every k: with TMA bulk stores and the unpredicated
+    // interior fill it beats the warp-local variant at config 4 too (254 vs
+    // 283 us; config 3 25.6 vs 27.7 us; profiles/r01_choices).
+    // SPCONV_B200_BUILD=warp selects the warp-local kernel.
     const char* bsel = std::getenv("SPCONV_B200_BUILD");
-    const bool warp_build = bsel ? !std::strcmp(bsel, "warp") : bp.k >= 7;
+    const bool warp_build = bsel && !std::strcmp(bsel, "warp");
     if (warp_build) {
         switch (bp.k) {
             case 1: return dense ? launch_w<1, true>(bp, st) : launch_w<1, false>(bp, st);
