@@ -150,7 +150,18 @@ __global__ void __launch_bounds__(256) csc_build_kernel(const CscParams P) {
         dval = P.vals;
         o = base + excl;
     }
-    if (c < P.cols && cnt > 0) {
+    if (KC && DENSE && S == 1 && cnt == KC * KC) {
+        // Interior column at stride 1 (every tap lands): the unrolled K x K
+        // pattern, x and y stepping with j and i descending.
+        const int x0 = a + P.p - (KC - 1), y0 = b + P.p - (KC - 1);
+#pragma unroll
+        for (int jj = 0; jj < KC; ++jj)
+#pragma unroll
+            for (int ii = 0; ii < KC; ++ii) {
+                drow[o + jj * KC + ii] = (x0 + jj) * P.no + y0 + ii;
+                dval[o + jj * KC + ii] = s_taps[(KC - 1 - jj) * KC + (KC - 1 - ii)];
+            }
+    } else if (c < P.cols && cnt > 0) {
         const int x0 = (a + P.p - jtop) / S, y0 = (b + P.p - itop) / S;  // exact: jtop == a+p (mod s)
         int xrow = x0 * P.no;
         for (int j = jtop; j > jlo; j -= S, xrow += P.no) {
