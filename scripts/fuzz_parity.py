@@ -1,0 +1,111 @@
+#!/usr/bin/env python
+"""Randomised GPU parity fuzzing (a long-running complement to tests/):
+random geometries (m, n up to 300, k up to 11, s up to 4, p up to k), dense /
+zero-tap / non-finite kernels, CSR and CSC layouts, batches 1-9 through the
+default path and every forced path, padded ldx, the fused and two-kernel band
+forms; every output compared BIT-EXACTLY with the oracle's ordered-fmaf
+restatement and every matrix with the oracle's build.
+
+    python scripts/fuzz_parity.py SECONDS [SEED] > report.txt
+"""
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_2411_19419_b200 as sp  # noqa: E402
+from oracle import Oracle  # noqa: E402
+
+PATHS = [None, "spmv", "spmv_plain", "banded", "tiled", "tiled_notma", "generic"]
+
+
+def bits(a):
+    a = np.ascontiguousarray(a, np.float32)
+    v = a.view(np.uint32).copy()
+    v[np.isnan(a)] = 0x7FC00000
+    return v
+
+
+def main():
+    secs = float(sys.argv[1])
+    seed = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+    rng = np.random.default_rng(seed)
+    orc = Oracle()
+    t_end = time.time() + secs
+    cases = fails = 0
+    while time.time() < t_end:
+        k = int(rng.choice([1, 2, 3, 3, 3, 5, 5, 7, 7, 11]))
+        s = int(rng.choice([1, 1, 2, 2, 3, 4]))
+        p = int(rng.integers(0, k + 1))
+        m = int(rng.integers(max(1, k - 2 * p), 300))
+        n = int(rng.choice([int(rng.integers(max(1, k - 2 * p), 300)), 4 * int(rng.integers(1, 70))]))
+        if orc.spec_check(m, n, k, s, p):
+            continue
+        kern = rng.standard_normal(k * k).astype(np.float32)
+        mode = rng.integers(0, 10)
+        if mode == 0:
+            kern[rng.random(k * k) < 0.3] = 0.0
+        elif mode == 1:
+            kern[rng.integers(0, k * k)] = np.nan
+        batch = int(rng.integers(1, 10))
+        X = rng.standard_normal((batch, m * n)).astype(np.float32)
+        if rng.random() < 0.1:
+            X[0, rng.integers(0, m * n)] = np.inf
+        layout = sp.Layout.CSC if rng.random() < 0.25 else sp.Layout.CSR
+        spec = sp.ConvSpec(m, n, k, s, p)
+        t = sp.build_transform(sp.Kernel(k, kern.astype(np.float64)), spec, layout=layout)
+        rp, ri, rv = orc.build_native(m, n, k, s, p, kern)
+        ptr = np.empty(t.rows + 1, np.int32)
+        idx = np.empty(max(t.nnz, 1), np.int32)
+        val = np.empty(max(t.nnz, 1), np.float32)
+        if layout == sp.Layout.CSR:
+            t.copy_native(ptr, idx, val)
+            ok = np.array_equal(ptr, rp) and np.array_equal(idx[:t.nnz], ri) and np.array_equal(
+                bits(val[:t.nnz]), bits(rv))
+        else:
+            cp, ci, cv = t.export()
+            p64, i64, v64 = orc.build_transform(m, n, k, s, p, kern.astype(np.float64))
+            wp, wi, wv = orc.transpose(t.rows, t.cols, p64, i64, v64)
+            ok = np.array_equal(cp, wp) and np.array_equal(ci, wi) and np.array_equal(bits(cv), bits(wv))
+        want = orc.spmm_native(rp, ri, rv, X)
+        pad = int(rng.choice([0, 0, 4]))
+        Xd = torch.zeros(batch, m * n + pad, device="cuda")
+        Xd[:, :m * n] = torch.from_numpy(X)
+        path = PATHS[int(rng.integers(0, len(PATHS)))] if rng.random() < 0.4 else None
+        env = {}
+        if path:
+            env["SPCONV_B200_PATH"] = path
+        if rng.random() < 0.3:
+            env["SPCONV_B200_FUSED"] = str(int(rng.integers(0, 2)))
+        if rng.random() < 0.2:
+            env["SPCONV_B200_CHECK"] = str(rng.choice(["side", "same"]))
+        for kk, vv in env.items():
+            os.environ[kk] = vv
+        try:
+            Y = sp.spmm(t, Xd[:, :m * n])
+            torch.cuda.synchronize()
+            got = Y.cpu().numpy()
+            ok_y = np.array_equal(bits(got), bits(want))
+        except (ValueError, RuntimeError) as e:  # a forced path may not support the geometry
+            ok_y = path is not None and ("unsupported" in str(e) or "longer than" in str(e))
+            if not ok_y:
+                print("ERROR", (m, n, k, s, p), batch, env, e)
+        finally:
+            for kk in env:
+                del os.environ[kk]
+        cases += 1
+        if not (ok and ok_y):
+            fails += 1
+            print("FAIL", (m, n, k, s, p), "mode", int(mode), "batch", batch, "layout", layout, "env", env,
+                  "matrix_ok", ok, "y_ok", ok_y, "kernel", t.last_kernel, flush=True)
+        t.close()
+    print(f"fuzz: {cases} cases, {fails} failures (seed {seed}, {secs:.0f} s)")
+    return 1 if fails else 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
