@@ -63,7 +63,13 @@ def ncu_traffic(cfg: int, batch: int):
     batch, from the newest committed ncu --set full capture (profiles/*/
     ncu_summary.json, written by scripts/make_profiles.py); None if absent."""
     import glob
-    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "ncu_summary.json")), reverse=True):
+    paths = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "ncu_summary.json")), reverse=True)
+    latest = os.path.join(ROOT, "profiles", "LATEST")  # tag of the newest evidence pass (make_profiles.py)
+    if os.path.exists(latest):
+        with open(latest) as f:
+            first = os.path.join(ROOT, "profiles", f.read().strip(), "ncu_summary.json")
+        paths = [first] + [q for q in paths if q != first]
+    for path in paths:
         try:
             with open(path) as f:
                 j = json.load(f)

@@ -99,6 +99,9 @@ def main():
             shutil.copy(p, os.path.join(dst, f))
     with open(os.path.join(dst, "ncu_summary.json"), "w") as o:
         json.dump(summary, o, indent=1)
+    if summary:  # bench.py reads roofline.traffic from the newest pass
+        with open(os.path.join(ROOT, "profiles", "LATEST"), "w") as o:
+            o.write(os.path.basename(dst.rstrip("/")) + "\n")
     print(json.dumps(summary, indent=1))
 
 
