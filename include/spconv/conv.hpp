@@ -96,8 +96,10 @@ struct Transform {
 
 enum class TransformRoute { Spgemm, ColumnGather };
 
-/// One-time on-device build of T (replaces inc/conv.hpp:179-204).  Kernel
-/// taps are narrowed to fp32; taps that are exactly zero are not stored.
+/// One-time on-device build of T (replaces inc/conv.hpp:179-204).  Entries
+/// are stored where the double tap is non-zero, with their exact double
+/// values (ptr/idx/val, write_transform and convolve match the reference bit
+/// for bit); the fp32 batch kernels apply the taps narrowed to fp32.
 inline Transform build_transform(const Kernel& kern, const ConvSpec& spec,
                                  Layout layout = Layout::CSR,
                                  TransformRoute route = TransformRoute::Spgemm) {
@@ -105,11 +107,10 @@ inline Transform build_transform(const Kernel& kern, const ConvSpec& spec,
     if (kern.k != spec.k)
         throw std::invalid_argument("build_conv_matrix: kernel side " + std::to_string(kern.k) +
                                     " does not match spec " + spec.str());
-    std::vector<float> taps(kern.values.begin(), kern.values.end());
     spconv_csr* h = nullptr;
-    detail::check(spconv_build_transform(spec.m, spec.n, spec.k, spec.s, spec.p, taps.data(),
-                                         layout == Layout::CSR ? 0 : 1, detail::default_device(),
-                                         nullptr, &h));
+    detail::check(spconv_build_transform_f64(spec.m, spec.n, spec.k, spec.s, spec.p, kern.values.data(),
+                                             layout == Layout::CSR ? 0 : 1, detail::default_device(),
+                                             nullptr, &h));
     return Transform{spec, SparseMatrix(h)};
 }
 
@@ -159,7 +160,7 @@ inline void write_transform(std::ostream& os, const Transform& t) {
     os.write(buf.data(), static_cast<std::streamsize>(len));
 }
 
-/// read_transform (inc/conv.hpp:226-244); values are narrowed to fp32.
+/// read_transform (inc/conv.hpp:226-244); values are kept exactly.
 inline Transform read_transform(std::istream& is) {
     std::string text((std::istreambuf_iterator<char>(is)), std::istreambuf_iterator<char>());
     spconv_csr* h = nullptr;

@@ -82,7 +82,7 @@ public:
         host_ = std::make_shared<HostCopy>();
     }
 
-    /// Uploads a host CSR (ptr/idx int64, fp64 values narrowed to fp32).
+    /// Uploads a host CSR (ptr/idx int64, fp64 values; the fp32 kernels read them narrowed).
     static SparseMatrix from_csr(index_t rows, index_t cols, const std::vector<index_t>& ptr,
                                  const std::vector<index_t>& idx, const std::vector<double>& val) {
         if (static_cast<index_t>(ptr.size()) != rows + 1)
@@ -192,7 +192,7 @@ inline DenseVector spmv(const SparseMatrix& m, const DenseVector& x, int threads
     return spmv(m, std::span<const double>(x), threads);
 }
 
-/// read_sparse (inc/sparse.hpp:409-432): values narrowed to fp32 on upload.
+/// read_sparse (inc/sparse.hpp:409-432): values kept exactly (fp32 kernels read them narrowed).
 inline SparseMatrix read_sparse(std::istream& is, Layout layout = Layout::CSR) {
     std::string text((std::istreambuf_iterator<char>(is)), std::istreambuf_iterator<char>());
     spconv_csr* h = nullptr;

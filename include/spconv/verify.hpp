@@ -1,11 +1,12 @@
 // Drop-in replacement for the reference's spconv/verify.hpp
 // (inc/verify.hpp:24-169): the exhaustive small-size sweep, run against the
-// DEVICE path -- the CSR transform and its CSC relayout built and applied on
-// the GPU, checked against device comparators (fp64 direct_conv / im2col,
-// bit-identical to inc/reference.hpp, and fp32 direct_conv, bit-identical to
-// the SpMV).  Same VerifyOptions / VerifyReport names; the fp32 device path is
-// judged by the condition-relative bound 1e-5 * sum|w*a| (max_rel_dev) where
-// the fp64 reference used conv_tol on absolute deviations.
+// DEVICE path -- the CSR transform (built from the double taps, exact values)
+// and its CSC relayout built and applied on the GPU.  The reference's own
+// check runs in fp64 on the device (fp64 SpMM of both layouts vs the fp64
+// direct_conv / im2col comparators, bit-identical to inc/reference.hpp), so
+// max_conv_dev / max_layout_dev are the reference's numbers.  The fp32 batch
+// path is checked on the same handles: bit-equal to the fp32 direct_conv,
+// CSR == CSC, and within 1e-5 * sum|w*a| of fp64 (max_rel_dev, an extra field).
 #pragma once
 
 #include <cstdint>

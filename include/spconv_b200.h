@@ -70,6 +70,24 @@ int spconv_build_transform(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p
                            const float* kernel_kxk, int layout, int device, void* stream,
                            spconv_csr** out);
 
+/* build_transform(kernel, spec, layout) (inc/conv.hpp:179-204) for the
+ * reference's own tap type, double.  Entries are kept exactly where the
+ * reference keeps them (double tap != 0.0, inc/sparse.hpp:335).  When every
+ * tap is an fp32 number this IS spconv_build_transform.  Otherwise the handle
+ * also keeps the exact fp64 value of every entry (built on the device from
+ * the taps): export, the text writer and spconv_spmm_f64 /
+ * spconv_convolve_host_f64 use them -- bit-identical to the reference for any
+ * double taps -- while the fp32 kernels (spmv / spmm / convolve_host) apply
+ * the fp32-narrowed taps. */
+int spconv_build_transform_f64(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
+                               const double* kernel_kxk, int layout, int device, void* stream,
+                               spconv_csr** out);
+
+/* "%.17g" of v as the device text writer renders it (exact: glibc's
+ * correctly rounded output), NUL-terminated into out (>= 32 bytes); returns
+ * the length.  Host-callable (no device work). */
+int spconv_format_g17(double v, char* out);
+
 /* SparseMatrix::layout() (inc/sparse.hpp:121): 0 = CSR, 1 = CSC. */
 int spconv_csr_layout(const spconv_csr* h, int* layout);
 
@@ -86,8 +104,9 @@ int spconv_matrix_from_host(int64_t rows, int64_t cols, int layout, const int64_
                             const int64_t* idx, const double* vals, int device, void* stream,
                             spconv_csr** out);
 
-/* Uploads an arbitrary host CSR (int64 ptr/idx, double values narrowed to
- * fp32) -- the device image of a reference SparseMatrix
+/* Uploads an arbitrary host CSR (int64 ptr/idx, double values; the fp32
+ * kernels read them narrowed, and when some value is not an fp32 number the
+ * exact doubles are kept too, for export / text / the fp64 SpMM) -- the device image of a reference SparseMatrix
  * (inc/sparse.hpp:121-130) for spmv on matrices not built here (e.g. read
  * with read_sparse, inc/sparse.hpp:412-432).  Columns must be strictly
  * ascending per row (the CSR contract of inc/sparse.hpp:77-83). */
@@ -139,8 +158,9 @@ int spconv_convolve_host(const spconv_csr* h, const float* X_host, float* Y_host
  * acc = 0.0; acc = acc + (double)val * x[col] over the stored entries in
  * order, one rounded multiply and one rounded add each (inc/sparse.hpp:185-191
  * as its Release build evaluates it).  Bit-identical to the reference's
- * spmv() whenever the stored values equal the reference's, i.e. for
- * fp32-representable taps. */
+ * spmv() whenever the stored values equal the reference's: always for
+ * handles from spconv_build_transform_f64 / host uploads (they keep exact
+ * values when fp32 cannot hold them), and for fp32 taps otherwise. */
 int spconv_spmm_f64(const spconv_csr* h, const double* X_dev, int64_t ldx, double* Y_dev, int64_t ldy,
                     int64_t batch, void* stream);
 
@@ -154,8 +174,8 @@ int spconv_convolve_host_f64(const spconv_csr* h, const double* X_host, double* 
  * transform_header_line != 0, write_transform (inc/conv.hpp:217-224):
  * "%%transform m n k s p csr|csc" then write_sparse (inc/sparse.hpp:400-406):
  * "%%sparse coordinate real", "rows cols nnz", one "row col value" line per
- * entry (1-based, storage order -- column-major for CSC, value = "%.17g" of the fp32 value widened
- * to double).  Byte-identical to the reference's output for the same matrix.
+ * entry (1-based, storage order -- column-major for CSC, value = "%.17g" of the entry's
+ * exact double when the handle keeps one, else of the fp32 value widened).  Byte-identical to the reference's output for the same matrix.
  * buf == NULL: only *len (the text size in bytes) is computed; otherwise the
  * text is copied to buf (cap >= *len bytes, no terminator). */
 int spconv_csr_write_text(const spconv_csr* h, int transform_header_line, char* buf, int64_t cap,
@@ -164,7 +184,7 @@ int spconv_csr_write_text(const spconv_csr* h, int transform_header_line, char* 
 /* read_transform (inc/conv.hpp:226-244) + read_sparse (inc/sparse.hpp:412-432)
  * of `len` bytes of text: same header checks, range / duplicate checks and
  * messages (status 3 where the reference throws std::runtime_error, 1 for
- * std::invalid_argument).  Values are narrowed to fp32.  A matrix that equals
+ * std::invalid_argument).  Values are kept exactly (see spconv_csr_from_host).  A matrix that equals
  * the conv transform of its own taps comes back as a built conv handle
  * (band kernels apply); anything else as a generic CSR with the geometry
  * attached.  The file's layout (csr / csc) is the handle's layout. */
@@ -214,13 +234,16 @@ int spconv_time_apply(int method, const spconv_csr* h, int64_t batch, int64_t m,
  * m, n <= max_dim, p <= 3, s <= 3, k <= min(m,n) + 2p, the Theorem 2.1 count
  * against the brute-force overlap count and nnz(T), and for `seeds` seeded
  * cases (the reference's inputs: derive_seed(base_seed, case), nonzero
- * kernels) the device CSR transform, its device CSC relayout, the fp32 device
- * direct_conv and the fp64 device direct_conv / im2col_conv.  Checks: fp64
- * comparators agree within 1e-10; the fp32 sparse outputs are within
- * 1e-5 * sum|w*a| of the fp64 reference and BIT-equal to the fp32 direct_conv;
- * CSR and CSC outputs are bit-equal.  counts = {specs, conv_cases,
- * clipped_specs, failures}; devs = {max |sparse or im2col - reference|,
- * max |CSR - CSC|, max condition-relative fp32 deviation}; `failures` gets the
+ * kernels) the device CSR transform built from the double taps
+ * (spconv_build_transform_f64) and its device CSC relayout.  The reference's
+ * own check (inc/verify.hpp:124-155), in fp64 on the device: both layouts
+ * through spconv_spmm_f64, the fp64 direct_conv and im2col_conv, all within
+ * 1e-10 (the reference's conv_tol) and CSR == CSC.  The fp32 contract on the
+ * same handles: spmv within 1e-5 * sum|w*a| of the fp64 result on the same
+ * fp32-rounded data, BIT-equal to the fp32 direct_conv, CSR == CSC bit for
+ * bit.  counts = {specs, conv_cases, clipped_specs, failures}; devs = {the
+ * reference's max_conv_dev, max_layout_dev (fp64 leg), max condition-relative
+ * fp32 deviation}; `failures` gets the
  * first (at most 20) failure lines, '
 '-separated. */
 int spconv_run_verification(int64_t max_dim, int seeds, uint64_t base_seed, int device, int64_t counts[4],

@@ -67,8 +67,11 @@ _decl("spconv_spmm_f64", [_vp, _vp, _i64, _vp, _i64, _i64, _vp])
 _decl("spconv_csr_last_kernel", [_vp], C.c_char_p)
 _decl("spconv_csr_write_text", [_vp, C.c_int, _vp, _i64, _P(_i64)])
 _decl("spconv_transform_read", [_vp, _i64, C.c_int, _vp, _P(_vp)])
+_decl("spconv_sparse_read", [_vp, _i64, C.c_int, C.c_int, _vp, _P(_vp)])
 _decl("spconv_csr_free", [_vp])
 _decl("spconv_build_transform", [_i64] * 5 + [_vp, C.c_int, C.c_int, _vp, _P(_vp)])
+_decl("spconv_build_transform_f64", [_i64] * 5 + [_vp, C.c_int, C.c_int, _vp, _P(_vp)])
+_decl("spconv_format_g17", [C.c_double, C.c_char_p])
 _decl("spconv_csr_layout", [_vp, _P(C.c_int)])
 _decl("spconv_relayout", [_vp, C.c_int, _vp, _P(_vp)])
 _decl("spconv_direct_conv", [_i64] * 5 + [C.c_int, _vp, _vp, _vp, _vp, _i64, _vp])
@@ -266,6 +269,15 @@ class Transform:
             pass
 
 
+def read_sparse(text: bytes, layout: int = Layout.CSR, device: int = 0, stream=None) -> Transform:
+    """read_sparse (inc/sparse.hpp:409-432): a generic matrix (spec None)."""
+    if isinstance(text, str):
+        text = text.encode()
+    h = _vp()
+    _check(lib.spconv_sparse_read(text, len(text), layout, device, _stream_handle(stream), C.byref(h)))
+    return Transform(h.value, None, device)
+
+
 def read_transform(text: bytes, device: int = 0, stream=None) -> Transform:
     """read_transform (inc/conv.hpp:226-244): parse, validate, upload (fp32)."""
     if isinstance(text, str):
@@ -277,16 +289,26 @@ def read_transform(text: bytes, device: int = 0, stream=None) -> Transform:
     return Transform(h.value, ConvSpec(*spec5), device)
 
 
+def format_g17(v: float) -> str:
+    """The text writer's "%.17g" of a double (exact; host-callable)."""
+    buf = C.create_string_buffer(32)
+    n = lib.spconv_format_g17(C.c_double(v), buf)
+    return buf.raw[:n].decode()
+
+
 def build_transform(kern: Kernel, spec: ConvSpec, layout: int = Layout.CSR, device: int = 0,
                     stream=None) -> Transform:
     """On-device build of T in CSR or CSC layout (replaces inc/conv.hpp:179-204;
-    both reference routes give the same matrix)."""
+    both reference routes give the same matrix).  The taps are the reference's
+    doubles: entries are kept where the double tap is non-zero, and taps fp32
+    cannot represent keep their exact values for export / text / spmm_f64
+    (spconv_build_transform_f64); the fp32 kernels apply the narrowed taps."""
     if kern.k != spec.k:
         raise ValueError(f"build_conv_matrix: kernel side {kern.k} does not match spec {spec.str()}")
-    k32 = np.ascontiguousarray(kern.values, np.float32)
+    k64 = np.ascontiguousarray(kern.values, np.float64)
     h = _vp()
-    _check(lib.spconv_build_transform(spec.m, spec.n, spec.k, spec.s, spec.p, k32.ctypes.data,
-                                      layout, device, _stream_handle(stream), C.byref(h)))
+    _check(lib.spconv_build_transform_f64(spec.m, spec.n, spec.k, spec.s, spec.p, k64.ctypes.data,
+                                          layout, device, _stream_handle(stream), C.byref(h)))
     return Transform(h.value, spec, device)
 
 

@@ -547,7 +547,7 @@ int attach_csc_conv(spconv_csr* h, cudaStream_t st) {
 
 // CSC storage given on the host (already validated), uploaded synchronously.
 int attach_csc_host(spconv_csr* h, const std::vector<int32_t>& cp, const std::vector<int32_t>& ci,
-                    const std::vector<float>& cv, cudaStream_t st) {
+                    const std::vector<float>& cv, const double* cv64, cudaStream_t st) {
     const size_t cp_bytes = ((size_t)(h->cols + 1) * 4 + 255) & ~size_t(255);
     const size_t ix_bytes = ((size_t)std::max<int64_t>(h->nnz, 1) * 4 + 255) & ~size_t(255);
     char* mem = nullptr;
@@ -560,6 +560,11 @@ int attach_csc_host(spconv_csr* h, const std::vector<int32_t>& cp, const std::ve
     if (h->nnz > 0) {
         CK(cudaMemcpyAsync(h->csc_idx, ci.data(), (size_t)h->nnz * 4, cudaMemcpyHostToDevice, st));
         CK(cudaMemcpyAsync(h->csc_vals, cv.data(), (size_t)h->nnz * 4, cudaMemcpyHostToDevice, st));
+    }
+    if (cv64 && h->vals64) {  // exact values (the row-major side found some fp32 cannot hold)
+        CK(cudaMalloc(&h->csc_vals64, (size_t)std::max<int64_t>(h->nnz, 1) * 8));
+        if (h->nnz > 0)
+            CK(cudaMemcpyAsync(h->csc_vals64, cv64, (size_t)h->nnz * 8, cudaMemcpyHostToDevice, st));
     }
     CK(cudaStreamSynchronize(st));  // the host vectors die with the caller
     return SPCONV_OK;
@@ -819,6 +824,63 @@ int spconv_build_transform(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p
     return SPCONV_OK;
 }
 
+int spconv_build_transform_f64(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
+                               const double* kernel_kxk, int layout, int device, void* stream,
+                               spconv_csr** out) {
+    if (layout != 0 && layout != 1)
+        return fail(SPCONV_EINVAL, "spconv_build_transform_f64: layout must be 0 (csr) or 1 (csc)");
+    if (int rc = check_spec(m, n, k, s, p)) return rc;
+    if (!kernel_kxk || !out) return fail(SPCONV_EINVAL, "spconv_build_transform_f64: null argument");
+    *out = nullptr;
+    const int64_t kk = k * k;
+    if (kk >= (1ll << 24))
+        return fail(SPCONV_EINVAL, "spconv_build_transform_f64: kernel side " + std::to_string(k) + " too large");
+    std::vector<float> t32((size_t)kk);
+    bool exact = true;
+    for (int64_t q = 0; q < kk; ++q) {
+        t32[(size_t)q] = (float)kernel_kxk[q];
+        exact &= __builtin_bit_cast(uint64_t, (double)t32[(size_t)q]) == __builtin_bit_cast(uint64_t, kernel_kxk[q]);
+    }
+    if (exact)  // every tap is an fp32 number: the fp32 build is already exact
+        return spconv_build_transform(m, n, k, s, p, t32.data(), layout, device, stream, out);
+    // Build the structure from tags (q + 1 where the DOUBLE tap is non-zero,
+    // inc/sparse.hpp:335), then swap the tags for the values on the device.
+    std::vector<float> tag((size_t)kk);
+    for (int64_t q = 0; q < kk; ++q) tag[(size_t)q] = kernel_kxk[q] != 0.0 ? (float)(q + 1) : 0.0f;
+    spconv_csr* h = nullptr;
+    if (int rc = spconv_build_transform(m, n, k, s, p, tag.data(), layout, device, stream, &h)) return rc;
+    DeviceGuard dg(device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t t32_bytes = ((size_t)kk * 4 + 255) & ~size_t(255);
+    char* tt = nullptr;
+    cudaError_t e = cudaMallocAsync(&tt, t32_bytes + (size_t)kk * 8, st);
+    const size_t vb = (size_t)std::max<int64_t>(h->nnz, 1) * 8;
+    if (e == cudaSuccess) e = cudaMallocAsync(&h->vals64, vb, st);
+    if (e == cudaSuccess && h->layout == 1) e = cudaMallocAsync(&h->csc_vals64, vb, st);
+    // (pageable sources: staged by the driver before each call returns)
+    if (e == cudaSuccess) e = cudaMemcpyAsync(tt, t32.data(), (size_t)kk * 4, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(tt + t32_bytes, kernel_kxk, (size_t)kk * 8, cudaMemcpyHostToDevice, st);
+    const float* d32 = reinterpret_cast<const float*>(tt);
+    const double* d64 = reinterpret_cast<const double*>(tt + t32_bytes);
+    if (e == cudaSuccess) e = spb::launch_retag(h->vals, h->vals64, h->nnz, d32, d64, st);
+    if (e == cudaSuccess && h->layout == 1) e = spb::launch_retag(h->csc_vals, h->csc_vals64, h->nnz, d32, d64, st);
+    // the device taps (band check, CSC rebuilds) become the real fp32 taps
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h->taps, d32, (size_t)kk * 4, cudaMemcpyDeviceToDevice, st);
+    if (e == cudaSuccess && h->built) e = cudaEventRecord(h->built, st);  // side checks see the final values
+    if (tt) cudaFreeAsync(tt, st);
+    if (e != cudaSuccess) {
+        spconv_csr_free(h);
+        return cuda_fail(e, "spconv_build_transform_f64");
+    }
+    h->host_taps = t32;
+    h->host_taps64.assign(kernel_kxk, kernel_kxk + kk);
+    h->taps_dense = true;
+    for (float v : t32) h->taps_dense &= v != 0.0f && std::isfinite(v);
+    *out = h;
+    return SPCONV_OK;
+}
+
 int spconv_csr_layout(const spconv_csr* h, int* layout) {
     if (!h || !layout) return fail(SPCONV_EINVAL, "null argument");
     *layout = h->layout;
@@ -860,13 +922,27 @@ int spconv_matrix_from_host(int64_t rows, int64_t cols, int layout, const int64_
     for (int64_t c = 0; c <= cols; ++c) cp[(size_t)c] = (int32_t)ptr[c];
     for (int64_t e = 0; e < nnz; ++e) ci[(size_t)e] = (int32_t)idx[e], cv[(size_t)e] = (float)vals[e];
     DeviceGuard dg(device);
-    if (int rc = attach_csc_host(h, cp, ci, cv, static_cast<cudaStream_t>(stream))) {
+    if (int rc = attach_csc_host(h, cp, ci, cv, vals, static_cast<cudaStream_t>(stream))) {
         const std::string msg = g_err;
         spconv_csr_free(h);
         return fail(rc, msg);
     }
     *out = h;
     return SPCONV_OK;
+}
+
+// spconv_csr_export of the row-major arrays whatever h's layout (a non-owning view).
+static int export_row_major(const spconv_csr* h, int64_t* rp, int64_t* ri, double* rv) {
+    spconv_csr tmp;
+    tmp.device = h->device;
+    tmp.rows = h->rows;
+    tmp.cols = h->cols;
+    tmp.nnz = h->nnz;
+    tmp.row_ptr = h->row_ptr;
+    tmp.col_idx = h->col_idx;
+    tmp.vals = h->vals;
+    tmp.vals64 = h->vals64;
+    return spconv_csr_export(&tmp, rp, ri, rv);
 }
 
 int spconv_relayout(const spconv_csr* h, int layout, void* stream, spconv_csr** out) {
@@ -877,25 +953,16 @@ int spconv_relayout(const spconv_csr* h, int layout, void* stream, spconv_csr** 
         // A conv handle IS the transform of its taps: rebuild in the target
         // layout on the device (closed form; no host round trip).
         const Geom& g = h->g;
+        if (!h->host_taps64.empty())
+            return spconv_build_transform_f64(g.m, g.n, g.k, g.s, g.p, h->host_taps64.data(), layout, h->device,
+                                              stream, out);
         return spconv_build_transform(g.m, g.n, g.k, g.s, g.p, h->host_taps.data(), layout, h->device,
                                       stream, out);
     }
     // Matrices that came from the host: transposition of the host copy.
     std::vector<int64_t> rp((size_t)h->rows + 1), ri((size_t)std::max<int64_t>(h->nnz, 1));
     std::vector<double> rv((size_t)std::max<int64_t>(h->nnz, 1));
-    {
-        spconv_csr tmp;  // export the row-major arrays regardless of h's layout
-        tmp.device = h->device;
-        tmp.rows = h->rows;
-        tmp.cols = h->cols;
-        tmp.nnz = h->nnz;
-        tmp.row_ptr = h->row_ptr;
-        tmp.col_idx = h->col_idx;
-        tmp.vals = h->vals;
-        const int rc = spconv_csr_export(&tmp, rp.data(), ri.data(), rv.data());
-        tmp.row_ptr = nullptr;  // not owned
-        if (rc) return rc;
-    }
+    if (int rc = export_row_major(h, rp.data(), ri.data(), rv.data())) return rc;
     int rc;
     if (layout == 0) {
         rc = spconv_csr_from_host(h->rows, h->cols, rp.data(), ri.data(), rv.data(), h->device, stream, out);
@@ -939,7 +1006,11 @@ int spconv_csr_from_host(int64_t rows, int64_t cols, const int64_t* row_ptr,
         rp[r] = (int32_t)row_ptr[r];
     }
     rp[rows] = (int32_t)nnz;
-    for (int64_t e = 0; e < nnz; ++e) ci[e] = (int32_t)col_idx[e], vv[e] = (float)vals[e];
+    bool exact = true;
+    for (int64_t e = 0; e < nnz; ++e) {
+        ci[e] = (int32_t)col_idx[e], vv[e] = (float)vals[e];
+        exact &= __builtin_bit_cast(uint64_t, (double)vv[e]) == __builtin_bit_cast(uint64_t, vals[e]);
+    }
     DeviceGuard dg(device);
     if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
     auto* h = new (std::nothrow) spconv_csr();
@@ -967,9 +1038,14 @@ int spconv_csr_from_host(int64_t rows, int64_t cols, const int64_t* row_ptr,
         e = cudaMemcpyAsync(h->col_idx, ci.data(), ci.size() * 4, cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(h->vals, vv.data(), vv.size() * 4, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess && !exact) {  // keep the exact values next to the fp32 ones
+        e = cudaMalloc(&h->vals64, (size_t)std::max<int64_t>(nnz, 1) * 8);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(h->vals64, vals, (size_t)nnz * 8, cudaMemcpyHostToDevice, st);
+    }
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // host vectors die here
     if (e != cudaSuccess) {
         cudaFree(csr);
+        if (h->vals64) cudaFree(h->vals64);
         delete h;
         return cuda_fail(e, "spconv_csr_from_host upload");
     }
@@ -1021,7 +1097,10 @@ int spconv_csr_export(const spconv_csr* h, int64_t* row_ptr, int64_t* col_idx, d
         CK(cudaMemcpy(tmp.data(), h->layout ? h->csc_idx : h->col_idx, tmp.size() * 4, cudaMemcpyDeviceToHost));
         for (size_t i = 0; i < tmp.size(); ++i) col_idx[i] = tmp[i];
     }
-    if (vals && h->nnz > 0) {
+    const double* v64 = h->layout ? h->csc_vals64 : h->vals64;
+    if (vals && h->nnz > 0 && v64) {
+        CK(cudaMemcpy(vals, v64, (size_t)h->nnz * 8, cudaMemcpyDeviceToHost));
+    } else if (vals && h->nnz > 0) {
         std::vector<float> tmp((size_t)h->nnz);
         CK(cudaMemcpy(tmp.data(), h->layout ? h->csc_vals : h->vals, tmp.size() * 4, cudaMemcpyDeviceToHost));
         for (size_t i = 0; i < tmp.size(); ++i) vals[i] = tmp[i];
@@ -1156,7 +1235,7 @@ int spconv_spmm_f64(const spconv_csr* h, const double* X_dev, int64_t ldx, doubl
         return fail(SPCONV_EINVAL, "spconv_spmm_f64: X and Y overlap");
     DeviceGuard dg(h->device);
     if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
-    spb::F64Params fp{h->row_ptr, h->col_idx, h->vals, X_dev, ldx, Y_dev, ldy, (int)h->rows, (int)batch};
+    spb::F64Params fp{h->row_ptr, h->col_idx, h->vals, h->vals64, X_dev, ldx, Y_dev, ldy, (int)h->rows, (int)batch};
     CK(spb::launch_spmm_f64(fp, static_cast<cudaStream_t>(stream)));
     const_cast<spconv_csr*>(h)->last_kernel.store("csr_spmm_f64");
     return SPCONV_OK;
@@ -1207,13 +1286,14 @@ int spconv_csr_write_text(const spconv_csr* h, int transform_header_line, char* 
     const int32_t* sp_ = csc ? h->csc_ptr : h->row_ptr;
     const int32_t* si_ = csc ? h->csc_idx : h->col_idx;
     const float* sv_ = csc ? h->csc_vals : h->vals;
+    const double* sv64 = csc ? h->csc_vals64 : h->vals64;
     const int64_t major = csc ? h->cols : h->rows;
     const int64_t blocks = (major + spb::text_rows_per_block() - 1) / spb::text_rows_per_block();
     cudaStream_t st = nullptr;
     unsigned long long* scratch = nullptr;
     CK(cudaMallocAsync(&scratch, (size_t)(blocks + 2) * 8, st));
     unsigned long long total = 0;
-    cudaError_t e = spb::render_entries(sp_, si_, sv_, (int)major, scratch, nullptr, head.size(), st, true, csc);
+    cudaError_t e = spb::render_entries(sp_, si_, sv_, sv64, (int)major, scratch, nullptr, head.size(), st, true, csc);
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(&total, scratch + blocks, 8, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
@@ -1236,7 +1316,7 @@ int spconv_csr_write_text(const spconv_csr* h, int transform_header_line, char* 
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(text, head.data(), head.size(), cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess)
-        e = spb::render_entries(sp_, si_, sv_, (int)major, scratch, text, head.size(), st, false, csc);
+        e = spb::render_entries(sp_, si_, sv_, sv64, (int)major, scratch, text, head.size(), st, false, csc);
     if (e == cudaSuccess) e = cudaMemcpyAsync(buf, text, (size_t)total, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     cudaFreeAsync(text, st);
@@ -1292,31 +1372,23 @@ int spconv_transform_read(const char* text, int64_t len, int device, void* strea
     // first row that stores all k*k of them), rebuild it on the device and
     // keep the built handle: identical arrays, plus the geometry the band
     // kernels need.  Otherwise keep the upload as a generic CSR.
-    std::vector<float> taps;
+    std::vector<double> taps;
     for (int64_t r = 0; r < rows && taps.empty(); ++r)
         if (ptr[(size_t)r + 1] - ptr[(size_t)r] == k * k)
-            for (int64_t q = 0; q < k * k; ++q) taps.push_back((float)val[(size_t)(ptr[(size_t)r] + q)]);
+            for (int64_t q = 0; q < k * k; ++q) taps.push_back(val[(size_t)(ptr[(size_t)r] + q)]);
     if (!taps.empty()) {
         spconv_csr* built = nullptr;
-        if (spconv_build_csr(m, n, k, s, p, taps.data(), device, stream, &built) == SPCONV_OK) {
+        if (spconv_build_transform_f64(m, n, k, s, p, taps.data(), csc ? 1 : 0, device, stream, &built) ==
+            SPCONV_OK) {
             bool same = built->nnz == nnz;
-            if (same) {
-                std::vector<int32_t> brp((size_t)rows + 1), bci((size_t)std::max<int64_t>(nnz, 1));
-                std::vector<float> bv((size_t)std::max<int64_t>(nnz, 1));
-                same = spconv_csr_copy(built, brp.data(), bci.data(), bv.data(), stream) == SPCONV_OK;
+            if (same) {  // the row-major arrays (exact values) must equal the file's
+                std::vector<int64_t> brp((size_t)rows + 1), bci((size_t)std::max<int64_t>(nnz, 1));
+                std::vector<double> bv((size_t)std::max<int64_t>(nnz, 1));
+                same = export_row_major(built, brp.data(), bci.data(), bv.data()) == SPCONV_OK;
                 for (int64_t r = 0; same && r <= rows; ++r) same = brp[(size_t)r] == ptr[(size_t)r];
                 for (int64_t e = 0; same && e < nnz; ++e)
                     same = bci[(size_t)e] == idx[(size_t)e] &&
-                           __builtin_bit_cast(uint32_t, bv[(size_t)e]) ==
-                               __builtin_bit_cast(uint32_t, (float)val[(size_t)e]);
-            }
-            if (same && csc) {
-                DeviceGuard dg(device);
-                if (int rc = attach_csc_conv(built, static_cast<cudaStream_t>(stream))) {
-                    const std::string msg = g_err;
-                    spconv_csr_free(built);
-                    return fail(rc, msg);
-                }
+                           __builtin_bit_cast(uint64_t, bv[(size_t)e]) == __builtin_bit_cast(uint64_t, val[(size_t)e]);
             }
             if (same) {
                 *out = built;
@@ -1335,7 +1407,7 @@ int spconv_transform_read(const char* text, int64_t len, int device, void* strea
         transpose_host(rows, cols, ptr.data(), idx.data(), val.data(), cp, ci, cv);
         std::vector<float> cvf(cv.begin(), cv.end());
         DeviceGuard dg(device);
-        if (int rc = attach_csc_host(h, cp, ci, cvf, static_cast<cudaStream_t>(stream))) {
+        if (int rc = attach_csc_host(h, cp, ci, cvf, cv.data(), static_cast<cudaStream_t>(stream))) {
             const std::string msg = g_err;
             spconv_csr_free(h);
             return fail(rc, msg);
@@ -1362,6 +1434,8 @@ int spconv_csr_free(spconv_csr* h) {
         if (h->chk_stream) cudaStreamDestroy(h->chk_stream);
         if (h->row_ptr) cudaFree(h->row_ptr);
         if (h->csc_ptr) cudaFree(h->csc_ptr);
+        if (h->vals64) cudaFree(h->vals64);
+        if (h->csc_vals64) cudaFree(h->csc_vals64);
     }
     delete h;
     return SPCONV_OK;

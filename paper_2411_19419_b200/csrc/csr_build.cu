@@ -416,4 +416,29 @@ cudaError_t launch_csr_build(const BuildParams& bp, bool dense, int block, size_
     return launch_k<0, false>(bp, block, smem, st);
 }
 
+// Exact-fp64 builds (spconv_build_transform_f64) run the fp32 build on tag
+// taps (float)(q + 1) -- the structure then follows the DOUBLE taps' zero
+// test, as inc/sparse.hpp:335 does -- and this pass swaps each tag for the
+// tap's fp32 and fp64 values.  One streaming pass: 4 B read, 12 B written.
+__global__ void __launch_bounds__(256) retag_kernel(float* vals, double* vals64, int64_t nnz, const float* t32,
+                                                    const double* t64) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
+        const int q = (int)vals[e] - 1;
+        vals[e] = __ldg(t32 + q);
+        __stcs(vals64 + e, __ldg(t64 + q));
+    }
+}
+
+cudaError_t launch_retag(float* vals, double* vals64, int64_t nnz, const float* t32, const double* t64,
+                         cudaStream_t st) {
+    if (nnz <= 0) return cudaSuccess;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t want = (nnz + 255) / 256;
+    const int grid = (int)(want < (int64_t)sms * 8 ? want : (int64_t)sms * 8);
+    retag_kernel<<<grid, 256, 0, st>>>(vals, vals64, nnz, t32, t64);
+    return cudaGetLastError();
+}
+
 }  // namespace spb

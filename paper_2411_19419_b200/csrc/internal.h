@@ -143,6 +143,7 @@ struct F64Params {
     const int32_t* row_ptr;
     const int32_t* col_idx;
     const float* vals;
+    const double* vals64;  // exact values when the handle keeps them (else NULL: vals widened)
     const double* X;
     int64_t ldx;
     double* Y;
@@ -150,6 +151,10 @@ struct F64Params {
     int rows, batch;
 };
 cudaError_t launch_spmm_f64(const F64Params& fp, cudaStream_t st);
+// Tag -> value pass of the exact-fp64 build: vals[e] holds (float)(q + 1) for
+// tap q; rewritten to t32[q], and vals64[e] = t64[q] (csr_build.cu).
+cudaError_t launch_retag(float* vals, double* vals64, int64_t nnz, const float* t32, const double* t64,
+                         cudaStream_t st);
 cudaError_t launch_spmv_unrolled(const GenericParams& gp, int kmax, cudaStream_t st);
 cudaError_t launch_spmv_warp(const SpecParams& sp, int kmax, bool spec, cudaStream_t st);
 
@@ -159,8 +164,8 @@ cudaError_t launch_band(int k, int s, const BandParams& bp, const CUtensorMap* t
                         BandShape* shape, int sms);
 cudaError_t launch_band_check(int k, int s, const BandParams& bp, cudaStream_t st, int sms);
 
-cudaError_t render_entries(const int32_t* row_ptr, const int32_t* col_idx, const float* vals, int rows,
-                           unsigned long long* scratch, char* out_dev, unsigned long long base,
+cudaError_t render_entries(const int32_t* row_ptr, const int32_t* col_idx, const float* vals,
+                           const double* vals64, int rows, unsigned long long* scratch, char* out_dev, unsigned long long base,
                            cudaStream_t st, bool size_only, bool swap);
 int text_rows_per_block();
 
@@ -204,6 +209,12 @@ struct spconv_csr {
     int32_t* csc_idx = nullptr;    // device row_idx[nnz]
     float* csc_vals = nullptr;     // device vals[nnz]
     std::vector<float> host_taps;  // conv handles: the k*k fp32 taps (relayout rebuilds from them)
+    // Exact fp64 values, kept only when some value is not an fp32 number
+    // (double taps / host values fp32 does not represent): what export, text
+    // and the fp64 SpMM read.  The fp32 kernels read vals (narrowed).
+    std::vector<double> host_taps64;  // conv handles built from such double taps
+    double* vals64 = nullptr;         // device [nnz], row-major order
+    double* csc_vals64 = nullptr;     // device [nnz], CSC storage order (layout 1)
     // Side stream of the band check (run_spmm): the check reads only the
     // immutable matrix, so it need not wait for the caller's stream and can
     // overlap the previous call's apply; the apply waits on chk_done.

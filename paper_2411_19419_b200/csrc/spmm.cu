@@ -157,8 +157,10 @@ __global__ void __launch_bounds__(256) csr_spmm_f64(const F64Params P) {
     for (int b = blockIdx.y; b < P.batch; b += gridDim.y) {
         const double* x = P.X + (int64_t)b * P.ldx;
         double acc = 0.0;
-        for (int e = e0; e < e1; ++e)
-            acc = __dadd_rn(acc, __dmul_rn((double)__ldg(P.vals + e), __ldg(x + __ldg(P.col_idx + e))));
+        for (int e = e0; e < e1; ++e) {
+            const double v = P.vals64 ? __ldg(P.vals64 + e) : (double)__ldg(P.vals + e);
+            acc = __dadd_rn(acc, __dmul_rn(v, __ldg(x + __ldg(P.col_idx + e))));
+        }
         P.Y[(int64_t)b * P.ldy + r] = acc;
     }
 }

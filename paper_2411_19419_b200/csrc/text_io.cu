@@ -128,6 +128,167 @@ __device__ int format_g17(float v, char* out) {
     return o;
 }
 
+// ---- "%.17g" of an arbitrary double ----------------------------------------
+// Handles that keep exact fp64 values (vals64: taps or entries that fp32 does
+// not represent) print them with the reference's own format.  v = M * 2^E
+// exactly; D = round_half_even(v * 10^(16-X)) is computed as an exact
+// quotient Num / Den of big integers (<= 1024 bits: 5^340 * 2^53 at the
+// subnormal end, 2^971 * 2^53 / 5^292 at the top), so every double -- normal,
+// subnormal, huge -- prints as glibc prints it.  Host + device: the CPU tests
+// compare it with snprintf.
+namespace {
+
+constexpr int kBigLimbs = 17;
+struct Big {
+    unsigned long long w[kBigLimbs];
+};
+
+__host__ __device__ inline void big_set(Big& a, unsigned long long v) {
+    a.w[0] = v;
+    for (int i = 1; i < kBigLimbs; ++i) a.w[i] = 0;
+}
+__host__ __device__ inline void big_mul_small(Big& a, unsigned long long m) {
+    unsigned __int128 c = 0;
+    for (int i = 0; i < kBigLimbs; ++i) {
+        c += (unsigned __int128)a.w[i] * m;
+        a.w[i] = (unsigned long long)c;
+        c >>= 64;
+    }
+}
+__host__ __device__ inline void big_mul_pow5(Big& a, int q) {
+    for (; q >= 27; q -= 27) big_mul_small(a, 7450580596923828125ull);  // 5^27
+    unsigned long long r = 1;
+    for (; q > 0; --q) r *= 5ull;
+    big_mul_small(a, r);
+}
+__host__ __device__ inline void big_shl(Big& a, int s) {
+    const int li = s >> 6, bo = s & 63;
+    for (int i = kBigLimbs - 1; i >= 0; --i) {
+        const unsigned long long lo = i - li >= 0 ? a.w[i - li] : 0ull;
+        const unsigned long long lo2 = i - li - 1 >= 0 ? a.w[i - li - 1] : 0ull;
+        a.w[i] = bo ? (lo << bo) | (lo2 >> (64 - bo)) : lo;
+    }
+}
+__host__ __device__ inline void big_shr1(Big& a) {
+    for (int i = 0; i < kBigLimbs; ++i) a.w[i] = (a.w[i] >> 1) | (i + 1 < kBigLimbs ? a.w[i + 1] << 63 : 0ull);
+}
+__host__ __device__ inline int big_cmp(const Big& a, const Big& b) {
+    for (int i = kBigLimbs - 1; i >= 0; --i)
+        if (a.w[i] != b.w[i]) return a.w[i] < b.w[i] ? -1 : 1;
+    return 0;
+}
+__host__ __device__ inline void big_sub(Big& a, const Big& b) {  // a -= b (a >= b)
+    unsigned long long borrow = 0;
+    for (int i = 0; i < kBigLimbs; ++i) {
+        const unsigned long long x = a.w[i], y = b.w[i];
+        const unsigned long long d = x - y - borrow;
+        borrow = (x < y) || (x - y < borrow) ? 1ull : 0ull;
+        a.w[i] = d;
+    }
+}
+
+// floor(M * 2^E * 10^k) (known to be < 2^64); *up = round-half-even adds one.
+__host__ __device__ inline unsigned long long scaled_floor64(unsigned long long M, int E, int k, bool* up) {
+    Big num, den;
+    big_set(num, M);
+    big_set(den, 1);
+    if (k >= 0) big_mul_pow5(num, k);
+    else big_mul_pow5(den, -k);
+    const int t = E + k;  // power of two
+    if (t >= 0) big_shl(num, t);
+    else big_shl(den, -t);
+    // quotient bits 63..0 by restoring division against den << 63
+    Big sh = den;
+    big_shl(sh, 63);
+    unsigned long long q = 0;
+    for (int b = 63; b >= 0; --b) {
+        if (big_cmp(num, sh) >= 0) {
+            big_sub(num, sh);
+            q |= 1ull << b;
+        }
+        big_shr1(sh);
+    }
+    // num = remainder < den; compare 2*rem with den
+    big_shl(num, 1);
+    const int c = big_cmp(num, den);
+    *up = c > 0 || (c == 0 && (q & 1ull));
+    return q;
+}
+
+}  // namespace
+
+__host__ __device__ int format_g17_f64(double v, char* out) {
+    unsigned long long bits;
+    memcpy(&bits, &v, 8);
+    int o = 0;
+    if (bits >> 63) out[o++] = '-';
+    const unsigned ex = (unsigned)(bits >> 52) & 0x7ffu;
+    const unsigned long long man = bits & 0xfffffffffffffull;
+    if (ex == 0x7ffu) {
+        const char* w = man ? "nan" : "inf";
+        for (int i = 0; i < 3; ++i) out[o++] = w[i];
+        return o;
+    }
+    if (ex == 0 && man == 0) {
+        out[o++] = '0';
+        return o;
+    }
+    const unsigned long long M = ex ? (man | (1ull << 52)) : man;
+    const int E = ex ? (int)ex - 1075 : -1074;
+    // X = floor(log10 v) exactly: the estimate is fixed on the TRUNCATED
+    // 17-digit quotient (a double can sit within half a unit of 10^X, where the
+    // rounded one would mislead); then the rounding may carry into 10^17.
+    int X = (int)floor(log10((double)M) + E * 0.30102999566398120);
+    unsigned long long D = 0;
+    for (int guard = 0; guard < 4; ++guard) {
+        bool up = false;
+        D = scaled_floor64(M, E, 16 - X, &up);
+        if (D >= 100000000000000000ull) {
+            ++X;
+        } else if (D < 10000000000000000ull) {
+            --X;
+        } else {
+            D += up ? 1ull : 0ull;
+            if (D == 100000000000000000ull) D = 10000000000000000ull, ++X;
+            break;
+        }
+    }
+    char dg[17];
+    for (int i = 16; i >= 0; --i) {
+        dg[i] = (char)('0' + (int)(D % 10ull));
+        D /= 10ull;
+    }
+    int last = 16;
+    while (last > 0 && dg[last] == '0') --last;
+    if (X >= -4 && X < 17) {
+        if (X >= 0) {
+            for (int i = 0; i <= X; ++i) out[o++] = dg[i];
+            if (last > X) {
+                out[o++] = '.';
+                for (int i = X + 1; i <= last; ++i) out[o++] = dg[i];
+            }
+        } else {
+            out[o++] = '0';
+            out[o++] = '.';
+            for (int i = 0; i < -X - 1; ++i) out[o++] = '0';
+            for (int i = 0; i <= last; ++i) out[o++] = dg[i];
+        }
+    } else {
+        out[o++] = dg[0];
+        if (last > 0) {
+            out[o++] = '.';
+            for (int i = 1; i <= last; ++i) out[o++] = dg[i];
+        }
+        out[o++] = 'e';
+        out[o++] = X < 0 ? '-' : '+';
+        const int ax = X < 0 ? -X : X;
+        if (ax >= 100) out[o++] = (char)('0' + ax / 100);
+        out[o++] = (char)('0' + (ax / 10) % 10);
+        out[o++] = (char)('0' + ax % 10);
+    }
+    return o;
+}
+
 namespace {
 
 __device__ __forceinline__ int format_u64(unsigned long long v, char* out) {
@@ -147,11 +308,16 @@ __device__ __forceinline__ int digits_u64(unsigned long long v) {
     return n;
 }
 
+// "%.17g" of entry e: the exact fp64 value when the handle keeps one.
+__device__ __forceinline__ int format_entry(const float* vals, const double* vals64, int e, char* out) {
+    return vals64 ? format_g17_f64(vals64[e], out) : format_g17(vals[e], out);
+}
+
 // Bytes of one entry line "r c v\n".
-__device__ __forceinline__ int line_bytes(int row, int col, float v) {
+__device__ __forceinline__ int line_bytes(int row, int col, const float* vals, const double* vals64, int e) {
     char tmp[32];
     return digits_u64((unsigned long long)row + 1) + digits_u64((unsigned long long)col + 1) +
-           format_g17(v, tmp) + 3;
+           format_entry(vals, vals64, e, tmp) + 3;
 }
 
 constexpr int kRowsPerBlock = 64;
@@ -159,7 +325,7 @@ constexpr int kStageBytes = 96 * 1024;
 
 // Pass 1: bytes of each block of kRowsPerBlock rows.
 __global__ void __launch_bounds__(256) text_size_kernel(const int32_t* row_ptr, const int32_t* col_idx,
-                                                        const float* vals, int rows,
+                                                        const float* vals, const double* vals64, int rows,
                                                         unsigned long long* block_bytes) {
     __shared__ unsigned long long s_sum;
     if (threadIdx.x == 0) s_sum = 0;
@@ -172,7 +338,7 @@ __global__ void __launch_bounds__(256) text_size_kernel(const int32_t* row_ptr, 
     int r = r0;
     for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
         while (row_ptr[r + 1] <= e) ++r;
-        local += (unsigned long long)line_bytes(r, col_idx[e], vals[e]);
+        local += (unsigned long long)line_bytes(r, col_idx[e], vals, vals64, e);
     }
     atomicAdd(&s_sum, local);
     __syncthreads();
@@ -207,7 +373,7 @@ __global__ void __launch_bounds__(1024) text_scan_kernel(unsigned long long* v, 
 
 // Pass 2: render each block's lines into shared memory, then copy out.
 __global__ void __launch_bounds__(256) text_write_kernel(const int32_t* row_ptr, const int32_t* col_idx,
-                                                         const float* vals, int rows,
+                                                         const float* vals, const double* vals64, int rows,
                                                          const unsigned long long* block_off,
                                                          char* out, int swap) {
     extern __shared__ unsigned char s_text[];
@@ -234,7 +400,7 @@ __global__ void __launch_bounds__(256) text_write_kernel(const int32_t* row_ptr,
             line[len++] = ' ';
             len += format_u64(b, line + len);
             line[len++] = ' ';
-            len += format_g17(vals[e], line + len);
+            len += format_entry(vals, vals64, e, line + len);
             line[len++] = '\n';
         }
         // exclusive scan of len over the CTA
@@ -295,15 +461,15 @@ cudaError_t init_pow5(int dev) {
 // index first (CSC: "row col" = "minor major").  The line length is symmetric
 // in the two indices, so the size pass needs no flag.
 // `scratch` holds (rows / 64 + 2) unsigned long longs.
-cudaError_t render_entries(const int32_t* row_ptr, const int32_t* col_idx, const float* vals, int rows,
-                           unsigned long long* scratch, char* out_dev, unsigned long long base,
+cudaError_t render_entries(const int32_t* row_ptr, const int32_t* col_idx, const float* vals,
+                           const double* vals64, int rows, unsigned long long* scratch, char* out_dev, unsigned long long base,
                            cudaStream_t st, bool size_only, bool swap) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaError_t e = init_pow5(dev);
     if (e != cudaSuccess) return e;
     const int blocks = (rows + kRowsPerBlock - 1) / kRowsPerBlock;
-    text_size_kernel<<<blocks, 256, 0, st>>>(row_ptr, col_idx, vals, rows, scratch);
+    text_size_kernel<<<blocks, 256, 0, st>>>(row_ptr, col_idx, vals, vals64, rows, scratch);
     text_scan_kernel<<<1, 1024, 0, st>>>(scratch, blocks, base);
     if (size_only) return cudaGetLastError();
     static std::atomic<bool> attr[64];  // per device (benign concurrent first use)
@@ -313,7 +479,7 @@ cudaError_t render_entries(const int32_t* row_ptr, const int32_t* col_idx, const
         if (e != cudaSuccess) return e;
         attr[dev & 63] = true;
     }
-    text_write_kernel<<<blocks, 256, kStageBytes + 256 * 64, st>>>(row_ptr, col_idx, vals, rows, scratch,
+    text_write_kernel<<<blocks, 256, kStageBytes + 256 * 64, st>>>(row_ptr, col_idx, vals, vals64, rows, scratch,
                                                                   out_dev, swap ? 1 : 0);
     return cudaGetLastError();
 }
@@ -321,3 +487,10 @@ cudaError_t render_entries(const int32_t* row_ptr, const int32_t* col_idx, const
 int text_rows_per_block() { return kRowsPerBlock; }
 
 }  // namespace spb
+
+extern "C" int spconv_format_g17(double v, char* out) {
+    if (!out) return -1;
+    const int n = spb::format_g17_f64(v, out);
+    out[n] = '\0';
+    return n;
+}

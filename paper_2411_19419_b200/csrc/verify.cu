@@ -444,7 +444,8 @@ int spconv_run_verification(int64_t max_dim, int seeds, uint64_t base_seed, int 
         if (fails.size() < max_failures) fails.push_back(msg);
     };
     cudaStream_t st = nullptr;
-    DevBuf b_a32, b_a64, b_k32, b_k64, b_y32c, b_y32s, b_d32, b_ref, b_mag, b_i2c, b_patch;
+    DevBuf b_a32, b_a64, b_a64u, b_k32, b_k64, b_k64u, b_y32c, b_y32s, b_d32, b_ref_r, b_ref, b_mag, b_i2c, b_y64c,
+        b_y64s, b_patch;
     uint64_t case_index = 0;
     int rc = SPCONV_OK;
     bool stop = false;  // a CUDA error, or max_failures collected (run_verification returns early)
@@ -497,10 +498,12 @@ int spconv_run_verification(int64_t max_dim, int seeds, uint64_t base_seed, int 
                                 if (!z) break;
                             }
                             std::vector<float> a32(a64.begin(), a64.end()), k32(k64.begin(), k64.end());
-                            // fp64 comparators see the fp32-rounded data the device path sees
+                            // fp32 leg: the fp64 comparators see the fp32-rounded data it sees
                             std::vector<double> a64r(a32.begin(), a32.end()), k64r(k32.begin(), k32.end());
+                            // One CSR build from the reference's double taps (exact fp64 values +
+                            // the fp32-narrowed ones) and its CSC relayout serve both legs.
                             spconv_csr *tc = nullptr, *tcsc = nullptr;
-                            if (spconv_build_transform(m, n, k, s, p, k32.data(), 0, device, st, &tc) != SPCONV_OK ||
+                            if (spconv_build_transform_f64(m, n, k, s, p, k64.data(), 0, device, st, &tc) != SPCONV_OK ||
                                 spconv_relayout(tc, 1, st, &tcsc) != SPCONV_OK) {
                                 rc = SPCONV_ECUDA;
                                 stop = true;
@@ -513,38 +516,54 @@ int spconv_run_verification(int64_t max_dim, int seeds, uint64_t base_seed, int 
                                 fail("nnz(T) " + std::to_string(nz) + " != bound " + std::to_string(bound) + " for " +
                                      ss);
                             std::vector<float> ycsr((size_t)P), ycsc((size_t)P), yd32((size_t)P);
-                            std::vector<double> yref((size_t)P), ymag((size_t)P), yi2c((size_t)P);
+                            std::vector<double> yref_r((size_t)P), ymag((size_t)P);
+                            std::vector<double> yref((size_t)P), yi2c((size_t)P), y64c((size_t)P), y64s((size_t)P);
                             cudaError_t e = cudaSuccess;
                             auto ok = [&](cudaError_t x) { return (e = (e == cudaSuccess ? x : e)) == cudaSuccess; };
                             ok(b_a32.reserve(mn * 4));
                             ok(b_a64.reserve(mn * 8));
+                            ok(b_a64u.reserve(mn * 8));
                             ok(b_k32.reserve(k * k * 4));
                             ok(b_k64.reserve(k * k * 8));
+                            ok(b_k64u.reserve(k * k * 8));
                             ok(b_y32c.reserve(P * 4));
                             ok(b_y32s.reserve(P * 4));
                             ok(b_d32.reserve(P * 4));
+                            ok(b_ref_r.reserve(P * 8));
                             ok(b_ref.reserve(P * 8));
                             ok(b_mag.reserve(P * 8));
                             ok(b_i2c.reserve(P * 8));
+                            ok(b_y64c.reserve(P * 8));
+                            ok(b_y64s.reserve(P * 8));
                             ok(b_patch.reserve(P * k * k * 8));
                             ok(cudaMemcpy(b_a32.p, a32.data(), mn * 4, cudaMemcpyHostToDevice));
                             ok(cudaMemcpy(b_a64.p, a64r.data(), mn * 8, cudaMemcpyHostToDevice));
+                            ok(cudaMemcpy(b_a64u.p, a64.data(), mn * 8, cudaMemcpyHostToDevice));
                             ok(cudaMemcpy(b_k32.p, k32.data(), k * k * 4, cudaMemcpyHostToDevice));
                             ok(cudaMemcpy(b_k64.p, k64r.data(), k * k * 8, cudaMemcpyHostToDevice));
+                            ok(cudaMemcpy(b_k64u.p, k64.data(), k * k * 8, cudaMemcpyHostToDevice));
                             int r1 = SPCONV_OK;
                             if (e == cudaSuccess) {
+                                // fp64 leg -- the reference's own check (inc/verify.hpp:124-155)
+                                r1 |= spconv_spmm_f64(tc, (const double*)b_a64u.p, mn, (double*)b_y64c.p, P, 1, st);
+                                r1 |= spconv_spmm_f64(tcsc, (const double*)b_a64u.p, mn, (double*)b_y64s.p, P, 1, st);
+                                r1 |= spconv_direct_conv(m, n, k, s, p, 1, b_k64u.p, b_a64u.p, b_ref.p, nullptr, 1, st);
+                                r1 |= spconv_im2col_conv(m, n, k, s, p, 1, b_k64u.p, b_a64u.p, b_i2c.p, b_patch.p, 1, st);
+                                // fp32 leg -- the batch kernels' contract
                                 r1 |= spconv_spmv(tc, (const float*)b_a32.p, (float*)b_y32c.p, st);
                                 r1 |= spconv_spmv(tcsc, (const float*)b_a32.p, (float*)b_y32s.p, st);
                                 r1 |= spconv_direct_conv(m, n, k, s, p, 0, b_k32.p, b_a32.p, b_d32.p, nullptr, 1, st);
-                                r1 |= spconv_direct_conv(m, n, k, s, p, 1, b_k64.p, b_a64.p, b_ref.p, b_mag.p, 1, st);
-                                r1 |= spconv_im2col_conv(m, n, k, s, p, 1, b_k64.p, b_a64.p, b_i2c.p, b_patch.p, 1, st);
+                                r1 |= spconv_direct_conv(m, n, k, s, p, 1, b_k64.p, b_a64.p, b_ref_r.p, b_mag.p, 1, st);
                             }
                             ok(cudaMemcpy(ycsr.data(), b_y32c.p, P * 4, cudaMemcpyDeviceToHost));
                             ok(cudaMemcpy(ycsc.data(), b_y32s.p, P * 4, cudaMemcpyDeviceToHost));
                             ok(cudaMemcpy(yd32.data(), b_d32.p, P * 4, cudaMemcpyDeviceToHost));
-                            ok(cudaMemcpy(yref.data(), b_ref.p, P * 8, cudaMemcpyDeviceToHost));
+                            ok(cudaMemcpy(yref_r.data(), b_ref_r.p, P * 8, cudaMemcpyDeviceToHost));
                             ok(cudaMemcpy(ymag.data(), b_mag.p, P * 8, cudaMemcpyDeviceToHost));
+                            ok(cudaMemcpy(yref.data(), b_ref.p, P * 8, cudaMemcpyDeviceToHost));
                             ok(cudaMemcpy(yi2c.data(), b_i2c.p, P * 8, cudaMemcpyDeviceToHost));
+                            ok(cudaMemcpy(y64c.data(), b_y64c.p, P * 8, cudaMemcpyDeviceToHost));
+                            ok(cudaMemcpy(y64s.data(), b_y64s.p, P * 8, cudaMemcpyDeviceToHost));
                             spconv_csr_free(tcsc);
                             spconv_csr_free(tc);
                             if (e != cudaSuccess || r1 != SPCONV_OK) {
@@ -555,29 +574,41 @@ int spconv_run_verification(int64_t max_dim, int seeds, uint64_t base_seed, int 
                                 break;
                             }
                             ++conv_cases;
-                            double dev = 0.0, rel = 0.0, ldev = 0.0;
-                            bool exact = true;
+                            // fp64 leg: the reference's deviations (its report's max_conv_dev /
+                            // max_layout_dev, both 0 on the reference's own grid)
+                            double dev = 0.0, ldev = 0.0;
                             for (int64_t t = 0; t < P; ++t) {
+                                dev = std::max(dev, std::fabs(y64c[t] - yref[t]));
+                                dev = std::max(dev, std::fabs(y64s[t] - yref[t]));
                                 dev = std::max(dev, std::fabs(yi2c[t] - yref[t]));
-                                const double d32 = std::fabs((double)ycsr[t] - yref[t]);
-                                dev = std::max(dev, std::max(d32, std::fabs((double)ycsc[t] - yref[t])));
-                                if (ymag[t] > 0) rel = std::max(rel, d32 / ymag[t]);
-                                else if (d32 > 0) rel = INFINITY;
-                                ldev = std::max(ldev, std::fabs((double)ycsr[t] - (double)ycsc[t]));
-                                exact &= std::memcmp(&ycsr[t], &yd32[t], 4) == 0;
+                                dev = std::max(dev, std::fabs(y64c[t] - yi2c[t]));
+                                ldev = std::max(ldev, std::fabs(y64c[t] - y64s[t]));
                             }
                             max_conv_dev = std::max(max_conv_dev, dev);
-                            max_rel_dev = std::max(max_rel_dev, rel);
                             max_layout_dev = std::max(max_layout_dev, ldev);
-                            double cdev = 0.0;
-                            for (int64_t t = 0; t < P; ++t) cdev = std::max(cdev, std::fabs(yi2c[t] - yref[t]));
-                            if (cdev > conv_tol || rel > f32_tol)
-                                fail("convolution mismatch (dev " + fmt17(dev) + ", rel " + fmt17(rel) + ") for " +
-                                     ss + " seed " + std::to_string(sd));
-                            if (!exact) fail("sparse != fp32 direct_conv for " + ss + " seed " + std::to_string(sd));
+                            if (dev > conv_tol)
+                                fail("convolution mismatch (dev " + fmt17(dev) + ") for " + ss + " seed " +
+                                     std::to_string(sd));
                             if (ldev > 0.0)
                                 fail("CSR/CSC mismatch (dev " + fmt17(ldev) + ") for " + ss + " seed " +
                                      std::to_string(sd));
+                            // fp32 leg: bit-equal to the fp32 direct_conv, CSR == CSC, and within
+                            // f32_tol * sum|w*a| of the fp64 result on the same rounded data
+                            double rel = 0.0;
+                            bool exact = true, same = true;
+                            for (int64_t t = 0; t < P; ++t) {
+                                const double d32 = std::fabs((double)ycsr[t] - yref_r[t]);
+                                if (ymag[t] > 0) rel = std::max(rel, d32 / ymag[t]);
+                                else if (d32 > 0) rel = INFINITY;
+                                exact &= std::memcmp(&ycsr[t], &yd32[t], 4) == 0;
+                                same &= std::memcmp(&ycsr[t], &ycsc[t], 4) == 0;
+                            }
+                            max_rel_dev = std::max(max_rel_dev, rel);
+                            if (rel > f32_tol)
+                                fail("fp32 convolution deviation (rel " + fmt17(rel) + ") for " + ss + " seed " +
+                                     std::to_string(sd));
+                            if (!exact) fail("sparse != fp32 direct_conv for " + ss + " seed " + std::to_string(sd));
+                            if (!same) fail("fp32 CSR/CSC mismatch for " + ss + " seed " + std::to_string(sd));
                         }
                         if (fails.size() >= max_failures) stop = true;
                     }

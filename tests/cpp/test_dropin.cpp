@@ -231,6 +231,38 @@ int main() {
         },
         "spmv: matrix has 4 columns but vector has 3 elements");
 
+    // The reference's own kernels (random_normal_kernel: doubles fp32 cannot
+    // hold) keep their exact values: an interior row of a k3 s1 p1 transform
+    // stores the 9 taps bit for bit, the text prints them with %.17g, and
+    // convolve equals the fp64 direct_conv bit for bit (same tap order).
+    {
+        const ConvSpec spec(6, 5, 3, 1, 1);
+        const Kernel kern = random_normal_kernel(3, 77);
+        const Transform t = build_transform(kern, spec);
+        const index_t r = 1 * 5 + 2;  // output (1, 2): all 9 taps land
+        CHECK(t.matrix.ptr()[r + 1] - t.matrix.ptr()[r] == 9);
+        for (int q = 0; q < 9; ++q) CHECK(t.matrix.val()[t.matrix.ptr()[r] + q] == kern.values[q]);
+        std::ostringstream os;
+        write_transform(os, t);
+        CHECK(os.str().find(" " + format_value(kern.values[4]) + "\n") != std::string::npos);
+        const Grid a = random_normal_grid(6, 5, 78);
+        CHECK(convolve(t, a).values == direct_conv(a, kern, spec).values);
+        std::istringstream is(os.str());
+        const Transform back = read_transform(is);
+        CHECK(back.matrix.val() == t.matrix.val());
+        // grid text round trip (inc/grid.hpp:54-89)
+        std::ostringstream gs;
+        write_grid(gs, a);
+        std::istringstream gi(gs.str());
+        CHECK(read_grid(gi).values == a.values);
+    }
+    expect_throw<std::runtime_error>(
+        [] {
+            std::istringstream is("2 2\n1 2 3\n");
+            read_grid(is);
+        },
+        "read_grid: expected 4 values, got 3");
+
     if (g_fail) {
         std::fprintf(stderr, "%d failure(s)\n", g_fail);
         return 1;

@@ -141,3 +141,42 @@ def test_read_reference_written_file(ref, orc):
     rev = b"\n".join(head) + b"\n" + b"\n".join(reversed(body.strip().split(b"\n"))) + b"\n"
     r2 = sp.read_transform(rev)
     assert np.array_equal(r2.export()[1], idx)
+
+
+def _glibc_g17(v):
+    import ctypes
+    libc = ctypes.CDLL(None)
+    buf = ctypes.create_string_buffer(64)
+    libc.snprintf(buf, 64, b"%.17g", ctypes.c_double(v))
+    return buf.value.decode()
+
+
+def test_format_g17_f64_matches_glibc():
+    """The fp64 renderer (values a handle keeps exactly, spconv_format_g17 --
+    the same code the device text writer runs) == glibc's %.17g, the
+    reference's format_value (inc/grid.hpp:54-59): random bit patterns over
+    the whole range, subnormals, the extremes, powers of ten and their
+    neighbours, exact decimal ties, the fixed/exponent switches."""
+    sp = _sp()
+    rng = np.random.default_rng(1)
+    vals = list(rng.integers(0, 2**64, 20000, dtype=np.uint64).view(np.float64))
+    vals += list(rng.standard_normal(5000)) + list(rng.standard_normal(2000) * 1e-300)
+    vals += list(rng.integers(1, 2**52, 2000, dtype=np.uint64).view(np.float64))  # subnormals
+    for e in range(-325, 309):
+        p = float(f"1e{e}")
+        vals += [p, np.nextafter(p, 0), np.nextafter(p, np.inf)]
+    vals += [5e-324, 2.2250738585072014e-308, 2.225073858507201e-308, 1.7976931348623157e308,
+             0.0, -0.0, 1e-4, 9.9999999999999995e-5, 1e17, 99999999999999984.0, 1e16, 0.5, 2.5,
+             0.1, 1 / 3, 2.0**-1074, 2.0**-1022, 2.0**1023, 123456789012345678.0, 9007199254740993.0]
+    vals += [float(x) for x in range(1, 3000, 7)] + [x / 64 for x in range(-500, 500, 3)]
+    bad = []
+    for v in vals:
+        v = float(v)
+        if v != v or v in (float("inf"), float("-inf")):
+            continue
+        g, w = sp.format_g17(v), _glibc_g17(v)
+        if g != w:
+            bad.append((v.hex(), g, w))
+    assert not bad, bad[:10]
+    for v, w in [(float("inf"), "inf"), (float("-inf"), "-inf"), (float("nan"), "nan"), (-float("nan"), "-nan")]:
+        assert sp.format_g17(v) == w == _glibc_g17(v)
