@@ -738,6 +738,7 @@ int spconv_build_csr(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
     bp.col_idx = h->col_idx;
     bp.vals = h->vals;
     bp.taps_out = h->taps;
+    bp.nnz_total = ht.nnz;
     {
         const char* bs = std::getenv("SPCONV_B200_BULK_STORE");
         bp.bulk_store = bs ? std::atoi(bs) : 1;

@@ -24,6 +24,7 @@
 // counts finishes row_ptr.  Entries are staged in shared memory at the global
 // offset's alignment and written back with 16-byte streaming stores, so HBM
 // sees each of the 8*nnz + 4*(rows+1) bytes exactly once.
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 
@@ -350,6 +351,153 @@ __global__ void __launch_bounds__(256) csr_build_warp(const BuildParams P) {
     }
 }
 
+// Persistent, double-buffered variant (unrolled k, staged): a grid of a few
+// CTAs per SM walks tiles of 256 rows.  Every row's global offset is closed
+// form -- sum_j W[j] * #{x' < x : j in J(x')} + sum_i nzcol(x, i) *
+// #{y' < y : i in I(y')}, the slide counts from per-tap [lo, hi) tables in
+// shared memory -- so there is no scan: a tile costs two CTA barriers, and
+// the TMA bulk store of tile t drains while tile t + 1 is generated in the
+// other staging buffer.
+template <int KC, bool DENSE>
+__global__ void __launch_bounds__(256) csr_build_persist(const BuildParams P) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int K1 = KC + 1, KK = KC * KC, R = 256;
+    constexpr int STAGE = (R * KK + 3 + 3) & ~3;  // words per staging array
+    const int t = threadIdx.x;
+    __shared__ int32_t s_sat[K1 * K1];
+    __shared__ float s_taps[KK];
+    __shared__ long long s_w[KC];
+    __shared__ int s_xlo[KC], s_xhi[KC], s_ylo[KC], s_yhi[KC];
+    for (int q = t; q < K1 * K1; q += R) s_sat[q] = P.small ? P.tab.sat[q] : __ldg(P.t.sat + q);
+    for (int q = t; q < KK; q += R) s_taps[q] = P.small ? P.tab.taps[q] : __ldg(P.t.taps + q);
+    for (int q = t; q < KC; q += R) {
+        s_w[q] = P.small ? P.tab.w[q] : __ldg(P.t.w + q);
+        // x' with tap q in J(x'): [xlo, xhi) (slides_before(x, q) = clamp(x, xlo, xhi) - xlo)
+        s_xlo[q] = (P.p - q <= 0) ? 0 : (P.p - q + P.s - 1) / P.s;
+        s_xhi[q] = max(s_xlo[q], (P.m + P.p - q - 1 < 0) ? 0 : (P.m + P.p - q - 1) / P.s + 1);
+        s_ylo[q] = (P.p - q <= 0) ? 0 : (P.p - q + P.s - 1) / P.s;
+        s_yhi[q] = max(s_ylo[q], (P.n + P.p - q - 1 < 0) ? 0 : (P.n + P.p - q - 1) / P.s + 1);
+    }
+    __syncthreads();
+    if (blockIdx.x == 0 && P.taps_out)
+        for (int q = t; q < KK; q += R) P.taps_out[q] = s_taps[q];
+
+    // global offset of row (x, y) and its entry count
+    auto row_offset = [&](int x, int y, int& cnt, int& jlo, int& jhi, int& ilo, int& ihi) -> int {
+        tap_range(x, P.m, KC, P.s, P.p, jlo, jhi);
+        tap_range(y, P.n, KC, P.s, P.p, ilo, ihi);
+        cnt = DENSE ? (jhi - jlo) * (ihi - ilo) : sat_rect(s_sat, K1, jlo, jhi, ilo, ihi);
+        long long off = 0;
+#pragma unroll
+        for (int q = 0; q < KC; ++q) {
+            const int sx = max(0, min(x, s_xhi[q]) - s_xlo[q]);
+            const int sy = max(0, min(y, s_yhi[q]) - s_ylo[q]);
+            const int nzc = DENSE ? (jhi - jlo) : sat_rect(s_sat, K1, jlo, jhi, q, q + 1);
+            off += s_w[q] * sx + (long long)nzc * sy;
+        }
+        return (int)off;
+    };
+
+    const int ntiles = (P.rows + R - 1) / R;
+    __shared__ int s_base[2], s_end[2];
+    int it = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        const int buf = it & 1;
+        int32_t* dcol = reinterpret_cast<int32_t*>(smem) + buf * 2 * STAGE;
+        float* dval = reinterpret_cast<float*>(dcol + STAGE);
+        const int r0 = tile * R;
+        const int r1 = min(P.rows, r0 + R);
+        // this thread's row: closed-form offset, written to row_ptr now
+        const int r = r0 + t;
+        int x = 0, y = 0, cnt = 0, off = 0, jlo = 0, jhi = 0, ilo = 0, ihi = 0;
+        if (r < r1) {
+            x = r / P.no;
+            y = r - x * P.no;
+            off = row_offset(x, y, cnt, jlo, jhi, ilo, ihi);
+            P.row_ptr[r] = off;
+            if (r == P.rows - 1) P.row_ptr[P.rows] = off + cnt;
+        }
+        // the tile's [base, end): row r0's offset and row (r1 - 1)'s end
+        if (t == 0) {
+            s_base[buf] = off;
+            bulk_wait_read<1>();  // this buffer's bulk store of two tiles ago has read it
+        }
+        if (r == r1 - 1) s_end[buf] = off + cnt;
+        __syncthreads();
+        const int base = s_base[buf], total = s_end[buf] - base;
+        const int mis = base & 3;
+        if (r < r1) {
+            int o = mis + off - base;
+            const int xr = P.s * x - P.p, yc = P.s * y - P.p;
+            if (DENSE && cnt == KK) {
+#pragma unroll
+                for (int j = 0; j < KC; ++j)
+#pragma unroll
+                    for (int i = 0; i < KC; ++i) {
+                        dcol[o + j * KC + i] = (xr + j) * P.n + yc + i;
+                        dval[o + j * KC + i] = s_taps[j * KC + i];
+                    }
+            } else {
+#pragma unroll
+                for (int j = 0; j < KC; ++j) {
+                    const int rowbase = (xr + j) * P.n + yc;
+                    const bool jin = j >= jlo && j < jhi;
+#pragma unroll
+                    for (int i = 0; i < KC; ++i) {
+                        const float v = s_taps[j * KC + i];
+                        const bool keep = jin && i >= ilo && i < ihi && (DENSE || v != 0.0f);
+                        if (keep) {
+                            dcol[o] = rowbase + i;
+                            dval[o] = v;
+                        }
+                        o += keep ? 1 : 0;
+                    }
+                }
+            }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        const int head = min(total, (4 - mis) & 3);
+        if (t < head) {
+            __stcs(P.col_idx + base + t, dcol[mis + t]);
+            __stcs(P.vals + base + t, dval[mis + t]);
+        }
+        const int nvec = (total - head) >> 2;
+        if (t == 0) {
+            if (nvec > 0) {
+                bulk_s2g(P.col_idx + base + head, dcol + mis + head, (uint32_t)nvec * 16u);
+                bulk_s2g(P.vals + base + head, dval + mis + head, (uint32_t)nvec * 16u);
+            }
+            bulk_commit();
+        }
+        const int done = head + 4 * nvec;
+        if (t < total - done) {
+            __stcs(P.col_idx + base + done + t, dcol[mis + done + t]);
+            __stcs(P.vals + base + done + t, dval[mis + done + t]);
+        }
+    }
+    if (t == 0) bulk_wait_read<0>();
+}
+
+template <int KC, bool DENSE>
+static cudaError_t launch_p(const BuildParams& bp, cudaStream_t st) {
+    constexpr int KK = KC * KC;
+    const size_t smem = (size_t)((256 * KK + 3 + 3) & ~3) * 4 * 2 * 2;  // 2 buffers x (col, val)
+    int dev = 0, sms = 148, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t e = cudaSuccess;
+    if (smem > 48 * 1024)
+        e = cudaFuncSetAttribute(csr_build_persist<KC, DENSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, csr_build_persist<KC, DENSE>, 256, smem);
+    if (e != cudaSuccess) return e;
+    const long long tiles = ((long long)bp.rows + 255) / 256;
+    const long long grid = std::min<long long>(tiles, (long long)sms * std::max(per_sm, 1));
+    csr_build_persist<KC, DENSE><<<(unsigned)grid, 256, smem, st>>>(bp);
+    return cudaGetLastError();
+}
+
 template <int KC, bool DENSE>
 static cudaError_t launch_w(BuildParams bp, cudaStream_t st) {
     constexpr int KK = KC * KC;
@@ -387,12 +535,25 @@ static cudaError_t launch_k(const BuildParams& bp, int block, size_t smem, cudaS
 
 cudaError_t launch_csr_build(const BuildParams& bp, bool dense, int block, size_t smem,
                              cudaStream_t st) {
-    // The block kernel for every k: with TMA bulk stores and the unpredicated
-    // interior fill it beats the warp-local variant at config 4 too (254 vs
-    // 283 us; config 3 25.6 vs 27.7 us; profiles/r01_choices).
-    // SPCONV_B200_BUILD=warp selects the warp-local kernel.
+    // Default: the persistent double-buffered kernel for k <= 5 (config 3
+    // build 22.5 -> 18.4 us, config 2 12.3 -> 10.2 us), the block kernel for
+    // larger k, whose 256-row double buffer would not leave room for a second
+    // CTA per SM (config 4: block 252 us, persistent 297 us; the block kernel
+    // also beats the warp-local one, 254 vs 283 us, profiles/r01_choices).
+    // SPCONV_B200_BUILD=block | warp | persist forces a kernel.
     const char* bsel = std::getenv("SPCONV_B200_BUILD");
     const bool warp_build = bsel && !std::strcmp(bsel, "warp");
+    const bool block_build = bsel && !std::strcmp(bsel, "block");
+    const bool persist_build = (bsel && !std::strcmp(bsel, "persist")) || (!warp_build && !block_build && bp.k <= 5);
+    if (persist_build && bp.stage) {
+        switch (bp.k) {
+            case 1: return dense ? launch_p<1, true>(bp, st) : launch_p<1, false>(bp, st);
+            case 3: return dense ? launch_p<3, true>(bp, st) : launch_p<3, false>(bp, st);
+            case 5: return dense ? launch_p<5, true>(bp, st) : launch_p<5, false>(bp, st);
+            case 7: return dense ? launch_p<7, true>(bp, st) : launch_p<7, false>(bp, st);
+            default: break;
+        }
+    }
     if (warp_build) {
         switch (bp.k) {
             case 1: return dense ? launch_w<1, true>(bp, st) : launch_w<1, false>(bp, st);

@@ -44,6 +44,7 @@ struct BuildParams {
     float* vals;
     float* taps_out;  // k*k taps copied here by block 0 (the handle's device tap table)
     int bulk_store;   // write staged entries back with TMA bulk stores (else 16-byte st.global)
+    long long nnz_total;  // total entries (the persistent build's last-tile bound)
 };
 
 // CSC build (csc_build.cu): the conv transform stored column-major.

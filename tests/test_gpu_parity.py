@@ -483,9 +483,9 @@ def test_band_check_reads_the_matrix(sp, orc, torch_cuda, spec, check, monkeypat
 
 
 @pytest.mark.parametrize("bulk_store", ["0", "1"])
-@pytest.mark.parametrize("variant", ["block", "warp"])
+@pytest.mark.parametrize("variant", ["block", "warp", "persist"])
 def test_build_variants_bitexact(sp, orc, variant, bulk_store, monkeypatch):
-    """Both CSR build kernels (block scan / warp-local, SPCONV_B200_BUILD), with
+    """The CSR build kernels (block scan / warp-local / persistent, SPCONV_B200_BUILD), with
     the staged entries written back by TMA bulk stores or by 16-byte stores
     (SPCONV_B200_BULK_STORE), give the oracle's arrays for every unrolled k,
     dense and zero-tap kernels; so does the CSC build."""
