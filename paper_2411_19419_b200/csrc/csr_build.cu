@@ -544,7 +544,8 @@ cudaError_t launch_csr_build(const BuildParams& bp, bool dense, int block, size_
     const char* bsel = std::getenv("SPCONV_B200_BUILD");
     const bool warp_build = bsel && !std::strcmp(bsel, "warp");
     const bool block_build = bsel && !std::strcmp(bsel, "block");
-    const bool persist_build = (bsel && !std::strcmp(bsel, "persist")) || (!warp_build && !block_build && bp.k <= 5);
+    const bool persist_build =
+        (bsel && !std::strcmp(bsel, "persist")) || (!bsel && bp.k <= 5);
     if (persist_build && bp.stage) {
         switch (bp.k) {
             case 1: return dense ? launch_p<1, true>(bp, st) : launch_p<1, false>(bp, st);
