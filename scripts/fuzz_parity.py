@@ -1,7 +1,9 @@
 #!/usr/bin/env python
 """Randomised GPU parity fuzzing (a long-running complement to tests/):
 random geometries (m, n up to 300, k up to 11, s up to 4, p up to k), dense /
-zero-tap / non-finite kernels, CSR and CSC layouts, batches 1-9 through the
+zero-tap / non-finite kernels and the reference's own double taps (exact
+fp64 values: export and the fp64 apply checked bit for bit), every build
+kernel, CSR and CSC layouts, batches 1-9 through the
 default path and every forced path, padded ldx, the fused and two-kernel band
 forms; every output compared BIT-EXACTLY with the oracle's ordered-fmaf
 restatement and every matrix with the oracle's build.
@@ -45,32 +47,48 @@ def main():
         n = int(rng.choice([int(rng.integers(max(1, k - 2 * p), 300)), 4 * int(rng.integers(1, 70))]))
         if orc.spec_check(m, n, k, s, p):
             continue
-        kern = rng.standard_normal(k * k).astype(np.float32)
+        kern64 = rng.standard_normal(k * k)  # mode 2: the reference's own double taps
+        kern = kern64.astype(np.float32)
         mode = rng.integers(0, 10)
         if mode == 0:
             kern[rng.random(k * k) < 0.3] = 0.0
         elif mode == 1:
             kern[rng.integers(0, k * k)] = np.nan
+        if mode != 2:
+            kern64 = kern.astype(np.float64)
         batch = int(rng.integers(1, 10))
         X = rng.standard_normal((batch, m * n)).astype(np.float32)
         if rng.random() < 0.1:
             X[0, rng.integers(0, m * n)] = np.inf
         layout = sp.Layout.CSC if rng.random() < 0.25 else sp.Layout.CSR
         spec = sp.ConvSpec(m, n, k, s, p)
-        t = sp.build_transform(sp.Kernel(k, kern.astype(np.float64)), spec, layout=layout)
+        build = str(rng.choice(["", "", "block", "warp", "persist"]))
+        if build:
+            os.environ["SPCONV_B200_BUILD"] = build
+        try:
+            t = sp.build_transform(sp.Kernel(k, kern64), spec, layout=layout)
+        finally:
+            os.environ.pop("SPCONV_B200_BUILD", None)
         rp, ri, rv = orc.build_native(m, n, k, s, p, kern)
         ptr = np.empty(t.rows + 1, np.int32)
         idx = np.empty(max(t.nnz, 1), np.int32)
         val = np.empty(max(t.nnz, 1), np.float32)
+        p64, i64, v64 = orc.build_transform(m, n, k, s, p, kern64)  # exact doubles
         if layout == sp.Layout.CSR:
-            t.copy_native(ptr, idx, val)
+            t.copy_native(ptr, idx, val)  # the fp32 arrays the kernels read
             ok = np.array_equal(ptr, rp) and np.array_equal(idx[:t.nnz], ri) and np.array_equal(
                 bits(val[:t.nnz]), bits(rv))
+            wp, wi, wv = p64, i64, v64
         else:
-            cp, ci, cv = t.export()
-            p64, i64, v64 = orc.build_transform(m, n, k, s, p, kern.astype(np.float64))
             wp, wi, wv = orc.transpose(t.rows, t.cols, p64, i64, v64)
-            ok = np.array_equal(cp, wp) and np.array_equal(ci, wi) and np.array_equal(bits(cv), bits(wv))
+        gp, gi, gv = t.export()
+        nz = int(wp[-1])
+        ok = ok if layout == sp.Layout.CSR else True
+        ok = ok and np.array_equal(gp, wp) and np.array_equal(gi[:nz], wi) and np.array_equal(
+            np.nan_to_num(gv[:nz], nan=7.0).view(np.uint64), np.nan_to_num(wv, nan=7.0).view(np.uint64))
+        if mode == 2 and ok:  # fp64 apply with the exact values == the oracle's fp64 restatement
+            y64 = sp.spmm_f64(t, torch.from_numpy(X[:1].astype(np.float64)).cuda()).cpu().numpy()[0]
+            ok = np.array_equal(y64.view(np.uint64), orc.spmv_f64(p64, i64, v64, X[0].astype(np.float64)).view(np.uint64))
         want = orc.spmm_native(rp, ri, rv, X)
         pad = int(rng.choice([0, 0, 4]))
         Xd = torch.zeros(batch, m * n + pad, device="cuda")
@@ -100,7 +118,7 @@ def main():
         cases += 1
         if not (ok and ok_y):
             fails += 1
-            print("FAIL", (m, n, k, s, p), "mode", int(mode), "batch", batch, "layout", layout, "env", env,
+            print("FAIL", (m, n, k, s, p), "mode", int(mode), "build", build, "batch", batch, "layout", layout, "env", env,
                   "matrix_ok", ok, "y_ok", ok_y, "kernel", t.last_kernel, flush=True)
         t.close()
     print(f"fuzz: {cases} cases, {fails} failures (seed {seed}, {secs:.0f} s)")
