@@ -542,6 +542,7 @@ cudaError_t launch_csr_build(const BuildParams& bp, bool dense, int block, size_
     // also beats the warp-local one, 254 vs 283 us, profiles/r01_choices).
     // SPCONV_B200_BUILD=block | warp | persist forces a kernel.
     const char* bsel = std::getenv("SPCONV_B200_BUILD");
+    if (bsel && !*bsel) bsel = nullptr;  // empty = unset
     const bool warp_build = bsel && !std::strcmp(bsel, "warp");
     const bool block_build = bsel && !std::strcmp(bsel, "block");
     const bool persist_build =
