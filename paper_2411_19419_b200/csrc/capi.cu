@@ -288,11 +288,28 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
     const bool band_geom = h->is_conv && h->band_tw > 0 && tma_ok;
     if (force == kBanded && !band_geom)
         return fail(SPCONV_EINVAL, "SPCONV_B200_PATH=banded: geometry unsupported");
-    if (band_geom && (force == kBanded || (force == kAuto && h->taps_dense))) {
+    // The blocked apply needs finite taps; exact-zero taps (not stored) take
+    // the masked (ZT) instantiations: k <= 7, so the mask fits 64 bits.
+    // (stored = the DOUBLE tap is non-zero when the handle has double taps: a
+    // tap that narrows to 0.0f is still an entry, applied as w = 0)
+    bool taps_finite = !h->host_taps.empty(), any_nz = false;
+    unsigned long long nzmask = 0;
+    for (size_t q = 0; q < h->host_taps.size(); ++q) {
+        taps_finite &= std::isfinite(h->host_taps[q]);
+        const bool stored = h->host_taps64.empty() ? h->host_taps[q] != 0.0f : h->host_taps64[q] != 0.0;
+        if (stored) {
+            any_nz = true;
+            if (q < 64) nzmask |= 1ull << q;
+        }
+    }
+    const bool band_taps = h->taps_dense || (taps_finite && any_nz && g.k <= 7);
+    if (band_geom && (force == kBanded || (force == kAuto && band_taps))) {
         const int sms = device_sm_count();
         spb::BandShape sh{};
         spb::BandParams bp{};
         bp.p = (int)g.p;
+        bp.zt = band_taps && !h->taps_dense ? 1 : 0;
+        bp.nzmask = nzmask;
         CK(spb::launch_band((int)g.k, (int)g.s, bp, nullptr, st, &sh, sms));
         bp.row_ptr = h->row_ptr;
         bp.col_idx = h->col_idx;
@@ -310,7 +327,7 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
         bp.no = (int)g.no;
         bp.tiles_y = (int)((g.no + sh.tw - 1) / sh.tw);
         bp.tiles = (int)(((g.mo + sh.th - 1) / sh.th) * bp.tiles_y);
-        bp.fast_allowed = h->taps_dense ? 1 : 0;
+        bp.fast_allowed = band_taps ? 1 : 0;
         bp.sy = (int)h->sy;
         bp.nnz = (int)h->nnz;
         const int cpt = sh.tw / 32;
@@ -339,11 +356,10 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
         // 376 us.  With a heavier matrix the producer's checks starve the
         // pipeline (config 4 at 64 images: 1,043 -> 1,531 us), so the check
         // stays a kernel of its own (profiles/r01v/exp.txt).
-        // SPCONV_B200_FUSED=0|1 overrides; the blocked path needs finite,
-        // non-zero taps.
+        // SPCONV_B200_FUSED=0|1 overrides; the blocked path needs finite taps.
         const char* fsel = std::getenv("SPCONV_B200_FUSED");
         const bool light = 8.0 * (double)h->nnz < 0.1 * 4.0 * (double)batch * (double)(h->rows + h->cols);
-        bp.fused = !side && h->taps_dense && (fsel ? !std::strcmp(fsel, "1") : light) ? 1 : 0;
+        bp.fused = !side && band_taps && (fsel ? !std::strcmp(fsel, "1") : light) ? 1 : 0;
         if (bp.fused) {
             const cudaError_t fe = spb::launch_band((int)g.k, (int)g.s, bp, &tmap, st, nullptr, sms);
             if (fe == cudaSuccess) {

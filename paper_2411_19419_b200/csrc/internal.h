@@ -100,6 +100,8 @@ struct BandParams {
     int sy;            // sum over output columns y of cy(y) (closed-form row starts)
     int nnz;
     int fused;         // host: launch the fused check + apply (+ fixup) instead of two kernels
+    int zt;            // some taps are exact zeros (not stored): masked footprint + checks
+    unsigned long long nzmask;  // bit j*k+i: tap (j, i) is non-zero (zt; k <= 7)
 };
 
 struct BandShape {

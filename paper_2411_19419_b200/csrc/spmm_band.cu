@@ -157,7 +157,11 @@ struct SegGeom {
     bool valid;
 };
 
-template <int K, int S, int TW>
+// ZT: the taps include exact zeros (not stored; bit j*K+i of P.nzmask marks
+// the non-zero ones).  The footprint is then the Theorem 2.1 prefix over the
+// mask: S0 = sum_j W[j] * slides_before(x, j) + sum_i nzcol(i) * slides_before(y0, i)
+// with W[j] = sum_i nz[j][i] * #{y : i lands}, nzcol(i) = sum_{j in J(x)} nz[j][i].
+template <int K, int S, int TW, bool ZT>
 __device__ __forceinline__ SegGeom seg_geom(const BandParams& P, long long seg) {
     SegGeom g;
     g.x = (int)(seg / P.tiles_y);
@@ -165,10 +169,36 @@ __device__ __forceinline__ SegGeom seg_geom(const BandParams& P, long long seg) 
     g.nr = min(TW, P.no - g.y0);
     g.r0 = g.x * P.no + g.y0;
     tap_range_dev(g.x, P.m, K, S, P.p, g.jlo, g.jhi);
-    g.cy0 = cum_taps<K, S>(g.y0, P.n, P.p);
-    g.S0 = (long long)cum_taps<K, S>(g.x, P.m, P.p) * P.sy + (long long)(g.jhi - g.jlo) * g.cy0;
-    g.L = (g.jhi - g.jlo) * (cum_taps<K, S>(g.y0 + g.nr, P.n, P.p) - g.cy0);
-    g.valid = g.S0 + g.L <= (long long)P.nnz;  // (zero taps: the prediction runs past the end)
+    if (!ZT) {
+        g.cy0 = cum_taps<K, S>(g.y0, P.n, P.p);
+        g.S0 = (long long)cum_taps<K, S>(g.x, P.m, P.p) * P.sy + (long long)(g.jhi - g.jlo) * g.cy0;
+        g.L = (g.jhi - g.jlo) * (cum_taps<K, S>(g.y0 + g.nr, P.n, P.p) - g.cy0);
+    } else {
+        const unsigned long long mk = P.nzmask;
+        long long s0 = 0;
+        int len = 0;
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            long long wj = 0;
+#pragma unroll
+            for (int i = 0; i < K; ++i)
+                if ((mk >> (j * K + i)) & 1ull) wj += slides_before(P.no, i, P.n, S, P.p);
+            s0 += wj * slides_before(g.x, j, P.m, S, P.p);
+        }
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            int nzc = 0;
+#pragma unroll
+            for (int j = 0; j < K; ++j) nzc += (j >= g.jlo && j < g.jhi && ((mk >> (j * K + i)) & 1ull)) ? 1 : 0;
+            const int b0 = slides_before(g.y0, i, P.n, S, P.p);
+            s0 += (long long)nzc * b0;
+            len += nzc * (slides_before(g.y0 + g.nr, i, P.n, S, P.p) - b0);
+        }
+        g.cy0 = 0;
+        g.S0 = s0;
+        g.L = len;
+    }
+    g.valid = g.S0 + g.L <= (long long)P.nnz;  // (a matrix that is not this transform may run past the end)
     return g;
 }
 
@@ -195,7 +225,7 @@ __device__ __forceinline__ void seg_issue(const BandParams& P, const SegGeom& g,
 // scan of cx * cy(y)), then every row checked from shared memory -- interior
 // rows with the fully unrolled k*k compare, clipped rows over their tap
 // range.  Returns the verdict (warp-uniform).
-template <int K, int S, int TW>
+template <int K, int S, int TW, bool ZT>
 __device__ __forceinline__ bool seg_verify(const BandParams& P, const SegGeom& g, const int* rp,
                                            const uint32_t (&w)[K * K], const uint32_t* s_w, int lane) {
     using C = CheckCfg<K, S, TW>;
@@ -203,13 +233,28 @@ __device__ __forceinline__ bool seg_verify(const BandParams& P, const SegGeom& g
     const int* cb = rp + C::RPW;
     const uint32_t* vb = reinterpret_cast<const uint32_t*>(cb + C::BUFW);
     const int cx = g.jhi - g.jlo;
+    const unsigned long long mk = ZT ? P.nzmask : 0ull;
+    int nzc[K];  // ZT: stored taps per tap column i over this segment's J(x)
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+        nzc[i] = 0;
+        if (ZT)
+#pragma unroll
+            for (int j = 0; j < K; ++j) nzc[i] += (j >= g.jlo && j < g.jhi && ((mk >> (j * K + i)) & 1ull)) ? 1 : 0;
+    }
     int off[RPL], ilo_[RPL], ihi_[RPL];
     int run = 0;
 #pragma unroll
     for (int q = 0; q < RPL; ++q) {
         const int l = lane + 32 * q;
         tap_range_dev(g.y0 + l, P.n, K, S, P.p, ilo_[q], ihi_[q]);
-        const int c = l < g.nr ? cx * (ihi_[q] - ilo_[q]) : 0;
+        int rc = cx * (ihi_[q] - ilo_[q]);
+        if (ZT) {
+            rc = 0;
+#pragma unroll
+            for (int i = 0; i < K; ++i) rc += (i >= ilo_[q] && i < ihi_[q]) ? nzc[i] : 0;
+        }
+        const int c = l < g.nr ? rc : 0;
         int inc = c;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -236,7 +281,26 @@ __device__ __forceinline__ bool seg_verify(const BandParams& P, const SegGeom& g
             const int rb = (S * g.x - P.p) * P.n + (S * y - P.p);
             const int* cl = cbs + off[q];
             const uint32_t* vl = vbs + off[q];
-            if (cx == K && ilo == 0 && ihi == K) {
+            if (ZT) {  // stored taps only, in (j, i) order
+                int e = 0;
+                if (cx == K && ilo == 0 && ihi == K) {
+#pragma unroll
+                    for (int j = 0; j < K; ++j)
+#pragma unroll
+                        for (int ii = 0; ii < K; ++ii)
+                            if ((mk >> (j * K + ii)) & 1ull) {
+                                bad |= (uint32_t)(cl[e] - (rb + j * P.n + ii)) | (vl[e] ^ w[j * K + ii]);
+                                ++e;
+                            }
+                } else {
+                    for (int j = g.jlo; j < g.jhi; ++j)
+                        for (int ii = ilo; ii < ihi; ++ii)
+                            if ((mk >> (j * K + ii)) & 1ull) {
+                                bad |= (uint32_t)(cl[e] - (rb + j * P.n + ii)) | (vl[e] ^ s_w[j * K + ii]);
+                                ++e;
+                            }
+                }
+            } else if (cx == K && ilo == 0 && ihi == K) {
 #pragma unroll
                 for (int j = 0; j < K; ++j)
 #pragma unroll
@@ -254,7 +318,7 @@ __device__ __forceinline__ bool seg_verify(const BandParams& P, const SegGeom& g
     return __all_sync(0xffffffffu, ok);
 }
 
-template <int K, int S, int TW>
+template <int K, int S, int TW, bool ZT>
 __global__ void __launch_bounds__(CheckCfg<K, S, TW>::WARPS * 32) conv_band_check(const BandParams P) {
     using C = CheckCfg<K, S, TW>;
     constexpr int KK = K * K;
@@ -269,7 +333,7 @@ __global__ void __launch_bounds__(CheckCfg<K, S, TW>::WARPS * 32) conv_band_chec
     int* rp = reinterpret_cast<int*>(smem + 128 + (size_t)warp * C::WARP_BYTES);
     SegGeom g{};
     if (live) {
-        g = seg_geom<K, S, TW>(P, seg);
+        g = seg_geom<K, S, TW, ZT>(P, seg);
         if (lane == 0) {
             mbar_init(bar, 1);
             mbar_fence_init();
@@ -286,7 +350,7 @@ __global__ void __launch_bounds__(CheckCfg<K, S, TW>::WARPS * 32) conv_band_chec
 #pragma unroll
     for (int q = 0; q < KK; ++q) w[q] = s_w[q];
     mbar_wait(bar, 0);
-    const bool ok = seg_verify<K, S, TW>(P, g, rp, w, s_w, lane);
+    const bool ok = seg_verify<K, S, TW, ZT>(P, g, rp, w, s_w, lane);
     if (lane == 0) P.seg_ok[seg] = ok ? 1 : 0;
 }
 
@@ -326,7 +390,12 @@ struct ItemIter {
 // consumers take the blocked path unconditionally; conv_band_fixup, launched
 // right after on the same stream, recomputes the rows of any segment that
 // failed its check from the CSR (normally none: it only reads the flags).
-template <int K, int S, int V, int CPT, int TH, int STAGES, int DELTA, bool FUSED>
+// ZT: some taps are exact zeros.  The blocked sums still run over all k*k
+// taps: for a finite x, fmaf(0, x, acc) == acc (acc starts at +0 and is never
+// -0), so they equal the stored-taps sums bit for bit; a thread whose sums are
+// not all finite (a non-finite x it read, where 0 * inf would differ) redoes
+// its outputs per entry from the CSR.
+template <int K, int S, int V, int CPT, int TH, int STAGES, int DELTA, bool FUSED, bool ZT = false>
 __global__ void __launch_bounds__(BandCfg<K, S, V, CPT, TH, STAGES, DELTA>::THREADS, 1)
     conv_spmm_band(const __grid_constant__ CUtensorMap tmap, const BandParams P) {
     using C = BandCfg<K, S, V, CPT, TH, STAGES, DELTA>;
@@ -374,7 +443,7 @@ __global__ void __launch_bounds__(BandCfg<K, S, V, CPT, TH, STAGES, DELTA>::THRE
         uint32_t cph = 0;
         auto seg_next = [&]() {  // geometry of the next segment, copies into slice cb
             if (cseg < nseg) {
-                vg = seg_geom<K, S, C::TW>(P, cseg);
+                vg = seg_geom<K, S, C::TW, ZT>(P, cseg);
                 vseg = cseg;
                 cseg += gridDim.x;
                 if (lane == 0 && vg.valid) {
@@ -415,7 +484,7 @@ __global__ void __launch_bounds__(BandCfg<K, S, V, CPT, TH, STAGES, DELTA>::THRE
                 if (g.valid) {
                     mbar_wait(&cbar[b], (cph >> b) & 1u);
                     cph ^= 1u << b;
-                    ok = seg_verify<K, S, C::TW>(P, g, cslice + b * SLICE, w, s_w, lane);
+                    ok = seg_verify<K, S, C::TW, ZT>(P, g, cslice + b * SLICE, w, s_w, lane);
                 }
                 if (lane == 0) P.seg_ok[sg] = ok ? 1 : 0;
             } else if (I.img < P.batch) {  // all checked: wait for the next free stage
@@ -477,6 +546,7 @@ __global__ void __launch_bounds__(BandCfg<K, S, V, CPT, TH, STAGES, DELTA>::THRE
         const float* xw = xs + (size_t)st * C::SF;
         float* ybase = P.Y + (long long)img * P.ldy;
 
+        bool per_entry = !fast;
         if (fast) {
             float acc[V][CPT];
 #pragma unroll
@@ -507,11 +577,19 @@ __global__ void __launch_bounds__(BandCfg<K, S, V, CPT, TH, STAGES, DELTA>::THRE
                     }
                 }
             }
+            if (ZT) {
+                float nf = 0.0f;  // NaN iff some sum is not finite
+#pragma unroll
+                for (int v = 0; v < V; ++v)
+#pragma unroll
+                    for (int c = 0; c < CPT; ++c) nf = fmaf(0.0f, acc[v][c], nf);
+                per_entry = nf != 0.0f;
+            }
             const int ycol = y0 + CPT * lane;
 #pragma unroll
             for (int v = 0; v < V; ++v) {
                 const int x = xb + v;
-                if (x >= P.mo) continue;
+                if (per_entry || x >= P.mo) continue;
                 float* yp = ybase + (long long)x * P.no + ycol;
                 if (vec_ok && ycol + CPT <= P.no) {
                     if (CPT == 4)
@@ -526,7 +604,8 @@ __global__ void __launch_bounds__(BandCfg<K, S, V, CPT, TH, STAGES, DELTA>::THRE
                         if (ycol + c < P.no) __stcs(yp + c, acc[v][c]);
                 }
             }
-        } else {
+        }
+        if (per_entry) {
             // Per-entry loop straight from the CSR (window-relative gathers).
             const int wr0 = S * tx * TH - P.p;
             const int wc0 = S * y0 - P.p - DELTA;
@@ -612,7 +691,7 @@ cudaError_t launch_pdl(Kern kern, unsigned grid, unsigned block, size_t smem, cu
 }
 
 // Fused check + apply (conv_spmm_band<..., true>) and its fixup kernel.
-template <int K, int S, int V, int CPT, int TH, int STAGES, int DELTA>
+template <int K, int S, int V, int CPT, int TH, int STAGES, int DELTA, bool ZT>
 cudaError_t run_fused(const BandParams& bp, const CUtensorMap* tmap, cudaStream_t st, int sms) {
     using C = BandCfg<K, S, V, CPT, TH, STAGES, DELTA>;
     using CC = CheckCfg<K, S, C::TW>;
@@ -620,7 +699,7 @@ cudaError_t run_fused(const BandParams& bp, const CUtensorMap* tmap, cudaStream_
     if constexpr (SMEM > 227 * 1024 || STAGES * 24 + 16 > 128) {
         return cudaErrorNotSupported;
     } else {
-        auto kern = conv_spmm_band<K, S, V, CPT, TH, STAGES, DELTA, true>;
+        auto kern = conv_spmm_band<K, S, V, CPT, TH, STAGES, DELTA, true, ZT>;
         static std::atomic<int> occ[64];  // per device; 0 = not yet queried
         int dev = 0;
         cudaGetDevice(&dev);
@@ -644,12 +723,12 @@ cudaError_t run_fused(const BandParams& bp, const CUtensorMap* tmap, cudaStream_
     }
 }
 
-template <int K, int S, int V, int CPT, int TH, int STAGES, int DELTA>
+template <int K, int S, int V, int CPT, int TH, int STAGES, int DELTA, bool ZT = false>
 cudaError_t run_cfg(const BandParams& bp, const CUtensorMap* tmap, cudaStream_t st, BandShape* shape,
                     int sms) {
     using C = BandCfg<K, S, V, CPT, TH, STAGES, DELTA>;
-    if (!shape && bp.fused) return run_fused<K, S, V, CPT, TH, STAGES, DELTA>(bp, tmap, st, sms);
-    auto kern = conv_spmm_band<K, S, V, CPT, TH, STAGES, DELTA, false>;
+    if (!shape && bp.fused) return run_fused<K, S, V, CPT, TH, STAGES, DELTA, ZT>(bp, tmap, st, sms);
+    auto kern = conv_spmm_band<K, S, V, CPT, TH, STAGES, DELTA, false, ZT>;
     static std::atomic<int> occ[64];  // per device; 0 = not yet queried
     int dev = 0;
     cudaGetDevice(&dev);
@@ -671,29 +750,38 @@ cudaError_t run_cfg(const BandParams& bp, const CUtensorMap* tmap, cudaStream_t 
     return cudaGetLastError();
 }
 
+template <int K, int S, int V, int CPT, int TH, int STAGES, bool ZT>
+cudaError_t run_delta_z(int delta, const BandParams& bp, const CUtensorMap* tmap, cudaStream_t st,
+                        BandShape* shape, int sms) {
+    switch (delta) {
+        case 0: return run_cfg<K, S, V, CPT, TH, STAGES, 0, ZT>(bp, tmap, st, shape, sms);
+        case 1: return run_cfg<K, S, V, CPT, TH, STAGES, 1, ZT>(bp, tmap, st, shape, sms);
+        case 2: return run_cfg<K, S, V, CPT, TH, STAGES, 2, ZT>(bp, tmap, st, shape, sms);
+        default: return run_cfg<K, S, V, CPT, TH, STAGES, 3, ZT>(bp, tmap, st, shape, sms);
+    }
+}
+
+// The default blocking of each (k, s); zero-tap transforms (bp.zt, only for
+// launches -- the shape query is blocking-only) take the ZT instantiation.
 template <int K, int S, int V, int CPT, int TH, int STAGES>
 cudaError_t run_delta(int delta, const BandParams& bp, const CUtensorMap* tmap, cudaStream_t st,
                       BandShape* shape, int sms) {
-    switch (delta) {
-        case 0: return run_cfg<K, S, V, CPT, TH, STAGES, 0>(bp, tmap, st, shape, sms);
-        case 1: return run_cfg<K, S, V, CPT, TH, STAGES, 1>(bp, tmap, st, shape, sms);
-        case 2: return run_cfg<K, S, V, CPT, TH, STAGES, 2>(bp, tmap, st, shape, sms);
-        default: return run_cfg<K, S, V, CPT, TH, STAGES, 3>(bp, tmap, st, shape, sms);
-    }
+    if (!shape && bp.zt) return run_delta_z<K, S, V, CPT, TH, STAGES, true>(delta, bp, tmap, st, shape, sms);
+    return run_delta_z<K, S, V, CPT, TH, STAGES, false>(delta, bp, tmap, st, shape, sms);
 }
 
 template <int K, int S, int TW>
 cudaError_t run_check(const BandParams& bp, cudaStream_t st, int sms) {
     (void)sms;
     using C = CheckCfg<K, S, TW>;
-    auto kern = conv_band_check<K, S, TW>;
-    static std::atomic<bool> init[64];
+    auto kern = bp.zt ? conv_band_check<K, S, TW, true> : conv_band_check<K, S, TW, false>;
+    static std::atomic<bool> init[2][64];
     int dev = 0;
     cudaGetDevice(&dev);
-    if (!init[dev & 63]) {
+    if (!init[bp.zt ? 1 : 0][dev & 63]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
         if (e != cudaSuccess) return e;
-        init[dev & 63] = true;
+        init[bp.zt ? 1 : 0][dev & 63] = true;
     }
     const long long segs = (long long)bp.mo * bp.tiles_y;
     const long long grid = (segs + C::WARPS - 1) / C::WARPS;
@@ -712,6 +800,11 @@ int band_tile_width(int k, int s) {
     return s == 1 ? 128 : 64;
 }
 
+int var_env() {
+    static const int v = std::getenv("SPCONV_B200_VARIANT") ? std::atoi(std::getenv("SPCONV_B200_VARIANT")) : 0;
+    return v;
+}
+
 // delta = (box start alignment shift) = (S*y0 - p) mod 4 with y0 a multiple
 // of the tile width: uniform over the launch.
 cudaError_t launch_band(int k, int s, const BandParams& bp, const CUtensorMap* tmap, cudaStream_t st,
@@ -719,7 +812,8 @@ cudaError_t launch_band(int k, int s, const BandParams& bp, const CUtensorMap* t
     const int delta = ((-bp.p) % 4 + 4) % 4;
     // Blocking variants for tuning experiments (SPCONV_B200_VARIANT; 0 = default),
     // instantiated only for the alignment shift of the benchmark configs.
-    static const int var = std::getenv("SPCONV_B200_VARIANT") ? std::atoi(std::getenv("SPCONV_B200_VARIANT")) : 0;
+    // (dense taps only: a zero-tap launch always takes the default blocking)
+    const int var = bp.zt ? 0 : var_env();
     // Defaults from the A/B runs (profiles/r01p/exp.txt): k3 s1 -- V = 16 rows
     // x 4 columns per thread, 64-row tiles, 4 stages (one CTA per SM; config 3
     // 404 -> 382 us); k7 s2 -- V = 8, 32-row tiles, 3 stages.

@@ -97,15 +97,19 @@ def test_fp32_kernels_apply_narrowed_taps(sp, ref, orc, torch_cuda):
     want = orc.spmm_native(*orc.build_native(*spec, kern.astype(np.float32)), X)
     assert np.array_equal(Y.cpu().numpy().view(np.uint32), want.view(np.uint32))
     # a non-zero double tap that narrows to 0.0f: stored (as the reference
-    # stores it), so the fp32 band path is off; outputs still follow the contract
+    # stores it) and applied as w = 0 by the masked band path
     kern2 = kernel64(ref, 3, 5, tiny=True)
     t2 = sp.build_transform(sp.Kernel(3, kern2), sp.ConvSpec(*spec))
+    X[2, 500] = np.inf  # under the stored zero tap too
     Y2 = sp.spmm(t2, torch.from_numpy(X).cuda())
     torch.cuda.synchronize()
-    assert t2.last_kernel not in BAND_KERNELS
+    assert t2.last_kernel in BAND_KERNELS
     ptr, idx, val = t2.export()
     want2 = orc.spmm_f32_fma(ptr, idx, val.astype(np.float32), X)
-    assert np.array_equal(Y2.cpu().numpy().view(np.uint32), want2.view(np.uint32))
+    got2 = Y2.cpu().numpy()
+    assert np.isnan(want2).any()  # 0 * inf under the stored zero tap
+    assert np.array_equal(np.isnan(got2), np.isnan(want2))  # (NaN payloads are not part of the contract)
+    assert np.array_equal(np.nan_to_num(got2, nan=7.0).view(np.uint32), np.nan_to_num(want2, nan=7.0).view(np.uint32))
 
 
 def test_relayout_and_read_keep_exact_values(sp, ref, torch_cuda):
