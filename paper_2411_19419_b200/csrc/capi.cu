@@ -359,7 +359,9 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
         // SPCONV_B200_FUSED=0|1 overrides; the blocked path needs finite taps.
         const char* fsel = std::getenv("SPCONV_B200_FUSED");
         const bool light = 8.0 * (double)h->nnz < 0.1 * 4.0 * (double)batch * (double)(h->rows + h->cols);
-        bp.fused = !side && band_taps && (fsel ? !std::strcmp(fsel, "1") : light) ? 1 : 0;
+        // (zero-tap kernels: the masked checks slow the fused producer -- config 3
+        // shape 431 us fused against 27 + 371 us as two kernels -- so two kernels)
+        bp.fused = !side && band_taps && (fsel ? !std::strcmp(fsel, "1") : light && !bp.zt) ? 1 : 0;
         if (bp.fused) {
             const cudaError_t fe = spb::launch_band((int)g.k, (int)g.s, bp, &tmap, st, nullptr, sms);
             if (fe == cudaSuccess) {

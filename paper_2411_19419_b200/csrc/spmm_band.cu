@@ -284,14 +284,16 @@ __device__ __forceinline__ bool seg_verify(const BandParams& P, const SegGeom& g
             if (ZT) {  // stored taps only, in (j, i) order
                 int e = 0;
                 if (cx == K && ilo == 0 && ihi == K) {
+                    // tap q sits at the popcount of the mask below it (row-invariant)
 #pragma unroll
                     for (int j = 0; j < K; ++j)
 #pragma unroll
-                        for (int ii = 0; ii < K; ++ii)
-                            if ((mk >> (j * K + ii)) & 1ull) {
-                                bad |= (uint32_t)(cl[e] - (rb + j * P.n + ii)) | (vl[e] ^ w[j * K + ii]);
-                                ++e;
-                            }
+                        for (int ii = 0; ii < K; ++ii) {
+                            const int q = j * K + ii;
+                            const int pos = __popcll(mk & ((1ull << q) - 1ull));
+                            if ((mk >> q) & 1ull)
+                                bad |= (uint32_t)(cl[pos] - (rb + j * P.n + ii)) | (vl[pos] ^ w[q]);
+                        }
                 } else {
                     for (int j = g.jlo; j < g.jhi; ++j)
                         for (int ii = ilo; ii < ihi; ++ii)
