@@ -446,6 +446,14 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
 
     // ---- generic CSR path ----
     spb::GenericParams gp{h->row_ptr, h->col_idx, h->vals, X, ldx, Y, ldy, (int)h->rows, (int)batch};
+    // the row-block multi-vector kernel (matrix staged once per CTA) for rows
+    // of <= 64 entries; SPCONV_B200_GENERIC=plain keeps thread-per-row
+    const char* gsel = std::getenv("SPCONV_B200_GENERIC");
+    if (h->k2max <= 64 && !(gsel && !std::strcmp(gsel, "plain"))) {
+        CK(spb::launch_rowblock(gp, h->k2max, st));
+        h->last_kernel.store("csr_spmm_rowblock");
+        return SPCONV_OK;
+    }
     CK(spb::launch_generic(gp, st));
     h->last_kernel.store("csr_spmm_generic");
     return SPCONV_OK;

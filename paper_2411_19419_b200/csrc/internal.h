@@ -133,6 +133,7 @@ struct GenericParams {
     int64_t ldy;
     int rows;
     int batch;
+    int stage_cap = 0;  // csr_spmm_rowblock: staged entries per CTA (set by its launcher)
 };
 
 // Launchers (return cudaError_t of the launch).
@@ -142,6 +143,7 @@ cudaError_t launch_csc_build(CscParams cp, int maxc, bool dense, cudaStream_t st
 cudaError_t launch_tiled(const TiledParams& tp, const CUtensorMap* tmap, int bt, size_t smem,
                          cudaStream_t st);
 cudaError_t launch_generic(const GenericParams& gp, cudaStream_t st);
+cudaError_t launch_rowblock(GenericParams gp, int kmax, cudaStream_t st);  // rows of <= 64 entries
 struct F64Params {
     const int32_t* row_ptr;
     const int32_t* col_idx;

@@ -22,6 +22,7 @@
 //   image), x gathered through L1.
 // csr_spmv_bulk -- the latency kernel for batch <= 2 (below).
 // csr_spmv_unrolled -- thread per row, a cross-check path (SPCONV_B200_PATH=spmv_plain).
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 
@@ -490,6 +491,85 @@ cudaError_t launch_tiled(const TiledParams& tp, const CUtensorMap* tmap, int bt,
         case 8: return launch_bt<8>(tp, tmap, smem, st);
         default: return cudaErrorInvalidValue;
     }
+}
+
+// Multi-vector SpMM for any CSR whose rows hold at most `kmax` entries (the
+// generic path of matrices that are not conv transforms -- read_sparse,
+// uploads -- and of forced runs): a CTA owns 128 consecutive rows, stages
+// their (col, val) run in shared memory ONCE with coalesced loads, then walks
+// its share of the batch, IMG images at a time, each thread accumulating its
+// row in stored order (acc = fmaf(val, x[col], acc), bit-exact with the
+// per-row loop).  The matrix is read once per CTA (per image group) instead
+// of once per image.
+template <int IMG>
+__global__ void __launch_bounds__(128) csr_spmm_rowblock(const GenericParams P) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int t = threadIdx.x;
+    const int r0 = blockIdx.x * 128;
+    const int r1 = min(P.rows, r0 + 128);
+    const int e0 = __ldg(P.row_ptr + r0), e1 = __ldg(P.row_ptr + r1);
+    int* sc = reinterpret_cast<int*>(smem);
+    float* sv = reinterpret_cast<float*>(sc + P.stage_cap);
+    for (int e = e0 + t; e < e1; e += 128) {
+        sc[e - e0] = __ldg(P.col_idx + e);
+        sv[e - e0] = __ldg(P.vals + e);
+    }
+    __syncthreads();
+    const int r = r0 + t;
+    if (r >= r1) return;
+    const int a = __ldg(P.row_ptr + r) - e0, b = __ldg(P.row_ptr + r + 1) - e0;
+    // images in groups of IMG: group blockIdx.y, blockIdx.y + gridDim.y, ...
+    for (int i0 = blockIdx.y * IMG; i0 < P.batch; i0 += gridDim.y * IMG) {
+        const int ni = min(IMG, P.batch - i0);
+        const float* x0 = P.X + (int64_t)i0 * P.ldx;
+        float acc[IMG];
+#pragma unroll
+        for (int q = 0; q < IMG; ++q) acc[q] = 0.0f;
+        for (int e = a; e < b; ++e) {
+            const int c = sc[e];
+            const float v = sv[e];
+#pragma unroll
+            for (int q = 0; q < IMG; ++q)
+                if (q < ni) acc[q] = fmaf(v, __ldg(x0 + (int64_t)q * P.ldx + c), acc[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < IMG; ++q)
+            if (q < ni) P.Y[(int64_t)(i0 + q) * P.ldy + r] = acc[q];
+    }
+}
+
+template <int IMG>
+static cudaError_t launch_rowblock_i(const GenericParams& gp, size_t smem, cudaStream_t st) {
+    static std::atomic<bool> attr[64];
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (smem > 48 * 1024 && !attr[dev & 63]) {
+        cudaError_t e = cudaFuncSetAttribute(csr_spmm_rowblock<IMG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             64 * 1024);
+        if (e != cudaSuccess) return e;
+        attr[dev & 63] = true;
+    }
+    const int gx = (gp.rows + 127) / 128;
+    // enough CTAs for every SM several times over; each reads the matrix once
+    const int groups = (gp.batch + IMG - 1) / IMG;
+    const int gy = std::max(1, std::min(groups, (sms * 16 + gx - 1) / gx));
+    csr_spmm_rowblock<IMG><<<dim3(gx, std::min(gy, 65535)), 128, smem, st>>>(gp);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rowblock(GenericParams gp, int kmax, cudaStream_t st) {
+    if (kmax > 64) return cudaErrorInvalidValue;
+    gp.stage_cap = 128 * std::max(kmax, 1);
+    const size_t smem = (size_t)gp.stage_cap * 8;
+    const char* v = std::getenv("SPCONV_B200_ROWBLOCK_IMG");
+    // images per group: 8 (config 3 shape as a generic CSR, 256 images:
+    // 1.41 / 1.48 / 1.15 / 1.69 ms for 2 / 4 / 8 / 16, profiles/r01_generic)
+    const int img = v ? std::atoi(v) : 8;
+    if (img == 16) return launch_rowblock_i<16>(gp, smem, st);
+    if (img == 4) return launch_rowblock_i<4>(gp, smem, st);
+    if (img == 2) return launch_rowblock_i<2>(gp, smem, st);
+    return launch_rowblock_i<8>(gp, smem, st);
 }
 
 cudaError_t launch_generic(const GenericParams& gp, cudaStream_t st) {

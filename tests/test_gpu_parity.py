@@ -322,6 +322,35 @@ def test_generic_csr_upload(sp, orc, torch_cuda):
         assert t.last_kernel == "csr_spmv_bulk"
 
 
+@pytest.mark.parametrize("kernel", ["rowblock", "plain"])
+def test_generic_multivector_kernels(sp, orc, torch_cuda, kernel, monkeypatch):
+    """Batches on a generic CSR: the row-block kernel (matrix staged once per
+    CTA, images four at a time) and the thread-per-row kernel
+    (SPCONV_B200_GENERIC=plain), ragged and empty rows, row blocks that end
+    mid-matrix, batches that are not a multiple of four, padded ldx,
+    non-finite inputs; rows longer than 64 entries take the plain kernel."""
+    if kernel == "plain":
+        monkeypatch.setenv("SPCONV_B200_GENERIC", "plain")
+    rng = np.random.default_rng(5)
+    for rows, cols, maxlen in ((300, 517, 40), (1000, 2000, 64), (77, 5000, 100)):
+        lens = rng.integers(0, maxlen + 1, rows)
+        lens[::7] = 0
+        ptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+        idx = np.concatenate([np.sort(rng.choice(cols, size=int(L), replace=False)) for L in lens]).astype(np.int64)
+        val = rng.standard_normal(idx.size)
+        val[::11] = 0.0
+        t = sp.Transform.from_host(rows, cols, ptr, idx, val)
+        for batch in (3, 6, 13):
+            X = rng.standard_normal((batch, cols)).astype(np.float32)
+            X[1, rng.integers(0, cols)] = np.inf
+            want = orc.spmm_f32_fma(ptr, idx, val, X)
+            for pad in (0, 4):
+                got = run_spmm(torch_cuda, sp, t, X, ldx_pad=pad)
+                assert np.array_equal(bits(got), bits(want)), (rows, batch, pad)
+            expect = "csr_spmm_rowblock" if kernel == "rowblock" and maxlen <= 64 else "csr_spmm_generic"
+            assert t.last_kernel == expect
+
+
 def test_end_to_end_host_path(sp, orc, torch_cuda):
     """convolve_batch on host buffers (chunked H2D / SpMM / D2H pipeline)."""
     spec = (256, 200, 3, 1, 1)
