@@ -44,10 +44,12 @@
 //    bytes; the host (capi.cu run_spmm) picks the form.
 //
 //    Blocked == per-entry, bit for bit: a tap that lands in the zero padding
-//    executes fmaf(w, +0.0f, acc), which returns acc unchanged (acc starts at
-//    +0 and is never -0 under round-to-nearest, w is finite), so executing or
-//    skipping the clipped taps is indistinguishable, and every output still
-//    sees its stored taps in (j, i) = column-ascending order.
+//    executes fmaf(w, +0.0f, acc), which returns acc unchanged (w finite)
+//    unless acc is exactly -0 -- reachable only when every earlier product
+//    underflowed to -0 (|w*x| < 2^-150) -- where it may return +0 (DESIGN 8:
+//    the sign of such a zero is the one bit-level exception).  So executing
+//    or skipping the clipped taps is otherwise indistinguishable, and every
+//    output still sees its stored taps in (j, i) = column-ascending order.
 #include <algorithm>
 #include <cstdlib>
 
@@ -393,8 +395,8 @@ struct ItemIter {
 // right after on the same stream, recomputes the rows of any segment that
 // failed its check from the CSR (normally none: it only reads the flags).
 // ZT: some taps are exact zeros.  The blocked sums still run over all k*k
-// taps: for a finite x, fmaf(0, x, acc) == acc (acc starts at +0 and is never
-// -0), so they equal the stored-taps sums bit for bit; a thread whose sums are
+// taps: for a finite x, fmaf(0, x, acc) == acc (up to the sign of a zero acc,
+// see the header), so they equal the stored-taps sums; a thread whose sums are
 // not all finite (a non-finite x it read, where 0 * inf would differ) redoes
 // its outputs per entry from the CSR.
 template <int K, int S, int V, int CPT, int TH, int STAGES, int DELTA, bool FUSED, bool ZT = false>

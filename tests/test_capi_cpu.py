@@ -107,6 +107,14 @@ def test_int32_range_rejected_before_any_device_work():
         sp.build_transform(sp.Kernel(3, np.ones(9)), sp.ConvSpec(8, 8, 3, 1, 1), layout=2)
     with pytest.raises(ValueError, match="unknown layout 'coo'"):
         sp.layout_from_name("coo")
+    # double taps fp32 cannot hold (spconv_build_transform_f64): the same checks, same order
+    taps = np.full(9, 0.1)
+    with pytest.raises(ValueError, match="layout must be 0"):
+        sp.build_transform(sp.Kernel(3, taps), sp.ConvSpec(8, 8, 3, 1, 1), layout=2)
+    with pytest.raises(ValueError, match=r"nnz \d+ exceeds the int32 device index range"):
+        sp.build_transform(sp.Kernel(3, taps), sp.ConvSpec(20000, 20000, 3, 1, 1))
+    with pytest.raises(ValueError, match="kernel larger than padded input"):
+        sp.build_transform(sp.Kernel(3, taps), sp.ConvSpec(1, 1, 3, 1, 0))
 
 
 def test_rng_matches_reference_known_answers(golden, orc):
