@@ -259,6 +259,13 @@ int spconv_sparse_read(const char* text, int64_t len, int layout, int device, vo
  * the first call).  The string is static. */
 const char* spconv_csr_last_kernel(const spconv_csr* h);
 
+/* Diagnostics: the verdicts of the last band check run on this handle (one per
+ * segment of output columns): *segments = how many, *failed = how many did
+ * not match the conv pattern (their rows were computed per entry).  0 failed
+ * means the blocked path served every row.  Synchronizes the device; status 1
+ * for a handle without band geometry. */
+int spconv_band_check_status(const spconv_csr* h, int64_t* segments, int64_t* failed);
+
 /* Frees the handle and its device memory (synchronises its device). */
 int spconv_csr_free(spconv_csr* h);
 

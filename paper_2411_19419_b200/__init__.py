@@ -65,6 +65,7 @@ _decl("spconv_convolve_host", [_vp, _vp, _vp, _i64])
 _decl("spconv_convolve_host_f64", [_vp, _vp, _vp, _i64])
 _decl("spconv_spmm_f64", [_vp, _vp, _i64, _vp, _i64, _i64, _vp])
 _decl("spconv_csr_last_kernel", [_vp], C.c_char_p)
+_decl("spconv_band_check_status", [_vp, _P(_i64), _P(_i64)])
 _decl("spconv_csr_write_text", [_vp, C.c_int, _vp, _i64, _P(_i64)])
 _decl("spconv_transform_read", [_vp, _i64, C.c_int, _vp, _P(_vp)])
 _decl("spconv_sparse_read", [_vp, _i64, C.c_int, C.c_int, _vp, _P(_vp)])
@@ -256,6 +257,12 @@ class Transform:
     def last_kernel(self) -> str:
         """Kernel(s) the last apply on this transform launched ("a+b" = two launches)."""
         return lib.spconv_csr_last_kernel(self._h).decode()
+
+    def band_check_status(self) -> Tuple[int, int]:
+        """(segments, failed) of the last band check (spconv_band_check_status)."""
+        a, b = _i64(), _i64()
+        _check(lib.spconv_band_check_status(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def close(self) -> None:
         if self._h and self._h.value:

@@ -310,6 +310,19 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
         bp.p = (int)g.p;
         bp.zt = band_taps && !h->taps_dense ? 1 : 0;
         bp.nzmask = nzmask;
+        if (bp.zt) {  // W[j] = sum over stored taps (j, i) of #{y : tap i lands in the input}
+            for (int64_t j = 0; j < g.k && j < 8; ++j) {
+                long long wj = 0;
+                for (int64_t i = 0; i < g.k; ++i) {
+                    if (!((nzmask >> (j * g.k + i)) & 1ull)) continue;
+                    // y with 0 <= s*y + i - p < n, y in [0, n_out): a closed range
+                    const int64_t lo = g.p - i <= 0 ? 0 : (g.p - i + g.s - 1) / g.s;
+                    const int64_t hi = g.n + g.p - i - 1 < 0 ? -1 : std::min<int64_t>(g.no - 1, (g.n + g.p - i - 1) / g.s);
+                    wj += std::max<int64_t>(0, hi - lo + 1);
+                }
+                bp.zw[j] = wj;
+            }
+        }
         CK(spb::launch_band((int)g.k, (int)g.s, bp, nullptr, st, &sh, sms));
         bp.row_ptr = h->row_ptr;
         bp.col_idx = h->col_idx;
@@ -1448,6 +1461,22 @@ const char* spconv_csr_last_kernel(const spconv_csr* h) {
     if (!h) return "";
     const char* k = h->last_kernel.load();
     return k ? k : "";
+}
+
+int spconv_band_check_status(const spconv_csr* h, int64_t* segments, int64_t* failed) {
+    if (!h || !segments || !failed) return fail(SPCONV_EINVAL, "spconv_band_check_status: null argument");
+    if (!h->seg_ok || h->band_tw <= 0) return fail(SPCONV_EINVAL, "spconv_band_check_status: no band geometry");
+    DeviceGuard dg(h->device);
+    if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
+    const int64_t n = h->g.mo * ((h->g.no + h->band_tw - 1) / h->band_tw);
+    std::vector<uint8_t> v((size_t)n);
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(v.data(), h->seg_ok, (size_t)n, cudaMemcpyDeviceToHost));
+    int64_t bad = 0;
+    for (uint8_t b : v) bad += b == 0;
+    *segments = n;
+    *failed = bad;
+    return SPCONV_OK;
 }
 
 int spconv_csr_free(spconv_csr* h) {

@@ -102,6 +102,7 @@ struct BandParams {
     int fused;         // host: launch the fused check + apply (+ fixup) instead of two kernels
     int zt;            // some taps are exact zeros (not stored): masked footprint + checks
     unsigned long long nzmask;  // bit j*k+i: tap (j, i) is non-zero (zt; k <= 7)
+    long long zw[8];            // zt: W[j] = sum_i nz[j][i] * #{y : tap i lands} (per handle)
 };
 
 struct BandShape {

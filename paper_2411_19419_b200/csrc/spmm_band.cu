@@ -180,13 +180,7 @@ __device__ __forceinline__ SegGeom seg_geom(const BandParams& P, long long seg) 
         long long s0 = 0;
         int len = 0;
 #pragma unroll
-        for (int j = 0; j < K; ++j) {
-            long long wj = 0;
-#pragma unroll
-            for (int i = 0; i < K; ++i)
-                if ((mk >> (j * K + i)) & 1ull) wj += slides_before(P.no, i, P.n, S, P.p);
-            s0 += wj * slides_before(g.x, j, P.m, S, P.p);
-        }
+        for (int j = 0; j < K; ++j) s0 += P.zw[j] * slides_before(g.x, j, P.m, S, P.p);
 #pragma unroll
         for (int i = 0; i < K; ++i) {
             int nzc = 0;

@@ -486,6 +486,7 @@ def test_band_check_reads_the_matrix(sp, orc, torch_cuda, spec, check, monkeypat
     ptr, idx, val = native_copy(t)
     clean = run_spmm(torch_cuda, sp, t, X)
     assert np.array_equal(bits(clean), bits(orc.spmm_native(ptr, idx, val, X)))
+    assert t.band_check_status()[1] == 0  # the untouched matrix passes every segment
     _, ci, cv = t.device_ptrs()
     dci = torch_cuda.as_tensor(_DevArray(ci, t.nnz, "<i4"), device="cuda")
     dcv = torch_cuda.as_tensor(_DevArray(cv, t.nnz, "<f4"), device="cuda")
@@ -506,6 +507,7 @@ def test_band_check_reads_the_matrix(sp, orc, torch_cuda, spec, check, monkeypat
     torch_cuda.cuda.synchronize()
     Y = run_spmm(torch_cuda, sp, t, X)
     assert t.last_kernel in BAND_KERNELS
+    assert 1 <= t.band_check_status()[1] <= 3  # only the tampered segments failed
     want = orc.spmm_native(ptr, idx, val, X)
     assert not np.array_equal(bits(want), bits(clean))
     assert np.array_equal(bits(Y), bits(want))

@@ -58,6 +58,8 @@ def test_zero_tap_band_bitexact(sp, orc, torch_cuda, spec, fused, monkeypatch):
         ptr, idx, val = native_copy(t)
         Y = run_spmm(torch_cuda, sp, t, X)
         assert t.last_kernel in BAND_KERNELS, t.last_kernel
+        segs, failed = t.band_check_status()
+        assert segs > 0 and failed == 0, (spec, frac, failed)  # the masked footprint matched everywhere
         want = orc.spmm_native(ptr, idx, val, X)
         assert np.array_equal(bits(Y), bits(want)), (spec, frac)
 
@@ -85,6 +87,7 @@ def test_zero_tap_band_check_reads_the_matrix(sp, orc, torch_cuda, fused, monkey
     torch_cuda.cuda.synchronize()
     Y = run_spmm(torch_cuda, sp, t, X)
     assert t.last_kernel in BAND_KERNELS
+    assert 1 <= t.band_check_status()[1] <= 2  # exactly the tampered segments failed
     want = orc.spmm_native(ptr, idx, val, X)
     assert not np.array_equal(bits(want), bits(clean))
     assert np.array_equal(bits(Y), bits(want))
