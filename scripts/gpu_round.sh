@@ -18,3 +18,6 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:csr_
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"csr_build" -s 3 -c 1 -o gpurun_out/prof_build_c3 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-secondary --e2e-steps 2 > gpurun_out/ncu_full_build3.log 2>&1; echo "ncu-full-build3 rc=$?" >> gpurun_out/status.txt
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"csr_build" -s 3 -c 1 -o gpurun_out/prof_build_c4 python bench.py --config 4 --steps 3 --warmup 3 --no-cpu-baseline --no-secondary --e2e-steps 2 > gpurun_out/ncu_full_build4.log 2>&1; echo "ncu-full-build4 rc=$?" >> gpurun_out/status.txt
 timeout 900 python scripts/exp_run.py gpurun_out/exp.txt "--config 3|" "--config 3 --batch 1024|" "--config 4|" "--config 4 --batch 64|" "--config 2|" "--config 3|SPCONV_B200_FUSED=0" > /dev/null 2>&1; echo "exp rc=$?" >> gpurun_out/status.txt
+# multi-rank path on the one GPU (2 ranks sharing it over gloo): barrier, max-over-ranks, gather
+SPCONV_B200_DIST_BACKEND=gloo timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 5 --warmup 3 --no-cpu-baseline --no-secondary --e2e-steps 2 --gather > gpurun_out/bench_2rank_gloo.log 2>&1; echo "2rank rc=$?" >> gpurun_out/status.txt
+timeout 300 python scripts/zt_probe.py > gpurun_out/zt.txt 2>&1; echo "zt rc=$?" >> gpurun_out/status.txt
