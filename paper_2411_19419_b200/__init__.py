@@ -382,8 +382,8 @@ def convolve_batch(t: Transform, X_host, Y_host=None):
 
 def spmm_f64(t: Transform, X, Y=None, stream=None):
     """Y[b] = T X[b] in fp64 with the reference's arithmetic (spconv_spmm_f64):
-    X [batch, cols] CUDA float64; bit-identical to the reference's spmv() for
-    fp32-representable taps."""
+    X [batch, cols] CUDA float64; bit-identical to the reference's spmv() (the
+    handle's exact double values are used when it keeps them)."""
     import torch
     if not (isinstance(X, torch.Tensor) and X.is_cuda and X.dtype == torch.float64):
         raise ValueError("spmm_f64: expected a CUDA float64 tensor")
@@ -399,7 +399,7 @@ def spmm_f64(t: Transform, X, Y=None, stream=None):
 def convolve(t: Transform, a) -> np.ndarray:
     """Reference-semantics apply of one m x n grid (inc/conv.hpp:207-215):
     fp64 in, fp64 device arithmetic with the reference's rounding, fp64 out --
-    bit-identical to the reference for fp32-representable taps."""
+    bit-identical to the reference (exact double taps included)."""
     a = np.asarray(a, dtype=np.float64)
     if t.spec is None:
         raise ValueError("convolve: transform has no geometry (generic CSR)")
