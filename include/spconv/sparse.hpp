@@ -67,6 +67,35 @@ struct Entry {
     double value;
 };
 
+/// Coordinate-format builder (inc/sparse.hpp:40-73): same checks and messages.
+/// SparseMatrix::compile turns it into compressed storage on the device.
+class Triplets {
+public:
+    Triplets(index_t rows, index_t cols) : rows_(rows), cols_(cols) {
+        if (rows < 1 || cols < 1)
+            throw std::invalid_argument("Triplets: dimensions must be at least 1x1, got " + std::to_string(rows) +
+                                        "x" + std::to_string(cols));
+    }
+
+    void reserve(std::size_t n) { entries_.reserve(n); }
+
+    void add(index_t row, index_t col, double value) {
+        if (row < 0 || row >= rows_ || col < 0 || col >= cols_)
+            throw std::invalid_argument("Triplets: entry (" + std::to_string(row) + ", " + std::to_string(col) +
+                                        ") outside " + std::to_string(rows_) + "x" + std::to_string(cols_));
+        entries_.push_back({row, col, value});
+    }
+
+    index_t rows() const { return rows_; }
+    index_t cols() const { return cols_; }
+    std::size_t size() const { return entries_.size(); }
+    const std::vector<Entry>& entries() const { return entries_; }
+
+private:
+    index_t rows_, cols_;
+    std::vector<Entry> entries_;
+};
+
 /// Compressed sparse matrix resident on the GPU, CSR or CSC.  Copies share the
 /// immutable device matrix.
 class SparseMatrix {
@@ -80,6 +109,24 @@ public:
         detail::check(spconv_csr_layout(h, &lay));
         layout_ = lay == 0 ? Layout::CSR : Layout::CSC;
         host_ = std::make_shared<HostCopy>();
+    }
+
+    /// compile (inc/sparse.hpp:85-119): sorted into `layout` order on the device,
+    /// duplicates rejected with the reference's message, explicit zeros kept.
+    static SparseMatrix compile(const Triplets& t, Layout layout) {
+        const std::size_t n = t.size();
+        std::vector<index_t> r(n), c(n);
+        std::vector<double> v(n);
+        for (std::size_t i = 0; i < n; ++i) {
+            r[i] = t.entries()[i].row;
+            c[i] = t.entries()[i].col;
+            v[i] = t.entries()[i].value;
+        }
+        spconv_csr* h = nullptr;
+        detail::check(spconv_matrix_from_coo(t.rows(), t.cols(), static_cast<int64_t>(n), r.data(), c.data(),
+                                             v.data(), layout == Layout::CSR ? 0 : 1, detail::default_device(),
+                                             nullptr, &h));
+        return SparseMatrix(h);
     }
 
     /// Uploads a host CSR (ptr/idx int64, fp64 values; the fp32 kernels read them narrowed).

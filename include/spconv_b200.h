@@ -114,6 +114,17 @@ int spconv_csr_from_host(int64_t rows, int64_t cols, const int64_t* row_ptr,
                          const int64_t* col_idx, const double* vals, int device, void* stream,
                          spconv_csr** out);
 
+/* SparseMatrix::compile(Triplets, layout) (inc/sparse.hpp:35-119): n host
+ * coordinate entries (row[i], col[i], vals[i]) in any order -> a matrix in
+ * `layout` (0 = CSR, 1 = CSC), compiled ON THE DEVICE (a radix sort of the
+ * (major, minor) keys, duplicate detection, ptr from the key boundaries).
+ * Same checks and messages: Triplets' dimension and range checks, and
+ * "SparseMatrix: duplicate entry at (r, c)" (status 1).  Explicit zeros are
+ * kept; values fp32 cannot hold are kept exactly too (see
+ * spconv_csr_from_host).  Synchronous. */
+int spconv_matrix_from_coo(int64_t rows, int64_t cols, int64_t n, const int64_t* row, const int64_t* col,
+                           const double* vals, int layout, int device, void* stream, spconv_csr** out);
+
 /* rows(), cols(), nnz(): inc/sparse.hpp:121-126. */
 int spconv_csr_shape(const spconv_csr* h, int64_t* rows, int64_t* cols, int64_t* nnz);
 

@@ -69,6 +69,7 @@ _decl("spconv_band_check_status", [_vp, _P(_i64), _P(_i64)])
 _decl("spconv_csr_write_text", [_vp, C.c_int, _vp, _i64, _P(_i64)])
 _decl("spconv_transform_read", [_vp, _i64, C.c_int, _vp, _P(_vp)])
 _decl("spconv_sparse_read", [_vp, _i64, C.c_int, C.c_int, _vp, _P(_vp)])
+_decl("spconv_matrix_from_coo", [_i64, _i64, _i64, _vp, _vp, _vp, C.c_int, C.c_int, _vp, _P(_vp)])
 _decl("spconv_csr_free", [_vp])
 _decl("spconv_build_transform", [_i64] * 5 + [_vp, C.c_int, C.c_int, _vp, _P(_vp)])
 _decl("spconv_build_transform_f64", [_i64] * 5 + [_vp, C.c_int, C.c_int, _vp, _P(_vp)])
@@ -274,6 +275,22 @@ class Transform:
             self.close()
         except Exception:
             pass
+
+
+def compile_triplets(rows: int, cols: int, row, col, val, layout: int = Layout.CSR, device: int = 0,
+                     stream=None) -> Transform:
+    """SparseMatrix::compile(Triplets, layout) (inc/sparse.hpp:35-119) on the
+    device: coordinates in any order, duplicates rejected (ValueError with the
+    reference's message), explicit zeros kept.  A generic matrix (spec None)."""
+    r = np.ascontiguousarray(row, np.int64)
+    c = np.ascontiguousarray(col, np.int64)
+    v = np.ascontiguousarray(val, np.float64)
+    if not (r.size == c.size == v.size):
+        raise ValueError("compile_triplets: row, col and val differ in length")
+    h = _vp()
+    _check(lib.spconv_matrix_from_coo(rows, cols, r.size, r.ctypes.data, c.ctypes.data, v.ctypes.data, layout,
+                                      device, _stream_handle(stream), C.byref(h)))
+    return Transform(h.value, None, device)
 
 
 def read_sparse(text: bytes, layout: int = Layout.CSR, device: int = 0, stream=None) -> Transform:

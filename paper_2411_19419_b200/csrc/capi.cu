@@ -1093,6 +1093,72 @@ int spconv_csr_from_host(int64_t rows, int64_t cols, const int64_t* row_ptr,
     return SPCONV_OK;
 }
 
+int spconv_matrix_from_coo(int64_t rows, int64_t cols, int64_t n, const int64_t* row, const int64_t* col,
+                           const double* vals, int layout, int device, void* stream, spconv_csr** out) {
+    if (!out) return fail(SPCONV_EINVAL, "spconv_matrix_from_coo: null argument");
+    *out = nullptr;
+    if (layout != 0 && layout != 1) return fail(SPCONV_EINVAL, "spconv_matrix_from_coo: layout must be 0 (csr) or 1 (csc)");
+    if (rows < 1 || cols < 1)
+        return fail(SPCONV_EINVAL, "Triplets: dimensions must be at least 1x1, got " + std::to_string(rows) + "x" +
+                                       std::to_string(cols));
+    if (rows >= (1ll << 31) || cols >= (1ll << 31) || n < 0 || n >= (1ll << 31))
+        return fail(SPCONV_EINVAL, "spconv_matrix_from_coo: sizes exceed the int32 range");
+    if (n > 0 && (!row || !col || !vals)) return fail(SPCONV_EINVAL, "spconv_matrix_from_coo: null argument");
+    bool exact = true;
+    for (int64_t i = 0; i < n; ++i) {  // Triplets::add's range check (inc/sparse.hpp:55-62)
+        if (row[i] < 0 || row[i] >= rows || col[i] < 0 || col[i] >= cols)
+            return fail(SPCONV_EINVAL, "Triplets: entry (" + std::to_string(row[i]) + ", " + std::to_string(col[i]) +
+                                           ") outside " + std::to_string(rows) + "x" + std::to_string(cols));
+        exact &= __builtin_bit_cast(uint64_t, (double)(float)vals[i]) == __builtin_bit_cast(uint64_t, vals[i]);
+    }
+    DeviceGuard dg(device);
+    if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    auto* h = new (std::nothrow) spconv_csr();
+    if (!h) return fail(SPCONV_ECUDA, "out of host memory");
+    h->device = device;
+    h->rows = rows;
+    h->cols = cols;
+    h->nnz = n;
+    // (major+1 ptr, idx, vals: same slack conventions as spconv_csr_from_host)
+    auto alloc = [&](int64_t major, int32_t** p, int32_t** ix, float** v, double** v64) -> cudaError_t {
+        const size_t pb = ((size_t)(major + 1) * 4 + 255) & ~size_t(255);
+        const size_t ib = ((size_t)std::max<int64_t>(n, 1) * 4 + 255) & ~size_t(255);
+        char* mem = nullptr;
+        cudaError_t e = cudaMalloc(&mem, pb + 2 * ib + 256);
+        if (e != cudaSuccess) return e;
+        *p = reinterpret_cast<int32_t*>(mem);
+        *ix = reinterpret_cast<int32_t*>(mem + pb);
+        *v = reinterpret_cast<float*>(mem + pb + ib);
+        if (!exact) e = cudaMalloc(v64, (size_t)std::max<int64_t>(n, 1) * 8);
+        return e;
+    };
+    long long dup = -1;
+    int64_t dr = 0, dc = 0;
+    int maxlen = 0, unused = 0;
+    cudaError_t e = cudaSuccess;
+    if (layout == 1) {  // the storage order first: compile() reports the first duplicate in it
+        h->layout = 1;
+        e = alloc(cols, &h->csc_ptr, &h->csc_idx, &h->csc_vals, &h->csc_vals64);
+        if (e == cudaSuccess)
+            e = spb::coo_compile(n, row, col, vals, rows, cols, false, h->csc_ptr, h->csc_idx, h->csc_vals,
+                                 h->csc_vals64, &dup, &dr, &dc, &unused, st);
+    }
+    // the row-major arrays every apply kernel reads
+    if (e == cudaSuccess && dup < 0) e = alloc(rows, &h->row_ptr, &h->col_idx, &h->vals, &h->vals64);
+    if (e == cudaSuccess && dup < 0)
+        e = spb::coo_compile(n, row, col, vals, rows, cols, true, h->row_ptr, h->col_idx, h->vals, h->vals64, &dup,
+                             &dr, &dc, &maxlen, st);
+    h->k2max = maxlen;
+    if (e != cudaSuccess || dup >= 0) {
+        spconv_csr_free(h);
+        if (e != cudaSuccess) return cuda_fail(e, "spconv_matrix_from_coo");
+        return fail(SPCONV_EINVAL, "SparseMatrix: duplicate entry at (" + std::to_string(dr) + ", " + std::to_string(dc) + ")");
+    }
+    *out = h;
+    return SPCONV_OK;
+}
+
 int spconv_csr_shape(const spconv_csr* h, int64_t* rows, int64_t* cols, int64_t* nnz) {
     if (!h) return fail(SPCONV_EINVAL, "null handle");
     if (rows) *rows = h->rows;

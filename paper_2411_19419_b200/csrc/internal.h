@@ -145,6 +145,11 @@ cudaError_t launch_tiled(const TiledParams& tp, const CUtensorMap* tmap, int bt,
                          cudaStream_t st);
 cudaError_t launch_generic(const GenericParams& gp, cudaStream_t st);
 cudaError_t launch_rowblock(GenericParams gp, int kmax, cudaStream_t st);  // rows of <= 64 entries
+// SparseMatrix::compile of host triplets on the device (coo.cu).
+cudaError_t coo_compile(long long n, const int64_t* r_host, const int64_t* c_host, const double* v_host,
+                        int64_t rows, int64_t cols, bool by_row, int32_t* ptr, int32_t* idx, float* v32,
+                        double* v64, long long* dup_index, int64_t* dup_r, int64_t* dup_c, int* max_len,
+                        cudaStream_t st);
 struct F64Params {
     const int32_t* row_ptr;
     const int32_t* col_idx;

@@ -263,6 +263,33 @@ int main() {
         },
         "read_grid: expected 4 values, got 3");
 
+    // Triplets + compile (inc/sparse.hpp:35-119), compiled on the device
+    {
+        Triplets t(3, 4);
+        t.add(2, 1, 5.0);
+        t.add(0, 3, -1.0);
+        t.add(0, 0, 0.0);  // explicit zero: kept
+        t.add(1, 2, 0.1);
+        const SparseMatrix a = SparseMatrix::compile(t, Layout::CSR);
+        CHECK((a.ptr() == std::vector<index_t>{0, 2, 3, 4}));
+        CHECK((a.idx() == std::vector<index_t>{0, 3, 2, 1}));
+        CHECK((a.val() == std::vector<double>{0.0, -1.0, 0.1, 5.0}));
+        const SparseMatrix b = SparseMatrix::compile(t, Layout::CSC);
+        CHECK(b.layout() == Layout::CSC);
+        CHECK((b.ptr() == std::vector<index_t>{0, 1, 2, 3, 4}));
+        CHECK((b.idx() == std::vector<index_t>{0, 2, 1, 0}));
+        CHECK(spmv(a, DenseVector{1, 2, 3, 4}) == spmv(b, DenseVector{1, 2, 3, 4}));
+    }
+    expect_throw<std::invalid_argument>(
+        [] {
+            Triplets t(2, 2);
+            t.add(1, 1, 1.0);
+            t.add(1, 1, 2.0);
+            SparseMatrix::compile(t, Layout::CSR);
+        },
+        "SparseMatrix: duplicate entry at (1, 1)");
+    expect_throw<std::invalid_argument>([] { Triplets(2, 2).add(2, 0, 1.0); }, "Triplets: entry (2, 0) outside 2x2");
+
     if (g_fail) {
         std::fprintf(stderr, "%d failure(s)\n", g_fail);
         return 1;

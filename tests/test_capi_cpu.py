@@ -130,3 +130,14 @@ def test_rng_matches_reference_known_answers(golden, orc):
         got = np.empty(1001)
         sp._check(sp.lib.spconv_random_normal(seed, 1001, got.ctypes.data))
         assert np.array_equal(got.view(np.uint64), orc.random_normal(seed, 1001).view(np.uint64))
+
+
+def test_coo_checks_before_any_device_work():
+    """spconv_matrix_from_coo: Triplets' dimension and range checks, same
+    messages, raised on the host (runs without a GPU)."""
+    with pytest.raises(ValueError, match=r"^Triplets: dimensions must be at least 1x1, got 0x3$"):
+        sp.compile_triplets(0, 3, [], [], [])
+    with pytest.raises(ValueError, match=r"^Triplets: entry \(2, 5\) outside 3x5$"):
+        sp.compile_triplets(3, 5, [0, 2], [1, 5], [1.0, 2.0])
+    with pytest.raises(ValueError, match="layout must be 0"):
+        sp.compile_triplets(3, 5, [0], [1], [1.0], layout=3)
