@@ -96,6 +96,26 @@ struct Transform {
 
 enum class TransformRoute { Spgemm, ColumnGather };
 
+/// P (inc/conv.hpp:125-135): the padding selector, built on the device.
+inline SparseMatrix build_padding_matrix(const ConvSpec& spec, Layout layout = Layout::CSR) {
+    spconv_csr* h = nullptr;
+    detail::check(spconv_build_padding_matrix(spec.m, spec.n, spec.k, spec.s, spec.p, layout == Layout::CSR ? 0 : 1,
+                                              detail::default_device(), nullptr, &h));
+    return SparseMatrix(h);
+}
+
+/// C (inc/conv.hpp:141-162): every tap of every placement, zeros included,
+/// built on the device.  build_transform == spgemm(C, P) (its Spgemm route).
+inline SparseMatrix build_conv_matrix(const Kernel& kern, const ConvSpec& spec, Layout layout = Layout::CSR) {
+    if (kern.k != spec.k)
+        throw std::invalid_argument("build_conv_matrix: kernel side " + std::to_string(kern.k) +
+                                    " does not match spec " + spec.str());
+    spconv_csr* h = nullptr;
+    detail::check(spconv_build_conv_matrix(spec.m, spec.n, spec.k, spec.s, spec.p, kern.values.data(),
+                                           layout == Layout::CSR ? 0 : 1, detail::default_device(), nullptr, &h));
+    return SparseMatrix(h);
+}
+
 /// One-time on-device build of T (replaces inc/conv.hpp:179-204).  Entries
 /// are stored where the double tap is non-zero, with their exact double
 /// values (ptr/idx/val, write_transform and convolve match the reference bit

@@ -222,6 +222,17 @@ inline SparseMatrix relayout(const SparseMatrix& m, Layout layout) {
     return SparseMatrix(h);
 }
 
+/// spgemm (inc/sparse.hpp:296-342), on the device: the reference's Gustavson
+/// sums bit for bit in fp64, exact zeros dropped.
+inline SparseMatrix spgemm(const SparseMatrix& a, const SparseMatrix& b, Layout out_layout = Layout::CSR) {
+    if (a.cols() != b.rows())
+        throw std::invalid_argument("spgemm: inner dimensions differ, " + std::to_string(a.cols()) + " vs " +
+                                    std::to_string(b.rows()));
+    spconv_csr* h = nullptr;
+    detail::check(spconv_spgemm(a.handle(), b.handle(), out_layout == Layout::CSR ? 0 : 1, nullptr, &h));
+    return SparseMatrix(h);
+}
+
 /// y = M x (inc/sparse.hpp:214-261).  `threads` is accepted for source
 /// compatibility and ignored: the product runs on the GPU.
 inline DenseVector spmv(const SparseMatrix& m, std::span<const double> x, int threads = 0) {

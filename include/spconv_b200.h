@@ -125,6 +125,26 @@ int spconv_csr_from_host(int64_t rows, int64_t cols, const int64_t* row_ptr,
 int spconv_matrix_from_coo(int64_t rows, int64_t cols, int64_t n, const int64_t* row, const int64_t* col,
                            const double* vals, int layout, int device, void* stream, spconv_csr** out);
 
+/* spgemm(a, b, layout) (inc/sparse.hpp:296-342) on the device: the products
+ * a_ik * b_kj expanded in the reference's order (a's row entries ascending,
+ * then b's row k ascending), stable-sorted by (i, j), each run summed in that
+ * order from 0.0 with one rounded multiply and one rounded add per product
+ * (the reference's Gustavson accumulator, bit for bit), entries that sum to
+ * exactly 0.0 dropped.  Operands' exact doubles are used when they keep them.
+ * "spgemm: inner dimensions differ, X vs Y" (status 1). */
+int spconv_spgemm(const spconv_csr* a, const spconv_csr* b, int layout, void* stream, spconv_csr** out);
+
+/* build_padding_matrix(spec, layout) (inc/conv.hpp:125-135): the selector P,
+ * (m+2p)(n+2p) x mn, one 1.0 per input pixel; built on the device. */
+int spconv_build_padding_matrix(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p, int layout, int device,
+                                void* stream, spconv_csr** out);
+
+/* build_conv_matrix(kernel, spec, layout) (inc/conv.hpp:141-162): C,
+ * m_out*n_out x (m+2p)(n+2p), all k*k taps per row (zeros included) at their
+ * padded-grid columns; built on the device, exact doubles kept. */
+int spconv_build_conv_matrix(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p, const double* kernel_kxk,
+                             int layout, int device, void* stream, spconv_csr** out);
+
 /* rows(), cols(), nnz(): inc/sparse.hpp:121-126. */
 int spconv_csr_shape(const spconv_csr* h, int64_t* rows, int64_t* cols, int64_t* nnz);
 

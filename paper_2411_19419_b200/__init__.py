@@ -70,6 +70,9 @@ _decl("spconv_csr_write_text", [_vp, C.c_int, _vp, _i64, _P(_i64)])
 _decl("spconv_transform_read", [_vp, _i64, C.c_int, _vp, _P(_vp)])
 _decl("spconv_sparse_read", [_vp, _i64, C.c_int, C.c_int, _vp, _P(_vp)])
 _decl("spconv_matrix_from_coo", [_i64, _i64, _i64, _vp, _vp, _vp, C.c_int, C.c_int, _vp, _P(_vp)])
+_decl("spconv_spgemm", [_vp, _vp, C.c_int, _vp, _P(_vp)])
+_decl("spconv_build_padding_matrix", [_i64] * 5 + [C.c_int, C.c_int, _vp, _P(_vp)])
+_decl("spconv_build_conv_matrix", [_i64] * 5 + [_vp, C.c_int, C.c_int, _vp, _P(_vp)])
 _decl("spconv_csr_free", [_vp])
 _decl("spconv_build_transform", [_i64] * 5 + [_vp, C.c_int, C.c_int, _vp, _P(_vp)])
 _decl("spconv_build_transform_f64", [_i64] * 5 + [_vp, C.c_int, C.c_int, _vp, _P(_vp)])
@@ -290,6 +293,33 @@ def compile_triplets(rows: int, cols: int, row, col, val, layout: int = Layout.C
     h = _vp()
     _check(lib.spconv_matrix_from_coo(rows, cols, r.size, r.ctypes.data, c.ctypes.data, v.ctypes.data, layout,
                                       device, _stream_handle(stream), C.byref(h)))
+    return Transform(h.value, None, device)
+
+
+def spgemm(a: Transform, b: Transform, layout: int = Layout.CSR, stream=None) -> Transform:
+    """spgemm (inc/sparse.hpp:296-342) on the device, bit-exact in fp64."""
+    h = _vp()
+    _check(lib.spconv_spgemm(a._h, b._h, layout, _stream_handle(stream), C.byref(h)))
+    return Transform(h.value, None, a.device)
+
+
+def build_padding_matrix(spec: ConvSpec, layout: int = Layout.CSR, device: int = 0, stream=None) -> Transform:
+    """P (inc/conv.hpp:125-135), built on the device."""
+    h = _vp()
+    _check(lib.spconv_build_padding_matrix(spec.m, spec.n, spec.k, spec.s, spec.p, layout, device,
+                                           _stream_handle(stream), C.byref(h)))
+    return Transform(h.value, None, device)
+
+
+def build_conv_matrix(kern: Kernel, spec: ConvSpec, layout: int = Layout.CSR, device: int = 0,
+                      stream=None) -> Transform:
+    """C (inc/conv.hpp:141-162), zero taps stored, built on the device."""
+    if kern.k != spec.k:
+        raise ValueError(f"build_conv_matrix: kernel side {kern.k} does not match spec {spec.str()}")
+    k64 = np.ascontiguousarray(kern.values, np.float64)
+    h = _vp()
+    _check(lib.spconv_build_conv_matrix(spec.m, spec.n, spec.k, spec.s, spec.p, k64.ctypes.data, layout, device,
+                                        _stream_handle(stream), C.byref(h)))
     return Transform(h.value, None, device)
 
 

@@ -1159,6 +1159,149 @@ int spconv_matrix_from_coo(int64_t rows, int64_t cols, int64_t n, const int64_t*
     return SPCONV_OK;
 }
 
+// A generic handle with row-major arrays for `nnz` entries over rows x cols
+// (+ fp64 values when `exact64`), same slack conventions as the uploads.
+static int new_generic(int64_t rows, int64_t cols, int64_t nnz, bool exact64, int device, spconv_csr** out) {
+    auto* h = new (std::nothrow) spconv_csr();
+    if (!h) return fail(SPCONV_ECUDA, "out of host memory");
+    h->device = device;
+    h->rows = rows;
+    h->cols = cols;
+    h->nnz = nnz;
+    const size_t pb = ((size_t)(rows + 1) * 4 + 255) & ~size_t(255);
+    const size_t ib = ((size_t)std::max<int64_t>(nnz, 1) * 4 + 255) & ~size_t(255);
+    char* mem = nullptr;
+    cudaError_t e = cudaMalloc(&mem, pb + 2 * ib + 256);
+    if (e == cudaSuccess) {
+        h->row_ptr = reinterpret_cast<int32_t*>(mem);
+        h->col_idx = reinterpret_cast<int32_t*>(mem + pb);
+        h->vals = reinterpret_cast<float*>(mem + pb + ib);
+        if (exact64) e = cudaMalloc(&h->vals64, (size_t)std::max<int64_t>(nnz, 1) * 8);
+    }
+    if (e != cudaSuccess) {
+        spconv_csr_free(h);
+        return cuda_fail(e, "cudaMalloc(matrix)");
+    }
+    *out = h;
+    return SPCONV_OK;
+}
+
+// A CSR handle returned in `layout`: CSC goes through relayout.
+static int finish_layout(spconv_csr* h, int layout, void* stream, spconv_csr** out) {
+    if (layout == 0) {
+        *out = h;
+        return SPCONV_OK;
+    }
+    const int rc = spconv_relayout(h, 1, stream, out);
+    const std::string msg = rc ? g_err : std::string();
+    spconv_csr_free(h);
+    return rc ? fail(rc, msg) : SPCONV_OK;
+}
+
+int spconv_spgemm(const spconv_csr* a, const spconv_csr* b, int layout, void* stream, spconv_csr** out) {
+    if (!a || !b || !out) return fail(SPCONV_EINVAL, "spconv_spgemm: null argument");
+    *out = nullptr;
+    if (layout != 0 && layout != 1) return fail(SPCONV_EINVAL, "spconv_spgemm: layout must be 0 (csr) or 1 (csc)");
+    if (a->cols != b->rows)
+        return fail(SPCONV_EINVAL, "spgemm: inner dimensions differ, " + std::to_string(a->cols) + " vs " +
+                                       std::to_string(b->rows));
+    if (a->device != b->device) return fail(SPCONV_EINVAL, "spconv_spgemm: operands on different devices");
+    if ((unsigned long long)a->rows * (unsigned long long)b->cols >= (1ull << 62))
+        return fail(SPCONV_EINVAL, "spconv_spgemm: result too large");
+    DeviceGuard dg(a->device);
+    if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    CK(cudaDeviceSynchronize());  // the operands' builds are complete
+    spb::SpgemmIn A{a->rows, a->cols, a->nnz, a->row_ptr, a->col_idx, a->vals, a->vals64};
+    spb::SpgemmIn B{b->rows, b->cols, b->nnz, b->row_ptr, b->col_idx, b->vals, b->vals64};
+    spb::SpgemmOut o{};
+    cudaError_t e = spb::spgemm_device(A, B, &o, st);
+    if (e == cudaErrorInvalidValue) return fail(SPCONV_EINVAL, "spconv_spgemm: more than 2^31 partial products");
+    CK(e);
+    bool inexact = false;
+    e = spb::spgemm_inexact(o, &inexact, st);
+    spconv_csr* h = nullptr;
+    int rc = e == cudaSuccess ? SPCONV_OK : cuda_fail(e, "spconv_spgemm");
+    if (rc == SPCONV_OK && o.nnz >= (1ll << 31)) rc = fail(SPCONV_EINVAL, "spconv_spgemm: result exceeds int32");
+    if (rc == SPCONV_OK) rc = new_generic(a->rows, b->cols, o.nnz, inexact, a->device, &h);
+    if (rc == SPCONV_OK) {
+        int maxlen = 0;
+        e = spb::spgemm_finish(o, a->rows, b->cols, h->row_ptr, h->col_idx, h->vals, h->vals64, &maxlen, st);
+        h->k2max = maxlen;
+        if (e != cudaSuccess) {
+            spconv_csr_free(h);
+            rc = cuda_fail(e, "spconv_spgemm");
+        }
+    }
+    if (o.mem) cudaFreeAsync(o.mem, st);
+    cudaStreamSynchronize(st);
+    if (rc != SPCONV_OK) return rc;
+    return finish_layout(h, layout, stream, out);
+}
+
+int spconv_build_padding_matrix(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p, int layout, int device,
+                                void* stream, spconv_csr** out) {
+    if (!out) return fail(SPCONV_EINVAL, "spconv_build_padding_matrix: null argument");
+    *out = nullptr;
+    if (int rc = check_spec(m, n, k, s, p)) return rc;
+    if (layout != 0 && layout != 1) return fail(SPCONV_EINVAL, "spconv_build_padding_matrix: layout must be 0 or 1");
+    const int64_t rows = (m + 2 * p) * (n + 2 * p);
+    if (rows >= (1ll << 31)) return fail(SPCONV_EINVAL, "spconv_build_padding_matrix: exceeds the int32 range");
+    DeviceGuard dg(device);
+    if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
+    spconv_csr* h = nullptr;
+    if (int rc = new_generic(rows, m * n, m * n, false, device, &h)) return rc;
+    h->k2max = 1;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaError_t e = spb::launch_padding_matrix((int)m, (int)n, (int)p, rows, h->row_ptr, h->col_idx, h->vals, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+        spconv_csr_free(h);
+        return cuda_fail(e, "spconv_build_padding_matrix");
+    }
+    return finish_layout(h, layout, stream, out);
+}
+
+int spconv_build_conv_matrix(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p, const double* kernel_kxk,
+                             int layout, int device, void* stream, spconv_csr** out) {
+    if (!out || !kernel_kxk) return fail(SPCONV_EINVAL, "spconv_build_conv_matrix: null argument");
+    *out = nullptr;
+    if (int rc = check_spec(m, n, k, s, p)) return rc;
+    if (layout != 0 && layout != 1) return fail(SPCONV_EINVAL, "spconv_build_conv_matrix: layout must be 0 or 1");
+    const Geom g = make_geom(m, n, k, s, p);
+    const int64_t rows = g.mo * g.no, cols = (m + 2 * p) * (n + 2 * p);
+    if (cols >= (1ll << 31) || rows * k * k >= (1ll << 31))
+        return fail(SPCONV_EINVAL, "spconv_build_conv_matrix: exceeds the int32 range");
+    std::vector<float> t32((size_t)(k * k));
+    bool exact = true;
+    for (int64_t q = 0; q < k * k; ++q) {
+        t32[(size_t)q] = (float)kernel_kxk[q];
+        exact &= __builtin_bit_cast(uint64_t, (double)t32[(size_t)q]) == __builtin_bit_cast(uint64_t, kernel_kxk[q]);
+    }
+    DeviceGuard dg(device);
+    if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
+    spconv_csr* h = nullptr;
+    if (int rc = new_generic(rows, cols, rows * k * k, !exact, device, &h)) return rc;
+    h->k2max = (int)(k * k);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    char* tt = nullptr;
+    cudaError_t e = cudaMallocAsync(&tt, (size_t)(k * k) * 12 + 256, st);
+    float* d32 = reinterpret_cast<float*>(tt);
+    double* d64 = reinterpret_cast<double*>(tt + (((size_t)(k * k) * 4 + 255) & ~size_t(255)));
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d32, t32.data(), (size_t)(k * k) * 4, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d64, kernel_kxk, (size_t)(k * k) * 8, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess)
+        e = spb::launch_conv_matrix((int)k, (int)s, (int)p, (int)n, (int)g.no, rows, d32, d64, h->row_ptr,
+                                    h->col_idx, h->vals, h->vals64, st);
+    if (tt) cudaFreeAsync(tt, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+        spconv_csr_free(h);
+        return cuda_fail(e, "spconv_build_conv_matrix");
+    }
+    return finish_layout(h, layout, stream, out);
+}
+
 int spconv_csr_shape(const spconv_csr* h, int64_t* rows, int64_t* cols, int64_t* nnz) {
     if (!h) return fail(SPCONV_EINVAL, "null handle");
     if (rows) *rows = h->rows;

@@ -145,6 +145,30 @@ cudaError_t launch_tiled(const TiledParams& tp, const CUtensorMap* tmap, int bt,
                          cudaStream_t st);
 cudaError_t launch_generic(const GenericParams& gp, cudaStream_t st);
 cudaError_t launch_rowblock(GenericParams gp, int kmax, cudaStream_t st);  // rows of <= 64 entries
+// spgemm on the device (coo.cu): the operands' row-major arrays (fp64 values
+// when the handle keeps them, else fp32 widened).
+struct SpgemmIn {
+    long long rows, cols, nnz;
+    const int32_t* ptr;
+    const int32_t* idx;
+    const float* v32;
+    const double* v64;
+};
+struct SpgemmOut {
+    long long nnz, max_len;
+    unsigned long long* keys_buf;  // sorted (row * cols + col) keys of the kept entries
+    double* vals_buf;              // their sums
+    void* mem;                     // owns both (cudaFreeAsync)
+};
+cudaError_t spgemm_device(const SpgemmIn& A, const SpgemmIn& B, SpgemmOut* out, cudaStream_t st);
+cudaError_t spgemm_finish(const SpgemmOut& o, long long nrows, long long ncols, int32_t* ptr, int32_t* idx, float* v32,
+                          double* v64, int* max_len, cudaStream_t st);
+cudaError_t spgemm_inexact(const SpgemmOut& o, bool* inexact, cudaStream_t st);
+cudaError_t launch_padding_matrix(int m, int n, int p, long long rows, int32_t* ptr, int32_t* idx, float* val,
+                                  cudaStream_t st);
+cudaError_t launch_conv_matrix(int k, int s, int p, int n, int no, long long rows, const float* t32,
+                               const double* t64, int32_t* ptr, int32_t* idx, float* v32, double* v64,
+                               cudaStream_t st);
 // SparseMatrix::compile of host triplets on the device (coo.cu).
 cudaError_t coo_compile(long long n, const int64_t* r_host, const int64_t* c_host, const double* v_host,
                         int64_t rows, int64_t cols, bool by_row, int32_t* ptr, int32_t* idx, float* v32,

@@ -83,3 +83,77 @@ def test_duplicates_rejected_like_compile(sp, layout, want):
     c = np.array([1, 0, 4, 1, 4, 2])
     with pytest.raises(ValueError, match="^" + re.escape("SparseMatrix: duplicate entry at " + want) + "$"):
         sp.compile_triplets(6, 6, r, c, np.ones(6), layout)
+
+
+# ---------------------------------------------------------------------------
+# spgemm and the factor matrices (inc/sparse.hpp:296-342, inc/conv.hpp:125-162)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("spec", [(9, 7, 3, 1, 1), (20, 17, 5, 2, 2), (12, 9, 4, 3, 2), (6, 6, 1, 1, 2)])
+@pytest.mark.parametrize("double_taps", [False, True])
+def test_spgemm_route_equals_build_transform(sp, ref, spec, double_taps):
+    """The reference's Spgemm route: spgemm(build_conv_matrix, build_padding_matrix)
+    == build_transform, bit for bit -- zero taps dropped by the accumulator,
+    exact doubles kept -- and == the reference's own build."""
+    m, n, k, s, p = spec
+    rng = np.random.default_rng(k * 11 + s)
+    kern = rng.standard_normal(k * k)
+    if not double_taps:
+        kern = kern.astype(np.float32).astype(np.float64)
+    if k > 1:
+        kern[0] = 0.0
+        kern[-1] = -0.0
+    cs = sp.ConvSpec(*spec)
+    C = sp.build_conv_matrix(sp.Kernel(k, kern), cs)
+    P = sp.build_padding_matrix(cs)
+    assert (C.rows, C.cols, C.nnz) == (cs.m_out * cs.n_out, (m + 2 * p) * (n + 2 * p), cs.m_out * cs.n_out * k * k)
+    assert (P.rows, P.cols, P.nnz) == ((m + 2 * p) * (n + 2 * p), m * n, m * n)
+    T = sp.spgemm(C, P)
+    B = sp.build_transform(sp.Kernel(k, kern), cs)
+    for a, b in zip(T.export(), B.export()):
+        assert np.array_equal(a.view(np.uint64) if a.dtype == np.float64 else a,
+                              b.view(np.uint64) if b.dtype == np.float64 else b)
+    rp, ri, rv = ref.build(*spec, kern).export()
+    gp, gi, gv = T.export()
+    assert np.array_equal(gp, rp) and np.array_equal(gi[:rp[-1]], ri) and np.array_equal(u64(gv[:rp[-1]]), u64(rv))
+    Tc = sp.spgemm(C, P, layout=1)
+    assert Tc.layout == 1 and np.array_equal(Tc.export()[0], ref.build(*spec, kern, layout=1).export()[0])
+
+
+def test_spgemm_random_matches_gustavson(sp):
+    """Random operands with cancellations and zeros: the reference's Gustavson
+    loop restated in Python (sequential fp64 sums in A-then-B order)."""
+    rng = np.random.default_rng(12)
+    def rand(rows, cols, dens):
+        d = rng.standard_normal((rows, cols)) * (rng.random((rows, cols)) < dens)
+        d[rng.random((rows, cols)) < 0.05] = 0.0
+        ptr = np.concatenate([[0], np.cumsum((d != 0).sum(1))]).astype(np.int64)
+        idx = np.nonzero(d)[1].astype(np.int64)
+        return ptr, idx, d[d != 0]
+    ap, ai, av = rand(33, 40, 0.2)
+    bp, bi, bv = rand(40, 27, 0.25)
+    bv[::9] = -av[0] if av.size else 1.0  # invite exact cancellations
+    A = sp.Transform.from_host(33, 40, ap, ai, av)
+    B = sp.Transform.from_host(40, 27, bp, bi, bv)
+    G = sp.spgemm(A, B)
+    want_p, want_i, want_v = [0], [], []
+    for i in range(33):
+        acc, order = {}, []
+        for ka in range(ap[i], ap[i + 1]):
+            k, a = ai[ka], av[ka]
+            for kb in range(bp[k], bp[k + 1]):
+                j = bi[kb]
+                if j not in acc:
+                    acc[j] = 0.0
+                    order.append(j)
+                acc[j] = acc[j] + a * bv[kb]
+        for j in sorted(order):
+            if acc[j] != 0.0:
+                want_i.append(j)
+                want_v.append(acc[j])
+        want_p.append(len(want_i))
+    gp, gi, gv = G.export()
+    assert np.array_equal(gp, want_p) and np.array_equal(gi[:len(want_i)], want_i)
+    assert np.array_equal(u64(gv[:len(want_v)]), u64(np.array(want_v)))
+    with pytest.raises(ValueError, match=r"^spgemm: inner dimensions differ, 40 vs 33$"):
+        sp.spgemm(A, G)
