@@ -222,6 +222,61 @@ inline SparseMatrix relayout(const SparseMatrix& m, Layout layout) {
     return SparseMatrix(h);
 }
 
+/// transposed / pruned / hstack_blocks / vstack_blocks (inc/sparse.hpp:276-395):
+/// the entries restaged as Triplets and compiled on the device (same checks,
+/// messages and results).
+inline SparseMatrix transposed(const SparseMatrix& m) {
+    Triplets t(m.cols(), m.rows());
+    t.reserve(static_cast<std::size_t>(m.nnz()));
+    for (const Entry& e : m.entries()) t.add(e.col, e.row, e.value);
+    return SparseMatrix::compile(t, m.layout());
+}
+
+inline SparseMatrix pruned(const SparseMatrix& m) {
+    Triplets t(m.rows(), m.cols());
+    t.reserve(static_cast<std::size_t>(m.nnz()));
+    for (const Entry& e : m.entries())
+        if (e.value != 0.0) t.add(e.row, e.col, e.value);
+    return SparseMatrix::compile(t, m.layout());
+}
+
+namespace detail {
+// hstack (along = true: columns) / vstack: shared checks, offsets, compile.
+inline SparseMatrix stack_blocks(std::span<const SparseMatrix> blocks, Layout out_layout, bool along_cols) {
+    const char* name = along_cols ? "hstack_blocks" : "vstack_blocks";
+    if (blocks.empty()) throw std::invalid_argument(std::string(name) + ": no blocks");
+    const index_t shared = along_cols ? blocks[0].rows() : blocks[0].cols();
+    index_t extent = 0;
+    std::size_t nnz = 0;
+    for (std::size_t b = 0; b < blocks.size(); ++b) {
+        const index_t have = along_cols ? blocks[b].rows() : blocks[b].cols();
+        if (have != shared)
+            throw std::invalid_argument(std::string(name) + ": block " + std::to_string(b) + " has " +
+                                        std::to_string(have) + (along_cols ? " rows" : " cols") + ", expected " +
+                                        std::to_string(shared));
+        extent += along_cols ? blocks[b].cols() : blocks[b].rows();
+        nnz += static_cast<std::size_t>(blocks[b].nnz());
+    }
+    Triplets t(along_cols ? shared : extent, along_cols ? extent : shared);
+    t.reserve(nnz);
+    index_t off = 0;
+    for (const SparseMatrix& blk : blocks) {
+        for (const Entry& e : blk.entries())
+            t.add(along_cols ? e.row : off + e.row, along_cols ? off + e.col : e.col, e.value);
+        off += along_cols ? blk.cols() : blk.rows();
+    }
+    return SparseMatrix::compile(t, out_layout);
+}
+}  // namespace detail
+
+inline SparseMatrix hstack_blocks(std::span<const SparseMatrix> blocks, Layout out_layout = Layout::CSR) {
+    return detail::stack_blocks(blocks, out_layout, true);
+}
+
+inline SparseMatrix vstack_blocks(std::span<const SparseMatrix> blocks, Layout out_layout = Layout::CSR) {
+    return detail::stack_blocks(blocks, out_layout, false);
+}
+
 /// spgemm (inc/sparse.hpp:296-342), on the device: the reference's Gustavson
 /// sums bit for bit in fp64, exact zeros dropped.
 inline SparseMatrix spgemm(const SparseMatrix& a, const SparseMatrix& b, Layout out_layout = Layout::CSR) {

@@ -290,6 +290,37 @@ int main() {
         "SparseMatrix: duplicate entry at (1, 1)");
     expect_throw<std::invalid_argument>([] { Triplets(2, 2).add(2, 0, 1.0); }, "Triplets: entry (2, 0) outside 2x2");
 
+    // transposed / pruned / hstack / vstack (inc/sparse.hpp:276-395) and the
+    // Spgemm route's pieces on the device: spgemm(C, P) == build_transform
+    {
+        Triplets t(2, 3);
+        t.add(0, 2, 1.5);
+        t.add(1, 0, 0.0);
+        t.add(1, 1, -2.0);
+        const SparseMatrix a = SparseMatrix::compile(t, Layout::CSR);
+        const SparseMatrix at = transposed(a);
+        CHECK(at.rows() == 3 && at.cols() == 2 && (at.ptr() == std::vector<index_t>{0, 1, 2, 3}));
+        CHECK((at.idx() == std::vector<index_t>{1, 1, 0}) && (at.val() == std::vector<double>{0.0, -2.0, 1.5}));
+        CHECK(pruned(a).nnz() == 2);
+        const std::vector<SparseMatrix> bl{a, a};
+        const SparseMatrix h = hstack_blocks(bl);
+        CHECK(h.rows() == 2 && h.cols() == 6 && (h.idx() == std::vector<index_t>{2, 5, 0, 1, 3, 4}));
+        const SparseMatrix v = vstack_blocks(bl, Layout::CSC);
+        CHECK(v.rows() == 4 && v.cols() == 3 && v.layout() == Layout::CSC && v.nnz() == 6);
+        const ConvSpec spec(7, 6, 3, 2, 1);
+        const Kernel kern = random_normal_kernel(3, 5);
+        const SparseMatrix T = spgemm(build_conv_matrix(kern, spec), build_padding_matrix(spec));
+        const Transform B = build_transform(kern, spec);
+        CHECK(T.ptr() == B.matrix.ptr() && T.idx() == B.matrix.idx() && T.val() == B.matrix.val());
+    }
+    expect_throw<std::invalid_argument>(
+        [] {
+            const std::vector<SparseMatrix> bl{SparseMatrix::compile(Triplets(2, 2), Layout::CSR),
+                                               SparseMatrix::compile(Triplets(3, 2), Layout::CSR)};
+            hstack_blocks(bl);
+        },
+        "hstack_blocks: block 1 has 3 rows, expected 2");
+
     if (g_fail) {
         std::fprintf(stderr, "%d failure(s)\n", g_fail);
         return 1;
