@@ -706,8 +706,24 @@ int spconv_nnz_bound(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p, int6
     return SPCONV_OK;
 }
 
+// Exact-fp64 fill of a tag build (spconv_build_transform_f64): device tables
+// of the taps' fp32 / fp64 values; `done` = the build kernel wrote vals64.
+struct F64Fill {
+    const float* t32;   // host k*k
+    const double* t64;  // host k*k
+    bool done;
+};
+
+static int build_csr_impl(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p, const float* kernel_kxk, int device,
+                          void* stream, spconv_csr** out, F64Fill* f64);
+
 int spconv_build_csr(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
                      const float* kernel_kxk, int device, void* stream, spconv_csr** out) {
+    return build_csr_impl(m, n, k, s, p, kernel_kxk, device, stream, out, nullptr);
+}
+
+static int build_csr_impl(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p, const float* kernel_kxk, int device,
+                          void* stream, spconv_csr** out, F64Fill* f64) {
     if (int rc = check_spec(m, n, k, s, p)) return rc;
     if (!kernel_kxk || !out) return fail(SPCONV_EINVAL, "spconv_build_csr: null argument");
     *out = nullptr;
@@ -828,7 +844,17 @@ int spconv_build_csr(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
         return fail(SPCONV_EINVAL, "spconv_build_csr: kernel side " + std::to_string(k) +
                                        " too large for the device build");
     }
-    e = spb::launch_csr_build(bp, ht.nonzero, block, smem, st);
+    if (f64) {  // exact values: vals64 (written by the fill, or by the caller's retag pass)
+        e = cudaMallocAsync(&h->vals64, (size_t)std::max<int64_t>(ht.nnz, 1) * 8, st);
+        if (k * k <= 25) {  // the fill's tables ride in the parameters (k <= 5)
+            std::copy(f64->t32, f64->t32 + k * k, bp.f64_t32);
+            std::copy(f64->t64, f64->t64 + k * k, bp.f64_t64);
+            bp.vals64 = h->vals64;
+        }
+    }
+    bool f64_done = false;
+    if (e == cudaSuccess) e = spb::launch_csr_build(bp, ht.nonzero, block, smem, &f64_done, st);
+    if (f64) f64->done = f64_done;
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     if (e == cudaSuccess) e = cudaStreamIsCapturing(st, &cap);
     if (e == cudaSuccess && cap == cudaStreamCaptureStatusNone) {  // (a captured build has no event)
@@ -838,6 +864,7 @@ int spconv_build_csr(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
     if (tab) cudaFreeAsync(tab, st);
     if (e != cudaSuccess) {
         if (h->built) cudaEventDestroy(h->built);
+        if (h->vals64) cudaFreeAsync(h->vals64, st);
         cudaFreeAsync(csr, st);
         cudaStreamSynchronize(st);
         delete h;
@@ -884,34 +911,47 @@ int spconv_build_transform_f64(int64_t m, int64_t n, int64_t k, int64_t s, int64
     if (exact)  // every tap is an fp32 number: the fp32 build is already exact
         return spconv_build_transform(m, n, k, s, p, t32.data(), layout, device, stream, out);
     // Build the structure from tags (q + 1 where the DOUBLE tap is non-zero,
-    // inc/sparse.hpp:335), then swap the tags for the values on the device.
+    // inc/sparse.hpp:335).  The persistent build (k <= 5) writes the real fp32
+    // values and the exact doubles from its staging; other builds get a
+    // tag -> value pass afterwards (retag_kernel).
     std::vector<float> tag((size_t)kk);
     for (int64_t q = 0; q < kk; ++q) tag[(size_t)q] = kernel_kxk[q] != 0.0 ? (float)(q + 1) : 0.0f;
-    spconv_csr* h = nullptr;
-    if (int rc = spconv_build_transform(m, n, k, s, p, tag.data(), layout, device, stream, &h)) return rc;
     DeviceGuard dg(device);
+    if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    F64Fill fill{t32.data(), kernel_kxk, false};
+    spconv_csr* h = nullptr;
+    if (int rc = build_csr_impl(m, n, k, s, p, tag.data(), device, stream, &h, &fill)) return rc;
+    int rc = SPCONV_OK;
+    if (layout == 1) rc = attach_csc_conv(h, st);  // (from the tags in h->taps)
+    // device tables of the values for the retag passes (none needed when the
+    // fill wrote them and there is no CSC storage)
+    const bool need_tables = !fill.done || h->layout == 1;
     const size_t t32_bytes = ((size_t)kk * 4 + 255) & ~size_t(255);
     char* tt = nullptr;
-    cudaError_t e = cudaMallocAsync(&tt, t32_bytes + (size_t)kk * 8, st);
-    const size_t vb = (size_t)std::max<int64_t>(h->nnz, 1) * 8;
-    if (e == cudaSuccess) e = cudaMallocAsync(&h->vals64, vb, st);
-    if (e == cudaSuccess && h->layout == 1) e = cudaMallocAsync(&h->csc_vals64, vb, st);
-    // (pageable sources: staged by the driver before each call returns)
-    if (e == cudaSuccess) e = cudaMemcpyAsync(tt, t32.data(), (size_t)kk * 4, cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess)
-        e = cudaMemcpyAsync(tt + t32_bytes, kernel_kxk, (size_t)kk * 8, cudaMemcpyHostToDevice, st);
+    cudaError_t e = rc || !need_tables ? cudaSuccess : cudaMallocAsync(&tt, t32_bytes + (size_t)kk * 8, st);
     const float* d32 = reinterpret_cast<const float*>(tt);
     const double* d64 = reinterpret_cast<const double*>(tt + t32_bytes);
-    if (e == cudaSuccess) e = spb::launch_retag(h->vals, h->vals64, h->nnz, d32, d64, st);
-    if (e == cudaSuccess && h->layout == 1) e = spb::launch_retag(h->csc_vals, h->csc_vals64, h->nnz, d32, d64, st);
+    // (pageable sources: staged by the driver before each call returns)
+    if (!rc && e == cudaSuccess && need_tables) e = cudaMemcpyAsync(tt, t32.data(), (size_t)kk * 4, cudaMemcpyHostToDevice, st);
+    if (!rc && e == cudaSuccess && need_tables)
+        e = cudaMemcpyAsync(tt + t32_bytes, kernel_kxk, (size_t)kk * 8, cudaMemcpyHostToDevice, st);
+    const size_t vb = (size_t)std::max<int64_t>(h->nnz, 1) * 8;
+    if (rc == SPCONV_OK && e == cudaSuccess && !fill.done) e = spb::launch_retag(h->vals, h->vals64, h->nnz, d32, d64, st);
+    if (rc == SPCONV_OK && e == cudaSuccess && h->layout == 1) {
+        e = cudaMallocAsync(&h->csc_vals64, vb, st);
+        if (e == cudaSuccess) e = spb::launch_retag(h->csc_vals, h->csc_vals64, h->nnz, d32, d64, st);
+    }
     // the device taps (band check, CSC rebuilds) become the real fp32 taps
-    if (e == cudaSuccess) e = cudaMemcpyAsync(h->taps, d32, (size_t)kk * 4, cudaMemcpyDeviceToDevice, st);
-    if (e == cudaSuccess && h->built) e = cudaEventRecord(h->built, st);  // side checks see the final values
+    if (rc == SPCONV_OK && e == cudaSuccess)
+        e = need_tables ? cudaMemcpyAsync(h->taps, d32, (size_t)kk * 4, cudaMemcpyDeviceToDevice, st)
+                        : cudaMemcpyAsync(h->taps, t32.data(), (size_t)kk * 4, cudaMemcpyHostToDevice, st);
+    if (rc == SPCONV_OK && e == cudaSuccess && h->built) e = cudaEventRecord(h->built, st);  // side checks see the values
     if (tt) cudaFreeAsync(tt, st);
-    if (e != cudaSuccess) {
+    if (rc != SPCONV_OK || e != cudaSuccess) {
+        const std::string msg = rc ? g_err : std::string();
         spconv_csr_free(h);
-        return cuda_fail(e, "spconv_build_transform_f64");
+        return rc ? fail(rc, msg) : cuda_fail(e, "spconv_build_transform_f64");
     }
     h->host_taps = t32;
     h->host_taps64.assign(kernel_kxk, kernel_kxk + kk);

@@ -358,7 +358,7 @@ __global__ void __launch_bounds__(256) csr_build_warp(const BuildParams P) {
 // shared memory -- so there is no scan: a tile costs two CTA barriers, and
 // the TMA bulk store of tile t drains while tile t + 1 is generated in the
 // other staging buffer.
-template <int KC, bool DENSE>
+template <int KC, bool DENSE, bool F64 = false>
 __global__ void __launch_bounds__(256) csr_build_persist(const BuildParams P) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int K1 = KC + 1, KK = KC * KC, R = 256;
@@ -370,6 +370,14 @@ __global__ void __launch_bounds__(256) csr_build_persist(const BuildParams P) {
     __shared__ int s_xlo[KC], s_xhi[KC], s_ylo[KC], s_yhi[KC];
     for (int q = t; q < K1 * K1; q += R) s_sat[q] = P.small ? P.tab.sat[q] : __ldg(P.t.sat + q);
     for (int q = t; q < KK; q += R) s_taps[q] = P.small ? P.tab.taps[q] : __ldg(P.t.taps + q);
+    // F64 (exact-fp64 builds): the taps above are tags; these are their values
+    __shared__ float s_r32[F64 ? KK : 1];
+    __shared__ double s_r64[F64 ? KK : 1];
+    if (F64)
+        for (int q = t; q < KK; q += R) {
+            s_r32[q] = P.f64_t32[q];
+            s_r64[q] = P.f64_t64[q];
+        }
     for (int q = t; q < KC; q += R) {
         s_w[q] = P.small ? P.tab.w[q] : __ldg(P.t.w + q);
         // x' with tap q in J(x'): [xlo, xhi) (slides_before(x, q) = clamp(x, xlo, xhi) - xlo)
@@ -403,8 +411,10 @@ __global__ void __launch_bounds__(256) csr_build_persist(const BuildParams P) {
     int it = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         const int buf = it & 1;
-        int32_t* dcol = reinterpret_cast<int32_t*>(smem) + buf * 2 * STAGE;
+        // per buffer: col, val (STAGE words each) and, for F64, STAGE doubles
+        int32_t* dcol = reinterpret_cast<int32_t*>(smem) + buf * (F64 ? 4 : 2) * STAGE;
         float* dval = reinterpret_cast<float*>(dcol + STAGE);
+        double* dv64 = reinterpret_cast<double*>(dcol + 2 * STAGE);
         const int r0 = tile * R;
         const int r1 = min(P.rows, r0 + R);
         // this thread's row: closed-form offset, written to row_ptr now
@@ -426,8 +436,10 @@ __global__ void __launch_bounds__(256) csr_build_persist(const BuildParams P) {
         __syncthreads();
         const int base = s_base[buf], total = s_end[buf] - base;
         const int mis = base & 3;
+        const int mis64 = base & 1;  // (doubles: 16-byte phase)
         if (r < r1) {
             int o = mis + off - base;
+            int o64 = mis64 + off - base;
             const int xr = P.s * x - P.p, yc = P.s * y - P.p;
             if (DENSE && cnt == KK) {
 #pragma unroll
@@ -435,7 +447,8 @@ __global__ void __launch_bounds__(256) csr_build_persist(const BuildParams P) {
 #pragma unroll
                     for (int i = 0; i < KC; ++i) {
                         dcol[o + j * KC + i] = (xr + j) * P.n + yc + i;
-                        dval[o + j * KC + i] = s_taps[j * KC + i];
+                        dval[o + j * KC + i] = F64 ? s_r32[j * KC + i] : s_taps[j * KC + i];
+                        if (F64) dv64[o64 + j * KC + i] = s_r64[j * KC + i];
                     }
             } else {
 #pragma unroll
@@ -448,9 +461,11 @@ __global__ void __launch_bounds__(256) csr_build_persist(const BuildParams P) {
                         const bool keep = jin && i >= ilo && i < ihi && (DENSE || v != 0.0f);
                         if (keep) {
                             dcol[o] = rowbase + i;
-                            dval[o] = v;
+                            dval[o] = F64 ? s_r32[j * KC + i] : v;
+                            if (F64) dv64[o64] = s_r64[j * KC + i];
                         }
                         o += keep ? 1 : 0;
+                        o64 += keep ? 1 : 0;
                     }
                 }
             }
@@ -463,11 +478,14 @@ __global__ void __launch_bounds__(256) csr_build_persist(const BuildParams P) {
             __stcs(P.vals + base + t, dval[mis + t]);
         }
         const int nvec = (total - head) >> 2;
+        const int head64 = min(total, mis64), nvec64 = (total - head64) >> 1;  // (F64)
+        if (F64 && t < head64) __stcs(P.vals64 + base + t, dv64[mis64 + t]);
         if (t == 0) {
             if (nvec > 0) {
                 bulk_s2g(P.col_idx + base + head, dcol + mis + head, (uint32_t)nvec * 16u);
                 bulk_s2g(P.vals + base + head, dval + mis + head, (uint32_t)nvec * 16u);
             }
+            if (F64 && nvec64 > 0) bulk_s2g(P.vals64 + base + head64, dv64 + mis64 + head64, (uint32_t)nvec64 * 16u);
             bulk_commit();
         }
         const int done = head + 4 * nvec;
@@ -475,27 +493,35 @@ __global__ void __launch_bounds__(256) csr_build_persist(const BuildParams P) {
             __stcs(P.col_idx + base + done + t, dcol[mis + done + t]);
             __stcs(P.vals + base + done + t, dval[mis + done + t]);
         }
+        const int done64 = head64 + 2 * nvec64;
+        if (F64 && t < total - done64) __stcs(P.vals64 + base + done64 + t, dv64[mis64 + done64 + t]);
     }
     if (t == 0) bulk_wait_read<0>();
 }
 
-template <int KC, bool DENSE>
-static cudaError_t launch_p(const BuildParams& bp, cudaStream_t st) {
+template <int KC, bool DENSE, bool F64>
+static cudaError_t launch_p_f(const BuildParams& bp, cudaStream_t st) {
     constexpr int KK = KC * KC;
-    const size_t smem = (size_t)((256 * KK + 3 + 3) & ~3) * 4 * 2 * 2;  // 2 buffers x (col, val)
+    const size_t smem = (size_t)((256 * KK + 3 + 3) & ~3) * 4 * 2 * (F64 ? 4 : 2);  // 2 buffers
     int dev = 0, sms = 148, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    auto kern = csr_build_persist<KC, DENSE, F64>;
     cudaError_t e = cudaSuccess;
-    if (smem > 48 * 1024)
-        e = cudaFuncSetAttribute(csr_build_persist<KC, DENSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess)
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, csr_build_persist<KC, DENSE>, 256, smem);
+    if (smem > 48 * 1024) e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
     if (e != cudaSuccess) return e;
     const long long tiles = ((long long)bp.rows + 255) / 256;
     const long long grid = std::min<long long>(tiles, (long long)sms * std::max(per_sm, 1));
-    csr_build_persist<KC, DENSE><<<(unsigned)grid, 256, smem, st>>>(bp);
+    kern<<<(unsigned)grid, 256, smem, st>>>(bp);
     return cudaGetLastError();
+}
+
+template <int KC, bool DENSE>
+static cudaError_t launch_p(const BuildParams& bp, cudaStream_t st) {
+    // (F64 instantiations for k <= 5: three staged arrays per buffer)
+    if (bp.vals64 && KC <= 5) return launch_p_f<KC, DENSE, KC <= 5>(bp, st);
+    return launch_p_f<KC, DENSE, false>(bp, st);
 }
 
 template <int KC, bool DENSE>
@@ -533,8 +559,11 @@ static cudaError_t launch_k(const BuildParams& bp, int block, size_t smem, cudaS
     return cudaGetLastError();
 }
 
-cudaError_t launch_csr_build(const BuildParams& bp, bool dense, int block, size_t smem,
+cudaError_t launch_csr_build(const BuildParams& bp_in, bool dense, int block, size_t smem, bool* f64_done,
                              cudaStream_t st) {
+    // The exact-fp64 fill exists in the persistent kernel for k <= 5; other
+    // launches build the tags only (the caller retags).
+    BuildParams bp = bp_in;
     // Default: the persistent double-buffered kernel for k <= 5 (config 3
     // build 22.5 -> 18.4 us, config 2 12.3 -> 10.2 us), the block kernel for
     // larger k, whose 256-row double buffer would not leave room for a second
@@ -547,6 +576,9 @@ cudaError_t launch_csr_build(const BuildParams& bp, bool dense, int block, size_
     const bool block_build = bsel && !std::strcmp(bsel, "block");
     const bool persist_build =
         (bsel && !std::strcmp(bsel, "persist")) || (!bsel && bp.k <= 5);
+    *f64_done = false;
+    if (!(persist_build && bp.stage && bp.k <= 5 && (bp.k & 1))) bp.vals64 = nullptr;
+    *f64_done = bp.vals64 != nullptr;
     if (persist_build && bp.stage) {
         switch (bp.k) {
             case 1: return dense ? launch_p<1, true>(bp, st) : launch_p<1, false>(bp, st);

@@ -45,6 +45,12 @@ struct BuildParams {
     float* taps_out;  // k*k taps copied here by block 0 (the handle's device tap table)
     int bulk_store;   // write staged entries back with TMA bulk stores (else 16-byte st.global)
     long long nnz_total;  // total entries (the persistent build's last-tile bound)
+    // Exact-fp64 builds (spconv_build_transform_f64): the taps above are TAGS
+    // (q + 1 where the double tap is non-zero); the persistent kernel (k <= 5)
+    // writes f64_t32[q] to vals and f64_t64[q] to vals64 from its staging.
+    float f64_t32[25];   // (k <= 5: in the parameters, no copies)
+    double f64_t64[25];
+    double* vals64;
 };
 
 // CSC build (csc_build.cu): the conv transform stored column-major.
@@ -138,7 +144,7 @@ struct GenericParams {
 };
 
 // Launchers (return cudaError_t of the launch).
-cudaError_t launch_csr_build(const BuildParams& bp, bool dense, int block, size_t smem,
+cudaError_t launch_csr_build(const BuildParams& bp, bool dense, int block, size_t smem, bool* f64_done,
                              cudaStream_t st);
 cudaError_t launch_csc_build(CscParams cp, int maxc, bool dense, cudaStream_t st);  // dense: no zero taps
 cudaError_t launch_tiled(const TiledParams& tp, const CUtensorMap* tmap, int bt, size_t smem,
