@@ -846,7 +846,7 @@ static int build_csr_impl(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
     }
     if (f64) {  // exact values: vals64 (written by the fill, or by the caller's retag pass)
         e = cudaMallocAsync(&h->vals64, (size_t)std::max<int64_t>(ht.nnz, 1) * 8, st);
-        if (k * k <= 25) {  // the fill's tables ride in the parameters (k <= 5)
+        if (k * k <= 121) {  // the fill's tables ride in the parameters (k <= 11)
             std::copy(f64->t32, f64->t32 + k * k, bp.f64_t32);
             std::copy(f64->t64, f64->t64 + k * k, bp.f64_t64);
             bp.vals64 = h->vals64;

@@ -75,7 +75,7 @@ __device__ __forceinline__ int slides_before(int x, int j, int dim, int s, int p
 
 // KC = compile-time kernel side (0: runtime P.k).  DENSE: every tap is
 // non-zero, so the zero-tap test folds away.
-template <int KC, bool DENSE>
+template <int KC, bool DENSE, bool F64 = false>
 __global__ void __launch_bounds__(256) csr_build_kernel(const BuildParams P) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int s_warp[32];
@@ -158,6 +158,10 @@ __global__ void __launch_bounds__(256) csr_build_kernel(const BuildParams P) {
     int o;
     // compile-time for the unrolled k (always staged): shared, not generic, accesses
     const bool staged = KC > 0 || P.stage != 0;
+    // F64 (exact-fp64 builds, unrolled k): the fp64 values staged after dval
+    double* dv64 = reinterpret_cast<double*>(reinterpret_cast<int32_t*>(smem) + tab_words + 2 * P.stage_words);
+    const int mis64 = base & 1;
+    int o64 = mis64 + excl;
     if (staged) {
         dcol = reinterpret_cast<int32_t*>(smem) + tab_words;
         dval = reinterpret_cast<float*>(dcol) + P.stage_words;
@@ -177,7 +181,8 @@ __global__ void __launch_bounds__(256) csr_build_kernel(const BuildParams P) {
 #pragma unroll
                 for (int i = 0; i < KC; ++i) {
                     dcol[o + j * KC + i] = rowbase + i;
-                    dval[o + j * KC + i] = s_taps[j * KC + i];
+                    dval[o + j * KC + i] = F64 ? P.f64_t32[j * KC + i] : s_taps[j * KC + i];
+                    if (F64) dv64[o64 + j * KC + i] = P.f64_t64[j * KC + i];
                 }
             }
         } else if (KC) {
@@ -192,9 +197,11 @@ __global__ void __launch_bounds__(256) csr_build_kernel(const BuildParams P) {
                     const bool keep = jin && i >= ilo && i < ihi && (DENSE || v != 0.0f);
                     if (keep) {
                         dcol[o] = rowbase + i;
-                        dval[o] = v;
+                        dval[o] = F64 ? P.f64_t32[j * KC + i] : v;
+                        if (F64) dv64[o64] = P.f64_t64[j * KC + i];
                     }
                     o += keep ? 1 : 0;
+                    o64 += keep ? 1 : 0;
                 }
             }
         } else {
@@ -227,10 +234,16 @@ __global__ void __launch_bounds__(256) csr_build_kernel(const BuildParams P) {
         const float4* sval = reinterpret_cast<const float4*>(dval + mis + head);
         int4* gcol = reinterpret_cast<int4*>(P.col_idx + base + head);
         float4* gval = reinterpret_cast<float4*>(P.vals + base + head);
+        const int head64 = min(total, mis64), nvec64 = (total - head64) >> 1;  // (F64: 2 doubles / 16 B)
+        if (F64 && t < head64) __stcs(P.vals64 + base + t, dv64[mis64 + t]);
         if (P.bulk_store) {  // the 16-byte body through the TMA engine: two instructions
-            if (t == 0 && nvec > 0) {
-                bulk_s2g(gcol, scol, (uint32_t)nvec * 16u);
-                bulk_s2g(gval, sval, (uint32_t)nvec * 16u);
+            if (t == 0 && (nvec > 0 || (F64 && nvec64 > 0))) {
+                if (nvec > 0) {
+                    bulk_s2g(gcol, scol, (uint32_t)nvec * 16u);
+                    bulk_s2g(gval, sval, (uint32_t)nvec * 16u);
+                }
+                if (F64 && nvec64 > 0)
+                    bulk_s2g(P.vals64 + base + head64, dv64 + mis64 + head64, (uint32_t)nvec64 * 16u);
                 bulk_commit_wait_read();
             }
         } else {
@@ -238,12 +251,18 @@ __global__ void __launch_bounds__(256) csr_build_kernel(const BuildParams P) {
                 __stcs(gcol + q, scol[q]);
                 __stcs(gval + q, sval[q]);
             }
+            if (F64)
+                for (int q = t; q < nvec64; q += R)
+                    __stcs(reinterpret_cast<double2*>(P.vals64 + base + head64) + q,
+                           reinterpret_cast<const double2*>(dv64 + mis64 + head64)[q]);
         }
         const int done = head + 4 * nvec;
         if (t < total - done) {
             __stcs(P.col_idx + base + done + t, dcol[mis + done + t]);
             __stcs(P.vals + base + done + t, dval[mis + done + t]);
         }
+        const int done64 = head64 + 2 * nvec64;
+        if (F64 && t < total - done64) __stcs(P.vals64 + base + done64 + t, dv64[mis64 + done64 + t]);
     }
 }
 
@@ -549,13 +568,16 @@ static cudaError_t launch_w(BuildParams bp, cudaStream_t st) {
 
 template <int KC, bool DENSE>
 static cudaError_t launch_k(const BuildParams& bp, int block, size_t smem, cudaStream_t st) {
+    // exact-fp64 builds (unrolled k): a third staging array of doubles
+    const bool f64 = KC > 0 && bp.vals64 && bp.stage;
+    if (f64) smem += (size_t)bp.stage_words * 8;
+    auto kern = f64 ? csr_build_kernel<KC, DENSE, (KC > 0)> : csr_build_kernel<KC, DENSE, false>;
     if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(csr_build_kernel<KC, DENSE>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
     const int grid = (bp.rows + block - 1) / block;
-    csr_build_kernel<KC, DENSE><<<grid, block, smem, st>>>(bp);
+    kern<<<grid, block, smem, st>>>(bp);
     return cudaGetLastError();
 }
 
@@ -576,8 +598,12 @@ cudaError_t launch_csr_build(const BuildParams& bp_in, bool dense, int block, si
     const bool block_build = bsel && !std::strcmp(bsel, "block");
     const bool persist_build =
         (bsel && !std::strcmp(bsel, "persist")) || (!bsel && bp.k <= 5);
-    *f64_done = false;
-    if (!(persist_build && bp.stage && bp.k <= 5 && (bp.k & 1))) bp.vals64 = nullptr;
+    // exact-fp64 fill: the persistent kernel (k <= 5) and the staged unrolled
+    // block kernel (k in {1, 3, 5, 7, 11}); anything else builds tags only
+    const bool unrolled = bp.k == 1 || bp.k == 3 || bp.k == 5 || bp.k == 7 || bp.k == 11;
+    const bool f64_ok = bp.stage && unrolled && !warp_build &&
+                        (persist_build ? bp.k <= 5 : (size_t)smem + (size_t)bp.stage_words * 8 <= 200 * 1024);
+    if (!f64_ok) bp.vals64 = nullptr;
     *f64_done = bp.vals64 != nullptr;
     if (persist_build && bp.stage) {
         switch (bp.k) {

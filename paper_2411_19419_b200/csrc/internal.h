@@ -48,8 +48,8 @@ struct BuildParams {
     // Exact-fp64 builds (spconv_build_transform_f64): the taps above are TAGS
     // (q + 1 where the double tap is non-zero); the persistent kernel (k <= 5)
     // writes f64_t32[q] to vals and f64_t64[q] to vals64 from its staging.
-    float f64_t32[25];   // (k <= 5: in the parameters, no copies)
-    double f64_t64[25];
+    float f64_t32[121];  // (k <= 11: in the parameters, no copies)
+    double f64_t64[121];
     double* vals64;
 };
 
