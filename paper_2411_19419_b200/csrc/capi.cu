@@ -916,12 +916,12 @@ int spconv_build_transform_f64(int64_t m, int64_t n, int64_t k, int64_t s, int64
     // tag -> value pass afterwards (retag_kernel).
     std::vector<float> tag((size_t)kk);
     for (int64_t q = 0; q < kk; ++q) tag[(size_t)q] = kernel_kxk[q] != 0.0 ? (float)(q + 1) : 0.0f;
-    DeviceGuard dg(device);
-    if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     F64Fill fill{t32.data(), kernel_kxk, false};
     spconv_csr* h = nullptr;
+    // (argument and int32-range checks first, inside: no device work before them)
     if (int rc = build_csr_impl(m, n, k, s, p, tag.data(), device, stream, &h, &fill)) return rc;
+    DeviceGuard dg(device);
     int rc = SPCONV_OK;
     if (layout == 1) rc = attach_csc_conv(h, st);  // (from the tags in h->taps)
     // device tables of the values for the retag passes (none needed when the
