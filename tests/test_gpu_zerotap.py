@@ -91,3 +91,29 @@ def test_zero_tap_band_check_reads_the_matrix(sp, orc, torch_cuda, fused, monkey
     want = orc.spmm_native(ptr, idx, val, X)
     assert not np.array_equal(bits(want), bits(clean))
     assert np.array_equal(bits(Y), bits(want))
+
+
+@pytest.mark.parametrize("spec", SPECS + [(64, 64, 4, 3, 2)])
+def test_zero_tap_latency_spmv_closed_form(sp, orc, torch_cuda, spec):
+    """Batch <= 2: the latency SpMV predicts each warp's run from the tap mask
+    (W[j] and the stored-tap column counts) and fetches it with no dependent
+    row_ptr load; bit-exact, including the prediction-mismatch path
+    (SPCONV_B200_SPEC_SKEW)."""
+    import os
+    m, n, k = spec[:3]
+    rng = np.random.default_rng(k + 100)
+    kern = zero_kernel(rng, k, 0.4)
+    _, X = problem(orc, 19, m, n, k, batch=2)
+    t = build(sp, spec, kern)
+    ptr, idx, val = native_copy(t)
+    want = orc.spmm_native(ptr, idx, val, X)
+    for b in (1, 2):
+        Y = run_spmm(torch_cuda, sp, t, X[:b])
+        assert t.last_kernel == "csr_spmv_bulk<spec>"
+        assert np.array_equal(bits(Y), bits(want[:b])), (spec, b)
+    os.environ["SPCONV_B200_SPEC_SKEW"] = "4"
+    try:
+        Y = run_spmm(torch_cuda, sp, t, X[:1])
+    finally:
+        del os.environ["SPCONV_B200_SPEC_SKEW"]
+    assert np.array_equal(bits(Y), bits(want[:1]))
