@@ -267,7 +267,32 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
             sp.sy = (int)h->sy;
             const char* sk = std::getenv("SPCONV_B200_SPEC_SKEW");
             sp.skew = sk ? std::atoi(sk) : 0;
-            const bool spec = h->is_conv && h->taps_dense && g.k <= 16;  // conv_run_bounds: k <= 16 lanes
+            // closed-form run bounds (conv_run_bounds: k <= 16 lanes); zero taps
+            // through the tap mask and W[j] (k <= 7, stored = non-zero double tap)
+            bool zt_ok = false;
+            if (h->is_conv && !h->taps_dense && g.k <= 7 && !h->host_taps.empty()) {
+                bool finite = true, any = false;
+                unsigned long long mk = 0;
+                for (size_t q = 0; q < h->host_taps.size(); ++q) {
+                    finite &= std::isfinite(h->host_taps[q]);
+                    const bool stored = h->host_taps64.empty() ? h->host_taps[q] != 0.0f : h->host_taps64[q] != 0.0;
+                    if (stored) any = true, mk |= 1ull << q;
+                }
+                zt_ok = finite && any;
+                sp.zt = zt_ok ? 1 : 0;
+                sp.nzmask = mk;
+                for (int64_t j = 0; zt_ok && j < g.k; ++j) {
+                    long long wj = 0;
+                    for (int64_t i = 0; i < g.k; ++i) {
+                        if (!((mk >> (j * g.k + i)) & 1ull)) continue;
+                        const int64_t lo = g.p - i <= 0 ? 0 : (g.p - i + g.s - 1) / g.s;
+                        const int64_t hi = g.n + g.p - i - 1 < 0 ? -1 : std::min<int64_t>(g.no - 1, (g.n + g.p - i - 1) / g.s);
+                        wj += std::max<int64_t>(0, hi - lo + 1);
+                    }
+                    sp.zw[j] = wj;
+                }
+            }
+            const bool spec = h->is_conv && (h->taps_dense || zt_ok) && g.k <= 16;
             for (int64_t b0 = 0; b0 < batch; b0 += 2) {  // <= 2 images per launch
                 sp.X = X + b0 * ldx;
                 sp.Y = Y + b0 * ldy;

@@ -128,6 +128,9 @@ struct SpecParams {
     int m, n, k, s, p, mo, no;
     int sy;    // sum over output columns y of cy(y)
     int skew;  // test hook: offsets the predicted row start (forces the mismatch path)
+    int zt;    // zero taps (k <= 7): row starts from the tap mask and W[j]
+    unsigned long long nzmask;
+    long long zw[8];
 };
 
 struct GenericParams {

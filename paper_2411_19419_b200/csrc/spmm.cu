@@ -296,18 +296,24 @@ __device__ __forceinline__ void conv_run_bounds(const SpecParams& P, int ra, int
     const int r = lane < 16 ? ra : rb;
     const int rr = min(r, P.rows - 1);
     const int x = rr / P.no, y = rr - x * P.no;
+    const int jlo = min(max(0, P.p - P.s * x), P.k), jhi = max(jlo, min(P.k, P.m + P.p - P.s * x));
     int tx = 0, ty = 0;
     if (j < P.k) {
         tx = slides_before_dev(x, j, P.m, P.s, P.p);
         ty = slides_before_dev(y, j, P.n, P.s, P.p);
+        if (P.zt) {  // zero taps: W[j] * sbx(j) + nzcol(x, i = j) * sby(i), one term per lane
+            int nzc = 0;
+            for (int jj = jlo; jj < jhi; ++jj) nzc += (int)((P.nzmask >> (jj * P.k + j)) & 1ull);
+            tx = (int)P.zw[j] * tx + nzc * ty;
+            ty = 0;
+        }
     }
 #pragma unroll
     for (int o = 8; o > 0; o >>= 1) {
         tx += __shfl_xor_sync(0xffffffffu, tx, o);
         ty += __shfl_xor_sync(0xffffffffu, ty, o);
     }
-    const int jlo = min(max(0, P.p - P.s * x), P.k), jhi = max(jlo, min(P.k, P.m + P.p - P.s * x));
-    const int E = r >= P.rows ? P.nnz : tx * P.sy + (jhi - jlo) * ty + P.skew;
+    const int E = r >= P.rows ? P.nnz : (P.zt ? tx : tx * P.sy + (jhi - jlo) * ty) + P.skew;
     Ea = __shfl_sync(0xffffffffu, E, 0);
     Eb = __shfl_sync(0xffffffffu, E, 16);
 }
