@@ -1,21 +1,37 @@
 #!/usr/bin/env python
 """Benchmark of the conv-as-SpMV hot path (BASELINE.json metric).
 
-Workload (default, --config 3): BASELINE config 3 -- a global batch of 256
+Workload (default, --config 3): BASELINE config 3 -- a GLOBAL batch of 256
 1024x1024 fp32 images, 3x3 kernel, s=1, p=1, applied as a batched SpMM of the
-CSR transform T (9,424,900 stored entries).  With N GPUs (torchrun, one rank
-per GPU) every rank builds its own CSR replica on its device and owns a
-contiguous slice of the batch; there is no collective on the data path.
+CSR transform T (9,424,900 stored entries), "sharded over 1/2/4/8 B200": with
+N GPUs (torchrun, one rank per GPU) rank r owns the contiguous slice
+shard.batch_slice(256, r, N) (256/N images) and builds its own CSR replica;
+there is no collective on the data path.  Scaling is therefore STRONG (the job
+is fixed as N grows).  Config 4 (4096^2 k7 s2 p3, a global batch of 64: 8 per
+GPU at N = 8) is reported beside it the same way.
 
-One step = one spconv_spmm call over this rank's images (the CSR band check
-+ the register-blocked apply: two launches), inputs resident in HBM (config
-3's 1 GB X slice is larger than the 126 MB L2, so no flush is needed; working
-sets under 2x L2 get a 512 MB scrub write + a 512 MB read between steps, outside the
-timed events, so L2 is cold and clean).
-Scaling is weak: each rank owns per_gpu_batch images.  value = whole-job
-nnz-MACs per second (total images x nnz / max-over-ranks device time).
-e2e = the same metric through the C ABI with pinned HOST buffers (H2D + SpMM
-+ D2H pipelined in the library).
+Inputs are the reference's own seeded generator (inc/rng.hpp via the
+library's spconv_random_normal): S = derive_seed(42, cfg), kernel =
+random_normal_kernel(k, derive_seed(S, 1)), image g = random_normal_grid(m, n,
+derive_seed(S, 2 + g)), rounded to fp32 -- the same data the oracle and the
+reference arm see.
+
+One step = one spconv_spmm call over this rank's slice (two launches: the
+fused check-and-apply + its fixup pass at config 3), inputs resident in HBM
+(config 3's 1 GB X slice is larger than the 126 MB L2, so no flush; working
+sets under 2x L2 get a 512 MB scrub write + 512 MB read between steps, outside
+the timed events).  Timing: barrier, synchronize, ONE CUDA-event window over
+the K steps on the launching stream, synchronize; the job time is the max
+over ranks of that window, cross-checked against the cross-rank wall clock
+(earliest rank start after the common barrier to the last rank's end).
+value = global images x nnz / job time (G nnz-MAC/s).
+
+After timing, images {0, b/2, b-1} of every rank's slice are checked bit for
+bit against the oracle's fp32 ordered-fmaf restatement (the checker, never on
+the timed path): "parity" in the line.
+
+e2e = the same metric through the C ABI (spconv_convolve_host) with pinned
+HOST buffers: H2D + SpMM + D2H inside the timed region.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 """
@@ -28,25 +44,27 @@ import statistics
 import sys
 import threading
 import time
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-# per_gpu_batch: images each rank owns (weak scaling: the job grows with N).
+# global_batch: the job's images, sharded over the ranks; seed = cfg index of
+# SURVEY 8(d)'s derive_seed(42, cfg) (configs[0] = config 1).
 CONFIGS = {
-    1: dict(spec=(64, 64, 3, 1, 1), per_gpu_batch=1, name="config1: 64x64 single image, k3 s1 p1"),
-    2: dict(spec=(512, 512, 5, 2, 2), per_gpu_batch=1,
+    1: dict(spec=(64, 64, 3, 1, 1), global_batch=1, seed=0, name="config1: 64x64 single image, k3 s1 p1"),
+    2: dict(spec=(512, 512, 5, 2, 2), global_batch=1, seed=1,
             name="config2: 512x512 single image, k5 s2 p2 SpMV"),
-    3: dict(spec=(1024, 1024, 3, 1, 1), per_gpu_batch=256,
-            name="config3: 1024x1024 images, k3 s1 p1, batched SpMM, 256 images per GPU"),
-    4: dict(spec=(4096, 4096, 7, 2, 3), per_gpu_batch=8,
-            name="config4: 4096x4096 images, k7 s2 p3, build + batched SpMM, 8 images per GPU "
-                 "(batch 64 over 8 GPUs)"),
+    3: dict(spec=(1024, 1024, 3, 1, 1), global_batch=256, seed=2,
+            name="config3: batch 256 of 1024x1024 images, k3 s1 p1, batched SpMM sharded over the GPUs"),
+    4: dict(spec=(4096, 4096, 7, 2, 3), global_batch=64, seed=3,
+            name="config4: batch 64 of 4096x4096 images, k7 s2 p3, build + batched SpMM sharded over the GPUs"),
 }
 METRIC = "SpMV-conv nnz-MAC/s (whole job) with HBM GB/s and CSR build ms"
 UNIT = "G nnz-MAC/s"
+BASE_SEED = 42
 
 
 def peaks():
@@ -80,6 +98,17 @@ def ncu_traffic(cfg: int, batch: int):
         if hits:
             return sum(e["dram_bytes_per_launch"] for e in hits), ", ".join(e["source"] for e in hits)
     return None, None
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 class ClockSampler:
@@ -150,20 +179,94 @@ def algorithmic_bytes(rows, cols, nnz, b):
     return 8 * nnz + 4 * (rows + 1) + 4 * b * (cols + rows)
 
 
+def mono() -> float:
+    """System-wide monotonic clock (comparable across the ranks of one node)."""
+    return time.clock_gettime(time.CLOCK_MONOTONIC)
+
+
+# ----------------------------------------------------------------------------
+# Inputs: the reference's generator (inc/rng.hpp), via the product library
+# ----------------------------------------------------------------------------
+
+def problem_kernel(sp, cfg_idx: int, k: int) -> np.ndarray:
+    """random_normal_kernel(k, derive_seed(S, 1)) rounded to fp32."""
+    S = sp.derive_seed(BASE_SEED, cfg_idx)
+    return sp.random_normal(sp.derive_seed(S, 1), k * k).astype(np.float32)
+
+
+def problem_images(sp, cfg_idx: int, first: int, count: int, cols: int, out=None, threads: int = 16):
+    """Images first .. first+count-1 of the config's global batch:
+    random_normal_grid(m, n, derive_seed(S, 2 + g)) rounded to fp32, generated
+    on host threads (one image per task) into `out` ([count, cols] float32)."""
+    S = sp.derive_seed(BASE_SEED, cfg_idx)
+    if out is None:
+        out = np.empty((count, cols), np.float32)
+
+    def one(i):
+        tmp = sp.random_normal(sp.derive_seed(S, 2 + first + i), cols)
+        out[i] = tmp  # fp32 rounding
+
+    with ThreadPoolExecutor(max(1, min(threads, os.cpu_count() or 1, count))) as ex:
+        list(ex.map(one, range(count)))
+    return out
+
+
+def pinned_images(sp, torch, cfg_idx, first, count, cols):
+    Xh = torch.empty(max(count, 1), cols, dtype=torch.float32, pin_memory=True)
+    problem_images(sp, cfg_idx, first, count, cols, out=Xh.numpy()[:count])
+    return Xh
+
+
+# ----------------------------------------------------------------------------
+# Parity: the oracle's fp32 restatement is the CHECKER of what was timed
+# ----------------------------------------------------------------------------
+
+def parity_check(spec, kern, Xh, Y, which):
+    """Images `which` of this rank's slice: the device output Y[i] against the
+    oracle's ordered-fmaf fp32 SpMV of the oracle-built CSR (bit for bit).
+    Returns (all_bitexact, worst relative deviation)."""
+    from oracle import Oracle
+    orc = Oracle()
+    ptr, idx, val = orc.build_native(*spec, kern)
+    X = np.stack([Xh[i].numpy() if hasattr(Xh[i], "numpy") else Xh[i] for i in which])
+    want = orc.spmm_native(ptr, idx, val, X)
+    got = np.stack([Y[i].cpu().numpy() for i in which])
+    same = bool(np.array_equal(got.view(np.uint32), want.view(np.uint32)))
+    dev = float(np.max(np.abs(got.astype(np.float64) - want) / np.maximum(1e-30, np.abs(want).astype(np.float64) + 1e-30)))
+    return same, dev
+
+
+def slice_probe(b: int):
+    return sorted({0, b // 2, max(b - 1, 0)}) if b > 0 else []
+
+
 # ----------------------------------------------------------------------------
 # CPU baseline: the reference's own convolve() (oracle/_ref) on a bounded sample
 # ----------------------------------------------------------------------------
 
-def cpu_baseline(spec, seconds: float = 10.0):
+def reference_inputs(ref, cfg_idx, m, n, k, count, threads):
+    """The reference generator's own grids (its random_normal_grid), rounded to
+    fp32 and widened back: the doubles of the fp32 values the device sees."""
+    S = ref.derive_seed(BASE_SEED, cfg_idx)
+    kern = ref.random_normal_kernel(k, ref.derive_seed(S, 1)).reshape(-1).astype(np.float32).astype(np.float64)
+    imgs = np.empty((count, m * n), np.float64)
+
+    def one(i):
+        imgs[i] = ref.random_normal_grid(m, n, ref.derive_seed(S, 2 + i)).reshape(-1).astype(np.float32)
+
+    with ThreadPoolExecutor(max(1, min(threads, count))) as ex:
+        list(ex.map(one, range(count)))
+    return kern, imgs
+
+
+def cpu_baseline(cfg, seconds: float = 10.0):
     import oracle
-    m, n, k, s, p = spec
+    m, n, k, s, p = cfg["spec"]
     cores = os.cpu_count() or 1
     ref = oracle.try_ref()
-    rng = np.random.default_rng(1)
-    kern = rng.standard_normal(k * k).astype(np.float32).astype(np.float64)
-    img = rng.standard_normal((1, m * n)).astype(np.float32).astype(np.float64)
     if ref is not None:
         kind = "reference"
+        kern, img = reference_inputs(ref, cfg["seed"], m, n, k, 1, 1)
         t0 = time.perf_counter()
         T = ref.build(m, n, k, s, p, kern)
         build_s = time.perf_counter() - t0
@@ -172,6 +275,9 @@ def cpu_baseline(spec, seconds: float = 10.0):
     else:
         kind = "port"
         orc = oracle.Oracle()
+        S = orc.derive_seed(BASE_SEED, cfg["seed"])
+        kern = orc.random_normal_f32(orc.derive_seed(S, 1), k * k).astype(np.float64)
+        img = orc.random_normal_f32(orc.derive_seed(S, 2), m * n).astype(np.float64)[None]
         t0 = time.perf_counter()
         ptr, idx, val = orc.build_transform(m, n, k, s, p, kern)
         build_s = time.perf_counter() - t0
@@ -198,52 +304,58 @@ def cpu_baseline(spec, seconds: float = 10.0):
         d1 = time.perf_counter() - s0
         single = {"value": nnz * reps1 / d1 / 1e9, "cores": 1, "us_per_image": d1 / reps1 * 1e6}
     return {"value": nnz * reps / dt / 1e9, "unit": UNIT, "cores": cores, "kind": kind,
+            "cpu": cpu_model(),
             "sample": f"{reps} single-image convolve() calls on {m}x{n} k{k} s{s} p{p} "
                       f"({dt:.1f} s, threads={cores}); build_transform {build_s * 1e3:.0f} ms",
             "build_ms": build_s * 1e3, "us_per_image": dt / reps * 1e6, "single_thread": single}
 
 
 def run_reference(args, cfg):
-    """--impl reference: the reference CPU path on this box's host cores."""
+    """--impl reference: the reference CPU path (oracle/_ref: the reference's
+    own headers compiled unmodified) on this box's host cores, the same
+    workload as our arm -- every step convolves the whole global batch (the
+    reference has no batch API: its convolve() per image, threads = all
+    cores).  Under torchrun only rank 0 runs."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     import oracle
-    spec = cfg["spec"]
-    m, n, k, s, p = spec
+    m, n, k, s, p = cfg["spec"]
+    B = args.global_batch or cfg["global_batch"]
     cores = os.cpu_count() or 1
     ref = oracle.try_ref()
-    rng = np.random.default_rng(1)
-    kern = rng.standard_normal(k * k).astype(np.float32).astype(np.float64)
-    imgs = rng.standard_normal((4, m * n)).astype(np.float32).astype(np.float64)
     if ref is not None:
         kind = "reference"
+        kern, imgs = reference_inputs(ref, cfg["seed"], m, n, k, B, cores)
         T = ref.build(m, n, k, s, p, kern)
         nnz = T.shape()[2]
-        step = lambda i: T.convolve(imgs[i % 4][None], threads=cores)  # noqa: E731
+        step = lambda: T.convolve(imgs, threads=cores)  # noqa: E731
     else:
         kind = "port"
         orc = oracle.Oracle()
+        S = orc.derive_seed(BASE_SEED, cfg["seed"])
+        kern = orc.random_normal_f32(orc.derive_seed(S, 1), k * k).astype(np.float64)
+        imgs = np.stack([orc.random_normal_f32(orc.derive_seed(S, 2 + g), m * n) for g in range(B)]).astype(np.float64)
         ptr, idx, val = orc.build_transform(m, n, k, s, p, kern)
         nnz = val.size
         cores = 1
-        step = lambda i: orc.spmv_f64(ptr, idx, val, imgs[i % 4])  # noqa: E731
-    for i in range(args.warmup):
-        step(i)
+        step = lambda: [orc.spmv_f64(ptr, idx, val, x) for x in imgs]  # noqa: E731
+    for _ in range(args.warmup):
+        step()
     t0 = time.perf_counter()
-    for i in range(args.steps):
-        step(i)
+    for _ in range(args.steps):
+        step()
     dt = time.perf_counter() - t0
-    value = nnz * args.steps / dt / 1e9
+    value = B * nnz * args.steps / dt / 1e9
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg["name"] + " -- one image per step (bounded CPU sample)",
-                   "m": m, "n": n, "k": k, "s": s, "p": p, "nnz": nnz},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
-                         "sample": f"{args.steps} single-image convolve() steps, threads={cores}"},
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["name"], "m": m, "n": n, "k": k, "s": s, "p": p, "nnz": nnz,
+                   "global_batch": B, "per_step": f"convolve() over all {B} images, threads={cores}"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "cpu": cpu_model(),
+                         "sample": f"{args.steps} steps of {B} convolve() calls each, threads={cores}"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -253,7 +365,7 @@ def run_reference(args, cfg):
 # Our arm
 # ----------------------------------------------------------------------------
 
-def timed_build(sp, torch, kern, spec, dev, stream, reps=5, warm=3):
+def timed_build(sp, torch, kern, spec, dev, stream, reps=5, warm=3, layout=0):
     """Device time of the one-time CSR build (kernel only: a GPU-side sleep
     queued first keeps the stream busy while the host enqueues the build, so
     the events bracket GPU work, not host latency) and host wall time of the call."""
@@ -266,7 +378,7 @@ def timed_build(sp, torch, kern, spec, dev, stream, reps=5, warm=3):
         torch.cuda._sleep(2_000_000)
         e0.record(stream)
         h0 = time.perf_counter()
-        t = sp.build_transform(kern, spec, device=dev.index, stream=stream)
+        t = sp.build_transform(kern, spec, layout=layout, device=dev.index, stream=stream)
         h1 = time.perf_counter()
         e1.record(stream)
         torch.cuda.synchronize(dev)
@@ -275,142 +387,242 @@ def timed_build(sp, torch, kern, spec, dev, stream, reps=5, warm=3):
     return t, statistics.median(x[0] for x in out), statistics.median(x[1] for x in out)
 
 
-def device_steps(sp, torch, t, b, steps, warmup, dev, stream, seed):
-    """Times `steps` spmm calls over a resident [b, cols] batch (CUDA events on
-    the launching stream).  Inputs smaller than 2x L2 get a 512 MB scrub
-    between steps, outside the events."""
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(seed)
-    X = torch.randn(max(b, 1), t.cols, generator=gen, device=dev, dtype=torch.float32)
-    Y = torch.empty(max(b, 1), t.rows, device=dev, dtype=torch.float32)
-    l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
-    need_flush = 4 * b * (t.cols + t.rows) + 8 * t.nnz < 2 * l2_bytes
-    scrub = torch.empty(512 << 20, dtype=torch.uint8, device=dev) if need_flush else None
-    # After the 512 MB write, a 512 MB read: L2 ends cold AND clean, so the
-    # timed kernel does not pay for write-backs of the scrub's dirty lines.
-    clean = torch.ones(128 << 20, dtype=torch.float32, device=dev) if need_flush else None
-    sink = torch.empty((), dtype=torch.float32, device=dev) if need_flush else None
+class L2Scrub:
+    """512 MB write + 512 MB read between steps (outside the events): L2 ends
+    cold AND clean, so a timed kernel pays neither for hits nor for write-backs."""
 
-    def flush(i):
-        scrub.fill_(i & 0xFF)
-        torch.sum(clean, dim=0, out=sink)
+    def __init__(self, torch, dev):
+        self.torch = torch
+        self.scrub = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+        self.clean = torch.ones(128 << 20, dtype=torch.float32, device=dev)
+        self.sink = torch.empty((), dtype=torch.float32, device=dev)
 
+    def __call__(self, i):
+        self.scrub.fill_(i & 0xFF)
+        self.torch.sum(self.clean, dim=0, out=self.sink)
+
+
+def needs_flush(torch, dev, rows, cols, nnz, b):
+    return 4 * b * (cols + rows) + 8 * nnz < 2 * torch.cuda.get_device_properties(dev).L2_cache_size
+
+
+def l2_note(torch, dev, rows, cols, nnz, b):
+    if needs_flush(torch, dev, rows, cols, nnz, b):
+        return "512 MB scrub write + 512 MB clean read between steps (outside events)"
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    return (f"working set larger than L2 (X+Y+T {(4 * b * (cols + rows) + 8 * nnz) / 1e6:.0f} MB"
+            f" > 2 x {l2 / 1e6:.0f} MB)")
+
+
+def window_steps(torch, fn, steps, warmup, dev, stream, flush=None):
+    """W untimed calls, then K timed calls.  Without a flush: ONE event window
+    over the K calls (returns its total ms).  With a flush between calls:
+    per-call windows (the flush stays outside), summed."""
     for i in range(warmup):
-        if scrub is not None:
+        if flush:
             flush(i)
-        sp.spmm(t, X[:b], Y[:b], stream=stream)
+        fn()
     torch.cuda.synchronize(dev)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(steps)]
+    if flush is None:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        return e0.elapsed_time(e1), None
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     for i in range(steps):
-        if scrub is not None:
-            flush(i)  # outside the events: evicts X, Y and T from L2
+        flush(i)
         ev[i][0].record(stream)
-        sp.spmm(t, X[:b], Y[:b], stream=stream)
+        fn()
         ev[i][1].record(stream)
     torch.cuda.synchronize(dev)
     ms = [a.elapsed_time(c) for a, c in ev]
-    l2 = ("512 MB scrub write + 512 MB clean read between steps (outside events)" if need_flush else
-          f"working set larger than L2 (X+Y+T {(4 * b * (t.cols + t.rows) + 8 * t.nnz) / 1e6:.0f} MB"
-          f" > 2 x {l2_bytes / 1e6:.0f} MB)")
-    return X, Y, ms, l2
+    return sum(ms), ms
 
 
-def secondary(sp, torch, dev, stream, steps, world=1):
-    """Extras: config 4 at its per-GPU batch (8 images; at N GPUs the job is
-    BASELINE's 'batch 64 over 8 B200' when N = 8: every rank times its own
-    slice, max over ranks) and, at N = 1 only, config 2 (single-image SpMV,
-    cold and warm L2) and config 3 in CSC layout -- kernel time, roofline
-    fraction and build."""
-    from paper_2411_19419_b200.shard import max_over_ranks
-    out = {}
-    peak, _ = peaks()
-    rng = np.random.default_rng(99)
-    for c in ((2, 4) if world == 1 else (4,)):
-        cfg = CONFIGS[c]
-        m, n, k, s, p = cfg["spec"]
-        b = cfg["per_gpu_batch"]
-        spec = sp.ConvSpec(m, n, k, s, p)
-        kern = sp.Kernel(k, rng.standard_normal(k * k).astype(np.float32))
-        t, bld_ms, _ = timed_build(sp, torch, kern, spec, dev, stream)
-        X, Y, ms, l2 = device_steps(sp, torch, t, b, steps, 3, dev, stream, 7)
-        alg = algorithmic_bytes(t.rows, t.cols, t.nnz, b)
-        mean = max_over_ranks(sum(ms), dev) / len(ms)  # max over ranks (identity at N = 1)
-        bld_ms = max_over_ranks(bld_ms, dev)
-        bb = 8 * t.nnz + 4 * (t.rows + 1)
-        out[f"config{c}"] = {
-            "workload": cfg["name"], "batch": b, "n_gpus": world, "global_batch": b * world,
-            "kernel": t.last_kernel, "ms_per_step": mean,
-            "ms_min": min(ms), "value": world * b * t.nnz / (mean * 1e-3) / 1e9, "unit": UNIT,
-            "gb_per_s": alg / (mean * 1e-3) / 1e9, "frac": alg / (mean * 1e-3) / 1e9 / peak,  # per GPU
-            "l2": l2, "build_ms_device": bld_ms, "build_frac": bb / (bld_ms * 1e-3) / 1e9 / peak,
-        }
-        if c == 2:
-            # warm: the paper's use (one build, repeated SpMV): 64 back-to-back
-            # single-image SpMVs over 8 different images, T L2-resident,
-            # chained by programmatic dependent launch
-            Xw = torch.randn(8, t.cols, device=dev, dtype=torch.float32)
-            Yw = torch.empty(8, t.rows, device=dev, dtype=torch.float32)
-            for i in range(8):
-                sp.spmm(t, Xw[i:i + 1], Yw[i:i + 1], stream=stream)
-            torch.cuda.synchronize(dev)
-            # one CUDA graph of the 64 launches: host enqueue cost out of the timing
-            cs = torch.cuda.Stream(dev)  # graphs are captured on a side stream
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=cs):
-                for i in range(64):
-                    sp.spmm(t, Xw[i % 8:i % 8 + 1], Yw[i % 8:i % 8 + 1], stream=cs)
-            with torch.cuda.stream(cs):
-                g.replay()
-            torch.cuda.synchronize(dev)
-            w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            with torch.cuda.stream(cs):
-                w0.record(cs)
-                g.replay()
-                w1.record(cs)
-            torch.cuda.synchronize(dev)
-            wm = w0.elapsed_time(w1) / 64
-            del g
-            out["config2"]["warm"] = {
-                "ms_per_step": wm, "value": t.nnz / (wm * 1e-3) / 1e9, "unit": UNIT,
-                "gb_per_s": alg / (wm * 1e-3) / 1e9,
-                "l2": "T (13.3 MB) L2-resident: one CUDA graph of 64 back-to-back SpMVs over 8 images, "
-                      "PDL-chained"}
-            del Xw, Yw
-        del X, Y
-        t.close()
+def device_line(sp, torch, t, X, Y, b, steps, dev, stream, peak, fn=None, alg=None):
+    """Kernel-side numbers of one single-GPU workload (no ranks involved)."""
+    fn = fn or (lambda: sp.spmm(t, X[:b], Y[:b], stream=stream))
+    flush = L2Scrub(torch, dev) if needs_flush(torch, dev, t.rows, t.cols, t.nnz, b) else None
+    tot, ms = window_steps(torch, fn, steps, 3, dev, stream, flush)
+    mean = tot / steps
+    alg = alg if alg is not None else algorithmic_bytes(t.rows, t.cols, t.nnz, b)
+    out = {"batch": b, "kernel": t.last_kernel, "ms_per_step": mean,
+           "value": b * t.nnz / (mean * 1e-3) / 1e9, "unit": UNIT,
+           "algorithmic_bytes": alg, "gb_per_s": alg / (mean * 1e-3) / 1e9,
+           "frac": alg / (mean * 1e-3) / 1e9 / peak, "l2": l2_note(torch, dev, t.rows, t.cols, t.nnz, b)}
+    if ms:
+        out["ms_min"] = min(ms)
+    return out
+
+
+def sharded_workload(sp, torch, cfg, args, dev, stream, world, rank, steps, warmup, want_e2e):
+    """One BASELINE config sharded over the ranks: build (device-timed), the K
+    timed steps (max over ranks, cross-checked against the cross-rank wall
+    clock), parity of the timed outputs, and (optionally) e2e through the C ABI."""
+    import torch.distributed as dist
+
+    from paper_2411_19419_b200.shard import batch_slice, max_over_ranks, sum_over_ranks
+    m, n, k, s, p = cfg["spec"]
+    B = args.global_batch if (args.global_batch and cfg is CONFIGS[args.config]) else cfg["global_batch"]
+    first, b = batch_slice(B, rank, world)
+    spec = sp.ConvSpec(m, n, k, s, p)
+    kern32 = problem_kernel(sp, cfg["seed"], k)
+    kern = sp.Kernel(k, kern32.astype(np.float64))
+    t, bld_dev, bld_host = timed_build(sp, torch, kern, spec, dev, stream)
+    rows, cols, nnz = t.rows, t.cols, t.nnz
+    Xh = pinned_images(sp, torch, cfg["seed"], first, b, cols)
+    X = Xh.to(dev, non_blocking=False)
+    Y = torch.empty(max(b, 1), rows, device=dev, dtype=torch.float32)
+    fn = (lambda: sp.spmm(t, X[:b], Y[:b], stream=stream))
+    flush = L2Scrub(torch, dev) if needs_flush(torch, dev, rows, cols, nnz, b) else None
+
+    sampler = ClockSampler(dev.index).start()
+    for i in range(warmup):
+        if flush:
+            flush(i)
+        fn()
+    torch.cuda.synchronize(dev)
     if world > 1:
-        return out
-    # config 3 in CSC layout: the CSC build (CSR arrays + column-major
-    # storage) and the apply through the same kernels
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    w0 = mono()
+    p0 = time.perf_counter()
+    tot, _ = window_steps(torch, fn, steps, 0, dev, stream, flush)
+    w1 = mono()
+    p1 = time.perf_counter()
+    sampler.stop()
+    ev_max = max_over_ranks(tot, dev)
+    job_wall = (max_over_ranks(w1, dev) + max_over_ranks(-w0, dev)) * 1e3
+    # The job time is the device time of the slowest rank; the wall clock
+    # from the common barrier to the last rank's end catches ranks that did
+    # not overlap (e.g. serialised on one device).  With a flush between
+    # steps the wall clock also counts the flushes, so it is not comparable.
+    job_ms = ev_max
+    timing = "cuda-events (max over ranks)"
+    if flush is None and job_wall > 1.25 * ev_max + 0.5:
+        job_ms, timing = job_wall, "cross-rank wall clock (exceeds the event time: ranks did not overlap)"
+    value = B * nnz * steps / (job_ms * 1e-3) / 1e9
+    local_ms = tot / steps
+    alg = algorithmic_bytes(rows, cols, nnz, b)
+    kernel = t.last_kernel
+
+    # ---- parity of what was timed (the oracle is the checker) ----
+    which = slice_probe(b)
+    same, rdev = parity_check(cfg["spec"], kern32, Xh, Y, which) if b > 0 else (True, 0.0)
+    all_same = max_over_ranks(0.0 if same else 1.0, dev) == 0.0
+    worst = max_over_ranks(rdev, dev)
+
+    e2e = None
+    if want_e2e:
+        Yh = torch.empty(max(b, 1), rows, dtype=torch.float32, pin_memory=True)
+        sp.convolve_batch(t, Xh[:b], Yh[:b])  # warm (workspace allocation)
+        e2e_steps = max(2, min(steps, args.e2e_steps))
+        if world > 1:
+            dist.barrier()
+        h0 = mono()
+        for _ in range(e2e_steps):
+            sp.convolve_batch(t, Xh[:b], Yh[:b])
+        h1 = mono()
+        e2e_ms = (max_over_ranks(h1, dev) + max_over_ranks(-h0, dev)) * 1e3
+        e2e = {"value": B * nnz * e2e_steps / (e2e_ms * 1e-3) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": int(sum_over_ranks(4 * b * cols, dev)),
+               "d2h_bytes_per_step": int(sum_over_ranks(4 * b * rows, dev)),
+               "steps": e2e_steps, "ms_per_step": e2e_ms / e2e_steps,
+               "path": "spconv_convolve_host (C ABI), pinned host buffers, cross-rank wall clock"}
+        e2e_ok = np.array_equal(Yh[which].numpy().view(np.uint32), Y[which].cpu().numpy().view(np.uint32))
+        e2e["parity"] = "bitexact (== the device-timed outputs)" if max_over_ranks(0.0 if e2e_ok else 1.0, dev) == 0.0 else "MISMATCH"
+        del Yh
+    res = {
+        "t": t, "B": B, "b": b, "rows": rows, "cols": cols, "nnz": nnz, "kernel": kernel,
+        "value": value, "job_ms": job_ms, "ev_max_ms": ev_max, "job_wall_ms": job_wall, "timing": timing,
+        "local_ms": local_ms, "alg": alg, "bld_dev": max_over_ranks(bld_dev, dev), "bld_host": bld_host,
+        "parity": "bitexact" if all_same else "MISMATCH", "parity_images": which,
+        "parity_max_rel_dev": worst, "e2e": e2e, "clocks": sampler.summary(p0, p1),
+        "l2": l2_note(torch, dev, rows, cols, nnz, b),
+    }
+    del X, Y, Xh
+    return res
+
+
+def secondary_single(sp, torch, dev, stream, steps, peak):
+    """N = 1 only: the per-rank workloads of the N = 2/4/8 runs on one GPU
+    (strong-scaling proxies), config 2's single-image SpMV (cold and warm L2),
+    and config 4's per-rank slice at N = 8."""
+    out = {}
+    # ---- config 3 per-rank slices at N = 2 / 4 / 8 ----
     cfg = CONFIGS[3]
     m, n, k, s, p = cfg["spec"]
+    kern32 = problem_kernel(sp, cfg["seed"], k)
+    t = sp.build_transform(sp.Kernel(k, kern32.astype(np.float64)), sp.ConvSpec(m, n, k, s, p),
+                           device=dev.index, stream=stream)
+    Xh = pinned_images(sp, torch, cfg["seed"], 0, 128, t.cols)
+    X = Xh.to(dev)
+    Y = torch.empty(128, t.rows, device=dev)
+    prox = {}
+    for g, b in ((2, 128), (4, 64), (8, 32)):
+        line = device_line(sp, torch, t, X, Y, b, steps, dev, stream, peak)
+        line["as_rank_of"] = f"N={g}: batch_slice(256, r, {g}) = {b} images"
+        prox[f"n{g}"] = line
+    out["config3_per_rank_proxy"] = prox
+    del X, Y, Xh
+    t.close()
+    # ---- config 4: the per-rank slice at N = 8 (8 images) ----
+    cfg = CONFIGS[4]
+    m, n, k, s, p = cfg["spec"]
+    kern32 = problem_kernel(sp, cfg["seed"], k)
+    t = sp.build_transform(sp.Kernel(k, kern32.astype(np.float64)), sp.ConvSpec(m, n, k, s, p),
+                           device=dev.index, stream=stream)
+    Xh = pinned_images(sp, torch, cfg["seed"], 0, 8, t.cols)
+    X = Xh.to(dev)
+    Y = torch.empty(8, t.rows, device=dev)
+    line = device_line(sp, torch, t, X, Y, 8, steps, dev, stream, peak)
+    line["as_rank_of"] = "N=8: batch_slice(64, r, 8) = 8 images"
+    out["config4_per_rank_proxy_n8"] = line
+    del X, Y, Xh
+    t.close()
+    # ---- config 2: one 512^2 image (cold L2) + the warm-L2 repeated SpMV ----
+    cfg = CONFIGS[2]
+    m, n, k, s, p = cfg["spec"]
+    kern32 = problem_kernel(sp, cfg["seed"], k)
     spec = sp.ConvSpec(m, n, k, s, p)
-    kern = sp.Kernel(k, rng.standard_normal(k * k).astype(np.float32))
-    cms = []
-    for i in range(8):
-        torch.cuda.synchronize(dev)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda._sleep(2_000_000)
-        e0.record(stream)
-        tc = sp.build_transform(kern, spec, layout=sp.Layout.CSC, device=dev.index, stream=stream)
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        if i >= 3:
-            cms.append(e0.elapsed_time(e1))
-        if i < 7:
-            tc.close()
-    cb = 2 * 8 * tc.nnz + 4 * (tc.rows + tc.cols + 2)
-    X, Y, ms, l2 = device_steps(sp, torch, tc, cfg["per_gpu_batch"], max(10, steps // 2), 3, dev, stream, 8)
-    mean = statistics.mean(ms)
-    alg = algorithmic_bytes(tc.rows, tc.cols, tc.nnz, cfg["per_gpu_batch"])
-    out["config3_csc"] = {
-        "workload": cfg["name"] + ", CSC layout", "batch": cfg["per_gpu_batch"], "kernel": tc.last_kernel,
-        "build_ms_device": statistics.median(cms), "build_bytes": cb,
-        "build_frac": cb / (statistics.median(cms) * 1e-3) / 1e9 / peak,
-        "ms_per_step": mean, "frac": alg / (mean * 1e-3) / 1e9 / peak}
-    del X, Y
-    tc.close()
+    kern = sp.Kernel(k, kern32.astype(np.float64))
+    t, bld_ms, _ = timed_build(sp, torch, kern, spec, dev, stream)
+    Xh = pinned_images(sp, torch, cfg["seed"], 0, 8, t.cols)
+    Xw = Xh.to(dev)
+    Yw = torch.empty(8, t.rows, device=dev)
+    line = device_line(sp, torch, t, Xw, Yw, 1, max(steps, 30), dev, stream, peak)
+    bb = 8 * t.nnz + 4 * (t.rows + 1)
+    line.update(workload=cfg["name"], build_ms_device=bld_ms, build_frac=bb / (bld_ms * 1e-3) / 1e9 / peak)
+    same, _ = parity_check(cfg["spec"], kern32, Xh, Yw, [0])
+    line["parity"] = "bitexact" if same else "MISMATCH"
+    # warm: the paper's use (one build, repeated SpMV): one CUDA graph of 64
+    # back-to-back single-image SpMVs over 8 images, T L2-resident, PDL-chained
+    cs = torch.cuda.Stream(dev)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=cs):
+        for i in range(64):
+            sp.spmm(t, Xw[i % 8:i % 8 + 1], Yw[i % 8:i % 8 + 1], stream=cs)
+    with torch.cuda.stream(cs):
+        g.replay()
+    torch.cuda.synchronize(dev)
+    w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(cs):
+        w0.record(cs)
+        g.replay()
+        w1.record(cs)
+    torch.cuda.synchronize(dev)
+    wm = w0.elapsed_time(w1) / 64
+    del g
+    alg = algorithmic_bytes(t.rows, t.cols, t.nnz, 1)
+    line["warm"] = {"ms_per_step": wm, "value": t.nnz / (wm * 1e-3) / 1e9, "unit": UNIT,
+                    "gb_per_s": alg / (wm * 1e-3) / 1e9,
+                    "l2": "T (13.3 MB) L2-resident: one CUDA graph of 64 back-to-back SpMVs over 8 images, PDL-chained"}
+    out["config2"] = line
+    del Xw, Yw, Xh
+    t.close()
     return out
 
 
@@ -419,7 +631,6 @@ def run_ours(args, cfg):
     import torch.distributed as dist
 
     import paper_2411_19419_b200 as sp
-    from paper_2411_19419_b200.shard import max_over_ranks, sum_over_ranks
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -438,124 +649,80 @@ def run_ours(args, cfg):
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
-
-    m, n, k, s, p = cfg["spec"]
-    # Weak scaling: every rank owns a fixed slice of `b` images (the batch
-    # shards with no collective); the whole job processes b * world images.
-    b = args.batch or cfg["per_gpu_batch"]
-    total_batch = b * world
-    spec = sp.ConvSpec(m, n, k, s, p)
-    rng = np.random.default_rng(1234)
-    kern = sp.Kernel(k, rng.standard_normal(k * k).astype(np.float32))
     stream = torch.cuda.current_stream(dev)
-
-    # ---- CSR build (one-time cost), device-timed: a local replica per rank ----
-    t, bld_dev, bld_host = timed_build(sp, torch, kern, spec, dev, stream)
-    rows, cols, nnz = t.rows, t.cols, t.nnz
-
-    # ---- timed region: inputs resident in HBM ----
-    sampler = ClockSampler(local).start()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    w0 = time.perf_counter()
-    X, Y, ms, l2 = device_steps(sp, torch, t, b, args.steps, args.warmup, dev, stream, 1000 + rank)
-    w1 = time.perf_counter()
-    if world > 1:
-        dist.barrier()
-    sampler.stop()
-    kernel = t.last_kernel
-    gather = None
-    if args.gather and world > 1:
-        # the optional final gather of every rank's outputs to rank 0 (NCCL
-        # over NVLink), timed separately from the step: max over ranks
-        from paper_2411_19419_b200.shard import gather_outputs
-        dist.barrier()
-        torch.cuda.synchronize(dev)
-        ge0, ge1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ge0.record(stream)
-        out = gather_outputs(Y[:b], total_batch)  # the result is ordered on the current stream
-        ge1.record(stream)
-        torch.cuda.synchronize(dev)
-        g_ms = max_over_ranks(ge0.elapsed_time(ge1), dev)
-        moved = 4 * (total_batch - b) * rows
-        gather = {"ms": g_ms, "bytes_to_root": moved, "gb_per_s": moved / (g_ms * 1e-3) / 1e9,
-                  "collective": f"torch.distributed.gather ({dist.get_backend()})"}
-        del out
-    launches_per_step = kernel.count("+") + 1
-    elapsed_ms = sum(ms)
-    max_ms = max_over_ranks(elapsed_ms, dev)
-    ms_per_step = max_ms / args.steps
-    value = total_batch * nnz * args.steps / (max_ms * 1e-3) / 1e9
-    launch_ms = elapsed_ms / args.steps  # this rank's average step (all launches of one call)
-    alg = algorithmic_bytes(rows, cols, nnz, b)
     peak, peak_src = peaks()
-    achieved = alg / (launch_ms * 1e-3) / 1e9
+    m, n, k, s, p = cfg["spec"]
+
+    main = sharded_workload(sp, torch, cfg, args, dev, stream, world, rank, args.steps, args.warmup, True)
+    t = main["t"]
+    b, B = main["b"], main["B"]
+    achieved = main["alg"] / (main["local_ms"] * 1e-3) / 1e9
     traffic, traffic_src = ncu_traffic(args.config, b)
-    clocks = sampler.summary(w0, w1)
+    bld_bytes = 8 * main["nnz"] + 4 * (main["rows"] + 1)
+    launches_per_step = main["kernel"].count("+") + 1
 
-    # ---- e2e through the C ABI with pinned host buffers ----
-    e2e_steps = max(2, min(args.steps, args.e2e_steps))
-    Xh = torch.empty(max(b, 1), cols, dtype=torch.float32, pin_memory=True)
-    Xh.copy_(X.cpu())
-    Yh = torch.empty(max(b, 1), rows, dtype=torch.float32, pin_memory=True)
-    del X, Y
-    sp.convolve_batch(t, Xh[:b], Yh[:b])  # warm (workspace allocation)
-    if world > 1:
-        dist.barrier()
-    h0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        sp.convolve_batch(t, Xh[:b], Yh[:b])
-    e2e_ms = (time.perf_counter() - h0) * 1e3
-    e2e_max = max_over_ranks(e2e_ms, dev)
-    e2e_value = total_batch * nnz * e2e_steps / (e2e_max * 1e-3) / 1e9
-    h2d = int(sum_over_ranks(4 * b * cols, dev))
-    d2h = int(sum_over_ranks(4 * b * rows, dev))
-    bld_bytes = 8 * nnz + 4 * (rows + 1)
-
-    extra = None
-    if not args.no_secondary:  # (collective timing at N > 1: every rank takes part)
-        extra = secondary(sp, torch, dev, stream, max(10, min(args.steps, 30)), world)
+    extra = {}
+    if not args.no_secondary:
+        if args.config != 4:  # BASELINE config 4 sharded the same way (every rank takes part)
+            c4 = sharded_workload(sp, torch, CONFIGS[4], args, dev, stream, world, rank,
+                                  max(10, min(args.steps, 30)), 3, False)
+            c4b = 8 * c4["nnz"] + 4 * (c4["rows"] + 1)
+            extra["config4"] = {
+                "workload": CONFIGS[4]["name"], "global_batch": c4["B"], "per_gpu_batch": c4["b"],
+                "n_gpus": world, "kernel": c4["kernel"], "ms_per_step": c4["job_ms"] / max(10, min(args.steps, 30)),
+                "value": c4["value"], "unit": UNIT, "timing": c4["timing"], "job_wall_ms": c4["job_wall_ms"],
+                "gb_per_s_per_gpu": c4["alg"] / (c4["local_ms"] * 1e-3) / 1e9,
+                "frac": c4["alg"] / (c4["local_ms"] * 1e-3) / 1e9 / peak,
+                "algorithmic_bytes_per_gpu": c4["alg"], "l2": c4["l2"],
+                "build_ms_device": c4["bld_dev"], "build_frac": c4b / (c4["bld_dev"] * 1e-3) / 1e9 / peak,
+                "parity": c4["parity"], "parity_images": c4["parity_images"]}
+            c4["t"].close()
+        if world == 1:
+            extra.update(secondary_single(sp, torch, dev, stream, max(10, min(args.steps, 30)), peak))
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(cfg["spec"], seconds=args.cpu_seconds)
+        cpu = cpu_baseline(cfg, seconds=args.cpu_seconds)
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f32", "data": "synthetic",
+            "metric": METRIC, "value": main["value"], "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": main["job_ms"] / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic (the reference's seeded generator, inc/rng.hpp)",
             "config": {
                 "workload": cfg["name"], "m": m, "n": n, "k": k, "s": s, "p": p,
-                "global_batch": total_batch, "per_gpu_batch": b, "rows": rows, "cols": cols,
-                "nnz": nnz, "parallelism": f"batch-dp{world} (CSR replica per GPU, no collective)",
+                "global_batch": B, "per_gpu_batch": b, "rows": main["rows"], "cols": main["cols"],
+                "nnz": main["nnz"],
+                "parallelism": f"batch-dp{world}: shard.batch_slice({B}, rank, {world}), CSR replica per GPU, "
+                               "no collective",
                 "why_this_config": ("BASELINE metric is quoted 'at 1/2/4/8 B200': configs[2] (batch 256 of "
                                     "1024^2, sharded over 1/2/4/8); configs[1] (single 512^2 SpMV, 14.6 MB, "
                                     "L2-sized) is reported under secondary.config2 (cold and warm)")
-                if args.config == 3 and not args.spec else None,
-                "l2": l2,
+                if args.config == 3 else None,
+                "l2": main["l2"],
             },
+            "timing": {"method": main["timing"], "event_max_ms": main["ev_max_ms"],
+                       "job_wall_ms": main["job_wall_ms"],
+                       "wall_over_event": main["job_wall_ms"] / main["ev_max_ms"] if main["ev_max_ms"] else None},
+            "parity": main["parity"],
+            "parity_detail": {"images_per_rank": main["parity_images"], "max_rel_dev": main["parity_max_rel_dev"],
+                              "against": "oracle/spconv_oracle.c fp32 ordered-fmaf SpMV of the oracle-built CSR"},
             "gb_per_s": achieved,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "algorithmic_bytes": alg, "kernel": kernel,
-                         "launch_ms": launch_ms, "peak_source": peak_src,
+                         "algorithmic_bytes": main["alg"], "kernel": main["kernel"],
+                         "launch_ms": main["local_ms"], "peak_source": peak_src,
                          "traffic_source": traffic_src,
-                         "note": "achieved = SURVEY 8(d) bytes of one spmm call (all its launches) / "
-                                 "its CUDA-event duration"},
-            "build": {"ms_device": bld_dev, "ms_host_wall": bld_host, "bytes": bld_bytes,
-                      "gb_per_s": bld_bytes / (bld_dev * 1e-3) / 1e9,
-                      "frac": bld_bytes / (bld_dev * 1e-3) / 1e9 / peak},
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "steps": e2e_steps,
-                    "ms_per_step": e2e_max / e2e_steps,
-                    "path": "spconv_convolve_host (C ABI), pinned host buffers"},
+                         "note": "achieved = SURVEY 8(d) bytes of one spmm call over rank 0's slice (all its "
+                                 "launches) / its CUDA-event duration"},
+            "build": {"ms_device": main["bld_dev"], "ms_host_wall": main["bld_host"], "bytes": bld_bytes,
+                      "gb_per_s": bld_bytes / (main["bld_dev"] * 1e-3) / 1e9,
+                      "frac": bld_bytes / (main["bld_dev"] * 1e-3) / 1e9 / peak},
+            "e2e": main["e2e"],
             "gpu_launches": args.steps * launches_per_step,
-            "clocks": clocks,
-            "gather": gather,
-            "secondary": extra,
+            "clocks": main["clocks"],
+            "secondary": extra or None,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
@@ -609,7 +776,7 @@ def run_densenet(args):
         else:
             line.update(value=ref["total_csr_us"], ms_per_step=ref["total_csr_us"] / 1e3,
                         cpu_baseline={"value": ref["total_csr_us"], "unit": "us", "cores": 1,
-                                      "kind": "reference",
+                                      "kind": "reference", "cpu": cpu_model(),
                                       "sample": f"{args.steps} trials per layer, threads=1"},
                         e2e={"value": ref["total_csr_us"], "unit": "us", "h2d_bytes_per_step": 0,
                              "d2h_bytes_per_step": 0},
@@ -629,7 +796,7 @@ def run_densenet(args):
     line = {
         "metric": metric, "value": res["total_device_us"], "unit": "us", "higher_is_better": False,
         "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": res["total_device_us"] / 1e3, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": res["total_device_us"] / 1e3, "scaling": "strong", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic",
         "config": {"workload": "densenet121 layer table (123 single-channel layers, paper Table 2)",
                    "timing": f"per layer: CUDA graph of {res['graph_reps']} SpMV launches, "
@@ -643,7 +810,7 @@ def run_densenet(args):
         "gpu_launches": len(res["layers"]),
         "paper_table1_us": PAPER_TABLE1_US,
         "cpu_baseline": None if ref is None else {
-            "value": ref["total_csr_us"], "unit": "us", "cores": 1, "kind": "reference",
+            "value": ref["total_csr_us"], "unit": "us", "cores": 1, "kind": "reference", "cpu": cpu_model(),
             "sample": "reference run_layer_bench, CSR-SpMV, threads=1",
             "csc_us": ref["total_csc_us"], "im2col_us": ref["total_im2col_us"]},
     }
@@ -660,14 +827,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, choices=sorted(CONFIGS), default=3)
-    ap.add_argument("--batch", type=int, default=0, help="override the per-GPU batch")
-    ap.add_argument("--spec", default="", help="tuning only: m,n,k,s,p replacing the config's geometry")
+    ap.add_argument("--global-batch", type=int, default=0, help="override the config's global batch")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-secondary", action="store_true", help="skip the config 2/4 extras")
-    ap.add_argument("--gather", action="store_true",
-                    help="N>1: also time the optional final gather of all outputs to rank 0")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the extra workloads")
     ap.add_argument("--workload", choices=["config", "densenet121"], default="config",
                     help="densenet121: the paper's Table 1 layer-table protocol")
     ap.add_argument("--report", default="", help="densenet121: write the per-layer markdown here")
@@ -675,9 +839,6 @@ def main():
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
     cfg = CONFIGS[args.config]
-    if args.spec:
-        spec = tuple(int(v) for v in args.spec.split(","))
-        cfg = dict(cfg, spec=spec, name=f"custom spec {spec} (tuning run, not a BASELINE config)")
     if args.workload == "densenet121":
         run_densenet(args)
     elif args.impl == "reference":

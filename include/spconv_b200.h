@@ -19,6 +19,12 @@
  * memory / internal error.  spconv_last_error() returns the calling thread's
  * last message.  A built handle is immutable: concurrent spconv_spmv /
  * spconv_spmm calls on different streams are safe.
+ *
+ * Stream ordering: a build returns once its kernels are enqueued on `stream`.
+ * Device-pointer applies (spconv_spmv / spconv_spmm) on that same stream are
+ * ordered after it; on another stream the caller orders them (an event), as
+ * with any CUDA producer.  The host-buffer calls (spconv_convolve_host*) and
+ * every synchronous call (export, copy, text) wait for the build themselves.
  */
 #ifndef SPCONV_B200_H
 #define SPCONV_B200_H
@@ -299,6 +305,22 @@ int spconv_band_check_status(const spconv_csr* h, int64_t* segments, int64_t* fa
 
 /* Frees the handle and its device memory (synchronises its device). */
 int spconv_csr_free(spconv_csr* h);
+
+/* Process-wide kernel-path options (no reference counterpart: the reference
+ * has one CPU loop).  The library chooses its kernels itself; an option only
+ * forces an alternative so tests can cross-check every kernel and A/B scripts
+ * can time the rejected variants.  name = value:
+ *   path       auto | banded | tiled | tiled_notma | generic | spmv | spmv_plain
+ *   fused      auto | 0 | 1          (band path: two kernels / fused check + apply)
+ *   generic    rowblock | plain      (generic CSR batches)
+ *   build      auto | block | warp | persist
+ *   bulk_store 1 | 0                 (TMA bulk write-back of staged build entries)
+ *   stage      lanes | bulk          (latency SpMV staging)
+ *   spec_skew  <int>                 (test hook: mispredicts closed-form row starts)
+ * Status 1 for an unknown name or value.  spconv_get_option writes the current
+ * value (NUL-terminated) into buf. */
+int spconv_set_option(const char* name, const char* value);
+int spconv_get_option(const char* name, char* buf, int64_t cap);
 
 #ifdef __cplusplus
 }

@@ -23,7 +23,7 @@ import numpy as np
 __all__ = [
     "ConvSpec", "Kernel", "Transform", "build_transform", "convolve", "convolve_batch",
     "spmv", "spmm", "spmm_f64", "nnz_bound", "read_transform", "relayout", "Layout", "layout_name",
-    "layout_from_name", "direct_conv", "im2col_conv", "run_verification", "library_path", "lib",
+    "layout_from_name", "derive_seed", "random_normal", "set_option", "get_option", "options", "direct_conv", "im2col_conv", "run_verification", "library_path", "lib",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -86,6 +86,56 @@ _decl("spconv_random_normal", [C.c_uint64, _i64, _vp])
 _decl("spconv_reference_host", [C.c_int] + [_i64] * 5 + [_vp, _vp, _vp, C.c_int])
 _decl("spconv_run_verification", [_i64, C.c_int, C.c_uint64, C.c_int, _vp, _vp, _vp, _i64])
 _decl("spconv_matrix_from_host", [_i64, _i64, C.c_int, _vp, _vp, _vp, C.c_int, _vp, _P(_vp)])
+_decl("spconv_set_option", [C.c_char_p, C.c_char_p])
+_decl("spconv_get_option", [C.c_char_p, C.c_char_p, _i64])
+
+
+def derive_seed(base: int, index: int) -> int:
+    """derive_seed (inc/rng.hpp): the reference's per-problem seed derivation."""
+    return int(lib.spconv_derive_seed(base, index))
+
+
+def random_normal(seed: int, count: int, out=None) -> np.ndarray:
+    """`count` standard normals of the reference's generator seeded by `seed`
+    (random_normal_grid / random_normal_kernel, inc/rng.hpp:80-92), float64.
+    Host code in the library (releases the GIL: callable from worker threads)."""
+    if out is None:
+        out = np.empty(count, np.float64)
+    assert out.dtype == np.float64 and out.flags.c_contiguous and out.size >= count
+    _check(lib.spconv_random_normal(seed, count, out.ctypes.data))
+    return out
+
+
+def set_option(name: str, value) -> None:
+    """Process-wide kernel-path option (spconv_set_option, include/spconv_b200.h):
+    forces an alternative kernel for cross-checks and A/B timing."""
+    _check(lib.spconv_set_option(name.encode(), str(value).encode()))
+
+
+def get_option(name: str) -> str:
+    buf = C.create_string_buffer(64)
+    _check(lib.spconv_get_option(name.encode(), buf, 64))
+    return buf.value.decode()
+
+
+class options:
+    """Context manager: ``with options(path="tiled", fused=1): ...`` sets the
+    options for the block and restores the previous values after it."""
+
+    def __init__(self, **kw):
+        self.kw = {k: v for k, v in kw.items() if v is not None}
+        self.old = {}
+
+    def __enter__(self):
+        for k, v in self.kw.items():
+            self.old[k] = get_option(k)
+            set_option(k, v)
+        return self
+
+    def __exit__(self, *exc):
+        for k, v in self.old.items():
+            set_option(k, v)
+        return False
 
 
 class Layout:

@@ -174,25 +174,15 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-// Kernel-path selection: SPCONV_B200_PATH = auto (default) | spmv | spmv_plain |
-// banded | tiled | tiled_notma | generic.  auto = the latency kernel for batch <= 2
-// (csr_spmv_bulk: closed-form row runs for dense-tap transforms), else the
-// band path (CSR band check + register-blocked apply) when instantiated for
-// (k, s) with dense taps, else tiled (TMA when the strides allow); generic for
-// uploaded matrices.  The overrides exist for cross-checking the paths.
+// Kernel-path selection (spconv_set_option "path"): auto (default) = the
+// latency kernel for batch <= 2 (csr_spmv_bulk: closed-form row runs for
+// conv transforms), else the band path (CSR band check + register-blocked
+// apply) when instantiated for (k, s) with finite taps, else tiled (TMA when
+// the strides allow); generic for uploaded matrices.  The forced values exist
+// for cross-checking the paths.
 enum Path { kAuto = 0, kBanded, kTiled, kTiledNoTma, kGeneric, kSpmv, kSpmvPlain };
 
-Path path_override() {
-    const char* e = std::getenv("SPCONV_B200_PATH");
-    if (!e) return kAuto;
-    if (!std::strcmp(e, "banded")) return kBanded;
-    if (!std::strcmp(e, "tiled")) return kTiled;
-    if (!std::strcmp(e, "tiled_notma")) return kTiledNoTma;
-    if (!std::strcmp(e, "generic")) return kGeneric;
-    if (!std::strcmp(e, "spmv")) return kSpmv;
-    if (!std::strcmp(e, "spmv_plain")) return kSpmvPlain;
-    return kAuto;
-}
+Path path_override() { return static_cast<Path>(spb::opt(spb::kOptPath)); }
 
 // 3-D tensor map over the batch X[b][m][n] (fp32) with the given box.
 int encode_x_map(CUtensorMap* tmap, const float* X, const Geom& g, int64_t ldx, int64_t batch,
@@ -265,8 +255,7 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
             sp.mo = (int)g.mo;
             sp.no = (int)g.no;
             sp.sy = (int)h->sy;
-            const char* sk = std::getenv("SPCONV_B200_SPEC_SKEW");
-            sp.skew = sk ? std::atoi(sk) : 0;
+            sp.skew = spb::opt(spb::kOptSpecSkew);
             // closed-form run bounds (conv_run_bounds: k <= 16 lanes); zero taps
             // through the tap mask and W[j] (k <= 7, stored = non-zero double tap)
             bool zt_ok = false;
@@ -293,6 +282,10 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
                 }
             }
             const bool spec = h->is_conv && (h->taps_dense || zt_ok) && g.k <= 16;
+            // Programmatic dependent launch lets the SpMV fetch the matrix before
+            // the previous kernel on the stream finishes -- never behind this
+            // handle's own build, whose writes are only visible at its end.
+            sp.pdl = h->applied.exchange(true) ? 1 : 0;
             for (int64_t b0 = 0; b0 < batch; b0 += 2) {  // <= 2 images per launch
                 sp.X = X + b0 * ldx;
                 sp.Y = Y + b0 * ldy;
@@ -373,33 +366,20 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
                    (reinterpret_cast<uintptr_t>(Y) % (4 * cpt) == 0);
         CUtensorMap tmap;
         if (int rc = encode_x_map(&tmap, X, g, ldx, batch, sh.wc, sh.wr, 1)) return rc;
-        // The check depends only on the (immutable) matrix: off the caller's
-        // stream it overlaps whatever precedes the call there (in a loop of
-        // calls: the previous apply).  That pays when the matrix dominates the
-        // call's bytes (config 4 at 8 images: 341 -> 319 us); when the images
-        // dominate, the check's CTAs delay the persistent apply's start
-        // (config 3: 401 -> 406 us, config 4 at 64 images: 1047 -> 1270 us,
-        // profiles/r01n/exp.txt), so it stays on the caller's stream.
-        // SPCONV_B200_CHECK=side|same overrides; never while the stream is
-        // being captured into a graph.
-        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-        CK(cudaStreamIsCapturing(st, &cap));
-        const char* csel = std::getenv("SPCONV_B200_CHECK");
-        const bool matrix_bound = 8.0 * (double)h->nnz > 4.0 * (double)batch * (double)(h->rows + h->cols);
-        const bool side = cap == cudaStreamCaptureStatusNone &&
-                          (csel ? !std::strcmp(csel, "side") : matrix_bound);
         // When the images dominate by far (matrix < 10 % of the call's bytes),
         // one fused kernel checks the matrix in its producer warps while it
         // applies, plus a fixup pass for failed segments: config 3 384 ->
         // 376 us.  With a heavier matrix the producer's checks starve the
         // pipeline (config 4 at 64 images: 1,043 -> 1,531 us), so the check
-        // stays a kernel of its own (profiles/r01v/exp.txt).
-        // SPCONV_B200_FUSED=0|1 overrides; the blocked path needs finite taps.
-        const char* fsel = std::getenv("SPCONV_B200_FUSED");
+        // stays a kernel of its own (profiles/r01v/exp.txt).  Option "fused"
+        // forces either form; the blocked path needs finite taps.  (zero-tap
+        // kernels: the masked checks slow the fused producer -- config 3 shape
+        // 431 us fused against 27 + 371 us as two kernels -- so two kernels.)
+        // Both forms run on the caller's stream only: the check sees exactly
+        // the matrix the stream order gives it.
+        const int fsel = spb::opt(spb::kOptFused);
         const bool light = 8.0 * (double)h->nnz < 0.1 * 4.0 * (double)batch * (double)(h->rows + h->cols);
-        // (zero-tap kernels: the masked checks slow the fused producer -- config 3
-        // shape 431 us fused against 27 + 371 us as two kernels -- so two kernels)
-        bp.fused = !side && band_taps && (fsel ? !std::strcmp(fsel, "1") : light && !bp.zt) ? 1 : 0;
+        bp.fused = band_taps && (fsel ? fsel == 2 : light && !bp.zt) ? 1 : 0;
         if (bp.fused) {
             const cudaError_t fe = spb::launch_band((int)g.k, (int)g.s, bp, &tmap, st, nullptr, sms);
             if (fe == cudaSuccess) {
@@ -410,19 +390,7 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
             cudaGetLastError();
             bp.fused = 0;  // this blocking has no fused instantiation
         }
-        if (side) {
-            std::lock_guard<std::mutex> lk(h->chk_mu);
-            if (!h->chk_stream) {
-                CK(cudaStreamCreateWithFlags(&h->chk_stream, cudaStreamNonBlocking));
-                CK(cudaEventCreateWithFlags(&h->chk_done, cudaEventDisableTiming));
-                if (h->built) CK(cudaStreamWaitEvent(h->chk_stream, h->built, 0));  // the matrix exists
-            }
-            CK(spb::launch_band_check((int)g.k, (int)g.s, bp, h->chk_stream, sms));
-            CK(cudaEventRecord(h->chk_done, h->chk_stream));
-            CK(cudaStreamWaitEvent(st, h->chk_done, 0));
-        } else {
-            CK(spb::launch_band_check((int)g.k, (int)g.s, bp, st, sms));
-        }
+        CK(spb::launch_band_check((int)g.k, (int)g.s, bp, st, sms));
         CK(spb::launch_band((int)g.k, (int)g.s, bp, &tmap, st, nullptr, sms));
         h->last_kernel.store("conv_band_check+conv_spmm_band");
         return SPCONV_OK;
@@ -486,8 +454,7 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
     spb::GenericParams gp{h->row_ptr, h->col_idx, h->vals, X, ldx, Y, ldy, (int)h->rows, (int)batch};
     // the row-block multi-vector kernel (matrix staged once per CTA) for rows
     // of <= 64 entries; SPCONV_B200_GENERIC=plain keeps thread-per-row
-    const char* gsel = std::getenv("SPCONV_B200_GENERIC");
-    if (h->k2max <= 64 && !(gsel && !std::strcmp(gsel, "plain"))) {
+    if (h->k2max <= 64 && spb::opt(spb::kOptGeneric) == 0) {
         CK(spb::launch_rowblock(gp, h->k2max, st));
         h->last_kernel.store("csr_spmm_rowblock");
         return SPCONV_OK;
@@ -598,10 +565,7 @@ int attach_csc_conv(spconv_csr* h, cudaStream_t st) {
     cp.col_ptr = h->csc_ptr;
     cp.row_idx = h->csc_idx;
     cp.vals = h->csc_vals;
-    {
-        const char* bs = std::getenv("SPCONV_B200_BULK_STORE");
-        cp.bulk_store = bs ? std::atoi(bs) : 1;
-    }
+    cp.bulk_store = spb::opt(spb::kOptBulkStoreOff) ? 0 : 1;
     const int64_t per_axis = std::min<int64_t>(g.k, (g.k + g.s - 1) / g.s);
     bool nonzero = true;
     for (float v : h->host_taps) nonzero &= v != 0.0f;
@@ -819,10 +783,7 @@ static int build_csr_impl(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
     bp.vals = h->vals;
     bp.taps_out = h->taps;
     bp.nnz_total = ht.nnz;
-    {
-        const char* bs = std::getenv("SPCONV_B200_BULK_STORE");
-        bp.bulk_store = bs ? std::atoi(bs) : 1;
-    }
+    bp.bulk_store = spb::opt(spb::kOptBulkStoreOff) ? 0 : 1;
     char* tab = nullptr;
     if (k <= spb::kSmallK) {  // tables ride in the kernel parameters: no copies, no allocation
         bp.small = 1;
@@ -971,7 +932,7 @@ int spconv_build_transform_f64(int64_t m, int64_t n, int64_t k, int64_t s, int64
     if (rc == SPCONV_OK && e == cudaSuccess)
         e = need_tables ? cudaMemcpyAsync(h->taps, d32, (size_t)kk * 4, cudaMemcpyDeviceToDevice, st)
                         : cudaMemcpyAsync(h->taps, t32.data(), (size_t)kk * 4, cudaMemcpyHostToDevice, st);
-    if (rc == SPCONV_OK && e == cudaSuccess && h->built) e = cudaEventRecord(h->built, st);  // side checks see the values
+    if (rc == SPCONV_OK && e == cudaSuccess && h->built) e = cudaEventRecord(h->built, st);  // host-buffer calls see the values
     if (tt) cudaFreeAsync(tt, st);
     if (rc != SPCONV_OK || e != cudaSuccess) {
         const std::string msg = rc ? g_err : std::string();
@@ -1481,9 +1442,7 @@ int spconv_convolve_host(const spconv_csr* hc, const float* X_host, float* Y_hos
     if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
     // Chunks of ~64 MB of input, double-buffered: H2D(c+1) || spmm(c) || D2H(c-1).
     const int64_t per_img = std::max<int64_t>(h->cols, 1) * 4;
-    static const int64_t chunk_bytes = std::getenv("SPCONV_B200_E2E_CHUNK_MB")
-                                           ? std::atoll(std::getenv("SPCONV_B200_E2E_CHUNK_MB")) << 20
-                                           : (64ll << 20);
+    constexpr int64_t chunk_bytes = 64ll << 20;  // (16 / 32 / 128 MB: no better, profiles/r01m)
     const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(batch, chunk_bytes / per_img));
     if (h->ws_chunk < chunk) {
         free_ws(h);
@@ -1499,6 +1458,9 @@ int spconv_convolve_host(const spconv_csr* hc, const float* X_host, float* Y_hos
         h->ws_chunk = chunk;
     }
     cudaStream_t s_in = h->ws_stream[0], s_cp = h->ws_stream[1], s_out = h->ws_stream[2];
+    // the build may still be in flight on its own stream (builds only enqueue)
+    if (h->built)
+        for (int s = 0; s < 3; ++s) CK(cudaStreamWaitEvent(h->ws_stream[s], h->built, 0));
     if (batch <= chunk) {
         // One chunk: nothing to overlap -- H2D, apply, D2H in order on one
         // stream and a single synchronisation (the latency path of small calls).
@@ -1570,6 +1532,7 @@ int spconv_convolve_host_f64(const spconv_csr* hc, const double* X_host, double*
     keep_pool_memory(h->device);
     if (!h->ws_stream[1]) CK(cudaStreamCreateWithFlags(&h->ws_stream[1], cudaStreamNonBlocking));
     cudaStream_t st = h->ws_stream[1];
+    if (h->built) CK(cudaStreamWaitEvent(st, h->built, 0));  // (builds only enqueue)
     const size_t xb = (size_t)(batch * h->cols) * 8, yb = (size_t)(batch * h->rows) * 8;
     char* buf = nullptr;
     CK(cudaMallocAsync(&buf, xb + yb, st));
@@ -1603,6 +1566,7 @@ int spconv_csr_write_text(const spconv_csr* h, int transform_header_line, char* 
     const double* sv64 = csc ? h->csc_vals64 : h->vals64;
     const int64_t major = csc ? h->cols : h->rows;
     const int64_t blocks = (major + spb::text_rows_per_block() - 1) / spb::text_rows_per_block();
+    CK(cudaDeviceSynchronize());  // the build (any stream) is complete
     cudaStream_t st = nullptr;
     unsigned long long* scratch = nullptr;
     CK(cudaMallocAsync(&scratch, (size_t)(blocks + 2) * 8, st));
@@ -1759,9 +1723,7 @@ int spconv_csr_free(spconv_csr* h) {
         DeviceGuard dg(h->device);
         cudaDeviceSynchronize();
         free_ws(h);
-        if (h->chk_done) cudaEventDestroy(h->chk_done);
         if (h->built) cudaEventDestroy(h->built);
-        if (h->chk_stream) cudaStreamDestroy(h->chk_stream);
         if (h->row_ptr) cudaFree(h->row_ptr);
         if (h->csc_ptr) cudaFree(h->csc_ptr);
         if (h->vals64) cudaFree(h->vals64);

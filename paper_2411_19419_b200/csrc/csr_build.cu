@@ -522,14 +522,20 @@ template <int KC, bool DENSE, bool F64>
 static cudaError_t launch_p_f(const BuildParams& bp, cudaStream_t st) {
     constexpr int KK = KC * KC;
     const size_t smem = (size_t)((256 * KK + 3 + 3) & ~3) * 4 * 2 * (F64 ? 4 : 2);  // 2 buffers
-    int dev = 0, sms = 148, per_sm = 0;
+    int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     auto kern = csr_build_persist<KC, DENSE, F64>;
-    cudaError_t e = cudaSuccess;
-    if (smem > 48 * 1024) e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
-    if (e != cudaSuccess) return e;
+    static std::atomic<int> occ[64];  // per device, queried once (0 = not yet)
+    if (!occ[dev & 63]) {
+        int o = 0;
+        cudaError_t e = cudaSuccess;
+        if (smem > 48 * 1024) e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, 256, smem);
+        if (e != cudaSuccess) return e;
+        occ[dev & 63] = std::max(o, 1);
+    }
+    const int per_sm = occ[dev & 63];
     const long long tiles = ((long long)bp.rows + 255) / 256;
     const long long grid = std::min<long long>(tiles, (long long)sms * std::max(per_sm, 1));
     kern<<<(unsigned)grid, 256, smem, st>>>(bp);
@@ -571,10 +577,17 @@ static cudaError_t launch_k(const BuildParams& bp, int block, size_t smem, cudaS
     // exact-fp64 builds (unrolled k): a third staging array of doubles
     const bool f64 = KC > 0 && bp.vals64 && bp.stage;
     if (f64) smem += (size_t)bp.stage_words * 8;
+    if (smem > 200 * 1024) return cudaErrorInvalidValue;
     auto kern = f64 ? csr_build_kernel<KC, DENSE, (KC > 0)> : csr_build_kernel<KC, DENSE, false>;
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // the opt-in limit is set once per device to the 200 KB cap every launch
+    // respects (a per-launch value could race with another thread's launch)
+    static std::atomic<bool> attr[2][64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!attr[f64 ? 1 : 0][dev & 63]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         if (e != cudaSuccess) return e;
+        attr[f64 ? 1 : 0][dev & 63] = true;
     }
     const int grid = (bp.rows + block - 1) / block;
     kern<<<grid, block, smem, st>>>(bp);
@@ -591,13 +604,10 @@ cudaError_t launch_csr_build(const BuildParams& bp_in, bool dense, int block, si
     // larger k, whose 256-row double buffer would not leave room for a second
     // CTA per SM (config 4: block 252 us, persistent 297 us; the block kernel
     // also beats the warp-local one, 254 vs 283 us, profiles/r01_choices).
-    // SPCONV_B200_BUILD=block | warp | persist forces a kernel.
-    const char* bsel = std::getenv("SPCONV_B200_BUILD");
-    if (bsel && !*bsel) bsel = nullptr;  // empty = unset
-    const bool warp_build = bsel && !std::strcmp(bsel, "warp");
-    const bool block_build = bsel && !std::strcmp(bsel, "block");
-    const bool persist_build =
-        (bsel && !std::strcmp(bsel, "persist")) || (!bsel && bp.k <= 5);
+    // Option build = block | warp | persist forces a kernel.
+    const int bsel = opt(kOptBuild);
+    const bool warp_build = bsel == 2;
+    const bool persist_build = bsel == 3 || (bsel == 0 && bp.k <= 5);
     // exact-fp64 fill: the persistent kernel (k <= 5) and the staged unrolled
     // block kernel (k in {1, 3, 5, 7, 11}); anything else builds tags only
     const bool unrolled = bp.k == 1 || bp.k == 3 || bp.k == 5 || bp.k == 7 || bp.k == 11;

@@ -11,6 +11,21 @@
 
 namespace spb {
 
+// Process-wide path options (options.cu, spconv_set_option): 0 = the library's
+// own choice everywhere.  Values follow the symbolic lists in options.cu.
+enum Opt {
+    kOptPath = 0,      // 0 auto, 1 banded, 2 tiled, 3 tiled_notma, 4 generic, 5 spmv, 6 spmv_plain
+    kOptFused,         // 0 auto, 1 two kernels, 2 fused check + apply
+    kOptGeneric,       // 0 row-block multi-vector kernel, 1 thread per row
+    kOptBuild,         // 0 auto, 1 block, 2 warp, 3 persist
+    kOptBulkStoreOff,  // 0 bulk (TMA) stores of staged entries, 1 per-thread 16-byte stores
+    kOptStage,         // 0 per-lane 16-byte staging (latency SpMV), 1 bulk copies
+    kOptSpecSkew,      // test hook: offsets the latency SpMV's predicted row starts
+    kOptCount
+};
+extern std::atomic<int> g_opt[kOptCount];
+inline int opt(Opt o) { return g_opt[o].load(std::memory_order_relaxed); }
+
 // Geometry of one padded, strided convolution (inc/conv.hpp:33-62).
 struct Geom {
     int64_t m, n, k, s, p;
@@ -128,6 +143,7 @@ struct SpecParams {
     int m, n, k, s, p, mo, no;
     int sy;    // sum over output columns y of cy(y)
     int skew;  // test hook: offsets the predicted row start (forces the mismatch path)
+    int pdl;   // host: launch as a programmatic dependent of the previous kernel
     int zt;    // zero taps (k <= 7): row starts from the tap mask and W[j]
     unsigned long long nzmask;
     long long zw[8];
@@ -259,13 +275,8 @@ struct spconv_csr {
     std::vector<double> host_taps64;  // conv handles built from such double taps
     double* vals64 = nullptr;         // device [nnz], row-major order
     double* csc_vals64 = nullptr;     // device [nnz], CSC storage order (layout 1)
-    // Side stream of the band check (run_spmm): the check reads only the
-    // immutable matrix, so it need not wait for the caller's stream and can
-    // overlap the previous call's apply; the apply waits on chk_done.
-    std::mutex chk_mu;
-    cudaStream_t chk_stream = nullptr;
-    cudaEvent_t chk_done = nullptr;
-    cudaEvent_t built = nullptr;  // recorded after the build on the build stream (side checks wait on it)
+    cudaEvent_t built = nullptr;  // recorded after the build on the build stream (host-buffer calls wait on it)
+    std::atomic<bool> applied{false};  // an apply was enqueued after the build (PDL is safe from then on)
     std::atomic<const char*> last_kernel{nullptr};  // diagnostics: last SpMM kernel launched
     // Workspace of spconv_convolve_host (lazily created, guarded by ws_mu).
     std::mutex ws_mu;

@@ -435,9 +435,8 @@ template <int KMAX>
 static cudaError_t launch_bulk_k(const SpecParams& sp, bool spec, cudaStream_t st) {
     using C = BulkCfg<KMAX>;
     // staging: per-lane 16-byte loads (default; config 2 14.6 vs 16.0 us, DenseNet
-    // table 144 vs 151 us, profiles/r01l) or bulk copies (SPCONV_B200_STAGE=bulk)
-    const char* sel = std::getenv("SPCONV_B200_STAGE");
-    const bool bulk = sel && !std::strcmp(sel, "bulk");
+    // table 144 vs 151 us, profiles/r01l) or bulk copies (option stage=bulk)
+    const bool bulk = opt(kOptStage) == 1;
     auto kern = spec ? (bulk ? csr_spmv_bulk<KMAX, true, true> : csr_spmv_bulk<KMAX, true, false>)
                      : (bulk ? csr_spmv_bulk<KMAX, false, true> : csr_spmv_bulk<KMAX, false, false>);
     static std::atomic<bool> attr_set[4][64];
@@ -458,7 +457,7 @@ static cudaError_t launch_bulk_k(const SpecParams& sp, bool spec, cudaStream_t s
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = sp.pdl ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, kern, sp);
 }
 
@@ -568,13 +567,8 @@ cudaError_t launch_rowblock(GenericParams gp, int kmax, cudaStream_t st) {
     if (kmax > 64) return cudaErrorInvalidValue;
     gp.stage_cap = 128 * std::max(kmax, 1);
     const size_t smem = (size_t)gp.stage_cap * 8;
-    const char* v = std::getenv("SPCONV_B200_ROWBLOCK_IMG");
     // images per group: 8 (config 3 shape as a generic CSR, 256 images:
     // 1.41 / 1.48 / 1.15 / 1.69 ms for 2 / 4 / 8 / 16, profiles/r01_generic)
-    const int img = v ? std::atoi(v) : 8;
-    if (img == 16) return launch_rowblock_i<16>(gp, smem, st);
-    if (img == 4) return launch_rowblock_i<4>(gp, smem, st);
-    if (img == 2) return launch_rowblock_i<2>(gp, smem, st);
     return launch_rowblock_i<8>(gp, smem, st);
 }
 

@@ -798,51 +798,19 @@ int band_tile_width(int k, int s) {
     return s == 1 ? 128 : 64;
 }
 
-int var_env() {
-    static const int v = std::getenv("SPCONV_B200_VARIANT") ? std::atoi(std::getenv("SPCONV_B200_VARIANT")) : 0;
-    return v;
-}
-
 // delta = (box start alignment shift) = (S*y0 - p) mod 4 with y0 a multiple
 // of the tile width: uniform over the launch.
 cudaError_t launch_band(int k, int s, const BandParams& bp, const CUtensorMap* tmap, cudaStream_t st,
                         BandShape* shape, int sms) {
     const int delta = ((-bp.p) % 4 + 4) % 4;
-    // Blocking variants for tuning experiments (SPCONV_B200_VARIANT; 0 = default),
-    // instantiated only for the alignment shift of the benchmark configs.
-    // (dense taps only: a zero-tap launch always takes the default blocking)
-    const int var = bp.zt ? 0 : var_env();
-    // Defaults from the A/B runs (profiles/r01p/exp.txt): k3 s1 -- V = 16 rows
-    // x 4 columns per thread, 64-row tiles, 4 stages (one CTA per SM; config 3
-    // 404 -> 382 us); k7 s2 -- V = 8, 32-row tiles, 3 stages.
-    if (k == 3 && s == 1) {
-        if (delta == 3 && var == 1) return run_cfg<3, 1, 4, 4, 16, 4, 3>(bp, tmap, st, shape, sms);
-        if (delta == 3 && var == 2) return run_cfg<3, 1, 4, 4, 32, 4, 3>(bp, tmap, st, shape, sms);
-        if (delta == 3 && var == 3) return run_cfg<3, 1, 4, 4, 32, 3, 3>(bp, tmap, st, shape, sms);
-        if (delta == 3 && var == 4) return run_cfg<3, 1, 2, 4, 16, 4, 3>(bp, tmap, st, shape, sms);
-        if (delta == 3 && var == 5) return run_cfg<3, 1, 8, 4, 64, 3, 3>(bp, tmap, st, shape, sms);
-        if (delta == 3 && var == 6) return run_cfg<3, 1, 8, 4, 64, 2, 3>(bp, tmap, st, shape, sms);
-        if (delta == 3 && var == 7) return run_cfg<3, 1, 16, 4, 64, 4, 3>(bp, tmap, st, shape, sms);
-        if (delta == 3 && var == 8) return run_cfg<3, 1, 16, 4, 64, 3, 3>(bp, tmap, st, shape, sms);
-        if (delta == 3 && var == 9) return run_cfg<3, 1, 16, 4, 64, 5, 3>(bp, tmap, st, shape, sms);
-        if (delta == 3 && var == 10) return run_cfg<3, 1, 16, 4, 32, 4, 3>(bp, tmap, st, shape, sms);
-        if (delta == 3 && var == 11) return run_cfg<3, 1, 8, 4, 32, 4, 3>(bp, tmap, st, shape, sms);
-        return run_delta<3, 1, 16, 4, 64, 4>(delta, bp, tmap, st, shape, sms);
-    }
+    // Blockings from the A/B runs (profiles/r01p/exp.txt, profiles/r01q): k3 s1
+    // -- V = 16 rows x 4 columns per thread, 64-row tiles, 4 stages (one CTA
+    // per SM; config 3 404 -> 382 us); k7 s2 -- V = 8, 32-row tiles, 3 stages.
+    if (k == 3 && s == 1) return run_delta<3, 1, 16, 4, 64, 4>(delta, bp, tmap, st, shape, sms);
     if (k == 5 && s == 1) return run_delta<5, 1, 4, 4, 32, 4>(delta, bp, tmap, st, shape, sms);
     if (k == 3 && s == 2) return run_delta<3, 2, 4, 2, 16, 4>(delta, bp, tmap, st, shape, sms);
     if (k == 5 && s == 2) return run_delta<5, 2, 4, 2, 16, 4>(delta, bp, tmap, st, shape, sms);
-    if (k == 7 && s == 2) {
-        if (delta == 1 && var == 1) return run_cfg<7, 2, 4, 2, 16, 4, 1>(bp, tmap, st, shape, sms);
-        if (delta == 1 && var == 2) return run_cfg<7, 2, 2, 2, 16, 3, 1>(bp, tmap, st, shape, sms);
-        if (delta == 1 && var == 3) return run_cfg<7, 2, 4, 2, 32, 2, 1>(bp, tmap, st, shape, sms);
-        if (delta == 1 && var == 4) return run_cfg<7, 2, 2, 2, 8, 4, 1>(bp, tmap, st, shape, sms);
-        if (delta == 1 && var == 5) return run_cfg<7, 2, 8, 2, 32, 3, 1>(bp, tmap, st, shape, sms);
-        if (delta == 1 && var == 6) return run_cfg<7, 2, 8, 2, 16, 4, 1>(bp, tmap, st, shape, sms);
-        if (delta == 1 && var == 7) return run_cfg<7, 2, 16, 2, 32, 3, 1>(bp, tmap, st, shape, sms);
-        if (delta == 1 && var == 8) return run_cfg<7, 2, 4, 2, 16, 3, 1>(bp, tmap, st, shape, sms);
-        return run_delta<7, 2, 8, 2, 32, 3>(delta, bp, tmap, st, shape, sms);
-    }
+    if (k == 7 && s == 2) return run_delta<7, 2, 8, 2, 32, 3>(delta, bp, tmap, st, shape, sms);
     return cudaErrorInvalidValue;
 }
 

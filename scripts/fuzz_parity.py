@@ -62,13 +62,9 @@ def main():
             X[0, rng.integers(0, m * n)] = np.inf
         layout = sp.Layout.CSC if rng.random() < 0.25 else sp.Layout.CSR
         spec = sp.ConvSpec(m, n, k, s, p)
-        build = str(rng.choice(["", "", "block", "warp", "persist"]))
-        if build:
-            os.environ["SPCONV_B200_BUILD"] = build
-        try:
+        build = str(rng.choice(["auto", "auto", "block", "warp", "persist"]))
+        with sp.options(build=build):
             t = sp.build_transform(sp.Kernel(k, kern64), spec, layout=layout)
-        finally:
-            os.environ.pop("SPCONV_B200_BUILD", None)
         rp, ri, rv = orc.build_native(m, n, k, s, p, kern)
         ptr = np.empty(t.rows + 1, np.int32)
         idx = np.empty(max(t.nnz, 1), np.int32)
@@ -96,15 +92,12 @@ def main():
         path = PATHS[int(rng.integers(0, len(PATHS)))] if rng.random() < 0.4 else None
         env = {}
         if path:
-            env["SPCONV_B200_PATH"] = path
+            env["path"] = path
         if rng.random() < 0.3:
-            env["SPCONV_B200_FUSED"] = str(int(rng.integers(0, 2)))
-        if rng.random() < 0.2:
-            env["SPCONV_B200_CHECK"] = str(rng.choice(["side", "same"]))
-        for kk, vv in env.items():
-            os.environ[kk] = vv
+            env["fused"] = str(int(rng.integers(0, 2)))
         try:
-            Y = sp.spmm(t, Xd[:, :m * n])
+            with sp.options(**env):
+                Y = sp.spmm(t, Xd[:, :m * n])
             torch.cuda.synchronize()
             got = Y.cpu().numpy()
             ok_y = np.array_equal(bits(got), bits(want))
@@ -112,9 +105,6 @@ def main():
             ok_y = path is not None and ("unsupported" in str(e) or "longer than" in str(e))
             if not ok_y:
                 print("ERROR", (m, n, k, s, p), batch, env, e)
-        finally:
-            for kk in env:
-                del os.environ[kk]
         cases += 1
         if not (ok and ok_y):
             fails += 1

@@ -57,3 +57,22 @@ def golden():
         js = json.load(f)
     npz = dict(np.load(os.path.join(GOLDEN, "golden.npz")))
     return js, npz
+
+
+@pytest.fixture
+def opts():
+    """opts(name=value, ...) sets process-wide kernel-path options
+    (spconv_set_option) for the rest of the test; restored afterwards."""
+    import paper_2411_19419_b200 as sp
+    saved = {}
+
+    def setter(**kw):
+        for k, v in kw.items():
+            if v is None:
+                continue
+            saved.setdefault(k, sp.get_option(k))
+            sp.set_option(k, v)
+
+    yield setter
+    for k, v in saved.items():
+        sp.set_option(k, v)

@@ -141,3 +141,23 @@ def test_coo_checks_before_any_device_work():
         sp.compile_triplets(3, 5, [0, 2], [1, 5], [1.0, 2.0])
     with pytest.raises(ValueError, match="layout must be 0"):
         sp.compile_triplets(3, 5, [0], [1], [1.0], layout=3)
+
+
+def test_path_options_roundtrip_and_errors():
+    """spconv_set_option / spconv_get_option: symbolic and integer values round
+    trip, unknown names and values are status 1, and the library's sources read
+    no environment variables (the options replace them)."""
+    with sp.options(path="tiled", fused="1", build="persist", spec_skew=-3):
+        assert sp.get_option("path") == "tiled"
+        assert sp.get_option("fused") == "1"
+        assert sp.get_option("build") == "persist"
+        assert sp.get_option("spec_skew") == "-3"
+    assert sp.get_option("path") == "auto" and sp.get_option("spec_skew") == "0"
+    with pytest.raises(ValueError, match="unknown option"):
+        sp.set_option("nope", "1")
+    with pytest.raises(ValueError, match="bad value"):
+        sp.set_option("path", "warp")
+    with pytest.raises(ValueError, match="integer"):
+        sp.set_option("spec_skew", "x")
+    for src in glob.glob(os.path.join(ROOT, "paper_2411_19419_b200", "csrc", "*.cu")):
+        assert "getenv" not in open(src).read(), src

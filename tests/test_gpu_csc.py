@@ -51,15 +51,9 @@ def csc_of(orc, spec, kern):
 
 
 def apply(torch, sp, t, X, path=None):
-    import os
     Xd = torch.from_numpy(np.ascontiguousarray(X, np.float32)).cuda()
-    if path:
-        os.environ["SPCONV_B200_PATH"] = path
-    try:
+    with sp.options(path=path):
         Y = sp.spmm(t, Xd)
-    finally:
-        if path:
-            del os.environ["SPCONV_B200_PATH"]
     torch.cuda.synchronize()
     return Y.cpu().numpy()
 

@@ -67,17 +67,8 @@ def run_spmm(torch, sp, t, X, path=None, ldx_pad=0):
     B, cols = X.shape
     Xd = torch.zeros(B, cols + ldx_pad, dtype=torch.float32, device="cuda")
     Xd[:, :cols] = torch.from_numpy(X)
-    old = os.environ.get("SPCONV_B200_PATH")
-    if path:
-        os.environ["SPCONV_B200_PATH"] = path
-    try:
+    with sp.options(path=path):
         Y = sp.spmm(t, Xd[:, :cols])
-    finally:
-        if path:
-            if old is None:
-                del os.environ["SPCONV_B200_PATH"]
-            else:
-                os.environ["SPCONV_B200_PATH"] = old
     torch.cuda.synchronize()
     return Y.cpu().numpy()
 
@@ -323,14 +314,14 @@ def test_generic_csr_upload(sp, orc, torch_cuda):
 
 
 @pytest.mark.parametrize("kernel", ["rowblock", "plain"])
-def test_generic_multivector_kernels(sp, orc, torch_cuda, kernel, monkeypatch):
+def test_generic_multivector_kernels(sp, orc, torch_cuda, kernel, opts):
     """Batches on a generic CSR: the row-block kernel (matrix staged once per
     CTA, images four at a time) and the thread-per-row kernel
-    (SPCONV_B200_GENERIC=plain), ragged and empty rows, row blocks that end
+    (option generic=plain), ragged and empty rows, row blocks that end
     mid-matrix, batches that are not a multiple of four, padded ldx,
     non-finite inputs; rows longer than 64 entries take the plain kernel."""
     if kernel == "plain":
-        monkeypatch.setenv("SPCONV_B200_GENERIC", "plain")
+        opts(generic="plain")
     rng = np.random.default_rng(5)
     for rows, cols, maxlen in ((300, 517, 40), (1000, 2000, 64), (77, 5000, 100)):
         lens = rng.integers(0, maxlen + 1, rows)
@@ -419,11 +410,11 @@ def test_band_path_is_default(sp, orc, torch_cuda, spec):
 
 
 @pytest.mark.parametrize("fused", ["0", "1"])
-def test_band_concurrent_streams(sp, orc, torch_cuda, fused, monkeypatch):
+def test_band_concurrent_streams(sp, orc, torch_cuda, fused, opts):
     """One immutable handle applied on two streams at once (the band check's
     per-segment bytes are rewritten with identical values: benign), with the
     check kernel and with the fused check-and-apply."""
-    monkeypatch.setenv("SPCONV_B200_FUSED", fused)
+    opts(fused=fused)
     spec = (256, 256, 3, 1, 1)
     kern, X = problem(orc, 12, 256, 256, 3, batch=16)
     t = build(sp, spec, kern)
@@ -452,11 +443,8 @@ def test_spmv_spec_mispredicted_rows(sp, orc, torch_cuda, skew):
     kern, X = problem(orc, 13, 64, 48, 5, batch=2)
     t = build(sp, spec, kern)
     want = orc.spmm_native(*orc.build_native(*spec, kern), X)
-    os.environ["SPCONV_B200_SPEC_SKEW"] = str(skew)
-    try:
+    with sp.options(spec_skew=skew):
         Y = run_spmm(torch_cuda, sp, t, X)
-    finally:
-        del os.environ["SPCONV_B200_SPEC_SKEW"]
     assert t.last_kernel == "csr_spmv_bulk<spec>"
     assert np.array_equal(bits(Y), bits(want))
 
@@ -469,17 +457,16 @@ class _DevArray:
                                          "version": 3}
 
 
-@pytest.mark.parametrize("check", ["side", "same", "fused"])
+@pytest.mark.parametrize("check", ["same", "fused"])
 @pytest.mark.parametrize("spec", [(256, 256, 3, 1, 1), (300, 260, 7, 2, 3)])
-def test_band_check_reads_the_matrix(sp, orc, torch_cuda, spec, check, monkeypatch):
+def test_band_check_reads_the_matrix(sp, orc, torch_cuda, spec, check, opts):
     """The band path re-reads T on every call: entries altered in device memory
     after the build (a value, a column moved far outside its tile's input
     window, a column moved to an earlier image row) are picked up by the next
     spmm -- the affected segments fail the check and take the per-entry loop --
     and the output is bit-exact vs the oracle on the altered CSR."""
-    # check kernel on a side stream / on the caller's stream / fused into the apply
-    monkeypatch.setenv("SPCONV_B200_CHECK", "side" if check == "side" else "same")
-    monkeypatch.setenv("SPCONV_B200_FUSED", "1" if check == "fused" else "0")
+    # check kernel on the caller's stream / fused into the apply
+    opts(fused="1" if check == "fused" else "0")
     m, n, k = spec[:3]
     kern, X = problem(orc, 14, m, n, k, batch=6)
     t = build(sp, spec, kern)
@@ -515,15 +502,14 @@ def test_band_check_reads_the_matrix(sp, orc, torch_cuda, spec, check, monkeypat
 
 @pytest.mark.parametrize("bulk_store", ["0", "1"])
 @pytest.mark.parametrize("variant", ["block", "warp", "persist"])
-def test_build_variants_bitexact(sp, orc, variant, bulk_store, monkeypatch):
-    """The CSR build kernels (block scan / warp-local / persistent, SPCONV_B200_BUILD), with
+def test_build_variants_bitexact(sp, orc, variant, bulk_store, opts):
+    """The CSR build kernels (block scan / warp-local / persistent, option build), with
     the staged entries written back by TMA bulk stores or by 16-byte stores
-    (SPCONV_B200_BULK_STORE), give the oracle's arrays for every unrolled k,
+    (option bulk_store), give the oracle's arrays for every unrolled k,
     dense and zero-tap kernels; so does the CSC build."""
     rng = np.random.default_rng(21)
-    monkeypatch.setenv("SPCONV_B200_BULK_STORE", bulk_store)
-    os.environ["SPCONV_B200_BUILD"] = variant
-    try:
+    opts(bulk_store=bulk_store, build=variant)
+    if True:
         for spec in [(70, 45, 1, 1, 1), (130, 97, 3, 1, 1), (64, 80, 5, 2, 2), (101, 77, 7, 2, 3),
                      (48, 50, 11, 3, 10), (33, 20, 3, 2, 0)]:
             k = spec[2]
@@ -540,18 +526,16 @@ def test_build_variants_bitexact(sp, orc, variant, bulk_store, monkeypatch):
                 got = tc.export()
                 assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
                 assert np.array_equal(got[2].view(np.uint64), want[2].view(np.uint64))
-    finally:
-        del os.environ["SPCONV_B200_BUILD"]
 
 
-@pytest.mark.parametrize("stage", ["bulk", "lsu"])
-def test_latency_spmv_staging_variants(sp, orc, torch_cuda, stage):
+@pytest.mark.parametrize("stage", ["bulk", "lanes"])
+def test_latency_spmv_staging_variants(sp, orc, torch_cuda, stage, opts):
     """Both stagings of the latency SpMV (bulk copies / per-lane 16-byte
-    loads, SPCONV_B200_STAGE), dense-tap (closed-form run) and zero-tap
+    loads, option stage), dense-tap (closed-form run) and zero-tap
     (row_ptr-driven) transforms, batch 1 and 2: bit-exact."""
     rng = np.random.default_rng(31)
-    os.environ["SPCONV_B200_STAGE"] = stage
-    try:
+    opts(stage=stage)
+    if True:
         for spec in [(512, 512, 5, 2, 2), (97, 130, 3, 1, 1), (64, 72, 7, 2, 3), (33, 35, 5, 3, 4)]:
             m, n, k = spec[:3]
             kern, X = problem(orc, 51, m, n, k, batch=2)
@@ -565,8 +549,6 @@ def test_latency_spmv_staging_variants(sp, orc, torch_cuda, stage):
                     Y = run_spmm(torch_cuda, sp, t, X[:b])
                     assert t.last_kernel.startswith("csr_spmv_bulk")
                     assert np.array_equal(bits(Y), bits(want[:b])), (spec, zero, b)
-    finally:
-        del os.environ["SPCONV_B200_STAGE"]
 
 
 @pytest.mark.parametrize("batch", [1, 2, 6])
@@ -584,13 +566,8 @@ def test_spmm_misaligned_buffers(sp, orc, torch_cuda, batch):
     Xd = xb[1:].view(batch, t.cols)
     Yd = yb[1:-1].view(batch, t.rows)
     for path in (None, "tiled", "generic"):
-        if path:
-            os.environ["SPCONV_B200_PATH"] = path
-        try:
+        with sp.options(path=path):
             sp.spmm(t, Xd, Yd)
-        finally:
-            if path:
-                del os.environ["SPCONV_B200_PATH"]
         torch.cuda.synchronize()
         got = yb.cpu().numpy()
         assert got[0] == -3.0 and got[-1] == -3.0, path
@@ -623,12 +600,11 @@ def test_spmm_in_cuda_graph(sp, orc, torch_cuda, spec, batch):
 @pytest.mark.parametrize("fused", ["0", "1"])
 @pytest.mark.parametrize("spec", [(1024, 1024, 3, 1, 1), (200, 132, 5, 1, 2), (130, 68, 3, 2, 0),
                                   (300, 260, 7, 2, 3), (97, 64, 5, 2, 2), (64, 40, 3, 1, 1)])
-def test_band_fused_and_two_kernel(sp, orc, torch_cuda, spec, fused, monkeypatch):
+def test_band_fused_and_two_kernel(sp, orc, torch_cuda, spec, fused, opts):
     """The fused check-and-apply (segments checked by the producer warps, a
     fixup pass after) and the two-kernel form give the same bit-exact results
     on every band geometry, including grids with more CTAs than work items."""
-    monkeypatch.setenv("SPCONV_B200_FUSED", fused)
-    monkeypatch.setenv("SPCONV_B200_CHECK", "same")
+    opts(fused=fused)
     m, n, k = spec[:3]
     kern, X = problem(orc, 18, m, n, k, batch=5)
     t = build(sp, spec, kern)

@@ -43,8 +43,8 @@ def zero_kernel(rng, k, frac):
 
 @pytest.mark.parametrize("fused", ["0", "1"])
 @pytest.mark.parametrize("spec", SPECS)
-def test_zero_tap_band_bitexact(sp, orc, torch_cuda, spec, fused, monkeypatch):
-    monkeypatch.setenv("SPCONV_B200_FUSED", fused)
+def test_zero_tap_band_bitexact(sp, orc, torch_cuda, spec, fused, opts):
+    opts(fused=fused)
     m, n, k = spec[:3]
     rng = np.random.default_rng(hash(spec) % 1000)
     for frac in (0.2, 0.5, 0.8):
@@ -65,8 +65,8 @@ def test_zero_tap_band_bitexact(sp, orc, torch_cuda, spec, fused, monkeypatch):
 
 
 @pytest.mark.parametrize("fused", ["0", "1"])
-def test_zero_tap_band_check_reads_the_matrix(sp, orc, torch_cuda, fused, monkeypatch):
-    monkeypatch.setenv("SPCONV_B200_FUSED", fused)
+def test_zero_tap_band_check_reads_the_matrix(sp, orc, torch_cuda, fused, opts):
+    opts(fused=fused)
     spec = (256, 256, 3, 1, 1)
     m, n, k = spec[:3]
     kern = np.array([0.5, 0.0, -1.25, 0.0, 2.0, 0.0, 0.75, 0.0, -0.5], np.float32)
@@ -98,7 +98,7 @@ def test_zero_tap_latency_spmv_closed_form(sp, orc, torch_cuda, spec):
     """Batch <= 2: the latency SpMV predicts each warp's run from the tap mask
     (W[j] and the stored-tap column counts) and fetches it with no dependent
     row_ptr load; bit-exact, including the prediction-mismatch path
-    (SPCONV_B200_SPEC_SKEW)."""
+    (option spec_skew)."""
     import os
     m, n, k = spec[:3]
     rng = np.random.default_rng(k + 100)
@@ -111,9 +111,6 @@ def test_zero_tap_latency_spmv_closed_form(sp, orc, torch_cuda, spec):
         Y = run_spmm(torch_cuda, sp, t, X[:b])
         assert t.last_kernel == "csr_spmv_bulk<spec>"
         assert np.array_equal(bits(Y), bits(want[:b])), (spec, b)
-    os.environ["SPCONV_B200_SPEC_SKEW"] = "4"
-    try:
+    with sp.options(spec_skew=4):
         Y = run_spmm(torch_cuda, sp, t, X[:1])
-    finally:
-        del os.environ["SPCONV_B200_SPEC_SKEW"]
     assert np.array_equal(bits(Y), bits(want[:1]))
