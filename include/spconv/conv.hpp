@@ -136,13 +136,13 @@ inline Transform build_transform(const Kernel& kern, const ConvSpec& spec,
 
 /// vec, SpMV, reshape (inc/conv.hpp:207-215) on the GPU.
 inline Grid convolve(const Transform& t, const Grid& a, int threads = 0) {
-    (void)threads;
+    const int nt = threads > 0 ? threads : thread_cap();
     if (a.rows != t.spec.m || a.cols != t.spec.n)
         throw std::invalid_argument("convolve: input is " + std::to_string(a.rows) + "x" +
                                     std::to_string(a.cols) + " but transform expects " +
                                     t.spec.str());
     DenseVector out(static_cast<std::size_t>(t.spec.output_len()));
-    detail::check(spconv_convolve_host_f64(t.matrix.handle(), a.values.data(), out.data(), 1));
+    detail::check(spconv_convolve_host_f64_threads(t.matrix.handle(), a.values.data(), out.data(), 1, nt));
     return Grid(t.spec.m_out(), t.spec.n_out(), std::move(out));
 }
 

@@ -288,16 +288,28 @@ inline SparseMatrix spgemm(const SparseMatrix& a, const SparseMatrix& b, Layout 
     return SparseMatrix(h);
 }
 
-/// y = M x (inc/sparse.hpp:214-261).  `threads` is accepted for source
-/// compatibility and ignored: the product runs on the GPU.
+/// Thread count used by spmv when the caller does not pass one
+/// (inc/sparse.hpp:171-176): SPCONV_THREADS, default 1.  On the device it
+/// selects only the reference's CSC partial-combine order (results of the
+/// reference's CSR path do not depend on it).
+inline int thread_cap() {
+    const char* env = std::getenv("SPCONV_THREADS");
+    if (env == nullptr) return 1;
+    const long v = std::strtol(env, nullptr, 10);
+    return v >= 1 ? static_cast<int>(v) : 1;
+}
+
+/// y = M x (inc/sparse.hpp:214-261) in fp64 on the GPU, bit-identical to the
+/// reference's spmv(m, x, threads) -- for CSC storage including its
+/// per-thread partial combine (spconv_convolve_host_f64_threads).
 inline DenseVector spmv(const SparseMatrix& m, std::span<const double> x, int threads = 0) {
-    (void)threads;
+    const int nt = threads > 0 ? threads : thread_cap();
     if (m.cols() != static_cast<index_t>(x.size()))
         throw std::invalid_argument("spmv: matrix has " + std::to_string(m.cols()) +
                                     " columns but vector has " + std::to_string(x.size()) +
                                     " elements");
     DenseVector y(static_cast<std::size_t>(m.rows()), 0.0);
-    detail::check(spconv_convolve_host_f64(m.handle(), x.data(), y.data(), 1));
+    detail::check(spconv_convolve_host_f64_threads(m.handle(), x.data(), y.data(), 1, nt));
     return y;
 }
 

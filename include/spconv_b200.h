@@ -69,9 +69,12 @@ int spconv_build_csr(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
  * storage layout of inc/sparse.hpp:24: 0 = CSR (same as spconv_build_csr),
  * 1 = CSC -- column c = a*n + b holds its rows in ascending order, built on
  * the device in closed form (csc_build.cu), bit-identical to the reference's
- * compile(..., Layout::CSC).  A CSC handle also holds the row-major arrays
- * the SpMV/SpMM kernels read; export / copy / device_ptrs / text show the
- * storage layout. */
+ * compile(..., Layout::CSC).  A CSC conv handle holds ONLY that storage:
+ * spconv_spmm / spconv_spmm_f64 read it (detail::spmv_csc_cols,
+ * inc/sparse.hpp:194-205, as a per-output gather at closed-form places,
+ * csc_apply.cu; for batches of the band geometries a CSC band check feeding
+ * the register-blocked apply, spmm_band.cu), checking it against the taps on
+ * every call. */
 int spconv_build_transform(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
                            const float* kernel_kxk, int layout, int device, void* stream,
                            spconv_csr** out);
@@ -158,10 +161,19 @@ int spconv_csr_shape(const spconv_csr* h, int64_t* rows, int64_t* cols, int64_t*
  * inc/conv.hpp:166); returns 1 for an uploaded generic CSR. */
 int spconv_csr_spec(const spconv_csr* h, int64_t spec5[5]);
 
-/* Device pointers of the storage arrays (read-only; owned by the handle):
- * ptr over the major dimension (rows for CSR, columns for CSC). */
+/* Device pointers of the storage arrays (owned by the handle): ptr over the
+ * major dimension (rows for CSR, columns for CSC).  Writing through them is
+ * allowed; every later apply follows the storage as it then stands (CSR: the
+ * band check re-reads it each call; CSC: once its arrays are handed out, each
+ * apply first checks them on the device and waits for the verdict, and an
+ * altered storage is applied with the reference's scatter semantics). */
 int spconv_csr_device_ptrs(const spconv_csr* h, const int32_t** row_ptr, const int32_t** col_idx,
                            const float** vals);
+
+/* Device bytes of the index / value arrays the handle holds (row-major,
+ * column-major, exact-fp64 copies): 8*nnz + 4*(major+1) per layout kept
+ * (+ 8*nnz per exact-value array).  A CSC conv transform holds one layout. */
+int spconv_csr_storage_bytes(const spconv_csr* h, int64_t* bytes);
 
 /* Synchronous export to host, widened to the reference's types: ptr(),
  * idx(), val() of inc/sparse.hpp:128-130, in the handle's layout (ptr has
@@ -201,11 +213,26 @@ int spconv_convolve_host(const spconv_csr* h, const float* X_host, float* Y_host
 int spconv_spmm_f64(const spconv_csr* h, const double* X_dev, int64_t ldx, double* Y_dev, int64_t ldy,
                     int64_t batch, void* stream);
 
+/* spconv_spmm_f64 with the reference's thread count (spmv(m, x, threads),
+ * inc/sparse.hpp:214-258): for a CSC matrix with nt = min(threads, cols) > 1
+ * the columns are cut into chunks of ceil(cols / nt), each chunk summed into a
+ * partial from 0.0 and the partials added to y in chunk order -- the
+ * reference's CSC combine, bit for bit.  threads <= 1, or a CSR matrix: the
+ * single-thread order (the reference's CSR rows do not depend on it). */
+int spconv_spmm_f64_threads(const spconv_csr* h, const double* X_dev, int64_t ldx, double* Y_dev, int64_t ldy,
+                            int64_t batch, int threads, void* stream);
+
 /* The reference-semantics apply on fp64 HOST buffers (the reference
  * Grid/DenseVector types, inc/grid.hpp:18-24), used by the drop-in
  * convolve()/spmv(): fp64 in, spconv_spmm_f64 on the device, fp64 out. */
 int spconv_convolve_host_f64(const spconv_csr* h, const double* X_host, double* Y_host,
                              int64_t batch);
+
+/* spconv_convolve_host_f64 with the reference's thread count (see
+ * spconv_spmm_f64_threads); the drop-in spmv / convolve pass
+ * threads > 0 ? threads : thread_cap() (SPCONV_THREADS, inc/sparse.hpp:171-176). */
+int spconv_convolve_host_f64_threads(const spconv_csr* h, const double* X_host, double* Y_host,
+                                     int64_t batch, int threads);
 
 /* Text form of the matrix, rendered on the device: with
  * transform_header_line != 0, write_transform (inc/conv.hpp:217-224):

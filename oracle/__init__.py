@@ -67,6 +67,7 @@ class Oracle:
         L.orc_transpose.argtypes = [i64, i64] + [C.c_void_p] * 6
         L.orc_spmv_csc_f64.argtypes = [i64] + [C.c_void_p] * 5 + [i64]
         L.orc_spmv_csc_f32_fma.argtypes = [i64] + [C.c_void_p] * 5 + [i64]
+        L.orc_spmv_csc_f64_threads.argtypes = [i64] + [C.c_void_p] * 5 + [i64, i64]
         self.L = L
 
     # -- rng.hpp ------------------------------------------------------------
@@ -189,6 +190,15 @@ class Oracle:
         self.L.orc_spmv_csc_f64(cols, _p(np.ascontiguousarray(ptr, np.int64)),
                                 _p(np.ascontiguousarray(idx, np.int64)),
                                 _p(np.ascontiguousarray(val, np.float64)), _p(x), _p(y), rows)
+        return y
+
+    def spmv_csc_f64_threads(self, rows, ptr, idx, val, x, threads) -> np.ndarray:
+        cols = ptr.size - 1
+        y = np.empty(rows, np.float64)
+        x = np.ascontiguousarray(x, np.float64)
+        self.L.orc_spmv_csc_f64_threads(cols, _p(np.ascontiguousarray(ptr, np.int64)),
+                                        _p(np.ascontiguousarray(idx, np.int64)),
+                                        _p(np.ascontiguousarray(val, np.float64)), _p(x), _p(y), rows, threads)
         return y
 
     def spmv_csc_f32_fma(self, rows, ptr, idx, val, x) -> np.ndarray:

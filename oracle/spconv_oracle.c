@@ -380,6 +380,36 @@ void orc_spmv_csc_f64(int64_t cols, const int64_t *ptr, const int64_t *idx, cons
     }
 }
 
+/* spmv with nt > 1 threads on a CSC matrix (inc/sparse.hpp:221-258): nt is
+ * capped at the column count, columns are cut into chunks of ceil(cols / nt),
+ * thread t scatters chunk t into its own partial vector (from 0.0), and the
+ * partials are added to y (from 0.0) in thread order. */
+void orc_spmv_csc_f64_threads(int64_t cols, const int64_t *ptr, const int64_t *idx, const double *val,
+                              const double *x, double *y, int64_t rows, int64_t nt) {
+    if (nt > cols) nt = cols > 0 ? cols : 1;
+    if (nt <= 1) {
+        orc_spmv_csc_f64(cols, ptr, idx, val, x, y, rows);
+        return;
+    }
+    const int64_t chunk = (cols + nt - 1) / nt;
+    double *part = (double *)malloc(sizeof(double) * (size_t)(rows > 0 ? rows : 1));
+    for (int64_t i = 0; i < rows; ++i) y[i] = 0.0;
+    for (int64_t t = 0; t < nt; ++t) {
+        int64_t lo = t * chunk < cols ? t * chunk : cols;
+        int64_t hi = lo + chunk < cols ? lo + chunk : cols;
+        for (int64_t i = 0; i < rows; ++i) part[i] = 0.0;
+        for (int64_t j = lo; j < hi; ++j) {
+            const double xj = x[j];
+            for (int64_t k = ptr[j]; k < ptr[j + 1]; ++k) {
+                const double prod = val[k] * xj;
+                part[idx[k]] = part[idx[k]] + prod;
+            }
+        }
+        for (int64_t i = 0; i < rows; ++i) y[i] = y[i] + part[i];
+    }
+    free(part);
+}
+
 /* The same scatter in fp32 with one rounding per step (fmaf): the device
  * contract for CSC transforms.  Per output it is the CSR ordered-fmaf chain,
  * so it is bit-identical to orc_spmv_csr_f32_fma on the transposed storage. */

@@ -64,6 +64,9 @@ _decl("spconv_spmm", [_vp, _vp, _i64, _vp, _i64, _i64, _vp])
 _decl("spconv_convolve_host", [_vp, _vp, _vp, _i64])
 _decl("spconv_convolve_host_f64", [_vp, _vp, _vp, _i64])
 _decl("spconv_spmm_f64", [_vp, _vp, _i64, _vp, _i64, _i64, _vp])
+_decl("spconv_csr_storage_bytes", [_vp, _P(_i64)])
+_decl("spconv_spmm_f64_threads", [_vp, _vp, _i64, _vp, _i64, _i64, C.c_int, _vp])
+_decl("spconv_convolve_host_f64_threads", [_vp, _vp, _vp, _i64, C.c_int])
 _decl("spconv_csr_last_kernel", [_vp], C.c_char_p)
 _decl("spconv_band_check_status", [_vp, _P(_i64), _P(_i64)])
 _decl("spconv_csr_write_text", [_vp, C.c_int, _vp, _i64, _P(_i64)])
@@ -308,6 +311,13 @@ class Transform:
         return buf.raw[: n.value]
 
     @property
+    def storage_bytes(self) -> int:
+        """Device bytes of the index / value arrays held (spconv_csr_storage_bytes)."""
+        b = _i64()
+        _check(lib.spconv_csr_storage_bytes(self._h, C.byref(b)))
+        return b.value
+
+    @property
     def last_kernel(self) -> str:
         """Kernel(s) the last apply on this transform launched ("a+b" = two launches)."""
         return lib.spconv_csr_last_kernel(self._h).decode()
@@ -477,10 +487,12 @@ def convolve_batch(t: Transform, X_host, Y_host=None):
     return Y_host
 
 
-def spmm_f64(t: Transform, X, Y=None, stream=None):
+def spmm_f64(t: Transform, X, Y=None, stream=None, threads: int = 1):
     """Y[b] = T X[b] in fp64 with the reference's arithmetic (spconv_spmm_f64):
-    X [batch, cols] CUDA float64; bit-identical to the reference's spmv() (the
-    handle's exact double values are used when it keeps them)."""
+    X [batch, cols] CUDA float64; bit-identical to the reference's spmv(m, x,
+    threads) (the handle's exact double values are used when it keeps them;
+    `threads` matters for CSC storage only: the reference's per-thread partial
+    combine, inc/sparse.hpp:243-258)."""
     import torch
     if not (isinstance(X, torch.Tensor) and X.is_cuda and X.dtype == torch.float64):
         raise ValueError("spmm_f64: expected a CUDA float64 tensor")
@@ -488,12 +500,12 @@ def spmm_f64(t: Transform, X, Y=None, stream=None):
         raise ValueError(f"spmm_f64: expected X of shape [batch, {t.cols}] with unit column stride")
     if Y is None:
         Y = torch.empty(X.shape[0], t.rows, dtype=torch.float64, device=X.device)
-    _check(lib.spconv_spmm_f64(t._h, X.data_ptr(), X.stride(0), Y.data_ptr(), Y.stride(0), X.shape[0],
-                               _stream_handle(stream)))
+    _check(lib.spconv_spmm_f64_threads(t._h, X.data_ptr(), X.stride(0), Y.data_ptr(), Y.stride(0), X.shape[0],
+                                       int(threads), _stream_handle(stream)))
     return Y
 
 
-def convolve(t: Transform, a) -> np.ndarray:
+def convolve(t: Transform, a, threads: int = 1) -> np.ndarray:
     """Reference-semantics apply of one m x n grid (inc/conv.hpp:207-215):
     fp64 in, fp64 device arithmetic with the reference's rounding, fp64 out --
     bit-identical to the reference (exact double taps included)."""
@@ -505,7 +517,7 @@ def convolve(t: Transform, a) -> np.ndarray:
         raise ValueError(f"convolve: input is {r}x{c} but transform expects {t.spec.str()}")
     a = np.ascontiguousarray(a)
     out = np.empty(t.rows, np.float64)
-    _check(lib.spconv_convolve_host_f64(t._h, a.ctypes.data, out.ctypes.data, 1))
+    _check(lib.spconv_convolve_host_f64_threads(t._h, a.ctypes.data, out.ctypes.data, 1, int(threads)))
     return out.reshape(t.spec.m_out, t.spec.n_out)
 
 

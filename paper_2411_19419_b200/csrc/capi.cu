@@ -223,6 +223,201 @@ int device_sm_count() {
     return sms;
 }
 
+// ---- CSC conv transforms: verdict words, tap tables, the exposed-storage protocol ----
+
+// One mapped (zero-copy) host word per CSC conv handle: device checks that
+// fail store 1 there, and the next host call on the handle reads it without a
+// synchronisation (a sticky verdict, like CUDA's sticky errors).
+std::mutex g_flag_mu;
+std::vector<int*> g_flag_free;
+
+int* flag_alloc() {
+    std::lock_guard<std::mutex> lk(g_flag_mu);
+    if (g_flag_free.empty()) {
+        int* page = nullptr;
+        constexpr int kWords = 1024;  // one 4 KB page of words; never released
+        if (cudaHostAlloc(reinterpret_cast<void**>(&page), kWords * sizeof(int),
+                          cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess)
+            return nullptr;
+        for (int i = kWords - 1; i >= 0; --i) g_flag_free.push_back(page + i);
+    }
+    int* w = g_flag_free.back();
+    g_flag_free.pop_back();
+    *reinterpret_cast<volatile int*>(w) = 0;
+    return w;
+}
+
+void flag_free(int* w) {
+    if (!w) return;
+    std::lock_guard<std::mutex> lk(g_flag_mu);
+    g_flag_free.push_back(w);
+}
+
+bool csc_native(const spconv_csr* h) { return h->layout == 1 && h->is_conv && !h->row_ptr && h->csc_ptr; }
+
+// Stored = the DOUBLE tap is non-zero when the handle keeps doubles (a tap that
+// narrows to 0.0f is still an entry), else the fp32 tap (inc/sparse.hpp:335).
+bool tap_stored(const spconv_csr* h, size_t q) {
+    return h->host_taps64.empty() ? h->host_taps[q] != 0.0f : h->host_taps64[q] != 0.0;
+}
+
+// W[j] = sum over stored (j, i) of #{y : 0 <= s y + i - p < n} (the CSC column
+// offsets' closed form; = sum_y cy(y) = sy for a kernel without zero taps).
+void csc_tables(const spconv_csr* h, spb::CscGatherParams& cp) {
+    const Geom& g = h->g;
+    cp.zt = 0;
+    for (int64_t j = 0; j < g.k && j < 32; ++j) {
+        uint32_t row = 0;
+        long long wj = 0;
+        for (int64_t i = 0; i < g.k; ++i) {
+            if (!tap_stored(h, (size_t)(j * g.k + i))) {
+                cp.zt = 1;
+                continue;
+            }
+            row |= 1u << i;
+            const int64_t lo = g.p - i <= 0 ? 0 : (g.p - i + g.s - 1) / g.s;
+            const int64_t hi = g.n + g.p - i - 1 < 0 ? -1 : std::min<int64_t>(g.no - 1, (g.n + g.p - i - 1) / g.s);
+            wj += std::max<int64_t>(0, hi - lo + 1);
+        }
+        cp.nzrow[j] = row;
+        cp.zw[j] = wj;
+    }
+}
+
+spb::CscGatherParams csc_params(const spconv_csr* h, bool f64) {
+    spb::CscGatherParams cp{};
+    const Geom& g = h->g;
+    cp.col_ptr = h->csc_ptr;
+    cp.row_idx = h->csc_idx;
+    cp.vals = h->csc_vals;
+    cp.vals64 = f64 ? h->csc_vals64 : nullptr;
+    cp.taps32 = h->taps;
+    cp.taps64 = f64 ? h->taps64 : nullptr;
+    cp.m = (int)g.m;
+    cp.n = (int)g.n;
+    cp.k = (int)g.k;
+    cp.s = (int)g.s;
+    cp.p = (int)g.p;
+    cp.mo = (int)g.mo;
+    cp.no = (int)g.no;
+    cp.rows = h->rows;
+    cp.cols = h->cols;
+    cp.nnz = h->nnz;
+    cp.fail = h->fail_flag;
+    csc_tables(h, cp);
+    return cp;
+}
+
+int csc_sticky(const spconv_csr* h, const char* who) {
+    if (h->fail_flag && !h->exposed.load() && *reinterpret_cast<volatile int*>(h->fail_flag))
+        return fail(SPCONV_ECUDA, std::string(who) +
+                                      ": the CSC storage no longer matches the transform of its taps "
+                                      "(a device check failed in an earlier call)");
+    return SPCONV_OK;
+}
+
+// Exposed CSC handles (spconv_csr_device_ptrs handed out the arrays): the
+// storage is checked on the device and the host waits for the verdict; when it
+// no longer is the transform of the taps, the call applies the storage as it
+// stands (repair_apply) -- the reference's scatter semantics.  Not capturable.
+int csc_exposed_clean(spconv_csr* h, cudaStream_t st, bool f64, bool* clean) {
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    CK(cudaStreamIsCapturing(st, &cap));
+    if (cap != cudaStreamCaptureStatusNone)
+        return fail(SPCONV_EINVAL, "a CSC handle whose arrays were handed out by spconv_csr_device_ptrs "
+                                   "cannot be applied under stream capture");
+    spb::CscGatherParams cp = csc_params(h, f64);
+    int* d = nullptr;
+    CK(cudaMallocAsync(&d, sizeof(int), st));
+    cp.fail = d;
+    cp.verify_only = 1;
+    int v = 1;
+    cudaError_t e = cudaMemsetAsync(d, 0, sizeof(int), st);
+    if (e == cudaSuccess) e = spb::launch_csc_gather(cp, f64, st, device_sm_count());
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&v, d, sizeof(int), cudaMemcpyDeviceToHost, st);
+    cudaFreeAsync(d, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "CSC storage check");
+    *clean = v == 0;
+    return SPCONV_OK;
+}
+
+// y = the reference's CSC scatter over the storage as it stands (inc/sparse.hpp:
+// 194-205, 243-258): entries in (column, position) order regrouped by row --
+// a stable counting sort on the host -- then the row-major kernels (fp32
+// ordered fmaf, or fp64 with the thread-chunk combine).
+int csc_repair_apply(spconv_csr* h, const void* X, int64_t ldx, void* Y, int64_t ldy, int64_t batch,
+                     cudaStream_t st, bool f64, int64_t chunk) {
+    const int64_t rows = h->rows, cols = h->cols, nnz = h->nnz;
+    std::vector<int32_t> cpv((size_t)cols + 1), ri((size_t)std::max<int64_t>(nnz, 1));
+    std::vector<float> cv((size_t)std::max<int64_t>(nnz, 1));
+    std::vector<double> cv64;
+    CK(cudaStreamSynchronize(st));
+    CK(cudaMemcpy(cpv.data(), h->csc_ptr, cpv.size() * 4, cudaMemcpyDeviceToHost));
+    if (nnz > 0) {
+        CK(cudaMemcpy(ri.data(), h->csc_idx, (size_t)nnz * 4, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(cv.data(), h->csc_vals, (size_t)nnz * 4, cudaMemcpyDeviceToHost));
+        if (f64 && h->csc_vals64) {
+            cv64.resize((size_t)nnz);
+            CK(cudaMemcpy(cv64.data(), h->csc_vals64, (size_t)nnz * 8, cudaMemcpyDeviceToHost));
+        }
+    }
+    for (int64_t c = 0; c < cols; ++c)
+        if (cpv[(size_t)c] < 0 || cpv[(size_t)c] > cpv[(size_t)c + 1] || cpv[(size_t)c + 1] > nnz)
+            return fail(SPCONV_EINVAL, "CSC storage altered through spconv_csr_device_ptrs: col_ptr is not "
+                                       "non-decreasing within [0, nnz]");
+    std::vector<int32_t> rp((size_t)rows + 1, 0);
+    int64_t used = 0;
+    for (int64_t c = 0; c < cols; ++c)
+        for (int32_t e = cpv[(size_t)c]; e < cpv[(size_t)c + 1]; ++e) {
+            if (ri[(size_t)e] < 0 || ri[(size_t)e] >= rows)
+                return fail(SPCONV_EINVAL, "CSC storage altered through spconv_csr_device_ptrs: row index " +
+                                               std::to_string(ri[(size_t)e]) + " out of range");
+            ++rp[(size_t)ri[(size_t)e] + 1];
+            ++used;
+        }
+    int64_t kmax = 0;
+    for (int64_t r = 0; r < rows; ++r) kmax = std::max<int64_t>(kmax, rp[(size_t)r + 1]), rp[(size_t)r + 1] += rp[(size_t)r];
+    std::vector<int32_t> cur(rp.begin(), rp.end() - 1), ci((size_t)std::max<int64_t>(used, 1));
+    std::vector<float> vv((size_t)std::max<int64_t>(used, 1));
+    std::vector<double> vv64(cv64.empty() ? 0 : (size_t)std::max<int64_t>(used, 1));
+    for (int64_t c = 0; c < cols; ++c)
+        for (int32_t e = cpv[(size_t)c]; e < cpv[(size_t)c + 1]; ++e) {
+            const int32_t d = cur[(size_t)ri[(size_t)e]]++;
+            ci[(size_t)d] = (int32_t)c;
+            vv[(size_t)d] = cv[(size_t)e];
+            if (!vv64.empty()) vv64[(size_t)d] = cv64[(size_t)e];
+        }
+    const size_t b_rp = ((rp.size() * 4) + 255) & ~size_t(255), b_ix = ((ci.size() * 4) + 255) & ~size_t(255);
+    char* mem = nullptr;
+    CK(cudaMalloc(&mem, b_rp + 2 * b_ix + vv64.size() * 8 + 256));
+    auto* d_rp = reinterpret_cast<int32_t*>(mem);
+    auto* d_ci = reinterpret_cast<int32_t*>(mem + b_rp);
+    auto* d_vv = reinterpret_cast<float*>(mem + b_rp + b_ix);
+    auto* d_v64 = vv64.empty() ? nullptr : reinterpret_cast<double*>(mem + b_rp + 2 * b_ix);
+    cudaError_t e = cudaMemcpy(d_rp, rp.data(), rp.size() * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(d_ci, ci.data(), ci.size() * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(d_vv, vv.data(), vv.size() * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && d_v64) e = cudaMemcpy(d_v64, vv64.data(), vv64.size() * 8, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        if (f64) {
+            spb::F64Params fp{d_rp, d_ci, d_vv, d_v64, static_cast<const double*>(X), ldx, static_cast<double*>(Y),
+                              ldy, (int)rows, (int)batch};
+            fp.chunk = chunk;
+            e = spb::launch_spmm_f64(fp, st);
+        } else {
+            spb::GenericParams gp{d_rp, d_ci, d_vv, static_cast<const float*>(X), ldx, static_cast<float*>(Y), ldy,
+                                  (int)rows, (int)batch};
+            e = spb::launch_generic(gp, st);
+        }
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(mem);
+    if (e != cudaSuccess) return cuda_fail(e, "CSC apply of the altered storage");
+    (void)kmax;
+    return SPCONV_OK;
+}
+
 int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
              int64_t batch, cudaStream_t st) {
     if (batch == 0) return SPCONV_OK;
@@ -233,8 +428,37 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
                         (reinterpret_cast<uintptr_t>(X) % 16 == 0) && encode_fn() != nullptr &&
                         g.m < (1ll << 30) && g.n < (1ll << 30);
 
+    // ---- CSC storage of a conv transform: the CSC kernels ----
+    const bool csc = csc_native(h);
+    if (csc) {
+        if (int rc = csc_sticky(h, "spconv_spmm")) return rc;
+        if (h->exposed.load()) {
+            bool clean = false;
+            if (int rc = csc_exposed_clean(h, st, false, &clean)) return rc;
+            if (!clean) {
+                h->last_kernel.store("csc_gather<verify>+csc_repair");
+                return csc_repair_apply(h, X, ldx, Y, ldy, batch, st, false, 0);
+            }
+        }
+        bool finite = true, any = false;
+        for (size_t q = 0; q < h->host_taps.size(); ++q) finite &= std::isfinite(h->host_taps[q]), any |= tap_stored(h, q);
+        const bool band = h->band_tw > 0 && tma_ok && (h->taps_dense || (finite && any && g.k <= 7));
+        if (force == kBanded && !band) return fail(SPCONV_EINVAL, "path=banded: geometry unsupported");
+        if (!(band && (force == kBanded || (force == kAuto && batch >= 3)))) {
+            spb::CscGatherParams cp = csc_params(h, false);
+            cp.X = X;
+            cp.ldx = ldx;
+            cp.Y = Y;
+            cp.ldy = ldy;
+            cp.batch = (int)batch;
+            CK(spb::launch_csc_gather(cp, false, st, device_sm_count()));
+            h->last_kernel.store("csc_gather");
+            return SPCONV_OK;
+        }
+    }
+
     // ---- latency path for one or two vectors ----
-    const bool spmv_ok = h->k2max <= 49;
+    const bool spmv_ok = h->k2max <= 49 && !csc;
     if ((force == kSpmv || force == kSpmvPlain) && !spmv_ok)
         return fail(SPCONV_EINVAL, "SPCONV_B200_PATH=spmv: rows longer than 49 entries");
     if (spmv_ok && (force == kSpmv || force == kSpmvPlain || (force == kAuto && batch <= 2))) {
@@ -303,7 +527,7 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
     }
 
     // ---- band path: CSR band check + register-blocked apply ----
-    const bool band_geom = h->is_conv && h->band_tw > 0 && tma_ok;
+    const bool band_geom = h->is_conv && h->band_tw > 0 && tma_ok && (h->row_ptr || csc);
     if (force == kBanded && !band_geom)
         return fail(SPCONV_EINVAL, "SPCONV_B200_PATH=banded: geometry unsupported");
     // The blocked apply needs finite taps; exact-zero taps (not stored) take
@@ -342,9 +566,12 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
             }
         }
         CK(spb::launch_band((int)g.k, (int)g.s, bp, nullptr, st, &sh, sms));
-        bp.row_ptr = h->row_ptr;
-        bp.col_idx = h->col_idx;
-        bp.vals = h->vals;
+        bp.row_ptr = csc ? h->csc_ptr : h->row_ptr;
+        bp.col_idx = csc ? h->csc_idx : h->col_idx;
+        bp.vals = csc ? h->csc_vals : h->vals;
+        bp.csc = csc ? 1 : 0;
+        bp.tiles_b = h->csc_tiles_b;
+        bp.fail_count = h->fail_flag;
         bp.taps = h->taps;
         bp.seg_ok = h->seg_ok;
         bp.X = X;
@@ -383,7 +610,7 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
         if (bp.fused) {
             const cudaError_t fe = spb::launch_band((int)g.k, (int)g.s, bp, &tmap, st, nullptr, sms);
             if (fe == cudaSuccess) {
-                h->last_kernel.store("conv_spmm_band<fused>+conv_band_fixup");
+                h->last_kernel.store(csc ? "conv_spmm_band<fused,csc>" : "conv_spmm_band<fused>+conv_band_fixup");
                 return SPCONV_OK;
             }
             if (fe != cudaErrorNotSupported) CK(fe);
@@ -392,9 +619,11 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
         }
         CK(spb::launch_band_check((int)g.k, (int)g.s, bp, st, sms));
         CK(spb::launch_band((int)g.k, (int)g.s, bp, &tmap, st, nullptr, sms));
-        h->last_kernel.store("conv_band_check+conv_spmm_band");
+        h->last_kernel.store(csc ? "conv_band_check<csc>+conv_spmm_band" : "conv_band_check+conv_spmm_band");
         return SPCONV_OK;
     }
+
+    if (csc) return fail(SPCONV_ECUDA, "spconv_spmm: internal error (CSC storage reached the row-major kernels)");
 
     // ---- tiled (per-entry) path ----
     if (h->is_conv && force != kGeneric) {
@@ -538,39 +767,6 @@ std::string sparse_header(const spconv_csr* h) {
     std::snprintf(buf, sizeof buf, "%%%%sparse coordinate real\n%lld %lld %lld\n", (long long)h->rows,
                   (long long)h->cols, (long long)h->nnz);
     return buf;
-}
-
-// CSC storage of a conv handle, built on the device from its taps
-// (csc_build.cu) after the CSR arrays on the same stream.
-int attach_csc_conv(spconv_csr* h, cudaStream_t st) {
-    const Geom& g = h->g;
-    const size_t cp_bytes = ((size_t)(h->cols + 1) * 4 + 255) & ~size_t(255);
-    const size_t ix_bytes = ((size_t)std::max<int64_t>(h->nnz, 1) * 4 + 255) & ~size_t(255);
-    char* mem = nullptr;
-    CK(cudaMallocAsync(&mem, cp_bytes + 2 * ix_bytes + 256, st));
-    h->csc_ptr = reinterpret_cast<int32_t*>(mem);
-    h->csc_idx = reinterpret_cast<int32_t*>(mem + cp_bytes);
-    h->csc_vals = reinterpret_cast<float*>(mem + cp_bytes + ix_bytes);
-    h->layout = 1;
-    spb::CscParams cp{};
-    cp.m = (int)g.m;
-    cp.n = (int)g.n;
-    cp.k = (int)g.k;
-    cp.s = (int)g.s;
-    cp.p = (int)g.p;
-    cp.mo = (int)g.mo;
-    cp.no = (int)g.no;
-    cp.cols = (int)h->cols;
-    cp.taps = h->taps;
-    cp.col_ptr = h->csc_ptr;
-    cp.row_idx = h->csc_idx;
-    cp.vals = h->csc_vals;
-    cp.bulk_store = spb::opt(spb::kOptBulkStoreOff) ? 0 : 1;
-    const int64_t per_axis = std::min<int64_t>(g.k, (g.k + g.s - 1) / g.s);
-    bool nonzero = true;
-    for (float v : h->host_taps) nonzero &= v != 0.0f;
-    CK(spb::launch_csc_build(cp, (int)(per_axis * per_axis), nonzero && !h->host_taps.empty(), st));
-    return SPCONV_OK;
 }
 
 // CSC storage given on the host (already validated), uploaded synchronously.
@@ -860,21 +1056,130 @@ static int build_csr_impl(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
     return SPCONV_OK;
 }
 
+static int relayout_host(const spconv_csr* h, int layout, void* stream, spconv_csr** out);
+
+// Kernel sides beyond the CSC kernels' 32 (k > 32): the CSR built on the device,
+// its CSC storage by the host transposition (a generic CSC handle, applied
+// through its row-major arrays).  Replaces *io.
+static int csc_of_wide_kernel(spconv_csr** io, void* stream) {
+    spconv_csr* c = nullptr;
+    const int rc = relayout_host(*io, 1, stream, &c);
+    spconv_csr_free(*io);
+    *io = c;
+    return rc;
+}
+
+// build_transform(kernel, spec, Layout::CSC): the CSC storage only, built in
+// closed form on the device (csc_build.cu); no row-major arrays -- the apply
+// kernels read the CSC storage (csc_apply.cu, conv_band_check<csc>).
+static int build_csc_impl(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p, const float* kernel_kxk, int device,
+                          void* stream, spconv_csr** out) {
+    if (int rc = check_spec(m, n, k, s, p)) return rc;
+    if (!kernel_kxk || !out) return fail(SPCONV_EINVAL, "spconv_build_transform: null argument");
+    *out = nullptr;
+    const Geom g = make_geom(m, n, k, s, p);
+    if (m * n >= (1ll << 31) || g.mo * g.no >= (1ll << 31))
+        return fail(SPCONV_EINVAL, "spconv_build_transform: " + spec_str(m, n, k, s, p) +
+                                       " exceeds the int32 device index range");
+    HostTables ht;
+    make_tables(g, kernel_kxk, ht);
+    if (ht.nnz >= (1ll << 31))
+        return fail(SPCONV_EINVAL, "spconv_build_transform: nnz " + std::to_string(ht.nnz) +
+                                       " exceeds the int32 device index range");
+    DeviceGuard dg(device);
+    if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    keep_pool_memory(device);
+    auto* h = new (std::nothrow) spconv_csr();
+    if (!h) return fail(SPCONV_ECUDA, "out of host memory");
+    h->device = device;
+    h->is_conv = true;
+    h->layout = 1;
+    h->g = g;
+    h->rows = g.mo * g.no;
+    h->cols = m * n;
+    h->nnz = ht.nnz;
+    h->k2max = (int)ht.k2max;
+    h->taps_dense = ht.dense;
+    h->host_taps.assign(kernel_kxk, kernel_kxk + k * k);
+    {
+        int64_t lo, hi;
+        for (int64_t yy = 0; yy < g.no; ++yy) tap_range(yy, g.n, g.k, g.s, g.p, lo, hi), h->sy += hi - lo;
+    }
+    h->fail_flag = flag_alloc();
+    if (!h->fail_flag) {
+        delete h;
+        return fail(SPCONV_ECUDA, "cudaHostAlloc(verdict words) failed");
+    }
+    const size_t cp_bytes = ((size_t)(h->cols + 1) * 4 + 255) & ~size_t(255);
+    const size_t ix_bytes = ((size_t)std::max<int64_t>(ht.nnz, 1) * 4 + 255) & ~size_t(255);
+    const size_t tap_bytes = ((size_t)(k * k) * 4 + 255) & ~size_t(255);
+    size_t seg_bytes = 0;
+    if (spb::band_supported((int)k, (int)s)) {  // CSC segments: one input row x band_tw input columns
+        h->band_tw = spb::band_tile_width((int)k, (int)s);
+        h->csc_tiles_b = (int)((n + h->band_tw - 1) / h->band_tw);
+        seg_bytes = ((size_t)(m * h->csc_tiles_b) + 255) & ~size_t(255);
+    }
+    char* mem = nullptr;
+    cudaError_t e = cudaMallocAsync(&mem, cp_bytes + 2 * ix_bytes + 256 + tap_bytes + seg_bytes, st);
+    if (e != cudaSuccess) {
+        flag_free(h->fail_flag);
+        delete h;
+        return cuda_fail(e, "cudaMallocAsync(CSC)");
+    }
+    h->csc_ptr = reinterpret_cast<int32_t*>(mem);
+    h->csc_idx = reinterpret_cast<int32_t*>(mem + cp_bytes);
+    h->csc_vals = reinterpret_cast<float*>(mem + cp_bytes + ix_bytes);
+    h->taps = reinterpret_cast<float*>(mem + cp_bytes + 2 * ix_bytes + 256);
+    if (seg_bytes) h->seg_ok = reinterpret_cast<uint8_t*>(mem + cp_bytes + 2 * ix_bytes + 256 + tap_bytes);
+    // (pageable source: staged by the driver before the call returns)
+    e = cudaMemcpyAsync(h->taps, kernel_kxk, (size_t)(k * k) * 4, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess && seg_bytes) e = cudaMemsetAsync(h->seg_ok, 1, seg_bytes, st);
+    if (e == cudaSuccess) {
+        spb::CscParams cp{};
+        cp.m = (int)g.m;
+        cp.n = (int)g.n;
+        cp.k = (int)g.k;
+        cp.s = (int)g.s;
+        cp.p = (int)g.p;
+        cp.mo = (int)g.mo;
+        cp.no = (int)g.no;
+        cp.cols = (int)h->cols;
+        cp.taps = h->taps;
+        cp.col_ptr = h->csc_ptr;
+        cp.row_idx = h->csc_idx;
+        cp.vals = h->csc_vals;
+        cp.bulk_store = spb::opt(spb::kOptBulkStoreOff) ? 0 : 1;
+        const int64_t per_axis = std::min<int64_t>(g.k, (g.k + g.s - 1) / g.s);
+        e = spb::launch_csc_build(cp, (int)(per_axis * per_axis), ht.nonzero, st);
+    }
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (e == cudaSuccess) e = cudaStreamIsCapturing(st, &cap);
+    if (e == cudaSuccess && cap == cudaStreamCaptureStatusNone) {
+        e = cudaEventCreateWithFlags(&h->built, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventRecord(h->built, st);
+    }
+    if (e != cudaSuccess) {
+        if (h->built) cudaEventDestroy(h->built);
+        cudaFreeAsync(mem, st);
+        cudaStreamSynchronize(st);
+        flag_free(h->fail_flag);
+        delete h;
+        return cuda_fail(e, "csc_build launch");
+    }
+    *out = h;
+    return SPCONV_OK;
+}
+
 int spconv_build_transform(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
                            const float* kernel_kxk, int layout, int device, void* stream,
                            spconv_csr** out) {
     if (layout != 0 && layout != 1)
         return fail(SPCONV_EINVAL, "spconv_build_transform: layout must be 0 (csr) or 1 (csc)");
+    if (layout == 1 && k <= 32) return build_csc_impl(m, n, k, s, p, kernel_kxk, device, stream, out);
     if (int rc = spconv_build_csr(m, n, k, s, p, kernel_kxk, device, stream, out)) return rc;
     if (layout == 0) return SPCONV_OK;
-    DeviceGuard dg(device);
-    if (int rc = attach_csc_conv(*out, static_cast<cudaStream_t>(stream))) {
-        const std::string msg = g_err;
-        spconv_csr_free(*out);
-        *out = nullptr;
-        return fail(rc, msg);
-    }
-    return SPCONV_OK;
+    return csc_of_wide_kernel(out, stream);
 }
 
 int spconv_build_transform_f64(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
@@ -906,10 +1211,19 @@ int spconv_build_transform_f64(int64_t m, int64_t n, int64_t k, int64_t s, int64
     F64Fill fill{t32.data(), kernel_kxk, false};
     spconv_csr* h = nullptr;
     // (argument and int32-range checks first, inside: no device work before them)
-    if (int rc = build_csr_impl(m, n, k, s, p, tag.data(), device, stream, &h, &fill)) return rc;
+    if (layout == 1 && k > 32) {  // (see csc_of_wide_kernel)
+        if (int rc = spconv_build_transform_f64(m, n, k, s, p, kernel_kxk, 0, device, stream, &h)) return rc;
+        if (int rc = csc_of_wide_kernel(&h, stream)) return rc;
+        *out = h;
+        return SPCONV_OK;
+    }
+    if (layout == 1) {  // CSC storage only, from the tags
+        if (int rc = build_csc_impl(m, n, k, s, p, tag.data(), device, stream, &h)) return rc;
+    } else {
+        if (int rc = build_csr_impl(m, n, k, s, p, tag.data(), device, stream, &h, &fill)) return rc;
+    }
     DeviceGuard dg(device);
     int rc = SPCONV_OK;
-    if (layout == 1) rc = attach_csc_conv(h, st);  // (from the tags in h->taps)
     // device tables of the values for the retag passes (none needed when the
     // fill wrote them and there is no CSC storage)
     const bool need_tables = !fill.done || h->layout == 1;
@@ -923,10 +1237,14 @@ int spconv_build_transform_f64(int64_t m, int64_t n, int64_t k, int64_t s, int64
     if (!rc && e == cudaSuccess && need_tables)
         e = cudaMemcpyAsync(tt + t32_bytes, kernel_kxk, (size_t)kk * 8, cudaMemcpyHostToDevice, st);
     const size_t vb = (size_t)std::max<int64_t>(h->nnz, 1) * 8;
-    if (rc == SPCONV_OK && e == cudaSuccess && !fill.done) e = spb::launch_retag(h->vals, h->vals64, h->nnz, d32, d64, st);
+    if (rc == SPCONV_OK && e == cudaSuccess && h->layout == 0 && !fill.done)
+        e = spb::launch_retag(h->vals, h->vals64, h->nnz, d32, d64, st);
     if (rc == SPCONV_OK && e == cudaSuccess && h->layout == 1) {
         e = cudaMallocAsync(&h->csc_vals64, vb, st);
         if (e == cudaSuccess) e = spb::launch_retag(h->csc_vals, h->csc_vals64, h->nnz, d32, d64, st);
+        // the exact taps on the device (the CSC kernels' fp64 checks and sums)
+        if (e == cudaSuccess) e = cudaMallocAsync(&h->taps64, (size_t)kk * 8, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(h->taps64, d64, (size_t)kk * 8, cudaMemcpyDeviceToDevice, st);
     }
     // the device taps (band check, CSC rebuilds) become the real fp32 taps
     if (rc == SPCONV_OK && e == cudaSuccess)
@@ -1011,6 +1329,8 @@ static int export_row_major(const spconv_csr* h, int64_t* rp, int64_t* ri, doubl
     return spconv_csr_export(&tmp, rp, ri, rv);
 }
 
+static int relayout_host(const spconv_csr* h, int layout, void* stream, spconv_csr** out);
+
 int spconv_relayout(const spconv_csr* h, int layout, void* stream, spconv_csr** out) {
     if (!h || !out) return fail(SPCONV_EINVAL, "spconv_relayout: null argument");
     if (layout != 0 && layout != 1) return fail(SPCONV_EINVAL, "spconv_relayout: layout must be 0 (csr) or 1 (csc)");
@@ -1025,7 +1345,11 @@ int spconv_relayout(const spconv_csr* h, int layout, void* stream, spconv_csr** 
         return spconv_build_transform(g.m, g.n, g.k, g.s, g.p, h->host_taps.data(), layout, h->device,
                                       stream, out);
     }
-    // Matrices that came from the host: transposition of the host copy.
+    return relayout_host(h, layout, stream, out);
+}
+
+// Matrices that came from the host: transposition of the host copy.
+static int relayout_host(const spconv_csr* h, int layout, void* stream, spconv_csr** out) {
     std::vector<int64_t> rp((size_t)h->rows + 1), ri((size_t)std::max<int64_t>(h->nnz, 1));
     std::vector<double> rv((size_t)std::max<int64_t>(h->nnz, 1));
     if (int rc = export_row_major(h, rp.data(), ri.data(), rv.data())) return rc;
@@ -1238,6 +1562,25 @@ int spconv_spgemm(const spconv_csr* a, const spconv_csr* b, int layout, void* st
     if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     CK(cudaDeviceSynchronize());  // the operands' builds are complete
+    // Gustavson runs over rows: a conv transform held only in CSC gets a
+    // row-major twin for the duration of the call (rebuilt from its taps).
+    spconv_csr *ta = nullptr, *tb = nullptr;
+    if (csc_native(a)) {
+        if (int rc = spconv_relayout(a, 0, stream, &ta)) return rc;
+        a = ta;
+    }
+    if (csc_native(b)) {
+        if (int rc = spconv_relayout(b, 0, stream, &tb)) {
+            spconv_csr_free(ta);
+            return rc;
+        }
+        b = tb;
+    }
+    struct Twins {
+        spconv_csr *a, *b;
+        ~Twins() { spconv_csr_free(a), spconv_csr_free(b); }
+    } twins{ta, tb};
+    CK(cudaStreamSynchronize(st));
     spb::SpgemmIn A{a->rows, a->cols, a->nnz, a->row_ptr, a->col_idx, a->vals, a->vals64};
     spb::SpgemmIn B{b->rows, b->cols, b->nnz, b->row_ptr, b->col_idx, b->vals, b->vals64};
     spb::SpgemmOut o{};
@@ -1350,9 +1693,24 @@ int spconv_csr_spec(const spconv_csr* h, int64_t spec5[5]) {
 int spconv_csr_device_ptrs(const spconv_csr* h, const int32_t** row_ptr, const int32_t** col_idx,
                            const float** vals) {
     if (!h) return fail(SPCONV_EINVAL, "null handle");
+    // Writable storage leaves the library's control: a CSC conv handle is
+    // checked before every later apply, which then follows the storage as it
+    // stands (row-major handles re-check every call anyway: the band check).
+    if (h->layout == 1) const_cast<spconv_csr*>(h)->exposed.store(true);
     if (row_ptr) *row_ptr = h->layout ? h->csc_ptr : h->row_ptr;
     if (col_idx) *col_idx = h->layout ? h->csc_idx : h->col_idx;
     if (vals) *vals = h->layout ? h->csc_vals : h->vals;
+    return SPCONV_OK;
+}
+
+int spconv_csr_storage_bytes(const spconv_csr* h, int64_t* bytes) {
+    if (!h || !bytes) return fail(SPCONV_EINVAL, "spconv_csr_storage_bytes: null argument");
+    int64_t b = 0;
+    if (h->row_ptr) b += 4 * (h->rows + 1) + 8 * h->nnz;
+    if (h->vals64) b += 8 * h->nnz;
+    if (h->csc_ptr) b += 4 * (h->cols + 1) + 8 * h->nnz;
+    if (h->csc_vals64) b += 8 * h->nnz;
+    *bytes = b;
     return SPCONV_OK;
 }
 
@@ -1498,6 +1856,11 @@ int spconv_convolve_host(const spconv_csr* hc, const float* X_host, float* Y_hos
 
 int spconv_spmm_f64(const spconv_csr* h, const double* X_dev, int64_t ldx, double* Y_dev, int64_t ldy,
                     int64_t batch, void* stream) {
+    return spconv_spmm_f64_threads(h, X_dev, ldx, Y_dev, ldy, batch, 1, stream);
+}
+
+int spconv_spmm_f64_threads(const spconv_csr* h, const double* X_dev, int64_t ldx, double* Y_dev, int64_t ldy,
+                            int64_t batch, int threads, void* stream) {
     if (!h) return fail(SPCONV_EINVAL, "spconv_spmm_f64: null handle");
     if (batch < 0) return fail(SPCONV_EINVAL, "spconv_spmm_f64: negative batch");
     if (batch == 0) return SPCONV_OK;
@@ -1511,14 +1874,52 @@ int spconv_spmm_f64(const spconv_csr* h, const double* X_dev, int64_t ldx, doubl
         return fail(SPCONV_EINVAL, "spconv_spmm_f64: X and Y overlap");
     DeviceGuard dg(h->device);
     if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
+    // The reference cuts the major dimension into min(threads, major) chunks
+    // of ceil(major / nt); only CSC sums depend on it (inc/sparse.hpp:221-258).
+    int64_t chunk = 0;
+    if (h->layout == 1 && threads > 1) {
+        const int64_t nt = std::min<int64_t>(threads, std::max<int64_t>(h->cols, 1));
+        if (nt > 1) chunk = (h->cols + nt - 1) / nt;
+    }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    auto* hm = const_cast<spconv_csr*>(h);
+    if (csc_native(h)) {
+        if (int rc = csc_sticky(h, "spconv_spmm_f64")) return rc;
+        if (h->exposed.load()) {
+            bool clean = false;
+            if (int rc = csc_exposed_clean(hm, st, true, &clean)) return rc;
+            if (!clean) {
+                hm->last_kernel.store("csc_gather<verify>+csc_repair");
+                return csc_repair_apply(hm, X_dev, ldx, Y_dev, ldy, batch, st, true, chunk);
+            }
+        }
+        spb::CscGatherParams cp = csc_params(h, true);
+        cp.X = X_dev;
+        cp.ldx = ldx;
+        cp.Y = Y_dev;
+        cp.ldy = ldy;
+        cp.batch = (int)batch;
+        cp.chunk = chunk;
+        CK(spb::launch_csc_gather(cp, true, st, device_sm_count()));
+        hm->last_kernel.store("csc_gather<f64>");
+        return SPCONV_OK;
+    }
     spb::F64Params fp{h->row_ptr, h->col_idx, h->vals, h->vals64, X_dev, ldx, Y_dev, ldy, (int)h->rows, (int)batch};
-    CK(spb::launch_spmm_f64(fp, static_cast<cudaStream_t>(stream)));
-    const_cast<spconv_csr*>(h)->last_kernel.store("csr_spmm_f64");
+    // (a CSC matrix from the host applies through its row-major arrays: the
+    // row-major order of entries is the column order within each row)
+    fp.chunk = chunk;
+    CK(spb::launch_spmm_f64(fp, st));
+    hm->last_kernel.store("csr_spmm_f64");
     return SPCONV_OK;
 }
 
 int spconv_convolve_host_f64(const spconv_csr* hc, const double* X_host, double* Y_host,
                              int64_t batch) {
+    return spconv_convolve_host_f64_threads(hc, X_host, Y_host, batch, 1);
+}
+
+int spconv_convolve_host_f64_threads(const spconv_csr* hc, const double* X_host, double* Y_host,
+                                     int64_t batch, int threads) {
     if (!hc) return fail(SPCONV_EINVAL, "spconv_convolve_host_f64: null handle");
     if (batch < 0) return fail(SPCONV_EINVAL, "spconv_convolve_host_f64: negative batch");
     if (batch == 0) return SPCONV_OK;
@@ -1539,8 +1940,8 @@ int spconv_convolve_host_f64(const spconv_csr* hc, const double* X_host, double*
     cudaError_t e = cudaMemcpyAsync(buf, X_host, xb, cudaMemcpyHostToDevice, st);
     int rc = SPCONV_OK;
     if (e == cudaSuccess)
-        rc = spconv_spmm_f64(h, reinterpret_cast<const double*>(buf), h->cols, reinterpret_cast<double*>(buf + xb),
-                             h->rows, batch, st);
+        rc = spconv_spmm_f64_threads(h, reinterpret_cast<const double*>(buf), h->cols,
+                                     reinterpret_cast<double*>(buf + xb), h->rows, batch, threads, st);
     if (e == cudaSuccess && rc == SPCONV_OK) e = cudaMemcpyAsync(Y_host, buf + xb, yb, cudaMemcpyDeviceToHost, st);
     cudaFreeAsync(buf, st);
     const cudaError_t es = cudaStreamSynchronize(st);
@@ -1659,14 +2060,20 @@ int spconv_transform_read(const char* text, int64_t len, int device, void* strea
         if (spconv_build_transform_f64(m, n, k, s, p, taps.data(), csc ? 1 : 0, device, stream, &built) ==
             SPCONV_OK) {
             bool same = built->nnz == nnz;
-            if (same) {  // the row-major arrays (exact values) must equal the file's
-                std::vector<int64_t> brp((size_t)rows + 1), bci((size_t)std::max<int64_t>(nnz, 1));
+            if (same) {  // the storage (exact values) must equal the file's, in the file's layout
+                const int64_t major = csc ? cols : rows;
+                std::vector<int64_t> brp((size_t)major + 1), bci((size_t)std::max<int64_t>(nnz, 1));
                 std::vector<double> bv((size_t)std::max<int64_t>(nnz, 1));
-                same = export_row_major(built, brp.data(), bci.data(), bv.data()) == SPCONV_OK;
-                for (int64_t r = 0; same && r <= rows; ++r) same = brp[(size_t)r] == ptr[(size_t)r];
+                same = spconv_csr_export(built, brp.data(), bci.data(), bv.data()) == SPCONV_OK;
+                std::vector<int32_t> fcp, fci;
+                std::vector<double> fcv;
+                if (same && csc) transpose_host(rows, cols, ptr.data(), idx.data(), val.data(), fcp, fci, fcv);
+                for (int64_t r = 0; same && r <= major; ++r)
+                    same = brp[(size_t)r] == (csc ? (int64_t)fcp[(size_t)r] : ptr[(size_t)r]);
                 for (int64_t e = 0; same && e < nnz; ++e)
-                    same = bci[(size_t)e] == idx[(size_t)e] &&
-                           __builtin_bit_cast(uint64_t, bv[(size_t)e]) == __builtin_bit_cast(uint64_t, val[(size_t)e]);
+                    same = bci[(size_t)e] == (csc ? (int64_t)fci[(size_t)e] : idx[(size_t)e]) &&
+                           __builtin_bit_cast(uint64_t, bv[(size_t)e]) ==
+                               __builtin_bit_cast(uint64_t, csc ? fcv[(size_t)e] : val[(size_t)e]);
             }
             if (same) {
                 *out = built;
@@ -1706,7 +2113,9 @@ int spconv_band_check_status(const spconv_csr* h, int64_t* segments, int64_t* fa
     if (!h->seg_ok || h->band_tw <= 0) return fail(SPCONV_EINVAL, "spconv_band_check_status: no band geometry");
     DeviceGuard dg(h->device);
     if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
-    const int64_t n = h->g.mo * ((h->g.no + h->band_tw - 1) / h->band_tw);
+    // CSR: one segment per output row x band_tw output columns; CSC storage:
+    // one per input row x band_tw input columns
+    const int64_t n = csc_native(h) ? h->g.m * h->csc_tiles_b : h->g.mo * ((h->g.no + h->band_tw - 1) / h->band_tw);
     std::vector<uint8_t> v((size_t)n);
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpy(v.data(), h->seg_ok, (size_t)n, cudaMemcpyDeviceToHost));
@@ -1728,7 +2137,9 @@ int spconv_csr_free(spconv_csr* h) {
         if (h->csc_ptr) cudaFree(h->csc_ptr);
         if (h->vals64) cudaFree(h->vals64);
         if (h->csc_vals64) cudaFree(h->csc_vals64);
+        if (h->taps64) cudaFree(h->taps64);
     }
+    flag_free(h->fail_flag);
     delete h;
     return SPCONV_OK;
 }

@@ -1,0 +1,217 @@
+// csc_apply.cu -- SpMV / SpMM of a conv transform held in CSC storage, reading
+// the CSC storage itself (no row-major copy).
+//
+// Replaces detail::spmv_csc_cols and spmv's CSC branch (inc/sparse.hpp:194-205,
+// 214-258).  The reference scatters column by column:
+//     y = 0; for j (column, ascending): for k in ptr[j]..ptr[j+1]: y[idx[k]] += val[k] * x[j]
+// so every output sees its entries in ascending column order -- the CSR row
+// loop's order.  With nt > 1 reference threads the columns are cut into
+// contiguous chunks of ceil(cols / nt); each thread scatters its chunk into a
+// partial vector starting from 0.0 and the partials are added to y in thread
+// order (inc/sparse.hpp:243-258).
+//
+// csc_gather<T, KC> -- one thread per output row r = (x, y), any k, s, p, dense
+// or zero-tap kernels (the batches of the band geometries go through
+// conv_band_check<csc> + conv_spmm_band instead, spmm_band.cu).  The entries of
+// row r sit at closed-form places in the CSC storage: tap (j, i) of r lives in
+// column (a, b) = (s x + j - p, s y + i - p) at rank
+//     #{stored (j', i') of that column with j' > j, or j' == j and i' > i}
+// (rows ascend there as j, i descend), i.e. pos = col_ptr[col] + rank.  So the
+// thread reads col_ptr[col], then row_idx[pos] and vals[pos] -- every entry of
+// the storage is read exactly once per call -- and checks them against (r, the
+// tap); the same threads also sweep col_ptr against its closed form
+// (csc_build.cu).  Storage equal to the transform of the handle's taps passes
+// every comparison; anything else sets the handle's failure flag.  The sums
+// themselves run over the stored taps in (j, i) = column-ascending order with
+// x gathered per image:
+//     fp32: acc = fmaf(w, x, acc)                          (the device contract)
+//     fp64: part = part + w * x, two roundings; y = y + part at every chunk
+//           boundary -- the reference's fp64 arithmetic and thread order.
+#include <algorithm>
+
+#include "internal.h"
+
+namespace spb {
+
+namespace {
+
+// #{x in [0, mo) : 0 <= s x + j - p < a}
+__device__ __forceinline__ int slides_below_g(int j, int a, int mo, int s, int p) {
+    if (a <= 0) return 0;
+    const int lo = p - j <= 0 ? 0 : (p - j + s - 1) / s;
+    const int b = a - 1 + p - j;
+    if (b < 0) return 0;
+    const int hi = min(mo - 1, b / s);
+    return max(0, hi - lo + 1);
+}
+
+__device__ __forceinline__ void tap_range_g(int x, int dim, int k, int s, int p, int& lo, int& hi) {
+    lo = max(0, p - s * x);
+    hi = min(k, dim + p - s * x);
+    lo = min(lo, k);
+    if (hi < lo) hi = lo;
+}
+
+template <typename T>
+struct Arith;
+template <>
+struct Arith<float> {
+    __device__ static float load(const void* X, long long i) { return __ldg(reinterpret_cast<const float*>(X) + i); }
+    __device__ static float step(float acc, float w, float x) { return fmaf(w, x, acc); }
+};
+template <>
+struct Arith<double> {
+    __device__ static double load(const void* X, long long i) {
+        return __ldg(reinterpret_cast<const double*>(X) + i);
+    }
+    __device__ static double step(double acc, double w, double x) { return __dadd_rn(acc, __dmul_rn(w, x)); }
+};
+
+constexpr int kBT = 4;  // images per pass over a row's taps
+
+}  // namespace
+
+// KC: compile-time kernel side (0: runtime P.k <= 32).
+template <typename T, int KC>
+__global__ void __launch_bounds__(256) csc_gather(const CscGatherParams P) {
+    constexpr bool F64 = sizeof(T) == 8;
+    __shared__ T s_w[1024];
+    __shared__ uint32_t s_w32[1024];
+    const int k = KC ? KC : P.k, kk = k * k, S = P.s;
+    for (int q = threadIdx.x; q < kk; q += blockDim.x) {
+        const float t32 = __ldg(P.taps32 + q);
+        s_w32[q] = __float_as_uint(t32);
+        if (F64)
+            s_w[q] = (T)(P.taps64 ? __ldg(P.taps64 + q) : (double)t32);
+        else
+            s_w[q] = (T)t32;
+    }
+    __syncthreads();
+    const long long gtid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long nthr = (long long)gridDim.x * blockDim.x;
+    bool bad = false;
+
+    // ---- col_ptr against its closed form (csc_build.cu) ----
+    if (!P.skip_sweep) {
+        for (long long c = gtid; c <= P.cols; c += nthr) {
+            long long want = P.nnz;
+            if (c < P.cols) {
+                const int a = (int)(c / P.n), b = (int)(c - (long long)a * P.n);
+                want = 0;
+                uint32_t nzj[KC ? KC : 32];
+#pragma unroll
+                for (int i = 0; i < (KC ? KC : 32); ++i) nzj[i] = 0;
+                for (int j = 0; j < k; ++j) {
+                    want += P.zw[j] * slides_below_g(j, a, P.mo, S, P.p);
+                    const int d = a + P.p - j;
+                    if (d >= 0 && d % S == 0 && d / S < P.mo)
+                        for (int i = 0; i < k; ++i) nzj[i] += (P.nzrow[j] >> i) & 1u;
+                }
+                for (int i = 0; i < k; ++i) want += (long long)nzj[i] * slides_below_g(i, b, P.no, S, P.p);
+            }
+            bad |= (long long)__ldg(P.col_ptr + c) != want;
+        }
+    }
+
+    // ---- rows ----
+    for (long long r = gtid; r < P.rows; r += nthr) {
+        const int x = (int)(r / P.no), y = (int)(r - (long long)x * P.no);
+        int jlo, jhi, ilo, ihi;
+        tap_range_g(x, P.m, k, S, P.p, jlo, jhi);
+        tap_range_g(y, P.n, k, S, P.p, ilo, ihi);
+        const long long rb = (long long)(S * x - P.p) * P.n + (S * y - P.p);  // column of tap (0, 0)
+        // verification: every stored tap of r at its closed-form place
+        for (int j = jlo; j < jhi; ++j) {
+            const int idxJ = min((k - 1 - j) / S, x);
+            const uint32_t nzr = P.nzrow[j];
+            for (int i = ilo; i < ihi; ++i) {
+                if (!((nzr >> i) & 1u)) continue;
+                const long long col = rb + (long long)j * P.n + i;
+                const int idxI = min((k - 1 - i) / S, y);
+                int rank;
+                if (!P.zt) {
+                    const int nI = idxI + 1 + min(i / S, P.no - 1 - y);
+                    rank = idxJ * nI + idxI;
+                } else {
+                    // I(b): taps i' = i + d s with y - d in [0, no)
+                    uint32_t mi = 0;
+                    for (int d = -min(i / S, P.no - 1 - y); d <= idxI; ++d) mi |= 1u << (i + d * S);
+                    rank = __popc(nzr & mi & ~((2u << i) - 1u));
+                    for (int d = 1; d <= idxJ; ++d) rank += __popc(P.nzrow[j + d * S] & mi);
+                }
+                const long long pos = (long long)__ldg(P.col_ptr + col) + rank;
+                if (pos < 0 || pos >= P.nnz) {
+                    bad = true;
+                    continue;
+                }
+                bad |= __ldg(P.row_idx + pos) != (int)r;
+                if (F64 && P.vals64)
+                    bad |= __double_as_longlong(__ldg(P.vals64 + pos)) !=
+                           __double_as_longlong((double)s_w[j * k + i]);
+                else
+                    bad |= __float_as_uint(__ldg(P.vals + pos)) != s_w32[j * k + i];
+            }
+        }
+        if (P.verify_only) continue;
+        // sums: stored taps in column-ascending order
+        for (int b0 = 0; b0 < P.batch; b0 += kBT) {
+            T acc[kBT], part[kBT];
+#pragma unroll
+            for (int u = 0; u < kBT; ++u) acc[u] = part[u] = (T)0;
+            long long cur = -1;
+            for (int j = jlo; j < jhi; ++j) {
+                const uint32_t nzr = P.nzrow[j];
+                for (int i = ilo; i < ihi; ++i) {
+                    if (!((nzr >> i) & 1u)) continue;
+                    const long long col = rb + (long long)j * P.n + i;
+                    const T w = s_w[j * k + i];
+                    if (F64 && P.chunk > 0) {
+                        const long long cid = col / P.chunk;
+                        if (cid != cur) {
+#pragma unroll
+                            for (int u = 0; u < kBT; ++u) {
+                                acc[u] = Arith<T>::step(acc[u], (T)1, part[u]);  // y + part (1 * part is exact)
+                                part[u] = (T)0;
+                            }
+                            cur = cid;
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < kBT; ++u)
+                        if (b0 + u < P.batch)
+                            part[u] = Arith<T>::step(part[u], w, Arith<T>::load(P.X, (long long)(b0 + u) * P.ldx + col));
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kBT; ++u) {
+                if (b0 + u >= P.batch) break;
+                const T v = (F64 && P.chunk > 0) ? Arith<T>::step(acc[u], (T)1, part[u]) : part[u];
+                reinterpret_cast<T*>(P.Y)[(long long)(b0 + u) * P.ldy + r] = v;
+            }
+        }
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) *P.fail = 1;
+}
+
+cudaError_t launch_csc_gather(const CscGatherParams& cp, bool f64, cudaStream_t st, int sms) {
+    if (cp.k > 32) return cudaErrorInvalidValue;
+    const long long work = std::max<long long>(cp.rows, cp.cols + 1);
+    const long long grid = std::max<long long>(1, std::min<long long>((work + 255) / 256, (long long)sms * 8));
+    auto pick = [&](auto kern3, auto kern5, auto kern7, auto kern0) {
+        switch (cp.k) {
+            case 3: return kern3;
+            case 5: return kern5;
+            case 7: return kern7;
+            default: return kern0;
+        }
+    };
+    if (f64)
+        pick(csc_gather<double, 3>, csc_gather<double, 5>, csc_gather<double, 7>, csc_gather<double, 0>)
+            <<<(unsigned)grid, 256, 0, st>>>(cp);
+    else
+        pick(csc_gather<float, 3>, csc_gather<float, 5>, csc_gather<float, 7>, csc_gather<float, 0>)
+            <<<(unsigned)grid, 256, 0, st>>>(cp);
+    return cudaGetLastError();
+}
+
+}  // namespace spb

@@ -124,7 +124,39 @@ struct BandParams {
     int zt;            // some taps are exact zeros (not stored): masked footprint + checks
     unsigned long long nzmask;  // bit j*k+i: tap (j, i) is non-zero (zt; k <= 7)
     long long zw[8];            // zt: W[j] = sum_i nz[j][i] * #{y : tap i lands} (per handle)
+    // CSC storage (csc = 1): row_ptr / col_idx / vals above hold col_ptr /
+    // row_idx / vals of the column-major storage, the check verifies it
+    // segment by segment (one input image row x TW input columns, tiles_b
+    // segments per input row) and the apply never reads it per entry.
+    int csc;
+    int tiles_b;
+    int* fail_count;  // csc: set to 1 when a segment fails (the handle's sticky verdict)
 };
+
+// CSC-storage SpMV / SpMM of a conv transform (csc_apply.cu).
+struct CscGatherParams {
+    const int32_t* col_ptr;
+    const int32_t* row_idx;
+    const float* vals;
+    const double* vals64;  // exact values when the handle keeps them (fp64 mode compares / applies them)
+    const float* taps32;   // device k*k fp32 taps (what vals must equal)
+    const double* taps64;  // device k*k exact taps (NULL: taps32 widened)
+    const void* X;         // float or double, image-major
+    int64_t ldx;
+    void* Y;
+    int64_t ldy;
+    int batch;
+    int m, n, k, s, p, mo, no;
+    long long rows, cols, nnz;
+    int zt;                   // some taps are exact zeros (not stored)
+    uint32_t nzrow[32];       // bit i of nzrow[j]: tap (j, i) is stored (all ones for dense taps); k <= 32
+    long long zw[32];         // W[j] = sum_i nz[j][i] * #{y : tap i lands}
+    long long chunk;          // fp64: columns per reference thread (0: one thread)
+    int verify_only;          // 1: check the storage, no sums
+    int skip_sweep;           // 1: col_ptr already checked by the caller
+    int* fail;                // set to 1 when the storage is not the transform of the taps
+};
+cudaError_t launch_csc_gather(const CscGatherParams& cp, bool f64, cudaStream_t st, int sms);
 
 struct BandShape {
     int th, tw, wr, wc, smem, threads, occ;
@@ -209,6 +241,7 @@ struct F64Params {
     double* Y;
     int64_t ldy;
     int rows, batch;
+    long long chunk = 0;  // columns per reference thread (CSC thread-order combine; 0: one thread)
 };
 cudaError_t launch_spmm_f64(const F64Params& fp, cudaStream_t st);
 // Tag -> value pass of the exact-fp64 build: vals[e] holds (float)(q + 1) for
@@ -264,6 +297,10 @@ struct spconv_csr {
     // Storage layout (inc/sparse.hpp:24).  A CSC handle keeps its column-major
     // storage (what export / text / device_ptrs show) next to the row-major
     // arrays above, which every SpMV / SpMM kernel reads.
+    // A conv transform built in CSC (build_transform(layout = 1), relayout)
+    // keeps ONLY the column-major storage: row_ptr / col_idx / vals are NULL
+    // and every apply reads the CSC arrays (csc_apply.cu, conv_band_check<csc>).
+    // Matrices that arrive from the host in CSC keep both.
     int layout = 0;                // 0 = CSR, 1 = CSC
     int32_t* csc_ptr = nullptr;    // device col_ptr[cols+1] (layout 1)
     int32_t* csc_idx = nullptr;    // device row_idx[nnz]
@@ -275,6 +312,10 @@ struct spconv_csr {
     std::vector<double> host_taps64;  // conv handles built from such double taps
     double* vals64 = nullptr;         // device [nnz], row-major order
     double* csc_vals64 = nullptr;     // device [nnz], CSC storage order (layout 1)
+    double* taps64 = nullptr;         // device k*k exact taps (CSC conv handles built from double taps)
+    int csc_tiles_b = 0;           // CSC band check: segments per input row (band geometries)
+    int* fail_flag = nullptr;      // CSC conv: mapped host word, set by a device check that failed (sticky)
+    std::atomic<bool> exposed{false};  // spconv_csr_device_ptrs handed out the CSC arrays: verify before use
     cudaEvent_t built = nullptr;  // recorded after the build on the build stream (host-buffer calls wait on it)
     std::atomic<bool> applied{false};  // an apply was enqueued after the build (PDL is safe from then on)
     std::atomic<const char*> last_kernel{nullptr};  // diagnostics: last SpMM kernel launched

@@ -146,6 +146,8 @@ __global__ void __launch_bounds__(256) conv_spmm_tiled(const __grid_constant__ C
     }
 }
 
+// (chunk > 0: columns cut into chunks of `chunk`, one partial per chunk added
+// to y in chunk order -- the reference's CSC thread combine with nt threads.)
 // fp64 SpMM with the reference's own arithmetic: per row acc = 0.0; for each
 // stored entry in order acc = acc + (double)val * x (one rounded multiply, one
 // rounded add -- no contraction, as the reference's Release build evaluates
@@ -157,12 +159,19 @@ __global__ void __launch_bounds__(256) csr_spmm_f64(const F64Params P) {
     const int e0 = __ldg(P.row_ptr + r), e1 = __ldg(P.row_ptr + r + 1);
     for (int b = blockIdx.y; b < P.batch; b += gridDim.y) {
         const double* x = P.X + (int64_t)b * P.ldx;
-        double acc = 0.0;
+        double acc = 0.0, y = 0.0;
+        long long cur = -1;
         for (int e = e0; e < e1; ++e) {
             const double v = P.vals64 ? __ldg(P.vals64 + e) : (double)__ldg(P.vals + e);
-            acc = __dadd_rn(acc, __dmul_rn(v, __ldg(x + __ldg(P.col_idx + e))));
+            const int c = __ldg(P.col_idx + e);
+            if (P.chunk > 0 && c / P.chunk != cur) {  // the reference's per-thread partials (inc/sparse.hpp:243-258)
+                y = __dadd_rn(y, acc);
+                acc = 0.0;
+                cur = c / P.chunk;
+            }
+            acc = __dadd_rn(acc, __dmul_rn(v, __ldg(x + c)));
         }
-        P.Y[(int64_t)b * P.ldy + r] = acc;
+        P.Y[(int64_t)b * P.ldy + r] = P.chunk > 0 ? __dadd_rn(y, acc) : acc;
     }
 }
 

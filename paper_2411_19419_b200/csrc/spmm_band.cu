@@ -316,7 +316,162 @@ __device__ __forceinline__ bool seg_verify(const BandParams& P, const SegGeom& g
     return __all_sync(0xffffffffu, ok);
 }
 
+// ---------------------------------------------------------------------------
+// 1b. The same check over CSC storage (inc/sparse.hpp:24-32: col_ptr, row_idx,
+//     vals; csc_build.cu writes it).  Column c = (a, b) is input pixel (a, b);
+//     it holds the outputs (x, y) with s x + j - p = a, s y + i - p = b for a
+//     stored tap (j, i), rows ascending = j descending, then i descending.
+//     A CSC segment is one input row a x TW consecutive input columns; its
+//     entries are one contiguous run:
+//        S0 = sum_j W[j] * #{x : 0 <= s x + j - p < a} + sum_i nzJ(i) * #{y : 0 <= s y + i - p < b0}
+//        L  = sum_i nzJ(i) * #{y : b0 <= s y + i - p < b0 + nb}
+//     with W[j] = sum_i nz[j][i] * #{y : tap i lands} (= sy for dense taps)
+//     and nzJ(i) = #{stored (j, i) : j in J(a)} -- the closed form of
+//     csc_build.cu's col_ptr.  The same three bulk copies stage col_ptr and
+//     the run, and every column is compared with the taps landing on it.
+// ---------------------------------------------------------------------------
+
+// #{x in [0, mo) : 0 <= s x + j - p < a}: slides of tap row j that read an input row above a.
+__device__ __forceinline__ int slides_below(int j, int a, int mo, int s, int p) {
+    if (a <= 0) return 0;
+    const int lo = p - j <= 0 ? 0 : (p - j + s - 1) / s;  // s x >= p - j
+    const int b = a - 1 + p - j;                            // s x <= a - 1 + p - j
+    if (b < 0) return 0;
+    const int hi = min(mo - 1, b / s);
+    return max(0, hi - lo + 1);
+}
+
+// Bit j: tap row j lands on input row a for some output row x in [0, mo).
+template <int K, int S>
+__device__ __forceinline__ uint32_t tap_set_mask(int a, int mo, int p) {
+    uint32_t mk = 0;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        const int d = a + p - j;
+        if (d >= 0 && d % S == 0 && d / S < mo) mk |= 1u << j;
+    }
+    return mk;
+}
+
+// Stored taps of row j as K bits (bit i).
+template <int K, bool ZT>
+__device__ __forceinline__ uint32_t nz_row(unsigned long long nzmask, int j) {
+    return ZT ? (uint32_t)((nzmask >> (j * K)) & ((1ull << K) - 1ull)) : ((1u << K) - 1u);
+}
+
 template <int K, int S, int TW, bool ZT>
+__device__ __forceinline__ SegGeom seg_geom_csc(const BandParams& P, long long seg) {
+    SegGeom g;
+    g.x = (int)(seg / P.tiles_b);                                 // input row a
+    g.y0 = (int)(seg - (long long)g.x * P.tiles_b) * TW;          // first input column b0
+    g.nr = min(TW, P.n - g.y0);
+    g.r0 = g.x * P.n + g.y0;                                      // first column index
+    const uint32_t jm = tap_set_mask<K, S>(g.x, P.mo, P.p);
+    g.jlo = (int)jm;  // (the J(a) mask)
+    g.jhi = 0;
+    long long s0 = 0;
+    int len = 0;
+#pragma unroll
+    for (int j = 0; j < K; ++j) s0 += (ZT ? P.zw[j] : (long long)P.sy) * slides_below(j, g.x, P.mo, S, P.p);
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+        int nzj = 0;
+#pragma unroll
+        for (int j = 0; j < K; ++j) nzj += ((jm >> j) & 1u) && ((nz_row<K, ZT>(P.nzmask, j) >> i) & 1u) ? 1 : 0;
+        const int b0 = slides_below(i, g.y0, P.no, S, P.p);
+        s0 += (long long)nzj * b0;
+        len += nzj * (slides_below(i, g.y0 + g.nr, P.no, S, P.p) - b0);
+    }
+    g.cy0 = 0;
+    g.S0 = s0;
+    g.L = len;
+    g.valid = g.S0 + g.L <= (long long)P.nnz;
+    return g;
+}
+
+// Whole warp, CSC segment landed at `rp` (col_ptr words, then row_idx, vals):
+// per-column offsets by a warp scan of the column counts, col_ptr compared,
+// then each column's rows and values compared with the taps that land on it
+// (interior stride-1 columns of dense taps fully unrolled).
+template <int K, int S, int TW, bool ZT>
+__device__ __forceinline__ bool seg_verify_csc(const BandParams& P, const SegGeom& g, const int* rp,
+                                               const uint32_t (&w)[K * K], const uint32_t* s_w, int lane) {
+    using C = CheckCfg<K, S, TW>;
+    constexpr int RPL = TW / 32;  // columns per lane
+    const int* cb = rp + C::RPW;
+    const uint32_t* vb = reinterpret_cast<const uint32_t*>(cb + C::BUFW);
+    const uint32_t jm = (uint32_t)g.jlo;
+    const int a = g.x;
+    int off[RPL];
+    uint32_t im_[RPL];
+    int run = 0;
+#pragma unroll
+    for (int q = 0; q < RPL; ++q) {
+        const int l = lane + 32 * q;
+        const uint32_t im = tap_set_mask<K, S>(g.y0 + l, P.no, P.p);
+        int cnt = 0;
+#pragma unroll
+        for (int j = 0; j < K; ++j)
+            if ((jm >> j) & 1u) cnt += __popc(nz_row<K, ZT>(P.nzmask, j) & im);
+        im_[q] = im;
+        const int c = l < g.nr ? cnt : 0;
+        int inc = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += u;
+        }
+        off[q] = run + inc - c;
+        run += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    bool ok = run == g.L;
+    const int* rps = rp + (g.r0 & 3);
+    const int* cbs = cb + (int)(g.S0 & 3);
+    const uint32_t* vbs = vb + (int)(g.S0 & 3);
+    const int S0i = (int)g.S0;
+    constexpr uint32_t FULL = (1u << K) - 1u;
+    uint32_t bad = 0;
+#pragma unroll
+    for (int q = 0; q < RPL; ++q) {
+        const int l = lane + 32 * q;
+        if (l < g.nr) {
+            const int b = g.y0 + l;
+            ok &= rps[l] == S0i + off[q];
+            if (l == g.nr - 1) ok &= rps[g.nr] == S0i + g.L;
+            const uint32_t im = im_[q];
+            const int* cl = cbs + off[q];
+            const uint32_t* vl = vbs + off[q];
+            if (!ZT && S == 1 && jm == FULL && im == FULL) {
+                // every tap lands: rows (a + p - j, b + p - i) for j, i descending
+                const int rb = (a + P.p - (K - 1)) * P.no + (b + P.p - (K - 1));
+#pragma unroll
+                for (int jj = 0; jj < K; ++jj)
+#pragma unroll
+                    for (int ii = 0; ii < K; ++ii)
+                        bad |= (uint32_t)(cl[jj * K + ii] - (rb + jj * P.no + ii)) |
+                               (vl[jj * K + ii] ^ w[(K - 1 - jj) * K + (K - 1 - ii)]);
+            } else {
+                int e = 0;
+#pragma unroll
+                for (int j = K - 1; j >= 0; --j) {
+                    if (!((jm >> j) & 1u)) continue;
+                    const int xrow = (a + P.p - j) / S * P.no;
+                    const uint32_t cm = nz_row<K, ZT>(P.nzmask, j) & im;
+#pragma unroll
+                    for (int i = K - 1; i >= 0; --i) {
+                        if (!((cm >> i) & 1u)) continue;
+                        bad |= (uint32_t)(cl[e] - (xrow + (b + P.p - i) / S)) | (vl[e] ^ s_w[j * K + i]);
+                        ++e;
+                    }
+                }
+            }
+        }
+    }
+    ok &= bad == 0u;
+    return __all_sync(0xffffffffu, ok);
+}
+
+template <int K, int S, int TW, bool ZT, bool CSCM>
 __global__ void __launch_bounds__(CheckCfg<K, S, TW>::WARPS * 32) conv_band_check(const BandParams P) {
     using C = CheckCfg<K, S, TW>;
     constexpr int KK = K * K;
@@ -326,12 +481,13 @@ __global__ void __launch_bounds__(CheckCfg<K, S, TW>::WARPS * 32) conv_band_chec
     for (int q = threadIdx.x; q < KK; q += blockDim.x) s_w[q] = __float_as_uint(__ldg(P.taps + q));
 
     const long long seg = (long long)blockIdx.x * C::WARPS + warp;
-    const bool live = seg < (long long)P.mo * P.tiles_y;  // warp-uniform
+    constexpr bool csc = CSCM;
+    const bool live = seg < (csc ? (long long)P.m * P.tiles_b : (long long)P.mo * P.tiles_y);  // warp-uniform
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem) + warp;
     int* rp = reinterpret_cast<int*>(smem + 128 + (size_t)warp * C::WARP_BYTES);
     SegGeom g{};
     if (live) {
-        g = seg_geom<K, S, TW, ZT>(P, seg);
+        g = csc ? seg_geom_csc<K, S, TW, ZT>(P, seg) : seg_geom<K, S, TW, ZT>(P, seg);
         if (lane == 0) {
             mbar_init(bar, 1);
             mbar_fence_init();
@@ -341,15 +497,22 @@ __global__ void __launch_bounds__(CheckCfg<K, S, TW>::WARPS * 32) conv_band_chec
     __syncthreads();  // s_w (and the barrier inits) visible block-wide
     if (!live) return;
     if (!g.valid) {
-        if (lane == 0) P.seg_ok[seg] = 0;
+        if (lane == 0) {
+            P.seg_ok[seg] = 0;
+            if (csc) *P.fail_count = 1;
+        }
         return;
     }
     uint32_t w[KK];  // taps, compile-time indexed (full rows)
 #pragma unroll
     for (int q = 0; q < KK; ++q) w[q] = s_w[q];
     mbar_wait(bar, 0);
-    const bool ok = seg_verify<K, S, TW, ZT>(P, g, rp, w, s_w, lane);
-    if (lane == 0) P.seg_ok[seg] = ok ? 1 : 0;
+    const bool ok = csc ? seg_verify_csc<K, S, TW, ZT>(P, g, rp, w, s_w, lane)
+                        : seg_verify<K, S, TW, ZT>(P, g, rp, w, s_w, lane);
+    if (lane == 0) {
+        P.seg_ok[seg] = ok ? 1 : 0;
+        if (csc && !ok) *P.fail_count = 1;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -405,7 +568,7 @@ __global__ void __launch_bounds__(BandCfg<K, S, V, CPT, TH, STAGES, DELTA>::THRE
     unsigned long long* s_mask = reinterpret_cast<unsigned long long*>(empty + STAGES);  // per-stage row flags
     uint64_t* cbar = reinterpret_cast<uint64_t*>(s_mask + STAGES);                       // (FUSED) check slices
     float* xs = reinterpret_cast<float*>(smem + 128);
-    __shared__ uint32_t s_w[FUSED ? C::KK : 1];
+    __shared__ uint32_t s_w[C::KK];  // taps, runtime-indexed (checks, the CSC per-entry loop)
 
     const int t = threadIdx.x;
     const int lane = t & 31, warp = t >> 5;
@@ -422,8 +585,7 @@ __global__ void __launch_bounds__(BandCfg<K, S, V, CPT, TH, STAGES, DELTA>::THRE
         }
         mbar_fence_init();
     }
-    if (FUSED)
-        for (int q = t; q < C::KK; q += blockDim.x) s_w[q] = __float_as_uint(__ldg(P.taps + q));
+    for (int q = t; q < C::KK; q += blockDim.x) s_w[q] = __float_as_uint(__ldg(P.taps + q));
     __syncthreads();
 
     if (FUSED && warp == C::CWARPS) {
@@ -434,14 +596,15 @@ __global__ void __launch_bounds__(BandCfg<K, S, V, CPT, TH, STAGES, DELTA>::THRE
         for (int q = 0; q < C::KK; ++q) w[q] = s_w[q];
         int* cslice = reinterpret_cast<int*>(smem + 128 + (size_t)STAGES * C::SF * 4);
         constexpr int SLICE = (int)(CC::WARP_BYTES / 4);
-        const long long nseg = (long long)P.mo * P.tiles_y;
+        const bool csc = P.csc != 0;
+        const long long nseg = csc ? (long long)P.m * P.tiles_b : (long long)P.mo * P.tiles_y;
         long long cseg = blockIdx.x, vseg = -1;
         SegGeom vg{};
         int cb = 0;
         uint32_t cph = 0;
         auto seg_next = [&]() {  // geometry of the next segment, copies into slice cb
             if (cseg < nseg) {
-                vg = seg_geom<K, S, C::TW, ZT>(P, cseg);
+                vg = csc ? seg_geom_csc<K, S, C::TW, ZT>(P, cseg) : seg_geom<K, S, C::TW, ZT>(P, cseg);
                 vseg = cseg;
                 cseg += gridDim.x;
                 if (lane == 0 && vg.valid) {
@@ -482,9 +645,13 @@ __global__ void __launch_bounds__(BandCfg<K, S, V, CPT, TH, STAGES, DELTA>::THRE
                 if (g.valid) {
                     mbar_wait(&cbar[b], (cph >> b) & 1u);
                     cph ^= 1u << b;
-                    ok = seg_verify<K, S, C::TW, ZT>(P, g, cslice + b * SLICE, w, s_w, lane);
+                    ok = csc ? seg_verify_csc<K, S, C::TW, ZT>(P, g, cslice + b * SLICE, w, s_w, lane)
+                             : seg_verify<K, S, C::TW, ZT>(P, g, cslice + b * SLICE, w, s_w, lane);
                 }
-                if (lane == 0) P.seg_ok[sg] = ok ? 1 : 0;
+                if (lane == 0) {
+                    P.seg_ok[sg] = ok ? 1 : 0;
+                    if (csc && !ok) *P.fail_count = 1;
+                }
             } else if (I.img < P.batch) {  // all checked: wait for the next free stage
                 if (lane == 0) mbar_wait(&empty[it % STAGES], (uint32_t)(((it / STAGES) - 1) & 1));
                 __syncwarp();
@@ -501,15 +668,18 @@ __global__ void __launch_bounds__(BandCfg<K, S, V, CPT, TH, STAGES, DELTA>::THRE
         int it = 0;
         for (ItemIter I(P); I.img < P.batch; I.next(), ++it) {
             const int st = it % STAGES;
-            unsigned long long rows_ok = 0;
+            unsigned long long rows_ok = ~0ull;
+            if (!P.csc) {  // (CSC: the check verified the storage as a whole; no per-row flags)
+              rows_ok = 0;
 #pragma unroll
-            for (int h = 0; h < (TH + 31) / 32; ++h) {  // one lane per tile row
+              for (int h = 0; h < (TH + 31) / 32; ++h) {  // one lane per tile row
                 bool f = true;
                 if (32 * h + lane < TH) {
                     const int x = I.tx * TH + 32 * h + lane;
                     f = x >= P.mo || __ldg(P.seg_ok + (long long)x * P.tiles_y + I.ty) != 0;
                 }
                 rows_ok |= (unsigned long long)__ballot_sync(0xffffffffu, f) << (32 * h);
+              }
             }
             if (lane == 0) {
                 if (it >= STAGES) mbar_wait(&empty[st], (uint32_t)(((it / STAGES) - 1) & 1));
@@ -603,7 +773,30 @@ __global__ void __launch_bounds__(BandCfg<K, S, V, CPT, TH, STAGES, DELTA>::THRE
                 }
             }
         }
-        if (per_entry) {
+        if (per_entry && P.csc) {
+            // CSC storage (verified against these taps by the check): the
+            // stored taps of each output in (j, i) = column-ascending order,
+            // straight from the staged window.
+            for (int v = 0; v < V; ++v) {
+                const int x = xb + v;
+                if (x >= P.mo) break;
+                int jlo, jhi;
+                tap_range_dev(x, P.m, K, S, P.p, jlo, jhi);
+                for (int c = 0; c < CPT; ++c) {
+                    const int y = y0 + CPT * lane + c;
+                    if (y >= P.no) break;
+                    int ilo, ihi;
+                    tap_range_dev(y, P.n, K, S, P.p, ilo, ihi);
+                    const float* xo = xw + (S * (x - tx * TH)) * C::WC + S * (y - y0) + DELTA;
+                    float acc = 0.0f;
+                    for (int j = jlo; j < jhi; ++j)
+                        for (int ii = ilo; ii < ihi; ++ii)
+                            if (!ZT || ((P.nzmask >> (j * K + ii)) & 1ull))
+                                acc = fmaf(__uint_as_float(s_w[j * K + ii]), xo[j * C::WC + ii], acc);
+                    __stcs(ybase + (long long)x * P.no + y, acc);
+                }
+            }
+        } else if (per_entry) {
             // Per-entry loop straight from the CSR (window-relative gathers).
             const int wr0 = S * tx * TH - P.p;
             const int wc0 = S * y0 - P.p - DELTA;
@@ -715,6 +908,7 @@ cudaError_t run_fused(const BandParams& bp, const CUtensorMap* tmap, cudaStream_
         kern<<<(unsigned)grid, C::THREADS, SMEM, st>>>(*tmap, bp);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
+        if (bp.csc) return cudaSuccess;  // (failed CSC segments raise the handle's verdict instead)
         const long long segs = (long long)bp.mo * bp.tiles_y;
         return launch_pdl(conv_band_fixup<C::TW>, (unsigned)std::min<long long>((segs + 255) / 256, sms), 256, 0, st,
                           bp);
@@ -772,16 +966,18 @@ template <int K, int S, int TW>
 cudaError_t run_check(const BandParams& bp, cudaStream_t st, int sms) {
     (void)sms;
     using C = CheckCfg<K, S, TW>;
-    auto kern = bp.zt ? conv_band_check<K, S, TW, true> : conv_band_check<K, S, TW, false>;
-    static std::atomic<bool> init[2][64];
+    auto kern = bp.csc ? (bp.zt ? conv_band_check<K, S, TW, true, true> : conv_band_check<K, S, TW, false, true>)
+                       : (bp.zt ? conv_band_check<K, S, TW, true, false> : conv_band_check<K, S, TW, false, false>);
+    const int v = (bp.zt ? 1 : 0) + (bp.csc ? 2 : 0);
+    static std::atomic<bool> init[4][64];
     int dev = 0;
     cudaGetDevice(&dev);
-    if (!init[bp.zt ? 1 : 0][dev & 63]) {
+    if (!init[v][dev & 63]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
         if (e != cudaSuccess) return e;
-        init[bp.zt ? 1 : 0][dev & 63] = true;
+        init[v][dev & 63] = true;
     }
-    const long long segs = (long long)bp.mo * bp.tiles_y;
+    const long long segs = bp.csc ? (long long)bp.m * bp.tiles_b : (long long)bp.mo * bp.tiles_y;
     const long long grid = (segs + C::WARPS - 1) / C::WARPS;
     kern<<<(unsigned)grid, C::WARPS * 32, C::SMEM, st>>>(bp);
     return cudaGetLastError();

@@ -142,6 +142,28 @@ int main() {
                                                           tc.matrix.val());
         CHECK(spmv(g, Grid(3, 3, 1.0).values) == (std::vector<double>{4, 6, 4, 6, 9, 6, 4, 6, 4}));
         CHECK(relayout(g, Layout::CSR).ptr() == tr.matrix.ptr());
+        // spmv(m, x, threads) on CSC storage: the reference's per-thread
+        // partials over column chunks, added in thread order
+        // (inc/sparse.hpp:228-258), restated here on the exported storage.
+        const ConvSpec sp2(23, 19, 5, 2, 3);
+        std::vector<double> kv(25), xv(23 * 19);
+        for (int q = 0; q < 25; ++q) kv[q] = std::ldexp(1.0 + 0.37 * q, (q * 7) % 21 - 10);
+        for (size_t q = 0; q < xv.size(); ++q) xv[q] = std::ldexp(1.0 - 0.013 * (double)q, (int)(q * 5 % 31) - 15);
+        const Transform t2 = build_transform(Kernel(5, kv), sp2, Layout::CSC);
+        const auto& P = t2.matrix.ptr();
+        const auto& I = t2.matrix.idx();
+        const auto& V = t2.matrix.val();
+        for (int nt : {1, 3, 8}) {
+            const index_t cols = t2.matrix.cols(), chunk = (cols + nt - 1) / nt;
+            std::vector<double> want((size_t)t2.matrix.rows(), 0.0);
+            for (int th = 0; th < nt; ++th) {
+                std::vector<double> part(want.size(), 0.0);
+                for (index_t j = std::min<index_t>(th * chunk, cols); j < std::min<index_t>((th + 1) * chunk, cols); ++j)
+                    for (index_t e = P[j]; e < P[j + 1]; ++e) part[I[e]] = part[I[e]] + V[e] * xv[j];
+                for (size_t r = 0; r < want.size(); ++r) want[r] = nt == 1 ? part[r] : want[r] + part[r];
+            }
+            CHECK(spmv(t2.matrix, xv, nt) == want);
+        }
     }
     // entries / to_dense / read_sparse / flipped (inc/sparse.hpp, inc/conv.hpp)
     {

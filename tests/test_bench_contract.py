@@ -26,7 +26,7 @@ def test_bench_line_contract():
     for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
                 "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches", "clocks"):
         assert key in j, key
-    assert j["n_gpus"] == 1 and j["steps"] == 5 and j["warmup"] == 3 and j["scaling"] == "weak"
+    assert j["n_gpus"] == 1 and j["steps"] == 5 and j["warmup"] == 3 and j["scaling"] == "strong"
     assert j["value"] > 0 and j["higher_is_better"] is True and j["vs_baseline"] is None
     assert "workload" in j["config"] and "model" not in j["config"]
     r = j["roofline"]

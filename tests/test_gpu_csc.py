@@ -13,7 +13,7 @@ import hashlib
 import numpy as np
 import pytest
 
-from helpers import CONFIGS, golden_cases, problem, sha, sweep_specs, BAND_KERNELS
+from helpers import CONFIGS, CSC_BAND_KERNELS, golden_cases, problem, sha, sweep_specs, BAND_KERNELS
 
 pytestmark = pytest.mark.gpu
 
@@ -202,7 +202,7 @@ def test_csc_text_read_back(sp, orc, ref, torch_cuda):
     assert all(np.array_equal(a, b) for a, b in zip(r.export(), want))
     assert r.write_text() == data
     Y = apply(torch_cuda, sp, r, X)
-    assert r.last_kernel in BAND_KERNELS
+    assert r.last_kernel in BAND_KERNELS + CSC_BAND_KERNELS
     assert np.array_equal(bits(Y), bits(orc.spmm_native(*orc.build_native(*spec, kern), X)))
     # a non-conv csc matrix stays generic but keeps its layout
     lines = data.split(b"\n")
