@@ -558,17 +558,30 @@ def secondary_single(sp, torch, dev, stream, steps, peak):
     kern32 = problem_kernel(sp, cfg["seed"], k)
     t = sp.build_transform(sp.Kernel(k, kern32.astype(np.float64)), sp.ConvSpec(m, n, k, s, p),
                            device=dev.index, stream=stream)
-    Xh = pinned_images(sp, torch, cfg["seed"], 0, 128, t.cols)
+    Xh = pinned_images(sp, torch, cfg["seed"], 0, 256, t.cols)
     X = Xh.to(dev)
-    Y = torch.empty(128, t.rows, device=dev)
+    Y = torch.empty(256, t.rows, device=dev)
     prox = {}
     for g, b in ((2, 128), (4, 64), (8, 32)):
         line = device_line(sp, torch, t, X, Y, b, steps, dev, stream, peak)
         line["as_rank_of"] = f"N={g}: batch_slice(256, r, {g}) = {b} images"
         prox[f"n{g}"] = line
     out["config3_per_rank_proxy"] = prox
-    del X, Y, Xh
     t.close()
+    # ---- config 3 as a CSC transform (the reference's second layout): the
+    # handle holds the CSC storage only and every call streams it (CSC band
+    # check); algorithmic bytes 8 nnz + 4 (cols + 1) + 4 b (cols + rows)
+    tc = sp.build_transform(sp.Kernel(k, kern32.astype(np.float64)), sp.ConvSpec(m, n, k, s, p), layout=1,
+                            device=dev.index, stream=stream)
+    alg = 8 * tc.nnz + 4 * (tc.cols + 1) + 4 * 256 * (tc.cols + tc.rows)
+    line = device_line(sp, torch, tc, X, Y, 256, steps, dev, stream, peak, alg=alg)
+    same, _ = parity_check(cfg["spec"], kern32, Xh, Y, slice_probe(256))
+    line.update(parity="bitexact" if same else "MISMATCH", storage_bytes=tc.storage_bytes,
+                storage_bytes_csr_handle=8 * tc.nnz + 4 * (tc.rows + 1),
+                layout="csc (col_ptr / row_idx / vals only)")
+    out["config3_csc"] = line
+    tc.close()
+    del X, Y, Xh
     # ---- config 4: the per-rank slice at N = 8 (8 images) ----
     cfg = CONFIGS[4]
     m, n, k, s, p = cfg["spec"]

@@ -311,7 +311,7 @@ spb::CscGatherParams csc_params(const spconv_csr* h, bool f64) {
 int csc_sticky(const spconv_csr* h, const char* who) {
     if (h->fail_flag && !h->exposed.load() && *reinterpret_cast<volatile int*>(h->fail_flag))
         return fail(SPCONV_ECUDA, std::string(who) +
-                                      ": the CSC storage no longer matches the transform of its taps "
+                                      ": the stored matrix no longer matches the transform of its taps "
                                       "(a device check failed in an earlier call)");
     return SPCONV_OK;
 }
@@ -428,10 +428,10 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
                         (reinterpret_cast<uintptr_t>(X) % 16 == 0) && encode_fn() != nullptr &&
                         g.m < (1ll << 30) && g.n < (1ll << 30);
 
+    if (int rc = csc_sticky(h, "spconv_spmm")) return rc;
     // ---- CSC storage of a conv transform: the CSC kernels ----
     const bool csc = csc_native(h);
     if (csc) {
-        if (int rc = csc_sticky(h, "spconv_spmm")) return rc;
         if (h->exposed.load()) {
             bool clean = false;
             if (int rc = csc_exposed_clean(h, st, false, &clean)) return rc;
@@ -572,6 +572,11 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
         bp.csc = csc ? 1 : 0;
         bp.tiles_b = h->csc_tiles_b;
         bp.fail_count = h->fail_flag;
+        // Row-major storage handed out by spconv_csr_device_ptrs may change:
+        // the fused form then recomputes failed segments (conv_band_fixup).
+        // Otherwise a failed check can only mean corrupted memory: it raises
+        // the verdict word instead, and no fixup pass is launched.
+        bp.fixup = !csc && h->exposed.load() ? 1 : 0;
         bp.taps = h->taps;
         bp.seg_ok = h->seg_ok;
         bp.X = X;
@@ -610,7 +615,9 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
         if (bp.fused) {
             const cudaError_t fe = spb::launch_band((int)g.k, (int)g.s, bp, &tmap, st, nullptr, sms);
             if (fe == cudaSuccess) {
-                h->last_kernel.store(csc ? "conv_spmm_band<fused,csc>" : "conv_spmm_band<fused>+conv_band_fixup");
+                h->last_kernel.store(csc          ? "conv_spmm_band<fused,csc>"
+                                     : bp.fixup ? "conv_spmm_band<fused>+conv_band_fixup"
+                                                : "conv_spmm_band<fused>");
                 return SPCONV_OK;
             }
             if (fe != cudaErrorNotSupported) CK(fe);
@@ -942,6 +949,11 @@ static int build_csr_impl(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
         int64_t lo, hi;
         for (int64_t yy = 0; yy < g.no; ++yy) tap_range(yy, g.n, g.k, g.s, g.p, lo, hi), h->sy += hi - lo;
     }
+    h->fail_flag = flag_alloc();  // (the fused band apply's verdict word)
+    if (!h->fail_flag) {
+        delete h;
+        return fail(SPCONV_ECUDA, "cudaHostAlloc(verdict words) failed");
+    }
 
     // One stream-ordered allocation for the CSR (+256 B slack so prologue
     // reads one-past-the-end stay in bounds).
@@ -956,6 +968,7 @@ static int build_csr_impl(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
     char* csr = nullptr;
     cudaError_t e = cudaMallocAsync(&csr, rp_bytes + 2 * ix_bytes + 256 + tap_bytes + seg_bytes, st);
     if (e != cudaSuccess) {
+        flag_free(h->fail_flag);
         delete h;
         return cuda_fail(e, "cudaMallocAsync(CSR)");
     }
@@ -993,6 +1006,7 @@ static int build_csr_impl(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
         e = cudaMallocAsync(&tab, taps_b + sat_b + w_b, st);
         if (e != cudaSuccess) {
             cudaFreeAsync(csr, st);
+            flag_free(h->fail_flag);
             delete h;
             return cuda_fail(e, "cudaMallocAsync(tables)");
         }
@@ -1022,6 +1036,7 @@ static int build_csr_impl(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
     if (smem > 200 * 1024) {
         if (tab) cudaFreeAsync(tab, st);
         cudaFreeAsync(csr, st);
+        flag_free(h->fail_flag);
         delete h;
         return fail(SPCONV_EINVAL, "spconv_build_csr: kernel side " + std::to_string(k) +
                                        " too large for the device build");
@@ -1049,6 +1064,7 @@ static int build_csr_impl(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
         if (h->vals64) cudaFreeAsync(h->vals64, st);
         cudaFreeAsync(csr, st);
         cudaStreamSynchronize(st);
+        flag_free(h->fail_flag);
         delete h;
         return cuda_fail(e, "csr_build launch");
     }
@@ -1115,9 +1131,9 @@ static int build_csc_impl(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
     const size_t ix_bytes = ((size_t)std::max<int64_t>(ht.nnz, 1) * 4 + 255) & ~size_t(255);
     const size_t tap_bytes = ((size_t)(k * k) * 4 + 255) & ~size_t(255);
     size_t seg_bytes = 0;
-    if (spb::band_supported((int)k, (int)s)) {  // CSC segments: one input row x band_tw input columns
+    if (spb::band_supported((int)k, (int)s)) {  // CSC segments: one input row x s * band_tw input columns
         h->band_tw = spb::band_tile_width((int)k, (int)s);
-        h->csc_tiles_b = (int)((n + h->band_tw - 1) / h->band_tw);
+        h->csc_tiles_b = (int)((n + h->band_tw * s - 1) / (h->band_tw * s));  // (segments of s * band_tw columns)
         seg_bytes = ((size_t)(m * h->csc_tiles_b) + 255) & ~size_t(255);
     }
     char* mem = nullptr;
@@ -1696,7 +1712,7 @@ int spconv_csr_device_ptrs(const spconv_csr* h, const int32_t** row_ptr, const i
     // Writable storage leaves the library's control: a CSC conv handle is
     // checked before every later apply, which then follows the storage as it
     // stands (row-major handles re-check every call anyway: the band check).
-    if (h->layout == 1) const_cast<spconv_csr*>(h)->exposed.store(true);
+    const_cast<spconv_csr*>(h)->exposed.store(true);
     if (row_ptr) *row_ptr = h->layout ? h->csc_ptr : h->row_ptr;
     if (col_idx) *col_idx = h->layout ? h->csc_idx : h->col_idx;
     if (vals) *vals = h->layout ? h->csc_vals : h->vals;
@@ -2114,7 +2130,7 @@ int spconv_band_check_status(const spconv_csr* h, int64_t* segments, int64_t* fa
     DeviceGuard dg(h->device);
     if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
     // CSR: one segment per output row x band_tw output columns; CSC storage:
-    // one per input row x band_tw input columns
+    // one per input row x s * band_tw input columns
     const int64_t n = csc_native(h) ? h->g.m * h->csc_tiles_b : h->g.mo * ((h->g.no + h->band_tw - 1) / h->band_tw);
     std::vector<uint8_t> v((size_t)n);
     CK(cudaDeviceSynchronize());

@@ -130,7 +130,8 @@ struct BandParams {
     // segments per input row) and the apply never reads it per entry.
     int csc;
     int tiles_b;
-    int* fail_count;  // csc: set to 1 when a segment fails (the handle's sticky verdict)
+    int* fail_count;  // set to 1 when a segment fails and nothing repairs it (the handle's sticky verdict)
+    int fixup;        // fused CSR form: launch conv_band_fixup for failed segments (storage handed out)
 };
 
 // CSC-storage SpMV / SpMM of a conv transform (csc_apply.cu).

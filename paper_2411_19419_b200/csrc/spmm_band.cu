@@ -123,13 +123,20 @@ struct BandCfg {
 //    row_ptr matches its prediction and every entry matches the pattern, the
 //    segment's rows are exactly the conv rows.  Result: one byte per segment.
 // ---------------------------------------------------------------------------
-template <int K, int S, int TW>
+// PER: most entries per major index (k^2 for CSR rows; ceil(k/s)^2 for CSC
+// columns); SEG: majors per segment (TW output columns for CSR, TWC = s * TW
+// input columns for CSC -- the same input footprint, so a CSC segment of the
+// apply's tile width never holds more entries than a CSR one).
+template <int K, int S, int TW, int PER = K * K, int SEG = TW>
 struct CheckCfg {
     static constexpr int KK = K * K;
-    static constexpr int RUN = TW * KK;                    // entries of a full segment
+    static constexpr int TWC = S * TW;                     // CSC segment width (input columns)
+    static constexpr int RUN = SEG * PER;                  // entries of a full segment
     static constexpr int BUFW = (RUN + 3 + 3) / 4 * 4;     // + alignment slack (16-byte bulk units)
-    static constexpr int RPW = (TW + 1 + 3 + 3) / 4 * 4;   // row_ptr words
-    static constexpr size_t WARP_BYTES = (size_t)(RPW + 2 * BUFW) * 4;
+    static constexpr int RPW = (TWC + 1 + 3 + 3) / 4 * 4;  // row_ptr / col_ptr words
+    static constexpr int OFFW = S > 1 ? TWC : 0;           // CSC, s > 1: per-column run offsets
+    static constexpr size_t WARP_BYTES = (size_t)(RPW + 2 * BUFW + OFFW) * 4;
+    static_assert(SEG * PER <= TW * KK || SEG == TWC, "");
     static constexpr int WARPS = 4;
     static constexpr size_t SMEM = 128 + (size_t)WARPS * WARP_BYTES;
     static_assert(SMEM <= 200 * 1024, "segment too large for shared memory");
@@ -200,9 +207,9 @@ __device__ __forceinline__ SegGeom seg_geom(const BandParams& P, long long seg) 
 
 // Lane 0: the three bulk copies of a valid segment (row_ptr, col_idx, vals)
 // into one staging slice of CheckCfg::WARP_BYTES, completing on `bar`.
-template <int K, int S, int TW>
+template <int K, int S, int TW, int PER = K * K, int SEG = TW>
 __device__ __forceinline__ void seg_issue(const BandParams& P, const SegGeom& g, int* rp, uint64_t* bar) {
-    using C = CheckCfg<K, S, TW>;
+    using C = CheckCfg<K, S, TW, PER, SEG>;
     int* cb = rp + C::RPW;
     int* vb = cb + C::BUFW;
     const int rbase = g.r0 & ~3;
@@ -359,6 +366,7 @@ __device__ __forceinline__ uint32_t nz_row(unsigned long long nzmask, int j) {
     return ZT ? (uint32_t)((nzmask >> (j * K)) & ((1ull << K) - 1ull)) : ((1u << K) - 1u);
 }
 
+// TW here = the CSC segment width (CheckCfg::TWC).
 template <int K, int S, int TW, bool ZT>
 __device__ __forceinline__ SegGeom seg_geom_csc(const BandParams& P, long long seg) {
     SegGeom g;
@@ -393,8 +401,35 @@ __device__ __forceinline__ SegGeom seg_geom_csc(const BandParams& P, long long s
 // per-column offsets by a warp scan of the column counts, col_ptr compared,
 // then each column's rows and values compared with the taps that land on it
 // (interior stride-1 columns of dense taps fully unrolled).
+// Interior CSC column of residue class (RA, RB) = (a + p, b + p) mod s: all
+// NJ x NI taps of the class land; rows r0 + dj * n_out + di, taps (JT - s dj, IT - s di).
+template <int K, int S, int RA, int RB>
+__device__ __forceinline__ uint32_t csc_interior(const int* cl, const uint32_t* vl, int a, int b, int p, int no,
+                                                 const uint32_t (&w)[K * K]) {
+    constexpr int NJ = (K - 1 - RA) / S + 1, JT = RA + S * (NJ - 1);
+    constexpr int NI = (K - 1 - RB) / S + 1, IT = RB + S * (NI - 1);
+    const int r0 = (a + p - JT) / S * no + (b + p - IT) / S;
+    uint32_t bad = 0;
+#pragma unroll
+    for (int dj = 0; dj < NJ; ++dj)
+#pragma unroll
+        for (int di = 0; di < NI; ++di)
+            bad |= (uint32_t)(cl[dj * NI + di] - (r0 + dj * no + di)) | (vl[dj * NI + di] ^ w[(JT - S * dj) * K + (IT - S * di)]);
+    return bad;
+}
+
+// #{i in [0, K) : i == rb (mod S), 0 <= (b + p - i) / S < no}: the taps landing on input column b.
+template <int K, int S>
+__device__ __forceinline__ int taps_on(int b, int p, int no) {
+    const int bp = b + p;
+    const int lo = max(0, bp - S * (no - 1)), hi = min(K - 1, bp);
+    const int first = lo + (((bp - lo) % S) + S) % S;  // first i >= lo with i == bp (mod S)
+    return first > hi ? 0 : (hi - first) / S + 1;
+}
+
+// (s = 1 in the fused producer's staging layout, CheckCfg<K, 1, TW>)
 template <int K, int S, int TW, bool ZT>
-__device__ __forceinline__ bool seg_verify_csc(const BandParams& P, const SegGeom& g, const int* rp,
+__device__ __forceinline__ bool seg_verify_csc_s1(const BandParams& P, const SegGeom& g, const int* rp,
                                                const uint32_t (&w)[K * K], const uint32_t* s_w, int lane) {
     using C = CheckCfg<K, S, TW>;
     constexpr int RPL = TW / 32;  // columns per lane
@@ -471,9 +506,151 @@ __device__ __forceinline__ bool seg_verify_csc(const BandParams& P, const SegGeo
     return __all_sync(0xffffffffu, ok);
 }
 
+template <int K, int S, int TW, bool ZT, int PER = K * K, int SEG = TW>
+__device__ __forceinline__ bool seg_verify_csc(const BandParams& P, const SegGeom& g, int* rp,
+                                               const uint32_t (&w)[K * K], const uint32_t* s_w, int lane) {
+    using C = CheckCfg<K, S, TW, PER, SEG>;
+    if constexpr (S == 1 && PER == K * K) return seg_verify_csc_s1<K, S, TW, ZT>(P, g, rp, w, s_w, lane);
+    constexpr int TWC = C::TWC;
+    constexpr int RPL = TWC / 32;  // columns per lane
+    const int* cb = rp + C::RPW;
+    const uint32_t* vb = reinterpret_cast<const uint32_t*>(cb + C::BUFW);
+    const uint32_t jm = (uint32_t)g.jlo;
+    const int a = g.x;
+    const int nj = __popc(jm);
+    const int* rps = rp + (g.r0 & 3);
+    const int S0i = (int)g.S0;
+    const int* cbs = cb + (int)(g.S0 & 3);
+    const uint32_t* vbs = vb + (int)(g.S0 & 3);
+    // 1. column counts in natural order: warp scan -> offsets; col_ptr compared
+    int run = 0, off[RPL];
+    uint32_t im_[RPL];  // (s = 1: the column tap masks, kept for pass 2)
+    bool ok = true;
+#pragma unroll
+    for (int q = 0; q < RPL; ++q) {
+        const int l = lane + 32 * q;
+        int cnt = 0;
+        if (ZT || S == 1) {
+            const uint32_t im = tap_set_mask<K, S>(g.y0 + l, P.no, P.p);
+            im_[q] = im;
+#pragma unroll
+            for (int j = 0; j < K; ++j)
+                if ((jm >> j) & 1u) cnt += __popc(nz_row<K, ZT>(P.nzmask, j) & im);
+        } else {
+            cnt = nj * taps_on<K, S>(g.y0 + l, P.p, P.no);
+        }
+        const int c = l < g.nr ? cnt : 0;
+        int inc = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += u;
+        }
+        off[q] = run + inc - c;
+        if (l < g.nr) {
+            ok &= rps[l] == S0i + off[q];
+            if (l == g.nr - 1) ok &= rps[g.nr] == S0i + g.L;
+        }
+        run += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    ok &= run == g.L;
+    uint32_t bad = 0;
+    if constexpr (S == 1) {
+        // 2. every column's rows and values against the taps landing on it
+        //    (interior columns of dense taps fully unrolled)
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) {
+            const int l = lane + 32 * q;
+            if (l >= g.nr) continue;
+            const int b = g.y0 + l;
+            const int* cl = cbs + off[q];
+            const uint32_t* vl = vbs + off[q];
+            const uint32_t im = im_[q];
+            if (!ZT && jm == (1u << K) - 1u && im == (1u << K) - 1u) {
+                const int rb = (a + P.p - (K - 1)) * P.no + (b + P.p - (K - 1));
+#pragma unroll
+                for (int jj = 0; jj < K; ++jj)
+#pragma unroll
+                    for (int ii = 0; ii < K; ++ii)
+                        bad |= (uint32_t)(cl[jj * K + ii] - (rb + jj * P.no + ii)) |
+                               (vl[jj * K + ii] ^ w[(K - 1 - jj) * K + (K - 1 - ii)]);
+            } else {
+                int e = 0;
+#pragma unroll
+                for (int j = K - 1; j >= 0; --j) {
+                    if (!((jm >> j) & 1u)) continue;
+                    const int xrow = (a + P.p - j) * P.no;
+                    const uint32_t cm = nz_row<K, ZT>(P.nzmask, j) & im;
+#pragma unroll
+                    for (int i = K - 1; i >= 0; --i) {
+                        if (!((cm >> i) & 1u)) continue;
+                        bad |= (uint32_t)(cl[e] - (xrow + (b + P.p - i))) | (vl[e] ^ s_w[j * K + i]);
+                        ++e;
+                    }
+                }
+            }
+        }
+    } else {
+        // 2. s > 1: lanes in residue-uniform order (pass q covers columns
+        //    b0 + s * lane + (q mod s) of its group), so every lane of a pass
+        //    has the same interior tap pattern: one warp-uniform branch.
+        static_assert(S == 2, "band geometries have s <= 2");
+        int* s_off = rp + C::RPW + 2 * C::BUFW;
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) s_off[lane + 32 * q] = off[q];
+        __syncwarp();
+        const int ra = (a + P.p) % S, NJ = (K - 1 - ra) / S + 1;
+#pragma unroll 1
+        for (int q = 0; q < RPL; ++q) {
+            const int l = (q / S) * 32 * S + S * lane + (q % S);
+            const int b = g.y0 + l;
+            const int rb = (b + P.p) % S;  // (warp-uniform)
+            const int o = s_off[l];
+            const int* cl = cbs + o;
+            const uint32_t* vl = vbs + o;
+            const bool live = l < g.nr;
+            const bool interior = !ZT && nj == NJ && taps_on<K, S>(b, P.p, P.no) == (K - 1 - rb) / S + 1;
+            if (live && interior) {
+                const int pat = ra * S + rb;
+                if (pat == 0)
+                    bad |= csc_interior<K, S, 0, 0>(cl, vl, a, b, P.p, P.no, w);
+                else if (pat == 1)
+                    bad |= csc_interior<K, S, 0, 1>(cl, vl, a, b, P.p, P.no, w);
+                else if (pat == 2)
+                    bad |= csc_interior<K, S, 1, 0>(cl, vl, a, b, P.p, P.no, w);
+                else
+                    bad |= csc_interior<K, S, 1, 1>(cl, vl, a, b, P.p, P.no, w);
+            } else if (live) {
+                const uint32_t im = tap_set_mask<K, S>(b, P.no, P.p);
+                int e = 0;
+#pragma unroll 1
+                for (int j = K - 1; j >= 0; --j) {
+                    if (!((jm >> j) & 1u)) continue;
+                    const int xrow = (a + P.p - j) / S * P.no;
+                    const uint32_t cm = nz_row<K, ZT>(P.nzmask, j) & im;
+#pragma unroll 1
+                    for (int i = K - 1; i >= 0; --i) {
+                        if (!((cm >> i) & 1u)) continue;
+                        bad |= (uint32_t)(cl[e] - (xrow + (b + P.p - i) / S)) | (vl[e] ^ s_w[j * K + i]);
+                        ++e;
+                    }
+                }
+            }
+        }
+    }
+    ok &= bad == 0u;
+    return __all_sync(0xffffffffu, ok);
+}
+
+// (CSC: the staging is sized for ceil(k/s)^2 entries per column)
+template <int K, int S, int TW>
+constexpr int csc_per() { return ((K + S - 1) / S) * ((K + S - 1) / S); }
+
 template <int K, int S, int TW, bool ZT, bool CSCM>
 __global__ void __launch_bounds__(CheckCfg<K, S, TW>::WARPS * 32) conv_band_check(const BandParams P) {
-    using C = CheckCfg<K, S, TW>;
+    constexpr int PER = CSCM ? csc_per<K, S, TW>() : K * K;
+    constexpr int SEG = CSCM ? S * TW : TW;
+    using C = CheckCfg<K, S, TW, PER, SEG>;
     constexpr int KK = K * K;
     extern __shared__ __align__(128) unsigned char smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -487,11 +664,11 @@ __global__ void __launch_bounds__(CheckCfg<K, S, TW>::WARPS * 32) conv_band_chec
     int* rp = reinterpret_cast<int*>(smem + 128 + (size_t)warp * C::WARP_BYTES);
     SegGeom g{};
     if (live) {
-        g = csc ? seg_geom_csc<K, S, TW, ZT>(P, seg) : seg_geom<K, S, TW, ZT>(P, seg);
+        g = csc ? seg_geom_csc<K, S, S * TW, ZT>(P, seg) : seg_geom<K, S, TW, ZT>(P, seg);
         if (lane == 0) {
             mbar_init(bar, 1);
             mbar_fence_init();
-            if (g.valid) seg_issue<K, S, TW>(P, g, rp, bar);
+            if (g.valid) seg_issue<K, S, TW, PER, SEG>(P, g, rp, bar);
         }
     }
     __syncthreads();  // s_w (and the barrier inits) visible block-wide
@@ -507,7 +684,7 @@ __global__ void __launch_bounds__(CheckCfg<K, S, TW>::WARPS * 32) conv_band_chec
 #pragma unroll
     for (int q = 0; q < KK; ++q) w[q] = s_w[q];
     mbar_wait(bar, 0);
-    const bool ok = csc ? seg_verify_csc<K, S, TW, ZT>(P, g, rp, w, s_w, lane)
+    const bool ok = csc ? seg_verify_csc<K, S, TW, ZT, PER, SEG>(P, g, rp, w, s_w, lane)
                         : seg_verify<K, S, TW, ZT>(P, g, rp, w, s_w, lane);
     if (lane == 0) {
         P.seg_ok[seg] = ok ? 1 : 0;
@@ -604,7 +781,7 @@ __global__ void __launch_bounds__(BandCfg<K, S, V, CPT, TH, STAGES, DELTA>::THRE
         uint32_t cph = 0;
         auto seg_next = [&]() {  // geometry of the next segment, copies into slice cb
             if (cseg < nseg) {
-                vg = csc ? seg_geom_csc<K, S, C::TW, ZT>(P, cseg) : seg_geom<K, S, C::TW, ZT>(P, cseg);
+                vg = csc ? seg_geom_csc<K, S, S * C::TW, ZT>(P, cseg) : seg_geom<K, S, C::TW, ZT>(P, cseg);
                 vseg = cseg;
                 cseg += gridDim.x;
                 if (lane == 0 && vg.valid) {
@@ -650,7 +827,7 @@ __global__ void __launch_bounds__(BandCfg<K, S, V, CPT, TH, STAGES, DELTA>::THRE
                 }
                 if (lane == 0) {
                     P.seg_ok[sg] = ok ? 1 : 0;
-                    if (csc && !ok) *P.fail_count = 1;
+                    if (!ok && !P.fixup) *P.fail_count = 1;
                 }
             } else if (I.img < P.batch) {  // all checked: wait for the next free stage
                 if (lane == 0) mbar_wait(&empty[it % STAGES], (uint32_t)(((it / STAGES) - 1) & 1));
@@ -908,7 +1085,7 @@ cudaError_t run_fused(const BandParams& bp, const CUtensorMap* tmap, cudaStream_
         kern<<<(unsigned)grid, C::THREADS, SMEM, st>>>(*tmap, bp);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
-        if (bp.csc) return cudaSuccess;  // (failed CSC segments raise the handle's verdict instead)
+        if (!bp.fixup) return cudaSuccess;  // (failed segments raise the handle's verdict instead)
         const long long segs = (long long)bp.mo * bp.tiles_y;
         return launch_pdl(conv_band_fixup<C::TW>, (unsigned)std::min<long long>((segs + 255) / 256, sms), 256, 0, st,
                           bp);
@@ -966,20 +1143,22 @@ template <int K, int S, int TW>
 cudaError_t run_check(const BandParams& bp, cudaStream_t st, int sms) {
     (void)sms;
     using C = CheckCfg<K, S, TW>;
+    using CS = CheckCfg<K, S, TW, csc_per<K, S, TW>(), S * TW>;  // (CSC staging)
     auto kern = bp.csc ? (bp.zt ? conv_band_check<K, S, TW, true, true> : conv_band_check<K, S, TW, false, true>)
                        : (bp.zt ? conv_band_check<K, S, TW, true, false> : conv_band_check<K, S, TW, false, false>);
     const int v = (bp.zt ? 1 : 0) + (bp.csc ? 2 : 0);
     static std::atomic<bool> init[4][64];
     int dev = 0;
     cudaGetDevice(&dev);
+    const size_t smem = bp.csc ? CS::SMEM : C::SMEM;
     if (!init[v][dev & 63]) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         init[v][dev & 63] = true;
     }
     const long long segs = bp.csc ? (long long)bp.m * bp.tiles_b : (long long)bp.mo * bp.tiles_y;
     const long long grid = (segs + C::WARPS - 1) / C::WARPS;
-    kern<<<(unsigned)grid, C::WARPS * 32, C::SMEM, st>>>(bp);
+    kern<<<(unsigned)grid, C::WARPS * 32, smem, st>>>(bp);
     return cudaGetLastError();
 }
 

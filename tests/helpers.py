@@ -72,6 +72,7 @@ def golden_cases(orc, js):
 
 # Kernel pairs of the band path (spconv_csr_last_kernel): the check kernel +
 # apply, or the fused check-and-apply + its fixup pass.
-BAND_KERNELS = ("conv_band_check+conv_spmm_band", "conv_spmm_band<fused>+conv_band_fixup")
+# (the fixup pass only once the storage was handed out by device_ptrs)
+BAND_KERNELS = ("conv_band_check+conv_spmm_band", "conv_spmm_band<fused>", "conv_spmm_band<fused>+conv_band_fixup")
 # ... and over CSC storage (the CSC band check; no fixup pass)
 CSC_BAND_KERNELS = ("conv_band_check<csc>+conv_spmm_band", "conv_spmm_band<fused,csc>")

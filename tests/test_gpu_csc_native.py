@@ -122,7 +122,7 @@ def test_csc_band_forms(sp, orc, torch_cuda, spec, fused):
         assert t.last_kernel in CSC_BAND_KERNELS
         assert np.array_equal(bits(Y), bits(csc_want(orc, t, Xn))), (spec, zero)
         segs, bad = t.band_check_status()
-        assert segs == m * -(-n // (128 if spec[3] == 1 else 64)) and bad == 0
+        assert segs == m * -(-n // 128) and bad == 0  # (s * band width input columns per segment)
 
 
 @pytest.mark.slow
