@@ -185,14 +185,16 @@ enum Path { kAuto = 0, kBanded, kTiled, kTiledNoTma, kGeneric, kSpmv, kSpmvPlain
 Path path_override() { return static_cast<Path>(spb::opt(spb::kOptPath)); }
 
 // 3-D tensor map over the batch X[b][m][n] (fp32) with the given box.
-int encode_x_map(CUtensorMap* tmap, const float* X, const Geom& g, int64_t ldx, int64_t batch,
-                 int box_c, int box_r, int box_b) {
+int encode_x_map(CUtensorMap* tmap, const void* X, const Geom& g, int64_t ldx, int64_t batch,
+                 int box_c, int box_r, int box_b, bool f64 = false) {
     std::memset(tmap, 0, sizeof *tmap);
+    const int64_t es = f64 ? 8 : 4;
     const cuuint64_t dims[3] = {(cuuint64_t)g.n, (cuuint64_t)g.m, (cuuint64_t)batch};
-    const cuuint64_t strides[2] = {(cuuint64_t)(g.n * 4), (cuuint64_t)(ldx * 4)};
+    const cuuint64_t strides[2] = {(cuuint64_t)(g.n * es), (cuuint64_t)(ldx * es)};
     const cuuint32_t box[3] = {(cuuint32_t)box_c, (cuuint32_t)box_r, (cuuint32_t)box_b};
     const cuuint32_t estr[3] = {1, 1, 1};
-    CUresult cr = encode_fn()(tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(X), dims,
+    CUresult cr = encode_fn()(tmap, f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                              const_cast<void*>(X), dims,
                               strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -418,6 +420,78 @@ int csc_repair_apply(spconv_csr* h, const void* X, int64_t ldx, void* Y, int64_t
     return SPCONV_OK;
 }
 
+// The blocked apply needs finite taps; exact-zero taps (not stored) take the
+// masked (ZT) instantiations: k <= 7, so the mask fits 64 bits.  (stored = the
+// DOUBLE tap is non-zero when the handle has double taps: a tap that narrows
+// to 0.0f is still an entry, applied as w = 0)
+bool band_taps_ok(const spconv_csr* h) {
+    bool finite = !h->host_taps.empty(), any = false;
+    for (size_t q = 0; q < h->host_taps.size(); ++q) finite &= std::isfinite(h->host_taps[q]), any |= tap_stored(h, q);
+    return h->taps_dense || (finite && any && h->g.k <= 7);
+}
+
+// BandParams of one band call (check + apply) over the handle's storage.
+int band_setup(spconv_csr* h, bool csc, bool f64, int64_t batch, const void* X, int64_t ldx, void* Y, int64_t ldy,
+               spb::BandParams& bp, spb::BandShape& sh, int sms, cudaStream_t st = nullptr) {
+    const Geom& g = h->g;
+    const bool band_taps = band_taps_ok(h);
+    unsigned long long nzmask = 0;
+    for (size_t q = 0; q < h->host_taps.size() && q < 64; ++q)
+        if (tap_stored(h, q)) nzmask |= 1ull << q;
+    bp = spb::BandParams{};
+    bp.p = (int)g.p;
+    bp.zt = band_taps && !h->taps_dense ? 1 : 0;
+    bp.nzmask = nzmask;
+    if (bp.zt) {  // W[j] = sum over stored taps (j, i) of #{y : tap i lands in the input}
+        for (int64_t j = 0; j < g.k && j < 8; ++j) {
+            long long wj = 0;
+            for (int64_t i = 0; i < g.k; ++i) {
+                if (!((nzmask >> (j * g.k + i)) & 1ull)) continue;
+                // y with 0 <= s*y + i - p < n, y in [0, n_out): a closed range
+                const int64_t lo = g.p - i <= 0 ? 0 : (g.p - i + g.s - 1) / g.s;
+                const int64_t hi = g.n + g.p - i - 1 < 0 ? -1 : std::min<int64_t>(g.no - 1, (g.n + g.p - i - 1) / g.s);
+                wj += std::max<int64_t>(0, hi - lo + 1);
+            }
+            bp.zw[j] = wj;
+        }
+    }
+    CK(f64 ? spb::launch_band64((int)g.k, (int)g.s, bp, nullptr, st, &sh, sms)
+           : spb::launch_band((int)g.k, (int)g.s, bp, nullptr, st, &sh, sms));
+    bp.row_ptr = csc ? h->csc_ptr : h->row_ptr;
+    bp.col_idx = csc ? h->csc_idx : h->col_idx;
+    bp.vals = csc ? h->csc_vals : h->vals;
+    bp.csc = csc ? 1 : 0;
+    bp.tiles_b = h->csc_tiles_b;
+    bp.fail_count = h->fail_flag;
+    // Row-major storage handed out by spconv_csr_device_ptrs may change: the
+    // fused form then recomputes failed segments (conv_band_fixup).  Otherwise
+    // a failed check can only mean corrupted memory: it raises the verdict
+    // word instead, and no fixup pass is launched.
+    bp.fixup = !csc && h->exposed.load() ? 1 : 0;
+    bp.taps = h->taps;
+    bp.taps64 = f64 ? h->taps64 : nullptr;
+    bp.vals64 = f64 ? h->vals64 : nullptr;
+    bp.seg_ok = h->seg_ok;
+    bp.X = static_cast<const float*>(X);
+    bp.ldx = ldx;
+    bp.Y = static_cast<float*>(Y);
+    bp.ldy = ldy;
+    bp.batch = (int)batch;
+    bp.m = (int)g.m;
+    bp.n = (int)g.n;
+    bp.mo = (int)g.mo;
+    bp.no = (int)g.no;
+    bp.tiles_y = (int)((g.no + sh.tw - 1) / sh.tw);
+    bp.tiles = (int)(((g.mo + sh.th - 1) / sh.th) * bp.tiles_y);
+    bp.fast_allowed = band_taps ? 1 : 0;
+    bp.sy = (int)h->sy;
+    bp.nnz = (int)h->nnz;
+    const int cpt = sh.tw / 32, es = f64 ? 8 : 4;
+    bp.y_vec = (ldy % cpt == 0) && (g.no % cpt == 0) && (reinterpret_cast<uintptr_t>(Y) % (es * cpt) == 0) &&
+               (!f64 || reinterpret_cast<uintptr_t>(Y) % 16 == 0);
+    return SPCONV_OK;
+}
+
 int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
              int64_t batch, cudaStream_t st) {
     if (batch == 0) return SPCONV_OK;
@@ -530,74 +604,14 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
     const bool band_geom = h->is_conv && h->band_tw > 0 && tma_ok && (h->row_ptr || csc);
     if (force == kBanded && !band_geom)
         return fail(SPCONV_EINVAL, "SPCONV_B200_PATH=banded: geometry unsupported");
-    // The blocked apply needs finite taps; exact-zero taps (not stored) take
-    // the masked (ZT) instantiations: k <= 7, so the mask fits 64 bits.
-    // (stored = the DOUBLE tap is non-zero when the handle has double taps: a
-    // tap that narrows to 0.0f is still an entry, applied as w = 0)
-    bool taps_finite = !h->host_taps.empty(), any_nz = false;
-    unsigned long long nzmask = 0;
-    for (size_t q = 0; q < h->host_taps.size(); ++q) {
-        taps_finite &= std::isfinite(h->host_taps[q]);
-        const bool stored = h->host_taps64.empty() ? h->host_taps[q] != 0.0f : h->host_taps64[q] != 0.0;
-        if (stored) {
-            any_nz = true;
-            if (q < 64) nzmask |= 1ull << q;
-        }
-    }
-    const bool band_taps = h->taps_dense || (taps_finite && any_nz && g.k <= 7);
+    const bool band_taps = band_taps_ok(h);
     if (band_geom && (force == kBanded || (force == kAuto && band_taps))) {
         const int sms = device_sm_count();
         spb::BandShape sh{};
         spb::BandParams bp{};
-        bp.p = (int)g.p;
-        bp.zt = band_taps && !h->taps_dense ? 1 : 0;
-        bp.nzmask = nzmask;
-        if (bp.zt) {  // W[j] = sum over stored taps (j, i) of #{y : tap i lands in the input}
-            for (int64_t j = 0; j < g.k && j < 8; ++j) {
-                long long wj = 0;
-                for (int64_t i = 0; i < g.k; ++i) {
-                    if (!((nzmask >> (j * g.k + i)) & 1ull)) continue;
-                    // y with 0 <= s*y + i - p < n, y in [0, n_out): a closed range
-                    const int64_t lo = g.p - i <= 0 ? 0 : (g.p - i + g.s - 1) / g.s;
-                    const int64_t hi = g.n + g.p - i - 1 < 0 ? -1 : std::min<int64_t>(g.no - 1, (g.n + g.p - i - 1) / g.s);
-                    wj += std::max<int64_t>(0, hi - lo + 1);
-                }
-                bp.zw[j] = wj;
-            }
-        }
-        CK(spb::launch_band((int)g.k, (int)g.s, bp, nullptr, st, &sh, sms));
-        bp.row_ptr = csc ? h->csc_ptr : h->row_ptr;
-        bp.col_idx = csc ? h->csc_idx : h->col_idx;
-        bp.vals = csc ? h->csc_vals : h->vals;
-        bp.csc = csc ? 1 : 0;
-        bp.tiles_b = h->csc_tiles_b;
-        bp.fail_count = h->fail_flag;
-        // Row-major storage handed out by spconv_csr_device_ptrs may change:
-        // the fused form then recomputes failed segments (conv_band_fixup).
-        // Otherwise a failed check can only mean corrupted memory: it raises
-        // the verdict word instead, and no fixup pass is launched.
-        bp.fixup = !csc && h->exposed.load() ? 1 : 0;
-        bp.taps = h->taps;
-        bp.seg_ok = h->seg_ok;
-        bp.X = X;
-        bp.ldx = ldx;
-        bp.Y = Y;
-        bp.ldy = ldy;
-        bp.batch = (int)batch;
-        bp.m = (int)g.m;
-        bp.n = (int)g.n;
-        bp.mo = (int)g.mo;
-        bp.no = (int)g.no;
-        bp.tiles_y = (int)((g.no + sh.tw - 1) / sh.tw);
-        bp.tiles = (int)(((g.mo + sh.th - 1) / sh.th) * bp.tiles_y);
-        bp.fast_allowed = band_taps ? 1 : 0;
-        bp.sy = (int)h->sy;
-        bp.nnz = (int)h->nnz;
-        const int cpt = sh.tw / 32;
-        bp.y_vec = (ldy % cpt == 0) && (g.no % cpt == 0) &&
-                   (reinterpret_cast<uintptr_t>(Y) % (4 * cpt) == 0);
+        if (int rc = band_setup(h, csc, false, batch, X, ldx, Y, ldy, bp, sh, sms)) return rc;
         CUtensorMap tmap;
-        if (int rc = encode_x_map(&tmap, X, g, ldx, batch, sh.wc, sh.wr, 1)) return rc;
+        if (int rc = encode_x_map(&tmap, X, g, ldx, batch, sh.wc, sh.wr, 1, false)) return rc;
         // When the images dominate by far (matrix < 10 % of the call's bytes),
         // one fused kernel checks the matrix in its producer warps while it
         // applies, plus a fixup pass for failed segments: config 3 384 ->
@@ -1258,10 +1272,11 @@ int spconv_build_transform_f64(int64_t m, int64_t n, int64_t k, int64_t s, int64
     if (rc == SPCONV_OK && e == cudaSuccess && h->layout == 1) {
         e = cudaMallocAsync(&h->csc_vals64, vb, st);
         if (e == cudaSuccess) e = spb::launch_retag(h->csc_vals, h->csc_vals64, h->nnz, d32, d64, st);
-        // the exact taps on the device (the CSC kernels' fp64 checks and sums)
-        if (e == cudaSuccess) e = cudaMallocAsync(&h->taps64, (size_t)kk * 8, st);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(h->taps64, d64, (size_t)kk * 8, cudaMemcpyDeviceToDevice, st);
     }
+    // the exact taps on the device (the fp64 band sums, the CSC kernels' fp64 checks and sums)
+    if (rc == SPCONV_OK && e == cudaSuccess) e = cudaMallocAsync(&h->taps64, (size_t)kk * 8, st);
+    if (rc == SPCONV_OK && e == cudaSuccess)  // (pageable source: staged before the call returns)
+        e = cudaMemcpyAsync(h->taps64, kernel_kxk, (size_t)kk * 8, cudaMemcpyHostToDevice, st);
     // the device taps (band check, CSC rebuilds) become the real fp32 taps
     if (rc == SPCONV_OK && e == cudaSuccess)
         e = need_tables ? cudaMemcpyAsync(h->taps, d32, (size_t)kk * 4, cudaMemcpyDeviceToDevice, st)
@@ -1899,16 +1914,37 @@ int spconv_spmm_f64_threads(const spconv_csr* h, const double* X_dev, int64_t ld
     }
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     auto* hm = const_cast<spconv_csr*>(h);
-    if (csc_native(h)) {
-        if (int rc = csc_sticky(h, "spconv_spmm_f64")) return rc;
-        if (h->exposed.load()) {
-            bool clean = false;
-            if (int rc = csc_exposed_clean(hm, st, true, &clean)) return rc;
-            if (!clean) {
-                hm->last_kernel.store("csc_gather<verify>+csc_repair");
-                return csc_repair_apply(hm, X_dev, ldx, Y_dev, ldy, batch, st, true, chunk);
-            }
+    if (int rc = csc_sticky(h, "spconv_spmm_f64")) return rc;
+    const bool csc = csc_native(h);
+    if (csc && h->exposed.load()) {
+        bool clean = false;
+        if (int rc = csc_exposed_clean(hm, st, true, &clean)) return rc;
+        if (!clean) {
+            hm->last_kernel.store("csc_gather<verify>+csc_repair");
+            return csc_repair_apply(hm, X_dev, ldx, Y_dev, ldy, batch, st, true, chunk);
         }
+    }
+    // Batches of the band geometries: the band check (CSR or CSC storage)
+    // and the register-blocked apply in fp64 (spmm_band.cu, T = double) --
+    // the reference's per-entry multiply and add, in its order.
+    const Geom& g = h->g;
+    const bool tma64 = h->is_conv && g.n % 2 == 0 && ldx % 2 == 0 && reinterpret_cast<uintptr_t>(X_dev) % 16 == 0 &&
+                       encode_fn() != nullptr && g.m < (1ll << 30) && g.n < (1ll << 30);
+    if (chunk == 0 && batch >= 3 && tma64 && h->band_tw > 0 && (h->row_ptr || csc) && band_taps_ok(h) &&
+        path_override() != kGeneric) {
+        const int sms = device_sm_count();
+        spb::BandParams bp;
+        spb::BandShape sh;
+        if (int rc = band_setup(hm, csc, true, batch, X_dev, ldx, Y_dev, ldy, bp, sh, sms, st)) return rc;
+        bp.fused = 0;
+        CUtensorMap tmap;
+        if (int rc = encode_x_map(&tmap, X_dev, g, ldx, batch, sh.wc, sh.wr, 1, true)) return rc;
+        CK(spb::launch_band_check((int)g.k, (int)g.s, bp, st, sms));
+        CK(spb::launch_band64((int)g.k, (int)g.s, bp, &tmap, st, nullptr, sms));
+        hm->last_kernel.store(csc ? "conv_band_check<csc>+conv_spmm_band<f64>" : "conv_band_check+conv_spmm_band<f64>");
+        return SPCONV_OK;
+    }
+    if (csc) {
         spb::CscGatherParams cp = csc_params(h, true);
         cp.X = X_dev;
         cp.ldx = ldx;

@@ -132,6 +132,10 @@ struct BandParams {
     int tiles_b;
     int* fail_count;  // set to 1 when a segment fails and nothing repairs it (the handle's sticky verdict)
     int fixup;        // fused CSR form: launch conv_band_fixup for failed segments (storage handed out)
+    // fp64 apply (spconv_spmm_f64; X / Y then hold doubles): the exact taps and
+    // per-entry values when the handle keeps them (NULL: the fp32 ones widened)
+    const double* taps64;
+    const double* vals64;
 };
 
 // CSC-storage SpMV / SpMM of a conv transform (csc_apply.cu).
@@ -257,6 +261,9 @@ int band_tile_width(int k, int s);
 cudaError_t launch_band(int k, int s, const BandParams& bp, const CUtensorMap* tmap, cudaStream_t st,
                         BandShape* shape, int sms);
 cudaError_t launch_band_check(int k, int s, const BandParams& bp, cudaStream_t st, int sms);
+// The same apply in fp64 (X / Y doubles; the check kernel above runs first).
+cudaError_t launch_band64(int k, int s, const BandParams& bp, const CUtensorMap* tmap, cudaStream_t st,
+                          BandShape* shape, int sms);
 
 cudaError_t render_entries(const int32_t* row_ptr, const int32_t* col_idx, const float* vals,
                            const double* vals64, int rows, unsigned long long* scratch, char* out_dev, unsigned long long base,

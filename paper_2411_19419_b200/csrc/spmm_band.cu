@@ -79,6 +79,11 @@ __device__ __forceinline__ int slides_before(int x, int j, int dim, int s, int p
 }
 
 constexpr int round_up(int v, int m) { return (v + m - 1) / m * m; }
+
+// One stored entry of a row: fp32 fmaf (the device contract) or the
+// reference's fp64 multiply then add, two roundings (inc/sparse.hpp:185-191).
+__device__ __forceinline__ float band_step(float acc, float w, float x) { return fmaf(w, x, acc); }
+__device__ __forceinline__ double band_step(double acc, double w, double x) { return __dadd_rn(acc, __dmul_rn(w, x)); }
 constexpr int cmax(int a, int b) { return a > b ? a : b; }
 
 }  // namespace
@@ -86,22 +91,25 @@ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 // ---------------------------------------------------------------------------
 // Geometry of one instantiation.
 // ---------------------------------------------------------------------------
-template <int K, int S, int V, int CPT, int TH, int STAGES, int DELTA>
+// T: the element type of images and sums (float: the fp32 contract; double:
+// the reference's own arithmetic, spconv_spmm_f64).
+template <int K, int S, int V, int CPT, int TH, int STAGES, int DELTA, typename T = float>
 struct BandCfg {
-    static_assert(S * CPT == 4, "thread columns must start 16-byte aligned in the window");
+    static constexpr int E = 16 / (int)sizeof(T);       // elements per 16-byte vector
+    static_assert((S * CPT) % E == 0, "thread columns must start 16-byte aligned in the window");
     static_assert(TH % V == 0, "TH must be a multiple of V");
     static constexpr int KK = K * K;
     static constexpr int TW = 32 * CPT;                 // output columns per tile
     static constexpr int NX = S * (CPT - 1) + K;        // window columns one thread reads per row
-    static constexpr int NV4 = (DELTA + NX + 3) / 4;    // float4 loads per row
+    static constexpr int NV4 = (DELTA + NX + E - 1) / E;  // 16-byte loads per row
     static constexpr int JJ = S * (V - 1) + K;          // window rows one thread reads
     static constexpr int WR = S * (TH - 1) + K;         // window rows
-    static constexpr int WC = cmax(round_up(S * (TW - 1) + K + DELTA, 4), 4 * 31 + 4 * NV4);
+    static constexpr int WC = cmax(round_up(S * (TW - 1) + K + DELTA, E), S * CPT * 31 + E * NV4);
     static constexpr int WIN = WR * WC;
     static constexpr int CWARPS = TH / V;               // consumer warps
     static constexpr int THREADS = 32 * (CWARPS + 1);   // + one producer warp
-    static constexpr int SF = round_up(WIN, 32);        // floats per stage (128-byte aligned)
-    static constexpr size_t SMEM = 128 + (size_t)STAGES * SF * 4;
+    static constexpr int SF = round_up(WIN, 128 / (int)sizeof(T));  // elements per stage (128-byte aligned)
+    static constexpr size_t SMEM = 128 + (size_t)STAGES * SF * sizeof(T);
     static_assert(WC <= 256 && WR <= 256, "TMA box limit");
     static_assert(TH <= 64, "at most two producer lanes per tile row");
     static_assert(STAGES * 24 <= 128, "barriers + flag masks fit the 128-byte header");
@@ -733,19 +741,23 @@ struct ItemIter {
 // see the header), so they equal the stored-taps sums; a thread whose sums are
 // not all finite (a non-finite x it read, where 0 * inf would differ) redoes
 // its outputs per entry from the CSR.
-template <int K, int S, int V, int CPT, int TH, int STAGES, int DELTA, bool FUSED, bool ZT = false>
-__global__ void __launch_bounds__(BandCfg<K, S, V, CPT, TH, STAGES, DELTA>::THREADS, 1)
+template <int K, int S, int V, int CPT, int TH, int STAGES, int DELTA, bool FUSED, bool ZT = false,
+          typename T = float>
+__global__ void __launch_bounds__(BandCfg<K, S, V, CPT, TH, STAGES, DELTA, T>::THREADS, 1)
     conv_spmm_band(const __grid_constant__ CUtensorMap tmap, const BandParams P) {
-    using C = BandCfg<K, S, V, CPT, TH, STAGES, DELTA>;
+    using C = BandCfg<K, S, V, CPT, TH, STAGES, DELTA, T>;
     using CC = CheckCfg<K, S, C::TW>;
+    constexpr bool F64 = sizeof(T) == 8;
+    static_assert(!FUSED || !F64, "the fp64 apply runs after a separate check");
     static_assert(!FUSED || STAGES * 24 + 16 <= 128, "check barriers fit the 128-byte header");
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
     uint64_t* empty = full + STAGES;
     unsigned long long* s_mask = reinterpret_cast<unsigned long long*>(empty + STAGES);  // per-stage row flags
     uint64_t* cbar = reinterpret_cast<uint64_t*>(s_mask + STAGES);                       // (FUSED) check slices
-    float* xs = reinterpret_cast<float*>(smem + 128);
+    T* xs = reinterpret_cast<T*>(smem + 128);
     __shared__ uint32_t s_w[C::KK];  // taps, runtime-indexed (checks, the CSC per-entry loop)
+    __shared__ T s_wt[C::KK];        // the taps the sums use (fp64: the exact taps)
 
     const int t = threadIdx.x;
     const int lane = t & 31, warp = t >> 5;
@@ -762,7 +774,11 @@ __global__ void __launch_bounds__(BandCfg<K, S, V, CPT, TH, STAGES, DELTA>::THRE
         }
         mbar_fence_init();
     }
-    for (int q = t; q < C::KK; q += blockDim.x) s_w[q] = __float_as_uint(__ldg(P.taps + q));
+    for (int q = t; q < C::KK; q += blockDim.x) {
+        const float t32 = __ldg(P.taps + q);
+        s_w[q] = __float_as_uint(t32);
+        s_wt[q] = F64 && P.taps64 ? (T)__ldg(P.taps64 + q) : (T)t32;
+    }
     __syncthreads();
 
     if (FUSED && warp == C::CWARPS) {
@@ -804,7 +820,7 @@ __global__ void __launch_bounds__(BandCfg<K, S, V, CPT, TH, STAGES, DELTA>::THRE
                 if (lane == 0) {
                     const int wr0 = S * I.tx * TH - P.p;
                     const int wc0 = S * I.ty * C::TW - P.p - DELTA;
-                    mbar_expect_tx(&full[st], (uint32_t)(C::WIN * 4));
+                    mbar_expect_tx(&full[st], (uint32_t)(C::WIN * sizeof(T)));
                     tma_load_3d(xs + (size_t)st * C::SF, &tmap, wc0, wr0, I.img, &full[st]);
                 }
                 __syncwarp();
@@ -863,7 +879,7 @@ __global__ void __launch_bounds__(BandCfg<K, S, V, CPT, TH, STAGES, DELTA>::THRE
                 s_mask[st] = rows_ok;
                 const int wr0 = S * I.tx * TH - P.p;
                 const int wc0 = S * I.ty * C::TW - P.p - DELTA;
-                mbar_expect_tx(&full[st], (uint32_t)(C::WIN * 4));
+                mbar_expect_tx(&full[st], (uint32_t)(C::WIN * sizeof(T)));
                 tma_load_3d(xs + (size_t)st * C::SF, &tmap, wc0, wr0, I.img, &full[st]);
             }
             __syncwarp();
@@ -872,9 +888,9 @@ __global__ void __launch_bounds__(BandCfg<K, S, V, CPT, TH, STAGES, DELTA>::THRE
     }
 
     // ---- consumers ----
-    float w[C::KK];
+    T w[C::KK];
 #pragma unroll
-    for (int q = 0; q < C::KK; ++q) w[q] = __ldg(P.taps + q);
+    for (int q = 0; q < C::KK; ++q) w[q] = s_wt[q];
     const bool vec_ok = P.y_vec != 0;
     constexpr unsigned long long VMASK = (1ull << V) - 1ull;
 
@@ -888,27 +904,33 @@ __global__ void __launch_bounds__(BandCfg<K, S, V, CPT, TH, STAGES, DELTA>::THRE
         // This warp's rows must all lie in verified segments (and the taps be
         // finite and non-zero) for the blocked path.
         const bool fast = FUSED || (P.fast_allowed && ((s_mask[st] >> (warp * V)) & VMASK) == VMASK);
-        const float* xw = xs + (size_t)st * C::SF;
-        float* ybase = P.Y + (long long)img * P.ldy;
+        const T* xw = xs + (size_t)st * C::SF;
+        T* ybase = reinterpret_cast<T*>(P.Y) + (long long)img * P.ldy;
 
         bool per_entry = !fast;
         if (fast) {
-            float acc[V][CPT];
+            T acc[V][CPT];
 #pragma unroll
             for (int v = 0; v < V; ++v)
 #pragma unroll
-                for (int c = 0; c < CPT; ++c) acc[v][c] = 0.0f;
-            const float* xt = xw + (S * warp * V) * C::WC + 4 * lane;
+                for (int c = 0; c < CPT; ++c) acc[v][c] = (T)0;
+            const T* xt = xw + (S * warp * V) * C::WC + S * CPT * lane;
 #pragma unroll
             for (int jj = 0; jj < C::JJ; ++jj) {
-                float xr[4 * C::NV4];
+                T xr[C::E * C::NV4];
 #pragma unroll
                 for (int q = 0; q < C::NV4; ++q) {
-                    const float4 f = *reinterpret_cast<const float4*>(xt + jj * C::WC + 4 * q);
-                    xr[4 * q] = f.x;
-                    xr[4 * q + 1] = f.y;
-                    xr[4 * q + 2] = f.z;
-                    xr[4 * q + 3] = f.w;
+                    if constexpr (F64) {
+                        const double2 f = *reinterpret_cast<const double2*>(xt + jj * C::WC + 2 * q);
+                        xr[2 * q] = f.x;
+                        xr[2 * q + 1] = f.y;
+                    } else {
+                        const float4 f = *reinterpret_cast<const float4*>(xt + jj * C::WC + 4 * q);
+                        xr[4 * q] = f.x;
+                        xr[4 * q + 1] = f.y;
+                        xr[4 * q + 2] = f.z;
+                        xr[4 * q + 3] = f.w;
+                    }
                 }
 #pragma unroll
                 for (int v = 0; v < V; ++v) {
@@ -918,25 +940,35 @@ __global__ void __launch_bounds__(BandCfg<K, S, V, CPT, TH, STAGES, DELTA>::THRE
                         for (int c = 0; c < CPT; ++c)
 #pragma unroll
                             for (int ii = 0; ii < K; ++ii)
-                                acc[v][c] = fmaf(w[j * K + ii], xr[DELTA + S * c + ii], acc[v][c]);
+                                acc[v][c] = band_step(acc[v][c], w[j * K + ii], xr[DELTA + S * c + ii]);
                     }
                 }
             }
             if (ZT) {
-                float nf = 0.0f;  // NaN iff some sum is not finite
+                T nf = (T)0;  // NaN iff some sum is not finite
 #pragma unroll
                 for (int v = 0; v < V; ++v)
 #pragma unroll
-                    for (int c = 0; c < CPT; ++c) nf = fmaf(0.0f, acc[v][c], nf);
-                per_entry = nf != 0.0f;
+                    for (int c = 0; c < CPT; ++c) nf = fma((T)0, acc[v][c], nf);
+                per_entry = nf != (T)0;
             }
             const int ycol = y0 + CPT * lane;
 #pragma unroll
             for (int v = 0; v < V; ++v) {
                 const int x = xb + v;
                 if (per_entry || x >= P.mo) continue;
-                float* yp = ybase + (long long)x * P.no + ycol;
-                if (vec_ok && ycol + CPT <= P.no) {
+                T* yp = ybase + (long long)x * P.no + ycol;
+                if constexpr (F64) {
+                    if (vec_ok && ycol + CPT <= P.no) {
+#pragma unroll
+                        for (int c = 0; c + 1 < CPT; c += 2)
+                            __stcs(reinterpret_cast<double2*>(yp + c), make_double2(acc[v][c], acc[v][c + 1]));
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < CPT; ++c)
+                            if (ycol + c < P.no) __stcs(yp + c, acc[v][c]);
+                    }
+                } else if (vec_ok && ycol + CPT <= P.no) {
                     if (CPT == 4)
                         __stcs(reinterpret_cast<float4*>(yp),
                                make_float4(acc[v][0], acc[v][CPT > 1 ? 1 : 0], acc[v][CPT > 2 ? 2 : 0],
@@ -964,12 +996,12 @@ __global__ void __launch_bounds__(BandCfg<K, S, V, CPT, TH, STAGES, DELTA>::THRE
                     if (y >= P.no) break;
                     int ilo, ihi;
                     tap_range_dev(y, P.n, K, S, P.p, ilo, ihi);
-                    const float* xo = xw + (S * (x - tx * TH)) * C::WC + S * (y - y0) + DELTA;
-                    float acc = 0.0f;
+                    const T* xo = xw + (S * (x - tx * TH)) * C::WC + S * (y - y0) + DELTA;
+                    T acc = (T)0;
                     for (int j = jlo; j < jhi; ++j)
                         for (int ii = ilo; ii < ihi; ++ii)
                             if (!ZT || ((P.nzmask >> (j * K + ii)) & 1ull))
-                                acc = fmaf(__uint_as_float(s_w[j * K + ii]), xo[j * C::WC + ii], acc);
+                                acc = band_step(acc, s_wt[j * K + ii], xo[j * C::WC + ii]);
                     __stcs(ybase + (long long)x * P.no + y, acc);
                 }
             }
@@ -985,7 +1017,7 @@ __global__ void __launch_bounds__(BandCfg<K, S, V, CPT, TH, STAGES, DELTA>::THRE
                     if (y >= P.no) break;
                     const int r = x * P.no + y;
                     const int e1 = __ldg(P.row_ptr + r + 1);
-                    float acc = 0.0f;
+                    T acc = (T)0;
                     for (int e = __ldg(P.row_ptr + r); e < e1; ++e) {
                         const int col = __ldg(P.col_idx + e);
                         if ((unsigned)col >= (unsigned)(P.m * P.n)) __trap();  // not a CSR of this shape
@@ -993,10 +1025,12 @@ __global__ void __launch_bounds__(BandCfg<K, S, V, CPT, TH, STAGES, DELTA>::THRE
                         const int dr = ri - wr0, dc = col - ri * P.n - wc0;
                         // a column outside the staged window (a row that is not a conv
                         // row) is read from the image itself
-                        const float xv = ((unsigned)dr < (unsigned)C::WR && (unsigned)dc < (unsigned)C::WC)
-                                             ? xw[dr * C::WC + dc]
-                                             : __ldg(P.X + (long long)img * P.ldx + col);
-                        acc = fmaf(__ldg(P.vals + e), xv, acc);
+                        const T xv = ((unsigned)dr < (unsigned)C::WR && (unsigned)dc < (unsigned)C::WC)
+                                         ? xw[dr * C::WC + dc]
+                                         : __ldg(reinterpret_cast<const T*>(P.X) + (long long)img * P.ldx + col);
+                        // (fp64: the exact value when the handle keeps one)
+                        const T v = F64 && P.vals64 ? (T)__ldg(P.vals64 + e) : (T)__ldg(P.vals + e);
+                        acc = band_step(acc, v, xv);
                     }
                     __stcs(ybase + r, acc);
                 }
@@ -1139,6 +1173,44 @@ cudaError_t run_delta(int delta, const BandParams& bp, const CUtensorMap* tmap, 
     return run_delta_z<K, S, V, CPT, TH, STAGES, false>(delta, bp, tmap, st, shape, sms);
 }
 
+// fp64 apply (two-kernel form only: the check runs first, as for fp32).
+template <int K, int S, int V, int CPT, int TH, int STAGES, int DELTA, bool ZT>
+cudaError_t run_cfg64(const BandParams& bp, const CUtensorMap* tmap, cudaStream_t st, BandShape* shape, int sms) {
+    using C = BandCfg<K, S, V, CPT, TH, STAGES, DELTA, double>;
+    static_assert(C::SMEM <= 227 * 1024, "fp64 blocking exceeds shared memory");
+    auto kern = conv_spmm_band<K, S, V, CPT, TH, STAGES, DELTA, false, ZT, double>;
+    static std::atomic<int> occ[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!occ[dev & 63]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+        if (e != cudaSuccess) return e;
+        int o = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, C::THREADS, C::SMEM);
+        if (e != cudaSuccess) return e;
+        occ[dev & 63] = std::max(o, 1);
+    }
+    if (shape) {
+        *shape = BandShape{TH, C::TW, C::WR, C::WC, (int)C::SMEM, C::THREADS, occ[dev & 63]};
+        return cudaSuccess;
+    }
+    const long long items = (long long)bp.tiles * bp.batch;
+    const long long grid = std::min<long long>(items, (long long)occ[dev & 63] * sms);
+    kern<<<(unsigned)grid, C::THREADS, C::SMEM, st>>>(*tmap, bp);
+    return cudaGetLastError();
+}
+
+template <int K, int S, int V, int CPT, int TH, int STAGES>
+cudaError_t run_delta64(int delta, const BandParams& bp, const CUtensorMap* tmap, cudaStream_t st, BandShape* shape,
+                        int sms) {
+    const bool zt = !shape && bp.zt;
+    if (delta == 0)
+        return zt ? run_cfg64<K, S, V, CPT, TH, STAGES, 0, true>(bp, tmap, st, shape, sms)
+                  : run_cfg64<K, S, V, CPT, TH, STAGES, 0, false>(bp, tmap, st, shape, sms);
+    return zt ? run_cfg64<K, S, V, CPT, TH, STAGES, 1, true>(bp, tmap, st, shape, sms)
+              : run_cfg64<K, S, V, CPT, TH, STAGES, 1, false>(bp, tmap, st, shape, sms);
+}
+
 template <int K, int S, int TW>
 cudaError_t run_check(const BandParams& bp, cudaStream_t st, int sms) {
     (void)sms;
@@ -1186,6 +1258,19 @@ cudaError_t launch_band(int k, int s, const BandParams& bp, const CUtensorMap* t
     if (k == 3 && s == 2) return run_delta<3, 2, 4, 2, 16, 4>(delta, bp, tmap, st, shape, sms);
     if (k == 5 && s == 2) return run_delta<5, 2, 4, 2, 16, 4>(delta, bp, tmap, st, shape, sms);
     if (k == 7 && s == 2) return run_delta<7, 2, 8, 2, 32, 3>(delta, bp, tmap, st, shape, sms);
+    return cudaErrorInvalidValue;
+}
+
+// fp64 blockings: the tile widths of the fp32 ones (the check's segments), 16-byte
+// double2 window loads, smaller V / TH for the doubled registers and windows.
+cudaError_t launch_band64(int k, int s, const BandParams& bp, const CUtensorMap* tmap, cudaStream_t st,
+                          BandShape* shape, int sms) {
+    const int delta = ((-bp.p) % 2 + 2) % 2;
+    if (k == 3 && s == 1) return run_delta64<3, 1, 8, 4, 32, 4>(delta, bp, tmap, st, shape, sms);
+    if (k == 5 && s == 1) return run_delta64<5, 1, 4, 4, 32, 4>(delta, bp, tmap, st, shape, sms);
+    if (k == 3 && s == 2) return run_delta64<3, 2, 4, 2, 16, 4>(delta, bp, tmap, st, shape, sms);
+    if (k == 5 && s == 2) return run_delta64<5, 2, 4, 2, 16, 4>(delta, bp, tmap, st, shape, sms);
+    if (k == 7 && s == 2) return run_delta64<7, 2, 4, 2, 16, 4>(delta, bp, tmap, st, shape, sms);
     return cudaErrorInvalidValue;
 }
 

@@ -427,6 +427,59 @@ int spconv_reference_host(int mode, int64_t m, int64_t n, int64_t k, int64_t s, 
     return SPCONV_OK;
 }
 
+// The padding-matrix laws for one (m, n, p): bit 0 set when P^T P is not the
+// identity, bit 1 when P vec(A) is not A zero-padded; -1 on a library error.
+static int padding_laws(int64_t m, int64_t n, int64_t p, uint64_t seed, int device, cudaStream_t st) {
+    const int64_t mn = m * n, pr = m + 2 * p, pc = n + 2 * p, rows = pr * pc;
+    spconv_csr *pm = nullptr, *pt = nullptr, *ptp = nullptr;
+    int out = -1;
+    do {
+        if (spconv_build_padding_matrix(m, n, 1, 1, p, 0, device, st, &pm) != SPCONV_OK) break;
+        int64_t r = 0, c = 0, z = 0;
+        spconv_csr_shape(pm, &r, &c, &z);
+        std::vector<int64_t> ptr((size_t)r + 1), idx((size_t)std::max<int64_t>(z, 1));
+        std::vector<double> val((size_t)std::max<int64_t>(z, 1));
+        if (spconv_csr_export(pm, ptr.data(), idx.data(), val.data()) != SPCONV_OK) break;
+        // transposed (inc/sparse.hpp:276-282): the swapped entries, compiled on the device
+        std::vector<int64_t> tr((size_t)std::max<int64_t>(z, 1)), tc((size_t)std::max<int64_t>(z, 1));
+        for (int64_t i = 0; i < r; ++i)
+            for (int64_t e = ptr[(size_t)i]; e < ptr[(size_t)i + 1]; ++e) tr[(size_t)e] = idx[(size_t)e], tc[(size_t)e] = i;
+        if (spconv_matrix_from_coo(c, r, z, tr.data(), tc.data(), val.data(), 0, device, st, &pt) != SPCONV_OK) break;
+        if (spconv_spgemm(pt, pm, 0, st, &ptp) != SPCONV_OK) break;
+        int64_t r2 = 0, c2 = 0, z2 = 0;
+        spconv_csr_shape(ptp, &r2, &c2, &z2);
+        bool identity = r2 == mn && c2 == mn && z2 == mn;
+        if (identity) {
+            std::vector<int64_t> p2((size_t)r2 + 1), i2((size_t)std::max<int64_t>(z2, 1));
+            std::vector<double> v2((size_t)std::max<int64_t>(z2, 1));
+            if (spconv_csr_export(ptp, p2.data(), i2.data(), v2.data()) != SPCONV_OK) break;
+            for (int64_t i = 0; i < r2 && identity; ++i)
+                for (int64_t e = p2[(size_t)i]; e < p2[(size_t)i + 1]; ++e)
+                    identity &= i2[(size_t)e] == i && v2[(size_t)e] == 1.0;
+        }
+        // P vec(A) (random_normal_grid(m, n, seed)) against A zero-padded
+        const std::vector<double> a = normals(seed, mn);
+        DevBuf da, dy;
+        if (da.reserve((size_t)mn * 8) != cudaSuccess || dy.reserve((size_t)rows * 8) != cudaSuccess) break;
+        std::vector<double> y((size_t)rows);
+        if (cudaMemcpy(da.p, a.data(), (size_t)mn * 8, cudaMemcpyHostToDevice) != cudaSuccess) break;
+        if (spconv_spmm_f64(pm, (const double*)da.p, mn, (double*)dy.p, rows, 1, st) != SPCONV_OK) break;
+        if (cudaMemcpy(y.data(), dy.p, (size_t)rows * 8, cudaMemcpyDeviceToHost) != cudaSuccess) break;
+        bool pad_ok = true;
+        for (int64_t rr = 0; rr < pr && pad_ok; ++rr)
+            for (int64_t cc = 0; cc < pc && pad_ok; ++cc) {
+                const bool inside = rr >= p && rr < p + m && cc >= p && cc < p + n;
+                const double want = inside ? a[(size_t)((rr - p) * n + (cc - p))] : 0.0;
+                pad_ok = y[(size_t)(rr * pc + cc)] == want;
+            }
+        out = (identity ? 0 : 1) | (pad_ok ? 0 : 2);
+    } while (false);
+    spconv_csr_free(ptp);
+    spconv_csr_free(pt);
+    spconv_csr_free(pm);
+    return out;
+}
+
 int spconv_run_verification(int64_t max_dim, int seeds, uint64_t base_seed, int device, int64_t counts[4],
                             double devs[3], char* failures, int64_t cap) {
     if (!counts || !devs) return spb_fail(SPCONV_EINVAL, "spconv_run_verification: null argument");
@@ -483,10 +536,23 @@ int spconv_run_verification(int64_t max_dim, int seeds, uint64_t base_seed, int 
                             }
                             if (any0) ++clipped;
                         }
-                        // The padding-matrix laws (inc/verify.hpp:84-112) concern P, which the
-                        // device build never materialises; their input draw is consumed so the
-                        // conv cases below see the reference's seeds.
-                        if (k == 1 && s == 1) ++case_index;
+                        // Padding-matrix laws, which depend only on (m, n, p)
+                        // (inc/verify.hpp:96-122): P built on the device, P^T by a
+                        // device compile of the swapped entries, P^T P by the device
+                        // spgemm -- the identity; P vec(A) by the fp64 SpMV -- A
+                        // zero-padded, exactly.
+                        if (k == 1 && s == 1) {
+                            const uint64_t pseed = derive_seed(base_seed, case_index++);
+                            const int plaw = padding_laws(m, n, p, pseed, device, st);
+                            if (plaw < 0) {
+                                rc = SPCONV_ECUDA;
+                                stop = true;
+                                break;
+                            }
+                            if (plaw & 1) fail("PtP != identity for " + ss);
+                            if (plaw & 2) fail("P*vec(A) != zero-padded A for " + ss);
+                            if (fails.size() >= max_failures) stop = true;
+                        }
                         for (int sd = 0; sd < seeds && !stop; ++sd) {
                             const uint64_t cs = derive_seed(base_seed, case_index++);
                             const std::vector<double> a64 = normals(cs, mn);
