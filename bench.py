@@ -581,7 +581,39 @@ def secondary_single(sp, torch, dev, stream, steps, peak):
                 layout="csc (col_ptr / row_idx / vals only)")
     out["config3_csc"] = line
     tc.close()
-    del X, Y, Xh
+    del X, Y
+    # ---- config 3 in the reference's own arithmetic (fp64 images, per-entry
+    # double multiply then add: spconv_spmm_f64, bit-identical to the
+    # reference's convolve()); bytes 8 nnz + 4 (rows + 1) + 8 b (cols + rows)
+    # (the check streams col_idx + fp32 vals; the exact taps are applied)
+    t64 = sp.build_transform(sp.Kernel(k, kern32.astype(np.float64)), sp.ConvSpec(m, n, k, s, p),
+                             device=dev.index, stream=stream)
+    X64 = Xh.to(dev).double()
+    Y64 = torch.empty(256, t64.rows, device=dev, dtype=torch.float64)
+    alg = 8 * t64.nnz + 4 * (t64.rows + 1) + 8 * 256 * (t64.cols + t64.rows)
+    line = device_line(sp, torch, t64, X64, Y64, 256, steps, dev, stream, peak, alg=alg,
+                       fn=lambda: sp.spmm_f64(t64, X64, Y64, stream=stream))
+    line["kernel"] = t64.last_kernel
+    from oracle import Oracle
+    orc = Oracle()
+    ptr, idx, val = orc.build_transform(m, n, k, s, p, kern32.astype(np.float64))
+    same = all(np.array_equal(Y64[i].cpu().numpy().view(np.uint64),
+                              orc.spmv_f64(ptr, idx, val, X64[i].cpu().numpy()).view(np.uint64))
+               for i in slice_probe(256))
+    # e2e: the drop-in call shape (fp64 host buffers through spconv_convolve_host_f64)
+    Xh64 = Xh.double().pin_memory()
+    Yh64 = torch.empty(256, t64.rows, dtype=torch.float64).pin_memory()
+    sp.convolve_batch_f64(t64, Xh64, Yh64)
+    h0 = time.perf_counter()
+    sp.convolve_batch_f64(t64, Xh64, Yh64)
+    e2e_ms = (time.perf_counter() - h0) * 1e3
+    line.update(parity="bitexact (vs the fp64 restatement of spmv_csr_rows)" if same else "MISMATCH",
+                dtype="f64", e2e={"value": 256 * t64.nnz / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "ms": e2e_ms,
+                                  "h2d_bytes_per_step": 8 * 256 * t64.cols, "d2h_bytes_per_step": 8 * 256 * t64.rows,
+                                  "path": "spconv_convolve_host_f64 (C ABI), pinned fp64 host buffers"})
+    out["config3_f64"] = line
+    t64.close()
+    del X64, Y64, Xh64, Yh64, Xh
     # ---- config 4: the per-rank slice at N = 8 (8 images) ----
     cfg = CONFIGS[4]
     m, n, k, s, p = cfg["spec"]

@@ -22,7 +22,7 @@ import numpy as np
 
 __all__ = [
     "ConvSpec", "Kernel", "Transform", "build_transform", "convolve", "convolve_batch",
-    "spmv", "spmm", "spmm_f64", "nnz_bound", "read_transform", "relayout", "Layout", "layout_name",
+    "spmv", "spmm", "spmm_f64", "convolve_batch_f64", "nnz_bound", "read_transform", "relayout", "Layout", "layout_name",
     "layout_from_name", "derive_seed", "random_normal", "set_option", "get_option", "options", "direct_conv", "im2col_conv", "run_verification", "library_path", "lib",
 ]
 
@@ -484,6 +484,28 @@ def convolve_batch(t: Transform, X_host, Y_host=None):
     if n != batch * t.cols:
         raise ValueError(f"convolve_batch: expected {batch}x{t.cols} input values, got {n}")
     _check(lib.spconv_convolve_host(t._h, _ptr(X_host), _ptr(Y_host), batch))
+    return Y_host
+
+
+def convolve_batch_f64(t: Transform, X_host, Y_host=None, threads: int = 1):
+    """The reference-semantics apply on HOST fp64 buffers [batch, cols] ->
+    [batch, rows] (spconv_convolve_host_f64_threads): bit-identical to the
+    reference's convolve() / spmv(m, x, threads) of every image."""
+    if isinstance(X_host, np.ndarray):
+        X_host = np.ascontiguousarray(X_host, np.float64)
+        batch = X_host.shape[0] if X_host.ndim == 2 else 1
+        if Y_host is None:
+            Y_host = np.empty((batch, t.rows), np.float64)
+    else:  # torch CPU tensor
+        import torch
+        assert X_host.device.type == "cpu" and X_host.dtype == torch.float64 and X_host.is_contiguous()
+        batch = X_host.shape[0] if X_host.dim() == 2 else 1
+        if Y_host is None:
+            Y_host = torch.empty(batch, t.rows, dtype=torch.float64, pin_memory=X_host.is_pinned())
+    n = X_host.size if isinstance(X_host, np.ndarray) else X_host.numel()
+    if n != batch * t.cols:
+        raise ValueError(f"convolve_batch_f64: expected {batch}x{t.cols} input values, got {n}")
+    _check(lib.spconv_convolve_host_f64_threads(t._h, _ptr(X_host), _ptr(Y_host), batch, int(threads)))
     return Y_host
 
 

@@ -584,13 +584,24 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
             // the previous kernel on the stream finishes -- never behind this
             // handle's own build, whose writes are only visible at its end.
             sp.pdl = h->applied.exchange(true) ? 1 : 0;
+            sp.X = X;
+            // The windowed kernel (one round trip) wins on matrices that arrive
+            // from HBM -- config 2 cold: 12.3 -> 10.2 us; on small, L2-resident
+            // transforms chained in a graph the bulk-staged kernel, which
+            // prefetches the matrix under the previous kernel (PDL), is faster
+            // (config 2 warm 3.0 vs 4.3 us; DenseNet layers 1.0-2.5 vs 1.7-4.7 us;
+            // scripts/probe_spmv.py).  So: the window from 8 MB of matrix up.
+            // Option stage=lanes / bulk forces either kernel.
+            const int stage = spb::opt(spb::kOptStage);
+            const bool big = 8.0 * (double)h->nnz >= 8.0 * (1 << 20);
+            const bool win = spec && spb::spmv_win_ok(sp) && (stage == 2 || (stage == 0 && big));
             for (int64_t b0 = 0; b0 < batch; b0 += 2) {  // <= 2 images per launch
                 sp.X = X + b0 * ldx;
                 sp.Y = Y + b0 * ldy;
                 sp.batch = (int)std::min<int64_t>(2, batch - b0);
-                CK(spb::launch_spmv_warp(sp, h->k2max, spec, st));
+                CK(win ? spb::launch_spmv_win(sp, h->k2max, st) : spb::launch_spmv_warp(sp, h->k2max, spec, st));
             }
-            h->last_kernel.store(spec ? "csr_spmv_bulk<spec>" : "csr_spmv_bulk");
+            h->last_kernel.store(win ? "conv_spmv_win" : spec ? "csr_spmv_bulk<spec>" : "csr_spmv_bulk");
             return SPCONV_OK;
         }
         spb::GenericParams gp{h->row_ptr, h->col_idx, h->vals, X, ldx, Y, ldy, (int)h->rows,

@@ -19,7 +19,7 @@ enum Opt {
     kOptGeneric,       // 0 row-block multi-vector kernel, 1 thread per row
     kOptBuild,         // 0 auto, 1 block, 2 warp, 3 persist
     kOptBulkStoreOff,  // 0 bulk (TMA) stores of staged entries, 1 per-thread 16-byte stores
-    kOptStage,         // 0 per-lane 16-byte staging (latency SpMV), 1 bulk copies
+    kOptStage,         // latency SpMV: 0 auto (window kernel from 8 MB of matrix), 1 bulk-staged, 2 window
     kOptSpecSkew,      // test hook: offsets the latency SpMV's predicted row starts
     kOptCount
 };
@@ -255,6 +255,9 @@ cudaError_t launch_retag(float* vals, double* vals64, int64_t nnz, const float* 
                          cudaStream_t st);
 cudaError_t launch_spmv_unrolled(const GenericParams& gp, int kmax, cudaStream_t st);
 cudaError_t launch_spmv_warp(const SpecParams& sp, int kmax, bool spec, cudaStream_t st);
+// One-round-trip latency SpMV of conv transforms (matrix run + input window together).
+bool spmv_win_ok(const SpecParams& sp);
+cudaError_t launch_spmv_win(const SpecParams& sp, int kmax, cudaStream_t st);
 
 bool band_supported(int k, int s);
 int band_tile_width(int k, int s);

@@ -29,7 +29,7 @@ const OptSpec kSpecs[] = {
     {"generic", kOptGeneric, {"rowblock", "plain", nullptr}},
     {"build", kOptBuild, {"auto", "block", "warp", "persist", nullptr}},
     {"bulk_store", kOptBulkStoreOff, {"1", "0", nullptr}},
-    {"stage", kOptStage, {"lanes", "bulk", nullptr}},
+    {"stage", kOptStage, {"auto", "bulk", "window", nullptr}},
     {"spec_skew", kOptSpecSkew, {nullptr}},
 };
 

@@ -440,6 +440,204 @@ __global__ void __launch_bounds__(128) csr_spmv_bulk(const SpecParams P) {
     }
 }
 
+// Windowed latency SpMV (conv transforms, batch <= 2): ONE memory round trip.
+// csr_spmv_bulk stages a warp's matrix run, then gathers x through the staged
+// columns -- two dependent trips.  Here every lane issues cp.async 16-byte
+// copies of its share of the warp's row_ptr / (col, val) run (closed-form
+// bounds) AND of the input window the warp's 32 outputs read: k input rows x
+// (31 s + k) columns per image, addresses closed-form too -- all in flight
+// together.  Each lane then walks its row from shared memory: an entry whose
+// column lies in the window reads x there, any other (a matrix that is not its
+// geometry's transform) reads x from global memory, so the sums are the
+// per-entry ordered fmaf chain whatever the matrix holds.  Under programmatic
+// dependent launch the matrix copies leave before griddepcontrol.wait, the
+// window copies right after it.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
+template <int K, int S>
+struct WinCfg {
+    static constexpr int KK = K * K;
+    static constexpr int RUN = 32 * KK;                   // max entries of a 32-row run
+    static constexpr int BUFW = (RUN + 3 + 3) / 4 * 4;
+    static constexpr int RPW = 40;
+    static constexpr int WC = (S * 31 + K + 3 + 3) / 4 * 4;  // window columns (+ 16-byte alignment slack)
+    static constexpr int WINF = 2 * K * WC;                   // two images
+    static constexpr int WARPS = 4;
+    static constexpr size_t WARP_BYTES = (size_t)(RPW + 2 * BUFW + WINF) * 4;
+    static constexpr size_t SMEM = 128 + WARPS * WARP_BYTES;
+};
+
+template <int K, int S>
+__global__ void __launch_bounds__(128) conv_spmv_win(const SpecParams P) {
+    using W = WinCfg<K, S>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int r0 = (blockIdx.x * W::WARPS + warp) * 32;
+    if (r0 >= P.rows) return;  // warp-uniform; no block-wide barrier follows
+    const int nr = min(32, P.rows - r0);
+    int* rp = reinterpret_cast<int*>(smem + 128 + (size_t)warp * W::WARP_BYTES);
+    int* cb = rp + W::RPW;
+    float* vb = reinterpret_cast<float*>(cb + W::BUFW);
+    float* win = vb + W::BUFW;
+
+    int E0, E1;
+    conv_run_bounds(P, r0, r0 + nr, E0, E1);
+    const bool issue = E0 >= 0 && E1 >= E0 && E1 - E0 <= W::RUN && E1 <= P.nnz;
+    const int rbase = r0 & ~3;
+    const int rq = (r0 + nr + 1 - rbase + 3) >> 2;
+    const int ebase = E0 & ~3;
+    const int nv = issue && E1 > E0 ? (E1 - ebase + 3) >> 2 : 0;
+    // the matrix run: 16-byte loads into registers (all in flight), stored
+    // to shared memory once they land (below)
+    constexpr int NV = (W::BUFW / 4 + 31) / 32;
+    int4 cr[NV], vr[NV];
+#pragma unroll
+    for (int u = 0; u < NV; ++u) {
+        const int q = lane + 32 * u;
+        if (q < nv) {
+            cr[u] = __ldg(reinterpret_cast<const int4*>(P.col_idx + ebase) + q);
+            vr[u] = __ldg(reinterpret_cast<const int4*>(P.vals + ebase) + q);
+        }
+    }
+    const int4 rr = lane < rq ? __ldg(reinterpret_cast<const int4*>(P.row_ptr + rbase) + lane) : make_int4(0, 0, 0, 0);
+    // the input window of the warp's first output-row segment: K input rows
+    const int x = r0 / P.no, y0 = r0 - x * P.no;
+    const int wa0 = S * x - P.p;                          // input row of tap row 0
+    const int c0 = max(S * y0 - P.p, 0) & ~3;             // first window column (16-byte aligned)
+    const int c1 = min(S * (y0 + 31) + K - 1 - P.p, P.n - 1);
+    const int nq = c1 >= c0 ? min((c1 - c0) / 4 + 1, W::WC / 4) : 0;  // 16-byte units per row
+    // x may be the previous kernel's output: the window copies wait for it.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    for (int bi = 0; bi < P.batch; ++bi) {
+        const float* Xb = P.X + (int64_t)bi * P.ldx + c0;
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            const int a = wa0 + j;
+            if (a >= 0 && a < P.m)
+                for (int q = lane; q < nq; q += 32)
+                    cp_async16(win + (bi * K + j) * W::WC + 4 * q, Xb + (int64_t)a * P.n + 4 * q);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < NV; ++u) {
+        const int q = lane + 32 * u;
+        if (q < nv) {
+            reinterpret_cast<int4*>(cb)[q] = cr[u];
+            reinterpret_cast<int4*>(vb)[q] = vr[u];
+        }
+    }
+    if (lane < rq) reinterpret_cast<int4*>(rp)[lane] = rr;
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncwarp();
+    const int* rps = rp + (r0 & 3);
+    const bool hit = issue && rps[0] == E0 && rps[nr] == E1;
+    if (lane >= nr) return;
+    const int y = y0 + lane;
+    int a0, cnt;
+    const int* cs;
+    const float* vs;
+    if (hit) {
+        a0 = rps[lane];
+        cnt = rps[lane + 1] - a0;
+        cs = cb + (a0 - ebase);
+        vs = vb + (a0 - ebase);
+    } else {
+        a0 = __ldg(P.row_ptr + r0 + lane);
+        cnt = __ldg(P.row_ptr + r0 + lane + 1) - a0;
+        cs = P.col_idx + a0;
+        vs = P.vals + a0;
+    }
+    // A row of this warp's output-row segment whose K x K taps all land reads
+    // its entries' x from the window when their columns are the pattern's.
+    const bool full = hit && y < P.no && cnt == W::KK && S * x - P.p >= 0 && S * x - P.p + K <= P.m &&
+                      S * y - P.p >= 0 && S * y - P.p + K <= P.n;
+    const int colb = (S * x - P.p) * P.n + (S * y - P.p);   // column of tap (0, 0)
+    const int wcol = S * y - P.p - c0;                       // its window column
+    for (int bi = 0; bi < P.batch; ++bi) {
+        const float* X = P.X + (int64_t)bi * P.ldx;
+        const float* wb = win + bi * K * W::WC;
+        float acc = 0.0f;
+        if (full) {
+            float xv[W::KK], vv[W::KK];
+            bool pat = true;
+#pragma unroll
+            for (int q = 0; q < W::KK; ++q) {
+                const int j = q / K, i = q % K;
+                const int c = cs[q];
+                pat &= c == colb + j * P.n + i;
+                vv[q] = vs[q];
+                xv[q] = wb[j * W::WC + wcol + i];
+            }
+            if (pat) {
+#pragma unroll
+                for (int q = 0; q < W::KK; ++q) acc = fmaf(vv[q], xv[q], acc);
+            } else {
+                for (int q = 0; q < W::KK; ++q) acc = fmaf(vv[q], __ldg(X + cs[q]), acc);
+            }
+        } else {
+            for (int q = 0; q < cnt; ++q) acc = fmaf(vs[q], __ldg(X + cs[q]), acc);
+        }
+        P.Y[(int64_t)bi * P.ldy + r0 + lane] = acc;
+    }
+}
+
+template <int K, int S>
+static cudaError_t launch_win_ks(const SpecParams& sp, cudaStream_t st) {
+    using W = WinCfg<K, S>;
+    static std::atomic<bool> attr_set[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!attr_set[dev & 63]) {
+        cudaError_t e = cudaFuncSetAttribute(conv_spmv_win<K, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)W::SMEM);
+        if (e != cudaSuccess) return e;
+        attr_set[dev & 63] = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)((sp.rows + 32 * W::WARPS - 1) / (32 * W::WARPS)));
+    cfg.blockDim = dim3(32 * W::WARPS);
+    cfg.dynamicSmemBytes = W::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = sp.pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, conv_spmv_win<K, S>, sp);
+}
+
+// The windowed kernel: conv transforms (closed-form runs) of the instantiated
+// (k, s) -- the BASELINE and DenseNet121 geometries -- whose window rows are
+// 16-byte aligned (n, ldx multiples of 4, X aligned).
+bool spmv_win_ok(const SpecParams& sp) {
+    const bool ks = (sp.s == 1 && (sp.k == 1 || sp.k == 3 || sp.k == 5 || sp.k == 7)) ||
+                    (sp.s == 2 && (sp.k == 2 || sp.k == 3 || sp.k == 5 || sp.k == 7));
+    return ks && sp.n % 4 == 0 && sp.ldx % 4 == 0 && reinterpret_cast<uintptr_t>(sp.X) % 16 == 0;
+}
+
+cudaError_t launch_spmv_win(const SpecParams& sp, int kmax, cudaStream_t st) {
+    (void)kmax;
+    if (sp.batch < 1 || sp.batch > 2 || !spmv_win_ok(sp)) return cudaErrorInvalidValue;
+    if (sp.s == 1) {
+        switch (sp.k) {
+            case 1: return launch_win_ks<1, 1>(sp, st);
+            case 3: return launch_win_ks<3, 1>(sp, st);
+            case 5: return launch_win_ks<5, 1>(sp, st);
+            case 7: return launch_win_ks<7, 1>(sp, st);
+        }
+    } else {
+        switch (sp.k) {
+            case 2: return launch_win_ks<2, 2>(sp, st);
+            case 3: return launch_win_ks<3, 2>(sp, st);
+            case 5: return launch_win_ks<5, 2>(sp, st);
+            case 7: return launch_win_ks<7, 2>(sp, st);
+        }
+    }
+    return cudaErrorInvalidValue;
+}
+
 template <int KMAX>
 static cudaError_t launch_bulk_k(const SpecParams& sp, bool spec, cudaStream_t st) {
     using C = BulkCfg<KMAX>;

@@ -76,3 +76,8 @@ def golden_cases(orc, js):
 BAND_KERNELS = ("conv_band_check+conv_spmm_band", "conv_spmm_band<fused>", "conv_spmm_band<fused>+conv_band_fixup")
 # ... and over CSC storage (the CSC band check; no fixup pass)
 CSC_BAND_KERNELS = ("conv_band_check<csc>+conv_spmm_band", "conv_spmm_band<fused,csc>")
+
+# The latency SpMV of conv transforms (batch <= 2): one round trip with the
+# input window staged beside the matrix run, or the bulk-staged kernel
+# (options stage=window / bulk; auto picks by matrix size and eligibility).
+LATENCY_SPEC = ("conv_spmv_win", "csr_spmv_bulk<spec>")

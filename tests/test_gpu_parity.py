@@ -13,7 +13,7 @@ import os
 import numpy as np
 import pytest
 
-from helpers import CONFIGS, golden_cases, problem, sha, sweep_specs, zero_tap_kernel, BAND_KERNELS
+from helpers import LATENCY_SPEC, CONFIGS, golden_cases, problem, sha, sweep_specs, zero_tap_kernel, BAND_KERNELS
 
 pytestmark = pytest.mark.gpu
 
@@ -434,18 +434,20 @@ def test_band_concurrent_streams(sp, orc, torch_cuda, fused, opts):
         assert np.array_equal(bits(Y.cpu().numpy()), bits(want))
 
 
+@pytest.mark.parametrize("stage", ["window", "bulk"])
 @pytest.mark.parametrize("skew", [1, -1, 3])
-def test_spmv_spec_mispredicted_rows(sp, orc, torch_cuda, skew):
+def test_spmv_spec_mispredicted_rows(sp, orc, torch_cuda, skew, stage):
     """The latency SpMV's closed-form run prediction never decides the result:
     with the predicted run bounds deliberately skewed (test hook), every warp
-    takes the reload path and the output is still bit-exact."""
+    takes the reload path and the output is still bit-exact (the windowed
+    kernel and the bulk-staged one)."""
     spec = (64, 48, 5, 2, 2)
     kern, X = problem(orc, 13, 64, 48, 5, batch=2)
     t = build(sp, spec, kern)
     want = orc.spmm_native(*orc.build_native(*spec, kern), X)
-    with sp.options(spec_skew=skew):
+    with sp.options(spec_skew=skew, stage=stage):
         Y = run_spmm(torch_cuda, sp, t, X)
-    assert t.last_kernel == "csr_spmv_bulk<spec>"
+    assert t.last_kernel == ("conv_spmv_win" if stage == "window" else "csr_spmv_bulk<spec>")
     assert np.array_equal(bits(Y), bits(want))
 
 
@@ -528,7 +530,7 @@ def test_build_variants_bitexact(sp, orc, variant, bulk_store, opts):
                 assert np.array_equal(got[2].view(np.uint64), want[2].view(np.uint64))
 
 
-@pytest.mark.parametrize("stage", ["bulk", "lanes"])
+@pytest.mark.parametrize("stage", ["bulk", "window", "auto"])
 def test_latency_spmv_staging_variants(sp, orc, torch_cuda, stage, opts):
     """Both stagings of the latency SpMV (bulk copies / per-lane 16-byte
     loads, option stage), dense-tap (closed-form run) and zero-tap
@@ -547,7 +549,7 @@ def test_latency_spmv_staging_variants(sp, orc, torch_cuda, stage, opts):
                 want = orc.spmm_native(*orc.build_native(*spec, kv), X)
                 for b in (1, 2):
                     Y = run_spmm(torch_cuda, sp, t, X[:b])
-                    assert t.last_kernel.startswith("csr_spmv_bulk")
+                    assert t.last_kernel in LATENCY_SPEC
                     assert np.array_equal(bits(Y), bits(want[:b])), (spec, zero, b)
 
 
