@@ -330,6 +330,11 @@ const char* spconv_csr_last_kernel(const spconv_csr* h);
  * for a handle without band geometry. */
 int spconv_band_check_status(const spconv_csr* h, int64_t* segments, int64_t* failed);
 
+/* The per-segment verdicts themselves (1 = the segment's stored entries are
+ * the transform's), in segment order: output row x, then column segment
+ * (CSR), or input row, then column segment (CSC); *n = the segment count. */
+int spconv_band_check_flags(const spconv_csr* h, uint8_t* out, int64_t cap, int64_t* n);
+
 /* Frees the handle and its device memory (synchronises its device). */
 int spconv_csr_free(spconv_csr* h);
 

@@ -65,6 +65,7 @@ _decl("spconv_convolve_host", [_vp, _vp, _vp, _i64])
 _decl("spconv_convolve_host_f64", [_vp, _vp, _vp, _i64])
 _decl("spconv_spmm_f64", [_vp, _vp, _i64, _vp, _i64, _i64, _vp])
 _decl("spconv_csr_storage_bytes", [_vp, _P(_i64)])
+_decl("spconv_band_check_flags", [_vp, _vp, _i64, _P(_i64)])
 _decl("spconv_spmm_f64_threads", [_vp, _vp, _i64, _vp, _i64, _i64, C.c_int, _vp])
 _decl("spconv_convolve_host_f64_threads", [_vp, _vp, _vp, _i64, C.c_int])
 _decl("spconv_csr_last_kernel", [_vp], C.c_char_p)
@@ -327,6 +328,14 @@ class Transform:
         a, b = _i64(), _i64()
         _check(lib.spconv_band_check_status(self._h, C.byref(a), C.byref(b)))
         return a.value, b.value
+
+    def band_check_flags(self) -> np.ndarray:
+        """Per-segment verdicts of the last band check (spconv_band_check_flags)."""
+        n = _i64()
+        _check(lib.spconv_band_check_flags(self._h, None, 0, C.byref(n)))
+        out = np.empty(max(n.value, 1), np.uint8)
+        _check(lib.spconv_band_check_flags(self._h, out.ctypes.data, out.size, C.byref(n)))
+        return out[: n.value]
 
     def close(self) -> None:
         if self._h and self._h.value:

@@ -483,6 +483,14 @@ int band_setup(spconv_csr* h, bool csc, bool f64, int64_t batch, const void* X, 
     bp.no = (int)g.no;
     bp.tiles_y = (int)((g.no + sh.tw - 1) / sh.tw);
     bp.tiles = (int)(((g.mo + sh.th - 1) / sh.th) * bp.tiles_y);
+    bp.seg_div = spb::band_seg_div((int)g.k, (int)g.s);
+    const int segw = sh.tw / bp.seg_div;
+    bp.tiles_y_chk = (int)((g.no + segw - 1) / segw);
+    // X rows TMA cannot describe (pitch not a multiple of 16 bytes, misaligned
+    // base): the producer stages windows with cp.async element copies
+    const int64_t eb = f64 ? 8 : 4;
+    bp.notma = !((g.n * eb) % 16 == 0 && (ldx * eb) % 16 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0 &&
+                 encode_fn() != nullptr && g.m < (1ll << 30) && g.n < (1ll << 30)) ? 1 : 0;
     bp.fast_allowed = band_taps ? 1 : 0;
     bp.sy = (int)h->sy;
     bp.nnz = (int)h->nnz;
@@ -516,7 +524,7 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
         }
         bool finite = true, any = false;
         for (size_t q = 0; q < h->host_taps.size(); ++q) finite &= std::isfinite(h->host_taps[q]), any |= tap_stored(h, q);
-        const bool band = h->band_tw > 0 && tma_ok && (h->taps_dense || (finite && any && g.k <= 7));
+        const bool band = h->band_tw > 0 && (h->taps_dense || (finite && any && g.k <= 7));
         if (force == kBanded && !band) return fail(SPCONV_EINVAL, "path=banded: geometry unsupported");
         if (!(band && (force == kBanded || (force == kAuto && batch >= 3)))) {
             spb::CscGatherParams cp = csc_params(h, false);
@@ -612,7 +620,7 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
     }
 
     // ---- band path: CSR band check + register-blocked apply ----
-    const bool band_geom = h->is_conv && h->band_tw > 0 && tma_ok && (h->row_ptr || csc);
+    const bool band_geom = h->is_conv && h->band_tw > 0 && (h->row_ptr || csc);
     if (force == kBanded && !band_geom)
         return fail(SPCONV_EINVAL, "SPCONV_B200_PATH=banded: geometry unsupported");
     const bool band_taps = band_taps_ok(h);
@@ -622,7 +630,9 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
         spb::BandParams bp{};
         if (int rc = band_setup(h, csc, false, batch, X, ldx, Y, ldy, bp, sh, sms)) return rc;
         CUtensorMap tmap;
-        if (int rc = encode_x_map(&tmap, X, g, ldx, batch, sh.wc, sh.wr, 1, false)) return rc;
+        std::memset(&tmap, 0, sizeof tmap);
+        if (!bp.notma)
+            if (int rc = encode_x_map(&tmap, X, g, ldx, batch, sh.wc, sh.wr, 1, false)) return rc;
         // When the images dominate by far (matrix < 10 % of the call's bytes),
         // one fused kernel checks the matrix in its producer warps while it
         // applies, plus a fixup pass for failed segments: config 3 384 ->
@@ -636,8 +646,9 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
         // the matrix the stream order gives it.
         const int fsel = spb::opt(spb::kOptFused);
         const bool light = 8.0 * (double)h->nnz < 0.1 * 4.0 * (double)batch * (double)(h->rows + h->cols);
-        bp.fused = band_taps && (fsel ? fsel == 2 : light && !bp.zt) ? 1 : 0;
+        bp.fused = band_taps && bp.seg_div == 1 && (fsel ? fsel == 2 : light && !bp.zt) ? 1 : 0;
         if (bp.fused) {
+            h->checked.store(true);
             const cudaError_t fe = spb::launch_band((int)g.k, (int)g.s, bp, &tmap, st, nullptr, sms);
             if (fe == cudaSuccess) {
                 h->last_kernel.store(csc          ? "conv_spmm_band<fused,csc>"
@@ -649,6 +660,7 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
             cudaGetLastError();
             bp.fused = 0;  // this blocking has no fused instantiation
         }
+        h->checked.store(true);
         CK(spb::launch_band_check((int)g.k, (int)g.s, bp, st, sms));
         CK(spb::launch_band((int)g.k, (int)g.s, bp, &tmap, st, nullptr, sms));
         h->last_kernel.store(csc ? "conv_band_check<csc>+conv_spmm_band" : "conv_band_check+conv_spmm_band");
@@ -988,7 +1000,8 @@ static int build_csr_impl(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
     size_t seg_bytes = 0;
     if (spb::band_supported((int)k, (int)s)) {
         h->band_tw = spb::band_tile_width((int)k, (int)s);
-        seg_bytes = ((size_t)(g.mo * ((g.no + h->band_tw - 1) / h->band_tw)) + 255) & ~size_t(255);
+        const int64_t segw = h->band_tw / spb::band_seg_div((int)k, (int)s);
+        seg_bytes = ((size_t)(g.mo * ((g.no + segw - 1) / segw)) + 255) & ~size_t(255);
     }
     char* csr = nullptr;
     cudaError_t e = cudaMallocAsync(&csr, rp_bytes + 2 * ix_bytes + 256 + tap_bytes + seg_bytes, st);
@@ -1158,7 +1171,8 @@ static int build_csc_impl(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
     size_t seg_bytes = 0;
     if (spb::band_supported((int)k, (int)s)) {  // CSC segments: one input row x s * band_tw input columns
         h->band_tw = spb::band_tile_width((int)k, (int)s);
-        h->csc_tiles_b = (int)((n + h->band_tw * s - 1) / (h->band_tw * s));  // (segments of s * band_tw columns)
+        const int64_t segw = h->band_tw / spb::band_seg_div((int)k, (int)s);
+        h->csc_tiles_b = (int)((n + segw * s - 1) / (segw * s));  // (segments of s * segment-width columns)
         seg_bytes = ((size_t)(m * h->csc_tiles_b) + 255) & ~size_t(255);
     }
     char* mem = nullptr;
@@ -1175,7 +1189,6 @@ static int build_csc_impl(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
     if (seg_bytes) h->seg_ok = reinterpret_cast<uint8_t*>(mem + cp_bytes + 2 * ix_bytes + 256 + tap_bytes);
     // (pageable source: staged by the driver before the call returns)
     e = cudaMemcpyAsync(h->taps, kernel_kxk, (size_t)(k * k) * 4, cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess && seg_bytes) e = cudaMemsetAsync(h->seg_ok, 1, seg_bytes, st);
     if (e == cudaSuccess) {
         spb::CscParams cp{};
         cp.m = (int)g.m;
@@ -1939,17 +1952,18 @@ int spconv_spmm_f64_threads(const spconv_csr* h, const double* X_dev, int64_t ld
     // and the register-blocked apply in fp64 (spmm_band.cu, T = double) --
     // the reference's per-entry multiply and add, in its order.
     const Geom& g = h->g;
-    const bool tma64 = h->is_conv && g.n % 2 == 0 && ldx % 2 == 0 && reinterpret_cast<uintptr_t>(X_dev) % 16 == 0 &&
-                       encode_fn() != nullptr && g.m < (1ll << 30) && g.n < (1ll << 30);
-    if (chunk == 0 && batch >= 3 && tma64 && h->band_tw > 0 && (h->row_ptr || csc) && band_taps_ok(h) &&
-        path_override() != kGeneric) {
+    if (chunk == 0 && batch >= 3 && h->is_conv && h->band_tw > 0 && spb::band64_supported((int)g.k, (int)g.s) &&
+        (h->row_ptr || csc) && band_taps_ok(h) && path_override() != kGeneric) {
         const int sms = device_sm_count();
         spb::BandParams bp;
         spb::BandShape sh;
         if (int rc = band_setup(hm, csc, true, batch, X_dev, ldx, Y_dev, ldy, bp, sh, sms, st)) return rc;
         bp.fused = 0;
         CUtensorMap tmap;
-        if (int rc = encode_x_map(&tmap, X_dev, g, ldx, batch, sh.wc, sh.wr, 1, true)) return rc;
+        std::memset(&tmap, 0, sizeof tmap);
+        if (!bp.notma)
+            if (int rc = encode_x_map(&tmap, X_dev, g, ldx, batch, sh.wc, sh.wr, 1, true)) return rc;
+        hm->checked.store(true);
         CK(spb::launch_band_check((int)g.k, (int)g.s, bp, st, sms));
         CK(spb::launch_band64((int)g.k, (int)g.s, bp, &tmap, st, nullptr, sms));
         hm->last_kernel.store(csc ? "conv_band_check<csc>+conv_spmm_band<f64>" : "conv_band_check+conv_spmm_band<f64>");
@@ -2178,7 +2192,11 @@ int spconv_band_check_status(const spconv_csr* h, int64_t* segments, int64_t* fa
     if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
     // CSR: one segment per output row x band_tw output columns; CSC storage:
     // one per input row x s * band_tw input columns
-    const int64_t n = csc_native(h) ? h->g.m * h->csc_tiles_b : h->g.mo * ((h->g.no + h->band_tw - 1) / h->band_tw);
+    const int64_t segw = h->band_tw / spb::band_seg_div((int)h->g.k, (int)h->g.s);
+    const int64_t n = csc_native(h) ? h->g.m * h->csc_tiles_b : h->g.mo * ((h->g.no + segw - 1) / segw);
+    *segments = n;
+    *failed = 0;
+    if (!h->checked.load()) return SPCONV_OK;  // (no check has run: nothing failed)
     std::vector<uint8_t> v((size_t)n);
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpy(v.data(), h->seg_ok, (size_t)n, cudaMemcpyDeviceToHost));
@@ -2186,6 +2204,23 @@ int spconv_band_check_status(const spconv_csr* h, int64_t* segments, int64_t* fa
     for (uint8_t b : v) bad += b == 0;
     *segments = n;
     *failed = bad;
+    return SPCONV_OK;
+}
+
+int spconv_band_check_flags(const spconv_csr* h, uint8_t* out, int64_t cap, int64_t* n) {
+    if (!h || !n) return fail(SPCONV_EINVAL, "spconv_band_check_flags: null argument");
+    int64_t seg = 0, bad = 0;
+    if (int rc = spconv_band_check_status(h, &seg, &bad)) return rc;
+    *n = seg;
+    if (out) {
+        if (cap < seg) return fail(SPCONV_EINVAL, "spconv_band_check_flags: buffer too small");
+        if (!h->checked.load()) {
+            std::memset(out, 1, (size_t)seg);
+            return SPCONV_OK;
+        }
+        DeviceGuard dg(h->device);
+        CK(cudaMemcpy(out, h->seg_ok, (size_t)seg, cudaMemcpyDeviceToHost));
+    }
     return SPCONV_OK;
 }
 

@@ -136,6 +136,9 @@ struct BandParams {
     // per-entry values when the handle keeps them (NULL: the fp32 ones widened)
     const double* taps64;
     const double* vals64;
+    int notma;         // X rows not 16-byte pitched (or windows wider than a TMA box): cp.async staging
+    int seg_div;       // check segments per apply tile width (k = 11: smaller segments)
+    int tiles_y_chk;   // check segments across n_out (CSR storage) = ceil(n_out / (TW / seg_div))
 };
 
 // CSC-storage SpMV / SpMM of a conv transform (csc_apply.cu).
@@ -261,6 +264,8 @@ cudaError_t launch_spmv_win(const SpecParams& sp, int kmax, cudaStream_t st);
 
 bool band_supported(int k, int s);
 int band_tile_width(int k, int s);
+int band_seg_div(int k, int s);       // check segments per tile width
+bool band64_supported(int k, int s);  // fp64 apply instantiated
 cudaError_t launch_band(int k, int s, const BandParams& bp, const CUtensorMap* tmap, cudaStream_t st,
                         BandShape* shape, int sms);
 cudaError_t launch_band_check(int k, int s, const BandParams& bp, cudaStream_t st, int sms);
@@ -326,7 +331,8 @@ struct spconv_csr {
     double* taps64 = nullptr;         // device k*k exact taps (CSC conv handles built from double taps)
     int csc_tiles_b = 0;           // CSC band check: segments per input row (band geometries)
     int* fail_flag = nullptr;      // CSC conv: mapped host word, set by a device check that failed (sticky)
-    std::atomic<bool> exposed{false};  // spconv_csr_device_ptrs handed out the CSC arrays: verify before use
+    std::atomic<bool> exposed{false};
+    std::atomic<bool> checked{false};  // a band check has been enqueued (seg_ok holds verdicts)  // spconv_csr_device_ptrs handed out the CSC arrays: verify before use
     cudaEvent_t built = nullptr;  // recorded after the build on the build stream (host-buffer calls wait on it)
     std::atomic<bool> applied{false};  // an apply was enqueued after the build (PDL is safe from then on)
     std::atomic<const char*> last_kernel{nullptr};  // diagnostics: last SpMM kernel launched
