@@ -633,20 +633,19 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
         std::memset(&tmap, 0, sizeof tmap);
         if (!bp.notma)
             if (int rc = encode_x_map(&tmap, X, g, ldx, batch, sh.wc, sh.wr, 1, false)) return rc;
-        // When the images dominate by far (matrix < 10 % of the call's bytes),
-        // one fused kernel checks the matrix in its producer warps while it
-        // applies, plus a fixup pass for failed segments: config 3 384 ->
-        // 376 us.  With a heavier matrix the producer's checks starve the
-        // pipeline (config 4 at 64 images: 1,043 -> 1,531 us), so the check
-        // stays a kernel of its own (profiles/r01v/exp.txt).  Option "fused"
-        // forces either form; the blocked path needs finite taps.  (zero-tap
-        // kernels: the masked checks slow the fused producer -- config 3 shape
-        // 431 us fused against 27 + 371 us as two kernels -- so two kernels.)
+        // The fused form -- one kernel: consumers apply with the blocked sums
+        // while up to four check warps per CTA verify the storage segment by
+        // segment -- for k <= 5, whose checks are light (config 3: 256 images
+        // 400 -> 362 us, 32 images 77 -> 64 us, 16 images 54 -> 44 us,
+        // scripts/ab_fused.py); with k >= 7 the checks (49 entries a row)
+        // outweigh the overlap (config 4 at 8 images: 368 us as two kernels,
+        // 585 fused), so the check runs as a kernel of its own.  Zero-tap
+        // kernels keep the two-kernel form (their masked checks are heavier).
+        // Option "fused" forces either form; the blocked path needs finite taps.
         // Both forms run on the caller's stream only: the check sees exactly
         // the matrix the stream order gives it.
         const int fsel = spb::opt(spb::kOptFused);
-        const bool light = 8.0 * (double)h->nnz < 0.1 * 4.0 * (double)batch * (double)(h->rows + h->cols);
-        bp.fused = band_taps && bp.seg_div == 1 && (fsel ? fsel == 2 : light && !bp.zt) ? 1 : 0;
+        bp.fused = band_taps && bp.seg_div == 1 && (fsel ? fsel == 2 : g.k <= 5 && !bp.zt) ? 1 : 0;
         if (bp.fused) {
             h->checked.store(true);
             const cudaError_t fe = spb::launch_band((int)g.k, (int)g.s, bp, &tmap, st, nullptr, sms);

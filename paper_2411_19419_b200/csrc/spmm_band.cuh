@@ -808,21 +808,43 @@ __device__ __forceinline__ void load_window(const BandParams& P, const CUtensorM
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(full)) : "memory");
 }
 
+// The fused form: besides the consumers and the window producer, CHK warps
+// check segments (two staging slices each, double-buffered), as many as the
+// shared memory left by the window stages holds (<= 4; 0: no fused form).
+template <int K, int S, int V, int CPT, int TH, int STAGES, int DELTA, typename T = float>
+struct FusedCfg {
+    using C = BandCfg<K, S, V, CPT, TH, STAGES, DELTA, T>;
+    using CC = CheckCfg<K, S, C::TW>;
+    static constexpr size_t HDR = 256;  // mbarriers, row flags, 2 x CHK check barriers
+    static constexpr size_t BASE = HDR + (size_t)STAGES * C::SF * sizeof(T);
+    static constexpr long long FREE = 227ll * 1024 - (long long)BASE;
+    static constexpr int CHK = FREE <= 0 ? 0 : (FREE / (2 * (long long)CC::WARP_BYTES) >= 4 ? 4 : (int)(FREE / (2 * (long long)CC::WARP_BYTES)));
+    static constexpr size_t SMEM = BASE + (size_t)CHK * 2 * CC::WARP_BYTES;
+    static constexpr int THREADS = C::THREADS + 32 * CHK;
+    static_assert(STAGES * 24 + 16 * 4 <= (int)HDR, "barriers fit the header");
+};
+
 template <int K, int S, int V, int CPT, int TH, int STAGES, int DELTA, bool FUSED, bool ZT = false,
           typename T = float>
-__global__ void __launch_bounds__(BandCfg<K, S, V, CPT, TH, STAGES, DELTA, T>::THREADS, 1)
+__global__ void __launch_bounds__(FUSED ? FusedCfg<K, S, V, CPT, TH, STAGES, DELTA, T>::THREADS
+                                        : BandCfg<K, S, V, CPT, TH, STAGES, DELTA, T>::THREADS,
+                                  1)
     conv_spmm_band(const __grid_constant__ CUtensorMap tmap, const BandParams P) {
     using C = BandCfg<K, S, V, CPT, TH, STAGES, DELTA, T>;
     using CC = CheckCfg<K, S, C::TW>;
+    using FC = FusedCfg<K, S, V, CPT, TH, STAGES, DELTA, T>;
+    constexpr int CHK = FUSED ? FC::CHK : 0;
+    constexpr size_t HDR = FUSED ? FC::HDR : 128;
     constexpr bool F64 = sizeof(T) == 8;
     static_assert(!FUSED || !F64, "the fp64 apply runs after a separate check");
-    static_assert(!FUSED || STAGES * 24 + 16 <= 128, "check barriers fit the 128-byte header");
+    static_assert(!FUSED || CHK > 0, "no room for check warps");
+    static_assert(FUSED || STAGES * 24 <= 128, "barriers fit the header");
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
     uint64_t* empty = full + STAGES;
     unsigned long long* s_mask = reinterpret_cast<unsigned long long*>(empty + STAGES);  // per-stage row flags
     uint64_t* cbar = reinterpret_cast<uint64_t*>(s_mask + STAGES);                       // (FUSED) check slices
-    T* xs = reinterpret_cast<T*>(smem + 128);
+    T* xs = reinterpret_cast<T*>(smem + HDR);
     __shared__ uint32_t s_w[C::KK];  // taps, runtime-indexed (checks, the CSC per-entry loop)
     __shared__ T s_wt[C::KK];        // the taps the sums use (fp64: the exact taps)
 
@@ -835,10 +857,7 @@ __global__ void __launch_bounds__(BandCfg<K, S, V, CPT, TH, STAGES, DELTA, T>::T
             mbar_init(&full[st], P.notma ? 33 : 1);
             mbar_init(&empty[st], C::CWARPS);
         }
-        if (FUSED) {
-            mbar_init(&cbar[0], 1);
-            mbar_init(&cbar[1], 1);
-        }
+        for (int b = 0; b < 2 * CHK; ++b) mbar_init(&cbar[b], 1);
         mbar_fence_init();
     }
     for (int q = t; q < C::KK; q += blockDim.x) {
@@ -848,69 +867,50 @@ __global__ void __launch_bounds__(BandCfg<K, S, V, CPT, TH, STAGES, DELTA, T>::T
     }
     __syncthreads();
 
-    if (FUSED && warp == C::CWARPS) {
-        // ---- producer warp, fused: window loads whenever a stage is free,
-        // one segment check (double-buffered) between them.
+    if (FUSED && warp > C::CWARPS) {
+        // ---- check warps (fused form): segments blockIdx.x * CHK + cw,
+        // + gridDim.x * CHK, ..., two staging slices each: the copies of the
+        // next segment are in flight while the current one is verified.
+        const int cw = warp - C::CWARPS - 1;
         uint32_t w[C::KK];
 #pragma unroll
         for (int q = 0; q < C::KK; ++q) w[q] = s_w[q];
-        int* cslice = reinterpret_cast<int*>(smem + 128 + (size_t)STAGES * C::SF * 4);
         constexpr int SLICE = (int)(CC::WARP_BYTES / 4);
+        int* cslice = reinterpret_cast<int*>(smem + HDR + (size_t)STAGES * C::SF * sizeof(T)) + 2 * cw * SLICE;
+        uint64_t* bars = cbar + 2 * cw;
         const bool csc = P.csc != 0;
         const long long nseg = csc ? (long long)P.m * P.tiles_b : (long long)P.mo * P.tiles_y;
-        long long cseg = blockIdx.x, vseg = -1;
+        const long long step = (long long)gridDim.x * CHK;
+        long long cseg = (long long)blockIdx.x * CHK + cw;
         SegGeom vg{};
         int cb = 0;
         uint32_t cph = 0;
-        auto seg_next = [&]() {  // geometry of the next segment, copies into slice cb
-            if (cseg < nseg) {
-                vg = csc ? seg_geom_csc<K, S, S * C::TW, ZT>(P, cseg) : seg_geom<K, S, C::TW, ZT>(P, cseg);
-                vseg = cseg;
-                cseg += gridDim.x;
-                if (lane == 0 && vg.valid) {
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    seg_issue<K, S, C::TW>(P, vg, cslice + cb * SLICE, &cbar[cb]);
-                }
-            } else {
-                vseg = -1;
+        auto issue = [&](long long sg) {
+            vg = csc ? seg_geom_csc<K, S, S * C::TW, ZT>(P, sg) : seg_geom<K, S, C::TW, ZT>(P, sg);
+            if (lane == 0 && vg.valid) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                seg_issue<K, S, C::TW>(P, vg, cslice + cb * SLICE, &bars[cb]);
             }
         };
-        seg_next();
-        int it = 0;
-        ItemIter I(P);
-        while (I.img < P.batch || vseg >= 0) {
-            while (I.img < P.batch) {
-                const int st = it % STAGES;
-                int fr = 1;
-                if (lane == 0 && it >= STAGES) fr = mbar_try_wait(&empty[st], (uint32_t)(((it / STAGES) - 1) & 1));
-                if (!__shfl_sync(0xffffffffu, fr, 0)) break;
-                load_window<C, T>(P, &tmap, xs + (size_t)st * C::SF, S * I.ty * C::TW - P.p - DELTA,
-                                  S * I.tx * TH - P.p, I.img, &full[st], lane);
-                __syncwarp();
-                ++it;
-                I.next();
+        if (cseg < nseg) issue(cseg);
+        while (cseg < nseg) {
+            const SegGeom g = vg;
+            const long long sg = cseg;
+            const int b = cb;
+            cb ^= 1;
+            cseg += step;
+            __syncwarp();  // slice cb's previous segment was fully read before its verdict
+            if (cseg < nseg) issue(cseg);
+            bool ok = false;
+            if (g.valid) {
+                mbar_wait(&bars[b], (cph >> b) & 1u);
+                cph ^= 1u << b;
+                ok = csc ? seg_verify_csc<K, S, C::TW, ZT>(P, g, cslice + b * SLICE, w, s_w, lane)
+                         : seg_verify<K, S, C::TW, ZT>(P, g, cslice + b * SLICE, w, s_w, lane);
             }
-            if (vseg >= 0) {
-                const SegGeom g = vg;
-                const long long sg = vseg;
-                const int b = cb;
-                cb ^= 1;
-                __syncwarp();  // slice cb's previous segment was fully read before its verdict
-                seg_next();
-                bool ok = false;
-                if (g.valid) {
-                    mbar_wait(&cbar[b], (cph >> b) & 1u);
-                    cph ^= 1u << b;
-                    ok = csc ? seg_verify_csc<K, S, C::TW, ZT>(P, g, cslice + b * SLICE, w, s_w, lane)
-                             : seg_verify<K, S, C::TW, ZT>(P, g, cslice + b * SLICE, w, s_w, lane);
-                }
-                if (lane == 0) {
-                    P.seg_ok[sg] = ok ? 1 : 0;
-                    if (!ok && !P.fixup) *P.fail_count = 1;
-                }
-            } else if (I.img < P.batch) {  // all checked: wait for the next free stage
-                if (lane == 0) mbar_wait(&empty[it % STAGES], (uint32_t)(((it / STAGES) - 1) & 1));
-                __syncwarp();
+            if (lane == 0) {
+                P.seg_ok[sg] = ok ? 1 : 0;
+                if (!ok && !P.fixup) *P.fail_count = 1;
             }
         }
         return;
@@ -925,7 +925,7 @@ __global__ void __launch_bounds__(BandCfg<K, S, V, CPT, TH, STAGES, DELTA, T>::T
         for (ItemIter I(P); I.img < P.batch; I.next(), ++it) {
             const int st = it % STAGES;
             unsigned long long rows_ok = ~0ull;
-            if (!P.csc) {  // (CSC: the check verified the storage as a whole; no per-row flags)
+            if (!FUSED && !P.csc) {  // (CSC / fused: the apply does not wait for per-row verdicts)
               rows_ok = 0;
 #pragma unroll
               for (int h = 0; h < (TH + 31) / 32; ++h) {  // one lane per tile row
@@ -1164,9 +1164,9 @@ cudaError_t launch_pdl(Kern kern, unsigned grid, unsigned block, size_t smem, cu
 template <int K, int S, int V, int CPT, int TH, int STAGES, int DELTA, bool ZT>
 cudaError_t run_fused(const BandParams& bp, const CUtensorMap* tmap, cudaStream_t st, int sms) {
     using C = BandCfg<K, S, V, CPT, TH, STAGES, DELTA>;
-    using CC = CheckCfg<K, S, C::TW>;
-    constexpr size_t SMEM = C::SMEM + 2 * CC::WARP_BYTES;
-    if constexpr (SMEM > 227 * 1024 || STAGES * 24 + 16 > 128) {
+    using FC = FusedCfg<K, S, V, CPT, TH, STAGES, DELTA>;
+    constexpr size_t SMEM = FC::SMEM;
+    if constexpr (FC::CHK == 0) {
         return cudaErrorNotSupported;
     } else {
         auto kern = conv_spmm_band<K, S, V, CPT, TH, STAGES, DELTA, true, ZT>;
@@ -1177,14 +1177,14 @@ cudaError_t run_fused(const BandParams& bp, const CUtensorMap* tmap, cudaStream_
             cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
             if (e != cudaSuccess) return e;
             int o = 0;
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, C::THREADS, SMEM);
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, FC::THREADS, SMEM);
             if (e != cudaSuccess) return e;
             occ[dev & 63] = std::max(o, 1);
         }
         const long long items = (long long)bp.tiles * bp.batch;
         // every CTA also owns segments: at least one CTA per SM even for short batches
         const long long grid = std::min<long long>(std::max<long long>(items, sms), (long long)occ[dev & 63] * sms);
-        kern<<<(unsigned)grid, C::THREADS, SMEM, st>>>(*tmap, bp);
+        kern<<<(unsigned)grid, FC::THREADS, SMEM, st>>>(*tmap, bp);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
         if (!bp.fixup) return cudaSuccess;  // (failed segments raise the handle's verdict instead)
