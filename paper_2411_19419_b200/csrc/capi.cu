@@ -1870,9 +1870,28 @@ int spconv_convolve_host(const spconv_csr* hc, const float* X_host, float* Y_hos
         h->ws_chunk = chunk;
     }
     cudaStream_t s_in = h->ws_stream[0], s_cp = h->ws_stream[1], s_out = h->ws_stream[2];
-    // the build may still be in flight on its own stream (builds only enqueue)
-    if (h->built)
+    // the build may still be in flight on its own stream (builds only enqueue);
+    // once the workspace streams wait for it, everything later is ordered after it
+    if (h->built && !h->ws_built_waited) {
         for (int s = 0; s < 3; ++s) CK(cudaStreamWaitEvent(h->ws_stream[s], h->built, 0));
+        h->ws_built_waited = true;
+    }
+    // A page-locked Y is device-addressable: single-image calls have the
+    // kernel write y straight into host memory (posted PCIe writes, no D2H
+    // copy).  X still travels by the copy engine: reading the input windows
+    // over PCIe from the kernel was slower (56^2 k3: 26.5 against 16.8 us a
+    // call, scripts/probe_host.py).
+    cudaPointerAttributes ay{};
+    const bool y_pinned = cudaPointerGetAttributes(&ay, Y_host) == cudaSuccess && ay.type == cudaMemoryTypeHost &&
+                          ay.devicePointer;
+    cudaGetLastError();  // (clear the query's error state for pageable pointers)
+    if (y_pinned && batch <= 2) {
+        CK(cudaMemcpyAsync(h->ws_x[0], X_host, (size_t)(batch * h->cols * 4), cudaMemcpyHostToDevice, s_cp));
+        if (int rc = run_spmm(h, h->ws_x[0], h->cols, static_cast<float*>(ay.devicePointer), h->rows, batch, s_cp))
+            return rc;
+        CK(cudaStreamSynchronize(s_cp));
+        return SPCONV_OK;
+    }
     if (batch <= chunk) {
         // One chunk: nothing to overlap -- H2D, apply, D2H in order on one
         // stream and a single synchronisation (the latency path of small calls).

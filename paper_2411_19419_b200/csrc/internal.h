@@ -343,4 +343,5 @@ struct spconv_csr {
     float* ws_x[2] = {nullptr, nullptr};
     float* ws_y[2] = {nullptr, nullptr};
     int64_t ws_chunk = 0;
+    bool ws_built_waited = false;  // the workspace streams are ordered after the build
 };

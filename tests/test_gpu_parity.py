@@ -355,6 +355,25 @@ def test_end_to_end_host_path(sp, orc, torch_cuda):
     assert np.array_equal(bits(Yp.numpy()), bits(want))
 
 
+@pytest.mark.parametrize("spec", [(56, 56, 3, 1, 1), (224, 224, 7, 2, 3), (14, 14, 1, 1, 0), (28, 28, 2, 2, 0),
+                                  (7, 7, 3, 1, 1), (30, 30, 5, 3, 2)])
+def test_host_path_single_images(sp, orc, torch_cuda, spec):
+    """Single images (and pairs) on host buffers -- the DenseNet call shape.
+    Page-locked Y: the kernel writes y straight into host memory; pageable
+    buffers: copies both ways.  Bit-exact either way."""
+    m, n, k = spec[:3]
+    kern, X = problem(orc, 9, m, n, k, batch=2)
+    t = build(sp, spec, kern)
+    want = orc.spmm_native(*orc.build_native(*spec, kern), X)
+    for b in (1, 2):
+        Xp = torch_cuda.from_numpy(X[:b].copy()).pin_memory()
+        Yp = torch_cuda.empty(b, t.rows).pin_memory()
+        sp.convolve_batch(t, Xp, Yp)
+        assert np.array_equal(bits(Yp.numpy()), bits(want[:b])), (spec, b, t.last_kernel)
+        Y = sp.convolve_batch(t, X[:b].copy())  # pageable
+        assert np.array_equal(bits(Y), bits(want[:b])), (spec, b)
+
+
 def test_reference_semantics_convolve(sp, orc, golden):
     """The fp64-in/fp64-out convolve() mirror computes in fp64 with the
     reference's rounding: BIT-identical to the reference's convolve() on
