@@ -56,4 +56,4 @@ for spec in ((512, 512, 5, 2, 2), (56, 56, 3, 1, 1), (224, 224, 7, 2, 3), (28, 2
             out[key] = {"kernel": t.last_kernel, "cold_us_median": float(np.median(cold)), "warm_us": warm}
             print(key, out[key], flush=True)
     t.close()
-json.dump(out, open("gpurun_out/probe_spmv.json", "w"), indent=1)
+json.dump(out, open("gpurun_out/probes/probe_spmv.json" if __import__("os").path.isdir("gpurun_out/probes") else "gpurun_out/probe_spmv.json", "w"), indent=1)
