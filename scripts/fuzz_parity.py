@@ -25,6 +25,13 @@ from oracle import Oracle  # noqa: E402
 PATHS = [None, "spmv", "spmv_plain", "banded", "tiled", "tiled_notma", "generic"]
 
 
+def bits64(a):
+    a = np.ascontiguousarray(a, np.float64)
+    v = a.view(np.uint64).copy()
+    v[np.isnan(a)] = 0x7FF8000000000000
+    return v
+
+
 def bits(a):
     a = np.ascontiguousarray(a, np.float32)
     v = a.view(np.uint32).copy()
@@ -82,9 +89,14 @@ def main():
         ok = ok if layout == sp.Layout.CSR else True
         ok = ok and np.array_equal(gp, wp) and np.array_equal(gi[:nz], wi) and np.array_equal(
             np.nan_to_num(gv[:nz], nan=7.0).view(np.uint64), np.nan_to_num(wv, nan=7.0).view(np.uint64))
-        if mode == 2 and ok:  # fp64 apply with the exact values == the oracle's fp64 restatement
-            y64 = sp.spmm_f64(t, torch.from_numpy(X[:1].astype(np.float64)).cuda()).cpu().numpy()[0]
-            ok = np.array_equal(y64.view(np.uint64), orc.spmv_f64(p64, i64, v64, X[0].astype(np.float64)).view(np.uint64))
+        if ok:  # fp64 apply (exact values; the band path for batches; CSC with a random thread count)
+            X64 = X.astype(np.float64) * (1.0 + 2.0 ** -30)
+            nt = int(rng.choice([1, 1, 2, 3, 8])) if layout == sp.Layout.CSC else 1
+            y64 = sp.spmm_f64(t, torch.from_numpy(X64).cuda(), threads=nt).cpu().numpy()
+            for b in range(batch):
+                w64 = (orc.spmv_csc_f64_threads(t.rows, wp, wi, wv, X64[b], nt) if layout == sp.Layout.CSC
+                       else orc.spmv_f64(p64, i64, v64, X64[b]))
+                ok = ok and np.array_equal(bits64(y64[b]), bits64(w64))
         want = orc.spmm_native(rp, ri, rv, X)
         pad = int(rng.choice([0, 0, 4]))
         Xd = torch.zeros(batch, m * n + pad, device="cuda")
@@ -95,6 +107,8 @@ def main():
             env["path"] = path
         if rng.random() < 0.3:
             env["fused"] = str(int(rng.integers(0, 2)))
+        if rng.random() < 0.3:
+            env["stage"] = str(rng.choice(["bulk", "window"]))
         try:
             with sp.options(**env):
                 Y = sp.spmm(t, Xd[:, :m * n])
