@@ -374,6 +374,25 @@ def test_host_path_single_images(sp, orc, torch_cuda, spec):
         assert np.array_equal(bits(Y), bits(want[:b])), (spec, b)
 
 
+@pytest.mark.slow
+def test_config3_auto_path_bench_batches(sp, orc, torch_cuda):
+    """BASELINE config 3 through the default (auto) path at the bench's
+    per-GPU batches -- 96 and 32 images, the fused check-and-apply --
+    images {0, b/2, b-1} bit-exact vs the oracle."""
+    spec = (1024, 1024, 3, 1, 1)
+    kern, X = problem(orc, 2, 1024, 1024, 3, batch=3)
+    t = build(sp, spec, kern)
+    ptr, idx, val = orc.build_native(*spec, kern)
+    for batch in (96, 32):
+        Xd = torch_cuda.from_numpy(np.repeat(X, (batch + 2) // 3, axis=0)[:batch]).cuda()
+        Y = sp.spmm(t, Xd)
+        torch_cuda.cuda.synchronize()
+        assert t.last_kernel in BAND_KERNELS, t.last_kernel
+        for i in (0, batch // 2, batch - 1):
+            want = orc.spmm_native(ptr, idx, val, Xd[i].cpu().numpy()[None])[0]
+            assert np.array_equal(bits(Y[i].cpu().numpy()), bits(want)), (batch, i)
+
+
 def test_reference_semantics_convolve(sp, orc, golden):
     """The fp64-in/fp64-out convolve() mirror computes in fp64 with the
     reference's rounding: BIT-identical to the reference's convolve() on
