@@ -607,7 +607,9 @@ cudaError_t launch_csr_build(const BuildParams& bp_in, bool dense, int block, si
     // Option build = block | warp | persist forces a kernel.
     const int bsel = opt(kOptBuild);
     const bool warp_build = bsel == 2;
-    const bool persist_build = bsel == 3 || (bsel == 0 && bp.k <= 5);
+    // (exact-fp64 builds: the staged block kernel, config 3 32.6 against 34.7 us
+    // persistent, config 2 equal -- profiles/r02_exp/build_ab.txt)
+    const bool persist_build = bsel == 3 || (bsel == 0 && bp.k <= 5 && !bp.vals64);
     // exact-fp64 fill: the persistent kernel (k <= 5) and the staged unrolled
     // block kernel (k in {1, 3, 5, 7, 11}); anything else builds tags only
     const bool unrolled = bp.k == 1 || bp.k == 3 || bp.k == 5 || bp.k == 7 || bp.k == 11;
