@@ -1,0 +1,29 @@
+// band_k2.cu -- band-path instantiations for k = 2 (spmm_band.cuh).
+// Blockings (V rows x CPT columns per consumer thread, TH-row tiles, STAGES
+// deep): the A/B runs of profiles/r01p, r01q and r02 (fp64: smaller V / TH).
+#include "spmm_band.cuh"
+
+namespace spb {
+
+cudaError_t band_k2(int op, int s, const BandParams& bp, const CUtensorMap* tmap, cudaStream_t st, BandShape* sh,
+                    int sms) {
+    const int d32 = ((-bp.p) % 4 + 4) % 4, d64 = ((-bp.p) % 2 + 2) % 2;
+    if (s == 1) {
+        if (op == 0) return run_delta<2, 1, 16, 4, 64, 4>(d32, bp, tmap, st, sh, sms);
+        if (op == 1) return run_check<2, 1, 128>(bp, st, sms);
+        return cudaErrorNotSupported;
+    }
+    if (s == 2) {
+        if (op == 0) return run_delta<2, 2, 8, 2, 32, 4>(d32, bp, tmap, st, sh, sms);
+        if (op == 1) return run_check<2, 2, 64>(bp, st, sms);
+        return cudaErrorNotSupported;
+    }
+    if (s == 3) {
+        if (op == 0) return run_delta<2, 3, 8, 2, 16, 4>(d32, bp, tmap, st, sh, sms);
+        if (op == 1) return run_check<2, 3, 64>(bp, st, sms);
+        return cudaErrorNotSupported;
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace spb

@@ -9,6 +9,8 @@ namespace spb {
 // Per-k entry points (band_k*.cu).  op 0: fp32 apply, 1: check, 2: fp64 apply.
 cudaError_t band_k1(int op, int s, const BandParams& bp, const CUtensorMap* tmap, cudaStream_t st, BandShape* sh,
                     int sms);
+cudaError_t band_k2(int op, int s, const BandParams& bp, const CUtensorMap* tmap, cudaStream_t st, BandShape* sh,
+                    int sms);
 cudaError_t band_k3(int op, int s, const BandParams& bp, const CUtensorMap* tmap, cudaStream_t st, BandShape* sh,
                     int sms);
 cudaError_t band_k5(int op, int s, const BandParams& bp, const CUtensorMap* tmap, cudaStream_t st, BandShape* sh,
@@ -24,6 +26,7 @@ cudaError_t dispatch(int op, int k, int s, const BandParams& bp, const CUtensorM
     if (s < 1 || s > 3) return cudaErrorInvalidValue;
     switch (k) {
         case 1: return band_k1(op, s, bp, tmap, st, sh, sms);
+        case 2: return band_k2(op, s, bp, tmap, st, sh, sms);
         case 3: return band_k3(op, s, bp, tmap, st, sh, sms);
         case 5: return band_k5(op, s, bp, tmap, st, sh, sms);
         case 7: return band_k7(op, s, bp, tmap, st, sh, sms);
@@ -33,9 +36,9 @@ cudaError_t dispatch(int op, int k, int s, const BandParams& bp, const CUtensorM
 }
 }  // namespace
 
-// k in {1, 3, 5, 7, 11} (the BASELINE / config-5 / DenseNet121 sides), s in {1, 2, 3}.
+// k in {1, 2, 3, 5, 7, 11} (the BASELINE / config-5 / DenseNet121 sides), s in {1, 2, 3}.
 bool band_supported(int k, int s) {
-    return (k == 1 || k == 3 || k == 5 || k == 7 || k == 11) && s >= 1 && s <= 3;
+    return (k == 1 || k == 2 || k == 3 || k == 5 || k == 7 || k == 11) && s >= 1 && s <= 3;
 }
 
 // Output columns per tile (32 threads x CPT): 128 at s = 1, 64 at s = 2, 3.

@@ -16,7 +16,7 @@ target = sys.argv[1]
 warm = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 SPECS = {"c3": ((1024, 1024, 3, 1, 1), 256, 0), "c3b32": ((1024, 1024, 3, 1, 1), 32, 0),
          "c3csc": ((1024, 1024, 3, 1, 1), 256, 1), "c3f64": ((1024, 1024, 3, 1, 1), 256, 0),
-         "c4": ((4096, 4096, 7, 2, 3), 8, 0), "c2": ((512, 512, 5, 2, 2), 1, 0),
+         "c4": ((4096, 4096, 7, 2, 3), 8, 0), "c4csc": ((4096, 4096, 7, 2, 3), 8, 1), "c2": ((512, 512, 5, 2, 2), 1, 0),
          "build3": ((1024, 1024, 3, 1, 1), 0, 0), "build4": ((4096, 4096, 7, 2, 3), 0, 0),
          "c5k11": ((257, 193, 11, 1, 10), 256, 0)}
 spec, b, layout = SPECS[target]

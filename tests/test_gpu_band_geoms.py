@@ -1,4 +1,4 @@
-"""GPU: the band path over every instantiated geometry -- k in {1, 3, 5, 7, 11},
+"""GPU: the band path over every instantiated geometry -- k in {1, 2, 3, 5, 7, 11},
 s in {1, 2, 3} -- with TMA windows (16-byte row pitch) and with cp.async
 element staging (odd widths: BASELINE config 5's 257 x 193), CSR and CSC
 storage, dense and zero-tap kernels, both check forms, fp32 and fp64.
@@ -12,7 +12,7 @@ from helpers import BAND_KERNELS, CSC_BAND_KERNELS, problem
 
 pytestmark = pytest.mark.gpu
 
-KS = [(k, s) for k in (1, 3, 5, 7, 11) for s in (1, 2, 3)]
+KS = [(k, s) for k in (1, 2, 3, 5, 7, 11) for s in (1, 2, 3)]
 
 
 @pytest.fixture(scope="module")

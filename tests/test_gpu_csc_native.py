@@ -72,7 +72,7 @@ def csc_want(orc, t, X):
 SPECS = [(64, 64, 3, 1, 1), (300, 260, 7, 2, 3), (257, 193, 5, 3, 4), (130, 68, 3, 2, 0), (101, 76, 5, 1, 2),
          (101, 77, 5, 1, 2),
          (257, 193, 11, 1, 10), (70, 45, 1, 1, 1), (33, 29, 7, 1, 6), (96, 40, 5, 2, 1)]
-BAND = {(k, s) for k in (1, 3, 5, 7, 11) for s in (1, 2, 3)}
+BAND = {(k, s) for k in (1, 2, 3, 5, 7, 11) for s in (1, 2, 3)}
 
 
 @pytest.mark.parametrize("zero", [False, True])
