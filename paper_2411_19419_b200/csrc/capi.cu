@@ -1904,10 +1904,27 @@ int spconv_convolve_host(const spconv_csr* hc, const float* X_host, float* Y_hos
     cudaEvent_t* ev_in = h->ws_ev[0];
     cudaEvent_t* ev_cp = h->ws_ev[1];
     cudaEvent_t* ev_out = h->ws_ev[2];
+    // Chunk sizes ramp up from 1/8 of a chunk and back down at the end: the
+    // first H2D and the last D2H are the pipeline's only unoverlapped copies.
+    std::vector<int64_t> sizes;
+    {
+        std::vector<int64_t> ramp;
+        for (int64_t r = std::max<int64_t>(1, chunk / 8); r < chunk; r *= 2) ramp.push_back(r);
+        int64_t rampsum = 0;
+        for (int64_t r : ramp) rampsum += r;
+        if (batch >= 2 * rampsum + 2 * chunk) {
+            int64_t left = batch - 2 * rampsum;
+            sizes = ramp;
+            while (left > 0) sizes.push_back(std::min(chunk, left)), left -= chunk;
+            for (auto it = ramp.rbegin(); it != ramp.rend(); ++it) sizes.push_back(*it);
+        } else {
+            for (int64_t left = batch; left > 0; left -= chunk) sizes.push_back(std::min(chunk, left));
+        }
+    }
     int c = 0;
-    for (int64_t b0 = 0; b0 < batch; b0 += chunk, ++c) {
+    for (int64_t b0 = 0; c < (int)sizes.size(); b0 += sizes[(size_t)c], ++c) {
         const int i = c & 1;
-        const int64_t nb = std::min(chunk, batch - b0);
+        const int64_t nb = sizes[(size_t)c];
         if (c >= 2) CK(cudaStreamWaitEvent(s_in, ev_cp[i], 0));  // spmm(c-2) done reading ws_x[i]
         CK(cudaMemcpyAsync(h->ws_x[i], X_host + b0 * h->cols, (size_t)(nb * h->cols * 4),
                            cudaMemcpyHostToDevice, s_in));
