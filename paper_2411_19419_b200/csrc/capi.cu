@@ -594,15 +594,19 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
             sp.pdl = h->applied.exchange(true) ? 1 : 0;
             sp.X = X;
             // The windowed kernel (one round trip) wins on matrices that arrive
-            // from HBM -- config 2 cold: 12.3 -> 10.2 us; on small, L2-resident
-            // transforms chained in a graph the bulk-staged kernel, which
+            // from HBM -- config 2 cold: 12.3 -> 10.2 us; on L2-resident
+            // transforms chained back to back the bulk-staged kernel, which
             // prefetches the matrix under the previous kernel (PDL), is faster
             // (config 2 warm 3.0 vs 4.3 us; DenseNet layers 1.0-2.5 vs 1.7-4.7 us;
-            // scripts/probe_spmv.py).  So: the window from 8 MB of matrix up.
-            // Option stage=lanes / bulk forces either kernel.
+            // profiles/r02_exp/probe_spmv.txt).  So: the window from 8 MB of
+            // matrix up, except in a graph being captured (replays run back to
+            // back: the warm case).  Option stage = bulk / window forces either.
             const int stage = spb::opt(spb::kOptStage);
             const bool big = 8.0 * (double)h->nnz >= 8.0 * (1 << 20);
-            const bool win = spec && spb::spmv_win_ok(sp) && (stage == 2 || (stage == 0 && big));
+            cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+            if (stage == 0 && big) CK(cudaStreamIsCapturing(st, &cap));
+            const bool win = spec && spb::spmv_win_ok(sp) &&
+                             (stage == 2 || (stage == 0 && big && cap == cudaStreamCaptureStatusNone));
             for (int64_t b0 = 0; b0 < batch; b0 += 2) {  // <= 2 images per launch
                 sp.X = X + b0 * ldx;
                 sp.Y = Y + b0 * ldy;
