@@ -515,6 +515,24 @@ def sharded_workload(sp, torch, cfg, args, dev, stream, world, rank, steps, warm
     all_same = max_over_ranks(0.0 if same else 1.0, dev) == 0.0
     worst = max_over_ranks(rdev, dev)
 
+    gather = None
+    if want_e2e and getattr(args, "gather", False):
+        # the optional final gather of every rank's slice on rank 0 (BASELINE
+        # north_star; NCCL over NVLink), timed on its own: not part of the step
+        from paper_2411_19419_b200.shard import gather_outputs
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        g0 = mono()
+        full = gather_outputs(Y[:b], B)
+        torch.cuda.synchronize(dev)
+        g1 = mono()
+        gms = (max_over_ranks(g1, dev) + max_over_ranks(-g0, dev)) * 1e3
+        moved = 4 * (B - b) * rows  # bytes that reach rank 0 from the others
+        gather = {"ms": gms, "bytes_to_root": moved, "gb_per_s": moved / (gms * 1e-3) / 1e9 if gms > 0 else None,
+                  "backend": dist.get_backend() if world > 1 else None,
+                  "ok": bool(full is None or tuple(full.shape) == (B, rows))}
+        del full
     e2e = None
     if want_e2e:
         Yh = torch.empty(max(b, 1), rows, dtype=torch.float32, pin_memory=True)
@@ -539,7 +557,7 @@ def sharded_workload(sp, torch, cfg, args, dev, stream, world, rank, steps, warm
         "t": t, "B": B, "b": b, "rows": rows, "cols": cols, "nnz": nnz, "kernel": kernel,
         "value": value, "job_ms": job_ms, "ev_max_ms": ev_max, "job_wall_ms": job_wall, "timing": timing,
         "local_ms": local_ms, "alg": alg, "bld_dev": max_over_ranks(bld_dev, dev), "bld_host": bld_host,
-        "parity": "bitexact" if all_same else "MISMATCH", "parity_images": which,
+        "parity": "bitexact" if all_same else "MISMATCH", "parity_images": which, "gather": gather,
         "parity_max_rel_dev": worst, "e2e": e2e, "clocks": sampler.summary(p0, p1),
         "l2": l2_note(torch, dev, rows, cols, nnz, b),
     }
@@ -765,6 +783,7 @@ def run_ours(args, cfg):
                       "gb_per_s": bld_bytes / (main["bld_dev"] * 1e-3) / 1e9,
                       "frac": bld_bytes / (main["bld_dev"] * 1e-3) / 1e9 / peak},
             "e2e": main["e2e"],
+            "gather": main["gather"],
             "gpu_launches": args.steps * launches_per_step,
             "clocks": main["clocks"],
             "secondary": extra or None,
@@ -877,6 +896,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true", help="skip the extra workloads")
+    ap.add_argument("--gather", action="store_true", help="also time the optional final gather on rank 0")
     ap.add_argument("--workload", choices=["config", "densenet121"], default="config",
                     help="densenet121: the paper's Table 1 layer-table protocol")
     ap.add_argument("--report", default="", help="densenet121: write the per-layer markdown here")
