@@ -11,16 +11,19 @@ cudaError_t band_k2(int op, int s, const BandParams& bp, const CUtensorMap* tmap
     if (s == 1) {
         if (op == 0) return run_delta<2, 1, 16, 4, 64, 4>(d32, bp, tmap, st, sh, sms);
         if (op == 1) return run_check<2, 1, 128>(bp, st, sms);
+        if (op == 2) return run_delta64<2, 1, 8, 4, 32, 4>(d64, bp, tmap, st, sh, sms);
         return cudaErrorNotSupported;
     }
     if (s == 2) {
         if (op == 0) return run_delta<2, 2, 8, 2, 32, 4>(d32, bp, tmap, st, sh, sms);
         if (op == 1) return run_check<2, 2, 64>(bp, st, sms);
+        if (op == 2) return run_delta64<2, 2, 4, 2, 16, 4>(d64, bp, tmap, st, sh, sms);
         return cudaErrorNotSupported;
     }
     if (s == 3) {
         if (op == 0) return run_delta<2, 3, 8, 2, 16, 4>(d32, bp, tmap, st, sh, sms);
         if (op == 1) return run_check<2, 3, 64>(bp, st, sms);
+        if (op == 2) return run_delta64<2, 3, 4, 2, 16, 2>(d64, bp, tmap, st, sh, sms);
         return cudaErrorNotSupported;
     }
     return cudaErrorInvalidValue;

@@ -23,6 +23,7 @@ cudaError_t band_k3(int op, int s, const BandParams& bp, const CUtensorMap* tmap
     if (s == 3) {
         if (op == 0) return run_delta<3, 3, 4, 2, 16, 4>(d32, bp, tmap, st, sh, sms);
         if (op == 1) return run_check<3, 3, 64>(bp, st, sms);
+        if (op == 2) return run_delta64<3, 3, 4, 2, 16, 2>(d64, bp, tmap, st, sh, sms);
         return cudaErrorNotSupported;
     }
     return cudaErrorInvalidValue;

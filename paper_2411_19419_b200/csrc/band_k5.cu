@@ -23,6 +23,7 @@ cudaError_t band_k5(int op, int s, const BandParams& bp, const CUtensorMap* tmap
     if (s == 3) {
         if (op == 0) return run_delta<5, 3, 4, 2, 16, 3>(d32, bp, tmap, st, sh, sms);
         if (op == 1) return run_check<5, 3, 64>(bp, st, sms);
+        if (op == 2) return run_delta64<5, 3, 4, 2, 16, 2>(d64, bp, tmap, st, sh, sms);
         return cudaErrorNotSupported;
     }
     return cudaErrorInvalidValue;

@@ -11,6 +11,7 @@ cudaError_t band_k7(int op, int s, const BandParams& bp, const CUtensorMap* tmap
     if (s == 1) {
         if (op == 0) return run_delta<7, 1, 8, 4, 32, 4>(d32, bp, tmap, st, sh, sms);
         if (op == 1) return run_check<7, 1, 128>(bp, st, sms);
+        if (op == 2) return run_delta64<7, 1, 4, 4, 16, 4>(d64, bp, tmap, st, sh, sms);
         return cudaErrorNotSupported;
     }
     if (s == 2) {
@@ -22,6 +23,7 @@ cudaError_t band_k7(int op, int s, const BandParams& bp, const CUtensorMap* tmap
     if (s == 3) {
         if (op == 0) return run_delta<7, 3, 4, 2, 16, 3>(d32, bp, tmap, st, sh, sms);
         if (op == 1) return run_check<7, 3, 64>(bp, st, sms);
+        if (op == 2) return run_delta64<7, 3, 4, 2, 16, 2>(d64, bp, tmap, st, sh, sms);
         return cudaErrorNotSupported;
     }
     return cudaErrorInvalidValue;

@@ -51,7 +51,8 @@ int band_tile_width(int k, int s) {
 // segments are 32 output columns (a warp's row-per-lane), the others the tile width.
 int band_seg_div(int k, int s) { return k == 11 ? band_tile_width(k, s) / 32 : 1; }
 
-bool band64_supported(int k, int s) { return ((k == 3 || k == 5) && s <= 2) || (k == 7 && s == 2); }
+// fp64 applies: every band geometry but k = 11 (121 double taps would not fit the registers)
+bool band64_supported(int k, int s) { return band_supported(k, s) && k != 11; }
 
 cudaError_t launch_band(int k, int s, const BandParams& bp, const CUtensorMap* tmap, cudaStream_t st,
                         BandShape* shape, int sms) {
