@@ -639,17 +639,17 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
             if (int rc = encode_x_map(&tmap, X, g, ldx, batch, sh.wc, sh.wr, 1, false)) return rc;
         // The fused form -- one kernel: consumers apply with the blocked sums
         // while up to four check warps per CTA verify the storage segment by
-        // segment -- for k <= 5, whose checks are light (config 3: 256 images
-        // 400 -> 362 us, 32 images 77 -> 64 us, 16 images 54 -> 44 us,
-        // scripts/ab_fused.py); with k >= 7 the checks (49 entries a row)
-        // outweigh the overlap (config 4 at 8 images: 368 us as two kernels,
-        // 585 fused), so the check runs as a kernel of its own.  Zero-tap
-        // kernels keep the two-kernel form (their masked checks are heavier).
-        // Option "fused" forces either form; the blocked path needs finite taps.
+        // segment -- where the checks are light: k <= 2, or k = 3 at s = 1
+        // (config 3: 256 images 400 -> 362 us, 32 images 77 -> 64 us; pruned
+        // k3: 416 -> 388 us).  Heavier checks outweigh the overlap (k5 s1 at 32
+        // images: 106 us as two kernels, 126 fused; config 4 at 8 images: 368
+        // against 585 us), so there the check runs as a kernel of its own
+        // (profiles/r02_exp/ab_forms.txt).  Option "fused" forces either form;
+        // the blocked path needs finite taps.
         // Both forms run on the caller's stream only: the check sees exactly
         // the matrix the stream order gives it.
         const int fsel = spb::opt(spb::kOptFused);
-        bp.fused = band_taps && bp.seg_div == 1 && (fsel ? fsel == 2 : g.k <= 5 && !bp.zt) ? 1 : 0;
+        bp.fused = band_taps && bp.seg_div == 1 && (fsel ? fsel == 2 : g.k <= 2 || (g.k == 3 && g.s == 1)) ? 1 : 0;
         if (bp.fused) {
             h->checked.store(true);
             const cudaError_t fe = spb::launch_band((int)g.k, (int)g.s, bp, &tmap, st, nullptr, sms);
