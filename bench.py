@@ -236,6 +236,17 @@ def parity_check(spec, kern, Xh, Y, which):
     return same, dev
 
 
+def orc_native(spec, kern32):
+    from oracle import Oracle
+    return Oracle().build_native(*spec, kern32)
+
+
+def spmm_oracle(ptr, idx, val, Xh, which):
+    from oracle import Oracle
+    X = np.stack([Xh[i].numpy() if hasattr(Xh[i], "numpy") else Xh[i] for i in which])
+    return Oracle().spmm_native(ptr, idx, val, X)
+
+
 def slice_probe(b: int):
     return sorted({0, b // 2, max(b - 1, 0)}) if b > 0 else []
 
@@ -646,6 +657,34 @@ def secondary_single(sp, torch, dev, stream, steps, peak):
     out["config4_per_rank_proxy_n8"] = line
     del X, Y, Xh
     t.close()
+    # ---- off the BASELINE shapes: config 5's widest geometry (257 x 193, k11
+    # s1 p10: odd width -> cp.async staging; 121 FMAs an output -> FMA-bound)
+    # and config 3's matrix uploaded as a generic CSR (no conv geometry: the
+    # row-block kernel) -- 256 images each
+    for name, spec, generic in (("config5_k11", (257, 193, 11, 1, 10), False),
+                                ("config3_generic_csr", (1024, 1024, 3, 1, 1), True)):
+        mm, nn, kk, ss, pp = spec
+        kv = problem_kernel(sp, 4 if not generic else 2, kk)
+        tt = sp.build_transform(sp.Kernel(kk, kv.astype(np.float64)), sp.ConvSpec(*spec), device=dev.index,
+                                stream=stream)
+        if generic:
+            ptr, idx, val = tt.export()
+            tt.close()
+            tt = sp.Transform.from_host(1024 * 1024, 1024 * 1024, ptr, idx, val, device=dev.index)
+        Xh = pinned_images(sp, torch, 4 if not generic else 2, 0, 256, tt.cols)
+        X = Xh.to(dev)
+        Y = torch.empty(256, tt.rows, device=dev)
+        line = device_line(sp, torch, tt, X, Y, 256, steps, dev, stream, peak)
+        line["workload"] = f"{spec}, 256 images" + (" (uploaded as a generic CSR)" if generic else "")
+        line["gflop_per_s"] = 2 * 256 * tt.nnz / (line["ms_per_step"] * 1e-3) / 1e9
+        if not generic:
+            ptr, idx, val = orc_native(spec, kv)
+            want = spmm_oracle(ptr, idx, val, Xh, slice_probe(256))
+            got = np.stack([Y[i].cpu().numpy() for i in slice_probe(256)])
+            line["parity"] = "bitexact" if np.array_equal(got.view(np.uint32), want.view(np.uint32)) else "MISMATCH"
+        out[name] = line
+        del X, Y, Xh
+        tt.close()
     # ---- config 2: one 512^2 image (cold L2) + the warm-L2 repeated SpMV ----
     cfg = CONFIGS[2]
     m, n, k, s, p = cfg["spec"]
