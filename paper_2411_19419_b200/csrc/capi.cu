@@ -604,7 +604,10 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
             const int stage = spb::opt(spb::kOptStage);
             const bool big = 8.0 * (double)h->nnz >= 8.0 * (1 << 20);
             cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-            if (stage == 0 && big) CK(cudaStreamIsCapturing(st, &cap));
+            if (stage == 0 && big && cudaStreamIsCapturing(st, &cap) != cudaSuccess) {
+                cudaGetLastError();  // (legacy stream during another thread's global capture)
+                cap = cudaStreamCaptureStatusActive;
+            }
             const bool win = spec && spb::spmv_win_ok(sp) &&
                              (stage == 2 || (stage == 0 && big && cap == cudaStreamCaptureStatusNone));
             for (int64_t b0 = 0; b0 < batch; b0 += 2) {  // <= 2 images per launch
