@@ -378,8 +378,7 @@ int csc_repair_apply(spconv_csr* h, const void* X, int64_t ldx, void* Y, int64_t
             ++rp[(size_t)ri[(size_t)e] + 1];
             ++used;
         }
-    int64_t kmax = 0;
-    for (int64_t r = 0; r < rows; ++r) kmax = std::max<int64_t>(kmax, rp[(size_t)r + 1]), rp[(size_t)r + 1] += rp[(size_t)r];
+    for (int64_t r = 0; r < rows; ++r) rp[(size_t)r + 1] += rp[(size_t)r];
     std::vector<int32_t> cur(rp.begin(), rp.end() - 1), ci((size_t)std::max<int64_t>(used, 1));
     std::vector<float> vv((size_t)std::max<int64_t>(used, 1));
     std::vector<double> vv64(cv64.empty() ? 0 : (size_t)std::max<int64_t>(used, 1));
@@ -416,7 +415,6 @@ int csc_repair_apply(spconv_csr* h, const void* X, int64_t ldx, void* Y, int64_t
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     cudaFree(mem);
     if (e != cudaSuccess) return cuda_fail(e, "CSC apply of the altered storage");
-    (void)kmax;
     return SPCONV_OK;
 }
 

@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(256) csc_gather(const CscGatherParams P) {
     bool bad = false;
 
     // ---- col_ptr against its closed form (csc_build.cu) ----
-    if (!P.skip_sweep) {
+    {
         for (long long c = gtid; c <= P.cols; c += nthr) {
             long long want = P.nnz;
             if (c < P.cols) {

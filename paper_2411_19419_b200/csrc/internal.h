@@ -161,7 +161,6 @@ struct CscGatherParams {
     long long zw[32];         // W[j] = sum_i nz[j][i] * #{y : tap i lands}
     long long chunk;          // fp64: columns per reference thread (0: one thread)
     int verify_only;          // 1: check the storage, no sums
-    int skip_sweep;           // 1: col_ptr already checked by the caller
     int* fail;                // set to 1 when the storage is not the transform of the taps
 };
 cudaError_t launch_csc_gather(const CscGatherParams& cp, bool f64, cudaStream_t st, int sms);
