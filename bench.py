@@ -905,6 +905,7 @@ def run_densenet(args):
                    "timing": f"per layer: CUDA graph of {res['graph_reps']} SpMV launches, "
                              f"{args.steps} replays; totals = sum of per-layer means"},
         "total_device_sem_us": res["total_device_sem_us"],
+        "total_csc_device_us": res["total_csc_device_us"],
         "network_graph_us": res["network_graph_us"],
         "total_build_us": res["total_build_us"],
         "e2e": {"value": res["total_host_us"], "unit": "us", "h2d_bytes_per_step": h2d,

@@ -8,7 +8,9 @@ built once on the device (build time reported separately, as
 
 * ``device``: one SpMV on a device-resident image, timed as a CUDA graph of
   ``graph_reps`` back-to-back launches replayed per trial (launch overhead
-  amortised the way a GPU-resident network would see it);
+  amortised the way a GPU-resident network would see it); the same for the
+  layer as a CSC transform (the reference's CSC-SpMV column: the CSC storage
+  itself is read), its output checked equal to the CSR one;
 * ``host``: the reference's call shape -- an fp32 image in pinned host memory,
   H2D + SpMV + D2H through the C ABI (``spconv_convolve_host``) per trial.
 
@@ -112,6 +114,32 @@ def run_table_bench(layers: List[LayerConfig] = None, trials: int = 100, warmup:
                 ev[i][1].record(stream)
             torch.cuda.synchronize(dev)
             dev_us = [a_.elapsed_time(b_) * 1e3 / graph_reps for a_, b_ in ev]
+            # the same layer as a CSC transform (the reference's CSC-SpMV column):
+            # the CSC storage itself is read (csc_gather), cross-checked bit for bit
+            tc = build_transform(Kernel(L.k, w.reshape(-1)), spec, layout=1, device=device, stream=stream)
+            yc = torch.empty(t.rows, dtype=torch.float32, device=dev)
+            spmv(tc, x, yc, stream=stream)
+            torch.cuda.synchronize(dev)
+            if not torch.equal(yc, y):
+                raise RuntimeError(f"CSC / CSR outputs differ for layer '{L.name}'")
+            gc = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gc, stream=stream):
+                for _ in range(graph_reps):
+                    spmv(tc, x, yc, stream=stream)
+            for _ in range(warmup):
+                gc.replay()
+            torch.cuda.synchronize(dev)
+            evc = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(trials)]
+            for i in range(trials):
+                evc[i][0].record(stream)
+                gc.replay()
+                evc[i][1].record(stream)
+            torch.cuda.synchronize(dev)
+            csc_us = [a_.elapsed_time(b_) * 1e3 / graph_reps for a_, b_ in evc]
+            csc_kernel = tc.last_kernel
+            del gc
+            tc.close()
             # host call shape: pinned fp32 image in, fp32 out (H2D + SpMV + D2H)
             xh = torch.from_numpy(a.reshape(1, -1)).pin_memory()
             yh = torch.empty(1, t.rows, dtype=torch.float32).pin_memory()
@@ -124,9 +152,11 @@ def run_table_bench(layers: List[LayerConfig] = None, trials: int = 100, warmup:
                 host_us.append((time.perf_counter() - h0) * 1e6)
             dm, ds = _stats(dev_us)
             hm, hs = _stats(host_us)
+            cm, cs_ = _stats(csc_us)
             rows.append(dict(layer=L.name, m=L.m, n=L.n, k=L.k, s=L.s, p=L.p, nnz=t.nnz,
                              kernel=kernel_name, device_mean_us=dm, device_sem_us=ds,
-                             host_mean_us=hm, host_sem_us=hs, build_time_us=build_us))
+                             host_mean_us=hm, host_sem_us=hs, build_time_us=build_us,
+                             csc_kernel=csc_kernel, csc_device_mean_us=cm, csc_device_sem_us=cs_))
             keep.append((t, x, y, g))
             graphs_all.append((t, x, y))
         # whole network: every layer's SpMV back to back in one graph
@@ -153,6 +183,7 @@ def run_table_bench(layers: List[LayerConfig] = None, trials: int = 100, warmup:
     return {
         "layers": rows,
         "total_device_us": tot("device_mean_us"), "total_device_sem_us": rss("device_sem_us"),
+        "total_csc_device_us": tot("csc_device_mean_us"),
         "total_host_us": tot("host_mean_us"), "total_host_sem_us": rss("host_sem_us"),
         "total_build_us": tot("build_time_us"),
         "network_graph_us": nm, "network_graph_sem_us": ns,
@@ -162,19 +193,20 @@ def run_table_bench(layers: List[LayerConfig] = None, trials: int = 100, warmup:
 
 def markdown(res: Dict, ref: Dict = None) -> str:
     """Per-layer table in the reference report's shape (inc/bench.hpp:318-349)."""
-    out = ["| layer | m | n | k | s | p | nnz | device mean us | sem | host mean us | sem | build us |"
-           + (" reference CSR-SpMV us |" if ref else ""),
-           "|---|---|---|---|---|---|---|---|---|---|---|---|" + ("---|" if ref else "")]
+    out = ["| layer | m | n | k | s | p | nnz | device CSR us | sem | device CSC us | host mean us | sem | build us |"
+           + (" reference CSR-SpMV us | reference CSC-SpMV us |" if ref else ""),
+           "|---|---|---|---|---|---|---|---|---|---|---|---|---|" + ("---|---|" if ref else "")]
     for i, r in enumerate(res["layers"]):
         line = (f"| {r['layer']} | {r['m']} | {r['n']} | {r['k']} | {r['s']} | {r['p']} | {r['nnz']} | "
-                f"{r['device_mean_us']:.3f} | {r['device_sem_us']:.3f} | {r['host_mean_us']:.3f} | "
-                f"{r['host_sem_us']:.3f} | {r['build_time_us']:.1f} |")
+                f"{r['device_mean_us']:.3f} | {r['device_sem_us']:.3f} | {r['csc_device_mean_us']:.3f} | "
+                f"{r['host_mean_us']:.3f} | {r['host_sem_us']:.3f} | {r['build_time_us']:.1f} |")
         if ref:
-            line += f" {ref['layers'][i]['CSR-SpMV'][0]:.3f} |"
+            line += f" {ref['layers'][i]['CSR-SpMV'][0]:.3f} | {ref['layers'][i]['CSC-SpMV'][0]:.3f} |"
         out.append(line)
     line = (f"| TOTAL | | | | | | | {res['total_device_us']:.3f} | {res['total_device_sem_us']:.3f} | "
-            f"{res['total_host_us']:.3f} | {res['total_host_sem_us']:.3f} | {res['total_build_us']:.1f} |")
+            f"{res['total_csc_device_us']:.3f} | {res['total_host_us']:.3f} | {res['total_host_sem_us']:.3f} | "
+            f"{res['total_build_us']:.1f} |")
     if ref:
-        line += f" {ref['total_csr_us']:.3f} |"
+        line += f" {ref['total_csr_us']:.3f} | {ref['total_csc_us']:.3f} |"
     out.append(line)
     return "\n".join(out) + "\n"
