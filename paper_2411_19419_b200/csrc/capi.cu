@@ -307,6 +307,10 @@ spb::CscGatherParams csc_params(const spconv_csr* h, bool f64) {
     cp.nnz = h->nnz;
     cp.fail = h->fail_flag;
     csc_tables(h, cp);
+    if (g.k <= 7 && h->host_taps64.empty() && h->host_taps.size() == (size_t)(g.k * g.k)) {
+        cp.inline_taps = 1;
+        for (size_t q = 0; q < h->host_taps.size(); ++q) cp.it32[q] = h->host_taps[q];
+    }
     return cp;
 }
 
@@ -531,6 +535,13 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
             cp.Y = Y;
             cp.ldy = ldy;
             cp.batch = (int)batch;
+            if (batch <= 2 && cp.inline_taps) {
+                // (no PDL right behind the handle's own build: its writes are visible at its end)
+                const bool pdl = h->applied.exchange(true);
+                CK(spb::launch_csc_gather_lat(cp, st, device_sm_count(), pdl));
+                h->last_kernel.store("csc_gather_lat");
+                return SPCONV_OK;
+            }
             CK(spb::launch_csc_gather(cp, false, st, device_sm_count()));
             h->last_kernel.store("csc_gather");
             return SPCONV_OK;

@@ -193,6 +193,138 @@ __global__ void __launch_bounds__(256) csc_gather(const CscGatherParams P) {
     if (__syncthreads_or(bad) && threadIdx.x == 0) *P.fail = 1;
 }
 
+// One or two images, k <= 7, dense or zero-tap fp32 taps (the DenseNet
+// CSC-SpMV column): the same reads and checks as csc_gather with a row's loads
+// issued all at once -- col_ptr of its k^2 columns, then their (row, value)
+// entries, both before griddepcontrol.wait (the matrix is never the previous
+// kernel's output), then the x gathers -- and the taps in the kernel
+// parameters.  Launched as a programmatic dependent, a chained call fetches
+// and checks its matrix while the previous kernel runs.
+template <int KC>
+__global__ void __launch_bounds__(128) csc_gather_lat(const CscGatherParams P) {
+    constexpr int KK = KC * KC;
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const long long gtid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long nthr = (long long)gridDim.x * blockDim.x;
+    const int S = P.s;
+    bool bad = false;
+    for (long long c = gtid; c <= P.cols; c += nthr) {  // col_ptr against its closed form
+        long long want = P.nnz;
+        if (c < P.cols) {
+            const int a = (int)(c / P.n), b = (int)(c - (long long)a * P.n);
+            want = 0;
+            int nzj[KC];
+#pragma unroll
+            for (int i = 0; i < KC; ++i) nzj[i] = 0;
+#pragma unroll
+            for (int j = 0; j < KC; ++j) {
+                want += P.zw[j] * slides_below_g(j, a, P.mo, S, P.p);
+                const int d = a + P.p - j;
+                if (d >= 0 && d % S == 0 && d / S < P.mo)
+#pragma unroll
+                    for (int i = 0; i < KC; ++i) nzj[i] += (P.nzrow[j] >> i) & 1u;
+            }
+#pragma unroll
+            for (int i = 0; i < KC; ++i) want += (long long)nzj[i] * slides_below_g(i, b, P.no, S, P.p);
+        }
+        bad |= (long long)__ldg(P.col_ptr + c) != want;
+    }
+    const long long r = gtid;
+    bool live = r < P.rows;
+    int x = 0, y = 0, jlo = 0, jhi = 0, ilo = 0, ihi = 0;
+    long long rb = 0;
+    if (live) {
+        x = (int)(r / P.no);
+        y = (int)(r - (long long)x * P.no);
+        tap_range_g(x, P.m, KC, S, P.p, jlo, jhi);
+        tap_range_g(y, P.n, KC, S, P.p, ilo, ihi);
+        rb = (long long)(S * x - P.p) * P.n + (S * y - P.p);
+    }
+    bool st[KK];
+    int cp[KK];
+#pragma unroll
+    for (int q = 0; q < KK; ++q) {
+        const int j = q / KC, i = q - j * KC;
+        st[q] = live && j >= jlo && j < jhi && i >= ilo && i < ihi && ((P.nzrow[j] >> i) & 1u);
+        cp[q] = st[q] ? __ldg(P.col_ptr + rb + (long long)j * P.n + i) : 0;
+    }
+    int rw[KK];
+    uint32_t vw[KK];
+#pragma unroll
+    for (int q = 0; q < KK; ++q) {
+        const int j = q / KC, i = q - j * KC;
+        rw[q] = (int)r;
+        vw[q] = __float_as_uint(P.it32[q]);
+        if (!st[q]) continue;
+        const int idxJ = min((KC - 1 - j) / S, x), idxI = min((KC - 1 - i) / S, y);
+        int rank;
+        if (!P.zt) {
+            rank = idxJ * (idxI + 1 + min(i / S, P.no - 1 - y)) + idxI;
+        } else {
+            uint32_t mi = 0;
+            for (int d = -min(i / S, P.no - 1 - y); d <= idxI; ++d) mi |= 1u << (i + d * S);
+            rank = __popc(P.nzrow[j] & mi & ~((2u << i) - 1u));
+            for (int d = 1; d <= idxJ; ++d) rank += __popc(P.nzrow[j + d * S] & mi);
+        }
+        const long long pos = (long long)cp[q] + rank;
+        if (pos < 0 || pos >= P.nnz) {
+            bad = true;
+            continue;
+        }
+        rw[q] = __ldg(P.row_idx + pos);
+        vw[q] = __float_as_uint(__ldg(P.vals + pos));
+    }
+#pragma unroll
+    for (int q = 0; q < KK; ++q)
+        if (st[q]) bad |= rw[q] != (int)r || vw[q] != __float_as_uint(P.it32[q]);
+    // x may be the previous kernel's output: the gathers wait for it
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (live) {
+        for (int b = 0; b < P.batch; ++b) {
+            const float* X = reinterpret_cast<const float*>(P.X) + (long long)b * P.ldx;
+            float xv[KK];
+#pragma unroll
+            for (int q = 0; q < KK; ++q) {
+                const int j = q / KC, i = q - j * KC;
+                xv[q] = st[q] ? __ldg(X + rb + (long long)j * P.n + i) : 0.0f;
+            }
+            float acc = 0.0f;
+#pragma unroll
+            for (int q = 0; q < KK; ++q)
+                if (st[q]) acc = fmaf(P.it32[q], xv[q], acc);
+            reinterpret_cast<float*>(P.Y)[(long long)b * P.ldy + r] = acc;
+        }
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) *P.fail = 1;
+}
+
+cudaError_t launch_csc_gather_lat(const CscGatherParams& cp, cudaStream_t st, int sms, bool pdl) {
+    (void)sms;
+    if (cp.batch > 2 || cp.k > 7 || !cp.inline_taps) return cudaErrorInvalidValue;
+    const long long work = std::max<long long>(cp.rows, cp.cols + 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)((cp.rows + 127) / 128 > 0 ? (cp.rows + 127) / 128 : 1));
+    // (the col_ptr sweep strides over the same threads: enough of them for cols + 1)
+    if ((long long)cfg.gridDim.x * 128 < work) cfg.gridDim.x = (unsigned)((work + 127) / 128);
+    cfg.blockDim = dim3(128);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    switch (cp.k) {
+        case 1: return cudaLaunchKernelEx(&cfg, csc_gather_lat<1>, cp);
+        case 2: return cudaLaunchKernelEx(&cfg, csc_gather_lat<2>, cp);
+        case 3: return cudaLaunchKernelEx(&cfg, csc_gather_lat<3>, cp);
+        case 4: return cudaLaunchKernelEx(&cfg, csc_gather_lat<4>, cp);
+        case 5: return cudaLaunchKernelEx(&cfg, csc_gather_lat<5>, cp);
+        case 6: return cudaLaunchKernelEx(&cfg, csc_gather_lat<6>, cp);
+        case 7: return cudaLaunchKernelEx(&cfg, csc_gather_lat<7>, cp);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
 cudaError_t launch_csc_gather(const CscGatherParams& cp, bool f64, cudaStream_t st, int sms) {
     if (cp.k > 32) return cudaErrorInvalidValue;
     const long long work = std::max<long long>(cp.rows, cp.cols + 1);

@@ -162,8 +162,12 @@ struct CscGatherParams {
     long long chunk;          // fp64: columns per reference thread (0: one thread)
     int verify_only;          // 1: check the storage, no sums
     int* fail;                // set to 1 when the storage is not the transform of the taps
+    int inline_taps;          // k <= 7: the fp32 taps below (the latency kernel reads them from here)
+    float it32[49];
 };
 cudaError_t launch_csc_gather(const CscGatherParams& cp, bool f64, cudaStream_t st, int sms);
+// One or two fp32 images, k <= 7 (taps inline): loads issued a row at a time, PDL-chained.
+cudaError_t launch_csc_gather_lat(const CscGatherParams& cp, cudaStream_t st, int sms, bool pdl);
 
 struct BandShape {
     int th, tw, wr, wc, smem, threads, occ;

@@ -97,8 +97,8 @@ def test_csc_native_apply(sp, orc, torch_cuda, spec, zero):
         assert np.array_equal(bits(Y), bits(want[:b])), (spec, b)
         if b >= 3 and (k, s) in BAND and (not zero or k <= 7):  # (zero-tap masks: k <= 7)
             assert t.last_kernel in CSC_BAND_KERNELS, t.last_kernel
-        else:
-            assert t.last_kernel == "csc_gather", t.last_kernel
+        else:  # (one or two images, k <= 7: the row-at-a-time PDL form)
+            assert t.last_kernel == ("csc_gather_lat" if b <= 2 and k <= 7 else "csc_gather"), t.last_kernel
     assert t.band_check_status()[1] == 0 if (k, s) in BAND else True
 
 
