@@ -203,6 +203,22 @@ int spconv_spmm(const spconv_csr* h, const float* X_dev, int64_t ldx, float* Y_d
  * PCIe overlap. */
 int spconv_convolve_host(const spconv_csr* h, const float* X_host, float* Y_host, int64_t batch);
 
+/* Grouped apply: y_dev[i] = T_i x_dev[i] for i < count, every member a
+ * transform of its own (one vector each), all on one device, in ONE launch
+ * for the CSR members (group.cu); CSC members apply as spconv_spmv would.
+ * Each y is bit-identical to spconv_spmv(hs[i], x_dev[i], y_dev[i]).  The y
+ * ranges may not overlap each other or any x.  The layer-table loop of
+ * inc/bench.hpp:202-349 (one convolve per layer) as a single call. */
+int spconv_spmv_group(const spconv_csr* const* hs, int64_t count, const float* const* x_dev,
+                      float* const* y_dev, void* stream);
+
+/* spconv_spmv_group on HOST vectors (x_host[i]: cols_i floats, y_host[i]:
+ * rows_i floats, any host memory): the inputs are packed into a page-locked
+ * staging buffer, copied in one transfer, applied in one launch, and the
+ * outputs copied back in one transfer; returns when every y is written. */
+int spconv_convolve_host_group(const spconv_csr* const* hs, int64_t count, const float* const* x_host,
+                               float* const* y_host);
+
 /* fp64 SpMM on device buffers with the reference's own arithmetic: per row
  * acc = 0.0; acc = acc + (double)val * x[col] over the stored entries in
  * order, one rounded multiply and one rounded add each (inc/sparse.hpp:185-191

@@ -1960,6 +1960,177 @@ int spconv_convolve_host(const spconv_csr* hc, const float* X_host, float* Y_hos
     return SPCONV_OK;
 }
 
+// ---- grouped apply (group.cu) ----
+
+// Members' y ranges pairwise disjoint and disjoint from every x (x ranges may
+// share memory): one sweep over the ranges sorted by start.
+static bool group_ranges_ok(const spconv_csr* const* hs, int64_t count, const float* const* xs,
+                            float* const* ys) {
+    struct R {
+        const float* a;
+        const float* b;
+        bool out;
+    };
+    std::vector<R> v;
+    v.reserve((size_t)(2 * count));
+    for (int64_t i = 0; i < count; ++i) {
+        if (hs[i]->cols > 0) v.push_back({xs[i], xs[i] + hs[i]->cols, false});
+        if (hs[i]->rows > 0) v.push_back({ys[i], ys[i] + hs[i]->rows, true});
+    }
+    std::sort(v.begin(), v.end(), [](const R& p, const R& q) { return p.a < q.a; });
+    const float* yend = nullptr;
+    const float* xend = nullptr;
+    for (const R& r : v) {
+        if (r.out) {
+            if ((yend && r.a < yend) || (xend && r.a < xend)) return false;
+            if (!yend || r.b > yend) yend = r.b;
+        } else {
+            if (yend && r.a < yend) return false;
+            if (!xend || r.b > xend) xend = r.b;
+        }
+    }
+    return true;
+}
+
+static int group_check(const char* who, const spconv_csr* const* hs, int64_t count, const void* const* xs,
+                       void* const* ys, int* device) {
+    if (count < 0) return fail(SPCONV_EINVAL, std::string(who) + ": negative count");
+    if (count > 0 && (!hs || !xs || !ys)) return fail(SPCONV_EINVAL, std::string(who) + ": null array");
+    for (int64_t i = 0; i < count; ++i) {
+        if (!hs[i]) return fail(SPCONV_EINVAL, std::string(who) + ": null handle");
+        if ((hs[i]->cols > 0 && !xs[i]) || (hs[i]->rows > 0 && !ys[i]))
+            return fail(SPCONV_EINVAL, std::string(who) + ": null buffer");
+        if (hs[i]->device != hs[0]->device) return fail(SPCONV_EINVAL, std::string(who) + ": handles on different devices");
+        if (hs[i]->rows > INT32_MAX) return fail(SPCONV_EINVAL, std::string(who) + ": matrix too large");
+    }
+    *device = count > 0 ? hs[0]->device : 0;
+    return SPCONV_OK;
+}
+
+// Enqueue the group on `st`: CSR members in launches of up to kGroupMax, the
+// others one apply each.
+static int run_group(const spconv_csr* const* hs, int64_t count, const float* const* xs, float* const* ys,
+                     cudaStream_t st) {
+    spb::GroupParams gp;
+    gp.count = 0;
+    int blocks = 0;
+    auto flush = [&]() -> int {
+        if (gp.count > 0) CK(spb::launch_spmv_group(gp, blocks, st));
+        gp.count = 0;
+        blocks = 0;
+        return SPCONV_OK;
+    };
+    for (int64_t i = 0; i < count; ++i) {
+        auto* h = const_cast<spconv_csr*>(hs[i]);
+        if (h->rows == 0) continue;
+        if (!h->row_ptr) {  // CSC-only storage: its own apply
+            if (int rc = run_spmm(h, xs[i], h->cols, ys[i], h->rows, 1, st)) return rc;
+            continue;
+        }
+        const int nb = spb::group_blocks(h->rows);
+        if (gp.count == spb::kGroupMax || (int64_t)blocks + nb > INT32_MAX / 2)
+            if (int rc = flush()) return rc;
+        gp.m[gp.count++] = {h->row_ptr, h->col_idx, h->vals, xs[i], ys[i], (int)h->rows, blocks};
+        blocks += nb;
+        h->last_kernel.store("csr_spmv_group");
+    }
+    return flush();
+}
+
+int spconv_spmv_group(const spconv_csr* const* hs, int64_t count, const float* const* x_dev, float* const* y_dev,
+                      void* stream) {
+    int dev = 0;
+    if (int rc = group_check("spconv_spmv_group", hs, count, reinterpret_cast<const void* const*>(x_dev),
+                             reinterpret_cast<void* const*>(y_dev), &dev))
+        return rc;
+    if (count == 0) return SPCONV_OK;
+    if (!group_ranges_ok(hs, count, x_dev, y_dev))
+        return fail(SPCONV_EINVAL, "spconv_spmv_group: a y overlaps another member's x or y");
+    DeviceGuard dg(dev);
+    if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
+    return run_group(hs, count, x_dev, y_dev, static_cast<cudaStream_t>(stream));
+}
+
+namespace {
+// Per-device staging of spconv_convolve_host_group (grown on demand, kept).
+struct GroupWs {
+    std::mutex mu;
+    cudaStream_t st = nullptr;
+    float* pin_in = nullptr;
+    float* pin_out = nullptr;
+    float* dx = nullptr;
+    float* dy = nullptr;
+    size_t cap_in = 0, cap_out = 0;  // floats
+};
+GroupWs g_group_ws[64];
+}  // namespace
+
+int spconv_convolve_host_group(const spconv_csr* const* hs, int64_t count, const float* const* x_host,
+                               float* const* y_host) {
+    int dev = 0;
+    if (int rc = group_check("spconv_convolve_host_group", hs, count, reinterpret_cast<const void* const*>(x_host),
+                             reinterpret_cast<void* const*>(y_host), &dev))
+        return rc;
+    if (count == 0) return SPCONV_OK;
+    if (dev < 0 || dev >= 64) return fail(SPCONV_EINVAL, "spconv_convolve_host_group: device index");
+    DeviceGuard dg(dev);
+    if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
+    // packed layout, members 16-byte aligned (the band / TMA paths of CSC members)
+    std::vector<size_t> xo((size_t)count), yo((size_t)count);
+    size_t nin = 0, nout = 0;
+    for (int64_t i = 0; i < count; ++i) {
+        xo[(size_t)i] = nin;
+        yo[(size_t)i] = nout;
+        nin += ((size_t)hs[i]->cols + 3) & ~size_t(3);
+        nout += ((size_t)hs[i]->rows + 3) & ~size_t(3);
+    }
+    GroupWs& w = g_group_ws[dev];
+    std::lock_guard<std::mutex> lk(w.mu);
+    if (!w.st) CK(cudaStreamCreateWithFlags(&w.st, cudaStreamNonBlocking));
+    if (w.cap_in < nin) {
+        if (w.pin_in) cudaFreeHost(w.pin_in), w.pin_in = nullptr;
+        if (w.dx) cudaFree(w.dx), w.dx = nullptr;
+        w.cap_in = 0;
+        CK(cudaHostAlloc(&w.pin_in, nin * 4, cudaHostAllocDefault));
+        CK(cudaMalloc(&w.dx, nin * 4));
+        w.cap_in = nin;
+    }
+    if (w.cap_out < nout) {
+        if (w.pin_out) cudaFreeHost(w.pin_out), w.pin_out = nullptr;
+        if (w.dy) cudaFree(w.dy), w.dy = nullptr;
+        w.cap_out = 0;
+        CK(cudaHostAlloc(&w.pin_out, nout * 4, cudaHostAllocDefault));
+        CK(cudaMalloc(&w.dy, nout * 4));
+        w.cap_out = nout;
+    }
+    // builds only enqueue: wait for those not yet seen complete
+    for (int64_t i = 0; i < count; ++i) {
+        auto* h = const_cast<spconv_csr*>(hs[i]);
+        if (!h->built || h->build_seen.load()) continue;
+        if (cudaEventQuery(h->built) == cudaSuccess) {
+            h->build_seen.store(true);
+            continue;
+        }
+        cudaGetLastError();
+        CK(cudaStreamWaitEvent(w.st, h->built, 0));
+    }
+    for (int64_t i = 0; i < count; ++i)
+        if (hs[i]->cols > 0) std::memcpy(w.pin_in + xo[(size_t)i], x_host[i], (size_t)hs[i]->cols * 4);
+    CK(cudaMemcpyAsync(w.dx, w.pin_in, nin * 4, cudaMemcpyHostToDevice, w.st));
+    std::vector<const float*> xs((size_t)count);
+    std::vector<float*> ys((size_t)count);
+    for (int64_t i = 0; i < count; ++i) xs[(size_t)i] = w.dx + xo[(size_t)i], ys[(size_t)i] = w.dy + yo[(size_t)i];
+    if (int rc = run_group(hs, count, xs.data(), ys.data(), w.st)) {
+        cudaStreamSynchronize(w.st);
+        return rc;
+    }
+    CK(cudaMemcpyAsync(w.pin_out, w.dy, nout * 4, cudaMemcpyDeviceToHost, w.st));
+    CK(cudaStreamSynchronize(w.st));
+    for (int64_t i = 0; i < count; ++i)
+        if (hs[i]->rows > 0) std::memcpy(y_host[i], w.pin_out + yo[(size_t)i], (size_t)hs[i]->rows * 4);
+    return SPCONV_OK;
+}
+
 int spconv_spmm_f64(const spconv_csr* h, const double* X_dev, int64_t ldx, double* Y_dev, int64_t ldy,
                     int64_t batch, void* stream) {
     return spconv_spmm_f64_threads(h, X_dev, ldx, Y_dev, ldy, batch, 1, stream);

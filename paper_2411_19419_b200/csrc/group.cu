@@ -1,0 +1,68 @@
+// group.cu -- one launch applies a list of CSR transforms, each to its own
+// vector (spconv_spmv_group / spconv_convolve_host_group).
+//
+// The DenseNet121 table (inc/bench.hpp:202-349) is 123 small transforms
+// (7^2 .. 224^2 outputs, 1-49 entries a row): applied one kernel at a time,
+// the device time is launch-bound (123 launches, ~1 us of work each) and a
+// host-buffer call per layer pays the box's ~9 us launch+sync round trip
+// (scripts/probe_host_lat.cu).  Here every layer's rows become CTAs of ONE
+// grid: CTA b finds its member by a binary search over the members' first
+// block, each thread owns one output row and evaluates it exactly as the
+// per-layer kernels do -- acc = +0.0f; for e in row (stored order):
+// acc = fmaf(vals[e], x[col_idx[e]], acc) -- so the outputs are bit-identical
+// to spconv_spmv on each member (the reference's row loop,
+// inc/sparse.hpp:180-192, evaluated in fp32 with fmaf).
+//
+// Loads are issued in groups of G entries (all column indices and values,
+// then all x gathers), so a 9-entry row costs three dependent round trips
+// (row_ptr, entries, x) whatever its length up to G.
+#include "internal.h"
+
+namespace spb {
+
+namespace {
+
+constexpr int kThreads = 128;
+constexpr int kG = 16;
+
+__global__ void __launch_bounds__(kThreads) csr_spmv_group(const GroupParams P) {
+    // member owning this block: the last m with blk0[m] <= blockIdx.x
+    int lo = 0, hi = P.count - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (P.m[mid].blk0 <= (int)blockIdx.x) lo = mid;
+        else hi = mid - 1;
+    }
+    const GroupMember& M = P.m[lo];
+    const int r = ((int)blockIdx.x - M.blk0) * kThreads + (int)threadIdx.x;
+    if (r >= M.rows) return;
+    const int e0 = __ldg(M.row_ptr + r), e1 = __ldg(M.row_ptr + r + 1);
+    float acc = 0.0f;
+    for (int e = e0; e < e1; e += kG) {
+        int c[kG];
+        float v[kG], xv[kG];
+#pragma unroll
+        for (int q = 0; q < kG; ++q) {
+            c[q] = e + q < e1 ? __ldg(M.col_idx + e + q) : 0;
+            v[q] = e + q < e1 ? __ldg(M.vals + e + q) : 0.0f;
+        }
+#pragma unroll
+        for (int q = 0; q < kG; ++q) xv[q] = e + q < e1 ? __ldg(M.x + c[q]) : 0.0f;
+#pragma unroll
+        for (int q = 0; q < kG; ++q)
+            if (e + q < e1) acc = fmaf(v[q], xv[q], acc);
+    }
+    M.y[r] = acc;
+}
+
+}  // namespace
+
+cudaError_t launch_spmv_group(const GroupParams& gp, int blocks, cudaStream_t st) {
+    if (gp.count <= 0 || blocks <= 0) return cudaSuccess;
+    csr_spmv_group<<<blocks, kThreads, 0, st>>>(gp);
+    return cudaGetLastError();
+}
+
+int group_blocks(int64_t rows) { return (int)((rows + kThreads - 1) / kThreads); }
+
+}  // namespace spb

@@ -169,6 +169,25 @@ cudaError_t launch_csc_gather(const CscGatherParams& cp, bool f64, cudaStream_t 
 // One or two fp32 images, k <= 7 (taps inline): loads issued a row at a time, PDL-chained.
 cudaError_t launch_csc_gather_lat(const CscGatherParams& cp, cudaStream_t st, int sms, bool pdl);
 
+// One launch over a list of CSR transforms, each applied to its own vector
+// (group.cu).  Member m owns blocks [blk0, next blk0) of the grid.
+struct GroupMember {
+    const int32_t* row_ptr;
+    const int32_t* col_idx;
+    const float* vals;
+    const float* x;
+    float* y;
+    int rows;
+    int blk0;
+};
+constexpr int kGroupMax = 128;  // members per launch (6 KB of kernel parameters)
+struct GroupParams {
+    int count;
+    GroupMember m[kGroupMax];
+};
+cudaError_t launch_spmv_group(const GroupParams& gp, int blocks, cudaStream_t st);
+int group_blocks(int64_t rows);
+
 struct BandShape {
     int th, tw, wr, wc, smem, threads, occ;
 };
@@ -337,6 +356,7 @@ struct spconv_csr {
     std::atomic<bool> exposed{false};
     std::atomic<bool> checked{false};  // a band check has been enqueued (seg_ok holds verdicts)  // spconv_csr_device_ptrs handed out the CSC arrays: verify before use
     cudaEvent_t built = nullptr;  // recorded after the build on the build stream (host-buffer calls wait on it)
+    std::atomic<bool> build_seen{false};  // the built event has been observed complete
     std::atomic<bool> applied{false};  // an apply was enqueued after the build (PDL is safe from then on)
     std::atomic<const char*> last_kernel{nullptr};  // diagnostics: last SpMM kernel launched
     // Workspace of spconv_convolve_host (lazily created, guarded by ws_mu).

@@ -20,7 +20,10 @@ restated in numpy) within the north-star tolerance
 |y - ref| <= 1e-5 * sum|w x|, as the reference harness cross-checks its
 methods (inc/bench.hpp:218-233).  Totals are sums of per-layer means and the
 root-sum-square of per-layer SEMs (inc/bench.hpp:284-349).  A whole-network
-graph (all 123 layers back to back) gives the end-to-end pass time.
+graph (all 123 layers back to back) gives the end-to-end pass time, and the
+grouped apply (``spmv_group``: the 123 layers in ONE launch; on host arrays
+``convolve_group``: one packed copy each way) the same pass without the
+per-layer launches.
 """
 from __future__ import annotations
 
@@ -63,7 +66,7 @@ def run_table_bench(layers: List[LayerConfig] = None, trials: int = 100, warmup:
                     graph_reps: int = 20, seed: int = 42, device: int = 0) -> Dict:
     import torch
 
-    from . import ConvSpec, Kernel, build_transform, spmv
+    from . import ConvSpec, Kernel, build_transform, convolve_group, spmv, spmv_group
     from . import lib, _check
 
     layers = layers or densenet121_layers()
@@ -175,11 +178,73 @@ def run_table_bench(layers: List[LayerConfig] = None, trials: int = 100, warmup:
             e1.record(stream)
             torch.cuda.synchronize(dev)
             net_us.append(e0.elapsed_time(e1) * 1e3)
+        # whole network as ONE grouped launch (spconv_spmv_group): every
+        # layer's output checked equal to its own SpMV's, then a graph of
+        # graph_reps grouped launches replayed per trial
+        ts = [t for t, _, _ in graphs_all]
+        xs = [x for _, x, _ in graphs_all]
+        yg = [torch.empty_like(y) for _, _, y in graphs_all]
+        spmv_group(ts, xs, yg, stream=stream)
+        torch.cuda.synchronize(dev)
+        for (t, x, y), z in zip(graphs_all, yg):
+            if not torch.equal(y, z):
+                raise RuntimeError("grouped and per-layer outputs differ")
+        ggr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(ggr, stream=stream):
+            for _ in range(graph_reps):
+                spmv_group(ts, xs, yg, stream=stream)
+        for _ in range(warmup):
+            ggr.replay()
+        torch.cuda.synchronize(dev)
+        grp_us = []
+        for _ in range(trials):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ggr.replay()
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            grp_us.append(e0.elapsed_time(e1) * 1e3 / graph_reps)
+        del ggr
+    # the whole table end to end through the host-buffer grouped call: the
+    # images as numpy arrays in, numpy arrays out (convolve_group)
+    imgs = [x.cpu().numpy() for x in xs]
+    want = [y.cpu().numpy() for _, _, y in graphs_all]
+    got = convolve_group(ts, imgs)
+    if not all(np.array_equal(a_.view(np.uint32), b_.view(np.uint32)) for a_, b_ in zip(got, want)):
+        raise RuntimeError("host grouped outputs differ from the per-layer SpMVs")
+    for _ in range(warmup):
+        convolve_group(ts, imgs)
+    e2e_py = []
+    for _ in range(trials):
+        h0 = time.perf_counter()
+        convolve_group(ts, imgs)
+        e2e_py.append((time.perf_counter() - h0) * 1e6)
+    # the C-ABI call itself, its pointer arrays set up once (what a C / C++
+    # caller holds): pageable host images in, pageable outputs out
+    outs = [np.empty(t.rows, np.float32) for t in ts]
+    nl = len(ts)
+    H = np.fromiter((t._h.value for t in ts), np.uintp, nl)
+    X = np.fromiter((x.__array_interface__["data"][0] for x in imgs), np.uintp, nl)
+    Y = np.fromiter((y.__array_interface__["data"][0] for y in outs), np.uintp, nl)
+    call = lambda: _check(lib.spconv_convolve_host_group(H.ctypes.data, nl, X.ctypes.data, Y.ctypes.data))  # noqa: E731
+    call()
+    if not all(np.array_equal(a_.view(np.uint32), b_.view(np.uint32)) for a_, b_ in zip(outs, want)):
+        raise RuntimeError("host grouped outputs differ from the per-layer SpMVs")
+    for _ in range(warmup):
+        call()
+    e2e_grp = []
+    for _ in range(trials):
+        h0 = time.perf_counter()
+        call()
+        e2e_grp.append((time.perf_counter() - h0) * 1e6)
     for t, *_ in keep:
         t.close()
     tot = lambda key: sum(r[key] for r in rows)  # noqa: E731
     rss = lambda key: math.sqrt(sum(r[key] ** 2 for r in rows))  # noqa: E731
     nm, ns = _stats(net_us)
+    gm, gs = _stats(grp_us)
+    em, es = _stats(e2e_grp)
+    pm, ps = _stats(e2e_py)
     return {
         "layers": rows,
         "total_device_us": tot("device_mean_us"), "total_device_sem_us": rss("device_sem_us"),
@@ -187,6 +252,9 @@ def run_table_bench(layers: List[LayerConfig] = None, trials: int = 100, warmup:
         "total_host_us": tot("host_mean_us"), "total_host_sem_us": rss("host_sem_us"),
         "total_build_us": tot("build_time_us"),
         "network_graph_us": nm, "network_graph_sem_us": ns,
+        "network_group_us": gm, "network_group_sem_us": gs,
+        "e2e_group_us": em, "e2e_group_sem_us": es,
+        "e2e_group_python_us": pm, "e2e_group_python_sem_us": ps,
         "trials": trials, "warmup": warmup, "graph_reps": graph_reps,
     }
 
