@@ -326,20 +326,40 @@ int csc_sticky(const spconv_csr* h, const char* who) {
 // storage is checked on the device and the host waits for the verdict; when it
 // no longer is the transform of the taps, the call applies the storage as it
 // stands (repair_apply) -- the reference's scatter semantics.  Not capturable.
+int band_setup(spconv_csr* h, bool csc, bool f64, int64_t batch, const void* X, int64_t ldx, void* Y, int64_t ldy,
+               spb::BandParams& bp, spb::BandShape& sh, int sms, cudaStream_t st);
+bool band_taps_ok(const spconv_csr* h);
+
 int csc_exposed_clean(spconv_csr* h, cudaStream_t st, bool f64, bool* clean) {
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     CK(cudaStreamIsCapturing(st, &cap));
     if (cap != cudaStreamCaptureStatusNone)
         return fail(SPCONV_EINVAL, "a CSC handle whose arrays were handed out by spconv_csr_device_ptrs "
                                    "cannot be applied under stream capture");
-    spb::CscGatherParams cp = csc_params(h, f64);
     int* d = nullptr;
     CK(cudaMallocAsync(&d, sizeof(int), st));
-    cp.fail = d;
-    cp.verify_only = 1;
     int v = 1;
     cudaError_t e = cudaMemsetAsync(d, 0, sizeof(int), st);
-    if (e == cudaSuccess) e = spb::launch_csc_gather(cp, f64, st, device_sm_count());
+    const Geom& g = h->g;
+    if (h->band_tw > 0 && h->csc_tiles_b > 0 && band_taps_ok(h) && spb::band_supported((int)g.k, (int)g.s)) {
+        // band geometries: the CSC band check itself (segment by segment,
+        // the kernel the batched apply runs), its verdict into d
+        spb::BandParams bp{};
+        spb::BandShape sh{};
+        const int sms = device_sm_count();
+        if (int rc = band_setup(h, true, false, 1, nullptr, 0, nullptr, 0, bp, sh, sms, st)) {
+            cudaFreeAsync(d, st);
+            return rc;
+        }
+        bp.fail_count = d;
+        h->checked.store(true);
+        if (e == cudaSuccess) e = spb::launch_band_check((int)g.k, (int)g.s, bp, st, sms);
+    } else {
+        spb::CscGatherParams cp = csc_params(h, f64);
+        cp.fail = d;
+        cp.verify_only = 1;
+        if (e == cudaSuccess) e = spb::launch_csc_gather(cp, f64, st, device_sm_count());
+    }
     if (e == cudaSuccess) e = cudaMemcpyAsync(&v, d, sizeof(int), cudaMemcpyDeviceToHost, st);
     cudaFreeAsync(d, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);

@@ -570,6 +570,80 @@ __device__ __forceinline__ bool seg_verify_csc(const BandParams& P, const SegGeo
     }
     ok &= run == g.L;
     uint32_t bad = 0;
+    if constexpr (S >= 3 && !ZT) {
+        // Interior segment (every column receives every tap of its residue
+        // class): the run is periodic -- S consecutive columns hold
+        // D = NJ * K entries, and the next S columns the same taps on rows
+        // one output column further.  Each lane owns fixed positions r of a
+        // block of G periods (its expected row offset and tap computed once),
+        // and the warp walks the run in blocks: consecutive lanes read
+        // consecutive words (no bank conflicts, unlike a lane per column).
+        // s = 3 (k7: 326 -> 243 us at 2048^2 x 32 images); s = 2 keeps the
+        // residue-uniform unrolled compares below, which measured faster
+        // (config 4: 546 against 589 us, scripts/probe_csc_check.py).
+        const int ra = (a + P.p) % S, NJ = (K - 1 - ra) / S + 1;
+        bool inter = nj == NJ && g.nr == TWC;
+#pragma unroll
+        for (int c = 0; c < S; ++c) {
+            const int bl = g.y0 + c, bh = g.y0 + TWC - S + c;
+            inter &= taps_on<K, S>(bl, P.p, P.no) == (K - 1 - (bl + P.p) % S) / S + 1;
+            inter &= taps_on<K, S>(bh, P.p, P.no) == (K - 1 - (bh + P.p) % S) / S + 1;
+        }
+        if (inter) {
+            constexpr int DMAX = ((K + S - 1) / S) * K;
+            constexpr int UC = DMAX > 64 ? (DMAX + 31) / 32 : 2;
+            const int D = NJ * K;
+            const int G = cmax(1, 32 * UC / D);
+            const int JT = ra + S * (NJ - 1);
+            const int xr = (a + P.p - JT) / S;
+            int rowu[UC], ru[UC], gpu[UC];
+            uint32_t tapu[UC];
+#pragma unroll
+            for (int u = 0; u < UC; ++u) {
+                const int r = lane + 32 * u;
+                const int gp = r / D, rr = r - gp * D;
+                // the period's column holding position rr (columns in order from
+                // the segment's first, each with NJ * NI(residue) entries)
+                int cp = S - 1, eb = 0, ni = 1, it = 0, e0 = 0;
+                bool found = false;
+#pragma unroll
+                for (int c = 0; c < S; ++c) {
+                    const int rb = (g.y0 + c + P.p) % S;
+                    const int n_i = (K - 1 - rb) / S + 1;
+                    if (!found && rr < e0 + NJ * n_i) {
+                        found = true;
+                        cp = c;
+                        ni = n_i;
+                        it = rb + S * (n_i - 1);
+                        eb = e0;
+                    }
+                    e0 += NJ * n_i;
+                }
+                const int kk = rr - eb;
+                const int dj = kk / ni, di = kk - dj * ni;
+                ru[u] = r < G * D ? r : -1;
+                gpu[u] = gp;
+                rowu[u] = (xr + dj) * P.no + (g.y0 + cp + P.p - it) / S + gp + di;
+                tapu[u] = s_w[(JT - S * dj) * K + (it - S * di)];
+            }
+            const int full = (TW / G) * G;  // periods in whole blocks
+            const int step = G * D;
+            int g0 = 0, base = 0;
+#pragma unroll 1
+            for (; g0 < full; g0 += G, base += step) {
+#pragma unroll
+                for (int u = 0; u < UC; ++u)
+                    if (ru[u] >= 0)
+                        bad |= (uint32_t)(cbs[base + ru[u]] - (rowu[u] + g0)) | (vbs[base + ru[u]] ^ tapu[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < UC; ++u)  // the last, partial block
+                if (ru[u] >= 0 && g0 + gpu[u] < TW)
+                    bad |= (uint32_t)(cbs[base + ru[u]] - (rowu[u] + g0)) | (vbs[base + ru[u]] ^ tapu[u]);
+            ok &= bad == 0u;
+            return __all_sync(0xffffffffu, ok);
+        }
+    }
     if constexpr (S == 1) {
         // 2. every column's rows and values against the taps landing on it
         //    (interior columns of dense taps fully unrolled)

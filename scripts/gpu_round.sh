@@ -26,6 +26,7 @@ nc prof_spmm_c2_b1 "conv_spmv_win" 3 1 c2
 nc prof_build_c3 "csr_build" 3 1 build3
 nc prof_build_c4 "csr_build" 3 1 build4
 nc prof_k11_c5_b256 "conv_band_check|conv_spmm_band" 6 2 c5k11
+nc prof_group_densenet "csr_spmv_group" 3 1 group
 # the reports are large: summarise them on the box and bring back the text
 TAG=${TAG:-r02}
 python scripts/make_profiles.py $TAG gpurun_out > gpurun_out/make_profiles.log 2>&1

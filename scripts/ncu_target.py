@@ -3,7 +3,8 @@ capture of the last launch(es) (gpu_round.sh).   python scripts/ncu_target.py <t
 
 targets: c3 (config 3, 256 images, CSR), c3b32 (32 images), c3csc (CSC storage),
 c3f64 (fp64 apply), c4 (config 4, 8 images), c2 (config 2 single image),
-build3 / build4 (the CSR builds), c5k11 (257 x 193, k11 s1 p10, 256 images)."""
+build3 / build4 (the CSR builds), c5k11 (257 x 193, k11 s1 p10, 256 images),
+group (the DenseNet121 table in one grouped launch)."""
 import sys
 
 import numpy as np
@@ -19,6 +20,20 @@ SPECS = {"c3": ((1024, 1024, 3, 1, 1), 256, 0), "c3b32": ((1024, 1024, 3, 1, 1),
          "c4": ((4096, 4096, 7, 2, 3), 8, 0), "c4csc": ((4096, 4096, 7, 2, 3), 8, 1), "c2": ((512, 512, 5, 2, 2), 1, 0),
          "build3": ((1024, 1024, 3, 1, 1), 0, 0), "build4": ((4096, 4096, 7, 2, 3), 0, 0),
          "c5k11": ((257, 193, 11, 1, 10), 256, 0)}
+if target == "group":
+    from paper_2411_19419_b200.layers import densenet121_layers
+    ts, xs = [], []
+    for li, L in enumerate(densenet121_layers()):
+        rng = np.random.default_rng([42, li])
+        ts.append(sp.build_transform(sp.Kernel(L.k, rng.standard_normal(L.k * L.k).astype(np.float32)),
+                                     sp.ConvSpec(L.m, L.n, L.k, L.s, L.p)))
+        xs.append(torch.randn(L.m * L.n, device="cuda"))
+    ys = [torch.empty(t.rows, device="cuda") for t in ts]
+    for _ in range(warm + 1):
+        sp.spmv_group(ts, xs, ys)
+    torch.cuda.synchronize()
+    print(target, ts[0].last_kernel)
+    sys.exit(0)
 spec, b, layout = SPECS[target]
 k = spec[2]
 kern = sp.Kernel(k, np.random.default_rng(0).standard_normal(k * k).astype(np.float32))

@@ -232,3 +232,47 @@ def test_csc_wide_kernel_and_spgemm(sp, orc, torch_cuda):
     eye = sp.Transform.from_host(T.cols, T.cols, np.arange(T.cols + 1), np.arange(T.cols), np.ones(T.cols))
     G = sp.spgemm(T, eye)
     assert all(np.array_equal(a, b) for a, b in zip(G.export(), Tcsr.export()))
+
+
+@pytest.mark.parametrize("spec", [(64, 300, 7, 2, 3), (40, 290, 3, 2, 1), (50, 280, 5, 2, 2), (30, 400, 7, 3, 3),
+                                  (48, 300, 11, 2, 5), (36, 390, 5, 3, 0)])
+def test_csc_band_check_detects_interior_changes(sp, orc, torch_cuda, spec):
+    """Exposed CSC storage of a band geometry is verified by the CSC band check
+    itself; a value or a row index changed in the middle of an interior segment
+    (the periodic s >= 2 verification) is caught, and the output is the
+    reference's scatter over the altered arrays.  An untouched exposed handle
+    passes the same check."""
+    m, n, k, s, p = spec
+    kern, X = problem(orc, 44, m, n, k, batch=4)
+    t = build(sp, spec, kern)
+    clean = apply(torch_cuda, sp, t, X)
+    cp_d, ci_d, cv_d = t.device_ptrs()
+    assert np.array_equal(bits(apply(torch_cuda, sp, t, X)), bits(clean))
+    assert t.last_kernel != "csc_gather<verify>+csc_repair"
+    assert t.band_check_status()[1] == 0
+    cp, ci, cv = t.export()
+    dci = torch_cuda.as_tensor(_DevArray(ci_d, t.nnz, "<i4"), device="cuda")
+    dcv = torch_cuda.as_tensor(_DevArray(cv_d, t.nnz, "<f4"), device="cuda")
+    a, b = m // 2, 2 * s * 64 - 3  # an input column in the middle of the second segment
+    col = a * n + b
+    e0, e1 = int(cp[col]), int(cp[col + 1])
+    assert e1 - e0 >= 2
+    for what in ("value", "row"):
+        ci2, cv2 = ci.copy(), cv.copy()
+        e = (e0 + e1) // 2
+        if what == "value":
+            cv2[e] = np.float32(cv2[e] * -2.0 + 1.0)
+            dcv[e] = float(cv2[e])
+        else:
+            ci2[e] = (ci2[e] + 1) % t.rows
+            dci[e] = int(ci2[e])
+        torch_cuda.cuda.synchronize()
+        Y = apply(torch_cuda, sp, t, X)
+        assert t.last_kernel == "csc_gather<verify>+csc_repair", (what, t.last_kernel)
+        want = np.stack([orc.spmv_csc_f32_fma(t.rows, cp, ci2, cv2, x) for x in X])
+        assert np.array_equal(bits(Y), bits(want)), what
+        dcv[e] = float(cv[e])
+        dci[e] = int(ci[e])
+        torch_cuda.cuda.synchronize()
+    assert np.array_equal(bits(apply(torch_cuda, sp, t, X)), bits(clean))
+    assert t.last_kernel != "csc_gather<verify>+csc_repair"
