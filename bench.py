@@ -914,6 +914,10 @@ def run_densenet(args):
                 "path": "spconv_convolve_host_group (C ABI): the 123 pageable host images in, 123 outputs "
                         "out, one call (host pack, one H2D, one grouped SpMV launch, one D2H, unpack)",
                 "python_api_us": res["e2e_group_python_us"]},
+        "e2e_f64": {"value": res["e2e_group_f64_us"], "unit": "us", "h2d_bytes_per_step": 2 * h2d,
+                    "d2h_bytes_per_step": 2 * d2h,
+                    "path": "spconv_convolve_host_group_f64 (C ABI): the reference's fp64 arithmetic, every "
+                            "layer's output bit-identical to its per-layer fp64 SpMV (= the reference's convolve)"},
         "e2e_per_layer": {"value": res["total_host_us"], "unit": "us", "h2d_bytes_per_step": h2d,
                           "d2h_bytes_per_step": d2h,
                           "path": "spconv_convolve_host per layer (pinned fp32 image, H2D + SpMV + D2H), "

@@ -219,6 +219,15 @@ int spconv_spmv_group(const spconv_csr* const* hs, int64_t count, const float* c
 int spconv_convolve_host_group(const spconv_csr* const* hs, int64_t count, const float* const* x_host,
                                float* const* y_host);
 
+/* The fp64 forms: the reference's own arithmetic per member (one rounded
+ * multiply and one rounded add per entry, inc/sparse.hpp:185-191), each y
+ * bit-identical to spconv_spmm_f64 on that member -- and so to the
+ * reference's spmv() / convolve() -- in one launch for the CSR members. */
+int spconv_spmv_group_f64(const spconv_csr* const* hs, int64_t count, const double* const* x_dev,
+                          double* const* y_dev, void* stream);
+int spconv_convolve_host_group_f64(const spconv_csr* const* hs, int64_t count, const double* const* x_host,
+                                   double* const* y_host);
+
 /* fp64 SpMM on device buffers with the reference's own arithmetic: per row
  * acc = 0.0; acc = acc + (double)val * x[col] over the stored entries in
  * order, one rounded multiply and one rounded add each (inc/sparse.hpp:185-191

@@ -68,6 +68,8 @@ _decl("spconv_csr_storage_bytes", [_vp, _P(_i64)])
 _decl("spconv_band_check_flags", [_vp, _vp, _i64, _P(_i64)])
 _decl("spconv_spmv_group", [_vp, _i64, _vp, _vp, _vp])
 _decl("spconv_convolve_host_group", [_vp, _i64, _vp, _vp])
+_decl("spconv_spmv_group_f64", [_vp, _i64, _vp, _vp, _vp])
+_decl("spconv_convolve_host_group_f64", [_vp, _i64, _vp, _vp])
 _decl("spconv_spmm_f64_threads", [_vp, _vp, _i64, _vp, _i64, _i64, C.c_int, _vp])
 _decl("spconv_convolve_host_f64_threads", [_vp, _vp, _vp, _i64, C.c_int])
 _decl("spconv_csr_last_kernel", [_vp], C.c_char_p)
@@ -466,53 +468,72 @@ def spmv(t: Transform, x, y=None, stream=None):
 
 def spmv_group(ts, xs, ys=None, stream=None):
     """ys[i] = ts[i] xs[i] for every member in one launch (spconv_spmv_group):
-    a list of transforms, each with its own CUDA float32 vector; each output
-    is bit-identical to spmv(ts[i], xs[i])."""
+    a list of transforms, each with its own CUDA vector.  float32 vectors:
+    each output bit-identical to spmv(ts[i], xs[i]); float64 vectors: the
+    reference's arithmetic (spconv_spmv_group_f64), each output bit-identical
+    to spmm_f64 on that member."""
     import torch
-    ts, xs = list(ts), [_dev_f32(x, "spmv_group").contiguous() for x in xs]
+    ts, xs = list(ts), list(xs)
     if len(ts) != len(xs):
         raise ValueError("spmv_group: one vector per transform")
-    for t, x in zip(ts, xs):
+    f64 = bool(xs) and xs[0].dtype == torch.float64
+    dt = torch.float64 if f64 else torch.float32
+    for i, (t, x) in enumerate(zip(ts, xs)):
+        if not isinstance(x, torch.Tensor) or not x.is_cuda or x.dtype != dt:
+            raise ValueError(f"spmv_group: expected CUDA {dt} vectors (all of one dtype)")
         if x.numel() != t.cols:
             raise ValueError(f"spmv_group: matrix has {t.cols} columns but vector has {x.numel()} elements")
+        xs[i] = x.contiguous()
     if ys is None:
-        ys = [torch.empty(t.rows, dtype=torch.float32, device=x.device) for t, x in zip(ts, xs)]
+        ys = [torch.empty(t.rows, dtype=dt, device=x.device) for t, x in zip(ts, xs)]
     n = len(ts)
-    H = (C.c_void_p * n)(*[t._h for t in ts])
-    X = (C.c_void_p * n)(*[x.data_ptr() for x in xs])
-    Y = (C.c_void_p * n)(*[y.data_ptr() for y in ys])
-    _check(lib.spconv_spmv_group(H, n, X, Y, _stream_handle(stream)))
+    H = np.fromiter((t._h.value for t in ts), np.uintp, n)
+    X = np.fromiter((x.data_ptr() for x in xs), np.uintp, n)
+    Y = np.fromiter((y.data_ptr() for y in ys), np.uintp, n)
+    fn = lib.spconv_spmv_group_f64 if f64 else lib.spconv_spmv_group
+    _check(fn(H.ctypes.data, n, X.ctypes.data, Y.ctypes.data, _stream_handle(stream)))
     return ys
 
 
-def convolve_group(ts, images, out=None):
-    """Host vectors in, host vectors out (spconv_convolve_host_group): one
-    packed transfer each way and one launch for the whole list.  Returns one
-    float32 vector per transform, views into a single output array (``out``,
-    float32 of sum(rows) elements, is used when given)."""
+def _convolve_group(ts, images, out, dt, fn, who):
     ts = list(ts)
     n = len(ts)
     if len(images) != n:
-        raise ValueError("convolve_group: one image per transform")
+        raise ValueError(f"{who}: one image per transform")
     xs = []
     for t, x in zip(ts, images):
-        if type(x) is not np.ndarray or x.dtype != np.float32 or not x.flags.c_contiguous:
-            x = np.ascontiguousarray(x, np.float32)
+        if type(x) is not np.ndarray or x.dtype != dt or not x.flags.c_contiguous:
+            x = np.ascontiguousarray(x, dt)
         if x.size != t.cols:
-            raise ValueError(f"convolve_group: matrix has {t.cols} columns but image has {x.size} elements")
+            raise ValueError(f"{who}: matrix has {t.cols} columns but image has {x.size} elements")
         xs.append(x)
     rows = np.fromiter((t.rows for t in ts), np.int64, n)
     off = np.zeros(n + 1, np.int64)
     np.cumsum(rows, out=off[1:])
     if out is None:
-        out = np.empty(int(off[-1]), np.float32)
-    elif out.dtype != np.float32 or out.size < off[-1] or not out.flags.c_contiguous:
-        raise ValueError("convolve_group: out must be a contiguous float32 array of sum(rows) elements")
+        out = np.empty(int(off[-1]), dt)
+    elif out.dtype != dt or out.size < off[-1] or not out.flags.c_contiguous:
+        raise ValueError(f"{who}: out must be a contiguous {np.dtype(dt).name} array of sum(rows) elements")
     H = np.fromiter((t._h.value for t in ts), np.uintp, n)
     X = np.fromiter((x.__array_interface__["data"][0] for x in xs), np.uintp, n)
-    Y = out.__array_interface__["data"][0] + 4 * off[:-1].astype(np.uintp)
-    _check(lib.spconv_convolve_host_group(H.ctypes.data, n, X.ctypes.data, Y.ctypes.data))
+    Y = out.__array_interface__["data"][0] + np.dtype(dt).itemsize * off[:-1].astype(np.uintp)
+    _check(fn(H.ctypes.data, n, X.ctypes.data, Y.ctypes.data))
     return [out[a:b] for a, b in zip(off[:-1].tolist(), off[1:].tolist())]
+
+
+def convolve_group(ts, images, out=None):
+    """Host vectors in, host vectors out (spconv_convolve_host_group, fp32):
+    one packed transfer each way and one launch for the whole list.  Returns
+    one vector per transform, views into a single output array (``out``, of
+    sum(rows) elements, is used when given)."""
+    return _convolve_group(ts, images, out, np.float32, lib.spconv_convolve_host_group, "convolve_group")
+
+
+def convolve_group_f64(ts, images, out=None):
+    """convolve_group in the reference's fp64 arithmetic
+    (spconv_convolve_host_group_f64): each output bit-identical to the
+    reference's convolve() of that layer."""
+    return _convolve_group(ts, images, out, np.float64, lib.spconv_convolve_host_group_f64, "convolve_group_f64")
 
 
 def spmm(t: Transform, X, Y=None, stream=None):

@@ -1983,23 +1983,25 @@ int spconv_convolve_host(const spconv_csr* hc, const float* X_host, float* Y_hos
 // ---- grouped apply (group.cu) ----
 
 // Members' y ranges pairwise disjoint and disjoint from every x (x ranges may
-// share memory): one sweep over the ranges sorted by start.
-static bool group_ranges_ok(const spconv_csr* const* hs, int64_t count, const float* const* xs,
-                            float* const* ys) {
+// share memory): one sweep over the byte ranges sorted by start.
+static bool group_ranges_ok(const spconv_csr* const* hs, int64_t count, const void* const* xs, void* const* ys,
+                            size_t es) {
     struct R {
-        const float* a;
-        const float* b;
+        const char* a;
+        const char* b;
         bool out;
     };
     std::vector<R> v;
     v.reserve((size_t)(2 * count));
     for (int64_t i = 0; i < count; ++i) {
-        if (hs[i]->cols > 0) v.push_back({xs[i], xs[i] + hs[i]->cols, false});
-        if (hs[i]->rows > 0) v.push_back({ys[i], ys[i] + hs[i]->rows, true});
+        const char* x = static_cast<const char*>(xs[i]);
+        const char* y = static_cast<const char*>(ys[i]);
+        if (hs[i]->cols > 0) v.push_back({x, x + es * hs[i]->cols, false});
+        if (hs[i]->rows > 0) v.push_back({y, y + es * hs[i]->rows, true});
     }
     std::sort(v.begin(), v.end(), [](const R& p, const R& q) { return p.a < q.a; });
-    const float* yend = nullptr;
-    const float* xend = nullptr;
+    const char* yend = nullptr;
+    const char* xend = nullptr;
     for (const R& r : v) {
         if (r.out) {
             if ((yend && r.a < yend) || (xend && r.a < xend)) return false;
@@ -2028,14 +2030,14 @@ static int group_check(const char* who, const spconv_csr* const* hs, int64_t cou
 }
 
 // Enqueue the group on `st`: CSR members in launches of up to kGroupMax, the
-// others one apply each.
-static int run_group(const spconv_csr* const* hs, int64_t count, const float* const* xs, float* const* ys,
+// others one apply each (fp32: spconv_spmv's path; fp64: spconv_spmm_f64's).
+static int run_group(const spconv_csr* const* hs, int64_t count, const void* const* xs, void* const* ys, bool f64,
                      cudaStream_t st) {
     spb::GroupParams gp;
     gp.count = 0;
     int blocks = 0;
     auto flush = [&]() -> int {
-        if (gp.count > 0) CK(spb::launch_spmv_group(gp, blocks, st));
+        if (gp.count > 0) CK(spb::launch_spmv_group(gp, blocks, f64, st));
         gp.count = 0;
         blocks = 0;
         return SPCONV_OK;
@@ -2044,65 +2046,79 @@ static int run_group(const spconv_csr* const* hs, int64_t count, const float* co
         auto* h = const_cast<spconv_csr*>(hs[i]);
         if (h->rows == 0) continue;
         if (!h->row_ptr) {  // CSC-only storage: its own apply
-            if (int rc = run_spmm(h, xs[i], h->cols, ys[i], h->rows, 1, st)) return rc;
+            if (int rc = f64 ? spconv_spmm_f64(h, static_cast<const double*>(xs[i]), h->cols,
+                                               static_cast<double*>(ys[i]), h->rows, 1, st)
+                             : run_spmm(h, static_cast<const float*>(xs[i]), h->cols, static_cast<float*>(ys[i]),
+                                        h->rows, 1, st))
+                return rc;
             continue;
         }
         const int nb = spb::group_blocks(h->rows);
         if (gp.count == spb::kGroupMax || (int64_t)blocks + nb > INT32_MAX / 2)
             if (int rc = flush()) return rc;
-        gp.m[gp.count++] = {h->row_ptr, h->col_idx, h->vals, xs[i], ys[i], (int)h->rows, blocks};
+        gp.m[gp.count++] = {h->row_ptr, h->col_idx, h->vals, f64 ? h->vals64 : nullptr, xs[i], ys[i],
+                            (int)h->rows, blocks};
         blocks += nb;
-        h->last_kernel.store("csr_spmv_group");
+        h->last_kernel.store(f64 ? "csr_spmv_group<f64>" : "csr_spmv_group");
     }
     return flush();
 }
 
-int spconv_spmv_group(const spconv_csr* const* hs, int64_t count, const float* const* x_dev, float* const* y_dev,
-                      void* stream) {
+static int spmv_group_impl(const char* who, const spconv_csr* const* hs, int64_t count, const void* const* xs,
+                           void* const* ys, bool f64, void* stream) {
     int dev = 0;
-    if (int rc = group_check("spconv_spmv_group", hs, count, reinterpret_cast<const void* const*>(x_dev),
-                             reinterpret_cast<void* const*>(y_dev), &dev))
-        return rc;
+    if (int rc = group_check(who, hs, count, xs, ys, &dev)) return rc;
     if (count == 0) return SPCONV_OK;
-    if (!group_ranges_ok(hs, count, x_dev, y_dev))
-        return fail(SPCONV_EINVAL, "spconv_spmv_group: a y overlaps another member's x or y");
+    if (!group_ranges_ok(hs, count, xs, ys, f64 ? 8 : 4))
+        return fail(SPCONV_EINVAL, std::string(who) + ": a y overlaps another member's x or y");
     DeviceGuard dg(dev);
     if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
-    return run_group(hs, count, x_dev, y_dev, static_cast<cudaStream_t>(stream));
+    return run_group(hs, count, xs, ys, f64, static_cast<cudaStream_t>(stream));
+}
+
+int spconv_spmv_group(const spconv_csr* const* hs, int64_t count, const float* const* x_dev, float* const* y_dev,
+                      void* stream) {
+    return spmv_group_impl("spconv_spmv_group", hs, count, reinterpret_cast<const void* const*>(x_dev),
+                           reinterpret_cast<void* const*>(y_dev), false, stream);
+}
+
+int spconv_spmv_group_f64(const spconv_csr* const* hs, int64_t count, const double* const* x_dev,
+                          double* const* y_dev, void* stream) {
+    return spmv_group_impl("spconv_spmv_group_f64", hs, count, reinterpret_cast<const void* const*>(x_dev),
+                           reinterpret_cast<void* const*>(y_dev), true, stream);
 }
 
 namespace {
-// Per-device staging of spconv_convolve_host_group (grown on demand, kept).
+// Per-device staging of spconv_convolve_host_group(_f64) (grown on demand, kept).
 struct GroupWs {
     std::mutex mu;
     cudaStream_t st = nullptr;
-    float* pin_in = nullptr;
-    float* pin_out = nullptr;
-    float* dx = nullptr;
-    float* dy = nullptr;
-    size_t cap_in = 0, cap_out = 0;  // floats
+    char* pin_in = nullptr;
+    char* pin_out = nullptr;
+    char* dx = nullptr;
+    char* dy = nullptr;
+    size_t cap_in = 0, cap_out = 0;  // bytes
 };
 GroupWs g_group_ws[64];
 }  // namespace
 
-int spconv_convolve_host_group(const spconv_csr* const* hs, int64_t count, const float* const* x_host,
-                               float* const* y_host) {
+static int convolve_host_group_impl(const char* who, const spconv_csr* const* hs, int64_t count,
+                                    const void* const* x_host, void* const* y_host, bool f64) {
     int dev = 0;
-    if (int rc = group_check("spconv_convolve_host_group", hs, count, reinterpret_cast<const void* const*>(x_host),
-                             reinterpret_cast<void* const*>(y_host), &dev))
-        return rc;
+    if (int rc = group_check(who, hs, count, x_host, y_host, &dev)) return rc;
     if (count == 0) return SPCONV_OK;
-    if (dev < 0 || dev >= 64) return fail(SPCONV_EINVAL, "spconv_convolve_host_group: device index");
+    if (dev < 0 || dev >= 64) return fail(SPCONV_EINVAL, std::string(who) + ": device index");
     DeviceGuard dg(dev);
     if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
+    const size_t es = f64 ? 8 : 4;
     // packed layout, members 16-byte aligned (the band / TMA paths of CSC members)
     std::vector<size_t> xo((size_t)count), yo((size_t)count);
     size_t nin = 0, nout = 0;
     for (int64_t i = 0; i < count; ++i) {
         xo[(size_t)i] = nin;
         yo[(size_t)i] = nout;
-        nin += ((size_t)hs[i]->cols + 3) & ~size_t(3);
-        nout += ((size_t)hs[i]->rows + 3) & ~size_t(3);
+        nin += ((size_t)hs[i]->cols * es + 15) & ~size_t(15);
+        nout += ((size_t)hs[i]->rows * es + 15) & ~size_t(15);
     }
     GroupWs& w = g_group_ws[dev];
     std::lock_guard<std::mutex> lk(w.mu);
@@ -2111,16 +2127,16 @@ int spconv_convolve_host_group(const spconv_csr* const* hs, int64_t count, const
         if (w.pin_in) cudaFreeHost(w.pin_in), w.pin_in = nullptr;
         if (w.dx) cudaFree(w.dx), w.dx = nullptr;
         w.cap_in = 0;
-        CK(cudaHostAlloc(&w.pin_in, nin * 4, cudaHostAllocDefault));
-        CK(cudaMalloc(&w.dx, nin * 4));
+        CK(cudaHostAlloc(&w.pin_in, nin, cudaHostAllocDefault));
+        CK(cudaMalloc(&w.dx, nin));
         w.cap_in = nin;
     }
     if (w.cap_out < nout) {
         if (w.pin_out) cudaFreeHost(w.pin_out), w.pin_out = nullptr;
         if (w.dy) cudaFree(w.dy), w.dy = nullptr;
         w.cap_out = 0;
-        CK(cudaHostAlloc(&w.pin_out, nout * 4, cudaHostAllocDefault));
-        CK(cudaMalloc(&w.dy, nout * 4));
+        CK(cudaHostAlloc(&w.pin_out, nout, cudaHostAllocDefault));
+        CK(cudaMalloc(&w.dy, nout));
         w.cap_out = nout;
     }
     // builds only enqueue: wait for those not yet seen complete
@@ -2135,20 +2151,34 @@ int spconv_convolve_host_group(const spconv_csr* const* hs, int64_t count, const
         CK(cudaStreamWaitEvent(w.st, h->built, 0));
     }
     for (int64_t i = 0; i < count; ++i)
-        if (hs[i]->cols > 0) std::memcpy(w.pin_in + xo[(size_t)i], x_host[i], (size_t)hs[i]->cols * 4);
-    CK(cudaMemcpyAsync(w.dx, w.pin_in, nin * 4, cudaMemcpyHostToDevice, w.st));
-    std::vector<const float*> xs((size_t)count);
-    std::vector<float*> ys((size_t)count);
+        if (hs[i]->cols > 0) std::memcpy(w.pin_in + xo[(size_t)i], x_host[i], (size_t)hs[i]->cols * es);
+    CK(cudaMemcpyAsync(w.dx, w.pin_in, nin, cudaMemcpyHostToDevice, w.st));
+    std::vector<const void*> xs((size_t)count);
+    std::vector<void*> ys((size_t)count);
     for (int64_t i = 0; i < count; ++i) xs[(size_t)i] = w.dx + xo[(size_t)i], ys[(size_t)i] = w.dy + yo[(size_t)i];
-    if (int rc = run_group(hs, count, xs.data(), ys.data(), w.st)) {
+    if (int rc = run_group(hs, count, xs.data(), ys.data(), f64, w.st)) {
         cudaStreamSynchronize(w.st);
         return rc;
     }
-    CK(cudaMemcpyAsync(w.pin_out, w.dy, nout * 4, cudaMemcpyDeviceToHost, w.st));
+    CK(cudaMemcpyAsync(w.pin_out, w.dy, nout, cudaMemcpyDeviceToHost, w.st));
     CK(cudaStreamSynchronize(w.st));
     for (int64_t i = 0; i < count; ++i)
-        if (hs[i]->rows > 0) std::memcpy(y_host[i], w.pin_out + yo[(size_t)i], (size_t)hs[i]->rows * 4);
+        if (hs[i]->rows > 0) std::memcpy(y_host[i], w.pin_out + yo[(size_t)i], (size_t)hs[i]->rows * es);
     return SPCONV_OK;
+}
+
+int spconv_convolve_host_group(const spconv_csr* const* hs, int64_t count, const float* const* x_host,
+                               float* const* y_host) {
+    return convolve_host_group_impl("spconv_convolve_host_group", hs, count,
+                                    reinterpret_cast<const void* const*>(x_host),
+                                    reinterpret_cast<void* const*>(y_host), false);
+}
+
+int spconv_convolve_host_group_f64(const spconv_csr* const* hs, int64_t count, const double* const* x_host,
+                                   double* const* y_host) {
+    return convolve_host_group_impl("spconv_convolve_host_group_f64", hs, count,
+                                    reinterpret_cast<const void* const*>(x_host),
+                                    reinterpret_cast<void* const*>(y_host), true);
 }
 
 int spconv_spmm_f64(const spconv_csr* h, const double* X_dev, int64_t ldx, double* Y_dev, int64_t ldy,

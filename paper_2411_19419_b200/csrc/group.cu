@@ -11,11 +11,16 @@
 // per-layer kernels do -- acc = +0.0f; for e in row (stored order):
 // acc = fmaf(vals[e], x[col_idx[e]], acc) -- so the outputs are bit-identical
 // to spconv_spmv on each member (the reference's row loop,
-// inc/sparse.hpp:180-192, evaluated in fp32 with fmaf).
+// inc/sparse.hpp:180-192, evaluated in fp32 with fmaf).  The fp64 form
+// evaluates the reference's own arithmetic -- acc = acc + val * x, one rounded
+// multiply and one rounded add per entry -- and is bit-identical to the
+// reference's spmv() (and to spconv_spmm_f64) on each member.
 //
 // Loads are issued in groups of G entries (all column indices and values,
 // then all x gathers), so a 9-entry row costs three dependent round trips
 // (row_ptr, entries, x) whatever its length up to G.
+#include <type_traits>
+
 #include "internal.h"
 
 namespace spb {
@@ -25,7 +30,9 @@ namespace {
 constexpr int kThreads = 128;
 constexpr int kG = 16;
 
+template <bool F64>
 __global__ void __launch_bounds__(kThreads) csr_spmv_group(const GroupParams P) {
+    using T = typename std::conditional<F64, double, float>::type;
     // member owning this block: the last m with blk0[m] <= blockIdx.x
     int lo = 0, hi = P.count - 1;
     while (lo < hi) {
@@ -36,30 +43,42 @@ __global__ void __launch_bounds__(kThreads) csr_spmv_group(const GroupParams P) 
     const GroupMember& M = P.m[lo];
     const int r = ((int)blockIdx.x - M.blk0) * kThreads + (int)threadIdx.x;
     if (r >= M.rows) return;
+    const T* x = static_cast<const T*>(M.x);
     const int e0 = __ldg(M.row_ptr + r), e1 = __ldg(M.row_ptr + r + 1);
-    float acc = 0.0f;
+    T acc = 0;
     for (int e = e0; e < e1; e += kG) {
         int c[kG];
-        float v[kG], xv[kG];
+        T v[kG], xv[kG];
 #pragma unroll
         for (int q = 0; q < kG; ++q) {
             c[q] = e + q < e1 ? __ldg(M.col_idx + e + q) : 0;
-            v[q] = e + q < e1 ? __ldg(M.vals + e + q) : 0.0f;
+            if constexpr (F64)
+                v[q] = e + q < e1 ? (M.vals64 ? __ldg(M.vals64 + e + q) : (double)__ldg(M.vals + e + q)) : 0.0;
+            else
+                v[q] = e + q < e1 ? __ldg(M.vals + e + q) : 0.0f;
         }
 #pragma unroll
-        for (int q = 0; q < kG; ++q) xv[q] = e + q < e1 ? __ldg(M.x + c[q]) : 0.0f;
+        for (int q = 0; q < kG; ++q) xv[q] = e + q < e1 ? __ldg(x + c[q]) : T(0);
 #pragma unroll
         for (int q = 0; q < kG; ++q)
-            if (e + q < e1) acc = fmaf(v[q], xv[q], acc);
+            if (e + q < e1) {
+                if constexpr (F64)  // the reference's rounded multiply, then rounded add (inc/sparse.hpp:185-191)
+                    acc = __dadd_rn(acc, __dmul_rn(v[q], xv[q]));
+                else
+                    acc = fmaf(v[q], xv[q], acc);
+            }
     }
-    M.y[r] = acc;
+    static_cast<T*>(M.y)[r] = acc;
 }
 
 }  // namespace
 
-cudaError_t launch_spmv_group(const GroupParams& gp, int blocks, cudaStream_t st) {
+cudaError_t launch_spmv_group(const GroupParams& gp, int blocks, bool f64, cudaStream_t st) {
     if (gp.count <= 0 || blocks <= 0) return cudaSuccess;
-    csr_spmv_group<<<blocks, kThreads, 0, st>>>(gp);
+    if (f64)
+        csr_spmv_group<true><<<blocks, kThreads, 0, st>>>(gp);
+    else
+        csr_spmv_group<false><<<blocks, kThreads, 0, st>>>(gp);
     return cudaGetLastError();
 }
 

@@ -175,8 +175,9 @@ struct GroupMember {
     const int32_t* row_ptr;
     const int32_t* col_idx;
     const float* vals;
-    const float* x;
-    float* y;
+    const double* vals64;  // fp64 group: the exact values when the handle keeps them
+    const void* x;         // float / double
+    void* y;
     int rows;
     int blk0;
 };
@@ -185,7 +186,7 @@ struct GroupParams {
     int count;
     GroupMember m[kGroupMax];
 };
-cudaError_t launch_spmv_group(const GroupParams& gp, int blocks, cudaStream_t st);
+cudaError_t launch_spmv_group(const GroupParams& gp, int blocks, bool f64, cudaStream_t st);
 int group_blocks(int64_t rows);
 
 struct BandShape {

@@ -66,7 +66,7 @@ def run_table_bench(layers: List[LayerConfig] = None, trials: int = 100, warmup:
                     graph_reps: int = 20, seed: int = 42, device: int = 0) -> Dict:
     import torch
 
-    from . import ConvSpec, Kernel, build_transform, convolve_group, spmv, spmv_group
+    from . import ConvSpec, Kernel, build_transform, convolve_group, spmm_f64, spmv, spmv_group
     from . import lib, _check
 
     layers = layers or densenet121_layers()
@@ -237,6 +237,25 @@ def run_table_bench(layers: List[LayerConfig] = None, trials: int = 100, warmup:
         h0 = time.perf_counter()
         call()
         e2e_grp.append((time.perf_counter() - h0) * 1e6)
+    # the same in the reference's fp64 arithmetic (spconv_convolve_host_group_f64):
+    # outputs checked bit for bit against each layer's own spmm_f64
+    imgs64 = [x.astype(np.float64) for x in imgs]
+    outs64 = [np.empty(t.rows, np.float64) for t in ts]
+    X64 = np.fromiter((x.__array_interface__["data"][0] for x in imgs64), np.uintp, nl)
+    Y64 = np.fromiter((y.__array_interface__["data"][0] for y in outs64), np.uintp, nl)
+    call64 = lambda: _check(lib.spconv_convolve_host_group_f64(H.ctypes.data, nl, X64.ctypes.data, Y64.ctypes.data))  # noqa: E731
+    call64()
+    for t, x, y in zip(ts, imgs64, outs64):
+        w = spmm_f64(t, torch.from_numpy(x).to(dev)[None])[0].cpu().numpy()
+        if not np.array_equal(w.view(np.uint64), y.view(np.uint64)):
+            raise RuntimeError("fp64 grouped outputs differ from the per-layer fp64 SpMVs")
+    for _ in range(warmup):
+        call64()
+    e2e_64 = []
+    for _ in range(trials):
+        h0 = time.perf_counter()
+        call64()
+        e2e_64.append((time.perf_counter() - h0) * 1e6)
     for t, *_ in keep:
         t.close()
     tot = lambda key: sum(r[key] for r in rows)  # noqa: E731
@@ -245,6 +264,7 @@ def run_table_bench(layers: List[LayerConfig] = None, trials: int = 100, warmup:
     gm, gs = _stats(grp_us)
     em, es = _stats(e2e_grp)
     pm, ps = _stats(e2e_py)
+    fm, fs = _stats(e2e_64)
     return {
         "layers": rows,
         "total_device_us": tot("device_mean_us"), "total_device_sem_us": rss("device_sem_us"),
@@ -255,6 +275,7 @@ def run_table_bench(layers: List[LayerConfig] = None, trials: int = 100, warmup:
         "network_group_us": gm, "network_group_sem_us": gs,
         "e2e_group_us": em, "e2e_group_sem_us": es,
         "e2e_group_python_us": pm, "e2e_group_python_sem_us": ps,
+        "e2e_group_f64_us": fm, "e2e_group_f64_sem_us": fs,
         "trials": trials, "warmup": warmup, "graph_reps": graph_reps,
     }
 
