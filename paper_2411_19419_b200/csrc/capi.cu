@@ -2053,11 +2053,12 @@ static int run_group(const spconv_csr* const* hs, int64_t count, const void* con
                 return rc;
             continue;
         }
-        const int nb = spb::group_blocks(h->rows);
+        const bool quad = h->k2max > 16;
+        const int nb = spb::group_blocks(h->rows, quad);
         if (gp.count == spb::kGroupMax || (int64_t)blocks + nb > INT32_MAX / 2)
             if (int rc = flush()) return rc;
         gp.m[gp.count++] = {h->row_ptr, h->col_idx, h->vals, f64 ? h->vals64 : nullptr, xs[i], ys[i],
-                            (int)h->rows, blocks};
+                            (int)h->rows, blocks, quad ? 1 : 0};
         blocks += nb;
         h->last_kernel.store(f64 ? "csr_spmv_group<f64>" : "csr_spmv_group");
     }

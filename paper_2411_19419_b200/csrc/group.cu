@@ -29,6 +29,7 @@ namespace {
 
 constexpr int kThreads = 128;
 constexpr int kG = 16;
+constexpr int kQ = 13;  // entries per lane and pass in the four-lanes-per-row form (52 a row)
 
 template <bool F64>
 __global__ void __launch_bounds__(kThreads) csr_spmv_group(const GroupParams P) {
@@ -41,9 +42,54 @@ __global__ void __launch_bounds__(kThreads) csr_spmv_group(const GroupParams P) 
         else hi = mid - 1;
     }
     const GroupMember& M = P.m[lo];
+    const T* x = static_cast<const T*>(M.x);
+    if (M.quad) {
+        // Rows longer than 16 entries (k = 5, 7 layers): four lanes per row
+        // load the row's entries together (lane q of the quad: entries q, q + 4,
+        // ...), so a 49-entry row costs the same three round trips as a short
+        // one; the quad's first lane then runs the ordered chain, taking each
+        // (value, x) pair from the lane that loaded it.
+        const int sub = threadIdx.x & 3, base = (threadIdx.x & 31) & ~3;
+        const int r = (((int)blockIdx.x - M.blk0) * kThreads + (int)threadIdx.x) >> 2;
+        const bool live = r < M.rows;
+        const int e0 = live ? __ldg(M.row_ptr + r) : 0, e1 = live ? __ldg(M.row_ptr + r + 1) : 0;
+        T acc = 0;
+        // (warp-uniform trip count: the shuffles need every lane)
+        const int nmax = __reduce_max_sync(0xffffffffu, e1 - e0);
+        for (int o = 0; o < nmax; o += 4 * kQ) {
+            const int e = e0 + o;
+            int c[kQ];
+            T v[kQ], xv[kQ];
+#pragma unroll
+            for (int q = 0; q < kQ; ++q) {
+                const int ee = e + sub + 4 * q;
+                c[q] = ee < e1 ? __ldg(M.col_idx + ee) : 0;
+                if constexpr (F64)
+                    v[q] = ee < e1 ? (M.vals64 ? __ldg(M.vals64 + ee) : (double)__ldg(M.vals + ee)) : 0.0;
+                else
+                    v[q] = ee < e1 ? __ldg(M.vals + ee) : 0.0f;
+            }
+#pragma unroll
+            for (int q = 0; q < kQ; ++q) xv[q] = e + sub + 4 * q < e1 ? __ldg(x + c[q]) : T(0);
+#pragma unroll
+            for (int q = 0; q < kQ; ++q)
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const T vv = __shfl_sync(0xffffffffu, v[q], base + t);
+                    const T xx = __shfl_sync(0xffffffffu, xv[q], base + t);
+                    if (e + 4 * q + t < e1) {
+                        if constexpr (F64)
+                            acc = __dadd_rn(acc, __dmul_rn(vv, xx));
+                        else
+                            acc = fmaf(vv, xx, acc);
+                    }
+                }
+        }
+        if (live && sub == 0) static_cast<T*>(M.y)[r] = acc;
+        return;
+    }
     const int r = ((int)blockIdx.x - M.blk0) * kThreads + (int)threadIdx.x;
     if (r >= M.rows) return;
-    const T* x = static_cast<const T*>(M.x);
     const int e0 = __ldg(M.row_ptr + r), e1 = __ldg(M.row_ptr + r + 1);
     T acc = 0;
     for (int e = e0; e < e1; e += kG) {
@@ -82,6 +128,6 @@ cudaError_t launch_spmv_group(const GroupParams& gp, int blocks, bool f64, cudaS
     return cudaGetLastError();
 }
 
-int group_blocks(int64_t rows) { return (int)((rows + kThreads - 1) / kThreads); }
+int group_blocks(int64_t rows, bool quad) { return (int)(((quad ? 4 : 1) * rows + kThreads - 1) / kThreads); }
 
 }  // namespace spb

@@ -180,14 +180,15 @@ struct GroupMember {
     void* y;
     int rows;
     int blk0;
+    int quad;  // 1: rows of more than 16 entries, four lanes per row (group.cu)
 };
-constexpr int kGroupMax = 128;  // members per launch (6 KB of kernel parameters)
+constexpr int kGroupMax = 128;  // members per launch (8 KB of kernel parameters)
 struct GroupParams {
     int count;
     GroupMember m[kGroupMax];
 };
 cudaError_t launch_spmv_group(const GroupParams& gp, int blocks, bool f64, cudaStream_t st);
-int group_blocks(int64_t rows);
+int group_blocks(int64_t rows, bool quad);
 
 struct BandShape {
     int th, tw, wr, wc, smem, threads, occ;
