@@ -146,6 +146,34 @@ inline Grid convolve(const Transform& t, const Grid& a, int threads = 0) {
     return Grid(t.spec.m_out(), t.spec.n_out(), std::move(out));
 }
 
+/// Grouped apply (new): each transform applied to its own image in one device
+/// call -- a network's layer loop (the reference calls convolve per layer,
+/// inc/bench.hpp:240-248).  fp64 in the reference's arithmetic: every output
+/// is bit-identical to convolve(*ts[i], images[i]) (threads = 1).
+inline std::vector<Grid> convolve_group(const std::vector<const Transform*>& ts, const std::vector<Grid>& images) {
+    if (ts.size() != images.size())
+        throw std::invalid_argument("convolve_group: " + std::to_string(ts.size()) + " transforms but " +
+                                    std::to_string(images.size()) + " images");
+    std::vector<const spconv_csr*> hs(ts.size());
+    std::vector<const double*> xs(ts.size());
+    std::vector<double*> ys(ts.size());
+    std::vector<Grid> out;
+    out.reserve(ts.size());
+    for (std::size_t i = 0; i < ts.size(); ++i) {
+        const Transform& t = *ts[i];
+        const Grid& a = images[i];
+        if (a.rows != t.spec.m || a.cols != t.spec.n)
+            throw std::invalid_argument("convolve: input is " + std::to_string(a.rows) + "x" +
+                                        std::to_string(a.cols) + " but transform expects " + t.spec.str());
+        out.emplace_back(t.spec.m_out(), t.spec.n_out(), DenseVector(static_cast<std::size_t>(t.spec.output_len())));
+        hs[i] = t.matrix.handle();
+        xs[i] = a.values.data();
+        ys[i] = out.back().values.data();
+    }
+    detail::check(spconv_convolve_host_group_f64(hs.data(), static_cast<int64_t>(ts.size()), xs.data(), ys.data()));
+    return out;
+}
+
 /// Batch apply (new; the reference loops convolve per image): `images`
 /// grids of m x n in, m_out x n_out out, one pipelined device pass.
 inline std::vector<Grid> convolve_batch(const Transform& t, const std::vector<Grid>& images) {

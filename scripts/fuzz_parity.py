@@ -45,7 +45,8 @@ def main():
     rng = np.random.default_rng(seed)
     orc = Oracle()
     t_end = time.time() + secs
-    cases = fails = 0
+    cases = fails = groups = 0
+    pending, group_at = [], 8
     while time.time() < t_end:
         k = int(rng.choice([1, 2, 3, 3, 3, 5, 5, 7, 7, 11]))
         s = int(rng.choice([1, 1, 2, 2, 3, 4]))
@@ -124,8 +125,33 @@ def main():
             fails += 1
             print("FAIL", (m, n, k, s, p), "mode", int(mode), "build", build, "batch", batch, "layout", layout, "env", env,
                   "matrix_ok", ok, "y_ok", ok_y, "kernel", t.last_kernel, flush=True)
-        t.close()
-    print(f"fuzz: {cases} cases, {fails} failures (seed {seed}, {secs:.0f} s)")
+        # every few cases the transform joins a pending group; groups of 2..40
+        # members are applied in one call (fp32 device / host, fp64 host) and
+        # each member compared with its own oracle output
+        if rng.random() < 0.3:
+            x0 = X[0].copy()
+            x64 = x0.astype(np.float64) * (1.0 + 2.0 ** -30)
+            pending.append((t, x0, want[0].copy(), x64, orc.spmv_f64(p64, i64, v64, x64)))
+            t = None
+        if len(pending) >= group_at:
+            gts = [q[0] for q in pending]
+            ys = sp.spmv_group(gts, [torch.from_numpy(q[1]).cuda() for q in pending])
+            torch.cuda.synchronize()
+            yh = sp.convolve_group(gts, [q[1] for q in pending])
+            y64 = sp.convolve_group_f64(gts, [q[3] for q in pending])
+            for q, a, b, c in zip(pending, ys, yh, y64):
+                if not (np.array_equal(bits(a.cpu().numpy()), bits(q[2])) and np.array_equal(bits(b), bits(q[2]))
+                        and np.array_equal(bits64(c), bits64(q[4]))):
+                    fails += 1
+                    print("FAIL group member", q[0].spec, q[0].layout, flush=True)
+            groups += 1
+            for q in pending:
+                q[0].close()
+            pending.clear()
+            group_at = int(rng.integers(2, 41))
+        if t is not None:
+            t.close()
+    print(f"fuzz: {cases} cases, {groups} groups, {fails} failures (seed {seed}, {secs:.0f} s)")
     return 1 if fails else 0
 
 

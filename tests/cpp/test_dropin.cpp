@@ -4,6 +4,7 @@
 // libspconv_b200.so.  Runs on the GPU (tests/test_dropin_cpp.py).  Exit 0 = pass.
 #include <cmath>
 #include <cstdio>
+#include <cstring>
 #include <sstream>
 #include <stdexcept>
 #include <string>
@@ -342,6 +343,28 @@ int main() {
             hstack_blocks(bl);
         },
         "hstack_blocks: block 1 has 3 rows, expected 2");
+
+    {   // grouped apply: each member bit-identical to its own convolve()
+        const std::vector<ConvSpec> specs{ConvSpec(9, 7, 3, 1, 1), ConvSpec(30, 30, 7, 2, 3), ConvSpec(5, 5, 1, 1, 0),
+                                          ConvSpec(16, 12, 5, 2, 2)};
+        std::vector<Transform> ts;
+        std::vector<Grid> as;
+        for (std::size_t i = 0; i < specs.size(); ++i) {
+            ts.push_back(build_transform(random_normal_kernel(specs[i].k, 30 + i), specs[i]));
+            as.push_back(random_normal_grid(specs[i].m, specs[i].n, 40 + i));
+        }
+        std::vector<const Transform*> tp;
+        for (const Transform& t : ts) tp.push_back(&t);
+        const std::vector<Grid> got = convolve_group(tp, as);
+        CHECK(got.size() == ts.size());
+        for (std::size_t i = 0; i < ts.size(); ++i) {
+            const Grid want = convolve(ts[i], as[i], 1);
+            CHECK(got[i].rows == want.rows && got[i].cols == want.cols &&
+                  std::memcmp(got[i].values.data(), want.values.data(), want.values.size() * sizeof(double)) == 0);
+        }
+        expect_throw<std::invalid_argument>([&] { convolve_group(tp, std::vector<Grid>(1, as[0])); },
+                                            "convolve_group: 4 transforms but 1 images");
+    }
 
     if (g_fail) {
         std::fprintf(stderr, "%d failure(s)\n", g_fail);
