@@ -737,27 +737,12 @@ __global__ void __launch_bounds__(128) csr_spmm_rowblock(const GenericParams P) 
         float acc[IMG];
 #pragma unroll
         for (int q = 0; q < IMG; ++q) acc[q] = 0.0f;
-        // entries EC at a time: every gather of the chunk (EC x IMG) issued
-        // before its FMAs, which then run in stored order per image
-        constexpr int EC = 4;
-        for (int e = a; e < b; e += EC) {
-            int c[EC];
-            float v[EC], xv[EC][IMG];
+        for (int e = a; e < b; ++e) {
+            const int c = sc[e];
+            const float v = sv[e];
 #pragma unroll
-            for (int u = 0; u < EC; ++u) {
-                c[u] = e + u < b ? sc[e + u] : 0;
-                v[u] = e + u < b ? sv[e + u] : 0.0f;
-            }
-#pragma unroll
-            for (int u = 0; u < EC; ++u)
-#pragma unroll
-                for (int q = 0; q < IMG; ++q)
-                    xv[u][q] = (e + u < b && q < ni) ? __ldg(x0 + (int64_t)q * P.ldx + c[u]) : 0.0f;
-#pragma unroll
-            for (int u = 0; u < EC; ++u)
-#pragma unroll
-                for (int q = 0; q < IMG; ++q)
-                    if (e + u < b && q < ni) acc[q] = fmaf(v[u], xv[u][q], acc[q]);
+            for (int q = 0; q < IMG; ++q)
+                if (q < ni) acc[q] = fmaf(v, __ldg(x0 + (int64_t)q * P.ldx + c), acc[q]);
         }
 #pragma unroll
         for (int q = 0; q < IMG; ++q)
