@@ -193,3 +193,26 @@ def test_group_f64_bitexact_vs_reference(sp, ref, torch_cuda):
         yh = sp.convolve_group_f64(ts, xs)
         for i, (y, w) in enumerate(zip(yh, want)):
             assert np.array_equal(u64(y), u64(w)), i
+
+
+def test_group_empty_matrix_member(sp, orc, torch_cuda):
+    """An all-zero kernel (no stored entries: every output +0.0) among other
+    members, fp32 and fp64, device and host forms."""
+    torch = torch_cuda
+    specs = [(12, 12, 3, 1, 1), (20, 20, 5, 2, 2), (9, 9, 3, 1, 1)]
+    kerns = [np.zeros(9), np.random.default_rng(1).standard_normal(25), np.random.default_rng(2).standard_normal(9)]
+    ts = [sp.build_transform(sp.Kernel(sp_[2], kk), sp.ConvSpec(*sp_)) for sp_, kk in zip(specs, kerns)]
+    assert ts[0].nnz == 0
+    xs = [np.random.default_rng(10 + i).standard_normal(t.cols).astype(np.float32) for i, t in enumerate(ts)]
+    ys = sp.spmv_group(ts, [torch.from_numpy(x).cuda() for x in xs])
+    yh = sp.convolve_group(ts, xs)
+    y64 = sp.convolve_group_f64(ts, [x.astype(np.float64) for x in xs])
+    torch.cuda.synchronize()
+    assert np.array_equal(bits(ys[0].cpu().numpy()), np.zeros(ts[0].rows, np.uint32))
+    assert np.array_equal(bits(yh[0]), np.zeros(ts[0].rows, np.uint32))
+    assert np.array_equal(u64(y64[0]), np.zeros(ts[0].rows, np.uint64))
+    for i in (1, 2):
+        one = sp.spmv(ts[i], torch.from_numpy(xs[i]).cuda())
+        torch.cuda.synchronize()
+        assert np.array_equal(bits(ys[i].cpu().numpy()), bits(one.cpu().numpy()))
+        assert np.array_equal(bits(yh[i]), bits(one.cpu().numpy()))
