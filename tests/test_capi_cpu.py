@@ -161,3 +161,22 @@ def test_path_options_roundtrip_and_errors():
         sp.set_option("spec_skew", "x")
     for src in glob.glob(os.path.join(ROOT, "paper_2411_19419_b200", "csrc", "*.cu")):
         assert "getenv" not in open(src).read(), src
+
+
+def test_group_argument_checks_without_a_device():
+    """The grouped entries validate their arguments before any device work:
+    a negative count, null arrays, and the empty group (a no-op)."""
+    L = sp.lib
+    for fn in (L.spconv_spmv_group, L.spconv_spmv_group_f64):
+        assert fn(None, -1, None, None, None) == 1
+        assert "negative count" in L.spconv_last_error().decode()
+        assert fn(None, 2, None, None, None) == 1
+        assert "null array" in L.spconv_last_error().decode()
+        assert fn(None, 0, None, None, None) == 0
+    for fn in (L.spconv_convolve_host_group, L.spconv_convolve_host_group_f64):
+        assert fn(None, -3, None, None) == 1
+        assert fn(None, 0, None, None) == 0
+    with pytest.raises(ValueError, match="one vector per transform"):
+        sp.spmv_group([], [np.zeros(3)])
+    with pytest.raises(ValueError, match="one image per transform"):
+        sp.convolve_group([], [np.zeros(3)])
