@@ -863,19 +863,34 @@ __device__ __forceinline__ void load_window(const BandParams& P, const CUtensorM
         return;
     }
     const T* X = reinterpret_cast<const T*>(P.X) + (long long)img * P.ldx;
-    for (int e = lane; e < C::WIN; e += 32) {
-        const int r = e / C::WC, c = e - r * C::WC;
-        const int gr = wr0 + r, gc = wc0 + c;
-        const bool in = (unsigned)gr < (unsigned)P.m && (unsigned)gc < (unsigned)P.n;
-        const T* src = in ? X + (long long)gr * P.n + gc : X;
-        if constexpr (sizeof(T) == 4)
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst + e)), "l"(src),
-                         "r"(in ? 4 : 0)
-                         : "memory");
-        else
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst + e)), "l"(src),
-                         "r"(in ? 8 : 0)
-                         : "memory");
+    // Row by row (the row's bounds and base pointer once), the row's columns
+    // unrolled: a few instructions per element copy -- the producer warp's
+    // issue rate is what feeds the consumers in this mode (k11 on 257 x 193:
+    // ~30 instructions an element with a div/mod per element starved them).
+    const uint32_t d0 = smem_u32(dst);
+    const unsigned m = (unsigned)P.m, n = (unsigned)P.n;
+#pragma unroll 1
+    for (int r = 0; r < C::WR; ++r) {
+        const int gr = wr0 + r;
+        const bool rin = (unsigned)gr < m;
+        const T* srow = X + (long long)(rin ? gr : 0) * P.n;
+        const uint32_t drow = d0 + (uint32_t)(r * C::WC * sizeof(T));
+#pragma unroll
+        for (int c0 = 0; c0 < C::WC; c0 += 32) {
+            const int c = c0 + lane;
+            if (C::WC % 32 != 0 && c >= C::WC) break;
+            const int gc = wc0 + c;
+            const bool in = rin && (unsigned)gc < n;
+            const T* src = in ? srow + gc : X;
+            if constexpr (sizeof(T) == 4)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(drow + 4u * (uint32_t)c), "l"(src),
+                             "r"(in ? 4 : 0)
+                             : "memory");
+            else
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(drow + 8u * (uint32_t)c), "l"(src),
+                             "r"(in ? 8 : 0)
+                             : "memory");
+        }
     }
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(full)) : "memory");
     // (+ one ordinary arrive: releases lane 0's earlier shared stores, the row flags)
