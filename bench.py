@@ -658,7 +658,7 @@ def secondary_single(sp, torch, dev, stream, steps, peak):
     del X, Y, Xh
     t.close()
     # ---- off the BASELINE shapes: config 5's widest geometry (257 x 193, k11
-    # s1 p10: odd width -> cp.async staging; 121 FMAs an output -> FMA-bound)
+    # s1 p10: odd width -> cp.async element staging; 121 FMAs an output)
     # and config 3's matrix uploaded as a generic CSR (no conv geometry: the
     # row-block kernel) -- 256 images each
     for name, spec, generic in (("config5_k11", (257, 193, 11, 1, 10), False),
