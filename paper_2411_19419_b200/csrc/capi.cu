@@ -186,11 +186,11 @@ Path path_override() { return static_cast<Path>(spb::opt(spb::kOptPath)); }
 
 // 3-D tensor map over the batch X[b][m][n] (fp32) with the given box.
 int encode_x_map(CUtensorMap* tmap, const void* X, const Geom& g, int64_t ldx, int64_t batch,
-                 int box_c, int box_r, int box_b, bool f64 = false) {
+                 int box_c, int box_r, int box_b, bool f64 = false, int64_t row_pitch = 0) {
     std::memset(tmap, 0, sizeof *tmap);
     const int64_t es = f64 ? 8 : 4;
     const cuuint64_t dims[3] = {(cuuint64_t)g.n, (cuuint64_t)g.m, (cuuint64_t)batch};
-    const cuuint64_t strides[2] = {(cuuint64_t)(g.n * es), (cuuint64_t)(ldx * es)};
+    const cuuint64_t strides[2] = {(cuuint64_t)((row_pitch > 0 ? row_pitch : g.n) * es), (cuuint64_t)(ldx * es)};
     const cuuint32_t box[3] = {(cuuint32_t)box_c, (cuuint32_t)box_r, (cuuint32_t)box_b};
     const cuuint32_t estr[3] = {1, 1, 1};
     CUresult cr = encode_fn()(tmap, f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
@@ -201,6 +201,39 @@ int encode_x_map(CUtensorMap* tmap, const void* X, const Geom& g, int64_t ldx, i
     if (cr != CUDA_SUCCESS)
         return fail(SPCONV_ECUDA, "cuTensorMapEncodeTiled failed with CUresult " +
                                       std::to_string((int)cr));
+    return SPCONV_OK;
+}
+
+// Band path over images whose rows TMA cannot describe (not 16-byte pitched,
+// or a misaligned base): one coalesced pass copies them into 16-byte pitched
+// rows (repitch.cu, a stream-ordered allocation freed once the launches are
+// enqueued) and the tensor map describes the copy, so the windows are TMA
+// boxes instead of element copies from one producer warp -- 1023^2 k3 at 64
+// images 388 -> see DESIGN.  The per-entry fallback keeps reading X itself.
+// Option repitch = off keeps the element staging.
+struct RepitchBuf {
+    void* p = nullptr;
+    cudaStream_t st = nullptr;
+    ~RepitchBuf() {
+        if (p) cudaFreeAsync(p, st);
+    }
+};
+
+int repitch_for_tma(const spconv_csr* h, const void* X, int64_t ldx, int64_t batch, bool f64, spb::BandParams& bp,
+                    const spb::BandShape& sh, CUtensorMap* tmap, RepitchBuf& rb, cudaStream_t st) {
+    const Geom& g = h->g;
+    if (!bp.notma || spb::opt(spb::kOptRepitch) == 1 || encode_fn() == nullptr) return SPCONV_OK;
+    if (g.m >= (1ll << 30) || g.n >= (1ll << 30)) return SPCONV_OK;
+    const int64_t es = f64 ? 8 : 4, E = 16 / es;
+    const int64_t np = (g.n + E - 1) / E * E;
+    const double bytes = (double)batch * (double)g.m * (double)np * (double)es;
+    if (bytes > 8.0 * (1ull << 30) || batch > 65535 || g.m * g.n > (1ll << 31))
+        return SPCONV_OK;  // (a huge batch keeps the element staging)
+    CK(cudaMallocAsync(&rb.p, (size_t)bytes, st));
+    rb.st = st;
+    CK(spb::launch_repitch(X, ldx, rb.p, (int)g.m, (int)g.n, np, batch, f64, st));
+    if (int rc = encode_x_map(tmap, rb.p, g, g.m * np, batch, sh.wc, sh.wr, 1, f64, np)) return rc;
+    bp.notma = 0;
     return SPCONV_OK;
 }
 
@@ -667,7 +700,9 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
         if (int rc = band_setup(h, csc, false, batch, X, ldx, Y, ldy, bp, sh, sms)) return rc;
         CUtensorMap tmap;
         std::memset(&tmap, 0, sizeof tmap);
-        if (!bp.notma)
+        RepitchBuf rbuf;
+        if (int rc = repitch_for_tma(h, X, ldx, batch, false, bp, sh, &tmap, rbuf, st)) return rc;
+        if (!bp.notma && !rbuf.p)
             if (int rc = encode_x_map(&tmap, X, g, ldx, batch, sh.wc, sh.wr, 1, false)) return rc;
         // The fused form -- one kernel: consumers apply with the blocked sums
         // while up to four check warps per CTA verify the storage segment by
@@ -2234,7 +2269,9 @@ int spconv_spmm_f64_threads(const spconv_csr* h, const double* X_dev, int64_t ld
         bp.fused = 0;
         CUtensorMap tmap;
         std::memset(&tmap, 0, sizeof tmap);
-        if (!bp.notma)
+        RepitchBuf rbuf;
+        if (int rc = repitch_for_tma(h, X_dev, ldx, batch, true, bp, sh, &tmap, rbuf, st)) return rc;
+        if (!bp.notma && !rbuf.p)
             if (int rc = encode_x_map(&tmap, X_dev, g, ldx, batch, sh.wc, sh.wr, 1, true)) return rc;
         hm->checked.store(true);
         CK(spb::launch_band_check((int)g.k, (int)g.s, bp, st, sms));

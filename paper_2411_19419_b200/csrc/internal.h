@@ -21,6 +21,7 @@ enum Opt {
     kOptBulkStoreOff,  // 0 bulk (TMA) stores of staged entries, 1 per-thread 16-byte stores
     kOptStage,         // latency SpMV: 0 auto (window kernel from 8 MB of matrix), 1 bulk-staged, 2 window
     kOptSpecSkew,      // test hook: offsets the latency SpMV's predicted row starts
+    kOptRepitch,       // band path on rows not 16-byte pitched: 0 auto (repitched copy + TMA), 1 off (element staging)
     kOptCount
 };
 extern std::atomic<int> g_opt[kOptCount];
@@ -188,6 +189,11 @@ struct GroupParams {
     GroupMember m[kGroupMax];
 };
 cudaError_t launch_spmv_group(const GroupParams& gp, int blocks, bool f64, cudaStream_t st);
+// Copy of `batch` images (rows of n elements at X[b*ldx + r*n + c]) into rows of
+// np >= n elements (Xp[(b*m + r)*np + c]): a 16-byte pitched layout TMA can
+// describe (repitch.cu).
+cudaError_t launch_repitch(const void* X, int64_t ldx, void* Xp, int m, int n, int64_t np, int64_t batch, bool f64,
+                           cudaStream_t st);
 int group_blocks(int64_t rows, bool quad);
 
 struct BandShape {

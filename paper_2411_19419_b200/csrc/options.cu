@@ -31,6 +31,7 @@ const OptSpec kSpecs[] = {
     {"bulk_store", kOptBulkStoreOff, {"1", "0", nullptr}},
     {"stage", kOptStage, {"auto", "bulk", "window", nullptr}},
     {"spec_skew", kOptSpecSkew, {nullptr}},
+    {"repitch", kOptRepitch, {"auto", "off", nullptr}},
 };
 
 }  // namespace

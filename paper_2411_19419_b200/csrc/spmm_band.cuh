@@ -1055,7 +1055,12 @@ __global__ void __launch_bounds__(FUSED ? FusedCfg<K, S, V, CPT, TH, STAGES, DEL
         const int img = I.img, tx = I.tx, ty = I.ty;
         const int xb = tx * TH + warp * V;  // this warp's first output row
         const int y0 = ty * C::TW;
-        mbar_wait(&full[st], (uint32_t)((it / STAGES) & 1));
+        // (element staging: the producer warp's issue slots are the limit, so
+        // the consumers sleep between polls instead of spinning beside it)
+        if (P.notma)
+            mbar_wait_backoff(&full[st], (uint32_t)((it / STAGES) & 1));
+        else
+            mbar_wait(&full[st], (uint32_t)((it / STAGES) & 1));
         // This warp's rows must all lie in verified segments (and the taps be
         // finite and non-zero) for the blocked path.
         const bool fast = FUSED || (P.fast_allowed && ((s_mask[st] >> (warp * V)) & VMASK) == VMASK);

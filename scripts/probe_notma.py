@@ -1,6 +1,7 @@
 """Event-timed batched applies on image widths whose rows are not 16-byte
-pitched (the cp.async element-staging producer), 256 images, L2 scrubbed
-between reps.  AB_ROOT selects another checkout's build for an A/B."""
+pitched, 256 images, L2 scrubbed between reps.  REPITCH=off keeps the cp.async
+element staging (default: a 16-byte pitched copy + TMA); AB_ROOT selects another
+checkout's build for an A/B."""
 import os
 import sys
 
@@ -11,6 +12,8 @@ sys.path.insert(0, os.environ.get("AB_ROOT", "."))
 import paper_2411_19419_b200 as sp  # noqa: E402
 
 scrub = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+if os.environ.get("REPITCH"):
+    sp.set_option("repitch", os.environ["REPITCH"])
 
 
 def timed(fn, reps=10):

@@ -101,3 +101,36 @@ def test_band_k11_reads_the_matrix(sp, orc, torch_cuda):
     Y = sp.spmm(t, torch_cuda.from_numpy(X).cuda()).cpu().numpy()
     assert np.array_equal(bits(Y), bits(orc.spmm_native(ptr, idx, val, X)))
     assert t.band_check_status()[1] == 1
+
+
+@pytest.mark.parametrize("ks", [(3, 1), (3, 2), (5, 3), (7, 1), (11, 1), (2, 2)])
+def test_odd_width_repitch_and_element_staging(sp, orc, torch_cuda, ks, opts):
+    """Rows not 16-byte pitched: the default path copies the images into
+    16-byte pitched rows and loads TMA windows from the copy; option
+    repitch = off stages them with cp.async element copies.  Both bit-equal to
+    the oracle, also with a misaligned base and a padded leading dimension,
+    fp32 and fp64."""
+    k, s = ks
+    p = k // 2
+    spec = (67, 193, k, s, p)
+    kern, X = problem(orc, 63, 67, 193, k, batch=5)
+    t = sp.build_transform(sp.Kernel(k, kern.astype(np.float64)), sp.ConvSpec(*spec))
+    want = orc.spmm_native(*orc.build_native(*spec, kern.astype(np.float32)), X)
+    ptr, idx, val = orc.build_transform(*spec, kern.astype(np.float64))
+    X64 = X.astype(np.float64) * 1.000001
+    w64 = np.stack([orc.spmv_f64(ptr, idx, val, x) for x in X64])
+    ld = t.cols + 3
+    for rp in ("auto", "off"):
+        opts(repitch=rp)
+        for off in (0, 1):  # (1: base 4 bytes past a 16-byte boundary)
+            buf = torch_cuda.zeros(off + 5 * ld, device="cuda")
+            Xd = buf[off:].view(5, ld)[:, : t.cols]
+            Xd.copy_(torch_cuda.from_numpy(X))
+            Y = sp.spmm(t, Xd).cpu().numpy()
+            assert t.last_kernel in BAND_KERNELS, t.last_kernel
+            assert np.array_equal(bits(Y), bits(want)), (ks, rp, off)
+            buf64 = torch_cuda.zeros(off + 5 * ld, dtype=torch_cuda.float64, device="cuda")
+            Xd64 = buf64[off:].view(5, ld)[:, : t.cols]
+            Xd64.copy_(torch_cuda.from_numpy(X64))
+            Y64 = sp.spmm_f64(t, Xd64).cpu().numpy()
+            assert np.array_equal(bits64(Y64), bits64(w64)), (ks, rp, off, t.last_kernel)
