@@ -298,12 +298,133 @@ __global__ void __launch_bounds__(128) csc_gather_lat(const CscGatherParams P) {
     if (__syncthreads_or(bad) && threadIdx.x == 0) *P.fail = 1;
 }
 
+// k >= 5 (25-49 taps a row): four lanes per row.  Lane q of the quad reads and
+// checks taps q, q + 4, ... (col_ptr, then the entry, then x), so a row's
+// loads are spread over four threads; the quad's first lane then runs the sum
+// in (j, i) order, taking each x from the lane that loaded it.
+template <int KC>
+__global__ void __launch_bounds__(128) csc_gather_lat4(const CscGatherParams P) {
+    constexpr int KK = KC * KC, NU = (KK + 3) / 4;
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const long long gtid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long nthr = (long long)gridDim.x * blockDim.x;
+    const int S = P.s;
+    bool bad = false;
+    for (long long c = gtid; c <= P.cols; c += nthr) {  // col_ptr against its closed form
+        long long want = P.nnz;
+        if (c < P.cols) {
+            const int a = (int)(c / P.n), b = (int)(c - (long long)a * P.n);
+            want = 0;
+            int nzj[KC];
+#pragma unroll
+            for (int i = 0; i < KC; ++i) nzj[i] = 0;
+#pragma unroll
+            for (int j = 0; j < KC; ++j) {
+                want += P.zw[j] * slides_below_g(j, a, P.mo, S, P.p);
+                const int d = a + P.p - j;
+                if (d >= 0 && d % S == 0 && d / S < P.mo)
+#pragma unroll
+                    for (int i = 0; i < KC; ++i) nzj[i] += (P.nzrow[j] >> i) & 1u;
+            }
+#pragma unroll
+            for (int i = 0; i < KC; ++i) want += (long long)nzj[i] * slides_below_g(i, b, P.no, S, P.p);
+        }
+        bad |= (long long)__ldg(P.col_ptr + c) != want;
+    }
+    const int sub = threadIdx.x & 3, base = (threadIdx.x & 31) & ~3;
+    const long long r = gtid >> 2;
+    const bool live = r < P.rows;
+    int x = 0, y = 0, jlo = 0, jhi = 0, ilo = 0, ihi = 0;
+    long long rb = 0;
+    if (live) {
+        x = (int)(r / P.no);
+        y = (int)(r - (long long)x * P.no);
+        tap_range_g(x, P.m, KC, S, P.p, jlo, jhi);
+        tap_range_g(y, P.n, KC, S, P.p, ilo, ihi);
+        rb = (long long)(S * x - P.p) * P.n + (S * y - P.p);
+    }
+    auto stored = [&](int q) {
+        const int j = q / KC, i = q - j * KC;
+        return live && q < KK && j >= jlo && j < jhi && i >= ilo && i < ihi && ((P.nzrow[j] >> i) & 1u);
+    };
+    bool st[NU];
+    int cp[NU];
+#pragma unroll
+    for (int u = 0; u < NU; ++u) {
+        const int q = sub + 4 * u, j = q / KC, i = q - j * KC;
+        st[u] = stored(q);
+        cp[u] = st[u] ? __ldg(P.col_ptr + rb + (long long)j * P.n + i) : 0;
+    }
+    // this lane's taps (compile-time parameter indices, selected by lane)
+    uint32_t tw[NU];
+#pragma unroll
+    for (int u = 0; u < NU; ++u) {
+        const float t0 = P.it32[4 * u];
+        const float t1 = 4 * u + 1 < KK ? P.it32[4 * u + 1] : 0.0f;
+        const float t2 = 4 * u + 2 < KK ? P.it32[4 * u + 2] : 0.0f;
+        const float t3 = 4 * u + 3 < KK ? P.it32[4 * u + 3] : 0.0f;
+        tw[u] = __float_as_uint(sub == 0 ? t0 : sub == 1 ? t1 : sub == 2 ? t2 : t3);
+    }
+    int rw[NU];
+    uint32_t vw[NU];
+#pragma unroll
+    for (int u = 0; u < NU; ++u) {
+        const int q = sub + 4 * u, j = q / KC, i = q - j * KC;
+        rw[u] = (int)r;
+        vw[u] = tw[u];
+        if (!st[u]) continue;
+        const int idxJ = min((KC - 1 - j) / S, x), idxI = min((KC - 1 - i) / S, y);
+        int rank;
+        if (!P.zt) {
+            rank = idxJ * (idxI + 1 + min(i / S, P.no - 1 - y)) + idxI;
+        } else {
+            uint32_t mi = 0;
+            for (int d = -min(i / S, P.no - 1 - y); d <= idxI; ++d) mi |= 1u << (i + d * S);
+            rank = __popc(P.nzrow[j] & mi & ~((2u << i) - 1u));
+            for (int d = 1; d <= idxJ; ++d) rank += __popc(P.nzrow[j + d * S] & mi);
+        }
+        const long long pos = (long long)cp[u] + rank;
+        if (pos < 0 || pos >= P.nnz) {
+            bad = true;
+            continue;
+        }
+        rw[u] = __ldg(P.row_idx + pos);
+        vw[u] = __float_as_uint(__ldg(P.vals + pos));
+    }
+#pragma unroll
+    for (int u = 0; u < NU; ++u)
+        if (st[u]) bad |= rw[u] != (int)r || vw[u] != tw[u];
+    // x may be the previous kernel's output: the gathers wait for it
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    for (int b = 0; b < P.batch; ++b) {
+        const float* X = reinterpret_cast<const float*>(P.X) + (long long)b * P.ldx;
+        float xv[NU];
+#pragma unroll
+        for (int u = 0; u < NU; ++u) {
+            const int q = sub + 4 * u, j = q / KC, i = q - j * KC;
+            xv[u] = st[u] ? __ldg(X + rb + (long long)j * P.n + i) : 0.0f;
+        }
+        float acc = 0.0f;
+#pragma unroll
+        for (int u = 0; u < NU; ++u)
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const float xx = __shfl_sync(0xffffffffu, xv[u], base + t);
+                const int q = 4 * u + t;
+                if (q < KK && stored(q)) acc = fmaf(P.it32[q], xx, acc);
+            }
+        if (live && sub == 0) reinterpret_cast<float*>(P.Y)[(long long)b * P.ldy + r] = acc;
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) *P.fail = 1;
+}
+
 cudaError_t launch_csc_gather_lat(const CscGatherParams& cp, cudaStream_t st, int sms, bool pdl) {
     (void)sms;
     if (cp.batch > 2 || cp.k > 7 || !cp.inline_taps) return cudaErrorInvalidValue;
-    const long long work = std::max<long long>(cp.rows, cp.cols + 1);
+    const bool quad = cp.k >= 5;
+    const long long work = std::max<long long>((quad ? 4 : 1) * cp.rows, cp.cols + 1);
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)((cp.rows + 127) / 128 > 0 ? (cp.rows + 127) / 128 : 1));
+    cfg.gridDim = dim3((unsigned)(((quad ? 4 : 1) * cp.rows + 127) / 128 > 0 ? ((quad ? 4 : 1) * cp.rows + 127) / 128 : 1));
     // (the col_ptr sweep strides over the same threads: enough of them for cols + 1)
     if ((long long)cfg.gridDim.x * 128 < work) cfg.gridDim.x = (unsigned)((work + 127) / 128);
     cfg.blockDim = dim3(128);
@@ -318,9 +439,9 @@ cudaError_t launch_csc_gather_lat(const CscGatherParams& cp, cudaStream_t st, in
         case 2: return cudaLaunchKernelEx(&cfg, csc_gather_lat<2>, cp);
         case 3: return cudaLaunchKernelEx(&cfg, csc_gather_lat<3>, cp);
         case 4: return cudaLaunchKernelEx(&cfg, csc_gather_lat<4>, cp);
-        case 5: return cudaLaunchKernelEx(&cfg, csc_gather_lat<5>, cp);
-        case 6: return cudaLaunchKernelEx(&cfg, csc_gather_lat<6>, cp);
-        case 7: return cudaLaunchKernelEx(&cfg, csc_gather_lat<7>, cp);
+        case 5: return cudaLaunchKernelEx(&cfg, csc_gather_lat4<5>, cp);
+        case 6: return cudaLaunchKernelEx(&cfg, csc_gather_lat4<6>, cp);
+        case 7: return cudaLaunchKernelEx(&cfg, csc_gather_lat4<7>, cp);
         default: return cudaErrorInvalidValue;
     }
 }
