@@ -733,7 +733,13 @@ __global__ void __launch_bounds__(128) csr_spmm_rowblock(const GenericParams P) 
     // images in groups of IMG: group blockIdx.y, blockIdx.y + gridDim.y, ...
     for (int i0 = blockIdx.y * IMG; i0 < P.batch; i0 += gridDim.y * IMG) {
         const int ni = min(IMG, P.batch - i0);
-        const float* x0 = P.X + (int64_t)i0 * P.ldx;
+        // per-image row pointers once per group (images past the batch alias
+        // the first: their sums are computed and dropped), so a gather is one
+        // address multiply-add and the load -- no 64-bit index arithmetic and
+        // no predicates in the entry loop
+        const float* xq[IMG];
+#pragma unroll
+        for (int q = 0; q < IMG; ++q) xq[q] = P.X + (int64_t)(i0 + (q < ni ? q : 0)) * P.ldx;
         float acc[IMG];
 #pragma unroll
         for (int q = 0; q < IMG; ++q) acc[q] = 0.0f;
@@ -741,8 +747,7 @@ __global__ void __launch_bounds__(128) csr_spmm_rowblock(const GenericParams P) 
             const int c = sc[e];
             const float v = sv[e];
 #pragma unroll
-            for (int q = 0; q < IMG; ++q)
-                if (q < ni) acc[q] = fmaf(v, __ldg(x0 + (int64_t)q * P.ldx + c), acc[q]);
+            for (int q = 0; q < IMG; ++q) acc[q] = fmaf(v, __ldg(xq[q] + c), acc[q]);
         }
 #pragma unroll
         for (int q = 0; q < IMG; ++q)

@@ -20,6 +20,19 @@ SPECS = {"c3": ((1024, 1024, 3, 1, 1), 256, 0), "c3b32": ((1024, 1024, 3, 1, 1),
          "c4": ((4096, 4096, 7, 2, 3), 8, 0), "c4csc": ((4096, 4096, 7, 2, 3), 8, 1), "c2": ((512, 512, 5, 2, 2), 1, 0),
          "build3": ((1024, 1024, 3, 1, 1), 0, 0), "build4": ((4096, 4096, 7, 2, 3), 0, 0),
          "c5k11": ((257, 193, 11, 1, 10), 256, 0)}
+if target == "generic3":  # config 3's matrix uploaded as a generic host CSR, 256 images
+    spec = (1024, 1024, 3, 1, 1)
+    t0 = sp.build_transform(sp.Kernel(3, np.random.default_rng(0).standard_normal(9).astype(np.float32)),
+                            sp.ConvSpec(*spec))
+    ptr, idx, val = t0.export()
+    t = sp.Transform.from_host(t0.rows, t0.cols, ptr, idx, val)
+    X = torch.randn(256, t.cols, device="cuda")
+    Y = torch.empty(256, t.rows, device="cuda")
+    for _ in range(warm + 1):
+        sp.spmm(t, X, Y)
+    torch.cuda.synchronize()
+    print(target, t.last_kernel)
+    sys.exit(0)
 if target == "group":
     from paper_2411_19419_b200.layers import densenet121_layers
     ts, xs = [], []
