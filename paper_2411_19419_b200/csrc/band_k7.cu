@@ -16,13 +16,13 @@ cudaError_t band_k7(int op, int s, const BandParams& bp, const CUtensorMap* tmap
     }
     if (s == 2) {
         if (op == 0) return run_delta<7, 2, 8, 2, 32, 3>(d32, bp, tmap, st, sh, sms);
-        if (op == 1) return run_check<7, 2, 64>(bp, st, sms);
+        if (op == 1) return bp.csc ? run_check<7, 2, 32>(bp, st, sms) : run_check<7, 2, 64>(bp, st, sms);
         if (op == 2) return run_delta64<7, 2, 4, 2, 16, 4>(d64, bp, tmap, st, sh, sms);
         return cudaErrorNotSupported;
     }
     if (s == 3) {
         if (op == 0) return run_delta<7, 3, 4, 2, 16, 3>(d32, bp, tmap, st, sh, sms);
-        if (op == 1) return run_check<7, 3, 64>(bp, st, sms);
+        if (op == 1) return bp.csc ? run_check<7, 3, 32>(bp, st, sms) : run_check<7, 3, 64>(bp, st, sms);
         if (op == 2) return run_delta64<7, 3, 4, 2, 16, 2>(d64, bp, tmap, st, sh, sms);
         return cudaErrorNotSupported;
     }

@@ -716,7 +716,11 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
         // Both forms run on the caller's stream only: the check sees exactly
         // the matrix the stream order gives it.
         const int fsel = spb::opt(spb::kOptFused);
-        bp.fused = band_taps && bp.seg_div == 1 && (fsel ? fsel == 2 : g.k <= 2 || (g.k == 3 && g.s == 1)) ? 1 : 0;
+        bp.fused = band_taps && bp.seg_div == 1 &&
+                           !(csc && spb::band_csc_seg_div((int)g.k, (int)g.s) != 1) &&
+                           (fsel ? fsel == 2 : g.k <= 2 || (g.k == 3 && g.s == 1))
+                       ? 1
+                       : 0;
         if (bp.fused) {
             h->checked.store(true);
             const cudaError_t fe = spb::launch_band((int)g.k, (int)g.s, bp, &tmap, st, nullptr, sms);
@@ -1241,7 +1245,7 @@ static int build_csc_impl(int64_t m, int64_t n, int64_t k, int64_t s, int64_t p,
     size_t seg_bytes = 0;
     if (spb::band_supported((int)k, (int)s)) {  // CSC segments: one input row x s * band_tw input columns
         h->band_tw = spb::band_tile_width((int)k, (int)s);
-        const int64_t segw = h->band_tw / spb::band_seg_div((int)k, (int)s);
+        const int64_t segw = h->band_tw / spb::band_csc_seg_div((int)k, (int)s);
         h->csc_tiles_b = (int)((n + segw * s - 1) / (segw * s));  // (segments of s * segment-width columns)
         seg_bytes = ((size_t)(m * h->csc_tiles_b) + 255) & ~size_t(255);
     }

@@ -295,6 +295,7 @@ cudaError_t launch_spmv_win(const SpecParams& sp, int kmax, cudaStream_t st);
 bool band_supported(int k, int s);
 int band_tile_width(int k, int s);
 int band_seg_div(int k, int s);       // check segments per tile width
+int band_csc_seg_div(int k, int s);   // the same for CSC storage
 bool band64_supported(int k, int s);  // fp64 apply instantiated
 cudaError_t launch_band(int k, int s, const BandParams& bp, const CUtensorMap* tmap, cudaStream_t st,
                         BandShape* shape, int sms);

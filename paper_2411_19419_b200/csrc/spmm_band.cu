@@ -51,6 +51,13 @@ int band_tile_width(int k, int s) {
 // segments are 32 output columns (a warp's row-per-lane), the others the tile width.
 int band_seg_div(int k, int s) { return k == 11 ? band_tile_width(k, s) / 32 : 1; }
 
+// CSC check segments (s * tile width / this input columns): k = 7 at s = 2, 3
+// checks s * 32 input columns a segment -- half the staging per warp, twice the
+// warps resident: config 4's CSC apply 546 -> 493 us, 2048^2 k7 s3 243 -> 204 us
+// (k3 s2 and k5 s2 measured slower that way: 260 -> 276, 185 -> 189 us;
+// scripts/probe_csc_check.py).
+int band_csc_seg_div(int k, int s) { return s >= 2 && k == 7 ? 2 : band_seg_div(k, s); }
+
 // fp64 applies: every band geometry but k = 11 (121 double taps would not fit the registers)
 bool band64_supported(int k, int s) { return band_supported(k, s) && k != 11; }
 

@@ -122,7 +122,8 @@ def test_csc_band_forms(sp, orc, torch_cuda, spec, fused):
         assert t.last_kernel in CSC_BAND_KERNELS
         assert np.array_equal(bits(Y), bits(csc_want(orc, t, Xn))), (spec, zero)
         segs, bad = t.band_check_status()
-        assert segs == m * -(-n // 128) and bad == 0  # (s * band width input columns per segment)
+        seg_cols = 64 if k == 7 else 128  # (s * the check's width input columns: k7 s2 checks 32-wide)
+        assert segs == m * -(-n // seg_cols) and bad == 0
 
 
 @pytest.mark.slow
