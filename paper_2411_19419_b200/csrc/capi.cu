@@ -229,7 +229,11 @@ int repitch_for_tma(const spconv_csr* h, const void* X, int64_t ldx, int64_t bat
     const double bytes = (double)batch * (double)g.m * (double)np * (double)es;
     if (bytes > 8.0 * (1ull << 30) || batch > 65535 || g.m * g.n > (1ll << 31))
         return SPCONV_OK;  // (a huge batch keeps the element staging)
-    CK(cudaMallocAsync(&rb.p, (size_t)bytes, st));
+    if (cudaMallocAsync(&rb.p, (size_t)bytes, st) != cudaSuccess) {  // (no room: keep the element staging)
+        cudaGetLastError();
+        rb.p = nullptr;
+        return SPCONV_OK;
+    }
     rb.st = st;
     CK(spb::launch_repitch(X, ldx, rb.p, (int)g.m, (int)g.n, np, batch, f64, st));
     if (int rc = encode_x_map(tmap, rb.p, g, g.m * np, batch, sh.wc, sh.wr, 1, f64, np)) return rc;
