@@ -657,7 +657,9 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
             // Programmatic dependent launch lets the SpMV fetch the matrix before
             // the previous kernel on the stream finishes -- never behind this
             // handle's own build, whose writes are only visible at its end.
-            sp.pdl = h->applied.exchange(true) ? 1 : 0;
+            // (nor when the storage was handed out: a kernel of the caller's may
+            // have just written it)
+            sp.pdl = h->applied.exchange(true) && !h->exposed.load() ? 1 : 0;
             sp.X = X;
             // The windowed kernel (one round trip) wins on matrices that arrive
             // from HBM -- config 2 cold: 12.3 -> 10.2 us; on L2-resident
@@ -702,6 +704,10 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
         spb::BandShape sh{};
         spb::BandParams bp{};
         if (int rc = band_setup(h, csc, false, batch, X, ldx, Y, ldy, bp, sh, sms)) return rc;
+        // the apply as a programmatic dependent: its check warps read the
+        // matrix before the previous kernel ends -- never right behind the
+        // handle's own build, nor over storage handed out to the caller
+        bp.pdl = h->applied.exchange(true) && !h->exposed.load() && spb::opt(spb::kOptPdl) == 0 ? 1 : 0;
         CUtensorMap tmap;
         std::memset(&tmap, 0, sizeof tmap);
         RepitchBuf rbuf;

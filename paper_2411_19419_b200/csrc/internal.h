@@ -22,6 +22,7 @@ enum Opt {
     kOptStage,         // latency SpMV: 0 auto (window kernel from 8 MB of matrix), 1 bulk-staged, 2 window
     kOptSpecSkew,      // test hook: offsets the latency SpMV's predicted row starts
     kOptRepitch,       // band path on rows not 16-byte pitched: 0 auto (repitched copy + TMA), 1 off (element staging)
+    kOptPdl,           // band apply as a programmatic dependent launch: 0 auto, 1 off
     kOptCount
 };
 extern std::atomic<int> g_opt[kOptCount];
@@ -140,6 +141,7 @@ struct BandParams {
     int notma;         // X rows not 16-byte pitched (or windows wider than a TMA box): cp.async staging
     int seg_div;       // check segments per apply tile width (k = 11: smaller segments)
     int tiles_y_chk;   // check segments across n_out (CSR storage) = ceil(n_out / (TW / seg_div))
+    int pdl;           // host: launch the apply as a programmatic dependent of the previous kernel
 };
 
 // CSC-storage SpMV / SpMM of a conv transform (csc_apply.cu).

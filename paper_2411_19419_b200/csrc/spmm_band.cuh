@@ -955,6 +955,12 @@ __global__ void __launch_bounds__(FUSED ? FusedCfg<K, S, V, CPT, TH, STAGES, DEL
         s_wt[q] = F64 && P.taps64 ? (T)__ldg(P.taps64 + q) : (T)t32;
     }
     __syncthreads();
+    // Programmatic dependent launch: the next call's CTAs may start as SMs free
+    // up.  What this grid reads before griddepcontrol.wait is the matrix and
+    // the taps only (never written by the previous kernel: the host launches it
+    // this way only after the handle's build and when its storage was never
+    // handed out); X, Y, the row flags and the verdicts wait.
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
     if (FUSED && warp > C::CWARPS) {
         // ---- check warps (fused form): segments blockIdx.x * CHK + cw,
@@ -974,6 +980,7 @@ __global__ void __launch_bounds__(FUSED ? FusedCfg<K, S, V, CPT, TH, STAGES, DEL
         SegGeom vg{};
         int cb = 0;
         uint32_t cph = 0;
+        bool waited = false;
         auto issue = [&](long long sg) {
             vg = csc ? seg_geom_csc<K, S, S * C::TW, ZT>(P, sg) : seg_geom<K, S, C::TW, ZT>(P, sg);
             if (lane == 0 && vg.valid) {
@@ -997,6 +1004,10 @@ __global__ void __launch_bounds__(FUSED ? FusedCfg<K, S, V, CPT, TH, STAGES, DEL
                 ok = csc ? seg_verify_csc<K, S, C::TW, ZT>(P, g, cslice + b * SLICE, w, s_w, lane)
                          : seg_verify<K, S, C::TW, ZT>(P, g, cslice + b * SLICE, w, s_w, lane);
             }
+            if (!waited) {  // (the previous kernel may still read the flags)
+                asm volatile("griddepcontrol.wait;" ::: "memory");
+                waited = true;
+            }
             if (lane == 0) {
                 P.seg_ok[sg] = ok ? 1 : 0;
                 if (!ok && !P.fixup) *P.fail_count = 1;
@@ -1010,6 +1021,7 @@ __global__ void __launch_bounds__(FUSED ? FusedCfg<K, S, V, CPT, TH, STAGES, DEL
         // lane per row, folded into a per-stage bit mask) and the window load
         // (one elected lane).  Running STAGES items ahead hides the flag
         // loads' latency from the consumers.
+        asm volatile("griddepcontrol.wait;" ::: "memory");
         int it = 0;
         for (ItemIter I(P); I.img < P.batch; I.next(), ++it) {
             const int st = it % STAGES;
@@ -1048,6 +1060,7 @@ __global__ void __launch_bounds__(FUSED ? FusedCfg<K, S, V, CPT, TH, STAGES, DEL
     for (int q = 0; q < C::KK; ++q) w[q] = s_wt[q];
     const bool vec_ok = P.y_vec != 0;
     constexpr unsigned long long VMASK = (1ull << V) - 1ull;
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // (Y may still be in use by the previous kernel)
 
     int it = 0;
     for (ItemIter I(P); I.img < P.batch; I.next(), ++it) {
@@ -1239,6 +1252,24 @@ __global__ void __launch_bounds__(256) conv_band_fixup(const BandParams P) {
 // ---------------------------------------------------------------------------
 namespace {
 
+// The apply kernels (fused or not): a programmatic dependent of the previous
+// kernel on the stream when bp.pdl (see conv_spmm_band's prologue).
+template <typename Kern>
+cudaError_t launch_band_kernel(Kern kern, unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+                               const CUtensorMap* tmap, const BandParams& bp) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = bp.pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, *tmap, bp);
+}
+
 template <typename Kern>
 cudaError_t launch_pdl(Kern kern, unsigned grid, unsigned block, size_t smem, cudaStream_t st, const BandParams& bp) {
     cudaLaunchConfig_t cfg = {};
@@ -1278,8 +1309,7 @@ cudaError_t run_fused(const BandParams& bp, const CUtensorMap* tmap, cudaStream_
         const long long items = (long long)bp.tiles * bp.batch;
         // every CTA also owns segments: at least one CTA per SM even for short batches
         const long long grid = std::min<long long>(std::max<long long>(items, sms), (long long)occ[dev & 63] * sms);
-        kern<<<(unsigned)grid, FC::THREADS, SMEM, st>>>(*tmap, bp);
-        cudaError_t e = cudaGetLastError();
+        cudaError_t e = launch_band_kernel(kern, (unsigned)grid, FC::THREADS, SMEM, st, tmap, bp);
         if (e != cudaSuccess) return e;
         if (!bp.fixup) return cudaSuccess;  // (failed segments raise the handle's verdict instead)
         const long long segs = (long long)bp.mo * bp.tiles_y;
@@ -1312,8 +1342,7 @@ cudaError_t run_cfg(const BandParams& bp, const CUtensorMap* tmap, cudaStream_t 
     }
     const long long items = (long long)bp.tiles * bp.batch;
     const long long grid = std::min<long long>(items, (long long)occ[dev & 63] * sms);
-    kern<<<(unsigned)grid, C::THREADS, C::SMEM, st>>>(*tmap, bp);
-    return cudaGetLastError();
+    return launch_band_kernel(kern, (unsigned)grid, C::THREADS, C::SMEM, st, tmap, bp);
 }
 
 template <int K, int S, int V, int CPT, int TH, int STAGES, bool ZT>
@@ -1368,8 +1397,7 @@ cudaError_t run_cfg64(const BandParams& bp, const CUtensorMap* tmap, cudaStream_
     }
     const long long items = (long long)bp.tiles * bp.batch;
     const long long grid = std::min<long long>(items, (long long)occ[dev & 63] * sms);
-    kern<<<(unsigned)grid, C::THREADS, C::SMEM, st>>>(*tmap, bp);
-    return cudaGetLastError();
+    return launch_band_kernel(kern, (unsigned)grid, C::THREADS, C::SMEM, st, tmap, bp);
 }
 
 template <int K, int S, int V, int CPT, int TH, int STAGES>
