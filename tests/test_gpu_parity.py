@@ -540,6 +540,36 @@ def test_band_check_reads_the_matrix(sp, orc, torch_cuda, spec, check, opts):
     assert np.array_equal(bits(Y), bits(want))
 
 
+@pytest.mark.parametrize("batch", [1, 6])
+def test_stream_ordered_change_of_handed_out_storage(sp, orc, torch_cuda, batch):
+    """A value changed by a kernel of the caller's on the same stream, with no
+    synchronisation before the next apply: stream order alone must make the
+    apply see it.  (Applies read the matrix before griddepcontrol.wait only
+    when launched as programmatic dependents, which storage handed out by
+    device_ptrs never is.)"""
+    torch = torch_cuda
+    spec = (256, 256, 3, 1, 1)
+    kern, X = problem(orc, 15, 256, 256, 3, batch=batch)
+    t = build(sp, spec, kern)
+    ptr, idx, val = native_copy(t)
+    Xd = torch.from_numpy(X).cuda()
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        for _ in range(3):  # (the handle is past its first apply: PDL would be allowed)
+            sp.spmm(t, Xd, stream=st)
+        _, _, cv = t.device_ptrs()
+        dcv = torch.as_tensor(_DevArray(cv, t.nnz, "<f4"), device="cuda")
+        for rep in range(4):
+            e = int(ptr[t.rows // 2 + 17 * rep]) + 1
+            val[e] = np.float32(val[e] * -3.0 + 0.5)
+            torch.cuda._sleep(200_000)  # (the caller's kernel runs long enough to overlap a PDL launch)
+            dcv[e] = float(val[e])      # a kernel on st
+            Y = sp.spmm(t, Xd, stream=st)
+            st.synchronize()
+            want = orc.spmm_native(ptr, idx, val, X)
+            assert np.array_equal(bits(Y.cpu().numpy()), bits(want)), (batch, rep, t.last_kernel)
+
+
 @pytest.mark.parametrize("bulk_store", ["0", "1"])
 @pytest.mark.parametrize("variant", ["block", "warp", "persist"])
 def test_build_variants_bitexact(sp, orc, variant, bulk_store, opts):
