@@ -2281,6 +2281,7 @@ int spconv_spmm_f64_threads(const spconv_csr* h, const double* X_dev, int64_t ld
         spb::BandShape sh;
         if (int rc = band_setup(hm, csc, true, batch, X_dev, ldx, Y_dev, ldy, bp, sh, sms, st)) return rc;
         bp.fused = 0;
+        bp.pdl = hm->applied.exchange(true) && !hm->exposed.load() && spb::opt(spb::kOptPdl) == 0 ? 1 : 0;
         CUtensorMap tmap;
         std::memset(&tmap, 0, sizeof tmap);
         RepitchBuf rbuf;
