@@ -25,6 +25,12 @@
  * ordered after it; on another stream the caller orders them (an event), as
  * with any CUDA producer.  The host-buffer calls (spconv_convolve_host*) and
  * every synchronous call (export, copy, text) wait for the build themselves.
+ * From a handle's second apply on, applies are launched as programmatic
+ * dependents of the kernel before them on the stream: they may start reading
+ * the handle's own storage before that kernel ends, but read x and write y
+ * only after it (stream order for the caller's data is unchanged).  Storage
+ * handed out by spconv_csr_device_ptrs is never read early (option pdl = off
+ * disables the early start altogether).
  */
 #ifndef SPCONV_B200_H
 #define SPCONV_B200_H
