@@ -19,7 +19,7 @@ SPECS = {"c3": ((1024, 1024, 3, 1, 1), 256, 0), "c3b32": ((1024, 1024, 3, 1, 1),
          "c3csc": ((1024, 1024, 3, 1, 1), 256, 1), "c3f64": ((1024, 1024, 3, 1, 1), 256, 0),
          "c4": ((4096, 4096, 7, 2, 3), 8, 0), "c4csc": ((4096, 4096, 7, 2, 3), 8, 1), "c2": ((512, 512, 5, 2, 2), 1, 0),
          "build3": ((1024, 1024, 3, 1, 1), 0, 0), "build4": ((4096, 4096, 7, 2, 3), 0, 0),
-         "c5k11": ((257, 193, 11, 1, 10), 256, 0)}
+         "c5k11": ((257, 193, 11, 1, 10), 256, 0), "k11a": ((1024, 1024, 11, 1, 5), 32, 0)}
 if target == "generic3":  # config 3's matrix uploaded as a generic host CSR, 256 images
     spec = (1024, 1024, 3, 1, 1)
     t0 = sp.build_transform(sp.Kernel(3, np.random.default_rng(0).standard_normal(9).astype(np.float32)),

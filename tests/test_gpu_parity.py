@@ -704,3 +704,32 @@ def test_fp64_path_bitexact_vs_reference_digests(sp, orc, golden, torch_cuda):
     tr = sp.relayout(tc, sp.Layout.CSR)
     a = np.linspace(-1, 1, 40 * 36).reshape(40, 36)
     assert np.array_equal(sp.convolve(tc, a).view(np.uint64), sp.convolve(tr, a).view(np.uint64))
+
+
+def test_band_apply_captured_in_a_graph(sp, orc, torch_cuda):
+    """Back-to-back band applies (programmatic dependent launches after the
+    first) captured in a CUDA graph and replayed: every replay's outputs are the
+    oracle's, with the inputs rewritten between replays."""
+    torch = torch_cuda
+    spec = (256, 256, 3, 1, 1)
+    kern, X = problem(orc, 16, 256, 256, 3, batch=8)
+    t = build(sp, spec, kern)
+    ptr, idx, val = native_copy(t)
+    Xd = torch.from_numpy(X).cuda()
+    Ys = [torch.empty(8, t.rows, device="cuda") for _ in range(3)]
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        sp.spmm(t, Xd, Ys[0], stream=st)  # (first apply outside the graph)
+    st.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        for Y in Ys:
+            sp.spmm(t, Xd, Y, stream=st)
+    for rep in range(3):
+        Xn = X * (1.0 + rep) - rep
+        Xd.copy_(torch.from_numpy(Xn.astype(np.float32)))
+        g.replay()
+        torch.cuda.synchronize()
+        want = orc.spmm_native(ptr, idx, val, Xn.astype(np.float32))
+        for Y in Ys:
+            assert np.array_equal(bits(Y.cpu().numpy()), bits(want)), rep
