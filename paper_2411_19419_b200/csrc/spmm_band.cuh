@@ -784,8 +784,12 @@ __global__ void __launch_bounds__(128) conv_band_check(const BandParams P) {
         }
     }
     __syncthreads();  // s_w (and the barrier inits) visible block-wide
+    // (as a programmatic dependent: the matrix and taps are read early, the
+    // flags -- which the kernel in front may still read -- written after it)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (!live) return;
     if (!g.valid) {
+        asm volatile("griddepcontrol.wait;" ::: "memory");
         if (lane == 0) {
             P.seg_ok[seg] = 0;
             if (csc) *P.fail_count = 1;
@@ -798,6 +802,7 @@ __global__ void __launch_bounds__(128) conv_band_check(const BandParams P) {
     mbar_wait(bar, 0);
     const bool ok = csc ? seg_verify_csc<K, S, TW, ZT, PER, SEG>(P, g, rp, w, s_w, lane)
                         : seg_verify<K, S, TW, ZT>(P, g, rp, w, s_w, lane);
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if (lane == 0) {
         P.seg_ok[seg] = ok ? 1 : 0;
         if (csc && !ok) *P.fail_count = 1;
@@ -1431,8 +1436,17 @@ cudaError_t run_check(const BandParams& bp, cudaStream_t st, int sms) {
     }
     const long long segs = bp.csc ? (long long)bp.m * bp.tiles_b : (long long)bp.mo * bp.tiles_y;
     const long long grid = (segs + warps - 1) / warps;
-    kern<<<(unsigned)grid, warps * 32, smem, st>>>(bp);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(warps * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = bp.pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, bp);
 }
 
 }  // namespace
