@@ -707,7 +707,7 @@ int run_spmm(spconv_csr* h, const float* X, int64_t ldx, float* Y, int64_t ldy,
         // the apply as a programmatic dependent: its check warps read the
         // matrix before the previous kernel ends -- never right behind the
         // handle's own build, nor over storage handed out to the caller
-        bp.pdl = h->applied.exchange(true) && !h->exposed.load() && spb::opt(spb::kOptPdl) == 0 ? 1 : 0;
+        bp.pdl = h->applied.exchange(true) && !h->exposed.load() && spb::opt(spb::kOptPdl) != 1 ? 1 : 0;
         CUtensorMap tmap;
         std::memset(&tmap, 0, sizeof tmap);
         RepitchBuf rbuf;
@@ -2281,7 +2281,7 @@ int spconv_spmm_f64_threads(const spconv_csr* h, const double* X_dev, int64_t ld
         spb::BandShape sh;
         if (int rc = band_setup(hm, csc, true, batch, X_dev, ldx, Y_dev, ldy, bp, sh, sms, st)) return rc;
         bp.fused = 0;
-        bp.pdl = hm->applied.exchange(true) && !hm->exposed.load() && spb::opt(spb::kOptPdl) == 0 ? 1 : 0;
+        bp.pdl = hm->applied.exchange(true) && !hm->exposed.load() && spb::opt(spb::kOptPdl) != 1 ? 1 : 0;
         CUtensorMap tmap;
         std::memset(&tmap, 0, sizeof tmap);
         RepitchBuf rbuf;

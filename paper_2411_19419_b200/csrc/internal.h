@@ -22,7 +22,7 @@ enum Opt {
     kOptStage,         // latency SpMV: 0 auto (window kernel from 8 MB of matrix), 1 bulk-staged, 2 window
     kOptSpecSkew,      // test hook: offsets the latency SpMV's predicted row starts
     kOptRepitch,       // band path on rows not 16-byte pitched: 0 auto (repitched copy + TMA), 1 off (element staging)
-    kOptPdl,           // band apply as a programmatic dependent launch: 0 auto, 1 off
+    kOptPdl,           // band kernels as programmatic dependent launches: 0 auto, 1 off, 2 the apply only (check normal)
     kOptCount
 };
 extern std::atomic<int> g_opt[kOptCount];

@@ -32,7 +32,7 @@ const OptSpec kSpecs[] = {
     {"stage", kOptStage, {"auto", "bulk", "window", nullptr}},
     {"spec_skew", kOptSpecSkew, {nullptr}},
     {"repitch", kOptRepitch, {"auto", "off", nullptr}},
-    {"pdl", kOptPdl, {"auto", "off", nullptr}},
+    {"pdl", kOptPdl, {"auto", "off", "apply_only", nullptr}},
 };
 
 }  // namespace

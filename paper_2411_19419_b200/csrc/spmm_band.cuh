@@ -1445,7 +1445,7 @@ cudaError_t run_check(const BandParams& bp, cudaStream_t st, int sms) {
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = bp.pdl ? 1 : 0;
+    cfg.numAttrs = bp.pdl && opt(kOptPdl) != 2 ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, kern, bp);
 }
 
