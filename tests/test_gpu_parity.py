@@ -733,3 +733,25 @@ def test_band_apply_captured_in_a_graph(sp, orc, torch_cuda):
         want = orc.spmm_native(ptr, idx, val, Xn.astype(np.float32))
         for Y in Ys:
             assert np.array_equal(bits(Y.cpu().numpy()), bits(want)), rep
+
+
+@pytest.mark.parametrize("fused", ["0", "1"])
+def test_programmatic_launch_modes_agree(sp, orc, torch_cuda, fused, opts):
+    """Back-to-back band applies with the programmatic dependent launch on
+    (both kernels / the apply only) and off give the oracle's bits every time,
+    the output buffer rewritten by each call."""
+    torch = torch_cuda
+    spec = (384, 256, 3, 1, 1)
+    kern, X = problem(orc, 17, 384, 256, 3, batch=12)
+    t = build(sp, spec, kern)
+    ptr, idx, val = native_copy(t)
+    want = orc.spmm_native(ptr, idx, val, X)
+    Xd = torch.from_numpy(X).cuda()
+    Y = torch.empty(12, t.rows, device="cuda")
+    for pdl in ("auto", "apply_only", "off", "auto"):
+        opts(pdl=pdl, fused=fused)
+        for _ in range(4):
+            Y.fill_(float("nan"))
+            sp.spmm(t, Xd, Y)
+        torch.cuda.synchronize()
+        assert np.array_equal(bits(Y.cpu().numpy()), bits(want)), (pdl, fused)
