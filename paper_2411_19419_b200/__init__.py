@@ -500,23 +500,26 @@ def _convolve_group(ts, images, out, dt, fn, who):
     n = len(ts)
     if len(images) != n:
         raise ValueError(f"{who}: one image per transform")
-    xs = []
-    for t, x in zip(ts, images):
-        if type(x) is not np.ndarray or x.dtype != dt or not x.flags.c_contiguous:
-            x = np.ascontiguousarray(x, dt)
-        if x.size != t.cols:
-            raise ValueError(f"{who}: matrix has {t.cols} columns but image has {x.size} elements")
-        xs.append(x)
+    cols = np.fromiter((t.cols for t in ts), np.int64, n)
     rows = np.fromiter((t.rows for t in ts), np.int64, n)
+    # one packed input (a single C-level copy), members addressed by offset
+    packed = np.concatenate([np.ravel(x) for x in images]).astype(dt, copy=False) if n else np.empty(0, dt)
+    sizes = np.fromiter((np.size(x) for x in images), np.int64, n)
+    if not np.array_equal(sizes, cols):
+        i = int(np.nonzero(sizes != cols)[0][0])
+        raise ValueError(f"{who}: matrix has {int(cols[i])} columns but image has {int(sizes[i])} elements")
+    xoff = np.zeros(n + 1, np.int64)
+    np.cumsum(cols, out=xoff[1:])
     off = np.zeros(n + 1, np.int64)
     np.cumsum(rows, out=off[1:])
     if out is None:
         out = np.empty(int(off[-1]), dt)
     elif out.dtype != dt or out.size < off[-1] or not out.flags.c_contiguous:
         raise ValueError(f"{who}: out must be a contiguous {np.dtype(dt).name} array of sum(rows) elements")
+    isz = np.dtype(dt).itemsize
     H = np.fromiter((t._h.value for t in ts), np.uintp, n)
-    X = np.fromiter((x.__array_interface__["data"][0] for x in xs), np.uintp, n)
-    Y = out.__array_interface__["data"][0] + np.dtype(dt).itemsize * off[:-1].astype(np.uintp)
+    X = packed.__array_interface__["data"][0] + isz * xoff[:-1].astype(np.uintp)
+    Y = out.__array_interface__["data"][0] + isz * off[:-1].astype(np.uintp)
     _check(fn(H.ctypes.data, n, X.ctypes.data, Y.ctypes.data))
     return [out[a:b] for a, b in zip(off[:-1].tolist(), off[1:].tolist())]
 
